@@ -1,0 +1,857 @@
+// ============================================================================
+// ORACLE — TEST INFRASTRUCTURE ONLY.
+//
+// A plain, slow, FP64 CPU implementation of what the hot path computes
+// (arXiv 2604.17538, §II).  Only tests/, __graft_entry__.smoke() and
+// bench.py's cpu_baseline / --impl reference legs may load this library.  The
+// product path (paper_2604_17538_b200/) never includes, links or calls it, and
+// this file includes no header of the product path.
+//
+// Every derivative comes from generic forward-mode jets (Dual<T,N>, nested for
+// second order); no hand-derived derivative chain appears here, so the
+// oracle's derivatives are independent of the CUDA kernels' analytic ones.
+//
+// Citations: P:n = /root/reference/PAPER.md line n (section / equation named);
+// S:n = SPEC.md line n.  "Reading #k" = DESIGN.md §3 row k (the readings of
+// the paper where it is silent, ambiguous or garbled).
+//
+// Parity pins: see tests/test_oracle_*.py.  Functions with no independent pin
+// are marked "parity unpinned" below and in DESIGN.md.
+// ============================================================================
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+#include <map>
+#include <utility>
+#include <algorithm>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+namespace orc {
+
+// ---------------------------------------------------------------------------
+// Forward-mode jets.  Dual<T,N>: value v and N partials, each of type T.
+// Dual<Dual<double,3>,3> carries value, gradient and Hessian.
+// ---------------------------------------------------------------------------
+template <class T, int N> struct Dual {
+  T v;
+  T d[N];
+  Dual() : v(0.0) { for (int i = 0; i < N; ++i) d[i] = T(0.0); }
+  Dual(double c) : v(c) { for (int i = 0; i < N; ++i) d[i] = T(0.0); }
+  explicit Dual(const T& c, bool) : v(c) { for (int i = 0; i < N; ++i) d[i] = T(0.0); }
+};
+
+inline double val(double x) { return x; }
+template <class T, int N> inline double val(const Dual<T, N>& x) { return val(x.v); }
+
+// lift a plain constant into any jet type
+template <class T> struct Lift { static T from(double c) { return T(c); } };
+
+#define ORC_BIN(OP)                                                                   \
+  template <class T, int N> Dual<T, N> operator OP(const Dual<T, N>& a, double b) {   \
+    Dual<T, N> r = a; r.v = a.v OP b; return r; }
+ORC_BIN(+)
+ORC_BIN(-)
+#undef ORC_BIN
+template <class T, int N> Dual<T, N> operator+(double a, const Dual<T, N>& b) { return b + a; }
+template <class T, int N> Dual<T, N> operator-(double a, const Dual<T, N>& b) {
+  Dual<T, N> r; r.v = a - b.v; for (int i = 0; i < N; ++i) r.d[i] = -b.d[i]; return r; }
+template <class T, int N> Dual<T, N> operator-(const Dual<T, N>& a) {
+  Dual<T, N> r; r.v = -a.v; for (int i = 0; i < N; ++i) r.d[i] = -a.d[i]; return r; }
+template <class T, int N> Dual<T, N> operator+(const Dual<T, N>& a, const Dual<T, N>& b) {
+  Dual<T, N> r; r.v = a.v + b.v; for (int i = 0; i < N; ++i) r.d[i] = a.d[i] + b.d[i]; return r; }
+template <class T, int N> Dual<T, N> operator-(const Dual<T, N>& a, const Dual<T, N>& b) {
+  Dual<T, N> r; r.v = a.v - b.v; for (int i = 0; i < N; ++i) r.d[i] = a.d[i] - b.d[i]; return r; }
+template <class T, int N> Dual<T, N> operator*(const Dual<T, N>& a, const Dual<T, N>& b) {
+  Dual<T, N> r; r.v = a.v * b.v;
+  for (int i = 0; i < N; ++i) r.d[i] = a.d[i] * b.v + a.v * b.d[i];
+  return r; }
+template <class T, int N> Dual<T, N> operator*(const Dual<T, N>& a, double b) {
+  Dual<T, N> r; r.v = a.v * b; for (int i = 0; i < N; ++i) r.d[i] = a.d[i] * b; return r; }
+template <class T, int N> Dual<T, N> operator*(double a, const Dual<T, N>& b) { return b * a; }
+template <class T, int N> Dual<T, N> operator/(const Dual<T, N>& a, const Dual<T, N>& b) {
+  Dual<T, N> r; r.v = a.v / b.v;
+  for (int i = 0; i < N; ++i) r.d[i] = (a.d[i] - r.v * b.d[i]) / b.v;
+  return r; }
+template <class T, int N> Dual<T, N> operator/(const Dual<T, N>& a, double b) {
+  Dual<T, N> r; r.v = a.v / b; for (int i = 0; i < N; ++i) r.d[i] = a.d[i] / b; return r; }
+template <class T, int N> Dual<T, N> operator/(double a, const Dual<T, N>& b) {
+  Dual<T, N> r; r.v = a / b.v;
+  for (int i = 0; i < N; ++i) r.d[i] = -(r.v * b.d[i]) / b.v;
+  return r; }
+template <class T, int N, class U> Dual<T, N>& operator+=(Dual<T, N>& a, const U& b) { a = a + b; return a; }
+template <class T, int N, class U> Dual<T, N>& operator-=(Dual<T, N>& a, const U& b) { a = a - b; return a; }
+template <class T, int N, class U> Dual<T, N>& operator*=(Dual<T, N>& a, const U& b) { a = a * b; return a; }
+
+// chain rule: value f, derivative fp (both of type T) applied to a's partials
+template <class T, int N> Dual<T, N> chain(const Dual<T, N>& a, const T& f, const T& fp) {
+  Dual<T, N> r; r.v = f; for (int i = 0; i < N; ++i) r.d[i] = fp * a.d[i]; return r; }
+
+using std::exp; using std::log; using std::log1p; using std::sqrt; using std::cbrt;
+using std::sin; using std::cos; using std::atan2;
+
+template <class T, int N> Dual<T, N> exp(const Dual<T, N>& a) { T e = exp(a.v); return chain(a, e, e); }
+template <class T, int N> Dual<T, N> log(const Dual<T, N>& a) { return chain(a, T(log(a.v)), T(1.0 / a.v)); }
+template <class T, int N> Dual<T, N> log1p(const Dual<T, N>& a) { return chain(a, T(log1p(a.v)), T(1.0 / (1.0 + a.v))); }
+template <class T, int N> Dual<T, N> sqrt(const Dual<T, N>& a) { T s = sqrt(a.v); return chain(a, s, T(0.5 / s)); }
+template <class T, int N> Dual<T, N> cbrt(const Dual<T, N>& a) { T c = cbrt(a.v); return chain(a, c, T(1.0 / (3.0 * c * c))); }
+template <class T, int N> Dual<T, N> sin(const Dual<T, N>& a) { return chain(a, T(sin(a.v)), T(cos(a.v))); }
+template <class T, int N> Dual<T, N> cos(const Dual<T, N>& a) { return chain(a, T(cos(a.v)), T(-sin(a.v))); }
+template <class T, int N> Dual<T, N> atan2(const Dual<T, N>& y, const Dual<T, N>& x) {
+  Dual<T, N> r; r.v = atan2(y.v, x.v);
+  T den = x.v * x.v + y.v * y.v;
+  for (int i = 0; i < N; ++i) r.d[i] = (x.v * y.d[i] - y.v * x.d[i]) / den;
+  return r; }
+
+template <class T> T sq(const T& x) { return x * x; }
+
+// ---------------------------------------------------------------------------
+// Small vector helpers (templated on the scalar type)
+// ---------------------------------------------------------------------------
+template <class T> struct V3 { T x[3]; };
+template <class T> T dot3(const T* a, const T* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+template <class T> void cross3(const T* a, const T* b, T* r) {
+  r[0] = a[1] * b[2] - a[2] * b[1];
+  r[1] = a[2] * b[0] - a[0] * b[2];
+  r[2] = a[0] * b[1] - a[1] * b[0]; }
+
+// ---------------------------------------------------------------------------
+// Smooth parameters (Reading #1: five named temperatures; P:42-44 give one
+// generic tau).
+// ---------------------------------------------------------------------------
+struct Smooth {
+  double tau_cmp, tau_min, tau_clip_alpha, tau_clip_t, tau_delta;
+  int trace_iters;
+};
+
+// ---------------------------------------------------------------------------
+// §II-A smooth operators
+// ---------------------------------------------------------------------------
+// sigma(x) = 1/(1+exp(-x)); branch only selects the overflow-safe form
+template <class T> T sigmoid(const T& x) {
+  if (val(x) >= 0) return 1.0 / (1.0 + exp(-x));
+  T e = exp(x);
+  return e / (1.0 + e);
+}
+// s+(x) = tau log(1 + exp(x/tau)); two algebraically equal branches
+template <class T> T softplus(const T& x, double tau) {
+  if (val(x) > 0) return x + tau * log1p(exp(-x / tau));
+  return tau * log1p(exp(x / tau));
+}
+// soft clip from two softplus: lo + s+(x-lo) - s+(x-hi)
+template <class T> T softclip(const T& x, double lo, double hi, double tau) {
+  return lo + softplus(x - lo, tau) - softplus(x - hi, tau);
+}
+// LSE(x) = tau log sum exp(x_i/tau), evaluated with the max shift
+template <class T> T lse(const T* x, int n, double tau) {
+  int im = 0;
+  for (int i = 1; i < n; ++i) if (val(x[i]) > val(x[im])) im = i;
+  T m = x[im];
+  T s = T(0.0);
+  for (int i = 0; i < n; ++i) s = s + exp((x[i] - m) / tau);
+  return m + tau * log(s);
+}
+// s_argmax(x)_i = exp(x_i/tau) / sum_j exp(x_j/tau)
+template <class T> void softargmax(const T* x, int n, double tau, T* out) {
+  int im = 0;
+  for (int i = 1; i < n; ++i) if (val(x[i]) > val(x[im])) im = i;
+  T m = x[im];
+  T s = T(0.0);
+  for (int i = 0; i < n; ++i) { out[i] = exp((x[i] - m) / tau); s = s + out[i]; }
+  for (int i = 0; i < n; ++i) out[i] = out[i] / s;
+}
+
+// ---------------------------------------------------------------------------
+// Geometry records (oracle's own layout; filled by oracle/oracle.py)
+// ---------------------------------------------------------------------------
+enum { K_HALFSPACE = 0, K_SQ = 1, K_PSQ = 2, K_XPSQ = 3, K_UNION = 10, K_INTER = 11, K_SUB = 12 };
+constexpr int MAXP = 8;       // planes per PSQ
+constexpr int MAXC = 32;      // children per operator
+constexpr int NI = 3 + MAXC;  // ints per node: type, n_children, n_planes, children[32]
+constexpr int NF = 93;        // floats per node (see oracle.py)
+
+struct Node {
+  int type, n_children, n_planes;
+  int child[MAXC];
+  double t[3], R[9];       // pose relative to parent: x_parent = R x_child + t
+  double eps[2][2];        // [endpoint][eps1, eps2]
+  double a[2][3];          // [endpoint][a_x, a_y, a_z]
+  double pl[2][MAXP][4];   // [endpoint][plane][n_x, n_y, n_z, h]
+  double ctrl[9];          // XPSQ control points p1, p2, p3
+  double up[3];            // XPSQ up hint
+  // XPSQ static data (Reading #7/#14)
+  int xcls;                // 0 point, 1 line, 2 curve
+  int frenet;              // 1: Frenet frame with constant binormal
+  double A[3], B[3], bhat[3], R0[9];
+};
+
+struct Mesh {
+  int V = 0, F = 0, E = 0;
+  std::vector<double> v;        // V x 3 local vertices
+  std::vector<int> f;           // F x 3
+  std::vector<int> e;           // E x 2  (lower index first)
+  std::vector<int> fe;          // F x 3  edge ids of (i0,i1),(i1,i2),(i2,i0)
+};
+
+struct Shape {
+  std::vector<Node> nodes;  // node 0 = root (empty => no SDF)
+  Mesh mesh;
+};
+
+struct Scene {
+  std::vector<Shape> shapes;
+  Smooth sp;
+};
+
+// unit quaternion (w,x,y,z) -> rotation matrix (row-major), after normalising
+static void quat_to_R(const double* q, double* R) {
+  double n = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  double w = q[0] / n, x = q[1] / n, y = q[2] / n, z = q[3] / n;
+  R[0] = 1 - 2 * (y * y + z * z); R[1] = 2 * (x * y - w * z);     R[2] = 2 * (x * z + w * y);
+  R[3] = 2 * (x * y + w * z);     R[4] = 1 - 2 * (x * x + z * z); R[5] = 2 * (y * z - w * x);
+  R[6] = 2 * (x * z - w * y);     R[7] = 2 * (y * z + w * x);     R[8] = 1 - 2 * (x * x + y * y);
+}
+
+static void normalize3(double* v) {
+  double n = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+  v[0] /= n; v[1] /= n; v[2] /= n;
+}
+
+// static XPSQ classification (Reading #7, #14): point / line / curve;
+// Frenet frame when the spline is genuinely curved, else a constant frame
+// built from the up hint by Gram-Schmidt.
+constexpr double XPSQ_EPS_POINT = 1e-6;   // |A|,|B| below this: point spline
+constexpr double XPSQ_EPS_LINE = 1e-2;    // |A| < 1e-2 |B|: snapped straight (A := 0)
+constexpr double XPSQ_EPS_FRAME = 1e-3;   // |BxA| < 1e-3 |A||B|: constant frame
+
+static void xpsq_static(Node& n) {
+  const double* p1 = n.ctrl; const double* p2 = n.ctrl + 3; const double* p3 = n.ctrl + 6;
+  for (int i = 0; i < 3; ++i) { n.A[i] = p1[i] - 2 * p2[i] + p3[i]; n.B[i] = 2 * (p2[i] - p1[i]); }
+  double nA = std::sqrt(dot3(n.A, n.A)), nB = std::sqrt(dot3(n.B, n.B));
+  double T0[3];
+  if (nA < XPSQ_EPS_POINT && nB < XPSQ_EPS_POINT) {
+    n.xcls = 0; T0[0] = 1; T0[1] = 0; T0[2] = 0;
+  } else if (nA < XPSQ_EPS_LINE * nB) {
+    n.xcls = 1; for (int i = 0; i < 3; ++i) { n.A[i] = 0.0; T0[i] = n.B[i]; }
+  } else {
+    n.xcls = 2;
+    for (int i = 0; i < 3; ++i) T0[i] = n.A[i] + n.B[i];
+    if (std::sqrt(dot3(T0, T0)) < XPSQ_EPS_POINT) for (int i = 0; i < 3; ++i) T0[i] = nB > XPSQ_EPS_POINT ? n.B[i] : n.A[i];
+  }
+  double bxa[3]; cross3(n.B, n.A, bxa);
+  n.frenet = (n.xcls == 2 && std::sqrt(dot3(bxa, bxa)) >= XPSQ_EPS_FRAME * nA * nB) ? 1 : 0;
+  if (n.frenet) {
+    for (int i = 0; i < 3; ++i) n.bhat[i] = bxa[i];
+    normalize3(n.bhat);
+  } else {
+    normalize3(T0);
+    double b[3] = {n.up[0], n.up[1], n.up[2]};
+    if (n.xcls == 0) {
+      // point spline: b = up, T0 = e_x made orthogonal to b
+      normalize3(b);
+      double e[3] = {1, 0, 0};
+      double c = dot3(e, b);
+      if (std::fabs(c) > 0.9) { e[0] = 0; e[1] = 1; c = dot3(e, b); }
+      for (int i = 0; i < 3; ++i) T0[i] = e[i] - c * b[i];
+      normalize3(T0);
+    } else {
+      double c = dot3(b, T0);
+      for (int i = 0; i < 3; ++i) b[i] -= c * T0[i];
+      normalize3(b);
+    }
+    for (int i = 0; i < 3; ++i) n.bhat[i] = b[i];
+    double N[3]; cross3(n.bhat, T0, N);
+    // R0 = [T0, N, b] as columns (row-major storage)
+    for (int i = 0; i < 3; ++i) { n.R0[i * 3 + 0] = T0[i]; n.R0[i * 3 + 1] = N[i]; n.R0[i * 3 + 2] = n.bhat[i]; }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Leaf SDFs in the leaf's local frame
+// ---------------------------------------------------------------------------
+constexpr double SQ_GUARD = 1e-12;  // |u|^p = exp(p log(u^2 + g)/2)
+
+// Half-space phi_N = x . n + h
+template <class T> T halfspace_phi(const T* y, const T* nrm, const T& h) {
+  return y[0] * nrm[0] + y[1] * nrm[1] + y[2] * nrm[2] + h;
+}
+
+// SQ inside-outside function, Eq. (1), with even powers
+// (x/a)^(2/e) = ((x/a)^2)^(1/e) and the guard of S:261.
+template <class T> T sq_f(const T* y, const T& e1, const T& e2, const T* a) {
+  T u0 = y[0] / a[0], u1 = y[1] / a[1], u2 = y[2] / a[2];
+  T A0 = exp(log(u0 * u0 + SQ_GUARD) / e2);
+  T A1 = exp(log(u1 * u1 + SQ_GUARD) / e2);
+  T C = exp(log(u2 * u2 + SQ_GUARD) / e1);
+  return exp((e2 / e1) * log(A0 + A1)) + C;
+}
+
+// SQ radial distance phi = |y| (1 - f^(-e1/2))  (Reading #2, P:72 garbled)
+template <class T> T sq_phi(const T* y, const T& e1, const T& e2, const T* a) {
+  T f = sq_f(y, e1, e2, a);
+  T r = sqrt(y[0] * y[0] + y[1] * y[1] + y[2] * y[2]);
+  return r * (1.0 - exp(-(e1 / 2.0) * log(f)));
+}
+
+// PSQ: smooth intersection Eq. (3) of an SQ and N half-spaces
+template <class T> T psq_phi(const T* y, const T& e1, const T& e2, const T* a,
+                             int np, const T (*pl)[4], double tau_min) {
+  T ops[1 + MAXP];
+  ops[0] = sq_phi(y, e1, e2, a);
+  for (int i = 0; i < np; ++i) ops[1 + i] = halfspace_phi(y, pl[i], pl[i][3]);
+  if (np == 0) return ops[0];
+  return lse(ops, 1 + np, tau_min);
+}
+
+// ---------------------------------------------------------------------------
+// XPSQ: projection onto the quadratic spline by the cubic of
+// P:112, soft Cardano (Eq. (6)), three PSQs, smooth minimum.
+// ---------------------------------------------------------------------------
+// Eq. (5): p(t) = (1-t)^2 p1 + 2t(1-t) p2 + t^2 p3 = p1 + B t + A t^2
+// stationarity (x - p(t)) . p'(t) = 0 gives c3 t^3 + c2 t^2 + c1 t + c0 = 0
+//   c3 = -2 A.A, c2 = -3 A.B, c1 = 2 A.w - B.B, c0 = B.w, w = x - p1
+//
+// Soft Cardano, literal (Reading #9, #10, #11, #12, #13):
+//   depressed cubic s^3 + P s + Q = 0 with t = s - b/3,
+//   Delta = -(4P^3 + 27Q^2); Delta- = -s+(-Delta), Delta+ = s+(Delta);
+//   t-  = Cardano real root with Delta- substituted,
+//   t+k = trigonometric form with Delta+ substituted, k = 0, 1, 2;
+//   both soft-clipped to (0,1);  t*_k = sig(-Delta/tau) t- + sig(Delta/tau) t+_k
+template <class T> void xpsq_roots(const Node& n, const T* y, const Smooth& sp, T* tk, double* delta_out,
+                                   double* wneg_out) {
+  const double* p1 = n.ctrl;
+  T w[3] = {y[0] - p1[0], y[1] - p1[1], y[2] - p1[2]};
+  if (delta_out) *delta_out = 0.0;
+  if (wneg_out) *wneg_out = 0.0;
+  if (n.xcls == 0) {  // point spline: any t projects to the same point
+    for (int k = 0; k < 3; ++k) tk[k] = T(0.5);
+    return;
+  }
+  const double* A = n.A; const double* B = n.B;
+  T Bw = w[0] * B[0] + w[1] * B[1] + w[2] * B[2];
+  double BB = dot3(B, B);
+  if (n.xcls == 1) {  // straight spline: the cubic degenerates to B.w - t B.B = 0
+    T t = softclip(Bw / BB, 0.0, 1.0, sp.tau_clip_t);
+    for (int k = 0; k < 3; ++k) tk[k] = t;
+    return;
+  }
+  double c3 = -2.0 * dot3(A, A);
+  double c2 = -3.0 * dot3(A, B);
+  T c1 = 2.0 * (w[0] * A[0] + w[1] * A[1] + w[2] * A[2]) - BB;
+  T c0 = Bw;
+  double b = c2 / c3;
+  T c = c1 / c3, d = c0 / c3;
+  T P = c - b * b / 3.0;
+  T Q = 2.0 * b * b * b / 27.0 - b * c / 3.0 + d;
+  T Delta = -(4.0 * P * P * P + 27.0 * Q * Q);
+  T Dm = -softplus(-Delta, sp.tau_delta);
+  T Dp = softplus(Delta, sp.tau_delta);
+  T wneg = sigmoid(-Delta / sp.tau_delta);
+  T wpos = sigmoid(Delta / sp.tau_delta);
+  if (delta_out) *delta_out = val(Delta);
+  if (wneg_out) *wneg_out = val(wneg);
+  T tm = T(0.0), tp[3] = {T(0.0), T(0.0), T(0.0)};
+  // A branch whose weight underflows to exactly 0 contributes exactly 0; it is
+  // skipped so that 0 * (non-finite derivative of a degenerate branch) cannot
+  // poison the jets (reading #34).
+  if (val(wneg) > 0.0) {
+    T D = -Dm / 108.0;
+    T sD = sqrt(D);
+    T s = cbrt(-Q / 2.0 + sD) + cbrt(-Q / 2.0 - sD);
+    tm = softclip(s - b / 3.0, 0.0, 1.0, sp.tau_clip_t);
+  }
+  if (val(wpos) > 0.0) {
+    T rho = exp(log(Q * Q / 4.0 + Dp / 108.0) / 6.0);
+    T th = atan2(sqrt(Dp / 108.0), -Q / 2.0);
+    for (int k = 0; k < 3; ++k) {
+      T s = 2.0 * rho * cos((th + 2.0 * M_PI * k) / 3.0);
+      tp[k] = softclip(s - b / 3.0, 0.0, 1.0, sp.tau_clip_t);
+    }
+  }
+  for (int k = 0; k < 3; ++k) {
+    if (val(wneg) > 0.0 && val(wpos) > 0.0) tk[k] = wneg * tm + wpos * tp[k];
+    else if (val(wneg) > 0.0) tk[k] = wneg * tm;
+    else tk[k] = wpos * tp[k];
+  }
+}
+
+// moving frame R(t) ("e.g. the Frenet frame"; Reading #7), row-major,
+// columns [T, bhat x T, bhat]
+template <class T> void xpsq_frame(const Node& n, const T& t, T* R) {
+  if (!n.frenet) { for (int i = 0; i < 9; ++i) R[i] = T(n.R0[i]); return; }
+  T pd[3];
+  for (int i = 0; i < 3; ++i) pd[i] = n.B[i] + 2.0 * n.A[i] * t;
+  T nn = sqrt(pd[0] * pd[0] + pd[1] * pd[1] + pd[2] * pd[2]);
+  T Tt[3] = {pd[0] / nn, pd[1] / nn, pd[2] / nn};
+  T bh[3] = {T(n.bhat[0]), T(n.bhat[1]), T(n.bhat[2])};
+  T N[3]; cross3(bh, Tt, N);
+  for (int i = 0; i < 3; ++i) { R[i * 3 + 0] = Tt[i]; R[i * 3 + 1] = N[i]; R[i * 3 + 2] = bh[i]; }
+}
+
+template <class T> T lerp(double a, double b, const T& t) { return a + (b - a) * t; }
+
+template <class T> T xpsq_phi(const Node& n, const T* y, const Smooth& sp) {
+  T tk[3];
+  xpsq_roots(n, y, sp, tk, nullptr, nullptr);
+  T phis[3];
+  for (int k = 0; k < 3; ++k) {
+    const T& t = tk[k];
+    // PSQ pose at the root: translation p(t) (Eq. (5)), rotation R(t)
+    T pt[3];
+    for (int i = 0; i < 3; ++i) pt[i] = n.ctrl[i] + n.B[i] * t + n.A[i] * (t * t);
+    T R[9];
+    xpsq_frame(n, t, R);
+    T dx[3] = {y[0] - pt[0], y[1] - pt[1], y[2] - pt[2]};
+    T yk[3];
+    for (int i = 0; i < 3; ++i) yk[i] = R[0 * 3 + i] * dx[0] + R[1 * 3 + i] * dx[1] + R[2 * 3 + i] * dx[2];
+    // schedules eps(t), a(t), P(t): linear between endpoint values, plane
+    // normals renormalised (Reading #8)
+    T e1 = lerp(n.eps[0][0], n.eps[1][0], t);
+    T e2 = lerp(n.eps[0][1], n.eps[1][1], t);
+    T a[3];
+    for (int i = 0; i < 3; ++i) a[i] = lerp(n.a[0][i], n.a[1][i], t);
+    T pl[MAXP][4];
+    for (int j = 0; j < n.n_planes; ++j) {
+      T nv[3];
+      for (int i = 0; i < 3; ++i) nv[i] = lerp(n.pl[0][j][i], n.pl[1][j][i], t);
+      T nn = sqrt(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]);
+      for (int i = 0; i < 3; ++i) pl[j][i] = nv[i] / nn;
+      pl[j][3] = lerp(n.pl[0][j][3], n.pl[1][j][3], t);
+    }
+    phis[k] = psq_phi(yk, e1, e2, a, n.n_planes, pl, sp.tau_min);
+  }
+  // smooth minimum of the three PSQ SDFs
+  T neg[3] = {-phis[0], -phis[1], -phis[2]};
+  return -lse(neg, 3, sp.tau_min);
+}
+
+// ---------------------------------------------------------------------------
+// Composite tree (Eqs. (2)-(4); n-ary single LSE, Reading #5;
+// subtraction LSE([phi1, -phi2]), Reading #4).  Each node has a pose relative
+// to its parent; y is in the parent frame.
+// ---------------------------------------------------------------------------
+template <class T> T node_phi(const Shape& sh, int idx, const T* yparent, const Smooth& sp) {
+  const Node& n = sh.nodes[idx];
+  T y[3];
+  T dx[3] = {yparent[0] - n.t[0], yparent[1] - n.t[1], yparent[2] - n.t[2]};
+  for (int i = 0; i < 3; ++i) y[i] = n.R[0 * 3 + i] * dx[0] + n.R[1 * 3 + i] * dx[1] + n.R[2 * 3 + i] * dx[2];
+  switch (n.type) {
+    case K_HALFSPACE: {
+      T nv[3] = {T(n.pl[0][0][0]), T(n.pl[0][0][1]), T(n.pl[0][0][2])};
+      return halfspace_phi(y, nv, T(n.pl[0][0][3]));
+    }
+    case K_SQ: case K_PSQ: {
+      T a[3] = {T(n.a[0][0]), T(n.a[0][1]), T(n.a[0][2])};
+      T pl[MAXP][4];
+      int np = n.type == K_SQ ? 0 : n.n_planes;
+      for (int j = 0; j < np; ++j) for (int i = 0; i < 4; ++i) pl[j][i] = T(n.pl[0][j][i]);
+      return psq_phi(y, T(n.eps[0][0]), T(n.eps[0][1]), a, np, pl, sp.tau_min);
+    }
+    case K_XPSQ:
+      return xpsq_phi(n, y, sp);
+    default: {
+      std::vector<T> ops(n.n_children);
+      for (int c = 0; c < n.n_children; ++c) ops[c] = node_phi(sh, n.child[c], y, sp);
+      if (n.type == K_UNION) {                       // Eq. (2): -LSE(-phi)
+        for (auto& o : ops) o = -o;
+        return -lse(ops.data(), n.n_children, sp.tau_min);
+      }
+      if (n.type == K_INTER)                         // Eq. (3): LSE(phi)
+        return lse(ops.data(), n.n_children, sp.tau_min);
+      ops[1] = -ops[1];                              // Eq. (4): LSE(phi1, -phi2)
+      return lse(ops.data(), 2, sp.tau_min);
+    }
+  }
+}
+
+// SDF of a shape placed with rotation R and translation t (body pose) at the
+// world point x: phi(R^T (x - t))
+template <class T> T shape_phi_world(const Shape& sh, const T* R, const T* t, const T* x, const Smooth& sp) {
+  T dx[3] = {x[0] - t[0], x[1] - t[1], x[2] - t[2]};
+  T y[3];
+  for (int i = 0; i < 3; ++i) y[i] = R[0 * 3 + i] * dx[0] + R[1 * 3 + i] * dx[1] + R[2 * 3 + i] * dx[2];
+  return node_phi(sh, 0, y, sp);
+}
+
+// ---------------------------------------------------------------------------
+// Mesh topology: unique edges keyed by the
+// sorted vertex pair; face_edges in the order (i0,i1), (i1,i2), (i2,i0).
+// ---------------------------------------------------------------------------
+static void build_topology(Mesh& m) {
+  std::map<std::pair<int, int>, int> key;
+  m.e.clear(); m.fe.assign(3 * m.F, -1);
+  for (int f = 0; f < m.F; ++f) {
+    for (int k = 0; k < 3; ++k) {
+      int a = m.f[3 * f + k], b = m.f[3 * f + (k + 1) % 3];
+      std::pair<int, int> p(std::min(a, b), std::max(a, b));
+      auto it = key.find(p);
+      int id;
+      if (it == key.end()) { id = (int)(m.e.size() / 2); key[p] = id; m.e.push_back(p.first); m.e.push_back(p.second); }
+      else id = it->second;
+      m.fe[3 * f + k] = id;
+    }
+  }
+  m.E = (int)(m.e.size() / 2);
+}
+
+// ---------------------------------------------------------------------------
+// Perturbed poses: world-frame left perturbation R <- exp([w]x) R, t <- t + dt
+// (Reading #28); exp truncated after the quadratic term, exact to second
+// order at w = 0 (all that first and second derivatives need).
+// ---------------------------------------------------------------------------
+template <class T> void perturbed_pose(const double* R, const double* t, const T* dt, const T* w, T* Rp, T* tp) {
+  T W[9] = {T(0.0), -w[2], w[1], w[2], T(0.0), -w[0], -w[1], w[0], T(0.0)};
+  T W2[9];
+  for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j)
+    W2[i * 3 + j] = W[i * 3 + 0] * W[0 * 3 + j] + W[i * 3 + 1] * W[1 * 3 + j] + W[i * 3 + 2] * W[2 * 3 + j];
+  T E[9];
+  for (int i = 0; i < 9; ++i) E[i] = W[i] + 0.5 * W2[i];
+  for (int i = 0; i < 3; ++i) E[i * 3 + i] = E[i * 3 + i] + 1.0;
+  for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j)
+    Rp[i * 3 + j] = E[i * 3 + 0] * R[0 * 3 + j] + E[i * 3 + 1] * R[1 * 3 + j] + E[i * 3 + 2] * R[2 * 3 + j];
+  for (int i = 0; i < 3; ++i) tp[i] = t[i] + dt[i];
+}
+
+using D3 = Dual<double, 3>;
+using H3 = Dual<D3, 3>;
+using D6 = Dual<double, 6>;
+using D12 = Dual<double, 12>;
+using N12 = Dual<D3, 12>;
+
+}  // namespace orc
+
+using namespace orc;
+
+// ============================================================================
+// extern "C" interface (test infrastructure)
+// ============================================================================
+extern "C" {
+
+int ora_version(void) { return 1; }
+
+void* ora_scene_create(int n_shapes, const int* node_counts, const int* node_ints, const float* node_floats,
+                       const int* mesh_vcounts, const float* mesh_v, const int* mesh_fcounts, const int* mesh_f,
+                       const double* smooth, int trace_iters) {
+  Scene* sc = new Scene;
+  sc->sp = Smooth{smooth[0], smooth[1], smooth[2], smooth[3], smooth[4], trace_iters};
+  sc->shapes.resize(n_shapes);
+  int ni = 0, vi = 0, fi = 0;
+  for (int s = 0; s < n_shapes; ++s) {
+    Shape& sh = sc->shapes[s];
+    sh.nodes.resize(node_counts[s]);
+    for (int k = 0; k < node_counts[s]; ++k, ++ni) {
+      Node& n = sh.nodes[k];
+      const int* I = node_ints + (size_t)ni * NI;
+      const float* Fv = node_floats + (size_t)ni * NF;
+      n.type = I[0]; n.n_children = I[1]; n.n_planes = I[2];
+      for (int c = 0; c < MAXC; ++c) n.child[c] = I[3 + c];
+      for (int i = 0; i < 3; ++i) n.t[i] = Fv[i];
+      double q[4] = {Fv[3], Fv[4], Fv[5], Fv[6]};
+      quat_to_R(q, n.R);
+      int o = 7;
+      for (int e = 0; e < 2; ++e) for (int i = 0; i < 2; ++i) n.eps[e][i] = Fv[o++];
+      for (int e = 0; e < 2; ++e) for (int i = 0; i < 3; ++i) n.a[e][i] = Fv[o++];
+      for (int e = 0; e < 2; ++e) for (int j = 0; j < MAXP; ++j) for (int i = 0; i < 4; ++i) n.pl[e][j][i] = Fv[o++];
+      for (int i = 0; i < 9; ++i) n.ctrl[i] = Fv[o++];
+      for (int i = 0; i < 3; ++i) n.up[i] = Fv[o++];
+      if (n.type == K_XPSQ) xpsq_static(n);
+    }
+    Mesh& m = sh.mesh;
+    m.V = mesh_vcounts[s]; m.F = mesh_fcounts[s];
+    m.v.resize(3 * m.V); m.f.resize(3 * m.F);
+    for (int i = 0; i < 3 * m.V; ++i) m.v[i] = mesh_v[3 * vi + i];
+    for (int i = 0; i < 3 * m.F; ++i) m.f[i] = mesh_f[3 * fi + i];
+    vi += m.V; fi += m.F;
+    if (m.F > 0) build_topology(m);
+  }
+  return sc;
+}
+
+void ora_scene_destroy(void* s) { delete (Scene*)s; }
+
+int ora_mesh_counts(void* s, int shape, int* V, int* E, int* F) {
+  Scene* sc = (Scene*)s;
+  const Mesh& m = sc->shapes[shape].mesh;
+  *V = m.V; *E = m.E; *F = m.F;
+  return 0;
+}
+int ora_mesh_topology(void* s, int shape, int* edges, int* face_edges) {
+  Scene* sc = (Scene*)s;
+  const Mesh& m = sc->shapes[shape].mesh;
+  std::memcpy(edges, m.e.data(), sizeof(int) * 2 * m.E);
+  std::memcpy(face_edges, m.fe.data(), sizeof(int) * 3 * m.F);
+  return 0;
+}
+
+// ---- unit entry points (pins) ----------------------------------------------
+double ora_sigmoid(double x) { return sigmoid(x); }
+double ora_softplus(double x, double tau) { return softplus(x, tau); }
+double ora_softclip(double x, double lo, double hi, double tau) { return softclip(x, lo, hi, tau); }
+double ora_lse(const double* x, int n, double tau) { return lse(x, n, tau); }
+void ora_softargmax(const double* x, int n, double tau, double* out) { softargmax(x, n, tau, out); }
+double ora_sq_f(const double* y, double e1, double e2, const double* a) { return sq_f(y, e1, e2, a); }
+double ora_sq_phi(const double* y, double e1, double e2, const double* a) { return sq_phi(y, e1, e2, a); }
+
+// XPSQ projection internals for node `node` of shape `shape`: t*, Delta, w_neg
+void ora_xpsq_roots(void* s, int shape, int node, const double* y, double* t, double* delta, double* wneg) {
+  Scene* sc = (Scene*)s;
+  xpsq_roots(sc->shapes[shape].nodes[node], y, sc->sp, t, delta, wneg);
+}
+// moving frame of an XPSQ node at parameter t (row-major 3x3)
+void ora_xpsq_frame(void* s, int shape, int node, double t, double* R) {
+  Scene* sc = (Scene*)s;
+  xpsq_frame(sc->shapes[shape].nodes[node], t, R);
+}
+int ora_xpsq_class(void* s, int shape, int node) {
+  Scene* sc = (Scene*)s;
+  const Node& n = sc->shapes[shape].nodes[node];
+  return n.xcls * 10 + n.frenet;
+}
+
+// ---- sdf_eval ----------------------------------------------------------------
+// For batch item b (shape_ids[b], pose poses[b] = t(3), q(w,x,y,z), pad) and
+// its P points (world), computes d, grad (3), hess (6: xx,xy,xz,yy,yz,zz),
+// and, if want_pose, dpose (6: d/dt, d/dtheta), d2pose (21: packed upper 6x6,
+// row-major), dxdpose (18: [i*6+j] = d(grad_i)/d(pose_j)).  Output layout:
+// point-major (n = b*P + j), field-minor.
+int ora_sdf_eval(void* s, const int* shape_ids, const double* poses, const double* points, long B, long P,
+                 int want_pose, double* d, double* g, double* h, double* dpose, double* d2pose, double* dxdpose) {
+  Scene* sc = (Scene*)s;
+  const Smooth& sp = sc->sp;
+  long total = B * P;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (long n = 0; n < total; ++n) {
+    long b = n / P;
+    const Shape& sh = sc->shapes[shape_ids[b]];
+    const double* pz = poses + 8 * b;
+    double R[9], t[3] = {pz[0], pz[1], pz[2]};
+    double q[4] = {pz[3], pz[4], pz[5], pz[6]};
+    quat_to_R(q, R);
+    // value, gradient, Hessian: hyper-dual jet in the world point
+    H3 X[3];
+    for (int i = 0; i < 3; ++i) {
+      X[i] = H3(0.0);
+      X[i].v.v = points[3 * n + i];
+      X[i].v.d[i] = 1.0;
+      X[i].d[i].v = 1.0;
+    }
+    H3 Rj[9], tj[3];
+    for (int i = 0; i < 9; ++i) Rj[i] = H3(R[i]);
+    for (int i = 0; i < 3; ++i) tj[i] = H3(t[i]);
+    H3 phi = shape_phi_world(sh, Rj, tj, X, sp);
+    d[n] = phi.v.v;
+    for (int i = 0; i < 3; ++i) g[3 * n + i] = phi.v.d[i];
+    const int hi[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+    for (int k = 0; k < 6; ++k) h[6 * n + k] = phi.d[hi[k][0]].d[hi[k][1]];
+    if (want_pose) {
+      // second order in the 6 pose seeds
+      using P6 = Dual<D6, 6>;
+      P6 dt[3], w[3], Rp[9], tp[3], Xp[3];
+      for (int i = 0; i < 3; ++i) {
+        dt[i] = P6(0.0); dt[i].v.d[i] = 1.0; dt[i].d[i].v = 1.0;
+        w[i] = P6(0.0); w[i].v.d[3 + i] = 1.0; w[i].d[3 + i].v = 1.0;
+        Xp[i] = P6(points[3 * n + i]);
+      }
+      perturbed_pose(R, t, dt, w, Rp, tp);
+      P6 ph = shape_phi_world(sh, Rp, tp, Xp, sp);
+      for (int j = 0; j < 6; ++j) dpose[6 * n + j] = ph.v.d[j];
+      int k = 0;
+      for (int i = 0; i < 6; ++i) for (int j = i; j < 6; ++j) d2pose[21 * n + k++] = ph.d[i].d[j];
+      // mixed: outer pose seeds, inner point seeds
+      using M6 = Dual<D3, 6>;
+      M6 dtm[3], wm[3], Rm[9], tm[3], Xm[3];
+      for (int i = 0; i < 3; ++i) {
+        dtm[i] = M6(0.0); dtm[i].d[i].v = 1.0;
+        wm[i] = M6(0.0); wm[i].d[3 + i].v = 1.0;
+        Xm[i] = M6(0.0); Xm[i].v.v = points[3 * n + i]; Xm[i].v.d[i] = 1.0;
+      }
+      perturbed_pose(R, t, dtm, wm, Rm, tm);
+      M6 pm = shape_phi_world(sh, Rm, tm, Xm, sp);
+      for (int i = 0; i < 3; ++i) for (int j = 0; j < 6; ++j) dxdpose[18 * n + i * 6 + j] = pm.d[j].d[i];
+    }
+  }
+  return 0;
+}
+
+// ---- contact manifold -------------------------------------------
+// One-sided reduced manifold: shape A (pairs[5i+3]) is the sampled mesh, shape
+// B (pairs[5i+4]) the SDF.  pairs[i] = {env, slotA, slotB, shapeA,
+// shapeB}; poses[(env*n_slot + slot)*8 + ...] = t(3), q(w,x,y,z), pad.
+// Contacts of pair i occupy rows [off_i, off_i + F_A) in input pair order.
+// Per contact c (row-major arrays):
+//   point[3], normal[3] (raw fused, Reading #24), depth, W, qv[3] (compact J),
+//   ddepth[12], dnormal[36] ([i*12+j] = d n_i / d q_j), dom (int),
+//   J[36] (literal sum_i z_i gamma_i J_i, [r*12+c]), z[6], dcand[6], gam[6].
+// q = (dt_A, dtheta_A, dt_B, dtheta_B), world-frame left twists (Reading #28).
+int ora_contact_manifold(void* s, const int* pairs, long n_pairs, const double* poses, long n_env, int n_slot,
+                         double* point, double* normal, double* depth, double* W, double* qv, double* ddepth,
+                         double* dnormal, int* dom, double* J, double* zout, double* dcand, double* gout,
+                         int n_threads) {
+  Scene* sc = (Scene*)s;
+  const Smooth sp = sc->sp;
+  (void)n_env;
+  std::vector<long> off(n_pairs + 1, 0);
+  for (long i = 0; i < n_pairs; ++i) off[i + 1] = off[i] + sc->shapes[pairs[5 * i + 3]].mesh.F;
+#ifdef _OPENMP
+  if (n_threads > 0) omp_set_num_threads(n_threads);
+#endif
+#pragma omp parallel for schedule(dynamic, 1)
+  for (long pi = 0; pi < n_pairs; ++pi) {
+    const int* pr = pairs + 5 * pi;
+    const Shape& SA = sc->shapes[pr[3]];
+    const Shape& SB = sc->shapes[pr[4]];
+    const Mesh& m = SA.mesh;
+    const double* pa = poses + 8 * ((long)pr[0] * n_slot + pr[1]);
+    const double* pb = poses + 8 * ((long)pr[0] * n_slot + pr[2]);
+    double RA[9], RB[9], tA[3] = {pa[0], pa[1], pa[2]}, tB[3] = {pb[0], pb[1], pb[2]};
+    double qa[4] = {pa[3], pa[4], pa[5], pa[6]}, qb[4] = {pb[3], pb[4], pb[5], pb[6]};
+    quat_to_R(qa, RA); quat_to_R(qb, RB);
+
+    // q-jet poses (first order, 12 seeds)
+    D12 dtA[3], wA[3], dtB[3], wB[3];
+    for (int i = 0; i < 3; ++i) {
+      dtA[i] = D12(0.0); dtA[i].d[i] = 1.0;
+      wA[i] = D12(0.0); wA[i].d[3 + i] = 1.0;
+      dtB[i] = D12(0.0); dtB[i].d[6 + i] = 1.0;
+      wB[i] = D12(0.0); wB[i].d[9 + i] = 1.0;
+    }
+    D12 RAq[9], tAq[3], RBq[9], tBq[3];
+    perturbed_pose(RA, tA, dtA, wA, RAq, tAq);
+    perturbed_pose(RB, tB, dtB, wB, RBq, tBq);
+    // the same poses lifted to the nested type (inner jet = world point)
+    N12 RBn[9], tBn[3];
+    auto lift = [](const D12& a) { N12 r(0.0); r.v.v = a.v; for (int j = 0; j < 12; ++j) r.d[j].v = a.d[j]; return r; };
+    for (int i = 0; i < 9; ++i) RBn[i] = lift(RBq[i]);
+    for (int i = 0; i < 3; ++i) tBn[i] = lift(tBq[i]);
+
+    // world position of a local point of A as a q-jet
+    auto world_of = [&](const double* v, D12* p) {
+      for (int i = 0; i < 3; ++i) p[i] = RAq[i * 3 + 0] * v[0] + RAq[i * 3 + 1] * v[1] + RAq[i * 3 + 2] * v[2] + tAq[i];
+    };
+    auto phi1 = [&](const D12* p) { return shape_phi_world(SB, RBq, tBq, p, sp); };
+    // second-order candidate evaluation: d, n = grad phi (world), both q-jets
+    auto cand = [&](const D12* p, D12& dd, D12* nn) {
+      N12 X[3];
+      for (int i = 0; i < 3; ++i) {
+        X[i] = N12(0.0);
+        X[i].v.v = p[i].v; X[i].v.d[i] = 1.0;
+        for (int j = 0; j < 12; ++j) X[i].d[j].v = p[i].d[j];
+      }
+      N12 ph = shape_phi_world(SB, RBn, tBn, X, sp);
+      dd = D12(0.0); dd.v = ph.v.v;
+      for (int j = 0; j < 12; ++j) dd.d[j] = ph.d[j].v;
+      for (int i = 0; i < 3; ++i) {
+        nn[i] = D12(0.0); nn[i].v = ph.v.d[i];
+        for (int j = 0; j < 12; ++j) nn[i].d[j] = ph.d[j].d[i];
+      }
+    };
+
+    // vertices: position, depth, normal
+    std::vector<D12> vp(3 * m.V), vd(m.V), vn(3 * m.V);
+    for (int k = 0; k < m.V; ++k) {
+      world_of(&m.v[3 * k], &vp[3 * k]);
+      cand(&vp[3 * k], vd[k], &vn[3 * k]);
+    }
+    // edges: sphere trace both corners (Fig. 2), 3 gated steps
+    // each (Reading #19, #20), soft clip to the edge (Reading #21), midpoint
+    std::vector<D12> ep(3 * m.E), ed(m.E), en(3 * m.E);
+    for (int e = 0; e < m.E; ++e) {
+      const double* vI = &m.v[3 * m.e[2 * e]];
+      const double* vII = &m.v[3 * m.e[2 * e + 1]];
+      double dl[3] = {vII[0] - vI[0], vII[1] - vI[1], vII[2] - vI[2]};
+      double L = std::sqrt(dot3(dl, dl));
+      double etl[3] = {dl[0] / L, dl[1] / L, dl[2] / L};
+      D12 pI[3], et[3];
+      world_of(vI, pI);
+      for (int i = 0; i < 3; ++i) et[i] = RAq[i * 3 + 0] * etl[0] + RAq[i * 3 + 1] * etl[1] + RAq[i * 3 + 2] * etl[2];
+      D12 alpha(0.0), beta(L);
+      for (int it = 0; it < sp.trace_iters; ++it) {
+        D12 x[3];
+        for (int i = 0; i < 3; ++i) x[i] = pI[i] + alpha * et[i];
+        D12 ph = phi1(x);
+        alpha = alpha + sigmoid(ph / sp.tau_cmp) * ph;
+      }
+      for (int it = 0; it < sp.trace_iters; ++it) {
+        D12 x[3];
+        for (int i = 0; i < 3; ++i) x[i] = pI[i] + beta * et[i];
+        D12 ph = phi1(x);
+        beta = beta - sigmoid(ph / sp.tau_cmp) * ph;
+      }
+      D12 at = softclip(alpha, 0.0, L, sp.tau_clip_alpha);
+      D12 bt = softclip(beta, 0.0, L, sp.tau_clip_alpha);
+      D12 ab = 0.5 * (at + bt);
+      for (int i = 0; i < 3; ++i) ep[3 * e + i] = pI[i] + ab * et[i];
+      cand(&ep[3 * e], ed[e], &en[3 * e]);
+    }
+    // per-face fusion
+    for (int f = 0; f < m.F; ++f) {
+      long c = off[pi] + f;
+      const D12* P6[6]; D12 dd[6]; const D12* N6[6];
+      for (int k = 0; k < 3; ++k) {
+        int vi = m.f[3 * f + k];
+        P6[k] = &vp[3 * vi]; dd[k] = vd[vi]; N6[k] = &vn[3 * vi];
+        int ei = m.fe[3 * f + k];
+        P6[3 + k] = &ep[3 * ei]; dd[3 + k] = ed[ei]; N6[3 + k] = &en[3 * ei];
+      }
+      D12 negd[6], z[6], gam[6];
+      for (int i = 0; i < 6; ++i) negd[i] = -dd[i];
+      softargmax(negd, 6, sp.tau_min, z);                   // z = s_argmax(-d)
+      for (int i = 0; i < 6; ++i) gam[i] = sigmoid(-dd[i] / sp.tau_cmp);  // [[d < 0]]
+      D12 n3[3] = {D12(0.0), D12(0.0), D12(0.0)}, Wf(0.0), q3[3] = {D12(0.0), D12(0.0), D12(0.0)};
+      D12 pt3[3] = {D12(0.0), D12(0.0), D12(0.0)};
+      for (int i = 0; i < 6; ++i) {
+        D12 zg = z[i] * gam[i];
+        for (int k = 0; k < 3; ++k) {
+          n3[k] = n3[k] + zg * N6[i][k];                     // n = sum z gamma n_i
+          q3[k] = q3[k] + zg * P6[i][k];
+          pt3[k] = pt3[k] + z[i] * P6[i][k];                 // reporting only
+        }
+        Wf = Wf + zg;
+      }
+      D12 dep = -lse(negd, 6, sp.tau_min);                 // smooth min (Reading #25)
+      // dominant candidate: argmax z_i gamma_i, lowest index on exact ties
+      int im = 0; double best = -1.0;
+      for (int i = 0; i < 6; ++i) { double v = val(z[i]) * val(gam[i]); if (v > best) { best = v; im = i; } }
+      // literal fused contact Jacobian J = sum z_i gamma_i J_i, J_i = [I, -[p-tA]x, -I, [p-tB]x]
+      double Jc[36] = {0};
+      for (int i = 0; i < 6; ++i) {
+        double zg = val(z[i]) * val(gam[i]);
+        double ra[3], rb[3];
+        for (int k = 0; k < 3; ++k) { ra[k] = P6[i][k].v - tA[k]; rb[k] = P6[i][k].v - tB[k]; }
+        double Ka[9] = {0, -ra[2], ra[1], ra[2], 0, -ra[0], -ra[1], ra[0], 0};
+        double Kb[9] = {0, -rb[2], rb[1], rb[2], 0, -rb[0], -rb[1], rb[0], 0};
+        for (int r = 0; r < 3; ++r) {
+          Jc[r * 12 + r] += zg;
+          Jc[r * 12 + 6 + r] -= zg;
+          for (int k = 0; k < 3; ++k) {
+            Jc[r * 12 + 3 + k] -= zg * Ka[r * 3 + k];
+            Jc[r * 12 + 9 + k] += zg * Kb[r * 3 + k];
+          }
+        }
+      }
+      for (int k = 0; k < 3; ++k) {
+        point[3 * c + k] = pt3[k].v;
+        normal[3 * c + k] = n3[k].v;
+        qv[3 * c + k] = q3[k].v;
+        for (int j = 0; j < 12; ++j) dnormal[36 * c + k * 12 + j] = n3[k].d[j];
+      }
+      depth[c] = dep.v; W[c] = Wf.v; dom[c] = im;
+      for (int j = 0; j < 12; ++j) ddepth[12 * c + j] = dep.d[j];
+      for (int k = 0; k < 36; ++k) J[36 * c + k] = Jc[k];
+      for (int i = 0; i < 6; ++i) { zout[6 * c + i] = z[i].v; dcand[6 * c + i] = dd[i].v; gout[6 * c + i] = gam[i].v; }
+    }
+  }
+  return 0;
+}
+
+int ora_max_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+}  // extern "C"

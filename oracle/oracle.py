@@ -1,0 +1,225 @@
+"""ctypes wrapper of the FP64 oracle (oracle/oracle.cpp).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs.  The product package never
+imports this module.  It packs the shared scene descriptions
+(paper_2604_17538_b200.synth) into the oracle's own record layout; it shares
+no code with the product binding.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(HERE, "liboracle.so")
+SRC = os.path.join(HERE, "oracle.cpp")
+
+MAXP, MAXC = 8, 32
+NI, NF = 3 + MAXC, 93
+TYPES = {"halfspace": 0, "sq": 1, "psq": 2, "xpsq": 3, "union": 10, "intersection": 11, "subtraction": 12}
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-fopenmp", "-fPIC", "-shared", "-o", LIB, SRC])
+    return LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(LIB)
+        d, i, l, p = C.c_double, C.c_int, C.c_long, C.c_void_p
+        L.ora_scene_create.restype = p
+        L.ora_scene_create.argtypes = [i, p, p, p, p, p, p, p, p, i]
+        L.ora_scene_destroy.argtypes = [p]
+        for n, a in (("ora_sigmoid", [d]), ("ora_softplus", [d, d]), ("ora_softclip", [d, d, d, d]),
+                     ("ora_lse", [p, i, d]), ("ora_sq_f", [p, d, d, p]), ("ora_sq_phi", [p, d, d, p])):
+            getattr(L, n).restype = d
+            getattr(L, n).argtypes = a
+        L.ora_softargmax.argtypes = [p, i, d, p]
+        L.ora_xpsq_roots.argtypes = [p, i, i, p, p, p, p]
+        L.ora_xpsq_frame.argtypes = [p, i, i, d, p]
+        L.ora_xpsq_class.argtypes = [p, i, i]
+        L.ora_mesh_counts.argtypes = [p, i, p, p, p]
+        L.ora_mesh_topology.argtypes = [p, i, p, p]
+        L.ora_sdf_eval.argtypes = [p, p, p, p, l, l, i, p, p, p, p, p, p]
+        L.ora_contact_manifold.argtypes = [p, p, l, p, l, i] + [p] * 12 + [i]
+        L.ora_max_threads.restype = i
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+# ---- unit functions ---------------------------------------------------------
+def sigmoid(x):
+    return lib().ora_sigmoid(float(x))
+
+
+def softplus(x, tau):
+    return lib().ora_softplus(float(x), float(tau))
+
+
+def softclip(x, lo, hi, tau):
+    return lib().ora_softclip(float(x), float(lo), float(hi), float(tau))
+
+
+def lse(xs, tau):
+    a = np.ascontiguousarray(xs, dtype=np.float64)
+    return lib().ora_lse(_ptr(a), len(a), float(tau))
+
+
+def softargmax(xs, tau):
+    a = np.ascontiguousarray(xs, dtype=np.float64)
+    out = np.zeros_like(a)
+    lib().ora_softargmax(_ptr(a), len(a), float(tau), _ptr(out))
+    return out
+
+
+def sq_f(y, eps, a):
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return lib().ora_sq_f(_ptr(y), float(eps[0]), float(eps[1]), _ptr(a))
+
+
+def sq_phi(y, eps, a):
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return lib().ora_sq_phi(_ptr(y), float(eps[0]), float(eps[1]), _ptr(a))
+
+
+# ---- scenes -----------------------------------------------------------------
+def _pack_nodes(nodes):
+    ints = np.zeros((len(nodes), NI), dtype=np.int32)
+    flts = np.zeros((len(nodes), NF), dtype=np.float32)
+    for k, n in enumerate(nodes):
+        ints[k, 0] = TYPES[n["type"]]
+        ints[k, 1] = len(n["children"])
+        np_ = len(n["planes"])
+        assert np_ <= MAXP and len(n["children"]) <= MAXC
+        ints[k, 2] = np_
+        ints[k, 3:3 + len(n["children"])] = n["children"]
+        row = list(n["pose"]) + list(n["eps"][0]) + list(n["eps"][1]) + list(n["a"][0]) + list(n["a"][1])
+        pl = np.zeros((2, MAXP, 4), dtype=np.float64)
+        for j, r in enumerate(n["planes"]):
+            pl[0, j] = r
+        p1 = n["planes1"] if n["planes1"] else n["planes"]
+        for j, r in enumerate(p1):
+            pl[1, j] = r
+        row += list(pl.ravel()) + list(n["ctrl"]) + list(n["up"])
+        assert len(row) == NF
+        flts[k] = row
+    return ints, flts
+
+
+class OracleScene:
+    def __init__(self, scene):
+        self.scene = scene
+        shapes = scene.shapes
+        counts, ints, flts, vc, vs, fc, fs = [], [], [], [], [], [], []
+        for s in shapes:
+            nodes = s.sdf or []
+            counts.append(len(nodes))
+            if nodes:
+                i_, f_ = _pack_nodes(nodes)
+                ints.append(i_)
+                flts.append(f_)
+            v = s.vertices if s.vertices is not None else np.zeros((0, 3), np.float32)
+            f = s.faces if s.faces is not None else np.zeros((0, 3), np.int32)
+            vc.append(len(v))
+            fc.append(len(f))
+            vs.append(v)
+            fs.append(f)
+        self._keep = [np.ascontiguousarray(np.array(counts, dtype=np.int32)),
+                      np.ascontiguousarray(np.concatenate(ints) if ints else np.zeros((1, NI), np.int32)),
+                      np.ascontiguousarray(np.concatenate(flts) if flts else np.zeros((1, NF), np.float32)),
+                      np.ascontiguousarray(np.array(vc, dtype=np.int32)),
+                      np.ascontiguousarray(np.concatenate(vs).astype(np.float32)),
+                      np.ascontiguousarray(np.array(fc, dtype=np.int32)),
+                      np.ascontiguousarray(np.concatenate(fs).astype(np.int32))]
+        sp = scene.smooth
+        self._sm = np.array([sp["tau_cmp"], sp["tau_min"], sp["tau_clip_alpha"], sp["tau_clip_t"], sp["tau_delta"]],
+                            dtype=np.float64)
+        k = self._keep
+        self.h = lib().ora_scene_create(len(shapes), _ptr(k[0]), _ptr(k[1]), _ptr(k[2]), _ptr(k[3]), _ptr(k[4]),
+                                        _ptr(k[5]), _ptr(k[6]), _ptr(self._sm), int(sp["trace_iters"]))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ora_scene_destroy(self.h)
+            self.h = None
+
+    def mesh_counts(self, shape):
+        V, E, F = C.c_int(), C.c_int(), C.c_int()
+        lib().ora_mesh_counts(self.h, shape, C.byref(V), C.byref(E), C.byref(F))
+        return V.value, E.value, F.value
+
+    def mesh_topology(self, shape):
+        V, E, F = self.mesh_counts(shape)
+        e = np.zeros((E, 2), np.int32)
+        fe = np.zeros((F, 3), np.int32)
+        lib().ora_mesh_topology(self.h, shape, _ptr(e), _ptr(fe))
+        return e, fe
+
+    def xpsq_roots(self, shape, node, y):
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        t = np.zeros(3)
+        dl, wn = C.c_double(), C.c_double()
+        lib().ora_xpsq_roots(self.h, shape, node, _ptr(y), _ptr(t), C.byref(dl), C.byref(wn))
+        return t, dl.value, wn.value
+
+    def xpsq_frame(self, shape, node, t):
+        R = np.zeros(9)
+        lib().ora_xpsq_frame(self.h, shape, node, float(t), _ptr(R))
+        return R.reshape(3, 3)
+
+    def xpsq_class(self, shape, node):
+        return lib().ora_xpsq_class(self.h, shape, node)
+
+    def sdf_eval(self, shape_ids, poses, points, P, want_pose=True):
+        shape_ids = np.ascontiguousarray(shape_ids, dtype=np.int32)
+        # float32 inputs are promoted exactly; float64 inputs (finite-difference
+        # tests) are used as given
+        poses = np.ascontiguousarray(poses, dtype=np.float64).reshape(-1, 8)
+        points = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+        B = len(shape_ids)
+        N = B * P
+        assert points.shape[0] == N
+        out = dict(d=np.zeros(N), grad=np.zeros((N, 3)), hess=np.zeros((N, 6)), dpose=np.zeros((N, 6)),
+                   d2pose=np.zeros((N, 21)), dxdpose=np.zeros((N, 18)))
+        lib().ora_sdf_eval(self.h, _ptr(shape_ids), _ptr(poses), _ptr(points), B, P, int(want_pose),
+                           *[_ptr(out[k]) for k in ("d", "grad", "hess", "dpose", "d2pose", "dxdpose")])
+        return out
+
+    def contact_manifold(self, pairs=None, poses=None, n_threads=0):
+        sc = self.scene
+        pairs = np.ascontiguousarray(sc.pairs if pairs is None else pairs, dtype=np.int32)
+        poses = np.ascontiguousarray(sc.poses if poses is None else poses, dtype=np.float64)
+        n_env, n_slot = poses.shape[0], poses.shape[1]
+        F = [self.mesh_counts(int(a))[2] for a in pairs[:, 3]]
+        Ct = int(sum(F))
+        out = dict(point=np.zeros((Ct, 3)), normal=np.zeros((Ct, 3)), depth=np.zeros(Ct), W=np.zeros(Ct),
+                   q=np.zeros((Ct, 3)), ddepth=np.zeros((Ct, 12)), dnormal=np.zeros((Ct, 3, 12)),
+                   dom=np.zeros(Ct, np.int32), J=np.zeros((Ct, 3, 12)), z=np.zeros((Ct, 6)),
+                   dcand=np.zeros((Ct, 6)), gamma=np.zeros((Ct, 6)))
+        lib().ora_contact_manifold(self.h, _ptr(pairs), len(pairs), _ptr(poses), n_env, n_slot,
+                                   *[_ptr(out[k]) for k in ("point", "normal", "depth", "W", "q", "ddepth",
+                                                            "dnormal", "dom", "J", "z", "dcand", "gamma")],
+                                   int(n_threads))
+        out["offsets"] = np.concatenate([[0], np.cumsum(F)]).astype(np.int64)
+        return out
+
+
+def max_threads():
+    return lib().ora_max_threads()

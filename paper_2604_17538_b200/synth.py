@@ -1,0 +1,447 @@
+"""Seeded synthetic inputs shared by the oracle, the CUDA path, the tests and
+bench.py.
+
+This module holds NO arithmetic of the method (no SDF, no projection, no
+trace, no fusion): it only builds shape *descriptions* (plain parameter
+dicts), static sampled-surface meshes (vertices + triangles, an input of the
+method) and poses.  Meshes of superquadrics are built from the
+textbook parametric superellipsoid surface (signed powers of cos/sin), not
+from the paper's implicit Eq. (1).
+
+Every float is generated in FP64 and rounded once to FP32; both the oracle
+and the CUDA path consume the identical FP32 values (SURVEY §8c.1 step 9,
+"input hygiene").
+
+Configs (BASELINE.json `configs`, recipe in DESIGN.md §4):
+  C1 single SQ on a plane, both directions, plus sdf_eval at 64 points
+  C2 MESH box on an SQ box, parallel / slightly tilted faces, 1k envs
+  C3 plane patch vs an 18-SQ smooth union, 16k envs
+  C4 20 capsule-like SQ links vs a cup (cylinder (-) cylinder (+) XPSQ handle)
+  C5 mixed sampled kinds x 32 SDF prototypes, 1k..1M envs
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+F32 = np.float32
+IDENTITY_POSE = [0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0]
+
+# default temperatures (reading #1), per unit
+# length scale ell
+DEFAULT_SMOOTH = dict(tau_cmp=1e-3, tau_min=1e-2, tau_clip_alpha=1e-3, tau_clip_t=1e-3, tau_delta=1e-4,
+                      trace_iters=3)
+
+
+def smooth_params(ell: float = 1.0) -> dict:
+    """Temperatures scaled to the scene length scale ell (lengths scale,
+    dimensionless ones do not)."""
+    p = dict(DEFAULT_SMOOTH)
+    for k in ("tau_cmp", "tau_min", "tau_clip_alpha"):
+        p[k] = float(F32(p[k] * ell))
+    return p
+
+
+# ---------------------------------------------------------------------------
+# shape descriptions
+# ---------------------------------------------------------------------------
+def _f32(x):
+    return [float(v) for v in np.asarray(x, dtype=np.float64).astype(F32).ravel()]
+
+
+@dataclass
+class Node:
+    type: str
+    pose: list = field(default_factory=lambda: list(IDENTITY_POSE))
+    children: list = field(default_factory=list)
+    eps: list = field(default_factory=lambda: [[1.0, 1.0], [1.0, 1.0]])
+    a: list = field(default_factory=lambda: [[1.0, 1.0, 1.0], [1.0, 1.0, 1.0]])
+    planes: list = field(default_factory=list)     # endpoint-0 rows [nx, ny, nz, h]
+    planes1: list = field(default_factory=list)    # endpoint-1 rows (XPSQ)
+    ctrl: list = field(default_factory=lambda: [0.0] * 9)
+    up: list = field(default_factory=lambda: [0.0, 0.0, 1.0])
+
+
+def _unit_rows(rows):
+    out = []
+    for r in rows:
+        n = np.asarray(r[:3], dtype=np.float64)
+        n = n / np.linalg.norm(n)
+        out.append(_f32([n[0], n[1], n[2], r[3]]))
+    return out
+
+
+def halfspace(n, h, pose=None):
+    """phi = y.n + h; inside where y.n + h <= 0."""
+    return Node("halfspace", pose=_f32(pose or IDENTITY_POSE), planes=_unit_rows([[*n, h]]))
+
+
+def sq(a, eps, pose=None):
+    return Node("sq", pose=_f32(pose or IDENTITY_POSE), eps=[_f32(eps), _f32(eps)], a=[_f32(a), _f32(a)])
+
+
+def psq(a, eps, planes, pose=None):
+    return Node("psq", pose=_f32(pose or IDENTITY_POSE), eps=[_f32(eps), _f32(eps)], a=[_f32(a), _f32(a)],
+                planes=_unit_rows(planes))
+
+
+def xpsq(ctrl, a0, eps0, a1=None, eps1=None, planes0=(), planes1=None, up=(0.0, 0.0, 1.0), pose=None):
+    a1 = a0 if a1 is None else a1
+    eps1 = eps0 if eps1 is None else eps1
+    planes1 = planes0 if planes1 is None else planes1
+    return Node("xpsq", pose=_f32(pose or IDENTITY_POSE), eps=[_f32(eps0), _f32(eps1)], a=[_f32(a0), _f32(a1)],
+                planes=_unit_rows(planes0), planes1=_unit_rows(planes1), ctrl=_f32(ctrl), up=_f32(up))
+
+
+def op(kind, children, pose=None):
+    assert kind in ("union", "intersection", "subtraction")
+    return Node(kind, pose=_f32(pose or IDENTITY_POSE), children=list(children))
+
+
+def flatten(root: Node) -> list:
+    """Pre-order node list, root first; children become indices."""
+    out = []
+
+    def rec(n: Node) -> int:
+        idx = len(out)
+        d = dict(type=n.type, pose=list(n.pose), eps=n.eps, a=n.a, planes=n.planes, planes1=n.planes1,
+                 ctrl=n.ctrl, up=n.up, children=[])
+        out.append(d)
+        d["children"] = [rec(c) for c in n.children]
+        return idx
+
+    rec(root)
+    return out
+
+
+@dataclass
+class Shape:
+    name: str
+    sdf: list | None            # flattened node list (root first) or None
+    vertices: np.ndarray | None  # [V,3] float32 local frame (sampled side)
+    faces: np.ndarray | None     # [F,3] int32
+
+
+def make_shape(name, root: Node | None, mesh=None) -> Shape:
+    v, f = (None, None) if mesh is None else mesh
+    return Shape(name, None if root is None else flatten(root),
+                 None if v is None else np.ascontiguousarray(v, dtype=F32),
+                 None if f is None else np.ascontiguousarray(f, dtype=np.int32))
+
+
+# ---------------------------------------------------------------------------
+# static sampled surfaces (inputs of the method)
+# ---------------------------------------------------------------------------
+def cube_grid(k: int):
+    """Closed triangulated cube surface [-1,1]^3 with k x k cells per face:
+    V = 6k^2 + 2, F = 12 k^2, outward winding."""
+    key = {}
+    verts = []
+
+    def vid(ix, iy, iz):
+        t = (ix, iy, iz)
+        if t not in key:
+            key[t] = len(verts)
+            verts.append([2.0 * ix / k - 1.0, 2.0 * iy / k - 1.0, 2.0 * iz / k - 1.0])
+        return key[t]
+
+    faces = []
+    for axis in range(3):
+        for side in (0, k):
+            u_ax, v_ax = [a for a in range(3) if a != axis]
+            for i in range(k):
+                for j in range(k):
+                    q = []
+                    for di, dj in ((0, 0), (1, 0), (1, 1), (0, 1)):
+                        c = [0, 0, 0]
+                        c[axis] = side
+                        c[u_ax] = i + di
+                        c[v_ax] = j + dj
+                        q.append(vid(*c))
+                    # orientation: outward normal along +axis when side == k
+                    e1 = np.subtract(verts[q[1]], verts[q[0]])
+                    e2 = np.subtract(verts[q[2]], verts[q[0]])
+                    nrm = np.cross(e1, e2)
+                    outward = (1.0 if side == k else -1.0)
+                    if nrm[axis] * outward < 0:
+                        q = q[::-1]
+                    faces.append([q[0], q[1], q[2]])
+                    faces.append([q[0], q[2], q[3]])
+    return np.asarray(verts, dtype=np.float64), np.asarray(faces, dtype=np.int32)
+
+
+def box_mesh(half, s: int):
+    """Polyhedral box with half sizes `half`, each face s x s cells."""
+    v, f = cube_grid(s)
+    return (v * np.asarray(half, dtype=np.float64)).astype(F32), f
+
+
+def _spow(x, e):
+    return np.sign(x) * np.abs(x) ** e
+
+
+def sq_mesh(a, eps, k: int):
+    """Cube-sphere topology (k x k per face) placed on the superellipsoid
+    surface by its textbook parametric form
+      x = a1 C(eta)^e1 C(w)^e2, y = a2 C(eta)^e1 S(w)^e2, z = a3 S(eta)^e1
+    with (eta, w) the latitude/longitude of the (tangent-warped) cube
+    direction."""
+    v, f = cube_grid(k)
+    w = np.tan(v * (math.pi / 4.0))
+    d = w / np.linalg.norm(w, axis=1, keepdims=True)
+    eta = np.arcsin(np.clip(d[:, 2], -1.0, 1.0))
+    om = np.arctan2(d[:, 1], d[:, 0])
+    e1, e2 = eps
+    ce = _spow(np.cos(eta), e1)
+    p = np.stack([a[0] * ce * _spow(np.cos(om), e2), a[1] * ce * _spow(np.sin(om), e2),
+                  a[2] * _spow(np.sin(eta), e1)], axis=1)
+    return p.astype(F32), f
+
+
+def plane_patch(n: int, m: int, sx: float, sy: float):
+    """n x m vertex grid on z = 0, centred, size sx x sy; 2 triangles/cell,
+    upward (+z) winding.  F = 2(n-1)(m-1)."""
+    xs = np.linspace(-sx / 2, sx / 2, n)
+    ys = np.linspace(-sy / 2, sy / 2, m)
+    X, Y = np.meshgrid(xs, ys, indexing="ij")
+    v = np.stack([X.ravel(), Y.ravel(), np.zeros(n * m)], axis=1)
+    f = []
+    for i in range(n - 1):
+        for j in range(m - 1):
+            a, b, c, d = i * m + j, (i + 1) * m + j, (i + 1) * m + j + 1, i * m + j + 1
+            f.append([a, b, c])
+            f.append([a, c, d])
+    return v.astype(F32), np.asarray(f, dtype=np.int32)
+
+
+# ---------------------------------------------------------------------------
+# poses
+# ---------------------------------------------------------------------------
+def quat_from_axis_angle(axis, ang):
+    axis = np.asarray(axis, dtype=np.float64)
+    axis = axis / np.linalg.norm(axis)
+    return np.concatenate([[math.cos(ang / 2)], math.sin(ang / 2) * axis])
+
+
+def quat_mul(p, q):
+    w1, x1, y1, z1 = p
+    w2, x2, y2, z2 = q
+    return np.array([w1 * w2 - x1 * x2 - y1 * y2 - z1 * z2, w1 * x2 + x1 * w2 + y1 * z2 - z1 * y2,
+                     w1 * y2 - x1 * z2 + y1 * w2 + z1 * x2, w1 * z2 + x1 * y2 - y1 * x2 + z1 * w2])
+
+
+def quat_to_mat(q):
+    q = np.asarray(q, dtype=np.float64)
+    q = q / np.linalg.norm(q)
+    w, x, y, z = q
+    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                     [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                     [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+
+
+def random_quats(rng, n):
+    """Uniform on SO(3) (normalised 4-D Gaussian; equivalent to the subgroup
+    algorithm of)."""
+    q = rng.standard_normal((n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    q[q[:, 0] < 0] *= -1
+    return q
+
+
+def pose_row(t, q):
+    return np.array([t[0], t[1], t[2], q[0], q[1], q[2], q[3], 0.0])
+
+
+# ---------------------------------------------------------------------------
+# scenes
+# ---------------------------------------------------------------------------
+@dataclass
+class Scene:
+    name: str
+    shapes: list
+    smooth: dict
+    pairs: np.ndarray          # [NP, 5] int32: env, slotA, slotB, shapeA (sampled), shapeB (SDF)
+    poses: np.ndarray          # [n_env, n_slot, 8] float32
+    ell: float = 1.0
+    points: np.ndarray | None = None    # sdf_eval queries [B*P, 3]
+    point_shapes: np.ndarray | None = None
+    point_poses: np.ndarray | None = None  # [B, 8]
+    P: int = 0
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def n_env(self):
+        return self.poses.shape[0]
+
+    @property
+    def n_slot(self):
+        return self.poses.shape[1]
+
+    def slice_envs(self, lo: int, hi: int) -> "Scene":
+        """Env range [lo, hi) with env ids renumbered from 0 (rank shard)."""
+        m = (self.pairs[:, 0] >= lo) & (self.pairs[:, 0] < hi)
+        pr = self.pairs[m].copy()
+        pr[:, 0] -= lo
+        return Scene(self.name, self.shapes, self.smooth, np.ascontiguousarray(pr),
+                     np.ascontiguousarray(self.poses[lo:hi]), self.ell, meta=dict(self.meta, env_lo=lo, env_hi=hi))
+
+
+def c1_scene() -> Scene:
+    """C1: SQ rounded box (a=(.20,.15,.10), eps=0.3) resting on z<=0 with
+    2e-3 penetration, 2 deg tilt, 17 deg yaw; both directions; plus sdf_eval
+    of the SQ at the 64 plane-patch points."""
+    a, eps = (0.20, 0.15, 0.10), (0.3, 0.3)
+    box = make_shape("sq_box", sq(a, eps), sq_mesh(a, eps, 3))
+    ground = make_shape("ground", halfspace((0, 0, 1), 0.0), plane_patch(8, 8, 0.6, 0.6))
+    q = quat_mul(quat_from_axis_angle((0, 0, 1), math.radians(17.0)),
+                 quat_from_axis_angle((1, 0, 0), math.radians(2.0)))
+    Rm = quat_to_mat(q)
+    vz = (box.vertices.astype(np.float64) @ Rm.T)[:, 2]
+    t = np.array([0.01, -0.02, -vz.min() - 2e-3])
+    poses = np.zeros((1, 2, 8))
+    poses[0, 0] = pose_row(t, q)
+    poses[0, 1] = pose_row((0, 0, 0), (1, 0, 0, 0))
+    pairs = np.array([[0, 0, 1, 0, 1], [0, 1, 0, 1, 0]], dtype=np.int32)
+    sc = Scene("C1", [box, ground], smooth_params(1.0), pairs, poses.astype(F32))
+    # sdf_eval: the box SDF at the 64 patch points lifted to z = 0.05
+    pts = ground.vertices.astype(np.float64).copy()
+    pts[:, 2] = 0.05 + 0.1 * (pts[:, 0] + 0.3)
+    sc.points = pts.astype(F32)
+    sc.point_shapes = np.array([0], dtype=np.int32)
+    sc.point_poses = poses[0, 0:1].astype(F32)
+    sc.P = 64
+    return sc
+
+
+def c2_scene(n_env: int = 1000, seed: int = 2) -> Scene:
+    """C2: MESH box side 0.2 (6x6 per face, V=218) on an SQ box
+    a=(.1,.1,.1), eps=0.1; B at origin; A at z = 0.2 - delta."""
+    rng = np.random.Generator(np.random.Philox(key=seed))
+    top = make_shape("mesh_box", None, box_mesh((0.1, 0.1, 0.1), 6))
+    base = make_shape("sq_box", sq((0.1, 0.1, 0.1), (0.1, 0.1)), None)
+    delta = rng.uniform(0.0, 0.01, n_env)
+    lat = rng.uniform(-0.05, 0.05, (n_env, 2))
+    yaw = rng.uniform(0.0, 2 * math.pi, n_env)
+    tilt = rng.uniform(0.0, math.radians(0.5), n_env) * (rng.uniform(size=n_env) < 0.5)
+    tax = rng.uniform(0.0, 2 * math.pi, n_env)
+    poses = np.zeros((n_env, 2, 8))
+    for e in range(n_env):
+        q = quat_mul(quat_from_axis_angle((math.cos(tax[e]), math.sin(tax[e]), 0.0), tilt[e]),
+                     quat_from_axis_angle((0, 0, 1), yaw[e]))
+        poses[e, 0] = pose_row((lat[e, 0], lat[e, 1], 0.2 - delta[e]), q)
+        poses[e, 1] = pose_row((0, 0, 0), (1, 0, 0, 0))
+    pairs = np.stack([np.arange(n_env), np.zeros(n_env), np.ones(n_env), np.zeros(n_env), np.ones(n_env)],
+                     axis=1).astype(np.int32)
+    return Scene("C2", [top, base], smooth_params(1.0), pairs, poses.astype(F32))
+
+
+def blob18(seed: int = 3, K: int = 18):
+    """Smooth union of K random SQs (the paper's 18-SQ armadillo stand-in,
+    P:176)."""
+    rng = np.random.Generator(np.random.Philox(key=seed + 1000))
+    kids = []
+    for _ in range(K):
+        a = rng.uniform(0.04, 0.12, 3)
+        eps = rng.uniform(0.3, 1.5, 2)
+        c = rng.uniform(-0.15, 0.15, 3)
+        q = random_quats(rng, 1)[0]
+        kids.append(sq(a, eps, pose=[*c, *q]))
+    return op("union", kids)
+
+
+def _node_surface_points(node: Node, n=400):
+    """Dense parametric surface samples of the SQ leaves of a tree, in the
+    tree's frame (for placing objects; input construction only)."""
+    pts = []
+
+    def rec(nd, Rp, tp):
+        R = quat_to_mat(nd.pose[3:7])
+        t = np.asarray(nd.pose[:3])
+        Rc, tc = Rp @ R, Rp @ t + tp
+        if nd.type in ("sq", "psq", "xpsq"):
+            if nd.type == "xpsq":
+                c = np.asarray(nd.ctrl).reshape(3, 3)
+                s = np.linspace(0, 1, 20)[:, None]
+                loc = (1 - s) ** 2 * c[0] + 2 * s * (1 - s) * c[1] + s ** 2 * c[2]
+            else:
+                v, _ = sq_mesh(nd.a[0], nd.eps[0], 8)
+                loc = v.astype(np.float64)
+            pts.append(loc @ Rc.T + tc)
+        for ch in nd.children:
+            rec(ch, Rc, tc)
+
+    rec(node, np.eye(3), np.zeros(3))
+    return np.concatenate(pts, axis=0)
+
+
+def c3_scene(n_env: int = 16384, seed: int = 3, K: int = 18) -> Scene:
+    """C3: 16x32 plane patch (0.4 x 0.8) sampled vs an 18-SQ smooth union."""
+    rng = np.random.Generator(np.random.Philox(key=seed))
+    root = blob18(seed, K)
+    surf = _node_surface_points(root)
+    obj = make_shape("blob%d" % K, root, None)
+    patch = make_shape("patch", None, plane_patch(16, 32, 0.4, 0.8))
+    qs = random_quats(rng, n_env)
+    lat = np.stack([rng.uniform(-0.1, 0.1, n_env), rng.uniform(-0.2, 0.2, n_env)], axis=1)
+    pen = rng.uniform(-0.01, 0.02, n_env)
+    poses = np.zeros((n_env, 2, 8))
+    for e in range(n_env):
+        Rm = quat_to_mat(qs[e])
+        zmin = (surf @ Rm.T)[:, 2].min()
+        poses[e, 0] = pose_row((0, 0, 0), (1, 0, 0, 0))
+        poses[e, 1] = pose_row((lat[e, 0], lat[e, 1], -zmin - pen[e]), qs[e])
+    pairs = np.stack([np.arange(n_env), np.zeros(n_env), np.ones(n_env), np.ones(n_env), np.zeros(n_env)],
+                     axis=1).astype(np.int32)
+    return Scene("C3", [obj, patch], smooth_params(1.0), pairs, poses.astype(F32))
+
+
+def cup() -> Node:
+    """Cup (Fig. 3): (outer cylinder (-) inner cylinder) (+) handle
+    swept along a quadratic spline."""
+    outer = sq((0.04, 0.04, 0.05), (0.1, 1.0))
+    inner = sq((0.035, 0.035, 0.05), (0.1, 1.0), pose=[0, 0, 0.006, 1, 0, 0, 0])
+    handle = xpsq(ctrl=[0.04, 0, 0.03, 0.075, 0, 0, 0.04, 0, -0.03], a0=(0.004, 0.006, 0.004), eps0=(0.2, 0.2),
+                  up=(0, 1, 0))
+    return op("union", [op("subtraction", [outer, inner]), handle])
+
+
+def c4_scene(n_env: int = 65536, seed: int = 4, n_links: int = 20) -> Scene:
+    """C4: 20 capsule-like SQ links (cube-sphere k=3) vs a cup, ell = 0.04."""
+    rng = np.random.Generator(np.random.Philox(key=seed))
+    cup_root = cup()
+    surf = _node_surface_points(cup_root)
+    shapes = [make_shape("cup", cup_root, None)]
+    link_a = []
+    for i in range(n_links):
+        lr = np.random.Generator(np.random.Philox(key=seed + 100 + i))
+        a = (float(lr.uniform(0.008, 0.012)),) * 2 + (float(lr.uniform(0.02, 0.03)),)
+        e1 = float(lr.uniform(0.5, 1.0))
+        shapes.append(make_shape("link%d" % i, sq(a, (e1, 1.0)), sq_mesh(a, (e1, 1.0), 3)))
+        link_a.append(a)
+    yaw = rng.uniform(0, 2 * math.pi, n_env)
+    # one shell placement per (env, link)
+    dirs = rng.standard_normal((n_env, n_links, 3))
+    dirs /= np.linalg.norm(dirs, axis=2, keepdims=True)
+    clr = rng.uniform(-0.004, 0.006, (n_env, n_links))
+    lq = random_quats(rng, n_env * n_links).reshape(n_env, n_links, 4)
+    poses = np.zeros((n_env, n_links + 1, 8))
+    # object surface support distance along each direction (from samples)
+    for e in range(n_env):
+        qo = quat_from_axis_angle((0, 0, 1), yaw[e])
+        poses[e, 0] = pose_row((0, 0, 0), qo)
+        S = surf @ quat_to_mat(qo).T
+        proj = dirs[e] @ S.T                              # [links, samples]
+        sup = proj.max(axis=1)
+        for i in range(n_links):
+            r = sup[i] + clr[e, i] + link_a[i][0]
+            poses[e, 1 + i] = pose_row(dirs[e, i] * r, lq[e, i])
+    pairs = np.stack([np.repeat(np.arange(n_env), n_links), np.tile(np.arange(1, n_links + 1), n_env),
+                      np.zeros(n_env * n_links), np.tile(np.arange(1, n_links + 1), n_env),
+                      np.zeros(n_env * n_links)], axis=1).astype(np.int32)
+    return Scene("C4", shapes, smooth_params(0.04), pairs, poses.astype(F32), ell=0.04)
+
+
+def random_points(rng, n, lo, hi):
+    return rng.uniform(lo, hi, (n, 3)).astype(F32)

@@ -1,0 +1,297 @@
+"""Pins of the oracle's contact manifold (§II-C):
+topology counts, sphere-trace special cases, box-on-plane closed
+forms, sphere-sphere candidate depths, the compact contact
+Jacobian, finite differences of every derivative output over the pose chart,
+rigid-motion invariance, weight partition, smooth-min bounds and sliding
+continuity."""
+import math
+
+import numpy as np
+import pytest
+
+from helpers import scene_of, pose8, perturb, rand_pose, skew
+from paper_2604_17538_b200 import synth
+
+TAU_CMP, TAU_MIN, TAU_CLIP = 1e-3, 1e-2, 1e-3
+
+
+def _sig(x):
+    return 1.0 / (1.0 + math.exp(-x)) if x >= 0 else math.exp(x) / (1.0 + math.exp(x))
+
+
+def _sp(x, t):
+    return x + t * math.log1p(math.exp(-x / t)) if x > 0 else t * math.log1p(math.exp(x / t))
+
+
+def _manifold(O, shapes, poses, pairs, ell=1.0):
+    sc = scene_of(shapes, ell=ell, pairs=pairs, poses=poses)
+    osc = O.OracleScene(sc)
+    return osc.contact_manifold(), osc
+
+
+def test_topology_counts(oracle_mod):
+    O = oracle_mod
+    cube = synth.make_shape("c", None, synth.box_mesh((0.5, 0.5, 0.5), 1))
+    tri = synth.make_shape("t", None, (np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0]], np.float32),
+                                       np.array([[0, 1, 2]], np.int32)))
+    k3 = synth.make_shape("s", None, synth.sq_mesh((1, 1, 1), (1, 1), 3))
+    patch = synth.make_shape("p", None, synth.plane_patch(16, 32, 0.4, 0.8))
+    box6 = synth.make_shape("b", None, synth.box_mesh((0.1, 0.1, 0.1), 6))
+    osc = O.OracleScene(scene_of([cube, tri, k3, patch, box6]))
+    assert osc.mesh_counts(0) == (8, 18, 12)
+    assert osc.mesh_counts(1) == (3, 3, 1)
+    assert osc.mesh_counts(2) == (56, 162, 108)         # SURVEY §8a (C4 link)
+    assert osc.mesh_counts(3) == (512, 1441, 930)       # SURVEY §8a (C3 patch)
+    assert osc.mesh_counts(4) == (218, 648, 432)        # SURVEY §8a (C2 box)
+    for s in range(5):
+        V, E, F = osc.mesh_counts(s)
+        e, fe = osc.mesh_topology(s)
+        faces = [osc.scene.shapes[s].faces][0]
+        assert np.all(e[:, 0] < e[:, 1])
+        assert len({tuple(x) for x in e}) == E            # unique
+        for f in range(F):                                # incidence closure
+            vs = faces[f]
+            for k in range(3):
+                a, b = sorted((vs[k], vs[(k + 1) % 3]))
+                assert tuple(e[fe[f, k]]) == (a, b)
+        if s in (0, 2, 4):
+            assert 2 * E == 3 * F and V - E + F == 2         # closed
+
+
+def _segment_scene(vI, vII, sphere_r=1.0):
+    """A thin triangle whose first edge is (vI, vII), against a sphere SDF at
+    the origin."""
+    v = np.array([vI, vII, [0.0, 0.0, 10.0]], np.float32)
+    tri = synth.make_shape("t", None, (v, np.array([[0, 1, 2]], np.int32)))
+    sph = synth.make_shape("s", synth.sq((sphere_r,) * 3, (1, 1)), None)
+    poses = np.zeros((1, 2, 8), np.float32)
+    poses[0, :, 3] = 1
+    return [tri, sph], poses, np.array([[0, 0, 1, 0, 1]], np.int32)
+
+
+def test_trace_examples(oracle_mod):
+    """S:509-511 (offset by y = 0.3 from the sphere centre, where the radial
+    SQ distance is degenerate, reading #2): unit sphere, edge
+    (-2,.3,0)->(2,.3,0): the two traces are mirror images, so p_e = (0,.3,0)
+    and phi = -0.7.  v_I inside at (0,.3,0), v_II = (2,.3,0): v_I does not
+    move (gate ~ 0), soft clip moves it inward by tau ln 2, v_II follows the
+    3-step sphere-trace recursion computed here with the exact sphere SDF."""
+    O = oracle_mod
+    shapes, poses, pairs = _segment_scene([-2, 0.3, 0], [2, 0.3, 0])
+    out, _ = _manifold(O, shapes, poses, pairs)
+    assert out["dcand"][0, 3] == pytest.approx(float(np.float32(0.3)) - 1.0, abs=1e-9)
+    shapes, poses, pairs = _segment_scene([0, 0.3, 0], [2, 0.3, 0])
+    out, _ = _manifold(O, shapes, poses, pairs)
+    y = float(np.float32(0.3))
+    phi = lambda x: math.hypot(x, y) - 1.0
+    be = 2.0
+    for _ in range(3):
+        p = phi(be)
+        be = be - _sig(p / TAU_CMP) * p
+    clip = lambda x: _sp(x, TAU_CLIP) - _sp(x - 2.0, TAU_CLIP)
+    al = 0.0 + _sig(phi(0.0) / TAU_CMP) * phi(0.0)
+    assert abs(al) < 1e-300
+    ab = 0.5 * (clip(0.0) + clip(be))
+    assert clip(0.0) == pytest.approx(TAU_CLIP * math.log(2.0), rel=1e-12)
+    assert out["dcand"][0, 3] == pytest.approx(phi(ab), abs=1e-9)
+    # edge entirely outside: phi(p_e) > 0
+    shapes, poses, pairs = _segment_scene([-2, 0, 3], [2, 0, 3])
+    out, _ = _manifold(O, shapes, poses, pairs)
+    assert out["dcand"][0, 3] > 0
+
+
+def _trace_halfspace(phi0, c, L, iters=3):
+    """Exact scalar recursion on a half-space: phi(alpha) = phi0 - c alpha."""
+    G = lambda p: _sig(p / TAU_CMP) * p
+    al = 0.0
+    for _ in range(iters):
+        al = al + G(phi0 - c * al)
+    return al
+
+
+def _box_on_plane(O, delta, tilt=0.0, yaw=0.3, s=2):
+    box = synth.make_shape("b", None, synth.box_mesh((0.1, 0.1, 0.1), s))
+    ground = synth.make_shape("g", synth.halfspace((0, 0, 1), 0.0), None)
+    q = synth.quat_mul(synth.quat_from_axis_angle((1, 0, 0), tilt), synth.quat_from_axis_angle((0, 0, 1), yaw))
+    poses = np.zeros((1, 2, 8))
+    poses[0, 0] = synth.pose_row((0.01, -0.02, 0.1 - delta), q)
+    poses[0, 1] = synth.pose_row((0, 0, 0), (1, 0, 0, 0))
+    return _manifold(O, [box, ground], poses, np.array([[0, 0, 1, 0, 1]], np.int32))
+
+
+@pytest.mark.parametrize("delta", [2e-3, 0.05])
+def test_box_on_plane_closed_form(oracle_mod, delta):
+    """Polyhedral box flat on z <= 0 with penetration delta:
+    every bottom-face candidate has d = -delta, so z = 1/6, W = gamma =
+    sigma(delta/tau_cmp), n = W (0,0,1), depth = -delta - tau_min ln 6.
+    Vertical-edge midpoints follow the 3-step scalar recursion."""
+    O = oracle_mod
+    out, osc = _box_on_plane(O, delta)
+    # penetration with FP32-rounded inputs (pose z and box half-size)
+    d32 = float(np.float32(0.1)) - float(np.float32(0.1 - delta))
+    bottom = np.all(np.abs(out["dcand"] + d32) < 1e-12, axis=1)
+    assert bottom.sum() == 2 * 2 * 2                   # s = 2: 8 bottom triangles
+    gam = _sig(d32 / TAU_CMP)
+    assert np.allclose(out["z"][bottom], 1.0 / 6.0, atol=1e-12)
+    assert np.allclose(out["W"][bottom], gam, atol=1e-12)
+    assert np.allclose(out["normal"][bottom], [0, 0, gam], atol=1e-12)
+    assert np.allclose(out["depth"][bottom], -d32 - TAU_MIN * math.log(6.0), atol=1e-7)
+    # vertical edges (length 0.1 with s=2): candidate depth from the recursion
+    L = 0.1
+    # trace from the lower vertex (inside, phi0 = -delta) upwards (c = -1) and
+    # from the upper vertex (phi0 = L - delta) downwards along -e_t
+    a3 = _trace_halfspace(-d32, -1.0, L)
+    b3 = L - _trace_halfspace(L - d32, 1.0, L)
+    clip = lambda x: _sp(x, TAU_CLIP) - _sp(x - L, TAU_CLIP)
+    abar = 0.5 * (clip(a3) + clip(b3))
+    d_mid = -d32 + abar
+    found = np.isclose(out["dcand"], d_mid, atol=1e-7) | np.isclose(out["dcand"], L - d32 - abar, atol=1e-7)
+    assert found.sum() >= 8
+    if delta == 0.05:   # SURVEY App. B asymptote: -delta/2 + tau ln2 / 2
+        assert d_mid == pytest.approx(-0.024653, abs=2e-6)
+
+
+def test_sphere_sphere_candidates(oracle_mod):
+    """SQ-sphere tessellation sampled vs an SQ-sphere SDF: every vertex
+    candidate depth is |p - c_B| - r_B exactly."""
+    O = oracle_mod
+    ra, rb = 0.1, 0.15
+    A = synth.make_shape("a", None, synth.sq_mesh((ra,) * 3, (1, 1), 3))
+    B = synth.make_shape("b", synth.sq((rb,) * 3, (1, 1)), None)
+    poses = np.zeros((1, 2, 8))
+    poses[0, 0] = synth.pose_row((0.2, 0.05, 0.03), synth.random_quats(np.random.default_rng(1), 1)[0])
+    poses[0, 1] = synth.pose_row((0.0, 0.0, 0.0), (1, 0, 0, 0))
+    poses = poses.astype(np.float32).astype(np.float64)
+    out, osc = _manifold(O, [A, B], poses, np.array([[0, 0, 1, 0, 1]], np.int32))
+    Rm = synth.quat_to_mat(poses[0, 0, 3:7])
+    vw = A.vertices.astype(np.float64) @ Rm.T + poses[0, 0, :3]
+    rb32 = float(np.float32(rb))
+    for f, tri in enumerate(A.faces):
+        for k in range(3):
+            assert out["dcand"][f, k] == pytest.approx(np.linalg.norm(vw[tri[k]]) - rb32, abs=1e-9)
+
+
+def _random_pair_scene(O, seed, kind):
+    rng = np.random.default_rng(seed)
+    if kind == "sq":
+        A = synth.make_shape("a", None, synth.sq_mesh((0.08, 0.06, 0.05), (0.7, 0.9), 2))
+        B = synth.make_shape("b", synth.sq((0.1, 0.08, 0.07), (0.5, 0.8)), None)
+        ell = 1.0
+        dist = 0.14
+    elif kind == "blob":
+        A = synth.make_shape("a", None, synth.sq_mesh((0.08, 0.06, 0.05), (0.7, 0.9), 2))
+        B = synth.make_shape("b", synth.blob18(3, 4), None)
+        ell = 1.0
+        dist = 0.18
+    else:
+        A = synth.make_shape("a", None, synth.sq_mesh((0.01, 0.01, 0.025), (0.8, 1.0), 2))
+        B = synth.make_shape("b", synth.cup(), None)
+        ell = 0.04
+        dist = 0.055
+    poses = np.zeros((1, 2, 8))
+    u = rng.normal(size=3)
+    u /= np.linalg.norm(u)
+    poses[0, 0] = synth.pose_row(dist * u, synth.random_quats(rng, 1)[0])
+    poses[0, 1] = synth.pose_row(rng.uniform(-0.01, 0.01, 3), synth.random_quats(rng, 1)[0])
+    return [A, B], poses, ell
+
+
+@pytest.mark.parametrize("kind,seed", [("sq", 1), ("sq", 2), ("blob", 3), ("cup", 4)])
+def test_manifold_derivatives_fd(oracle_mod, kind, seed):
+    """ddepth/dq and dnormal/dq (q = world left twists of A then B, reading
+    #28) vs central finite differences of the oracle's own values over the
+    exp-map chart; plus translation/rotation invariance of depth
+    (d/dq_B = -d/dq_A), weight partition, smooth-min bounds and the exact
+    compact Jacobian J = [W I, -[q - W tA]x, -W I, [q - W tB]x]."""
+    O = oracle_mod
+    shapes, poses, ell = _random_pair_scene(O, seed, kind)
+    poses = poses.astype(np.float32).astype(np.float64)   # the scene's FP32 inputs
+    pairs = np.array([[0, 0, 1, 0, 1]], np.int32)
+    base, osc = _manifold(O, shapes, poses, pairs, ell)
+    sp = osc.scene.smooth
+    # active faces only matter physically, but every face must pass
+    h = 1e-6 * ell
+    for j in range(12):
+        e = np.zeros(6)
+        e[j % 6] = h
+        pp, pm = poses.copy(), poses.copy()
+        slot = j // 6
+        pp[0, slot] = perturb(poses[0, slot], e)
+        pm[0, slot] = perturb(poses[0, slot], -e)
+        op_ = osc.contact_manifold(poses=pp)
+        om_ = osc.contact_manifold(poses=pm)
+        fd = (op_["depth"] - om_["depth"]) / (2 * h)
+        sc_d = np.maximum(1.0, np.abs(base["ddepth"]).max(1))
+        assert np.all(np.abs(fd - base["ddepth"][:, j]) <= 1e-5 * sc_d), (j, np.abs(fd - base["ddepth"][:, j]).max())
+        fdn = (op_["normal"] - om_["normal"]) / (2 * h)
+        sc_n = np.maximum(1.0 / ell, np.abs(base["dnormal"]).max((1, 2)))
+        err = np.abs(fdn - base["dnormal"][:, :, j]).max(1)
+        assert np.all(err <= 1e-4 * sc_n), (j, err.max())
+    # invariance under a common rigid motion of both bodies: a common
+    # translation gives d/dt_B = -d/dt_A; a common rotation about the world
+    # origin (dtheta_A = dtheta_B = w, dt_X = w x t_X) gives
+    # d/dth_A + d/dth_B + t_A x d/dt_A + t_B x d/dt_B = 0
+    g = base["ddepth"]
+    tol = 1e-9 * np.abs(g).max()
+    assert np.allclose(g[:, 6:9], -g[:, 0:3], atol=tol)
+    tA, tB = poses[0, 0, :3], poses[0, 1, :3]
+    assert np.allclose(g[:, 3:6] + g[:, 9:12] + np.cross(tA, g[:, 0:3]) + np.cross(tB, g[:, 6:9]), 0, atol=tol)
+    # weight partition, depth bounds (brute force on the 6 candidates)
+    assert np.allclose(base["z"].sum(1), 1.0, atol=1e-12)
+    dmin = base["dcand"].min(1)
+    assert np.all(base["depth"] <= dmin + 1e-15)
+    assert np.all(base["depth"] >= dmin - sp["tau_min"] * math.log(6.0) - 1e-15)
+    # dominant candidate = deepest (argmax z*gamma), lowest index on exact ties
+    assert np.all(base["dom"] == np.argmin(base["dcand"], axis=1))
+    # compact Jacobian equals the literal fused J (App. A.7)
+    for c in range(len(base["W"])):
+        W, q = base["W"][c], base["q"][c]
+        Jc = np.concatenate([W * np.eye(3), -skew(q - W * tA), -W * np.eye(3), skew(q - W * tB)], axis=1)
+        assert np.allclose(Jc, base["J"][c], atol=1e-12)
+
+
+def test_rigid_motion_invariance(oracle_mod):
+    """A common rigid motion T of both bodies leaves depth, W, dom unchanged
+    and rotates points, normals and q (S:547 equivariance)."""
+    O = oracle_mod
+    shapes, poses, ell = _random_pair_scene(O, 5, "blob")
+    poses = poses.astype(np.float32).astype(np.float64)
+    pairs = np.array([[0, 0, 1, 0, 1]], np.int32)
+    base, osc = _manifold(O, shapes, poses, pairs)
+    rng = np.random.default_rng(6)
+    qT = synth.random_quats(rng, 1)[0]
+    tT = rng.uniform(-0.5, 0.5, 3)
+    RT = synth.quat_to_mat(qT)
+    p2 = poses.copy()
+    for s in range(2):
+        p2[0, s, :3] = RT @ poses[0, s, :3] + tT
+        p2[0, s, 3:7] = synth.quat_mul(qT, poses[0, s, 3:7])
+    o2 = osc.contact_manifold(poses=p2)
+    assert np.allclose(o2["depth"], base["depth"], atol=1e-12)
+    assert np.allclose(o2["W"], base["W"], atol=1e-12)
+    assert np.array_equal(o2["dom"], base["dom"])
+    assert np.allclose(o2["normal"], base["normal"] @ RT.T, atol=1e-10)
+    assert np.allclose(o2["point"], base["point"] @ RT.T + tT, atol=1e-12)
+
+
+def test_sliding_box_stack_continuity(oracle_mod):
+    """S:553 / Fig. 4 analog: slide an SQ-box-sampled top over a MESH box...
+    here a MESH box over an SQ box: every fused contact point moves <= 50
+    delta per step of delta = 1e-3."""
+    O = oracle_mod
+    top = synth.make_shape("top", None, synth.box_mesh((0.1, 0.1, 0.1), 3))
+    base = synth.make_shape("base", synth.sq((0.1, 0.1, 0.1), (0.1, 0.1)), None)
+    osc = None
+    prev = None
+    for k in range(40):
+        poses = np.zeros((1, 2, 8))
+        poses[0, 0] = synth.pose_row((0.02 + 1e-3 * k, 0.0, 0.2 - 0.004), (1, 0, 0, 0))
+        poses[0, 1] = synth.pose_row((0, 0, 0), (1, 0, 0, 0))
+        if osc is None:
+            sc = scene_of([top, base], pairs=np.array([[0, 0, 1, 0, 1]], np.int32), poses=poses)
+            osc = O.OracleScene(sc)
+        out = osc.contact_manifold(poses=poses)
+        if prev is not None:
+            active = out["W"] > 1e-3
+            assert np.abs(out["point"] - prev)[active].max() <= 50 * 1e-3
+        prev = out["point"]
