@@ -1,0 +1,226 @@
+/*
+ * xpsq_cm.h — C ABI of the B200 (sm_100a) XPSQ SDF + smooth contact-manifold
+ * library (arXiv 2604.17538, "XPSQ analytical SDF primitives and smooth
+ * one-shot contact manifolds").
+ *
+ * Citations: P:n = PAPER.md line n (section / equation named in brackets).
+ *
+ * Two compute entry points follow the paper's statement of the problem:
+ *   cm_sdf_eval         sdf_eval(prims, poses, points) -> d, grad d, hess d
+ *                       (+ derivatives with respect to the poses)
+ *                       [§II-B, Eq. (1)-(6), P:52-126]
+ *   cm_contact_manifold contact_manifold(pairs, poses) -> points, normals,
+ *                       depths, Jacobians (+ pose derivatives)
+ *                       [§II-C, P:129-163]
+ *
+ * Conventions
+ *   - Ownership: the scene (shape library, sampled-surface topology, device
+ *     copies) is owned by the library behind the opaque cm_scene handle and is
+ *     immutable after creation.  Every batch input and output of a compute
+ *     call is a CALLER-OWNED DEVICE pointer (e.g. a torch tensor's data_ptr());
+ *     compute calls perform no allocation and no host<->device copy.
+ *   - Streams: compute calls take a cudaStream_t (passed as void*) and return
+ *     as soon as the work is enqueued; NULL means the legacy default stream.
+ *   - Errors: every function returns 0 (CM_OK) or a negative cm_status; the
+ *     message of the last failure on the calling thread is cm_last_error().
+ *     No C++ exception crosses the ABI.  Non-finite per-element inputs
+ *     propagate NaN into that element's outputs and do not fail the call.
+ *   - Poses: 8 floats per body: t = (x, y, z), unit quaternion q = (w, x, y, z)
+ *     (normalised by the library), 1 pad float.  A point x_local of a body is
+ *     at R(q) x_local + t in the world.
+ *   - Pose derivatives use world-frame left perturbations (twists): for a body
+ *     with pose (R, t), R <- exp([dtheta]x) R and t <- t + dt, coordinates
+ *     ordered (dt_x, dt_y, dt_z, dtheta_x, dtheta_y, dtheta_z).
+ *   - Sign convention: phi < 0 inside, > 0 outside ("gamma = [[d < 0]]").
+ *   - Thread safety: calls on distinct streams may run concurrently.
+ */
+#ifndef XPSQ_CM_H
+#define XPSQ_CM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CM_ABI_VERSION 1
+#define CM_MAX_PLANES 8      /* half-spaces per PSQ / XPSQ cross-section      */
+#define CM_MAX_CHILDREN 32   /* children per boolean node                     */
+#define CM_MAX_DEPTH 3       /* nesting of boolean nodes in one shape         */
+
+typedef enum cm_status {
+  CM_OK = 0,
+  CM_ERR_INVALID = -1,     /* bad argument, NULL pointer, bad index          */
+  CM_ERR_NONFINITE = -2,   /* non-finite shape parameter                     */
+  CM_ERR_UNSUPPORTED = -3, /* unsupported kind / depth / size                */
+  CM_ERR_ARITY = -4,       /* boolean arity (subtraction 2, others >= 2)     */
+  CM_ERR_EMPTY = -5,       /* empty input where one is required              */
+  CM_ERR_CUDA = -6,        /* CUDA runtime error (message has the detail)    */
+  CM_ERR_OOM = -7          /* device allocation failed at scene creation     */
+} cm_status;
+
+/* SDF node kinds.  Leaves: HALFSPACE phi = y.n + h; SQ radial
+ * distance from the inside-outside function of Eq. (1); PSQ = smooth
+ * intersection (Eq. (3)) of an SQ and N half-spaces; XPSQ = a PSQ swept
+ * along a quadratic spline (Eq. (5)).  Operators (Eq. (2)-(4),
+ * P:78-83): UNION -LSE(-phi_i), INTERSECTION LSE(phi_i) (n-ary, one LSE),
+ * SUBTRACTION LSE(phi_1, -phi_2) (binary). */
+typedef enum cm_node_type {
+  CM_HALFSPACE = 0,
+  CM_SQ = 1,
+  CM_PSQ = 2,
+  CM_XPSQ = 3,
+  CM_UNION = 10,
+  CM_INTERSECTION = 11,
+  CM_SUBTRACTION = 12
+} cm_node_type;
+
+/* One node of a shape's SDF tree; node 0 is the root.  Every node carries a
+ * pose relative to its parent (the root's is relative to the body frame).
+ * Leaf parameters ([e] = endpoint 0/1 of the XPSQ schedules; SQ, PSQ
+ * and HALFSPACE use endpoint 0 only):
+ *   eps[e] = (eps1, eps2) in [0.1, 2]; a[e] = (a_x, a_y, a_z) > 0;
+ *   planes[e][j] = (n_x, n_y, n_z, h), |n| = 1, inside where n.y + h <= 0;
+ *   HALFSPACE uses planes[0][0];
+ *   XPSQ: ctrl = p1, p2, p3 (Eq. (5)); up = up hint for straight/point
+ *   splines (the frame of a curved spline is its Frenet frame). */
+typedef struct cm_node {
+  int32_t type;                       /* cm_node_type                          */
+  int32_t n_children;                 /* operators only                        */
+  int32_t children[CM_MAX_CHILDREN];  /* node indices (> own index)            */
+  int32_t n_planes;                   /* PSQ / XPSQ (HALFSPACE: 1)             */
+  float pose[7];                      /* t(3), q(w,x,y,z) in the parent frame  */
+  float eps[2][2];
+  float a[2][3];
+  float planes[2][CM_MAX_PLANES][4];
+  float ctrl[9];
+  float up[3];
+} cm_node;
+
+/* A shape: optional SDF (n_nodes > 0) and optional sampled surface (the
+ * paper's mesh side): local-frame vertices [V,3] and triangles [F,3]
+ * (int32 vertex indices).  Host pointers, copied at scene creation. */
+typedef struct cm_shape_desc {
+  int32_t n_nodes;
+  const cm_node* nodes;
+  int32_t n_vertices;
+  const float* vertices;
+  int32_t n_faces;
+  const int32_t* faces;
+} cm_shape_desc;
+
+/* Temperatures of the smooth operators (§II-A; one generic tau in
+ * the paper, five named ones here — DESIGN.md reading #1), all > 0:
+ *   tau_cmp         gamma gate and sphere-trace gate
+ *   tau_min         boolean LSE, XPSQ smooth-min, depth softmax
+ *   tau_clip_alpha  soft clip of traced edge parameters
+ *   tau_clip_t      soft clip of the spline roots
+ *   tau_delta       soft Cardano discriminant gate
+ *   trace_iters     sphere-trace iterations per edge corner (3)      */
+typedef struct cm_smooth_params {
+  float tau_cmp, tau_min, tau_clip_alpha, tau_clip_t, tau_delta;
+  int32_t trace_iters;
+} cm_smooth_params;
+
+typedef struct cm_scene cm_scene;
+
+int cm_version(void);
+const char* cm_last_error(void);
+
+/* Validates and packs the shapes, builds each sampled surface's unique edges
+ * (sorted vertex pairs) and face->edge incidence, copies everything to
+ * device `device`.  Errors: CM_ERR_INVALID (bad index, degenerate edge,
+ * |n| != 1), CM_ERR_NONFINITE, CM_ERR_ARITY, CM_ERR_UNSUPPORTED (depth >
+ * CM_MAX_DEPTH, > CM_MAX_PLANES), CM_ERR_OOM, CM_ERR_CUDA. */
+int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smooth_params* sp, int device,
+                    cm_scene** out);
+int cm_scene_destroy(cm_scene* scene);
+
+/* V, E, F of shape `shape`'s sampled surface (0 if it has none). */
+int cm_shape_counts(const cm_scene* scene, int32_t shape, int32_t* V, int32_t* E, int32_t* F);
+/* Host copy of the topology the library built: edges [E,2] (lower index
+ * first), face_edges [F,3] (edges (i0,i1), (i1,i2), (i2,i0)). */
+int cm_shape_topology(const cm_scene* scene, int32_t shape, int32_t* edges, int32_t* face_edges);
+
+/* ---- sdf_eval --------------------------------------------------------------
+ * For batch item b in [0,B): shape shape_ids[b] placed at poses[b*8 .. +8];
+ * for its P query points n = b*P + j (world, points[n*3 .. +3]) computes the
+ * outputs selected by `flags` (SoA, N = B*P, field-major):
+ *   d[N]         phi (CM_SDF_VALUE)
+ *   grad[3*N]    d phi / d x                            (CM_SDF_GRAD)
+ *   hess[6*N]    xx, xy, xz, yy, yz, zz                 (CM_SDF_HESS)
+ *   dpose[6*N]   d phi / d(dt, dtheta)                  (CM_SDF_POSE_GRAD)
+ *   d2pose[21*N] packed upper triangle of the 6x6 pose Hessian, row-major
+ *                                                       (CM_SDF_POSE_HESS)
+ *   dxdpose[18*N] [i*6+j] = d (grad_i) / d pose_j       (CM_SDF_POSE_HESS)
+ * Unselected outputs may be NULL.  All pointers are device pointers. */
+#define CM_SDF_VALUE 1u
+#define CM_SDF_GRAD 2u
+#define CM_SDF_HESS 4u
+#define CM_SDF_POSE_GRAD 8u
+#define CM_SDF_POSE_HESS 16u
+int cm_sdf_eval(const cm_scene* scene, const int32_t* shape_ids, const float* poses, const float* points, int64_t B,
+                int64_t P, uint32_t flags, float* d, float* grad, float* hess, float* dpose, float* d2pose,
+                float* dxdpose, void* stream);
+
+/* ---- contact manifold ------------------------------------------------------
+ * pairs[5*i ..]: {env, slotA, slotB, shapeA (sampled surface), shapeB (SDF)}
+ * (device int32); poses [n_env, n_slot, 8] (device).  One-sided reduced
+ * manifold: one fused contact per face of shapeA's surface.
+ * Contacts of pair i occupy rows [offsets[i], offsets[i] + F(shapeA_i)) of
+ * every output array (offsets: device int64, e.g. from cm_manifold_offsets);
+ * n_contacts = C, the total (cm_manifold_size), is the stride of the fields.
+ * Outputs (device, field-major SoA over C contacts; a field is written iff its
+ * tier is selected, lower-tier fields are always written):
+ *   tier 0: point[3C] (sum z_i p_i, reporting only), normal[3C] (raw
+ *           fused sum z_i gamma_i n_i), depth[C] (smooth min of the
+ *           candidate depths), dom[C] (argmax z_i gamma_i, int8)
+ *   tier 1: W[C] = sum z_i gamma_i and q[3C] = sum z_i gamma_i p_i: the fused
+ *           3x12 contact Jacobian sum z_i gamma_i J_i is exactly
+ *           [W I, -[q - W tA]x, -W I, [q - W tB]x] (cm_expand_jacobian)
+ *   tier 2: ddepth[12C] and dnormal[36C] ([i*12+j] = d n_i / d q_j): the
+ *           derivatives with respect to q = (dt_A, dtheta_A, dt_B, dtheta_B). */
+#define CM_TIER0 0u
+#define CM_TIER1 1u
+#define CM_TIER2 2u
+#define CM_TIER_MASK 3u
+
+typedef struct cm_manifold_out {
+  float* point;
+  float* normal;
+  float* depth;
+  float* W;
+  float* q;
+  float* ddepth;
+  float* dnormal;
+  int8_t* dom;
+} cm_manifold_out;
+
+/* Number of contacts for a pair list given on the HOST (shapeA of each pair,
+ * stride `stride` int32 between entries). */
+int cm_manifold_size(const cm_scene* scene, const int32_t* shapeA_host, int64_t n_pairs, int64_t stride,
+                     int64_t* n_contacts);
+/* Device exclusive scan of F(shapeA_i) over the pairs -> offsets[n_pairs]
+ * (device int64).  Uses `workspace` of cm_manifold_offsets_workspace() bytes
+ * (device, caller-owned). */
+int64_t cm_manifold_offsets_workspace(int64_t n_pairs);
+int cm_manifold_offsets(const cm_scene* scene, const int32_t* pairs, int64_t n_pairs, int64_t* offsets,
+                        void* workspace, int64_t workspace_bytes, void* stream);
+int cm_contact_manifold(const cm_scene* scene, const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,
+                        const float* poses, int64_t n_env, int32_t n_slot, uint32_t flags,
+                        const cm_manifold_out* out, int64_t n_contacts, void* stream);
+
+/* Expands the compact Jacobian: J[36*C] ([r*12+c], device) from W, q and the
+ * pairs' poses. */
+int cm_expand_jacobian(const cm_scene* scene, const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,
+                       const float* poses, int64_t n_env, int32_t n_slot, const float* W, const float* q,
+                       int64_t n_contacts, float* J, void* stream);
+
+/* Number of kernel launches the library issued since scene creation (all
+ * scenes, this process) — instrumentation for bench.py's gpu_launches. */
+int64_t cm_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XPSQ_CM_H */

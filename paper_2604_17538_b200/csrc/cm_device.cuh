@@ -1,0 +1,758 @@
+// Device-side SDF evaluation for sm_100a: FP32 CUDA-core math with analytic
+// derivatives (SQ / PSQ / half-space / booleans) and compact forward-mode jets
+// (XPSQ), plus the smooth operators of §II-A.
+//
+// Citations: P:n = PAPER.md line n.  Derivative structure: DESIGN.md §5
+// (SURVEY Appendix A).  This file shares no code with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "cm_internal.h"
+
+namespace cmd {
+using namespace cmi;
+
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float LN2 = 0.6931471805599453f;
+constexpr float SQ_GUARD = 1e-12f;  // |u|^p = exp(p log(u^2 + g)/2)
+
+// MUFU approximations (ex2/lg2/rcp .approx: rel. error ~2^-22)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcpa(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// ---- §II-A smooth operators --------------------------------------
+// sigma(x) = 1 / (1 + e^-x)
+__device__ __forceinline__ float sigm(float x) { return rcpa(1.f + ex2(-x * LOG2E)); }
+// s+(x; tau) = tau log(1 + e^(x/tau)) = max(x,0) + tau log(1 + e^(-|x|/tau))
+__device__ __forceinline__ float softplus(float x, float tau, float itau) {
+  return fmaxf(x, 0.f) + (tau * LN2) * lg2(1.f + ex2(-fabsf(x) * (itau * LOG2E)));
+}
+// soft clip = lo + s+(x - lo) - s+(x - hi)  (two softplus)
+__device__ __forceinline__ float softclip(float x, float lo, float hi, float tau, float itau) {
+  return lo + softplus(x - lo, tau, itau) - softplus(x - hi, tau, itau);
+}
+// d softclip / dx = sigma((x-lo)/tau) - sigma((x-hi)/tau)
+__device__ __forceinline__ float softclip_d(float x, float lo, float hi, float itau) {
+  return sigm((x - lo) * itau) - sigm((x - hi) * itau);
+}
+
+// ---- results ---------------------------------------------------------------
+// packed symmetric 3x3: xx, xy, xz, yy, yz, zz
+template <int O> struct Res {
+  float v;
+  float g[3];
+  float h[6];
+};
+
+__device__ __forceinline__ constexpr int hidx3(int i, int j) {
+  return i <= j ? (i == 0 ? j : (i == 1 ? 2 + j : 5)) : (j == 0 ? i : (j == 1 ? 2 + i : 5));
+}
+
+// ---- rigid transforms -------------------------------------------------------
+__device__ __forceinline__ void quat_to_R(const float* q, float* R) {
+  float n = rsqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  float w = q[0] * n, x = q[1] * n, y = q[2] * n, z = q[3] * n;
+  R[0] = 1.f - 2.f * (y * y + z * z); R[1] = 2.f * (x * y - w * z);       R[2] = 2.f * (x * z + w * y);
+  R[3] = 2.f * (x * y + w * z);       R[4] = 1.f - 2.f * (x * x + z * z); R[5] = 2.f * (y * z - w * x);
+  R[6] = 2.f * (x * z - w * y);       R[7] = 2.f * (y * z + w * x);       R[8] = 1.f - 2.f * (x * x + y * y);
+}
+// y = R^T (x - t)
+__device__ __forceinline__ void to_local(const float* R, const float* t, const float* x, float* y) {
+  float d0 = x[0] - t[0], d1 = x[1] - t[1], d2 = x[2] - t[2];
+  y[0] = R[0] * d0 + R[3] * d1 + R[6] * d2;
+  y[1] = R[1] * d0 + R[4] * d1 + R[7] * d2;
+  y[2] = R[2] * d0 + R[5] * d1 + R[8] * d2;
+}
+__device__ __forceinline__ void rot_vec(const float* R, const float* a, float* b) {
+  b[0] = R[0] * a[0] + R[1] * a[1] + R[2] * a[2];
+  b[1] = R[3] * a[0] + R[4] * a[1] + R[5] * a[2];
+  b[2] = R[6] * a[0] + R[7] * a[1] + R[8] * a[2];
+}
+// H_w = R H R^T (packed in, packed out)
+__device__ __forceinline__ void rot_sym(const float* R, const float* h, float* o) {
+  float H[3][3] = {{h[0], h[1], h[2]}, {h[1], h[3], h[4]}, {h[2], h[4], h[5]}};
+  float M[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) M[i][j] = R[i * 3 + 0] * H[0][j] + R[i * 3 + 1] * H[1][j] + R[i * 3 + 2] * H[2][j];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = i; j < 3; ++j)
+      o[hidx3(i, j)] = M[i][0] * R[j * 3 + 0] + M[i][1] * R[j * 3 + 1] + M[i][2] * R[j * 3 + 2];
+}
+
+// ---- streaming LSE with derivatives (Eq. (2)-(4)) ---------
+// psi = tau log sum exp(v_i / tau),  grad = sum w g_i,
+// hess = sum w (H_i + g_i g_i^T / tau) - grad grad^T / tau
+template <int O> struct Acc {
+  float m, S;
+  float G[3];
+  float H[6];
+};
+template <int O> __device__ __forceinline__ void acc_init(Acc<O>& a) {
+  a.m = -INFINITY;
+  a.S = 0.f;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) a.G[i] = 0.f;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) a.H[k] = 0.f;
+}
+// fold s * r into the accumulator (itl = log2(e) / tau, itau = 1 / tau)
+template <int O> __device__ __forceinline__ void acc_fold(Acc<O>& a, float s, const Res<O>& r, float itl,
+                                                          float itau) {
+  float v = s * r.v;
+  float dm = v - a.m;
+  bool up = dm > 0.f;
+  float e = ex2(-fabsf(dm) * itl);
+  float cs = up ? e : 1.f;
+  float cn = up ? 1.f : e;
+  a.m = up ? v : a.m;
+  a.S = fmaf(a.S, cs, cn);
+  if constexpr (O >= 1) {
+    float g[3] = {s * r.g[0], s * r.g[1], s * r.g[2]};
+#pragma unroll
+    for (int i = 0; i < 3; ++i) a.G[i] = fmaf(a.G[i], cs, cn * g[i]);
+    if constexpr (O >= 2) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = i; j < 3; ++j) {
+          int k = hidx3(i, j);
+          a.H[k] = fmaf(a.H[k], cs, cn * fmaf(g[i] * g[j], itau, s * r.h[k]));
+        }
+    }
+  }
+}
+template <int O> __device__ __forceinline__ void acc_final(const Acc<O>& a, float s, float tau, float itau,
+                                                           Res<O>& r) {
+  r.v = s * fmaf(tau * LN2, lg2(a.S), a.m);
+  if constexpr (O >= 1) {
+    float iS = rcpa(a.S);
+    float g[3] = {a.G[0] * iS, a.G[1] * iS, a.G[2] * iS};
+#pragma unroll
+    for (int i = 0; i < 3; ++i) r.g[i] = s * g[i];
+    if constexpr (O >= 2) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = i; j < 3; ++j) {
+          int k = hidx3(i, j);
+          r.h[k] = s * fmaf(-g[i] * g[j], itau, a.H[k] * iS);
+        }
+    }
+  }
+}
+
+// ---- superquadric, analytic value / gradient / Hessian ----------------------
+// Eq. (1) with u_i = y_i / a_i, q_i = u_i^2 + g:
+//   A_i = q_i^(1/eps2) (i = 0, 1), S = A_0 + A_1, B = S^(eps2/eps1),
+//   C = q_2^(1/eps1), f = B + C;  phi = |y| (1 - f^(-eps1/2))  (reading #2).
+// Everything in the log2 domain so that large exponents (eps -> 0.1) cannot
+// overflow; beta = B/f, gamma = C/f, w_i = A_i/S are bounded ratios.
+// grad L = grad f / f = 2 p1 (beta w0 s0, beta w1 s1, gamma s2),
+//   s_i = u_i / (a_i q_i), c_i = d s_i / d y_i = (1 - 2 u_i^2/q_i) / (a_i^2 q_i),
+// F2 = hess f / f: F2_ij (i,j < 2) = 2 p1 beta [2 (p1 - p2) w_i w_j s_i s_j
+//   + delta_ij w_i (2 p2 s_i^2 + c_i)], F2_22 = 2 p1 gamma (2 p1 s2^2 + c2);
+// grad phi = (1-h) yh + k r h L;
+// hess phi = (1-h)(I - yh yh^T)/r + k h (yh L^T + L yh^T) + k r h (F2 - (1+k) L L^T)
+template <int O> __device__ __forceinline__ void sq_eval(const Leaf& Lf, const float* y, Res<O>& r) {
+  const float ia0 = Lf.ia[0], ia1 = Lf.ia[1], ia2 = Lf.ia[2];
+  const float p1 = Lf.p1, p2 = Lf.p2, m = Lf.m, k = Lf.k;
+  float u0 = y[0] * ia0, u1 = y[1] * ia1, u2 = y[2] * ia2;
+  float q0 = fmaf(u0, u0, SQ_GUARD), q1 = fmaf(u1, u1, SQ_GUARD), q2 = fmaf(u2, u2, SQ_GUARD);
+  float la0 = p2 * lg2(q0), la1 = p2 * lg2(q1), l3 = p1 * lg2(q2);
+  float lS = fmaxf(la0, la1) + lg2(1.f + ex2(-fabsf(la0 - la1)));
+  float lB = m * lS;
+  float lf = fmaxf(lB, l3) + lg2(1.f + ex2(-fabsf(lB - l3)));
+  float h = ex2(-k * lf);
+  float rr = fmaf(y[0], y[0], fmaf(y[1], y[1], y[2] * y[2]));
+  float ir = rsqrtf(fmaxf(rr, 1e-30f));
+  float rad = rr * ir;
+  float omh = 1.f - h;
+  r.v = rad * omh;
+  if constexpr (O >= 1) {
+    float w0 = ex2(la0 - lS), w1 = ex2(la1 - lS);
+    float be = ex2(lB - lf), ga = ex2(l3 - lf);
+    float iq0 = rcpa(q0), iq1 = rcpa(q1), iq2 = rcpa(q2);
+    float s0 = u0 * ia0 * iq0, s1 = u1 * ia1 * iq1, s2 = u2 * ia2 * iq2;
+    float tp1 = 2.f * p1;
+    float L0 = tp1 * be * w0 * s0, L1 = tp1 * be * w1 * s1, L2 = tp1 * ga * s2;
+    float yh0 = y[0] * ir, yh1 = y[1] * ir, yh2 = y[2] * ir;
+    float kh = k * h, krh = kh * rad;
+    r.g[0] = fmaf(omh, yh0, krh * L0);
+    r.g[1] = fmaf(omh, yh1, krh * L1);
+    r.g[2] = fmaf(omh, yh2, krh * L2);
+    if constexpr (O >= 2) {
+      float c0 = (1.f - 2.f * u0 * u0 * iq0) * ia0 * ia0 * iq0;
+      float c1 = (1.f - 2.f * u1 * u1 * iq1) * ia1 * ia1 * iq1;
+      float c2 = (1.f - 2.f * u2 * u2 * iq2) * ia2 * ia2 * iq2;
+      float tb = tp1 * be, dp = 2.f * (p1 - p2);
+      float ws0 = w0 * s0, ws1 = w1 * s1;
+      float F00 = tb * fmaf(dp * ws0, ws0, w0 * fmaf(2.f * p2 * s0, s0, c0));
+      float F01 = tb * dp * ws0 * ws1;
+      float F11 = tb * fmaf(dp * ws1, ws1, w1 * fmaf(2.f * p2 * s1, s1, c1));
+      float F22 = tp1 * ga * fmaf(tp1 * s2, s2, c2);
+      float a1 = omh * ir;          // (1-h)/r
+      float opk = 1.f + k;
+      float yh[3] = {yh0, yh1, yh2}, Lv[3] = {L0, L1, L2};
+      float F[6] = {F00, F01, 0.f, F11, 0.f, F22};
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = i; j < 3; ++j) {
+          int q = hidx3(i, j);
+          float v = a1 * ((i == j ? 1.f : 0.f) - yh[i] * yh[j]);
+          v = fmaf(kh, fmaf(yh[i], Lv[j], Lv[i] * yh[j]), v);
+          v = fmaf(krh, fmaf(-opk * Lv[i], Lv[j], F[q]), v);
+          r.h[q] = v;
+        }
+    }
+  }
+}
+
+// plane value n.y + h (gradient n, Hessian 0)
+template <int O> __device__ __forceinline__ void plane_eval(const float* pl, const float* y, Res<O>& r) {
+  r.v = fmaf(pl[0], y[0], fmaf(pl[1], y[1], fmaf(pl[2], y[2], pl[3])));
+  if constexpr (O >= 1) {
+    r.g[0] = pl[0]; r.g[1] = pl[1]; r.g[2] = pl[2];
+  }
+  if constexpr (O >= 2) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) r.h[k] = 0.f;
+  }
+}
+
+// ============================================================================
+// Compact forward-mode jets for the XPSQ: Jet<NV, O> carries the value, NV
+// first and NV(NV+1)/2 second partials (O = 0/1/2).
+// ============================================================================
+template <int NV, int O> struct Jet {
+  static constexpr int NH = NV * (NV + 1) / 2;
+  float v;
+  float g[NV];
+  float h[NH];
+};
+template <int NV> __device__ __forceinline__ constexpr int jhi(int k) {
+  return NV == 3 ? (k < 3 ? 0 : (k < 5 ? 1 : 2)) : (k < 2 ? 0 : 1);
+}
+template <int NV> __device__ __forceinline__ constexpr int jhj(int k) {
+  return NV == 3 ? (k < 3 ? k : (k < 5 ? k - 2 : 2)) : (k < 2 ? k : 1);
+}
+
+#define JT template <int NV, int O>
+#define JJ Jet<NV, O>
+
+JT __device__ __forceinline__ JJ jconst(float c) {
+  JJ r;
+  r.v = c;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) r.g[i] = 0.f;
+#pragma unroll
+  for (int k = 0; k < JJ::NH; ++k) r.h[k] = 0.f;
+  return r;
+}
+JT __device__ __forceinline__ JJ jvar(float c, int i) {
+  JJ r = jconst<NV, O>(c);
+  r.g[i] = 1.f;
+  return r;
+}
+JT __device__ __forceinline__ JJ operator+(const JJ& a, const JJ& b) {
+  JJ r;
+  r.v = a.v + b.v;
+  if constexpr (O >= 1) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) r.g[i] = a.g[i] + b.g[i];
+  }
+  if constexpr (O >= 2) {
+#pragma unroll
+    for (int k = 0; k < JJ::NH; ++k) r.h[k] = a.h[k] + b.h[k];
+  }
+  return r;
+}
+JT __device__ __forceinline__ JJ operator-(const JJ& a, const JJ& b) {
+  JJ r;
+  r.v = a.v - b.v;
+  if constexpr (O >= 1) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) r.g[i] = a.g[i] - b.g[i];
+  }
+  if constexpr (O >= 2) {
+#pragma unroll
+    for (int k = 0; k < JJ::NH; ++k) r.h[k] = a.h[k] - b.h[k];
+  }
+  return r;
+}
+JT __device__ __forceinline__ JJ operator-(const JJ& a) {
+  JJ r;
+  r.v = -a.v;
+  if constexpr (O >= 1) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) r.g[i] = -a.g[i];
+  }
+  if constexpr (O >= 2) {
+#pragma unroll
+    for (int k = 0; k < JJ::NH; ++k) r.h[k] = -a.h[k];
+  }
+  return r;
+}
+JT __device__ __forceinline__ JJ operator*(const JJ& a, float s) {
+  JJ r;
+  r.v = a.v * s;
+  if constexpr (O >= 1) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) r.g[i] = a.g[i] * s;
+  }
+  if constexpr (O >= 2) {
+#pragma unroll
+    for (int k = 0; k < JJ::NH; ++k) r.h[k] = a.h[k] * s;
+  }
+  return r;
+}
+JT __device__ __forceinline__ JJ operator*(float s, const JJ& a) { return a * s; }
+JT __device__ __forceinline__ JJ operator+(const JJ& a, float s) {
+  JJ r = a;
+  r.v = a.v + s;
+  return r;
+}
+JT __device__ __forceinline__ JJ operator+(float s, const JJ& a) { return a + s; }
+JT __device__ __forceinline__ JJ operator-(const JJ& a, float s) { return a + (-s); }
+JT __device__ __forceinline__ JJ operator-(float s, const JJ& a) { return (-a) + s; }
+JT __device__ __forceinline__ JJ operator*(const JJ& a, const JJ& b) {
+  JJ r;
+  r.v = a.v * b.v;
+  if constexpr (O >= 1) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) r.g[i] = fmaf(a.g[i], b.v, a.v * b.g[i]);
+  }
+  if constexpr (O >= 2) {
+#pragma unroll
+    for (int k = 0; k < JJ::NH; ++k) {
+      const int i = jhi<NV>(k), j = jhj<NV>(k);
+      r.h[k] = fmaf(a.h[k], b.v, fmaf(a.v, b.h[k], fmaf(a.g[i], b.g[j], a.g[j] * b.g[i])));
+    }
+  }
+  return r;
+}
+// unary chain: value f, first derivative f1, second derivative f2
+JT __device__ __forceinline__ JJ jchain(const JJ& a, float f, float f1, float f2) {
+  JJ r;
+  r.v = f;
+  if constexpr (O >= 1) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) r.g[i] = f1 * a.g[i];
+  }
+  if constexpr (O >= 2) {
+#pragma unroll
+    for (int k = 0; k < JJ::NH; ++k) {
+      const int i = jhi<NV>(k), j = jhj<NV>(k);
+      r.h[k] = fmaf(f1, a.h[k], f2 * a.g[i] * a.g[j]);
+    }
+  }
+  return r;
+}
+// binary chain F(a, b)
+JT __device__ __forceinline__ JJ jchain2(const JJ& a, const JJ& b, float f, float fa, float fb, float faa, float fab,
+                                         float fbb) {
+  JJ r;
+  r.v = f;
+  if constexpr (O >= 1) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) r.g[i] = fmaf(fa, a.g[i], fb * b.g[i]);
+  }
+  if constexpr (O >= 2) {
+#pragma unroll
+    for (int k = 0; k < JJ::NH; ++k) {
+      const int i = jhi<NV>(k), j = jhj<NV>(k);
+      float v = fmaf(fa, a.h[k], fb * b.h[k]);
+      v = fmaf(faa, a.g[i] * a.g[j], v);
+      v = fmaf(fbb, b.g[i] * b.g[j], v);
+      v = fmaf(fab, fmaf(a.g[i], b.g[j], a.g[j] * b.g[i]), v);
+      r.h[k] = v;
+    }
+  }
+  return r;
+}
+JT __device__ __forceinline__ JJ jinv(const JJ& a) {
+  float f = 1.f / a.v;
+  return jchain(a, f, -f * f, 2.f * f * f * f);
+}
+JT __device__ __forceinline__ JJ operator/(const JJ& a, const JJ& b) { return a * jinv(b); }
+JT __device__ __forceinline__ JJ jex2(const JJ& a) {
+  float f = ex2(a.v);
+  return jchain(a, f, f * LN2, f * (LN2 * LN2));
+}
+JT __device__ __forceinline__ JJ jlg2(const JJ& a) {
+  float iv = 1.f / a.v;
+  return jchain(a, lg2(a.v), iv * (1.f / LN2), -iv * iv * (1.f / LN2));
+}
+JT __device__ __forceinline__ JJ jsqrt(const JJ& a) {
+  float f = sqrtf(fmaxf(a.v, 0.f));
+  float fg = fmaxf(f, 1e-20f);
+  float f1 = 0.5f / fg;
+  return jchain(a, f, f1, -f1 / (2.f * fg * fg));
+}
+JT __device__ __forceinline__ JJ jrsqrt(const JJ& a) {
+  float f = rsqrtf(a.v);
+  float f3 = f * f * f;
+  return jchain(a, f, -0.5f * f3, 0.75f * f3 * f * f);
+}
+// real cube root (sign-preserving); derivatives guarded at 0 (the literal
+// formula's cusp, reading #15; excluded from parity)
+JT __device__ __forceinline__ JJ jcbrt(const JJ& a) {
+  float f = cbrtf(a.v);
+  float f2g = fmaxf(f * f, 1e-30f);
+  float f1 = 1.f / (3.f * f2g);
+  float f2 = -2.f * f1 / (3.f * (fabsf(a.v) > 1e-30f ? a.v : 1e-30f));
+  return jchain(a, f, f1, f2);
+}
+JT __device__ __forceinline__ JJ jcos(const JJ& a) {
+  float s, c;
+  sincosf(a.v, &s, &c);
+  return jchain(a, c, -s, -c);
+}
+JT __device__ __forceinline__ JJ jatan2(const JJ& y, const JJ& x) {
+  float r2 = fmaf(x.v, x.v, y.v * y.v);
+  float ir2 = 1.f / r2, ir4 = ir2 * ir2;
+  return jchain2(y, x, atan2f(y.v, x.v), x.v * ir2, -y.v * ir2, -2.f * x.v * y.v * ir4,
+                 (y.v * y.v - x.v * x.v) * ir4, 2.f * x.v * y.v * ir4);
+}
+// sigma(a) with derivatives s(1-s), s(1-s)(1-2s)
+JT __device__ __forceinline__ JJ jsigm(const JJ& a) {
+  float s = sigm(a.v);
+  float d = s * (1.f - s);
+  return jchain(a, s, d, d * (1.f - 2.f * s));
+}
+// s+(a; tau): derivative sigma(a/tau), second sigma(1-sigma)/tau
+JT __device__ __forceinline__ JJ jsoftplus(const JJ& a, float tau, float itau) {
+  float s = sigm(a.v * itau);
+  return jchain(a, softplus(a.v, tau, itau), s, s * (1.f - s) * itau);
+}
+JT __device__ __forceinline__ JJ jsoftclip(const JJ& a, float lo, float hi, float tau, float itau) {
+  float s1 = sigm((a.v - lo) * itau), s2 = sigm((a.v - hi) * itau);
+  return jchain(a, softclip(a.v, lo, hi, tau, itau), s1 - s2, (s1 * (1.f - s1) - s2 * (1.f - s2)) * itau);
+}
+// log2(2^a + 2^b) = max + log2(1 + 2^-(|a-b|))
+JT __device__ __forceinline__ JJ jlse2(const JJ& a, const JJ& b) {
+  float d = a.v - b.v;
+  float e = ex2(-fabsf(d));
+  float f = fmaxf(a.v, b.v) + lg2(1.f + e);
+  // weights wa = 2^a / (2^a + 2^b)
+  float wa = d > 0.f ? rcpa(1.f + e) : e * rcpa(1.f + e);
+  float wb = 1.f - wa;
+  float c = LN2 * wa * wb;
+  return jchain2(a, b, f, wa, wb, c, -c, c);
+}
+#undef JT
+#undef JJ
+
+template <int O> using J3 = Jet<3, O>;
+template <int O> using J2 = Jet<2, O>;
+
+// scalar-or-jet helpers for schedule parameters (float when constant)
+template <int O> __device__ __forceinline__ J3<O> lift(float x) { return jconst<3, O>(x); }
+
+// SQ radial distance on jets (same log2-domain formulas as sq_eval);
+// parameters are jets only when the XPSQ schedules vary along t.
+template <int O, class S>
+__device__ __forceinline__ J3<O> sq_jet(const J3<O>* y, const S& p1, const S& p2, const S& m, const S& k,
+                                        const S* ia) {
+  J3<O> u0 = y[0] * ia[0], u1 = y[1] * ia[1], u2 = y[2] * ia[2];
+  J3<O> q0 = u0 * u0 + SQ_GUARD, q1 = u1 * u1 + SQ_GUARD, q2 = u2 * u2 + SQ_GUARD;
+  J3<O> la0 = jlg2(q0) * p2, la1 = jlg2(q1) * p2, l3 = jlg2(q2) * p1;
+  J3<O> lS = jlse2(la0, la1);
+  J3<O> lB = lS * m;
+  J3<O> lf = jlse2(lB, l3);
+  J3<O> h = jex2(-(lf * k));
+  J3<O> rad = jsqrt(y[0] * y[0] + y[1] * y[1] + y[2] * y[2]);
+  return rad * (1.f - h);
+}
+
+// direct LSE_tau over n jets (n <= 9), sign s: s * LSE(s * x)
+template <int O> __device__ __forceinline__ J3<O> lse_jets(const J3<O>* x, int n, float s, float tau) {
+  float m = s * x[0].v;
+  for (int i = 1; i < n; ++i) m = fmaxf(m, s * x[i].v);
+  float itl = LOG2E / tau;
+  J3<O> S = jconst<3, O>(0.f);
+  for (int i = 0; i < n; ++i) S = S + jex2((x[i] * s - m) * itl);
+  J3<O> L = jlg2(S) * (tau * LN2) + m;
+  return L * s;
+}
+
+// soft Cardano on a 2-variable jet in (P, Q) (Eq. (6); DESIGN.md
+// readings #9-#13).  Negative branch: real root of s^3 + P- s + Q = 0 with
+// P-^3 = P^3 + s+(Delta)/4 (the cubic whose discriminant is Delta- =
+// -s+(-Delta)), computed in Cardano's cancellation-free form u + v,
+// u = cbrt(-Q/2 - sign(Q) sqrt(D)), v = -P-/(3u), D = -Delta-/108.  Positive
+// branch: trigonometric form with Delta+ = s+(Delta):
+// rho^6 = Q^2/4 + Delta+/108, theta = atan2(sqrt(Delta+/108), -Q/2),
+// s_k = 2 rho cos((theta + 2 pi k)/3).  Both soft-clipped to (0,1), blended by
+// sigma(-Delta/tau), sigma(Delta/tau).
+template <int O>
+__device__ __forceinline__ void soft_cardano(const J2<O>& P, const J2<O>& Q, float b3, const SmoothDev& sp,
+                                             J2<O>* t) {
+  const float td = sp.tau_delta, itd = 1.f / td;
+  const float tc = sp.tau_clip_t, itc = 1.f / tc;
+  J2<O> P3 = P * P * P;
+  J2<O> Delta = -(P3 * 4.f + Q * Q * 27.f);
+  J2<O> wneg = jsigm(-Delta * itd);
+  J2<O> wpos = jsigm(Delta * itd);
+  J2<O> tm = jconst<2, O>(0.f), tp[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) tp[k] = jconst<2, O>(0.f);
+  if (wneg.v > 0.f) {
+    J2<O> spD = jsoftplus(Delta, td, itd);          // s+(Delta)
+    J2<O> Pm = jcbrt(P3 + spD * 0.25f);
+    J2<O> D = jsoftplus(-Delta, td, itd) * (1.f / 108.f);
+    J2<O> sD = jsqrt(D);
+    J2<O> arg = (Q.v >= 0.f) ? (-Q * 0.5f - sD) : (-Q * 0.5f + sD);
+    J2<O> u = jcbrt(arg);
+    J2<O> s;
+    if (fabsf(u.v) > 1e-30f) s = u - Pm * jinv(u) * (1.f / 3.f);
+    else s = u;
+    tm = jsoftclip(s - b3, 0.f, 1.f, tc, itc);
+  }
+  if (wpos.v > 0.f) {
+    J2<O> Dp = jsoftplus(Delta, td, itd) * (1.f / 108.f);   // Delta+ / 108
+    J2<O> r6 = Q * Q * 0.25f + Dp;
+    J2<O> rho = jex2(jlg2(r6) * (1.f / 6.f));
+    J2<O> th = jatan2(jsqrt(Dp), -Q * 0.5f);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      J2<O> sk = rho * jcos((th + 6.283185307179586f * (float)k) * (1.f / 3.f)) * 2.f;
+      tp[k] = jsoftclip(sk - b3, 0.f, 1.f, tc, itc);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (wneg.v > 0.f && wpos.v > 0.f) t[k] = wneg * tm + wpos * tp[k];
+    else if (wneg.v > 0.f) t[k] = wneg * tm;
+    else t[k] = wpos * tp[k];
+  }
+}
+
+// XPSQ leaf in its local frame
+template <int O> __device__ void xpsq_eval(const Xpsq& X, const SmoothDev& sp, const float* y, Res<O>& out) {
+  const float tc = sp.tau_clip_t, itc = 1.f / tc;
+  float w[3] = {y[0] - X.p1[0], y[1] - X.p1[1], y[2] - X.p1[2]};
+  J3<O> tk[3];
+  if (X.cls == 0) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) tk[k] = jconst<3, O>(0.5f);
+  } else if (X.cls == 1) {
+    float s = X.Bn[0] * w[0] + X.Bn[1] * w[1] + X.Bn[2] * w[2];
+    J3<O> sj = jconst<3, O>(s);
+    if constexpr (O >= 1) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) sj.g[i] = X.Bn[i];
+    }
+    J3<O> t = jsoftclip(sj, 0.f, 1.f, tc, itc);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) tk[k] = t;
+  } else {
+    float Pv = X.gP[0] * w[0] + X.gP[1] * w[1] + X.gP[2] * w[2] + X.P0;
+    float Qv = X.gQ[0] * w[0] + X.gQ[1] * w[1] + X.gQ[2] * w[2] + X.Q0;
+    J2<O> P = jvar<2, O>(Pv, 0), Q = jvar<2, O>(Qv, 1);
+    J2<O> t2[3];
+    soft_cardano<O>(P, Q, X.b3, sp, t2);
+    // chain (P, Q) -> y: grad t = tP gP + tQ gQ; hess = [gP gQ] H [gP gQ]^T
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      tk[k].v = t2[k].v;
+      if constexpr (O >= 1) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) tk[k].g[i] = fmaf(t2[k].g[0], X.gP[i], t2[k].g[1] * X.gQ[i]);
+      }
+      if constexpr (O >= 2) {
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+          const int i = jhi<3>(q), j = jhj<3>(q);
+          float v = t2[k].h[0] * X.gP[i] * X.gP[j];
+          v = fmaf(t2[k].h[1], fmaf(X.gP[i], X.gQ[j], X.gQ[i] * X.gP[j]), v);
+          v = fmaf(t2[k].h[2], X.gQ[i] * X.gQ[j], v);
+          tk[k].h[q] = v;
+        }
+      }
+    }
+  }
+  J3<O> yj[3] = {jvar<3, O>(y[0], 0), jvar<3, O>(y[1], 1), jvar<3, O>(y[2], 2)};
+  J3<O> phis[3];
+  const float tmin = sp.tau_min;
+#pragma unroll 1
+  for (int k = 0; k < 3; ++k) {
+    const J3<O>& t = tk[k];
+    J3<O> tt = t * t;
+    J3<O> dx[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) dx[i] = yj[i] - (t * X.B[i] + tt * X.A[i] + X.p1[i]);
+    J3<O> yk[3];
+    if (X.frenet) {
+      J3<O> pd[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) pd[i] = t * (2.f * X.A[i]) + X.B[i];
+      J3<O> inv = jrsqrt(pd[0] * pd[0] + pd[1] * pd[1] + pd[2] * pd[2]);
+      J3<O> T[3] = {pd[0] * inv, pd[1] * inv, pd[2] * inv};
+      const float* b = X.bhat;
+      J3<O> N[3] = {T[2] * b[1] - T[1] * b[2], T[0] * b[2] - T[2] * b[0], T[1] * b[0] - T[0] * b[1]};
+      yk[0] = T[0] * dx[0] + T[1] * dx[1] + T[2] * dx[2];
+      yk[1] = N[0] * dx[0] + N[1] * dx[1] + N[2] * dx[2];
+      yk[2] = dx[0] * b[0] + dx[1] * b[1] + dx[2] * b[2];
+    } else {
+      const float* R = X.R0;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) yk[i] = dx[0] * R[0 * 3 + i] + dx[1] * R[1 * 3 + i] + dx[2] * R[2 * 3 + i];
+    }
+    J3<O> ops[1 + CM_MAX_PLANES];
+    if (X.varying) {
+      J3<O> e1 = t * X.deps[0] + X.eps0[0], e2 = t * X.deps[1] + X.eps0[1];
+      J3<O> ip1 = jinv(e1), ip2 = jinv(e2);
+      J3<O> m = e2 * ip1, kk = e1 * 0.5f;
+      J3<O> ia[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) ia[i] = jinv(t * X.da[i] + X.a0[i]);
+      ops[0] = sq_jet<O>(yk, ip1, ip2, m, kk, ia);
+      for (int j = 0; j < X.n_planes; ++j) {
+        J3<O> nv[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) nv[i] = t * X.dpl[j][i] + X.pl0[j][i];
+        J3<O> in = jrsqrt(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]);
+        ops[1 + j] = (nv[0] * yk[0] + nv[1] * yk[1] + nv[2] * yk[2]) * in + (t * X.dpl[j][3] + X.pl0[j][3]);
+      }
+    } else {
+      float e1 = X.eps0[0], e2 = X.eps0[1];
+      float ia[3] = {1.f / X.a0[0], 1.f / X.a0[1], 1.f / X.a0[2]};
+      ops[0] = sq_jet<O, float>(yk, 1.f / e1, 1.f / e2, e2 / e1, 0.5f * e1, ia);
+      for (int j = 0; j < X.n_planes; ++j)
+        ops[1 + j] = yk[0] * X.pl0[j][0] + yk[1] * X.pl0[j][1] + yk[2] * X.pl0[j][2] + X.pl0[j][3];
+    }
+    phis[k] = X.n_planes > 0 ? lse_jets<O>(ops, 1 + X.n_planes, 1.f, tmin) : ops[0];
+  }
+  // smooth minimum of the three PSQ SDFs
+  J3<O> phi = lse_jets<O>(phis, 3, -1.f, tmin);
+  out.v = phi.v;
+  if constexpr (O >= 1) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) out.g[i] = phi.g[i];
+  }
+  if constexpr (O >= 2) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) out.h[q] = phi.h[q];
+  }
+}
+
+// ---- leaf dispatch ---------------------------------------------------------
+template <int O, bool XP>
+__device__ __forceinline__ void leaf_eval(const SceneDev& S, int li, const float* x, Res<O>& r) {
+  const Leaf& L = S.leaves[li];
+  float y[3];
+  float t[3] = {L.t[0], L.t[1], L.t[2]};
+  const bool ident = L.rot_identity != 0;
+  float R[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R[i] = L.R[i];
+  if (ident) {
+    y[0] = x[0] - t[0]; y[1] = x[1] - t[1]; y[2] = x[2] - t[2];
+  } else {
+    to_local(R, t, x, y);
+  }
+  Res<O> l;
+  const int kind = L.kind;
+  if (kind == LK_SQ) {
+    sq_eval<O>(L, y, l);
+    const int np = L.n_planes;
+    if (np > 0) {
+      // PSQ: smooth intersection Eq. (3) with the half-spaces
+      const float tau = S.sp.tau_min, itau = 1.f / tau, itl = LOG2E * itau;
+      Acc<O> a;
+      acc_init(a);
+      acc_fold(a, 1.f, l, itl, itau);
+      for (int j = 0; j < np; ++j) {
+        Res<O> p;
+        plane_eval<O>(L.planes[j], y, p);
+        acc_fold(a, 1.f, p, itl, itau);
+      }
+      acc_final(a, 1.f, tau, itau, l);
+    }
+  } else if (XP && kind == LK_XPSQ) {
+    xpsq_eval<O>(S.xpsq[L.xidx], S.sp, y, l);
+  } else {
+    plane_eval<O>(L.planes[0], y, l);
+  }
+  r.v = l.v;
+  if constexpr (O >= 1) {
+    if (ident) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) r.g[i] = l.g[i];
+    } else {
+      rot_vec(R, l.g, r.g);
+    }
+  }
+  if constexpr (O >= 2) {
+    if (ident) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) r.h[k] = l.h[k];
+    } else {
+      rot_sym(R, l.h, r.h);
+    }
+  }
+}
+
+// ---- shape program interpreter ----------------------------------------------
+template <int O>
+__device__ __forceinline__ void fold_level(Acc<O>& a0, Acc<O>& a1, Acc<O>& a2, int lvl, float s, const Res<O>& r,
+                                           float itl, float itau) {
+  if (lvl == 0) acc_fold(a0, s, r, itl, itau);
+  else if (lvl == 1) acc_fold(a1, s, r, itl, itau);
+  else acc_fold(a2, s, r, itl, itau);
+}
+
+// phi, grad, hess of shape `sh` at the body-frame point x
+template <int O, bool XP> __device__ void eval_shape(const SceneDev& S, const ShapeRec& sh, const float* x, Res<O>& out) {
+  const float tau = S.sp.tau_min, itau = 1.f / tau, itl = LOG2E * itau;
+  if (sh.prog_len == 1) {  // single leaf: no accumulator needed
+    leaf_eval<O, XP>(S, S.prog[sh.prog_begin].idx, x, out);
+    return;
+  }
+  Acc<O> a0, a1, a2;
+  int lvl = -1;
+  const Instr* prog = S.prog + sh.prog_begin;
+  for (int pc = 0; pc < sh.prog_len; ++pc) {
+    const Instr in = prog[pc];
+    if (in.op == OP_BEGIN) {
+      ++lvl;
+      if (lvl == 0) acc_init(a0);
+      else if (lvl == 1) acc_init(a1);
+      else acc_init(a2);
+      continue;
+    }
+    Res<O> r;
+    if (in.op == OP_LEAF) {
+      leaf_eval<O, XP>(S, in.idx, x, r);
+    } else {
+      if (lvl == 0) acc_final(a0, in.out_sign, tau, itau, r);
+      else if (lvl == 1) acc_final(a1, in.out_sign, tau, itau, r);
+      else acc_final(a2, in.out_sign, tau, itau, r);
+      --lvl;
+    }
+    if (lvl < 0) out = r;
+    else fold_level(a0, a1, a2, lvl, in.child_sign, r, itl, itau);
+  }
+}
+
+}  // namespace cmd

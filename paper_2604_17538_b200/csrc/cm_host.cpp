@@ -1,0 +1,528 @@
+// Host side of the C ABI (include/xpsq_cm.h): validation, static packing of
+// the shape library (flattened SDF programs, leaf parameters, XPSQ static
+// data, sampled-surface topology), device residency, argument checks and
+// kernel dispatch.  No compute of the hot path runs here.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "cm_internal.h"
+#include "xpsq_cm.h"
+
+using namespace cmi;
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+struct Frame {
+  double R[9], t[3];
+};
+
+void quat_R(const float* q, double* R) {
+  double n = std::sqrt((double)q[0] * q[0] + (double)q[1] * q[1] + (double)q[2] * q[2] + (double)q[3] * q[3]);
+  double w = q[0] / n, x = q[1] / n, y = q[2] / n, z = q[3] / n;
+  R[0] = 1 - 2 * (y * y + z * z); R[1] = 2 * (x * y - w * z);     R[2] = 2 * (x * z + w * y);
+  R[3] = 2 * (x * y + w * z);     R[4] = 1 - 2 * (x * x + z * z); R[5] = 2 * (y * z - w * x);
+  R[6] = 2 * (x * z - w * y);     R[7] = 2 * (y * z + w * x);     R[8] = 1 - 2 * (x * x + y * y);
+}
+
+Frame compose(const Frame& p, const float* pose7) {
+  Frame c, r;
+  quat_R(pose7 + 3, c.R);
+  for (int i = 0; i < 3; ++i) c.t[i] = pose7[i];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      r.R[i * 3 + j] = p.R[i * 3 + 0] * c.R[0 * 3 + j] + p.R[i * 3 + 1] * c.R[1 * 3 + j] + p.R[i * 3 + 2] * c.R[2 * 3 + j];
+  for (int i = 0; i < 3; ++i)
+    r.t[i] = p.R[i * 3 + 0] * c.t[0] + p.R[i * 3 + 1] * c.t[1] + p.R[i * 3 + 2] * c.t[2] + p.t[i];
+  return r;
+}
+
+double dot3(const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+void cross3(const double* a, const double* b, double* r) {
+  r[0] = a[1] * b[2] - a[2] * b[1];
+  r[1] = a[2] * b[0] - a[0] * b[2];
+  r[2] = a[0] * b[1] - a[1] * b[0];
+}
+void unit3(double* v) {
+  double n = std::sqrt(dot3(v, v));
+  for (int i = 0; i < 3; ++i) v[i] /= n;
+}
+
+bool finite_all(const float* p, int n) {
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(p[i])) return false;
+  return true;
+}
+
+// XPSQ classification thresholds (reading #14; the same rule is
+// written independently in the oracle)
+constexpr double X_EPS_POINT = 1e-6, X_EPS_LINE = 1e-2, X_EPS_FRAME = 1e-3;
+
+Xpsq pack_xpsq(const cm_node& n) {
+  Xpsq X;
+  std::memset(&X, 0, sizeof(X));
+  double p1[3], p2[3], p3[3], A[3], B[3];
+  for (int i = 0; i < 3; ++i) { p1[i] = n.ctrl[i]; p2[i] = n.ctrl[3 + i]; p3[i] = n.ctrl[6 + i]; }
+  for (int i = 0; i < 3; ++i) { A[i] = p1[i] - 2 * p2[i] + p3[i]; B[i] = 2 * (p2[i] - p1[i]); }
+  double nA = std::sqrt(dot3(A, A)), nB = std::sqrt(dot3(B, B));
+  double T0[3] = {1, 0, 0};
+  if (nA < X_EPS_POINT && nB < X_EPS_POINT) {
+    X.cls = 0;
+  } else if (nA < X_EPS_LINE * nB) {
+    X.cls = 1;
+    for (int i = 0; i < 3; ++i) { A[i] = 0; T0[i] = B[i]; }
+  } else {
+    X.cls = 2;
+    for (int i = 0; i < 3; ++i) T0[i] = A[i] + B[i];
+    if (std::sqrt(dot3(T0, T0)) < X_EPS_POINT)
+      for (int i = 0; i < 3; ++i) T0[i] = nB > X_EPS_POINT ? B[i] : A[i];
+  }
+  double bxa[3];
+  cross3(B, A, bxa);
+  X.frenet = (X.cls == 2 && std::sqrt(dot3(bxa, bxa)) >= X_EPS_FRAME * nA * nB) ? 1 : 0;
+  double bh[3];
+  if (X.frenet) {
+    for (int i = 0; i < 3; ++i) bh[i] = bxa[i];
+    unit3(bh);
+  } else {
+    double up[3] = {n.up[0], n.up[1], n.up[2]};
+    if (X.cls == 0) {
+      unit3(up);
+      double e[3] = {1, 0, 0};
+      double c = dot3(e, up);
+      if (std::fabs(c) > 0.9) { e[0] = 0; e[1] = 1; c = dot3(e, up); }
+      for (int i = 0; i < 3; ++i) T0[i] = e[i] - c * up[i];
+      unit3(T0);
+    } else {
+      unit3(T0);
+      double c = dot3(up, T0);
+      for (int i = 0; i < 3; ++i) up[i] -= c * T0[i];
+      unit3(up);
+    }
+    for (int i = 0; i < 3; ++i) bh[i] = up[i];
+    double N[3];
+    cross3(bh, T0, N);
+    for (int i = 0; i < 3; ++i) {
+      X.R0[i * 3 + 0] = (float)T0[i];
+      X.R0[i * 3 + 1] = (float)N[i];
+      X.R0[i * 3 + 2] = (float)bh[i];
+    }
+  }
+  for (int i = 0; i < 3; ++i) {
+    X.p1[i] = (float)p1[i]; X.A[i] = (float)A[i]; X.B[i] = (float)B[i]; X.bhat[i] = (float)bh[i];
+  }
+  double BB = dot3(B, B);
+  if (X.cls == 1)
+    for (int i = 0; i < 3; ++i) X.Bn[i] = (float)(B[i] / BB);
+  if (X.cls == 2) {
+    // cubic of P:112: c3 t^3 + c2 t^2 + c1 t + c0, c3 = -2 A.A, c2 = -3 A.B,
+    // c1 = 2 A.w - B.B, c0 = B.w; monic b = c2/c3; depressed P, Q affine in w
+    double c3 = -2 * dot3(A, A), c2 = -3 * dot3(A, B), b = c2 / c3;
+    for (int i = 0; i < 3; ++i) {
+      X.gP[i] = (float)(2 * A[i] / c3);
+      X.gQ[i] = (float)((B[i] - (2 * b / 3) * A[i]) / c3);
+    }
+    X.P0 = (float)(-BB / c3 - b * b / 3);
+    X.Q0 = (float)(2 * b * b * b / 27 + (b / 3) * BB / c3);
+    X.b3 = (float)(b / 3);
+  }
+  X.n_planes = n.n_planes;
+  bool varying = false;
+  for (int i = 0; i < 2; ++i) {
+    X.eps0[i] = n.eps[0][i];
+    X.deps[i] = n.eps[1][i] - n.eps[0][i];
+    varying |= X.deps[i] != 0.f;
+  }
+  for (int i = 0; i < 3; ++i) {
+    X.a0[i] = n.a[0][i];
+    X.da[i] = n.a[1][i] - n.a[0][i];
+    varying |= X.da[i] != 0.f;
+  }
+  for (int j = 0; j < n.n_planes; ++j)
+    for (int i = 0; i < 4; ++i) {
+      X.pl0[j][i] = n.planes[0][j][i];
+      X.dpl[j][i] = n.planes[1][j][i] - n.planes[0][j][i];
+      varying |= X.dpl[j][i] != 0.f;
+    }
+  X.varying = varying ? 1 : 0;
+  return X;
+}
+
+template <class T> T* dev_copy(const std::vector<T>& v, int& rc) {
+  if (v.empty()) return nullptr;
+  T* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, v.size() * sizeof(T));
+  if (e != cudaSuccess) {
+    rc = CM_ERR_OOM;
+    g_err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
+    return nullptr;
+  }
+  e = cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    rc = CM_ERR_CUDA;
+    g_err = std::string("cudaMemcpy: ") + cudaGetErrorString(e);
+  }
+  return p;
+}
+}  // namespace
+
+struct cm_scene {
+  int device = 0;
+  SceneDev dev;
+  std::vector<ShapeRec> shapes;
+  std::vector<std::vector<int32_t>> edges, face_edges;
+  int max_V = 0, max_E = 0, max_F = 0;
+  int xp_class = 0;  // 0 no XPSQ shape, 1 every SDF shape uses XPSQ, 2 mixed
+  std::vector<void*> allocs;
+  float* scratch = nullptr;
+  int64_t scratch_floats = 0;
+};
+
+extern "C" {
+
+int cm_version(void) { return CM_ABI_VERSION; }
+const char* cm_last_error(void) { return g_err.c_str(); }
+
+int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smooth_params* sp, int device,
+                    cm_scene** out) {
+  if (!shapes || !sp || !out || n_shapes <= 0) return fail(CM_ERR_INVALID, "cm_scene_create: bad arguments");
+  *out = nullptr;
+  const float taus[5] = {sp->tau_cmp, sp->tau_min, sp->tau_clip_alpha, sp->tau_clip_t, sp->tau_delta};
+  for (float t : taus)
+    if (!(t > 0.f) || !std::isfinite(t)) return fail(CM_ERR_INVALID, "smooth params: every tau must be > 0 (S:28)");
+  if (sp->trace_iters < 0 || sp->trace_iters > 64) return fail(CM_ERR_INVALID, "trace_iters out of range");
+
+  std::vector<Instr> prog;
+  std::vector<Leaf> leaves;
+  std::vector<Xpsq> xps;
+  std::vector<ShapeRec> recs(n_shapes);
+  std::vector<float> verts;
+  std::vector<int32_t> edges_all, faces_all, fe_all;
+  cm_scene* sc = new cm_scene;
+  sc->device = device;
+  sc->edges.resize(n_shapes);
+  sc->face_edges.resize(n_shapes);
+  int n_sdf = 0, n_xp = 0;
+
+  for (int s = 0; s < n_shapes; ++s) {
+    const cm_shape_desc& d = shapes[s];
+    ShapeRec& r = recs[s];
+    std::memset(&r, 0, sizeof(r));
+    r.prog_begin = (int32_t)prog.size();
+    if (d.n_nodes > 0) {
+      if (!d.nodes) { delete sc; return fail(CM_ERR_INVALID, "shape " + std::to_string(s) + ": nodes is NULL"); }
+      // validate nodes
+      for (int k = 0; k < d.n_nodes; ++k) {
+        const cm_node& n = d.nodes[k];
+        std::string w = "shape " + std::to_string(s) + " node " + std::to_string(k) + ": ";
+        if (!finite_all(n.pose, 7) || !finite_all(&n.eps[0][0], 4) || !finite_all(&n.a[0][0], 6) ||
+            !finite_all(&n.planes[0][0][0], 2 * CM_MAX_PLANES * 4) || !finite_all(n.ctrl, 9) || !finite_all(n.up, 3)) {
+          delete sc;
+          return fail(CM_ERR_NONFINITE, w + "non-finite parameter");
+        }
+        const bool leaf = n.type <= CM_XPSQ;
+        if (leaf) {
+          if (n.type < 0) { delete sc; return fail(CM_ERR_UNSUPPORTED, w + "unknown node type"); }
+          int np = n.type == CM_HALFSPACE ? 1 : (n.type == CM_SQ ? 0 : n.n_planes);
+          if (np < 0 || np > CM_MAX_PLANES) { delete sc; return fail(CM_ERR_UNSUPPORTED, w + "too many planes"); }
+          int ends = n.type == CM_XPSQ ? 2 : 1;
+          for (int e = 0; e < ends; ++e)
+            for (int j = 0; j < np; ++j) {
+              const float* pl = n.planes[e][j];
+              double nn = std::sqrt((double)pl[0] * pl[0] + (double)pl[1] * pl[1] + (double)pl[2] * pl[2]);
+              if (std::fabs(nn - 1.0) > 1e-5) { delete sc; return fail(CM_ERR_INVALID, w + "plane normal not unit (S:172)"); }
+            }
+          if (n.type != CM_HALFSPACE)
+            for (int e = 0; e < ends; ++e) {
+              for (int i = 0; i < 2; ++i)
+                if (n.eps[e][i] < 0.1f - 1e-6f || n.eps[e][i] > 2.0f + 1e-6f) {
+                  delete sc;
+                  return fail(CM_ERR_INVALID, w + "eps outside [0.1, 2] (S:177)");
+                }
+              for (int i = 0; i < 3; ++i)
+                if (!(n.a[e][i] > 0.f)) { delete sc; return fail(CM_ERR_INVALID, w + "scale a must be > 0"); }
+            }
+        } else {
+          if (n.type != CM_UNION && n.type != CM_INTERSECTION && n.type != CM_SUBTRACTION) {
+            delete sc;
+            return fail(CM_ERR_UNSUPPORTED, w + "unknown node type");
+          }
+          if (n.type == CM_SUBTRACTION ? n.n_children != 2 : (n.n_children < 2 || n.n_children > CM_MAX_CHILDREN)) {
+            delete sc;
+            return fail(CM_ERR_ARITY, w + "arity (subtraction 2, union/intersection >= 2) (S:184)");
+          }
+          for (int c = 0; c < n.n_children; ++c)
+            if (n.children[c] <= k || n.children[c] >= d.n_nodes) {
+              delete sc;
+              return fail(CM_ERR_INVALID, w + "child index must point to a later node");
+            }
+        }
+      }
+      // flatten: depth-first emission with composed frames
+      bool uses_x = false;
+      int max_depth = 0;
+      struct Item { int node; float child_sign; Frame parent; int depth; };
+      std::string err;
+      std::function<bool(int, float, const Frame&, int)> emit;
+      emit = [&](int k, float cs, const Frame& parent, int depth) -> bool {
+        const cm_node& n = d.nodes[k];
+        Frame fr = compose(parent, n.pose);
+        if (n.type <= CM_XPSQ) {
+          Leaf L;
+          std::memset(&L, 0, sizeof(L));
+          bool ident = true;
+          for (int i = 0; i < 9; ++i) {
+            L.R[i] = (float)fr.R[i];
+            ident &= L.R[i] == ((i % 4 == 0) ? 1.f : 0.f);
+          }
+          for (int i = 0; i < 3; ++i) L.t[i] = (float)fr.t[i];
+          L.rot_identity = ident ? 1 : 0;
+          L.n_planes = n.type == CM_PSQ ? n.n_planes : (n.type == CM_HALFSPACE ? 1 : 0);
+          for (int j = 0; j < L.n_planes && n.type != CM_XPSQ; ++j)
+            for (int i = 0; i < 4; ++i) L.planes[j][i] = n.planes[0][j][i];
+          if (n.type == CM_HALFSPACE) {
+            L.kind = LK_HALFSPACE;
+          } else if (n.type == CM_XPSQ) {
+            L.kind = LK_XPSQ;
+            L.n_planes = 0;
+            L.xidx = (int32_t)xps.size();
+            xps.push_back(pack_xpsq(n));
+            uses_x = true;
+          } else {
+            L.kind = LK_SQ;
+            double e1 = n.eps[0][0], e2 = n.eps[0][1];
+            for (int i = 0; i < 3; ++i) L.ia[i] = (float)(1.0 / n.a[0][i]);
+            L.p1 = (float)(1.0 / e1);
+            L.p2 = (float)(1.0 / e2);
+            L.m = (float)(e2 / e1);
+            L.k = (float)(0.5 * e1);
+          }
+          prog.push_back(Instr{OP_LEAF, (int32_t)leaves.size(), cs, 1.f});
+          leaves.push_back(L);
+          return true;
+        }
+        if (depth >= CM_MAX_DEPTH) {
+          err = "boolean nesting deeper than CM_MAX_DEPTH";
+          return false;
+        }
+        max_depth = std::max(max_depth, depth + 1);
+        prog.push_back(Instr{OP_BEGIN, 0, 0.f, 0.f});
+        for (int c = 0; c < n.n_children; ++c) {
+          float s2 = n.type == CM_UNION ? -1.f : (n.type == CM_INTERSECTION ? 1.f : (c == 0 ? 1.f : -1.f));
+          if (!emit(n.children[c], s2, fr, depth + 1)) return false;
+        }
+        prog.push_back(Instr{OP_END, 0, cs, n.type == CM_UNION ? -1.f : 1.f});
+        return true;
+      };
+      Frame id;
+      for (int i = 0; i < 9; ++i) id.R[i] = (i % 4 == 0) ? 1.0 : 0.0;
+      id.t[0] = id.t[1] = id.t[2] = 0.0;
+      if (!emit(0, 1.f, id, 0)) { delete sc; return fail(CM_ERR_UNSUPPORTED, "shape " + std::to_string(s) + ": " + err); }
+      r.has_sdf = 1;
+      r.uses_xpsq = uses_x ? 1 : 0;
+      ++n_sdf;
+      n_xp += uses_x ? 1 : 0;
+    }
+    r.prog_len = (int32_t)prog.size() - r.prog_begin;
+
+    // sampled surface + topology: unique sorted edges,
+    // face_edges for (i0,i1), (i1,i2), (i2,i0)
+    if (d.n_faces > 0) {
+      if (!d.vertices || !d.faces || d.n_vertices < 3) {
+        delete sc;
+        return fail(CM_ERR_INVALID, "shape " + std::to_string(s) + ": mesh arrays");
+      }
+      if (!finite_all(d.vertices, 3 * d.n_vertices)) { delete sc; return fail(CM_ERR_NONFINITE, "mesh vertex"); }
+      const int V = d.n_vertices, F = d.n_faces;
+      std::vector<std::tuple<int, int, int>> keys;   // (lo, hi, face*3 + k)
+      keys.reserve(3 * F);
+      for (int f = 0; f < F; ++f)
+        for (int k = 0; k < 3; ++k) {
+          int a = d.faces[3 * f + k], b = d.faces[3 * f + (k + 1) % 3];
+          if (a < 0 || b < 0 || a >= V || b >= V || a == b) {
+            delete sc;
+            return fail(CM_ERR_INVALID, "shape " + std::to_string(s) + ": bad or degenerate face " + std::to_string(f));
+          }
+          keys.emplace_back(std::min(a, b), std::max(a, b), 3 * f + k);
+        }
+      std::sort(keys.begin(), keys.end());
+      std::vector<int32_t>& eg = sc->edges[s];
+      std::vector<int32_t>& fe = sc->face_edges[s];
+      fe.assign(3 * F, -1);
+      int E = 0;
+      for (size_t i = 0; i < keys.size(); ++i) {
+        if (i == 0 || std::get<0>(keys[i]) != std::get<0>(keys[i - 1]) || std::get<1>(keys[i]) != std::get<1>(keys[i - 1])) {
+          int a = std::get<0>(keys[i]), b = std::get<1>(keys[i]);
+          const float* va = d.vertices + 3 * a;
+          const float* vb = d.vertices + 3 * b;
+          if (va[0] == vb[0] && va[1] == vb[1] && va[2] == vb[2]) {
+            delete sc;
+            return fail(CM_ERR_INVALID, "degenerate (zero-length) edge (S:455)");
+          }
+          eg.push_back(a);
+          eg.push_back(b);
+          ++E;
+        }
+        fe[std::get<2>(keys[i])] = E - 1;
+      }
+      r.V = V; r.E = E; r.F = F;
+      r.v_off = (int32_t)(verts.size() / 3);
+      r.e_off = (int32_t)(edges_all.size() / 2);
+      r.f_off = (int32_t)(faces_all.size() / 3);
+      verts.insert(verts.end(), d.vertices, d.vertices + 3 * V);
+      edges_all.insert(edges_all.end(), eg.begin(), eg.end());
+      faces_all.insert(faces_all.end(), d.faces, d.faces + 3 * F);
+      fe_all.insert(fe_all.end(), fe.begin(), fe.end());
+      sc->max_V = std::max(sc->max_V, V);
+      sc->max_E = std::max(sc->max_E, E);
+      sc->max_F = std::max(sc->max_F, F);
+    }
+  }
+  sc->shapes = recs;
+  sc->xp_class = n_xp == 0 ? 0 : (n_xp == n_sdf ? 1 : 2);
+
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) { delete sc; return fail(CM_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)); }
+  int rc = CM_OK;
+  SceneDev& D = sc->dev;
+  std::memset(&D, 0, sizeof(D));
+  D.prog = dev_copy(prog, rc);
+  D.leaves = dev_copy(leaves, rc);
+  D.xpsq = dev_copy(xps, rc);
+  D.shapes = dev_copy(recs, rc);
+  D.verts = dev_copy(verts, rc);
+  D.edges = dev_copy(edges_all, rc);
+  D.faces = dev_copy(faces_all, rc);
+  D.face_edges = dev_copy(fe_all, rc);
+  for (const void* p : {(const void*)D.prog, (const void*)D.leaves, (const void*)D.xpsq, (const void*)D.shapes,
+                        (const void*)D.verts, (const void*)D.edges, (const void*)D.faces, (const void*)D.face_edges})
+    if (p) sc->allocs.push_back(const_cast<void*>(p));
+  D.sp = SmoothDev{sp->tau_cmp, sp->tau_min, sp->tau_clip_alpha, sp->tau_clip_t, sp->tau_delta, sp->trace_iters};
+  D.n_shapes = n_shapes;
+  // global scratch for sampled surfaces whose pair state exceeds the shared
+  // memory budget of two resident CTAs per SM (e.g. C3's 16x32 patch at tier 2)
+  if (rc == CM_OK && sc->max_F > 0) {
+    int64_t need = cml::manifold_smem_floats(sc->max_V, sc->max_E, 2);
+    if (need * 4 > cmi::kSmemBudget) {
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+      sc->scratch_floats = need * (int64_t)sms * 4;
+      e = cudaMalloc(&sc->scratch, sc->scratch_floats * sizeof(float));
+      if (e != cudaSuccess) { rc = CM_ERR_OOM; g_err = "scratch allocation failed"; }
+      else sc->allocs.push_back(sc->scratch);
+    }
+  }
+  if (rc != CM_OK) {
+    cm_scene_destroy(sc);
+    return rc;
+  }
+  *out = sc;
+  return CM_OK;
+}
+
+int cm_scene_destroy(cm_scene* sc) {
+  if (!sc) return CM_OK;
+  for (void* p : sc->allocs) cudaFree(p);
+  delete sc;
+  return CM_OK;
+}
+
+int cm_shape_counts(const cm_scene* sc, int32_t s, int32_t* V, int32_t* E, int32_t* F) {
+  if (!sc || s < 0 || s >= (int)sc->shapes.size() || !V || !E || !F) return fail(CM_ERR_INVALID, "cm_shape_counts");
+  *V = sc->shapes[s].V; *E = sc->shapes[s].E; *F = sc->shapes[s].F;
+  return CM_OK;
+}
+
+int cm_shape_topology(const cm_scene* sc, int32_t s, int32_t* edges, int32_t* face_edges) {
+  if (!sc || s < 0 || s >= (int)sc->shapes.size()) return fail(CM_ERR_INVALID, "cm_shape_topology");
+  if (edges) std::memcpy(edges, sc->edges[s].data(), sc->edges[s].size() * sizeof(int32_t));
+  if (face_edges) std::memcpy(face_edges, sc->face_edges[s].data(), sc->face_edges[s].size() * sizeof(int32_t));
+  return CM_OK;
+}
+
+int cm_sdf_eval(const cm_scene* sc, const int32_t* ids, const float* poses, const float* points, int64_t B, int64_t P,
+                uint32_t flags, float* d, float* grad, float* hess, float* dpose, float* d2pose, float* dxdpose,
+                void* stream) {
+  if (!sc || !ids || !poses || !points || !d) return fail(CM_ERR_INVALID, "cm_sdf_eval: NULL argument");
+  if (B < 0 || P < 0) return fail(CM_ERR_INVALID, "cm_sdf_eval: negative size");
+  if (B == 0 || P == 0) return CM_OK;
+  if (((uintptr_t)poses & 15) != 0) return fail(CM_ERR_INVALID, "cm_sdf_eval: poses must be 16-byte aligned");
+  if ((flags & CM_SDF_GRAD) && !grad) return fail(CM_ERR_INVALID, "cm_sdf_eval: grad is NULL");
+  if ((flags & CM_SDF_HESS) && !hess) return fail(CM_ERR_INVALID, "cm_sdf_eval: hess is NULL");
+  if ((flags & CM_SDF_POSE_GRAD) && !dpose) return fail(CM_ERR_INVALID, "cm_sdf_eval: dpose is NULL");
+  if ((flags & CM_SDF_POSE_HESS) && (!d2pose || !dxdpose)) return fail(CM_ERR_INVALID, "cm_sdf_eval: d2pose/dxdpose NULL");
+  int rc = cml::launch_sdf_eval(sc->dev, sc->xp_class != 0, ids, poses, points, B, P, flags, d,
+                                (flags & CM_SDF_GRAD) ? grad : nullptr, (flags & CM_SDF_HESS) ? hess : nullptr, dpose,
+                                d2pose, dxdpose, stream);
+  if (rc) return fail(rc, cml::last_cuda_error());
+  return CM_OK;
+}
+
+int cm_manifold_size(const cm_scene* sc, const int32_t* shapeA, int64_t n_pairs, int64_t stride, int64_t* n) {
+  if (!sc || (!shapeA && n_pairs > 0) || !n) return fail(CM_ERR_INVALID, "cm_manifold_size");
+  int64_t c = 0;
+  for (int64_t i = 0; i < n_pairs; ++i) {
+    int s = shapeA[i * stride];
+    if (s < 0 || s >= (int)sc->shapes.size()) return fail(CM_ERR_INVALID, "cm_manifold_size: bad shape id");
+    c += sc->shapes[s].F;
+  }
+  *n = c;
+  return CM_OK;
+}
+
+int64_t cm_manifold_offsets_workspace(int64_t n_pairs) { return cml::offsets_workspace(n_pairs); }
+
+int cm_manifold_offsets(const cm_scene* sc, const int32_t* pairs, int64_t n_pairs, int64_t* offsets, void* ws,
+                        int64_t ws_bytes, void* stream) {
+  if (!sc || !pairs || !offsets || !ws) return fail(CM_ERR_INVALID, "cm_manifold_offsets: NULL argument");
+  if (n_pairs > (int64_t)0x7fffffff) return fail(CM_ERR_UNSUPPORTED, "cm_manifold_offsets: too many pairs");
+  if (ws_bytes < cml::offsets_workspace(n_pairs)) return fail(CM_ERR_INVALID, "cm_manifold_offsets: workspace too small");
+  int rc = cml::launch_offsets(sc->dev, pairs, n_pairs, offsets, ws, ws_bytes, stream);
+  if (rc) return fail(rc, cml::last_cuda_error());
+  return CM_OK;
+}
+
+int cm_contact_manifold(const cm_scene* sc, const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,
+                        const float* poses, int64_t n_env, int32_t n_slot, uint32_t flags, const cm_manifold_out* out,
+                        int64_t n_contacts, void* stream) {
+  if (!sc || !pairs || !offsets || !poses || !out) return fail(CM_ERR_INVALID, "cm_contact_manifold: NULL argument");
+  if (n_pairs < 0 || n_env < 0 || n_slot <= 0 || n_contacts < 0) return fail(CM_ERR_INVALID, "cm_contact_manifold: sizes");
+  if (n_pairs == 0) return CM_OK;
+  const unsigned tier = flags & CM_TIER_MASK;
+  if (tier > 2) return fail(CM_ERR_INVALID, "cm_contact_manifold: tier");
+  if (!out->point || !out->normal || !out->depth || !out->dom) return fail(CM_ERR_INVALID, "tier-0 outputs are NULL");
+  if (tier >= 1 && (!out->W || !out->q)) return fail(CM_ERR_INVALID, "tier-1 outputs are NULL");
+  if (tier >= 2 && (!out->ddepth || !out->dnormal)) return fail(CM_ERR_INVALID, "tier-2 outputs are NULL");
+  if (sc->max_F == 0) return fail(CM_ERR_INVALID, "scene has no sampled surface");
+  int rc = cml::launch_manifold(sc->dev, sc->xp_class, sc->max_V, sc->max_E, pairs, n_pairs, offsets, poses, n_slot,
+                                flags, out, n_contacts, sc->scratch, sc->scratch_floats, stream);
+  if (rc) return fail(rc, cml::last_cuda_error());
+  return CM_OK;
+}
+
+int cm_expand_jacobian(const cm_scene* sc, const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,
+                       const float* poses, int64_t n_env, int32_t n_slot, const float* W, const float* q,
+                       int64_t n_contacts, float* J, void* stream) {
+  (void)n_env;
+  if (!sc || !pairs || !offsets || !poses || !W || !q || !J) return fail(CM_ERR_INVALID, "cm_expand_jacobian");
+  int rc = cml::launch_expand(pairs, n_pairs, offsets, sc->dev, poses, n_slot, W, q, n_contacts, J, stream);
+  if (rc) return fail(rc, cml::last_cuda_error());
+  return CM_OK;
+}
+
+int64_t cm_launch_count(void) { return cml::launch_count(); }
+
+}  // extern "C"

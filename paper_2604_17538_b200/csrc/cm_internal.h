@@ -1,0 +1,112 @@
+// Internal layouts shared by the host library (cm_host.cpp) and the sm_100a
+// kernels (cm_kernels.cu).  Not part of the ABI.
+#pragma once
+#include <stdint.h>
+
+#include "xpsq_cm.h"
+
+namespace cmi {
+
+// ---- shape program ---------------------------------------------------------
+// A shape's SDF tree is flattened into a postfix-like program evaluated with a
+// small stack of streaming LSE accumulators (one per open boolean node):
+//   BEGIN        open an accumulator
+//   LEAF k       evaluate leaf k, fold child_sign * result into the top
+//   END          close the top: out_sign * LSE(...), fold child_sign * it
+// Union: children -1, out -1 (-LSE(-phi), Eq. (2)); intersection +1, +1
+// (Eq. (3)); subtraction (+1, -1), out +1 (Eq. (4)).
+enum { OP_LEAF = 0, OP_BEGIN = 1, OP_END = 2 };
+struct Instr {
+  int32_t op;
+  int32_t idx;
+  float child_sign;
+  float out_sign;
+};
+
+enum { LK_HALFSPACE = 0, LK_SQ = 1, LK_XPSQ = 3 };
+
+// Leaf record (SQ / PSQ / half-space; XPSQ points into Xpsq[xidx]).
+// Frame: x_body = R y + t (composed down the tree on the host in FP64).
+struct Leaf {
+  float R[9];
+  float t[3];
+  int32_t kind;
+  int32_t n_planes;
+  int32_t rot_identity;
+  int32_t xidx;
+  float ia[3];            // 1 / a
+  float p1, p2, m, k;     // 1/eps1, 1/eps2, eps2/eps1, eps1/2
+  float planes[CM_MAX_PLANES][4];
+};
+
+// XPSQ static data: p(t) = p1 + B t + A t^2 (A := 0 for the
+// snapped straight class), projection cubic constants in the affine form
+//   P = gP . w + P0,  Q = gQ . w + Q0,  w = y - p1
+// (c3, c2 depend only on the spline; c1, c0 are affine in w), b3 = b/3.
+struct Xpsq {
+  float p1[3], A[3], B[3];
+  float gP[3], gQ[3], P0, Q0, b3;
+  float Bn[3];            // straight class: t = softclip(Bn . w)
+  float bhat[3];          // Frenet binormal (constant for a quadratic)
+  float R0[9];            // constant frame (straight / point / A || B)
+  int32_t cls;            // 0 point, 1 straight, 2 curve
+  int32_t frenet;
+  int32_t varying;        // schedules differ between the endpoints
+  int32_t n_planes;
+  float eps0[2], deps[2];
+  float a0[3], da[3];
+  float pl0[CM_MAX_PLANES][4], dpl[CM_MAX_PLANES][4];
+};
+
+struct ShapeRec {
+  int32_t prog_begin, prog_len;
+  int32_t has_sdf, uses_xpsq;
+  int32_t V, E, F;
+  int32_t v_off, e_off, f_off;   // into verts (x3), edges (x2), faces / face_edges (x3)
+  int32_t pad;
+};
+
+struct SmoothDev {
+  float tau_cmp, tau_min, tau_clip_alpha, tau_clip_t, tau_delta;
+  int32_t iters;
+};
+
+// everything a kernel needs to evaluate any shape of the scene
+struct SceneDev {
+  const Instr* prog;
+  const Leaf* leaves;
+  const Xpsq* xpsq;
+  const ShapeRec* shapes;
+  const float* verts;
+  const int32_t* edges;
+  const int32_t* faces;
+  const int32_t* face_edges;
+  SmoothDev sp;
+  int32_t n_shapes;
+};
+
+// per-pair candidate state above this many bytes goes to a global (L2
+// resident) scratch instead of shared memory, so that >= 2 CTAs fit per SM
+constexpr int64_t kSmemBudget = 110 * 1024;
+
+}  // namespace cmi
+
+// launchers implemented in cm_kernels.cu
+namespace cml {
+int launch_sdf_eval(const cmi::SceneDev& s, bool xp_class, const int32_t* shape_ids, const float* poses,
+                    const float* points, int64_t B, int64_t P, uint32_t flags, float* d, float* grad, float* hess,
+                    float* dpose, float* d2pose, float* dxdpose, void* stream);
+int launch_manifold(const cmi::SceneDev& s, int which_class, int max_V, int max_E, const int32_t* pairs,
+                    int64_t n_pairs, const int64_t* offsets, const float* poses, int32_t n_slot, uint32_t flags,
+                    const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats, void* stream);
+int launch_offsets(const cmi::SceneDev& s, const int32_t* pairs, int64_t n_pairs, int64_t* offsets, void* ws,
+                   int64_t ws_bytes, void* stream);
+int64_t offsets_workspace(int64_t n_pairs);
+int launch_expand(const int32_t* pairs, int64_t n_pairs, const int64_t* offsets, const cmi::SceneDev& s,
+                  const float* poses, int32_t n_slot, const float* W, const float* q, int64_t C, float* J,
+                  void* stream);
+int64_t manifold_smem_floats(int V, int E, int tier);
+int manifold_max_smem_bytes();
+const char* last_cuda_error();
+int64_t launch_count();
+}  // namespace cml

@@ -1,0 +1,506 @@
+// sm_100a kernels of the hot path (arXiv 2604.17538):
+//   k_sdf_eval          batched SDF value / gradient / Hessian (+ pose
+//                       derivatives) — §II-B, Eq. (1)-(6)
+//   k_contact_manifold  one CTA per (env, pair): sampled-surface vertices ->
+//                       sphere-traced edge points -> 6 candidates per face ->
+//                       softmax fusion -> SoA stores — §II-C
+//   k_face_counts / cub scan, k_expand_jacobian   (offsets, J expansion)
+//
+// Hot-path design: FP32 CUDA-core math (no tensor cores: the
+// path is not a dense contraction), MUFU ex2/lg2/rcp in the log domain,
+// pair-local candidate state in shared memory, field-major coalesced stores.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+
+#include "cm_device.cuh"
+#include "cm_internal.h"
+#include "cm_launch.h"
+
+using namespace cmi;
+using namespace cmd;
+
+using cml::check_launch;
+using cml::num_sms;
+
+// ============================================================================
+// contact manifold
+// ============================================================================
+// Per-pair candidate storage (field-major, stride = V or E):
+//   vertex fields: xb[3] (B-local), pw[3] (world), d, n[3] (world grad phi),
+//                  H[6] (world, tier 2)
+//   edge fields during the trace: aI, aII, daI[12], daII[12] (tier 2);
+//   after the midpoint phase:     pw[3], d, n[3], H[6], dab[12] (tier 2)
+__host__ __device__ constexpr int vfields(int tier) { return tier >= 2 ? 16 : 10; }
+__host__ __device__ constexpr int efields(int tier) { return tier >= 2 ? 26 : 7; }
+enum { VX = 0, VP = 3, VD = 6, VN = 7, VH = 10 };
+enum { EA = 0, EB = 1, EDA = 2, EDB = 14 };             // trace layout
+enum { EP = 0, ED = 3, EN = 4, EH = 7, EDAB = 13 };     // midpoint layout
+
+struct PairFrame {
+  float RA[9], tA[3], RB[9], tB[3];
+  float Rrel[9], trel[3];   // x_B = Rrel v_A + trel
+};
+
+__device__ __forceinline__ void pair_frame(const float* pa, const float* pb, PairFrame& F) {
+  float qa[4] = {pa[3], pa[4], pa[5], pa[6]}, qb[4] = {pb[3], pb[4], pb[5], pb[6]};
+  quat_to_R(qa, F.RA);
+  quat_to_R(qb, F.RB);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) { F.tA[i] = pa[i]; F.tB[i] = pb[i]; }
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      F.Rrel[i * 3 + j] = F.RB[0 * 3 + i] * F.RA[0 * 3 + j] + F.RB[1 * 3 + i] * F.RA[1 * 3 + j] +
+                          F.RB[2 * 3 + i] * F.RA[2 * 3 + j];
+  float dt[3] = {F.tA[0] - F.tB[0], F.tA[1] - F.tB[1], F.tA[2] - F.tB[2]};
+#pragma unroll
+  for (int i = 0; i < 3; ++i) F.trel[i] = F.RB[0 * 3 + i] * dt[0] + F.RB[1 * 3 + i] * dt[1] + F.RB[2 * 3 + i] * dt[2];
+}
+
+// g^T J(p) for J(p) = [I, -[p - tA]x, -I, [p - tB]x]: the A blocks
+// (t_A: g, theta_A: (p - tA) x g) and theta_B: g x (p - tB).  The t_B block is
+// exactly -(t_A block) and is reconstructed at store time.
+__device__ __forceinline__ void gJ(const float* g, const float* p, const PairFrame& F, float* o /*9*/) {
+  const float ra[3] = {p[0] - F.tA[0], p[1] - F.tA[1], p[2] - F.tA[2]};
+  const float rb[3] = {p[0] - F.tB[0], p[1] - F.tB[1], p[2] - F.tB[2]};
+  o[0] = g[0]; o[1] = g[1]; o[2] = g[2];
+  o[3] = ra[1] * g[2] - ra[2] * g[1];
+  o[4] = ra[2] * g[0] - ra[0] * g[2];
+  o[5] = ra[0] * g[1] - ra[1] * g[0];
+  o[6] = g[1] * rb[2] - g[2] * rb[1];
+  o[7] = g[2] * rb[0] - g[0] * rb[2];
+  o[8] = g[0] * rb[1] - g[1] * rb[0];
+}
+
+// derivative slots: 9 independent components (tA, thetaA, thetaB); tB = -tA
+constexpr int NDQ = 9;
+
+template <int TIER, bool XP>
+__global__ void __launch_bounds__(128) k_contact_manifold(SceneDev S, const int32_t* __restrict__ pairs,
+                                                          int64_t n_pairs, const int64_t* __restrict__ offsets,
+                                                          const float* __restrict__ poses, int32_t n_slot,
+                                                          cm_manifold_out out, int64_t C, int xp_filter,
+                                                          float* __restrict__ scratch, int64_t scratch_floats) {
+  extern __shared__ float smem[];
+  constexpr int OV = TIER >= 2 ? 2 : 1;   // order at vertices / midpoints
+  constexpr int OT = TIER >= 2 ? 1 : 0;   // order inside the trace
+  const SmoothDev sp = S.sp;
+  const float tcmp = sp.tau_cmp, itcmp = 1.f / tcmp;
+  const float tmin = sp.tau_min, itmin = 1.f / tmin;
+  const float tca = sp.tau_clip_alpha, itca = 1.f / tca;
+  float* st = scratch ? scratch + (int64_t)blockIdx.x * scratch_floats : smem;
+  __shared__ PairFrame Fs;
+  __shared__ ShapeRec SA, SB;
+
+  for (int64_t pi = blockIdx.x; pi < n_pairs; pi += gridDim.x) {
+    const int32_t* pr = pairs + 5 * pi;
+    const int env = __ldg(pr + 0), slA = __ldg(pr + 1), slB = __ldg(pr + 2);
+    const int shA = __ldg(pr + 3), shB = __ldg(pr + 4);
+    const ShapeRec sa = S.shapes[shA];
+    const ShapeRec sb = S.shapes[shB];
+    if (xp_filter >= 0 && sb.uses_xpsq != xp_filter) continue;   // uniform across the CTA
+    __syncthreads();   // previous pair's readers of Fs / st are done
+    if (threadIdx.x == 0) {
+      float pa[8], pb[8];
+      const float* a = poses + 8 * ((int64_t)env * n_slot + slA);
+      const float* b = poses + 8 * ((int64_t)env * n_slot + slB);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { pa[i] = __ldg(a + i); pb[i] = __ldg(b + i); }
+      pair_frame(pa, pb, Fs);
+      SA = sa;
+      SB = sb;
+    }
+    __syncthreads();
+    const PairFrame& F = Fs;
+    const int V = sa.V, E = sa.E, NF = sa.F;
+    float* sv = st;                                   // vertex block
+    float* se = st + (int64_t)vfields(TIER) * V;      // edge block
+    const float* lv = S.verts + 3 * (int64_t)sa.v_off;
+    const int32_t* ed = S.edges + 2 * (int64_t)sa.e_off;
+
+    // ---- phase 1: vertices: phi, n (and H) of B -------------
+    for (int v = threadIdx.x; v < V; v += blockDim.x) {
+      const float x[3] = {__ldg(lv + 3 * v), __ldg(lv + 3 * v + 1), __ldg(lv + 3 * v + 2)};
+      float xb[3], pw[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        xb[i] = F.Rrel[i * 3] * x[0] + F.Rrel[i * 3 + 1] * x[1] + F.Rrel[i * 3 + 2] * x[2] + F.trel[i];
+        pw[i] = F.RA[i * 3] * x[0] + F.RA[i * 3 + 1] * x[1] + F.RA[i * 3 + 2] * x[2] + F.tA[i];
+      }
+      Res<OV> r;
+      eval_shape<OV, XP>(S, SB, xb, r);
+      float n[3];
+      rot_vec(F.RB, r.g, n);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        sv[(VX + i) * V + v] = xb[i];
+        sv[(VP + i) * V + v] = pw[i];
+        sv[(VN + i) * V + v] = n[i];
+      }
+      sv[VD * V + v] = r.v;
+      if constexpr (TIER >= 2) {
+        float h[6];
+        rot_sym(F.RB, r.h, h);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) sv[(VH + k) * V + v] = h[k];
+      }
+    }
+    __syncthreads();
+
+    // ---- phase 2: sphere traces (Fig. 2), 2 per edge -------------
+    for (int j = threadIdx.x; j < 2 * E; j += blockDim.x) {
+      const int e = j < E ? j : j - E;
+      const int dir = j < E ? 0 : 1;     // 0: from v_I along +e_t; 1: from v_II along -e_t
+      const int vI = __ldg(ed + 2 * e), vII = __ldg(ed + 2 * e + 1);
+      const float dl[3] = {__ldg(lv + 3 * vII) - __ldg(lv + 3 * vI), __ldg(lv + 3 * vII + 1) - __ldg(lv + 3 * vI + 1),
+                           __ldg(lv + 3 * vII + 2) - __ldg(lv + 3 * vI + 2)};
+      const float L = sqrtf(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
+      const float iL = 1.f / L;
+      const float el[3] = {dl[0] * iL, dl[1] * iL, dl[2] * iL};
+      float eb[3], ew[3];
+      rot_vec(F.Rrel, el, eb);
+      rot_vec(F.RA, el, ew);
+      const float xI[3] = {sv[(VX + 0) * V + vI], sv[(VX + 1) * V + vI], sv[(VX + 2) * V + vI]};
+      const float pI[3] = {sv[(VP + 0) * V + vI], sv[(VP + 1) * V + vI], sv[(VP + 2) * V + vI]};
+      const int v0 = dir ? vII : vI;
+      float al = dir ? L : 0.f;
+      const float sgn = dir ? -1.f : 1.f;
+      float da[NDQ];
+#pragma unroll
+      for (int k = 0; k < NDQ; ++k) da[k] = 0.f;
+      for (int it = 0; it < sp.iters; ++it) {
+        float phi, g[3];
+        if (it == 0) {   // the corner itself: reuse the vertex evaluation (reading #22)
+          phi = sv[VD * V + v0];
+          g[0] = sv[(VN + 0) * V + v0]; g[1] = sv[(VN + 1) * V + v0]; g[2] = sv[(VN + 2) * V + v0];
+        } else {
+          const float xb[3] = {fmaf(al, eb[0], xI[0]), fmaf(al, eb[1], xI[1]), fmaf(al, eb[2], xI[2])};
+          Res<OT> r;
+          eval_shape<OT, XP>(S, SB, xb, r);
+          phi = r.v;
+          if constexpr (TIER >= 2) rot_vec(F.RB, r.g, g);
+        }
+        // gated step G(phi) = sigma(phi / tau) phi  (reading #20)
+        const float s = sigm(phi * itcmp);
+        if constexpr (TIER >= 2) {
+          // d alpha_{k+1} = d alpha_k + sgn G'(phi) [g^T J(p) dq + (g.e_t) d alpha_k]
+          const float Gp = fmaf(phi * s * (1.f - s), itcmp, s);
+          const float p[3] = {fmaf(al, ew[0], pI[0]), fmaf(al, ew[1], pI[1]), fmaf(al, ew[2], pI[2])};
+          float gj[NDQ];
+          gJ(g, p, F, gj);
+          const float ge = g[0] * ew[0] + g[1] * ew[1] + g[2] * ew[2];
+          const float c = sgn * Gp;
+#pragma unroll
+          for (int k = 0; k < NDQ; ++k) da[k] = fmaf(c, fmaf(ge, da[k], gj[k]), da[k]);
+        }
+        al = fmaf(sgn * s, phi, al);
+      }
+      // soft clip to the edge (reading #21)
+      const float at = softclip(al, 0.f, L, tca, itca);
+      se[(dir ? EB : EA) * E + e] = at;
+      if constexpr (TIER >= 2) {
+        const float cd = softclip_d(al, 0.f, L, itca);
+        const int base = dir ? EDB : EDA;
+#pragma unroll
+        for (int k = 0; k < NDQ; ++k) se[(base + k) * E + e] = cd * da[k];
+      }
+    }
+    __syncthreads();
+
+    // ---- phase 3: edge midpoints p_e = (p_I + p_II)/2 ----------------
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+      const int vI = __ldg(ed + 2 * e), vII = __ldg(ed + 2 * e + 1);
+      const float dl[3] = {__ldg(lv + 3 * vII) - __ldg(lv + 3 * vI), __ldg(lv + 3 * vII + 1) - __ldg(lv + 3 * vI + 1),
+                           __ldg(lv + 3 * vII + 2) - __ldg(lv + 3 * vI + 2)};
+      const float iL = rsqrtf(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
+      const float el[3] = {dl[0] * iL, dl[1] * iL, dl[2] * iL};
+      float eb[3], ew[3];
+      rot_vec(F.Rrel, el, eb);
+      rot_vec(F.RA, el, ew);
+      const float ab = 0.5f * (se[EA * E + e] + se[EB * E + e]);
+      float dab[NDQ];
+      if constexpr (TIER >= 2) {
+#pragma unroll
+        for (int k = 0; k < NDQ; ++k) dab[k] = 0.5f * (se[(EDA + k) * E + e] + se[(EDB + k) * E + e]);
+      }
+      float xb[3], pw[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        xb[i] = fmaf(ab, eb[i], sv[(VX + i) * V + vI]);
+        pw[i] = fmaf(ab, ew[i], sv[(VP + i) * V + vI]);
+      }
+      Res<OV> r;
+      eval_shape<OV, XP>(S, SB, xb, r);
+      float n[3];
+      rot_vec(F.RB, r.g, n);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        se[(EP + i) * E + e] = pw[i];
+        se[(EN + i) * E + e] = n[i];
+      }
+      se[ED * E + e] = r.v;
+      if constexpr (TIER >= 2) {
+        float h[6];
+        rot_sym(F.RB, r.h, h);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) se[(EH + k) * E + e] = h[k];
+#pragma unroll
+        for (int k = 0; k < NDQ; ++k) se[(EDAB + k) * E + e] = dab[k];
+      }
+    }
+    __syncthreads();
+
+    // ---- phase 4: per-face fusion -------------------------------
+    const int64_t off = __ldg(offsets + pi);
+    const int32_t* fv = S.faces + 3 * (int64_t)sa.f_off;
+    const int32_t* fe = S.face_edges + 3 * (int64_t)sa.f_off;
+    const float itlm = LOG2E * itmin;
+    for (int f = threadIdx.x; f < NF; f += blockDim.x) {
+      int cv[3], ce[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) { cv[k] = __ldg(fv + 3 * f + k); ce[k] = __ldg(fe + 3 * f + k); }
+      // candidate depths d_i; order [v_i0, v_i1, v_i2, e(i0,i1), e(i1,i2), e(i2,i0)]
+      float dc[6];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) { dc[k] = sv[VD * V + cv[k]]; dc[3 + k] = se[ED * E + ce[k]]; }
+      float dm = dc[0];
+#pragma unroll
+      for (int i = 1; i < 6; ++i) dm = fminf(dm, dc[i]);
+      float z[6], Z = 0.f;
+#pragma unroll
+      for (int i = 0; i < 6; ++i) { z[i] = ex2((dm - dc[i]) * itlm); Z += z[i]; }
+      const float iZ = 1.f / Z;
+      float zg[6];
+      float Wf = 0.f, best = -1.f;
+      int dom = 0;
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        z[i] *= iZ;                                   // z = s_argmax(-d)
+        const float gam = sigm(-dc[i] * itcmp);        // gamma = [[d < 0]]
+        zg[i] = z[i] * gam;
+        Wf += zg[i];
+        if (zg[i] > best) { best = zg[i]; dom = i; }
+      }
+      const float depth = fmaf(-tmin * LN2, lg2(Z), dm);   // smooth min (reading #25)
+      float nrm[3] = {0.f, 0.f, 0.f}, qv[3] = {0.f, 0.f, 0.f}, pt[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const bool isv = i < 3;
+        const int id = isv ? cv[i] : ce[i - 3];
+        const float* bp = isv ? sv + VP * V + id : se + EP * E + id;
+        const float* bn = isv ? sv + VN * V + id : se + EN * E + id;
+        const int sd = isv ? V : E;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const float p = bp[a * sd], nn = bn[a * sd];
+          nrm[a] = fmaf(zg[i], nn, nrm[a]);
+          qv[a] = fmaf(zg[i], p, qv[a]);
+          pt[a] = fmaf(z[i], p, pt[a]);
+        }
+      }
+      const int64_t c = off + f;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        out.point[a * C + c] = pt[a];
+        out.normal[a * C + c] = nrm[a];
+      }
+      out.depth[c] = depth;
+      out.dom[c] = (int8_t)dom;
+      if constexpr (TIER >= 1) {
+        out.W[c] = Wf;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) out.q[a * C + c] = qv[a];
+      }
+      if constexpr (TIER >= 2) {
+        // d depth = sum z_i d d_i;  d d_i = g^T J(p_i) (+ (g.e_t) d alpha_bar)
+        float dd[NDQ];
+#pragma unroll
+        for (int k = 0; k < NDQ; ++k) dd[k] = 0.f;
+        float ddi[6][NDQ];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          const bool isv = i < 3;
+          const int id = isv ? cv[i] : ce[i - 3];
+          const float* bp = isv ? sv + VP * V + id : se + EP * E + id;
+          const float* bn = isv ? sv + VN * V + id : se + EN * E + id;
+          const int sd = isv ? V : E;
+          const float p[3] = {bp[0], bp[sd], bp[2 * sd]};
+          const float g[3] = {bn[0], bn[sd], bn[2 * sd]};
+          gJ(g, p, F, ddi[i]);
+          if (!isv) {
+            const int vI = __ldg(ed + 2 * id), vII = __ldg(ed + 2 * id + 1);
+            float ew[3] = {sv[(VP + 0) * V + vII] - sv[(VP + 0) * V + vI], sv[(VP + 1) * V + vII] - sv[(VP + 1) * V + vI],
+                           sv[(VP + 2) * V + vII] - sv[(VP + 2) * V + vI]};
+            const float il = rsqrtf(ew[0] * ew[0] + ew[1] * ew[1] + ew[2] * ew[2]);
+            const float ge = (g[0] * ew[0] + g[1] * ew[1] + g[2] * ew[2]) * il;
+#pragma unroll
+            for (int k = 0; k < NDQ; ++k) ddi[i][k] = fmaf(ge, se[(EDAB + k) * E + id], ddi[i][k]);
+          }
+#pragma unroll
+          for (int k = 0; k < NDQ; ++k) dd[k] = fmaf(z[i], ddi[i][k], dd[k]);
+        }
+        // d n = sum_i [d(z_i gamma_i) n_i + z_i gamma_i d n_i]
+        //   d(z gamma)_i = z_i gamma_i [-(d d_i - d depth)/tau_min - (1 - gamma_i) d d_i / tau_cmp]
+        //   d n_i = [H, -H[p - tA]x, (-H), H[p - tB]x - [n]x] (+ H e_t d alpha_bar)
+        float dn[3][NDQ];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int k = 0; k < NDQ; ++k) dn[a][k] = 0.f;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          const bool isv = i < 3;
+          const int id = isv ? cv[i] : ce[i - 3];
+          const float* bp = isv ? sv + VP * V + id : se + EP * E + id;
+          const float* bn = isv ? sv + VN * V + id : se + EN * E + id;
+          const float* bh = isv ? sv + VH * V + id : se + EH * E + id;
+          const int sd = isv ? V : E;
+          const float p[3] = {bp[0], bp[sd], bp[2 * sd]};
+          const float nn[3] = {bn[0], bn[sd], bn[2 * sd]};
+          const float h6[6] = {bh[0], bh[sd], bh[2 * sd], bh[3 * sd], bh[4 * sd], bh[5 * sd]};
+          const float H[3][3] = {{h6[0], h6[1], h6[2]}, {h6[1], h6[3], h6[4]}, {h6[2], h6[4], h6[5]}};
+          const float gam = sigm(-dc[i] * itcmp);
+          float cz[NDQ];
+#pragma unroll
+          for (int k = 0; k < NDQ; ++k)
+            cz[k] = zg[i] * (-(ddi[i][k] - dd[k]) * itmin - (1.f - gam) * ddi[i][k] * itcmp);
+          const float ra[3] = {p[0] - F.tA[0], p[1] - F.tA[1], p[2] - F.tA[2]};
+          const float rb[3] = {p[0] - F.tB[0], p[1] - F.tB[1], p[2] - F.tB[2]};
+          const float w = zg[i];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            // H [r]x row a: (H_a1 r2 - H_a2 r1, H_a2 r0 - H_a0 r2, H_a0 r1 - H_a1 r0)
+            const float hka0 = H[a][1] * ra[2] - H[a][2] * ra[1];
+            const float hka1 = H[a][2] * ra[0] - H[a][0] * ra[2];
+            const float hka2 = H[a][0] * ra[1] - H[a][1] * ra[0];
+            const float hkb0 = H[a][1] * rb[2] - H[a][2] * rb[1];
+            const float hkb1 = H[a][2] * rb[0] - H[a][0] * rb[2];
+            const float hkb2 = H[a][0] * rb[1] - H[a][1] * rb[0];
+            // [n]x row a
+            const float nk0 = a == 0 ? 0.f : (a == 1 ? nn[2] : -nn[1]);
+            const float nk1 = a == 0 ? -nn[2] : (a == 1 ? 0.f : nn[0]);
+            const float nk2 = a == 0 ? nn[1] : (a == 1 ? -nn[0] : 0.f);
+            float dni[NDQ] = {H[a][0], H[a][1], H[a][2], -hka0, -hka1, -hka2, hkb0 - nk0, hkb1 - nk1, hkb2 - nk2};
+#pragma unroll
+            for (int k = 0; k < NDQ; ++k) dn[a][k] = fmaf(nn[a], cz[k], fmaf(w, dni[k], dn[a][k]));
+          }
+          if (!isv) {
+            const int vI = __ldg(ed + 2 * id), vII = __ldg(ed + 2 * id + 1);
+            float ew[3] = {sv[(VP + 0) * V + vII] - sv[(VP + 0) * V + vI], sv[(VP + 1) * V + vII] - sv[(VP + 1) * V + vI],
+                           sv[(VP + 2) * V + vII] - sv[(VP + 2) * V + vI]};
+            const float il = rsqrtf(ew[0] * ew[0] + ew[1] * ew[1] + ew[2] * ew[2]);
+            float he[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) he[a] = (H[a][0] * ew[0] + H[a][1] * ew[1] + H[a][2] * ew[2]) * il * w;
+#pragma unroll
+            for (int k = 0; k < NDQ; ++k) {
+              const float dk = se[(EDAB + k) * E + id];
+#pragma unroll
+              for (int a = 0; a < 3; ++a) dn[a][k] = fmaf(he[a], dk, dn[a][k]);
+            }
+          }
+        }
+        // store: q order (tA 0-2, thetaA 3-5, tB 6-8 = -tA, thetaB 9-11)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          out.ddepth[k * C + c] = dd[k];
+          out.ddepth[(3 + k) * C + c] = dd[3 + k];
+          out.ddepth[(6 + k) * C + c] = -dd[k];
+          out.ddepth[(9 + k) * C + c] = dd[6 + k];
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            out.dnormal[(a * 12 + k) * C + c] = dn[a][k];
+            out.dnormal[(a * 12 + 3 + k) * C + c] = dn[a][3 + k];
+            out.dnormal[(a * 12 + 6 + k) * C + c] = -dn[a][k];
+            out.dnormal[(a * 12 + 9 + k) * C + c] = dn[a][6 + k];
+          }
+      }
+    }
+  }
+}
+
+namespace cml {
+
+int64_t manifold_smem_floats(int V, int E, int tier) {
+  return (int64_t)vfields(tier) * V + (int64_t)efields(tier) * E;
+}
+
+int manifold_max_smem_bytes() {
+  static int m = 0;
+  if (!m) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&m, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (m <= 0) m = 227 * 1024;
+  }
+  return m;
+}
+
+template <int TIER, bool XP>
+static int launch_manifold_t(const SceneDev& s, int xp_filter, int max_V, int max_E, const int32_t* pairs,
+                             int64_t n_pairs, const int64_t* offsets, const float* poses, int32_t n_slot,
+                             const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats,
+                             cudaStream_t st) {
+  const int threads = 128;
+  const int64_t need = manifold_smem_floats(max_V, max_E, TIER) * 4;
+  const int static_smem = (int)(sizeof(PairFrame) + 2 * sizeof(ShapeRec));
+  const bool use_smem = need <= kSmemBudget && need + static_smem + 1024 <= manifold_max_smem_bytes();
+  int smem = use_smem ? (int)need : 0;
+  auto kern = k_contact_manifold<TIER, XP>;
+  static int configured = 0;
+  if (smem > configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = smem;
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)num_sms() * per_sm;
+  if (!use_smem) {
+    if (scratch == nullptr) {
+      set_error("manifold: surface too large for shared memory and no scratch");
+      return CM_ERR_UNSUPPORTED;
+    }
+    int64_t slots = scratch_floats / (need / 4);
+    if (grid > slots) grid = slots;
+    if (grid < 1) {
+      set_error("manifold: scratch too small");
+      return CM_ERR_UNSUPPORTED;
+    }
+  }
+  if (grid > n_pairs) grid = n_pairs;
+  if (grid < 1) return CM_OK;
+  kern<<<(unsigned)grid, threads, smem, st>>>(s, pairs, n_pairs, offsets, poses, n_slot, *out, C, xp_filter,
+                                              use_smem ? nullptr : scratch, use_smem ? 0 : need / 4);
+  return check_launch("k_contact_manifold");
+}
+
+int launch_manifold(const SceneDev& s, int which_class, int max_V, int max_E, const int32_t* pairs,
+                    int64_t n_pairs, const int64_t* offsets, const float* poses, int32_t n_slot, uint32_t flags,
+                    const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats, void* stream) {
+  // which_class: -1 every pair uses the same instantiation (lean if the scene
+  // has no XPSQ, general otherwise); 2 mixed scene: lean kernel on pairs whose
+  // SDF shape has no XPSQ, general kernel on the others.
+  cudaStream_t st = (cudaStream_t)stream;
+  const int tier = (int)(flags & CM_TIER_MASK);
+  auto run = [&](bool xp, int filt) -> int {
+#define CM_L(T, X) launch_manifold_t<T, X>(s, filt, max_V, max_E, pairs, n_pairs, offsets, poses, n_slot, out, C, \
+                                           scratch, scratch_floats, st)
+    if (xp) return tier >= 2 ? CM_L(2, true) : (tier == 1 ? CM_L(1, true) : CM_L(0, true));
+    return tier >= 2 ? CM_L(2, false) : (tier == 1 ? CM_L(1, false) : CM_L(0, false));
+#undef CM_L
+  };
+  if (which_class == 0) return run(false, -1);
+  if (which_class == 1) return run(true, -1);
+  int rc = run(false, 0);
+  if (rc) return rc;
+  return run(true, 1);
+}
+
+}  // namespace cml

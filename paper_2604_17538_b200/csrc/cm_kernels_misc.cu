@@ -1,0 +1,128 @@
+// sm_100a kernels of the hot path (arXiv 2604.17538):
+//   k_sdf_eval          batched SDF value / gradient / Hessian (+ pose
+//                       derivatives) — §II-B, Eq. (1)-(6)
+//   k_contact_manifold  one CTA per (env, pair): sampled-surface vertices ->
+//                       sphere-traced edge points -> 6 candidates per face ->
+//                       softmax fusion -> SoA stores — §II-C
+//   k_face_counts / cub scan, k_expand_jacobian   (offsets, J expansion)
+//
+// Hot-path design: FP32 CUDA-core math (no tensor cores: the
+// path is not a dense contraction), MUFU ex2/lg2/rcp in the log domain,
+// pair-local candidate state in shared memory, field-major coalesced stores.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cub/device/device_scan.cuh>
+
+#include "cm_internal.h"
+#include "cm_launch.h"
+
+using namespace cmi;
+
+namespace {
+std::atomic<int64_t> g_launches{0};
+thread_local char g_cuda_msg[256];
+}  // namespace
+
+namespace cml {
+void count_launch() { g_launches.fetch_add(1); }
+void set_error(const char* msg) { snprintf(g_cuda_msg, sizeof(g_cuda_msg), "%s", msg); }
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  g_launches.fetch_add(1);
+  if (e != cudaSuccess) {
+    snprintf(g_cuda_msg, sizeof(g_cuda_msg), "%s: %s", what, cudaGetErrorString(e));
+    return CM_ERR_CUDA;
+  }
+  return CM_OK;
+}
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// ---- offsets: exclusive scan of F(shapeA) over the pairs ---------------------
+__global__ void k_face_counts(const ShapeRec* __restrict__ shapes, const int32_t* __restrict__ pairs, int64_t n,
+                              int64_t* __restrict__ cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    cnt[i] = shapes[__ldg(pairs + 5 * i + 3)].F;
+}
+
+int64_t offsets_workspace(int64_t n_pairs) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (int64_t*)nullptr, (int64_t*)nullptr, (int)n_pairs);
+  return (int64_t)bytes + 256;
+}
+
+int launch_offsets(const SceneDev& s, const int32_t* pairs, int64_t n_pairs, int64_t* offsets, void* ws,
+                   int64_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t blocks = (n_pairs + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  if (blocks < 1) return CM_OK;
+  k_face_counts<<<(unsigned)blocks, 256, 0, st>>>(s.shapes, pairs, n_pairs, offsets);
+  int rc = check_launch("k_face_counts");
+  if (rc) return rc;
+  size_t bytes = (size_t)ws_bytes;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(ws, bytes, offsets, offsets, (int)n_pairs, st);
+  g_launches.fetch_add(1);
+  if (e != cudaSuccess) {
+    snprintf(g_cuda_msg, sizeof(g_cuda_msg), "offsets scan: %s", cudaGetErrorString(e));
+    return CM_ERR_CUDA;
+  }
+  return CM_OK;
+}
+
+// ---- J expansion (App. A.7): J = [W I, -[q - W tA]x, -W I, [q - W tB]x] ------
+__global__ void k_expand_jacobian(const ShapeRec* __restrict__ shapes, const int32_t* __restrict__ pairs,
+                                  int64_t n_pairs, const int64_t* __restrict__ offsets,
+                                  const float* __restrict__ poses, int32_t n_slot, const float* __restrict__ W,
+                                  const float* __restrict__ q, int64_t C, float* __restrict__ J) {
+  for (int64_t pi = blockIdx.x; pi < n_pairs; pi += gridDim.x) {
+    const int32_t* pr = pairs + 5 * pi;
+    const float* pa = poses + 8 * ((int64_t)pr[0] * n_slot + pr[1]);
+    const float* pb = poses + 8 * ((int64_t)pr[0] * n_slot + pr[2]);
+    const int nf = shapes[pr[3]].F;
+    const int64_t off = offsets[pi];
+    for (int f = threadIdx.x; f < nf; f += blockDim.x) {
+      const int64_t c = off + f;
+      const float w = W[c];
+      const float qa[3] = {q[c] - w * pa[0], q[C + c] - w * pa[1], q[2 * C + c] - w * pa[2]};
+      const float qb[3] = {q[c] - w * pb[0], q[C + c] - w * pb[1], q[2 * C + c] - w * pb[2]};
+      const float Ka[3][3] = {{0.f, -qa[2], qa[1]}, {qa[2], 0.f, -qa[0]}, {-qa[1], qa[0], 0.f}};
+      const float Kb[3][3] = {{0.f, -qb[2], qb[1]}, {qb[2], 0.f, -qb[0]}, {-qb[1], qb[0], 0.f}};
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          J[(r * 12 + k) * C + c] = r == k ? w : 0.f;
+          J[(r * 12 + 3 + k) * C + c] = -Ka[r][k];
+          J[(r * 12 + 6 + k) * C + c] = r == k ? -w : 0.f;
+          J[(r * 12 + 9 + k) * C + c] = Kb[r][k];
+        }
+    }
+  }
+}
+
+int launch_expand(const int32_t* pairs, int64_t n_pairs, const int64_t* offsets, const SceneDev& s,
+                  const float* poses, int32_t n_slot, const float* W, const float* q, int64_t C, float* J,
+                  void* stream) {
+  int64_t grid = n_pairs < 65535 ? n_pairs : 65535;
+  if (grid < 1) return CM_OK;
+  k_expand_jacobian<<<(unsigned)grid, 128, 0, (cudaStream_t)stream>>>(s.shapes, pairs, n_pairs, offsets, poses,
+                                                                       n_slot, W, q, C, J);
+  return check_launch("k_expand_jacobian");
+}
+
+const char* last_cuda_error() { return g_cuda_msg; }
+int64_t launch_count() { return g_launches.load(); }
+
+}  // namespace cml

@@ -1,0 +1,218 @@
+"""GPU parity of the CUDA path (called through the C ABI) against the FP64
+oracle on the same seeded inputs.  Needs a B200."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from helpers import scene_of, pose8
+from paper_2604_17538_b200 import synth
+import parity as PT
+
+pytestmark = pytest.mark.gpu
+
+ALL = 1 | 2 | 4 | 8 | 16
+
+
+@pytest.fixture(scope="module")
+def cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_17538_b200 import binding
+    binding.lib()
+    return torch
+
+
+def _report(name, rep):
+    os.makedirs(os.path.join(os.path.dirname(__file__), "..", "gpurun_out"), exist_ok=True)
+    with open(os.path.join(os.path.dirname(__file__), "..", "gpurun_out", "parity_%s.json" % name), "w") as f:
+        json.dump(rep, f, indent=1)
+
+
+def _sdf_shapes():
+    rng = np.random.default_rng(5)
+    return [
+        ("sq", synth.sq((0.3, 0.2, 0.25), (0.6, 0.9))),
+        ("sq_box01", synth.sq((0.1, 0.1, 0.1), (0.1, 0.1))),
+        ("sq_eps2", synth.sq((0.2, 0.15, 0.1), (1.9, 2.0), pose=[0.05, -0.02, 0.01, *synth.random_quats(rng, 1)[0]])),
+        ("psq", synth.psq((0.3, 0.3, 0.2), (0.8, 0.5), [[0, 0, 1, -0.05], [1, 1, 0, -0.1]])),
+        ("halfspace", synth.halfspace((0.2, 0.3, 1.0), 0.05)),
+        ("blob6", synth.blob18(3, 6)),
+        ("blob18", synth.blob18(3, 18)),
+        ("cup", synth.cup()),
+        ("xpsq_vary", synth.xpsq(ctrl=[-0.1, 0, 0, 0.05, 0.12, 0.02, 0.15, -0.03, 0.05], a0=(0.05, 0.04, 0.03),
+                                 eps0=(0.5, 0.8), a1=(0.03, 0.05, 0.04), eps1=(0.9, 0.4),
+                                 planes0=[[0, 0, 1, -0.01]], planes1=[[0, 1, 1, -0.005]])),
+        ("xpsq_line", synth.xpsq(ctrl=[-0.2, 0, 0, 0.0, 0.05, 0, 0.2, 0.1, 0], a0=(0.05, 0.05, 0.05), eps0=(1, 1))),
+        ("xpsq_point", synth.xpsq(ctrl=[0.02, 0.01, 0.0] * 3, a0=(0.08, 0.05, 0.06), eps0=(0.6, 0.7),
+                                  planes0=[[0, 0, 1, -0.02]])),
+    ]
+
+
+@pytest.mark.parametrize("k", range(11))
+def test_sdf_eval_parity(cuda, oracle_mod, k):
+    """Every primitive family, all outputs (value, gradient, Hessian, pose
+    gradient, pose Hessian, mixed), random poses, points spanning inside,
+    surface band and outside; B = 7 items x P = 333 points (ragged)."""
+    from paper_2604_17538_b200 import binding
+    name, root = _sdf_shapes()[k]
+    ell = 0.04 if name == "cup" else 1.0
+    sc = scene_of([synth.make_shape(name, root)], ell=ell)
+    osc = oracle_mod.OracleScene(sc)
+    S = binding.Scene(sc.shapes, sc.smooth)
+    rng = np.random.default_rng(100 + k)
+    B, P = 7, 333
+    poses = np.stack([pose8(rng.uniform(-0.1, 0.1, 3), synth.random_quats(rng, 1)[0]) for _ in range(B)]).astype(np.float32)
+    scale = 0.1 if name == "cup" else 0.45
+    loc = rng.uniform(-scale, scale, (B, P, 3))
+    pts = np.concatenate([loc[b] @ synth.quat_to_mat(poses[b, 3:7]).T + poses[b, :3] for b in range(B)]).astype(np.float32)
+    ids = np.zeros(B, np.int32)
+    gpu = PT.gpu_sdf(S, ids, poses, pts, P, ALL)
+    nf, rep = PT.sdf_parity(osc, gpu, ids, poses, pts, P, rng, ell)
+    _report("sdf_" + name, rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+    assert PT.excluded_fraction(rep) < 0.01, rep
+    # value-only and gradient-only instantiations agree with the full one
+    g0 = PT.gpu_sdf(S, ids, poses, pts, P, 1)
+    g1 = PT.gpu_sdf(S, ids, poses, pts, P, 1 | 2)
+    assert np.allclose(g0["d"], gpu["d"], atol=1e-6 * ell) and np.allclose(g1["grad"], gpu["grad"], atol=1e-5)
+
+
+def test_sdf_eval_mixed_batch(cuda, oracle_mod):
+    """A batch mixing every shape (lean and XPSQ instantiations in one call)."""
+    from paper_2604_17538_b200 import binding
+    shapes = [synth.make_shape(n, r) for n, r in _sdf_shapes() if n != "cup"]
+    sc = scene_of(shapes)
+    osc = oracle_mod.OracleScene(sc)
+    S = binding.Scene(sc.shapes, sc.smooth)
+    rng = np.random.default_rng(7)
+    B, P = 40, 37
+    ids = rng.integers(0, len(shapes), B).astype(np.int32)
+    poses = np.stack([pose8(rng.uniform(-0.1, 0.1, 3), synth.random_quats(rng, 1)[0]) for _ in range(B)]).astype(np.float32)
+    pts = rng.uniform(-0.5, 0.5, (B * P, 3)).astype(np.float32)
+    gpu = PT.gpu_sdf(S, ids, poses, pts, P, ALL)
+    nf, rep = PT.sdf_parity(osc, gpu, ids, poses, pts, P, rng, 1.0)
+    _report("sdf_mixed", rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+
+
+def test_sdf_eval_c1(cuda, oracle_mod):
+    from paper_2604_17538_b200 import binding
+    sc = synth.c1_scene()
+    osc = oracle_mod.OracleScene(sc)
+    S = binding.Scene(sc.shapes, sc.smooth)
+    gpu = PT.gpu_sdf(S, sc.point_shapes, sc.point_poses, sc.points, sc.P, ALL)
+    nf, rep = PT.sdf_parity(osc, gpu, sc.point_shapes, sc.point_poses, sc.points, sc.P, np.random.default_rng(0), 1.0)
+    _report("sdf_c1", rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+
+
+@pytest.mark.parametrize("tier", [0, 1, 2])
+def test_manifold_c1(cuda, oracle_mod, tier):
+    sc = synth.c1_scene()
+    osc = oracle_mod.OracleScene(sc)
+    gpu, _ = PT.gpu_manifold(sc, tier)
+    nf, rep = PT.manifold_parity(sc, osc, gpu, tier, np.arange(len(sc.pairs)), np.random.default_rng(1), sc.ell)
+    _report("manifold_c1_t%d" % tier, rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+    assert PT.excluded_fraction(rep) < 0.01
+
+
+def test_manifold_c2(cuda, oracle_mod):
+    """C2 at full size (1k envs, box on box, the pathological parallel-face
+    case): every pair compared."""
+    sc = synth.c2_scene(1000)
+    osc = oracle_mod.OracleScene(sc)
+    gpu, _ = PT.gpu_manifold(sc, 2)
+    nf, rep = PT.manifold_parity(sc, osc, gpu, 2, np.arange(len(sc.pairs)), np.random.default_rng(2), sc.ell)
+    _report("manifold_c2", rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+    assert PT.excluded_fraction(rep) < 0.01
+
+
+def test_manifold_c3_sampled(cuda, oracle_mod):
+    """C3 (16x32 patch vs 18-SQ union): GPU on 2048 envs (global-scratch
+    path), oracle on a seeded sample of 24 pairs."""
+    sc = synth.c3_scene(2048)
+    osc = oracle_mod.OracleScene(sc)
+    gpu, _ = PT.gpu_manifold(sc, 2)
+    idx = np.random.default_rng(3).choice(len(sc.pairs), 24, replace=False)
+    nf, rep = PT.manifold_parity(sc, osc, gpu, 2, np.sort(idx), np.random.default_rng(4), sc.ell)
+    _report("manifold_c3", rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+    assert PT.excluded_fraction(rep) < 0.01
+
+
+def test_manifold_c4_sampled(cuda, oracle_mod):
+    """C4 (20 SQ links vs the cup with its XPSQ handle, ell = 0.04): GPU on
+    512 envs x 20 pairs, oracle on a seeded sample of 40 pairs."""
+    sc = synth.c4_scene(512)
+    osc = oracle_mod.OracleScene(sc)
+    gpu, _ = PT.gpu_manifold(sc, 2)
+    idx = np.random.default_rng(5).choice(len(sc.pairs), 40, replace=False)
+    nf, rep = PT.manifold_parity(sc, osc, gpu, 2, np.sort(idx), np.random.default_rng(6), sc.ell)
+    _report("manifold_c4", rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+    assert PT.excluded_fraction(rep) < 0.01
+
+
+def test_manifold_edge_cases(cuda, oracle_mod):
+    """Empty pair list, a single-triangle mesh, far-apart bodies (all gates
+    closed) and tier-dependent NULL outputs."""
+    import torch
+    from paper_2604_17538_b200 import binding
+    tri = synth.make_shape("tri", None, (np.array([[0, 0, 0], [0.1, 0, 0], [0, 0.1, 0]], np.float32),
+                                         np.array([[0, 1, 2]], np.int32)))
+    sph = synth.make_shape("sph", synth.sq((0.05,) * 3, (1, 1)), None)
+    poses = np.zeros((2, 2, 8), np.float32)
+    poses[:, :, 3] = 1
+    poses[1, 1, :3] = (5.0, 5.0, 5.0)
+    pairs = np.array([[0, 0, 1, 0, 1], [1, 0, 1, 0, 1]], np.int32)
+    sc = scene_of([tri, sph], pairs=pairs, poses=poses)
+    osc = oracle_mod.OracleScene(sc)
+    gpu, S = PT.gpu_manifold(sc, 2)
+    nf, rep = PT.manifold_parity(sc, osc, gpu, 2, np.arange(2), np.random.default_rng(7), 1.0)
+    assert nf == 0, rep
+    assert gpu["W"][1] < 1e-6
+    # empty batch: no launch, no error
+    out = S.contact_manifold(torch.zeros((0, 5), dtype=torch.int32, device="cuda"),
+                             torch.zeros(0, dtype=torch.int64, device="cuda"), 0,
+                             torch.from_numpy(poses).cuda(), 2)
+    torch.cuda.synchronize()
+    assert out["depth"].numel() == 0
+
+
+def test_topology_matches_oracle(cuda, oracle_mod):
+    """Library-built topology equals the oracle's (as sets: edge ids may be
+    numbered differently; face_edges must name the same vertex pairs)."""
+    from paper_2604_17538_b200 import binding
+    for sc in (synth.c1_scene(), synth.c2_scene(4)):
+        osc = oracle_mod.OracleScene(sc)
+        S = binding.Scene(sc.shapes, sc.smooth)
+        for s, sh in enumerate(sc.shapes):
+            if sh.faces is None:
+                continue
+            assert S.counts(s) == osc.mesh_counts(s)
+            e1, fe1 = S.topology(s)
+            e2, fe2 = osc.mesh_topology(s)
+            assert {tuple(x) for x in e1} == {tuple(x) for x in e2}
+            assert np.array_equal(e1[fe1], e2[fe2])
+
+
+def test_expand_jacobian(cuda, oracle_mod):
+    """cm_expand_jacobian reproduces the oracle's literal sum z_i gamma_i J_i."""
+    import torch
+    sc = synth.c1_scene()
+    osc = oracle_mod.OracleScene(sc)
+    gpu, S = PT.gpu_manifold(sc, 1)
+    pairs_t = torch.from_numpy(sc.pairs).cuda()
+    poses_t = torch.from_numpy(sc.poses).cuda()
+    offs = torch.from_numpy(gpu["offsets"]).cuda()
+    J = S.expand_jacobian(pairs_t, offs, poses_t, torch.from_numpy(gpu["W"]).cuda(),
+                          torch.from_numpy(gpu["q"]).cuda(), gpu["C"]).cpu().numpy()
+    ref = osc.contact_manifold()
+    Jr = ref["J"].reshape(-1, 36).T
+    assert np.allclose(J, Jr, atol=1e-5 * max(1.0, np.abs(Jr).max()))
