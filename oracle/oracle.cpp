@@ -811,9 +811,11 @@ int ora_contact_manifold(void* s, const int* pairs, long n_pairs, const double* 
         Wf = Wf + zg;
       }
       D12 dep = -lse(negd, 6, sp.tau_min);                 // smooth min (Reading #25)
-      // dominant candidate: argmax z_i gamma_i, lowest index on exact ties
-      int im = 0; double best = -1.0;
-      for (int i = 0; i < 6; ++i) { double v = val(z[i]) * val(gam[i]); if (v > best) { best = v; im = i; } }
+      // dominant candidate: argmax z_i gamma_i, lowest index on exact ties.
+      // z_i and gamma_i both decrease strictly with d_i, so this is argmin d_i;
+      // taken on d so it stays defined when the weights underflow (reading #32)
+      int im = 0;
+      for (int i = 1; i < 6; ++i) if (val(dd[i]) < val(dd[im])) im = i;
       // literal fused contact Jacobian J = sum z_i gamma_i J_i, J_i = [I, -[p-tA]x, -I, [p-tB]x]
       double Jc[36] = {0};
       for (int i = 0; i < 6; ++i) {

@@ -453,9 +453,12 @@ JT __device__ __forceinline__ JJ jlse2(const JJ& a, const JJ& b) {
   float d = a.v - b.v;
   float e = ex2(-fabsf(d));
   float f = fmaxf(a.v, b.v) + lg2(1.f + e);
-  // weights wa = 2^a / (2^a + 2^b)
-  float wa = d > 0.f ? rcpa(1.f + e) : e * rcpa(1.f + e);
-  float wb = 1.f - wa;
+  // weights wa = 2^a / (2^a + 2^b), wb = 1 - wa, each formed directly: the
+  // small one multiplies huge derivatives of the other operand (e.g. an SQ
+  // coordinate near its axis plane), so 1 - wa would cancel catastrophically
+  const float ir = rcpa(1.f + e);
+  const float wa = d > 0.f ? ir : e * ir;
+  const float wb = d > 0.f ? e * ir : ir;
   float c = LN2 * wa * wb;
   return jchain2(a, b, f, wa, wb, c, -c, c);
 }

@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(128) k_contact_manifold(SceneDev S, const int3
       for (int i = 0; i < 6; ++i) { z[i] = ex2((dm - dc[i]) * itlm); Z += z[i]; }
       const float iZ = 1.f / Z;
       float zg[6];
-      float Wf = 0.f, best = -1.f;
+      float Wf = 0.f;
       int dom = 0;
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
@@ -282,7 +282,9 @@ __global__ void __launch_bounds__(128) k_contact_manifold(SceneDev S, const int3
         const float gam = sigm(-dc[i] * itcmp);        // gamma = [[d < 0]]
         zg[i] = z[i] * gam;
         Wf += zg[i];
-        if (zg[i] > best) { best = zg[i]; dom = i; }
+        // dominant candidate argmax z_i gamma_i = argmin d_i (both factors
+        // decrease with d_i); taken on d so it survives weight underflow
+        if (dc[i] < dc[dom]) dom = i;
       }
       const float depth = fmaf(-tmin * LN2, lg2(Z), dm);   // smooth min (reading #25)
       float nrm[3] = {0.f, 0.f, 0.f}, qv[3] = {0.f, 0.f, 0.f}, pt[3] = {0.f, 0.f, 0.f};
