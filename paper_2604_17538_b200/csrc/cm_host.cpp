@@ -456,9 +456,10 @@ int cm_shape_topology(const cm_scene* sc, int32_t s, int32_t* edges, int32_t* fa
 int cm_sdf_eval(const cm_scene* sc, const int32_t* ids, const float* poses, const float* points, int64_t B, int64_t P,
                 uint32_t flags, float* d, float* grad, float* hess, float* dpose, float* d2pose, float* dxdpose,
                 void* stream) {
-  if (!sc || !ids || !poses || !points || !d) return fail(CM_ERR_INVALID, "cm_sdf_eval: NULL argument");
+  if (!sc) return fail(CM_ERR_INVALID, "cm_sdf_eval: NULL scene");
   if (B < 0 || P < 0) return fail(CM_ERR_INVALID, "cm_sdf_eval: negative size");
-  if (B == 0 || P == 0) return CM_OK;
+  if (B == 0 || P == 0) return CM_OK;   // empty batch: nothing to launch
+  if (!ids || !poses || !points || !d) return fail(CM_ERR_INVALID, "cm_sdf_eval: NULL argument");
   if (((uintptr_t)poses & 15) != 0) return fail(CM_ERR_INVALID, "cm_sdf_eval: poses must be 16-byte aligned");
   if ((flags & CM_SDF_GRAD) && !grad) return fail(CM_ERR_INVALID, "cm_sdf_eval: grad is NULL");
   if ((flags & CM_SDF_HESS) && !hess) return fail(CM_ERR_INVALID, "cm_sdf_eval: hess is NULL");
@@ -487,7 +488,9 @@ int64_t cm_manifold_offsets_workspace(int64_t n_pairs) { return cml::offsets_wor
 
 int cm_manifold_offsets(const cm_scene* sc, const int32_t* pairs, int64_t n_pairs, int64_t* offsets, void* ws,
                         int64_t ws_bytes, void* stream) {
-  if (!sc || !pairs || !offsets || !ws) return fail(CM_ERR_INVALID, "cm_manifold_offsets: NULL argument");
+  if (!sc) return fail(CM_ERR_INVALID, "cm_manifold_offsets: NULL scene");
+  if (n_pairs == 0) return CM_OK;
+  if (!pairs || !offsets || !ws) return fail(CM_ERR_INVALID, "cm_manifold_offsets: NULL argument");
   if (n_pairs > (int64_t)0x7fffffff) return fail(CM_ERR_UNSUPPORTED, "cm_manifold_offsets: too many pairs");
   if (ws_bytes < cml::offsets_workspace(n_pairs)) return fail(CM_ERR_INVALID, "cm_manifold_offsets: workspace too small");
   int rc = cml::launch_offsets(sc->dev, pairs, n_pairs, offsets, ws, ws_bytes, stream);
@@ -498,9 +501,10 @@ int cm_manifold_offsets(const cm_scene* sc, const int32_t* pairs, int64_t n_pair
 int cm_contact_manifold(const cm_scene* sc, const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,
                         const float* poses, int64_t n_env, int32_t n_slot, uint32_t flags, const cm_manifold_out* out,
                         int64_t n_contacts, void* stream) {
-  if (!sc || !pairs || !offsets || !poses || !out) return fail(CM_ERR_INVALID, "cm_contact_manifold: NULL argument");
+  if (!sc || !out) return fail(CM_ERR_INVALID, "cm_contact_manifold: NULL argument");
   if (n_pairs < 0 || n_env < 0 || n_slot <= 0 || n_contacts < 0) return fail(CM_ERR_INVALID, "cm_contact_manifold: sizes");
-  if (n_pairs == 0) return CM_OK;
+  if (n_pairs == 0) return CM_OK;   // empty batch: nothing to launch
+  if (!pairs || !offsets || !poses) return fail(CM_ERR_INVALID, "cm_contact_manifold: NULL argument");
   const unsigned tier = flags & CM_TIER_MASK;
   if (tier > 2) return fail(CM_ERR_INVALID, "cm_contact_manifold: tier");
   if (!out->point || !out->normal || !out->depth || !out->dom) return fail(CM_ERR_INVALID, "tier-0 outputs are NULL");
