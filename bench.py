@@ -1,0 +1,322 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: smooth one-shot contact manifolds with full
+derivatives (tier 2) for every (environment, pair) of a large batch
+(arXiv 2604.17538 §II-C; BASELINE.json metric "contact-manifold evals/sec
+with derivatives").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5]
+  python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...
+  python bench.py --impl reference ...   (the FP64 oracle on host cores)
+
+One step = one cm_contact_manifold call (tier 2) over the rank's whole env
+shard.  Weak scaling: every rank owns n_env environments (global env ids
+[rank*n_env, (rank+1)*n_env), inputs keyed by global env index), no
+collective on the data path; timing is max over ranks.  Inputs (poses,
+pairs, offsets) are resident in HBM for `value`; `e2e` re-times the same
+step through the public API with the step's poses copied host->device from
+pinned memory and the fused depths copied back every step.  L2 is flushed
+(256 MiB write) between timed steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# Executed FP32 FLOPs per pair of the dominant kernel (FFMA = 2, FADD/FMUL =
+# 1), measured once with ncu on the same workload and frozen here (DESIGN.md
+# §7): profiles/r01_ncu_summary.md.  Bytes per pair are algorithmic (inputs:
+# two poses + the pair record; outputs: F contacts x 237 B at tier 2).
+FLOP_PER_PAIR = {"C5": None, "C4": None, "C3": None, "C2": None}
+OUT_BYTES_PER_CONTACT = {0: 33, 1: 45, 2: 237}
+IN_BYTES_PER_PAIR = 2 * 32 + 20
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4 at the 1965 MHz max SM clock
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def make_scene(workload, n_env, env_lo):
+    from paper_2604_17538_b200 import synth
+    if workload == "C5":
+        return synth.c5_scene(n_env, env_lo=env_lo)
+    if workload == "C4":
+        return synth.c4_scene(n_env, seed=4 + 1000 * (env_lo // max(n_env, 1)))
+    if workload == "C3":
+        return synth.c3_scene(n_env, seed=3 + 1000 * (env_lo // max(n_env, 1)))
+    if workload == "C2":
+        return synth.c2_scene(n_env, seed=2 + 1000 * (env_lo // max(n_env, 1)))
+    raise SystemExit("unknown workload " + workload)
+
+
+DEFAULT_NENV = {"C5": 1 << 20, "C4": 1 << 16, "C3": 1 << 14, "C2": 1000}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def oracle_rate(scene, budget_s=15.0, threads=0, max_pairs=None):
+    """The FP64 oracle (as it stands) on a bounded prefix of the workload's
+    pairs on the host cores: returns (pairs/s, pairs timed, cores)."""
+    from oracle import oracle as O
+    osc = O.OracleScene(scene)
+    cores = O.max_threads() if threads == 0 else threads
+    n = min(len(scene.pairs), max(cores, 8))
+    t0 = time.perf_counter()
+    osc.contact_manifold(pairs=scene.pairs[:n], n_threads=threads)
+    dt = time.perf_counter() - t0
+    per = dt / n
+    m = int(max(n, min(len(scene.pairs), budget_s / max(per, 1e-9))))
+    if max_pairs:
+        m = min(m, max_pairs)
+    t0 = time.perf_counter()
+    osc.contact_manifold(pairs=scene.pairs[:m], n_threads=threads)
+    dt = time.perf_counter() - t0
+    return m / dt, m, cores, dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n_env = args.n_env or DEFAULT_NENV[args.workload]
+    scene = make_scene(args.workload, min(n_env, 65536), 0)
+    from oracle import oracle as O
+    osc = O.OracleScene(scene)
+    cores = O.max_threads()
+    # each step: a bounded sample of the workload's pairs (same sample size
+    # every step) sized so that W + K steps take a few minutes at most
+    n = min(len(scene.pairs), max(cores, 8))
+    t0 = time.perf_counter()
+    osc.contact_manifold(pairs=scene.pairs[:n])
+    per = (time.perf_counter() - t0) / n
+    m = int(max(n, min(len(scene.pairs), 150.0 / max(args.steps + args.warmup, 1) / max(per, 1e-9))))
+    sample = scene.pairs[:m]
+    for _ in range(args.warmup):
+        osc.contact_manifold(pairs=sample)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        osc.contact_manifold(pairs=sample)
+    dt = (time.perf_counter() - t0) / args.steps
+    val = m / dt
+    line = {"impl": "reference", "metric": "contact-manifold evals/sec with derivatives (tier 2)", "value": val,
+            "unit": "pairs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "n_env_per_gpu": n_env, "tier": 2},
+            "cpu_baseline": {"value": val, "unit": "pairs/s", "cores": cores, "kind": "oracle",
+                             "sample": "first %d pairs of %s per step (FP64 jet oracle, OpenMP over pairs)"
+                                       % (m, args.workload)},
+            "e2e": {"value": val, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C5", choices=["C5", "C4", "C3", "C2"])
+    ap.add_argument("--n-env", type=int, default=0)
+    ap.add_argument("--tier", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--flop-per-pair", type=float, default=0.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2604_17538_b200 import binding
+
+    n_env = args.n_env or DEFAULT_NENV[args.workload]
+    t0 = time.time()
+    scene = make_scene(args.workload, n_env, rank * n_env)
+    gen_s = time.time() - t0
+    S = binding.Scene(scene.shapes, scene.smooth, device=local)
+    dev = torch.device("cuda", local)
+    pairs = torch.from_numpy(scene.pairs).to(dev)
+    poses = torch.from_numpy(scene.poses).to(dev)
+    offs = S.manifold_offsets(pairs)
+    C = S.manifold_size(scene.pairs)
+    out = S.alloc_manifold(C, args.tier, dev)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)   # 256 MiB > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step():
+        S.contact_manifold(pairs, offs, C, poses, args.tier, out)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = binding.launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    launches = binding.launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    times = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(np.sum(times))
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    n_pairs_all = len(scene.pairs) * world
+    value = n_pairs_all / (ms_per_step / 1e3)
+
+    # ---- end to end through the public API with host buffers --------------
+    e2e = None
+    if not args.no_e2e:
+        poses_h = torch.from_numpy(scene.poses).pin_memory()
+        depth_h = torch.empty(C, dtype=torch.float32).pin_memory()
+        poses_d = torch.empty_like(poses)
+        for _ in range(2):
+            poses_d.copy_(poses_h, non_blocking=True)
+            o = S.contact_manifold(pairs, offs, C, poses_d, args.tier, out)
+            depth_h.copy_(o["depth"], non_blocking=True)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(args.steps):
+            poses_d.copy_(poses_h, non_blocking=True)
+            o = S.contact_manifold(pairs, offs, C, poses_d, args.tier, out)
+            depth_h.copy_(o["depth"], non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": n_pairs_all / (float(te.item()) / 1e3), "unit": "pairs/s",
+               "h2d_bytes_per_step": int(poses_h.numel() * 4), "d2h_bytes_per_step": int(C * 4)}
+
+    # ---- roofline of the dominant kernel (k_contact_manifold) -------------
+    peaks, peak_src = load_peaks()
+    n_pairs = len(scene.pairs)
+    bytes_alg = n_pairs * IN_BYTES_PER_PAIR + C * OUT_BYTES_PER_CONTACT[args.tier]
+    # the step is exactly the k_contact_manifold launch(es) of one call (one
+    # lean + one XPSQ instantiation for scenes mixing both SDF classes)
+    kern_s = ms_per_step / 1e3
+    hbm_gbs = bytes_alg / kern_s / 1e9
+    fpp = args.flop_per_pair or FLOP_PER_PAIR.get(args.workload)
+    if fpp:
+        achieved = fpp * n_pairs / kern_s / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP32_PEAK_TFLOPS, "traffic": None,
+                "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
+                "flop_per_pair": fpp, "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks["hbm_gbs"],
+                                              "frac": hbm_gbs / peaks["hbm_gbs"], "peak_source": peak_src}}
+    else:
+        roof = {"bound": "hbm", "achieved": hbm_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": hbm_gbs / peaks["hbm_gbs"], "traffic": None, "peak_source": peak_src,
+                "note": "FLOP/pair not yet frozen; HBM fraction of algorithmic bytes only"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, m, cores, dt = oracle_rate(scene, budget_s=15.0)
+        cpu = {"value": rate, "unit": "pairs/s", "cores": cores, "kind": "oracle",
+               "sample": "first %d pairs of the %s shard, FP64 jet oracle, OpenMP over pairs, %.1f s" % (m, args.workload, dt)}
+
+    if rank == 0:
+        line = {"metric": "contact-manifold evals/sec with derivatives (tier 2)", "value": value, "unit": "pairs/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic",
+                "config": {"workload": args.workload, "n_env_per_gpu": n_env, "pairs_per_gpu": n_pairs,
+                           "contacts_per_gpu": C, "tier": args.tier, "l2": "flushed (256 MiB write) between steps",
+                           "parallelism": "env-sharded dp%d, no data-path collective" % world,
+                           "input_gen_s": round(gen_s, 1)},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -241,6 +241,16 @@ def quat_to_mat(q):
                      [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
 
 
+def quats_to_mats(q):
+    """Vectorised quat_to_mat over [n, 4] (w, x, y, z)."""
+    q = np.asarray(q, dtype=np.float64)
+    q = q / np.linalg.norm(q, axis=1, keepdims=True)
+    w, x, y, z = q[:, 0], q[:, 1], q[:, 2], q[:, 3]
+    return np.stack([np.stack([1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)], -1),
+                     np.stack([2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)], -1),
+                     np.stack([2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)], -1)], 1)
+
+
 def random_quats(rng, n):
     """Uniform on SO(3) (normalised 4-D Gaussian; equivalent to the subgroup
     algorithm of)."""
@@ -445,3 +455,199 @@ def c4_scene(n_env: int = 65536, seed: int = 4, n_links: int = 20) -> Scene:
 
 def random_points(rng, n, lo, hi):
     return rng.uniform(lo, hi, (n, 3)).astype(F32)
+
+
+# ---------------------------------------------------------------------------
+# C5: mixed sampled kinds x 32 SDF prototypes
+# ---------------------------------------------------------------------------
+def psq_mesh(a, eps, planes, k: int):
+    """Cube-sphere SQ mesh whose vertices outside a half-space are pulled
+    radially (towards the centre, which is inside every plane) onto the
+    plane: an input surface for the PSQ (star-shaped about its centre)."""
+    v, f = sq_mesh(a, eps, k)
+    v = v.astype(np.float64)
+    for pl in planes:
+        n = np.asarray(pl[:3], dtype=np.float64)
+        n = n / np.linalg.norm(n)
+        h = float(pl[3])
+        s = v @ n
+        out = s + h > 0
+        v[out] *= (-h / s[out])[:, None]
+    return v.astype(F32), f
+
+
+def xpsq_mesh(ctrl, a, eps2, nt: int, nth: int):
+    """Tube around the quadratic spline: nt rings of nth points on the
+    cross-section superellipse (a_y, a_z, exponent eps2) in the Frenet frame,
+    plus the two end-cap centres: V = nt nth + 2."""
+    c = np.asarray(ctrl, dtype=np.float64).reshape(3, 3)
+    A, B = c[0] - 2 * c[1] + c[2], 2 * (c[1] - c[0])
+    b = np.cross(B, A)
+    b = b / np.linalg.norm(b)
+    ts = np.linspace(0.0, 1.0, nt)
+    th = np.linspace(0.0, 2 * math.pi, nth, endpoint=False)
+    verts = []
+    for t in ts:
+        p = c[0] + B * t + A * t * t
+        T = B + 2 * A * t
+        T = T / np.linalg.norm(T)
+        N = np.cross(b, T)
+        for w in th:
+            verts.append(p + a[1] * _spow(math.cos(w), eps2) * N + a[2] * _spow(math.sin(w), eps2) * b)
+    verts.append(c[0] - a[0] * (B / np.linalg.norm(B)))
+    pe = c[0] + B + A
+    Te = (B + 2 * A) / np.linalg.norm(B + 2 * A)
+    verts.append(pe + a[0] * Te)
+    V = len(verts)
+    faces = []
+    for i in range(nt - 1):
+        for j in range(nth):
+            a0, a1 = i * nth + j, i * nth + (j + 1) % nth
+            b0, b1 = a0 + nth, a1 + nth
+            faces += [[a0, b0, b1], [a0, b1, a1]]
+    for j in range(nth):
+        faces.append([V - 2, (j + 1) % nth, j])
+        o = (nt - 1) * nth
+        faces.append([V - 1, o + j, o + (j + 1) % nth])
+    return np.asarray(verts, dtype=F32), np.asarray(faces, dtype=np.int32)
+
+
+def _fib_dirs(n=256):
+    i = np.arange(n) + 0.5
+    phi = np.arccos(1 - 2 * i / n)
+    th = math.pi * (1 + 5 ** 0.5) * i
+    return np.stack([np.cos(th) * np.sin(phi), np.sin(th) * np.sin(phi), np.cos(phi)], 1)
+
+
+def _support_table(points, dirs):
+    return (dirs @ np.asarray(points, dtype=np.float64).T).max(axis=1)
+
+
+def c5_library(seed: int = 5):
+    """16 sampled prototypes (spheres, MESH boxes, SQs, PSQs, curved XPSQs;
+    k = 3 or 4: V = 56 or 98) and 32 SDF prototypes (4 spheres, 4 boxes, 8
+    SQs, 6 PSQs, 6 curved XPSQs, 2 cups, 2 four-SQ blobs); lengths ~0.1."""
+    rng = np.random.Generator(np.random.Philox(key=seed + 2000))
+    sampled, sdf = [], []
+    for i in range(16):
+        kind = ["sphere", "box", "sq", "psq", "xpsq"][i % 5]
+        k = 3 if i % 2 == 0 else 4
+        if kind == "sphere":
+            r = float(rng.uniform(0.03, 0.06))
+            sampled.append(make_shape("s_sph%d" % i, None, sq_mesh((r, r, r), (1, 1), k)))
+        elif kind == "box":
+            h = rng.uniform(0.03, 0.06, 3)
+            sampled.append(make_shape("s_box%d" % i, None, box_mesh(h, k)))
+        elif kind == "sq":
+            a, e = rng.uniform(0.03, 0.07, 3), rng.uniform(0.3, 1.5, 2)
+            sampled.append(make_shape("s_sq%d" % i, None, sq_mesh(a, e, k)))
+        elif kind == "psq":
+            a, e = rng.uniform(0.04, 0.07, 3), rng.uniform(0.4, 1.2, 2)
+            pls = [[*rng.normal(size=3), -float(rng.uniform(0.01, 0.03))] for _ in range(int(rng.integers(1, 5)))]
+            sampled.append(make_shape("s_psq%d" % i, None, psq_mesh(a, e, pls, k)))
+        else:
+            ctrl = [-0.05, 0, 0, 0.0, 0.06, 0.0, 0.05, 0, 0.01]
+            a = (0.015, 0.02, 0.015)
+            nt, nth = (9, 6) if k == 3 else (12, 8)
+            sampled.append(make_shape("s_xpsq%d" % i, None, xpsq_mesh(ctrl, a, 0.5, nt, nth)))
+    for i in range(4):
+        r = float(rng.uniform(0.03, 0.07))
+        sdf.append(make_shape("sph%d" % i, sq((r, r, r), (1, 1))))
+    for i in range(4):
+        sdf.append(make_shape("box%d" % i, sq(rng.uniform(0.03, 0.07, 3), (0.1, 0.1))))
+    for i in range(8):
+        sdf.append(make_shape("sq%d" % i, sq(rng.uniform(0.03, 0.07, 3), rng.uniform(0.2, 1.8, 2))))
+    for i in range(6):
+        pls = [[*rng.normal(size=3), -float(rng.uniform(0.01, 0.03))] for _ in range(int(rng.integers(1, 5)))]
+        sdf.append(make_shape("psq%d" % i, psq(rng.uniform(0.04, 0.07, 3), rng.uniform(0.3, 1.5, 2), pls)))
+    for i in range(6):
+        p1 = rng.uniform(-0.06, -0.03, 3) * [1, 0.3, 0.3]
+        p3 = rng.uniform(0.03, 0.06, 3) * [1, 0.3, 0.3]
+        p2 = 0.5 * (p1 + p3) + rng.uniform(0.03, 0.06) * np.array([0, 1, 0.2])
+        sdf.append(make_shape("xpsq%d" % i, xpsq(np.concatenate([p1, p2, p3]), rng.uniform(0.01, 0.02, 3),
+                                                  rng.uniform(0.3, 1.0, 2))))
+    for i in range(2):
+        sdf.append(make_shape("cup%d" % i, cup()))
+    for i in range(2):
+        r2 = np.random.Generator(np.random.Philox(key=seed + 3000 + i))
+        kids = [sq(r2.uniform(0.015, 0.035, 3), r2.uniform(0.3, 1.5, 2),
+                   pose=[*r2.uniform(-0.04, 0.04, 3), *random_quats(r2, 1)[0]]) for _ in range(4)]
+        sdf.append(make_shape("blob4_%d" % i, op("union", kids)))
+    return sampled, sdf
+
+
+def _sdf_surface_samples(shape: Shape):
+    # dense samples of the SDF prototype's constituents, for placement only
+    root_nodes = shape.sdf
+    pts = []
+
+    def rec(k, R, t):
+        n = root_nodes[k]
+        Rc = R @ quat_to_mat(n["pose"][3:7])
+        tc = R @ np.asarray(n["pose"][:3]) + t
+        if n["type"] in ("sq", "psq"):
+            v, _ = sq_mesh(n["a"][0], n["eps"][0], 6)
+            pts.append(v.astype(np.float64) @ Rc.T + tc)
+        elif n["type"] == "xpsq":
+            v, _ = xpsq_mesh(n["ctrl"], n["a"][0], 0.5, 16, 8)
+            pts.append(v.astype(np.float64) @ Rc.T + tc)
+        for c in n["children"]:
+            rec(c, Rc, tc)
+
+    rec(0, np.eye(3), np.zeros(3))
+    return np.concatenate(pts)
+
+
+C5_BLOCK = 65536
+
+
+def c5_scene(n_env: int = 1 << 20, env_lo: int = 0, seed: int = 5) -> Scene:
+    """C5: one pair per env, uniform over (16 sampled x 32 SDF prototypes);
+    B at the origin with a uniform rotation, A on a random direction with a
+    support-gap clearance U[-0.025, 0.005] (about half the pairs have a
+    penetrating candidate);
+    ell = 0.1.  Envs [env_lo, env_lo + n_env) of a global sequence whose
+    random numbers are drawn per block of 65536 envs keyed by (seed, block),
+    so any rank can generate its own shard."""
+    sampled, sdf = c5_library(seed)
+    shapes = sampled + sdf
+    dirs = _fib_dirs(512)
+    supA = np.stack([_support_table(s.vertices, dirs) for s in sampled])
+    supB = np.stack([_support_table(_sdf_surface_samples(s), dirs) for s in sdf])
+    n_s = len(sampled)
+    poses = np.zeros((n_env, 2, 8))
+    pairs = np.zeros((n_env, 5), np.int32)
+    e = env_lo
+    while e < env_lo + n_env:
+        blk = e // C5_BLOCK
+        lo, hi = blk * C5_BLOCK, (blk + 1) * C5_BLOCK
+        rng = np.random.Generator(np.random.Philox(key=[seed, blk]))
+        ia = rng.integers(0, n_s, C5_BLOCK)
+        ib = rng.integers(0, len(sdf), C5_BLOCK)
+        qa = random_quats(rng, C5_BLOCK)
+        qb = random_quats(rng, C5_BLOCK)
+        u = rng.standard_normal((C5_BLOCK, 3))
+        u /= np.linalg.norm(u, axis=1, keepdims=True)
+        clr = rng.uniform(-0.025, 0.005, C5_BLOCK)
+        s, t = max(e, lo), min(env_lo + n_env, hi)
+        sl = slice(s - lo, t - lo)
+        # support of B along u (B rotated by qb) and of A along -u (A rotated by qa)
+        Rb = quats_to_mats(qb[sl])
+        Ra = quats_to_mats(qa[sl])
+        ub = np.einsum("nji,nj->ni", Rb, u[sl])
+        ua = np.einsum("nji,nj->ni", Ra, -u[sl])
+        hb = supB[ib[sl], np.argmax(ub @ dirs.T, axis=1)]
+        ha = supA[ia[sl], np.argmax(ua @ dirs.T, axis=1)]
+        dist = ha + hb + clr[sl]
+        o = slice(s - env_lo, t - env_lo)
+        poses[o, 0, :3] = u[sl] * dist[:, None]
+        poses[o, 0, 3:7] = qa[sl]
+        poses[o, 1, 3:7] = qb[sl]
+        pairs[o, 0] = np.arange(s - env_lo, t - env_lo)
+        pairs[o, 1] = 0
+        pairs[o, 2] = 1
+        pairs[o, 3] = ia[sl]
+        pairs[o, 4] = n_s + ib[sl]
+        e = t
+    return Scene("C5", shapes, smooth_params(0.1), pairs, poses.astype(F32), ell=0.1,
+                 meta=dict(env_lo=env_lo, n_sampled=n_s, n_sdf=len(sdf)))
