@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libxpsqcm.so")
+LIB_PATH = os.environ.get("XPSQCM_LIB") or os.path.join(HERE, "libxpsqcm.so")   # override: build experiments
 
 CM_MAX_PLANES = 8
 CM_MAX_CHILDREN = 32

@@ -29,7 +29,10 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), lib=None, build_dir=None) -> str:
+    global BUILD
+    lib = lib or LIB
+    BUILD = build_dir or os.path.join(HERE, "_build")
     os.makedirs(BUILD, exist_ok=True)
     deps = _deps()
     objs = []
@@ -38,7 +41,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
         objs.append(obj)
         if force or _stale(obj, deps):
-            cmd = [NVCC, *ARCH, *COMMON, "-c", os.path.join(CSRC, src), "-o", obj]
+            cmd = [NVCC, *ARCH, *COMMON, *["-D" + d for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
             if src.endswith(".cu"):
                 cmd += ["-Xptxas", "-v"] if verbose else []
             jobs.append(cmd)
@@ -54,9 +57,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         for l in logs:
             sys.stderr.write(l)
-    if force or jobs or _stale(LIB, objs):
-        run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs])
-    return LIB
+    if force or jobs or _stale(lib, objs):
+        run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib, *objs])
+    return lib
 
 
 if __name__ == "__main__":

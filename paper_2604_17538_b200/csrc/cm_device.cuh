@@ -172,7 +172,7 @@ template <int O> __device__ __forceinline__ void acc_final(const Acc<O>& a, floa
 //   + delta_ij w_i (2 p2 s_i^2 + c_i)], F2_22 = 2 p1 gamma (2 p1 s2^2 + c2);
 // grad phi = (1-h) yh + k r h L;
 // hess phi = (1-h)(I - yh yh^T)/r + k h (yh L^T + L yh^T) + k r h (F2 - (1+k) L L^T)
-template <int O> __device__ __forceinline__ void sq_eval(const Leaf& Lf, const float* y, Res<O>& r) {
+template <int O, class SP> __device__ __forceinline__ void sq_eval(const SP& Lf, const float* y, Res<O>& r) {
   const float ia0 = Lf.ia[0], ia1 = Lf.ia[1], ia2 = Lf.ia[2];
   const float p1 = Lf.p1, p2 = Lf.p2, m = Lf.m, k = Lf.k;
   float u0 = y[0] * ia0, u1 = y[1] * ia1, u2 = y[2] * ia2;
@@ -659,8 +659,196 @@ template <int O> __device__ void xpsq_eval(const Xpsq& X, const SmoothDev& sp, c
   }
 }
 
+// ---- XPSQ, analytic fast path (constant schedules) ---------------------------
+// phi_k(x) = psi(y_k(x, t_k(x))) with y = R(t)^T (x - p(t));
+// psi = PSQ at the root's pose, t_k from soft Cardano (2-variable jets
+// in (P, Q), chained to x).  With G = grad_y psi, H = hess_y psi, y_t = dy/dt:
+//   grad phi = R G + (G . y_t) grad t
+//   hess phi = M^T H M + (R'G) grad t^T + grad t (R'G)^T
+//              + (G . y_tt) grad t grad t^T + (G . y_t) hess t,
+//   M_i = R_col_i + (y_t)_i grad t,
+//   y_t  = (T'.d - T.p', N'.d - N.p', -b.p'),  d = x - p(t),
+//   y_tt = (T''.d - 2T'.p' - T.p'', N''.d - 2N'.p' - N.p'', -b.p''),
+// Frenet frame of the quadratic (constant binormal b):
+//   T' = (p'' - T (T.p''))/|p'|,  T'' = (-2 T' (T.p'') - T (T'.p''))/|p'|,
+//   N = b x T, N' = b x T', N'' = b x T''.
+struct XsqParams {
+  float ia[3];
+  float p1, p2, m, k;
+};
+
+template <int O>
+__device__ __forceinline__ void xpsq_root_t(const Xpsq& X, const SmoothDev& sp, const float* w, float* tv, float (*tg)[3],
+                                            float (*th)[6]) {
+  const float tc = sp.tau_clip_t, itc = 1.f / tc;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    tv[k] = 0.5f;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) tg[k][i] = 0.f;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) th[k][q] = 0.f;
+  }
+  if (X.cls == 1) {
+    const float s = X.Bn[0] * w[0] + X.Bn[1] * w[1] + X.Bn[2] * w[2];
+    const float v = softclip(s, 0.f, 1.f, tc, itc);
+    const float s1 = sigm(s * itc), s2 = sigm((s - 1.f) * itc);
+    const float d1 = s1 - s2, d2 = (s1 * (1.f - s1) - s2 * (1.f - s2)) * itc;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      tv[k] = v;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) tg[k][i] = d1 * X.Bn[i];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) th[k][q] = d2 * X.Bn[jhi<3>(q)] * X.Bn[jhj<3>(q)];
+    }
+  } else if (X.cls == 2) {
+    const float Pv = X.gP[0] * w[0] + X.gP[1] * w[1] + X.gP[2] * w[2] + X.P0;
+    const float Qv = X.gQ[0] * w[0] + X.gQ[1] * w[1] + X.gQ[2] * w[2] + X.Q0;
+    constexpr int OC = O;
+    J2<OC> t2[3];
+    soft_cardano<OC>(jvar<2, OC>(Pv, 0), jvar<2, OC>(Qv, 1), X.b3, sp, t2);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      tv[k] = t2[k].v;
+      if constexpr (O >= 1) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) tg[k][i] = fmaf(t2[k].g[0], X.gP[i], t2[k].g[1] * X.gQ[i]);
+      }
+      if constexpr (O >= 2) {
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+          const int i = jhi<3>(q), j = jhj<3>(q);
+          float v = t2[k].h[0] * X.gP[i] * X.gP[j];
+          v = fmaf(t2[k].h[1], fmaf(X.gP[i], X.gQ[j], X.gQ[i] * X.gP[j]), v);
+          th[k][q] = fmaf(t2[k].h[2], X.gQ[i] * X.gQ[j], v);
+        }
+      }
+    }
+  }
+}
+
+template <int O> __device__ void xpsq_eval_fast(const Xpsq& X, const SmoothDev& sp, const float* y, Res<O>& out) {
+  const float tau = sp.tau_min, itau = 1.f / tau, itl = LOG2E * itau;
+  const float w[3] = {y[0] - X.p1[0], y[1] - X.p1[1], y[2] - X.p1[2]};
+  float tv[3], tg[3][3], th[3][6];
+  xpsq_root_t<O>(X, sp, w, tv, tg, th);
+  XsqParams sq;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) sq.ia[i] = 1.f / X.a0[i];
+  sq.p1 = 1.f / X.eps0[0];
+  sq.p2 = 1.f / X.eps0[1];
+  sq.m = X.eps0[1] * sq.p1;
+  sq.k = 0.5f * X.eps0[0];
+  const float* b = X.frenet ? X.bhat : nullptr;
+  Acc<O> acc;
+  acc_init(acc);
+#pragma unroll 1
+  for (int k = 0; k < 3; ++k) {
+    const float t = tv[k];
+    float pd[3], d[3], T[3], N[3], bb[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      pd[i] = fmaf(2.f * X.A[i], t, X.B[i]);
+      d[i] = y[i] - fmaf(fmaf(X.A[i], t, X.B[i]), t, X.p1[i]);
+    }
+    float Tp[3] = {0.f, 0.f, 0.f}, Np[3] = {0.f, 0.f, 0.f}, Tpp[3] = {0.f, 0.f, 0.f}, Npp[3] = {0.f, 0.f, 0.f};
+    if (b) {
+      const float in = rsqrtf(pd[0] * pd[0] + pd[1] * pd[1] + pd[2] * pd[2]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) { T[i] = pd[i] * in; bb[i] = b[i]; }
+      N[0] = bb[1] * T[2] - bb[2] * T[1]; N[1] = bb[2] * T[0] - bb[0] * T[2]; N[2] = bb[0] * T[1] - bb[1] * T[0];
+      if constexpr (O >= 1) {
+        const float pdd[3] = {2.f * X.A[0], 2.f * X.A[1], 2.f * X.A[2]};
+        const float tp = T[0] * pdd[0] + T[1] * pdd[1] + T[2] * pdd[2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) Tp[i] = (pdd[i] - T[i] * tp) * in;
+        Np[0] = bb[1] * Tp[2] - bb[2] * Tp[1]; Np[1] = bb[2] * Tp[0] - bb[0] * Tp[2]; Np[2] = bb[0] * Tp[1] - bb[1] * Tp[0];
+        if constexpr (O >= 2) {
+          const float tpp = Tp[0] * pdd[0] + Tp[1] * pdd[1] + Tp[2] * pdd[2];
+#pragma unroll
+          for (int i = 0; i < 3; ++i) Tpp[i] = (-2.f * Tp[i] * tp - T[i] * tpp) * in;
+          Npp[0] = bb[1] * Tpp[2] - bb[2] * Tpp[1]; Npp[1] = bb[2] * Tpp[0] - bb[0] * Tpp[2];
+          Npp[2] = bb[0] * Tpp[1] - bb[1] * Tpp[0];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) { T[i] = X.R0[i * 3 + 0]; N[i] = X.R0[i * 3 + 1]; bb[i] = X.R0[i * 3 + 2]; }
+    }
+    const float yk[3] = {T[0] * d[0] + T[1] * d[1] + T[2] * d[2], N[0] * d[0] + N[1] * d[1] + N[2] * d[2],
+                         bb[0] * d[0] + bb[1] * d[1] + bb[2] * d[2]};
+    // PSQ at the root: SQ intersected with the cross-section planes
+    Res<O> r;
+    sq_eval<O>(sq, yk, r);
+    if (X.n_planes > 0) {
+      Acc<O> a;
+      acc_init(a);
+      acc_fold(a, 1.f, r, itl, itau);
+      for (int j = 0; j < X.n_planes; ++j) {
+        Res<O> pr;
+        plane_eval<O>(X.pl0[j], yk, pr);
+        acc_fold(a, 1.f, pr, itl, itau);
+      }
+      acc_final(a, 1.f, tau, itau, r);
+    }
+    Res<O> rk;
+    rk.v = r.v;
+    if constexpr (O >= 1) {
+      const float* G = r.g;
+      // y_t, s = G . y_t
+      const float yt[3] = {(Tp[0] * d[0] + Tp[1] * d[1] + Tp[2] * d[2]) - (T[0] * pd[0] + T[1] * pd[1] + T[2] * pd[2]),
+                           (Np[0] * d[0] + Np[1] * d[1] + Np[2] * d[2]) - (N[0] * pd[0] + N[1] * pd[1] + N[2] * pd[2]),
+                           -(bb[0] * pd[0] + bb[1] * pd[1] + bb[2] * pd[2])};
+      const float s = G[0] * yt[0] + G[1] * yt[1] + G[2] * yt[2];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) rk.g[a] = fmaf(s, tg[k][a], T[a] * G[0] + N[a] * G[1] + bb[a] * G[2]);
+      if constexpr (O >= 2) {
+        const float pdd[3] = {2.f * X.A[0], 2.f * X.A[1], 2.f * X.A[2]};
+        const float ytt[3] = {(Tpp[0] * d[0] + Tpp[1] * d[1] + Tpp[2] * d[2]) -
+                                  2.f * (Tp[0] * pd[0] + Tp[1] * pd[1] + Tp[2] * pd[2]) -
+                                  (T[0] * pdd[0] + T[1] * pdd[1] + T[2] * pdd[2]),
+                              (Npp[0] * d[0] + Npp[1] * d[1] + Npp[2] * d[2]) -
+                                  2.f * (Np[0] * pd[0] + Np[1] * pd[1] + Np[2] * pd[2]) -
+                                  (N[0] * pdd[0] + N[1] * pdd[1] + N[2] * pdd[2]),
+                              -(bb[0] * pdd[0] + bb[1] * pdd[1] + bb[2] * pdd[2])};
+        const float sg = G[0] * ytt[0] + G[1] * ytt[1] + G[2] * ytt[2];
+        float RpG[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) RpG[a] = Tp[a] * G[0] + Np[a] * G[1];
+        // M_i = col_i + yt_i grad t
+        float M[3][3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          M[0][a] = fmaf(yt[0], tg[k][a], T[a]);
+          M[1][a] = fmaf(yt[1], tg[k][a], N[a]);
+          M[2][a] = fmaf(yt[2], tg[k][a], bb[a]);
+        }
+        const float Hm[3][3] = {{r.h[0], r.h[1], r.h[2]}, {r.h[1], r.h[3], r.h[4]}, {r.h[2], r.h[4], r.h[5]}};
+        float HM[3][3];   // HM[i][b] = sum_j H_ij M_j,b
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) HM[i][c] = Hm[i][0] * M[0][c] + Hm[i][1] * M[1][c] + Hm[i][2] * M[2][c];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+          const int a = jhi<3>(q), c = jhj<3>(q);
+          float v = M[0][a] * HM[0][c] + M[1][a] * HM[1][c] + M[2][a] * HM[2][c];
+          v = fmaf(RpG[a], tg[k][c], fmaf(RpG[c], tg[k][a], v));
+          v = fmaf(sg * tg[k][a], tg[k][c], v);
+          rk.h[q] = fmaf(s, th[k][q], v);
+        }
+      }
+    }
+    acc_fold(acc, -1.f, rk, itl, itau);   // smooth minimum over the roots
+  }
+  acc_final(acc, -1.f, tau, itau, out);
+}
+
 // ---- leaf dispatch ---------------------------------------------------------
-template <int O, bool XP>
+// XP: 0 no XPSQ leaves, 1 constant-schedule XPSQ (analytic fast path),
+// 2 any XPSQ (jets when the schedules vary along t)
+template <int O, int XP>
 __device__ __forceinline__ void leaf_eval(const SceneDev& S, int li, const float* x, Res<O>& r) {
   const Leaf& L = S.leaves[li];
   float y[3];
@@ -692,8 +880,14 @@ __device__ __forceinline__ void leaf_eval(const SceneDev& S, int li, const float
       }
       acc_final(a, 1.f, tau, itau, l);
     }
-  } else if (XP && kind == LK_XPSQ) {
-    xpsq_eval<O>(S.xpsq[L.xidx], S.sp, y, l);
+  } else if (XP > 0 && kind == LK_XPSQ) {
+    const Xpsq& X = S.xpsq[L.xidx];
+    if constexpr (XP == 2) {
+      if (X.varying) xpsq_eval<O>(X, S.sp, y, l);   // schedules vary along t: jets
+      else xpsq_eval_fast<O>(X, S.sp, y, l);
+    } else {
+      xpsq_eval_fast<O>(X, S.sp, y, l);
+    }
   } else {
     plane_eval<O>(L.planes[0], y, l);
   }
@@ -726,7 +920,7 @@ __device__ __forceinline__ void fold_level(Acc<O>& a0, Acc<O>& a1, Acc<O>& a2, i
 }
 
 // phi, grad, hess of shape `sh` at the body-frame point x
-template <int O, bool XP> __device__ void eval_shape(const SceneDev& S, const ShapeRec& sh, const float* x, Res<O>& out) {
+template <int O, int XP> __device__ void eval_shape(const SceneDev& S, const ShapeRec& sh, const float* x, Res<O>& out) {
   const float tau = S.sp.tau_min, itau = 1.f / tau, itl = LOG2E * itau;
   if (sh.prog_len == 1) {  // single leaf: no accumulator needed
     leaf_eval<O, XP>(S, S.prog[sh.prog_begin].idx, x, out);

@@ -185,7 +185,7 @@ struct cm_scene {
   std::vector<ShapeRec> shapes;
   std::vector<std::vector<int32_t>> edges, face_edges;
   int max_V = 0, max_E = 0, max_F = 0;
-  int xp_class = 0;  // 0 no XPSQ shape, 1 every SDF shape uses XPSQ, 2 mixed
+  int class_mask = 0;  // bit c: SDF shapes of class c (0 SQ family, 1 XPSQ, 2 varying-schedule XPSQ)
   std::vector<void*> allocs;
   float* scratch = nullptr;
   int64_t scratch_floats = 0;
@@ -215,7 +215,6 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
   sc->device = device;
   sc->edges.resize(n_shapes);
   sc->face_edges.resize(n_shapes);
-  int n_sdf = 0, n_xp = 0;
 
   for (int s = 0; s < n_shapes; ++s) {
     const cm_shape_desc& d = shapes[s];
@@ -272,7 +271,7 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
         }
       }
       // flatten: depth-first emission with composed frames
-      bool uses_x = false;
+      int xclass = 0;
       int max_depth = 0;
       struct Item { int node; float child_sign; Frame parent; int depth; };
       std::string err;
@@ -300,7 +299,7 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
             L.n_planes = 0;
             L.xidx = (int32_t)xps.size();
             xps.push_back(pack_xpsq(n));
-            uses_x = true;
+            xclass = std::max(xclass, xps.back().varying ? 2 : 1);
           } else {
             L.kind = LK_SQ;
             double e1 = n.eps[0][0], e2 = n.eps[0][1];
@@ -332,9 +331,8 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
       id.t[0] = id.t[1] = id.t[2] = 0.0;
       if (!emit(0, 1.f, id, 0)) { delete sc; return fail(CM_ERR_UNSUPPORTED, "shape " + std::to_string(s) + ": " + err); }
       r.has_sdf = 1;
-      r.uses_xpsq = uses_x ? 1 : 0;
-      ++n_sdf;
-      n_xp += uses_x ? 1 : 0;
+      r.uses_xpsq = xclass;
+      sc->class_mask |= 1 << xclass;
     }
     r.prog_len = (int32_t)prog.size() - r.prog_begin;
 
@@ -392,7 +390,6 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
     }
   }
   sc->shapes = recs;
-  sc->xp_class = n_xp == 0 ? 0 : (n_xp == n_sdf ? 1 : 2);
 
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) { delete sc; return fail(CM_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)); }
@@ -465,7 +462,7 @@ int cm_sdf_eval(const cm_scene* sc, const int32_t* ids, const float* poses, cons
   if ((flags & CM_SDF_HESS) && !hess) return fail(CM_ERR_INVALID, "cm_sdf_eval: hess is NULL");
   if ((flags & CM_SDF_POSE_GRAD) && !dpose) return fail(CM_ERR_INVALID, "cm_sdf_eval: dpose is NULL");
   if ((flags & CM_SDF_POSE_HESS) && (!d2pose || !dxdpose)) return fail(CM_ERR_INVALID, "cm_sdf_eval: d2pose/dxdpose NULL");
-  int rc = cml::launch_sdf_eval(sc->dev, sc->xp_class != 0, ids, poses, points, B, P, flags, d,
+  int rc = cml::launch_sdf_eval(sc->dev, sc->class_mask, ids, poses, points, B, P, flags, d,
                                 (flags & CM_SDF_GRAD) ? grad : nullptr, (flags & CM_SDF_HESS) ? hess : nullptr, dpose,
                                 d2pose, dxdpose, stream);
   if (rc) return fail(rc, cml::last_cuda_error());
@@ -511,7 +508,7 @@ int cm_contact_manifold(const cm_scene* sc, const int32_t* pairs, int64_t n_pair
   if (tier >= 1 && (!out->W || !out->q)) return fail(CM_ERR_INVALID, "tier-1 outputs are NULL");
   if (tier >= 2 && (!out->ddepth || !out->dnormal)) return fail(CM_ERR_INVALID, "tier-2 outputs are NULL");
   if (sc->max_F == 0) return fail(CM_ERR_INVALID, "scene has no sampled surface");
-  int rc = cml::launch_manifold(sc->dev, sc->xp_class, sc->max_V, sc->max_E, pairs, n_pairs, offsets, poses, n_slot,
+  int rc = cml::launch_manifold(sc->dev, sc->class_mask, sc->max_V, sc->max_E, pairs, n_pairs, offsets, poses, n_slot,
                                 flags, out, n_contacts, sc->scratch, sc->scratch_floats, stream);
   if (rc) return fail(rc, cml::last_cuda_error());
   return CM_OK;

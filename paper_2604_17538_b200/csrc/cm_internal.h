@@ -60,7 +60,7 @@ struct Xpsq {
 
 struct ShapeRec {
   int32_t prog_begin, prog_len;
-  int32_t has_sdf, uses_xpsq;
+  int32_t has_sdf, uses_xpsq;   // uses_xpsq: SDF class 0 / 1 / 2 (see cm_device.cuh leaf_eval)
   int32_t V, E, F;
   int32_t v_off, e_off, f_off;   // into verts (x3), edges (x2), faces / face_edges (x3)
   int32_t pad;
@@ -93,10 +93,10 @@ constexpr int64_t kSmemBudget = 110 * 1024;
 
 // launchers implemented in cm_kernels.cu
 namespace cml {
-int launch_sdf_eval(const cmi::SceneDev& s, bool xp_class, const int32_t* shape_ids, const float* poses,
+int launch_sdf_eval(const cmi::SceneDev& s, int class_mask, const int32_t* shape_ids, const float* poses,
                     const float* points, int64_t B, int64_t P, uint32_t flags, float* d, float* grad, float* hess,
                     float* dpose, float* d2pose, float* dxdpose, void* stream);
-int launch_manifold(const cmi::SceneDev& s, int which_class, int max_V, int max_E, const int32_t* pairs,
+int launch_manifold(const cmi::SceneDev& s, int class_mask, int max_V, int max_E, const int32_t* pairs,
                     int64_t n_pairs, const int64_t* offsets, const float* poses, int32_t n_slot, uint32_t flags,
                     const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats, void* stream);
 int launch_offsets(const cmi::SceneDev& s, const int32_t* pairs, int64_t n_pairs, int64_t* offsets, void* ws,

@@ -78,8 +78,11 @@ __device__ __forceinline__ void gJ(const float* g, const float* p, const PairFra
 // derivative slots: 9 independent components (tA, thetaA, thetaB); tB = -tA
 constexpr int NDQ = 9;
 
-template <int TIER, bool XP>
-__global__ void __launch_bounds__(128) k_contact_manifold(SceneDev S, const int32_t* __restrict__ pairs,
+template <int TIER, int XP>
+#ifndef CM_MANIFOLD_MINBLOCKS
+#define CM_MANIFOLD_MINBLOCKS 2
+#endif
+__global__ void __launch_bounds__(128, CM_MANIFOLD_MINBLOCKS) k_contact_manifold(SceneDev S, const int32_t* __restrict__ pairs,
                                                           int64_t n_pairs, const int64_t* __restrict__ offsets,
                                                           const float* __restrict__ poses, int32_t n_slot,
                                                           cm_manifold_out out, int64_t C, int xp_filter,
@@ -317,13 +320,10 @@ __global__ void __launch_bounds__(128) k_contact_manifold(SceneDev S, const int3
         for (int a = 0; a < 3; ++a) out.q[a * C + c] = qv[a];
       }
       if constexpr (TIER >= 2) {
-        // d depth = sum z_i d d_i;  d d_i = g^T J(p_i) (+ (g.e_t) d alpha_bar)
-        float dd[NDQ];
-#pragma unroll
-        for (int k = 0; k < NDQ; ++k) dd[k] = 0.f;
-        float ddi[6][NDQ];
-#pragma unroll
-        for (int i = 0; i < 6; ++i) {
+        // d d_i = g^T J(p_i) (+ (g.e_t) d alpha_bar for edge points); computed
+        // on the fly in both passes (recomputing is cheaper than holding 6x9
+        // values live)
+        auto cand_dd = [&](int i, float* o, float* ew /*unit e_t, edges*/) {
           const bool isv = i < 3;
           const int id = isv ? cv[i] : ce[i - 3];
           const float* bp = isv ? sv + VP * V + id : se + EP * E + id;
@@ -331,18 +331,29 @@ __global__ void __launch_bounds__(128) k_contact_manifold(SceneDev S, const int3
           const int sd = isv ? V : E;
           const float p[3] = {bp[0], bp[sd], bp[2 * sd]};
           const float g[3] = {bn[0], bn[sd], bn[2 * sd]};
-          gJ(g, p, F, ddi[i]);
+          gJ(g, p, F, o);
           if (!isv) {
             const int vI = __ldg(ed + 2 * id), vII = __ldg(ed + 2 * id + 1);
-            float ew[3] = {sv[(VP + 0) * V + vII] - sv[(VP + 0) * V + vI], sv[(VP + 1) * V + vII] - sv[(VP + 1) * V + vI],
-                           sv[(VP + 2) * V + vII] - sv[(VP + 2) * V + vI]};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) ew[a] = sv[(VP + a) * V + vII] - sv[(VP + a) * V + vI];
             const float il = rsqrtf(ew[0] * ew[0] + ew[1] * ew[1] + ew[2] * ew[2]);
-            const float ge = (g[0] * ew[0] + g[1] * ew[1] + g[2] * ew[2]) * il;
 #pragma unroll
-            for (int k = 0; k < NDQ; ++k) ddi[i][k] = fmaf(ge, se[(EDAB + k) * E + id], ddi[i][k]);
+            for (int a = 0; a < 3; ++a) ew[a] *= il;
+            const float ge = g[0] * ew[0] + g[1] * ew[1] + g[2] * ew[2];
+#pragma unroll
+            for (int k = 0; k < NDQ; ++k) o[k] = fmaf(ge, se[(EDAB + k) * E + id], o[k]);
           }
+        };
+        // d depth = sum z_i d d_i
+        float dd[NDQ];
 #pragma unroll
-          for (int k = 0; k < NDQ; ++k) dd[k] = fmaf(z[i], ddi[i][k], dd[k]);
+        for (int k = 0; k < NDQ; ++k) dd[k] = 0.f;
+#pragma unroll 1
+        for (int i = 0; i < 6; ++i) {
+          float o[NDQ], ew[3];
+          cand_dd(i, o, ew);
+#pragma unroll
+          for (int k = 0; k < NDQ; ++k) dd[k] = fmaf(z[i], o[k], dd[k]);
         }
         // d n = sum_i [d(z_i gamma_i) n_i + z_i gamma_i d n_i]
         //   d(z gamma)_i = z_i gamma_i [-(d d_i - d depth)/tau_min - (1 - gamma_i) d d_i / tau_cmp]
@@ -352,10 +363,18 @@ __global__ void __launch_bounds__(128) k_contact_manifold(SceneDev S, const int3
         for (int a = 0; a < 3; ++a)
 #pragma unroll
           for (int k = 0; k < NDQ; ++k) dn[a][k] = 0.f;
-#pragma unroll
+#pragma unroll 1
         for (int i = 0; i < 6; ++i) {
           const bool isv = i < 3;
           const int id = isv ? cv[i] : ce[i - 3];
+          float cz[NDQ], ew[3];
+          cand_dd(i, cz, ew);
+          const float zgi = isv ? (i == 0 ? zg[0] : (i == 1 ? zg[1] : zg[2])) : (i == 3 ? zg[3] : (i == 4 ? zg[4] : zg[5]));
+          const float dci = isv ? sv[VD * V + id] : se[ED * E + id];
+          const float gam = sigm(-dci * itcmp);
+          const float c1 = -itmin, c2 = -(1.f - gam) * itcmp;
+#pragma unroll
+          for (int k = 0; k < NDQ; ++k) cz[k] = zgi * fmaf(c1 + c2, cz[k], itmin * dd[k]);
           const float* bp = isv ? sv + VP * V + id : se + EP * E + id;
           const float* bn = isv ? sv + VN * V + id : se + EN * E + id;
           const float* bh = isv ? sv + VH * V + id : se + EH * E + id;
@@ -364,14 +383,9 @@ __global__ void __launch_bounds__(128) k_contact_manifold(SceneDev S, const int3
           const float nn[3] = {bn[0], bn[sd], bn[2 * sd]};
           const float h6[6] = {bh[0], bh[sd], bh[2 * sd], bh[3 * sd], bh[4 * sd], bh[5 * sd]};
           const float H[3][3] = {{h6[0], h6[1], h6[2]}, {h6[1], h6[3], h6[4]}, {h6[2], h6[4], h6[5]}};
-          const float gam = sigm(-dc[i] * itcmp);
-          float cz[NDQ];
-#pragma unroll
-          for (int k = 0; k < NDQ; ++k)
-            cz[k] = zg[i] * (-(ddi[i][k] - dd[k]) * itmin - (1.f - gam) * ddi[i][k] * itcmp);
           const float ra[3] = {p[0] - F.tA[0], p[1] - F.tA[1], p[2] - F.tA[2]};
           const float rb[3] = {p[0] - F.tB[0], p[1] - F.tB[1], p[2] - F.tB[2]};
-          const float w = zg[i];
+          const float w = zgi;
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
             // H [r]x row a: (H_a1 r2 - H_a2 r1, H_a2 r0 - H_a0 r2, H_a0 r1 - H_a1 r0)
@@ -385,18 +399,14 @@ __global__ void __launch_bounds__(128) k_contact_manifold(SceneDev S, const int3
             const float nk0 = a == 0 ? 0.f : (a == 1 ? nn[2] : -nn[1]);
             const float nk1 = a == 0 ? -nn[2] : (a == 1 ? 0.f : nn[0]);
             const float nk2 = a == 0 ? nn[1] : (a == 1 ? -nn[0] : 0.f);
-            float dni[NDQ] = {H[a][0], H[a][1], H[a][2], -hka0, -hka1, -hka2, hkb0 - nk0, hkb1 - nk1, hkb2 - nk2};
+            const float dni[NDQ] = {H[a][0], H[a][1], H[a][2], -hka0, -hka1, -hka2, hkb0 - nk0, hkb1 - nk1, hkb2 - nk2};
 #pragma unroll
             for (int k = 0; k < NDQ; ++k) dn[a][k] = fmaf(nn[a], cz[k], fmaf(w, dni[k], dn[a][k]));
           }
           if (!isv) {
-            const int vI = __ldg(ed + 2 * id), vII = __ldg(ed + 2 * id + 1);
-            float ew[3] = {sv[(VP + 0) * V + vII] - sv[(VP + 0) * V + vI], sv[(VP + 1) * V + vII] - sv[(VP + 1) * V + vI],
-                           sv[(VP + 2) * V + vII] - sv[(VP + 2) * V + vI]};
-            const float il = rsqrtf(ew[0] * ew[0] + ew[1] * ew[1] + ew[2] * ew[2]);
             float he[3];
 #pragma unroll
-            for (int a = 0; a < 3; ++a) he[a] = (H[a][0] * ew[0] + H[a][1] * ew[1] + H[a][2] * ew[2]) * il * w;
+            for (int a = 0; a < 3; ++a) he[a] = (H[a][0] * ew[0] + H[a][1] * ew[1] + H[a][2] * ew[2]) * w;
 #pragma unroll
             for (int k = 0; k < NDQ; ++k) {
               const float dk = se[(EDAB + k) * E + id];
@@ -444,7 +454,7 @@ int manifold_max_smem_bytes() {
   return m;
 }
 
-template <int TIER, bool XP>
+template <int TIER, int XP>
 static int launch_manifold_t(const SceneDev& s, int xp_filter, int max_V, int max_E, const int32_t* pairs,
                              int64_t n_pairs, const int64_t* offsets, const float* poses, int32_t n_slot,
                              const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats,
@@ -483,26 +493,25 @@ static int launch_manifold_t(const SceneDev& s, int xp_filter, int max_V, int ma
   return check_launch("k_contact_manifold");
 }
 
-int launch_manifold(const SceneDev& s, int which_class, int max_V, int max_E, const int32_t* pairs,
+int launch_manifold(const SceneDev& s, int class_mask, int max_V, int max_E, const int32_t* pairs,
                     int64_t n_pairs, const int64_t* offsets, const float* poses, int32_t n_slot, uint32_t flags,
                     const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats, void* stream) {
-  // which_class: -1 every pair uses the same instantiation (lean if the scene
-  // has no XPSQ, general otherwise); 2 mixed scene: lean kernel on pairs whose
-  // SDF shape has no XPSQ, general kernel on the others.
+  // class_mask bit c: SDF shapes of class c present (0 SQ family, 1 constant
+  // schedule XPSQ, 2 varying-schedule XPSQ).  One instantiation per present
+  // class; with several classes each kernel skips the other classes' pairs.
   cudaStream_t st = (cudaStream_t)stream;
   const int tier = (int)(flags & CM_TIER_MASK);
-  auto run = [&](bool xp, int filt) -> int {
-#define CM_L(T, X) launch_manifold_t<T, X>(s, filt, max_V, max_E, pairs, n_pairs, offsets, poses, n_slot, out, C, \
-                                           scratch, scratch_floats, st)
-    if (xp) return tier >= 2 ? CM_L(2, true) : (tier == 1 ? CM_L(1, true) : CM_L(0, true));
-    return tier >= 2 ? CM_L(2, false) : (tier == 1 ? CM_L(1, false) : CM_L(0, false));
+  const bool multi = (class_mask & (class_mask - 1)) != 0;
+#define CM_L(T, X) launch_manifold_t<T, X>(s, multi ? X : -1, max_V, max_E, pairs, n_pairs, offsets, poses, n_slot, \
+                                           out, C, scratch, scratch_floats, st)
+#define CM_T(X) (tier >= 2 ? CM_L(2, X) : (tier == 1 ? CM_L(1, X) : CM_L(0, X)))
+  int rc = CM_OK;
+  if (class_mask & 1) rc = CM_T(0);
+  if (!rc && (class_mask & 2)) rc = CM_T(1);
+  if (!rc && (class_mask & 4)) rc = CM_T(2);
+#undef CM_T
 #undef CM_L
-  };
-  if (which_class == 0) return run(false, -1);
-  if (which_class == 1) return run(true, -1);
-  int rc = run(false, 0);
-  if (rc) return rc;
-  return run(true, 1);
+  return rc;
 }
 
 }  // namespace cml

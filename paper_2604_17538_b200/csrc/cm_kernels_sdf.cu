@@ -27,7 +27,7 @@ using cml::num_sms;
 // ============================================================================
 // sdf_eval
 // ============================================================================
-template <int O, bool XP, bool PG, bool PH>
+template <int O, int XP, bool PG, bool PH>
 __global__ void __launch_bounds__(256) k_sdf_eval(SceneDev S, const int32_t* __restrict__ shape_ids,
                                                   const float* __restrict__ poses, const float* __restrict__ points,
                                                   int64_t B, int64_t P, float* __restrict__ d,
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(256) k_sdf_eval(SceneDev S, const int32_t* __r
   }
 }
 
-template <int O, bool XP, bool PG, bool PH>
+template <int O, int XP, bool PG, bool PH>
 static int launch_sdf_t(const SceneDev& s, int xp_filter, const int32_t* ids, const float* poses, const float* pts,
                         int64_t B, int64_t P, float* d, float* g, float* h, float* dp, float* d2p, float* dxp,
                         cudaStream_t st) {
@@ -132,7 +132,7 @@ static int launch_sdf_t(const SceneDev& s, int xp_filter, const int32_t* ids, co
   return check_launch("k_sdf_eval");
 }
 
-template <bool XP>
+template <int XP>
 static int dispatch_sdf(const SceneDev& s, int xp_filter, const int32_t* ids, const float* poses, const float* pts,
                         int64_t B, int64_t P, uint32_t flags, float* d, float* g, float* h, float* dp, float* d2p,
                         float* dxp, cudaStream_t st) {
@@ -151,16 +151,21 @@ static int dispatch_sdf(const SceneDev& s, int xp_filter, const int32_t* ids, co
 
 namespace cml {
 
-int launch_sdf_eval(const SceneDev& s, bool xp_class, const int32_t* ids, const float* poses, const float* pts,
+int launch_sdf_eval(const SceneDev& s, int class_mask, const int32_t* ids, const float* poses, const float* pts,
                     int64_t B, int64_t P, uint32_t flags, float* d, float* g, float* h, float* dp, float* d2p,
                     float* dxp, void* stream) {
-  // xp_class: the scene contains XPSQ shapes; run the general instantiation on
-  // them and the lean one on the rest
+  // class_mask bit c: the scene has SDF shapes of class c (0 SQ family, 1
+  // constant-schedule XPSQ, 2 varying-schedule XPSQ); one instantiation per
+  // present class, each filtering its own shapes when several are present
   cudaStream_t st = (cudaStream_t)stream;
-  if (!xp_class) return dispatch_sdf<false>(s, -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, st);
-  int rc = dispatch_sdf<false>(s, 0, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, st);
-  if (rc) return rc;
-  return dispatch_sdf<true>(s, 1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, st);
+  const bool multi = (class_mask & (class_mask - 1)) != 0;
+  int rc = CM_OK;
+  if (class_mask & 1) rc = dispatch_sdf<0>(s, multi ? 0 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, st);
+  if (!rc && (class_mask & 2))
+    rc = dispatch_sdf<1>(s, multi ? 1 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, st);
+  if (!rc && (class_mask & 4))
+    rc = dispatch_sdf<2>(s, multi ? 2 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, st);
+  return rc;
 }
 
 }  // namespace cml
