@@ -14,6 +14,27 @@
 namespace cmd {
 using namespace cmi;
 
+// Code-size control: the XPSQ evaluators (and optionally the whole shape
+// interpreter) are kept out of line so that each exists once per derivative
+// order instead of once per call site; inlined, the XPSQ kernels exceed the
+// instruction cache (ncu: stalls on "no instructions").
+#ifndef CM_XPSQ_NOINLINE
+#define CM_XPSQ_NOINLINE 1
+#endif
+#ifndef CM_SHAPE_NOINLINE
+#define CM_SHAPE_NOINLINE 0
+#endif
+#if CM_XPSQ_NOINLINE
+#define CM_XINL __noinline__
+#else
+#define CM_XINL __forceinline__
+#endif
+#if CM_SHAPE_NOINLINE
+#define CM_SINL __noinline__
+#else
+#define CM_SINL
+#endif
+
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 constexpr float SQ_GUARD = 1e-12f;  // |u|^p = exp(p log(u^2 + g)/2)
@@ -536,7 +557,7 @@ __device__ __forceinline__ void soft_cardano(const J2<O>& P, const J2<O>& Q, flo
     J2<O> r6 = Q * Q * 0.25f + Dp;
     J2<O> rho = jex2(jlg2(r6) * (1.f / 6.f));
     J2<O> th = jatan2(jsqrt(Dp), -Q * 0.5f);
-#pragma unroll
+#pragma unroll 1
     for (int k = 0; k < 3; ++k) {
       J2<O> sk = rho * jcos((th + 6.283185307179586f * (float)k) * (1.f / 3.f)) * 2.f;
       tp[k] = jsoftclip(sk - b3, 0.f, 1.f, tc, itc);
@@ -551,7 +572,7 @@ __device__ __forceinline__ void soft_cardano(const J2<O>& P, const J2<O>& Q, flo
 }
 
 // XPSQ leaf in its local frame
-template <int O> __device__ void xpsq_eval(const Xpsq& X, const SmoothDev& sp, const float* y, Res<O>& out) {
+template <int O> __device__ CM_XINL void xpsq_eval(const Xpsq& X, const SmoothDev& sp, const float* y, Res<O>& out) {
   const float tc = sp.tau_clip_t, itc = 1.f / tc;
   float w[3] = {y[0] - X.p1[0], y[1] - X.p1[1], y[2] - X.p1[2]};
   J3<O> tk[3];
@@ -728,7 +749,7 @@ __device__ __forceinline__ void xpsq_root_t(const Xpsq& X, const SmoothDev& sp, 
   }
 }
 
-template <int O> __device__ void xpsq_eval_fast(const Xpsq& X, const SmoothDev& sp, const float* y, Res<O>& out) {
+template <int O> __device__ CM_XINL void xpsq_eval_fast(const Xpsq& X, const SmoothDev& sp, const float* y, Res<O>& out) {
   const float tau = sp.tau_min, itau = 1.f / tau, itl = LOG2E * itau;
   const float w[3] = {y[0] - X.p1[0], y[1] - X.p1[1], y[2] - X.p1[2]};
   float tv[3], tg[3][3], th[3][6];
@@ -920,7 +941,7 @@ __device__ __forceinline__ void fold_level(Acc<O>& a0, Acc<O>& a1, Acc<O>& a2, i
 }
 
 // phi, grad, hess of shape `sh` at the body-frame point x
-template <int O, int XP> __device__ void eval_shape(const SceneDev& S, const ShapeRec& sh, const float* x, Res<O>& out) {
+template <int O, int XP> __device__ CM_SINL void eval_shape(const SceneDev& S, const ShapeRec& sh, const float* x, Res<O>& out) {
   const float tau = S.sp.tau_min, itau = 1.f / tau, itl = LOG2E * itau;
   if (sh.prog_len == 1) {  // single leaf: no accumulator needed
     leaf_eval<O, XP>(S, S.prog[sh.prog_begin].idx, x, out);
