@@ -529,7 +529,7 @@ template <int O> __device__ __forceinline__ J3<O> lse_jets(const J3<O>* x, int n
 // s_k = 2 rho cos((theta + 2 pi k)/3).  Both soft-clipped to (0,1), blended by
 // sigma(-Delta/tau), sigma(Delta/tau).
 template <int O>
-__device__ __forceinline__ void soft_cardano(const J2<O>& P, const J2<O>& Q, float b3, const SmoothDev& sp,
+__device__ __forceinline__ bool soft_cardano(const J2<O>& P, const J2<O>& Q, float b3, const SmoothDev& sp,
                                              J2<O>* t) {
   const float td = sp.tau_delta, itd = 1.f / td;
   const float tc = sp.tau_clip_t, itc = 1.f / tc;
@@ -569,6 +569,7 @@ __device__ __forceinline__ void soft_cardano(const J2<O>& P, const J2<O>& Q, flo
     else if (wneg.v > 0.f) t[k] = wneg * tm;
     else t[k] = wpos * tp[k];
   }
+  return !(wpos.v > 0.f);
 }
 
 // XPSQ leaf in its local frame
@@ -698,8 +699,12 @@ struct XsqParams {
   float p1, p2, m, k;
 };
 
+// returns true when the three roots are bitwise identical (point / straight
+// splines, or the curved case when the positive-branch weight is exactly 0 in
+// FP32): then the three PSQ terms coincide and -LSE(-phi, -phi, -phi) =
+// phi - tau ln 3 exactly, so one PSQ evaluation suffices
 template <int O>
-__device__ __forceinline__ void xpsq_root_t(const Xpsq& X, const SmoothDev& sp, const float* w, float* tv, float (*tg)[3],
+__device__ __forceinline__ bool xpsq_root_t(const Xpsq& X, const SmoothDev& sp, const float* w, float* tv, float (*tg)[3],
                                             float (*th)[6]) {
   const float tc = sp.tau_clip_t, itc = 1.f / tc;
 #pragma unroll
@@ -728,7 +733,7 @@ __device__ __forceinline__ void xpsq_root_t(const Xpsq& X, const SmoothDev& sp, 
     const float Qv = X.gQ[0] * w[0] + X.gQ[1] * w[1] + X.gQ[2] * w[2] + X.Q0;
     constexpr int OC = O;
     J2<OC> t2[3];
-    soft_cardano<OC>(jvar<2, OC>(Pv, 0), jvar<2, OC>(Qv, 1), X.b3, sp, t2);
+    const bool single = soft_cardano<OC>(jvar<2, OC>(Pv, 0), jvar<2, OC>(Qv, 1), X.b3, sp, t2);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       tv[k] = t2[k].v;
@@ -746,14 +751,16 @@ __device__ __forceinline__ void xpsq_root_t(const Xpsq& X, const SmoothDev& sp, 
         }
       }
     }
+    return single;
   }
+  return true;
 }
 
 template <int O> __device__ CM_XINL void xpsq_eval_fast(const Xpsq& X, const SmoothDev& sp, const float* y, Res<O>& out) {
   const float tau = sp.tau_min, itau = 1.f / tau, itl = LOG2E * itau;
   const float w[3] = {y[0] - X.p1[0], y[1] - X.p1[1], y[2] - X.p1[2]};
   float tv[3], tg[3][3], th[3][6];
-  xpsq_root_t<O>(X, sp, w, tv, tg, th);
+  const bool single = xpsq_root_t<O>(X, sp, w, tv, tg, th);
   XsqParams sq;
 #pragma unroll
   for (int i = 0; i < 3; ++i) sq.ia[i] = 1.f / X.a0[i];
@@ -764,8 +771,9 @@ template <int O> __device__ CM_XINL void xpsq_eval_fast(const Xpsq& X, const Smo
   const float* b = X.frenet ? X.bhat : nullptr;
   Acc<O> acc;
   acc_init(acc);
+  const int n_roots = single ? 1 : 3;
 #pragma unroll 1
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < n_roots; ++k) {
     const float t = tv[k];
     float pd[3], d[3], T[3], N[3], bb[3];
 #pragma unroll
@@ -860,6 +868,11 @@ template <int O> __device__ CM_XINL void xpsq_eval_fast(const Xpsq& X, const Smo
           rk.h[q] = fmaf(s, th[k][q], v);
         }
       }
+    }
+    if (single) {   // three identical terms: -LSE(-phi x 3) = phi - tau ln 3
+      out = rk;
+      out.v = fmaf(-tau, 1.0986122886681098f, rk.v);
+      return;
     }
     acc_fold(acc, -1.f, rk, itl, itau);   // smooth minimum over the roots
   }
