@@ -78,11 +78,25 @@ __device__ __forceinline__ void gJ(const float* g, const float* p, const PairFra
 // derivative slots: 9 independent components (tA, thetaA, thetaB); tB = -tA
 constexpr int NDQ = 9;
 
+// optional per-phase cycle accounting (tools/phase_timing.py; off in the product build)
+#ifndef CM_PHASE_TIMING
+#define CM_PHASE_TIMING 0
+#endif
+#if CM_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[3][4];
+extern "C" int cm_debug_phase_cycles(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles));
+}
+#endif
+
 template <int TIER, int XP>
+#ifndef CM_MANIFOLD_THREADS
+#define CM_MANIFOLD_THREADS 128
+#endif
 #ifndef CM_MANIFOLD_MINBLOCKS
 #define CM_MANIFOLD_MINBLOCKS 2
 #endif
-__global__ void __launch_bounds__(128, CM_MANIFOLD_MINBLOCKS) k_contact_manifold(SceneDev S, const int32_t* __restrict__ pairs,
+__global__ void __launch_bounds__(CM_MANIFOLD_THREADS, CM_MANIFOLD_MINBLOCKS) k_contact_manifold(SceneDev S, const int32_t* __restrict__ pairs,
                                                           int64_t n_pairs, const int64_t* __restrict__ offsets,
                                                           const float* __restrict__ poses, int32_t n_slot,
                                                           cm_manifold_out out, int64_t C, int xp_filter,
@@ -98,6 +112,17 @@ __global__ void __launch_bounds__(128, CM_MANIFOLD_MINBLOCKS) k_contact_manifold
   __shared__ PairFrame Fs;
   __shared__ ShapeRec SA, SB;
 
+#if CM_PHASE_TIMING
+  long long t_mark = 0;
+#define CM_PT(k)                                                                             \
+  if (threadIdx.x == 0) {                                                                    \
+    long long t_now = clock64();                                                             \
+    if (k > 0) atomicAdd(&g_phase_cycles[XP][k - 1], (unsigned long long)(t_now - t_mark)); \
+    t_mark = t_now;                                                                          \
+  }
+#else
+#define CM_PT(k)
+#endif
   for (int64_t pi = blockIdx.x; pi < n_pairs; pi += gridDim.x) {
     const int32_t* pr = pairs + 5 * pi;
     const int env = __ldg(pr + 0), slA = __ldg(pr + 1), slB = __ldg(pr + 2);
@@ -117,6 +142,7 @@ __global__ void __launch_bounds__(128, CM_MANIFOLD_MINBLOCKS) k_contact_manifold
       SB = sb;
     }
     __syncthreads();
+    CM_PT(0);
     const PairFrame& F = Fs;
     const int V = sa.V, E = sa.E, NF = sa.F;
     float* sv = st;                                   // vertex block
@@ -152,6 +178,7 @@ __global__ void __launch_bounds__(128, CM_MANIFOLD_MINBLOCKS) k_contact_manifold
       }
     }
     __syncthreads();
+    CM_PT(1);
 
     // ---- phase 2: sphere traces (Fig. 2), 2 per edge -------------
     for (int j = threadIdx.x; j < 2 * E; j += blockDim.x) {
@@ -212,6 +239,7 @@ __global__ void __launch_bounds__(128, CM_MANIFOLD_MINBLOCKS) k_contact_manifold
       }
     }
     __syncthreads();
+    CM_PT(2);
 
     // ---- phase 3: edge midpoints p_e = (p_I + p_II)/2 ----------------
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
@@ -255,6 +283,7 @@ __global__ void __launch_bounds__(128, CM_MANIFOLD_MINBLOCKS) k_contact_manifold
       }
     }
     __syncthreads();
+    CM_PT(3);
 
     // ---- phase 4: per-face fusion -------------------------------
     const int64_t off = __ldg(offsets + pi);
@@ -434,6 +463,10 @@ __global__ void __launch_bounds__(128, CM_MANIFOLD_MINBLOCKS) k_contact_manifold
           }
       }
     }
+#if CM_PHASE_TIMING
+    __syncthreads();
+#endif
+    CM_PT(4);
   }
 }
 
@@ -459,7 +492,7 @@ static int launch_manifold_t(const SceneDev& s, int xp_filter, int max_V, int ma
                              int64_t n_pairs, const int64_t* offsets, const float* poses, int32_t n_slot,
                              const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats,
                              cudaStream_t st) {
-  const int threads = 128;
+  const int threads = CM_MANIFOLD_THREADS;
   const int64_t need = manifold_smem_floats(max_V, max_E, TIER) * 4;
   const int static_smem = (int)(sizeof(PairFrame) + 2 * sizeof(ShapeRec));
   const bool use_smem = need <= kSmemBudget && need + static_smem + 1024 <= manifold_max_smem_bytes();
