@@ -32,14 +32,48 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# Executed FP32 FLOPs per pair of the dominant kernel (FFMA = 2, FADD/FMUL =
-# 1), measured once with ncu on the same workload and frozen here (DESIGN.md
-# §7): profiles/r01_ncu_summary.md.  Bytes per pair are algorithmic (inputs:
-# two poses + the pair record; outputs: F contacts x 237 B at tier 2).
-FLOP_PER_PAIR = {"C5": None, "C4": None, "C3": None, "C2": None}
+# Algorithmic work per pair: FP32 FLOPs from the frozen cost
+# table paper_2604_17538_b200/costmodel.json (per SDF shape and derivative
+# order, measured once with ncu by tools/costmodel.py) composed with the
+# pair's structure:
+#   flop = M(mesh_A) + (V + E) [c(B,2) - c(hs,2)] + 2 E (iters - 1) [c(B,1) - c(hs,1)]
+# with M(mesh_A) the tier-2 manifold FLOPs of the mesh against a half-space.
+# Bytes per pair are algorithmic too (inputs: two poses + the pair record;
+# outputs: F contacts x 237 B at tier 2).
 OUT_BYTES_PER_CONTACT = {0: 33, 1: 45, 2: 237}
 IN_BYTES_PER_PAIR = 2 * 32 + 20
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4 at the 1965 MHz max SM clock
+
+
+def _cost_key(workload, shape, kind):
+    if workload == "C5":
+        return shape.name
+    if kind == "sdf":
+        return {"C1": "C1:", "C2": "C2:", "C3": "C3:", "C4": "C4:"}[workload] + (
+            {"blob18": "blob18"}.get(shape.name, shape.name))
+    return {"C2": "C2:", "C3": "C3:", "C4": "C4:", "C1": "C1:"}[workload] + shape.name
+
+
+def flop_per_launch(workload, scene, S):
+    """Algorithmic FP32 FLOPs of one tier-2 call over scene.pairs."""
+    with open(os.path.join(ROOT, "paper_2604_17538_b200", "costmodel.json")) as f:
+        cm = json.load(f)
+    hs1, hs2 = cm["halfspace_eval"]["order1"], cm["halfspace_eval"]["order2"]
+    it = scene.smooth["trace_iters"]
+    per_shape_pair = {}
+    total = 0.0
+    a_ids, b_ids = scene.pairs[:, 3], scene.pairs[:, 4]
+    keys, counts = np.unique(np.stack([a_ids, b_ids], 1), axis=0, return_counts=True)
+    for (a, b), n in zip(keys, counts):
+        sa, sb = scene.shapes[a], scene.shapes[b]
+        ka, kb = _cost_key(workload, sa, "mesh"), _cost_key(workload, sb, "sdf")
+        if ka not in cm["manifold_with_halfspace"] or kb not in cm["sdf"]:
+            return None
+        V, E, F = S.counts(int(a))
+        c = cm["manifold_with_halfspace"][ka]["flop_per_pair_total_with_halfspace"]
+        c += (V + E) * (cm["sdf"][kb]["order2"]["flop"] - hs2) + 2 * E * (it - 1) * (cm["sdf"][kb]["order1"]["flop"] - hs1)
+        total += n * c
+    return total
 
 
 def load_peaks():
@@ -185,7 +219,6 @@ def main():
     ap.add_argument("--tier", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--flop-per-pair", type=float, default=0.0)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -283,13 +316,15 @@ def main():
     # lean + one XPSQ instantiation for scenes mixing both SDF classes)
     kern_s = ms_per_step / 1e3
     hbm_gbs = bytes_alg / kern_s / 1e9
-    fpp = args.flop_per_pair or FLOP_PER_PAIR.get(args.workload)
+    flop_launch = flop_per_launch(args.workload, scene, S) if args.tier == 2 else None
+    fpp = flop_launch / n_pairs if flop_launch else None
     if fpp:
-        achieved = fpp * n_pairs / kern_s / 1e12
+        achieved = flop_launch / kern_s / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP32_PEAK_TFLOPS, "traffic": None,
                 "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
-                "flop_per_pair": fpp, "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks["hbm_gbs"],
+                "flop_per_pair": fpp, "flop_source": "costmodel.json (ncu-measured per-shape/order table, DESIGN.md §7)",
+                "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks["hbm_gbs"],
                                               "frac": hbm_gbs / peaks["hbm_gbs"], "peak_source": peak_src}}
     else:
         roof = {"bound": "hbm", "achieved": hbm_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",

@@ -1,0 +1,150 @@
+"""Frozen per-(SDF shape, derivative order) FP32 cost table for the roofline.
+
+  ncu --metrics <FP32 op counts> --csv --log-file costmodel_ncu.csv \
+      python tools/costmodel.py run
+  python tools/costmodel.py parse costmodel_ncu.csv   -> paper_2604_17538_b200/costmodel.json
+
+`run` launches, in a fixed order:
+  1. k_sdf_eval over 2^20 points for every C5 SDF prototype and every C2-C4
+     SDF shape, at order 1 (value + gradient) and order 2 (+ Hessian);
+  2. k_contact_manifold (tier 2) with a half-space SDF for each sampled mesh
+     of C2-C5, to measure the manifold's own arithmetic (trace recursion,
+     candidate derivative rows, per-face fusion) per pair.
+FLOPs = 2 FFMA + FADD + FMUL (+ the paired FFMA2/FADD2/FMUL2 x 2), counted
+per executed thread instruction.  Per-pair algorithmic FLOPs are then
+  overhead(mesh) + (V + E) c(B, 2) + 2 E (iters - 1) c(B, 1)
+(DESIGN.md §7).
+"""
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+NPTS = 1 << 20
+
+
+def sdf_shapes():
+    from paper_2604_17538_b200 import synth
+    sampled, sdf = synth.c5_library()
+    out = [(s.name, s) for s in sdf]
+    out.append(("C2:sq_box", synth.make_shape("C2:sq_box", synth.sq((0.1, 0.1, 0.1), (0.1, 0.1)))))
+    out.append(("C3:blob18", synth.make_shape("C3:blob18", synth.blob18(3, 18))))
+    out.append(("C4:cup", synth.make_shape("C4:cup", synth.cup())))
+    out.append(("C1:sq_box", synth.make_shape("C1:sq_box", synth.sq((0.2, 0.15, 0.1), (0.3, 0.3)))))
+    out.append(("C1:ground", synth.make_shape("C1:ground", synth.halfspace((0, 0, 1), 0.0))))
+    return out
+
+
+def meshes():
+    from paper_2604_17538_b200 import synth
+    sampled, _ = synth.c5_library()
+    out = [(s.name, s) for s in sampled]
+    out.append(("C2:mesh_box", synth.make_shape("C2:mesh_box", None, synth.box_mesh((0.1, 0.1, 0.1), 6))))
+    out.append(("C3:patch", synth.make_shape("C3:patch", None, synth.plane_patch(16, 32, 0.4, 0.8))))
+    c4 = synth.c4_scene(1)
+    out += [("C4:" + s.name, s) for s in c4.shapes[1:]]
+    c1 = synth.c1_scene()
+    out += [("C1:" + s.name, s) for s in c1.shapes]
+    return out
+
+
+def run():
+    import torch
+    from paper_2604_17538_b200 import binding, synth
+    rng = np.random.default_rng(0)
+    shapes = sdf_shapes()
+    names = [n for n, _ in shapes]
+    sc = binding.Scene([s for _, s in shapes], synth.smooth_params(0.1))
+    pts = torch.from_numpy(rng.uniform(-0.12, 0.12, (NPTS, 3)).astype(np.float32)).cuda()
+    poses = torch.zeros(1, 8, device="cuda")
+    poses[0, 3] = 1
+    for i, n in enumerate(names):
+        ids = torch.tensor([i], dtype=torch.int32, device="cuda")
+        for flags in (3, 7):
+            sc.sdf_eval(ids, poses, pts, NPTS, flags)
+    torch.cuda.synchronize()
+    # manifold overhead with a half-space SDF
+    ms = meshes()
+    hs = synth.make_shape("hs", synth.halfspace((0, 0, 1), 0.0))
+    for n, m in ms:
+        shp = [m, hs]
+        S = binding.Scene(shp, synth.smooth_params(0.1))
+        NP = 4096
+        poses_m = torch.zeros(NP, 2, 8, device="cuda")
+        poses_m[:, :, 3] = 1
+        poses_m[:, 0, 2] = torch.linspace(-0.05, 0.05, NP, device="cuda")
+        pairs_np = np.stack([np.arange(NP), np.zeros(NP), np.ones(NP), np.zeros(NP), np.ones(NP)], 1).astype(np.int32)
+        pairs = torch.from_numpy(pairs_np).cuda()
+        offs = S.manifold_offsets(pairs)
+        C = S.manifold_size(pairs_np)
+        S.contact_manifold(pairs, offs, C, poses_m, 2)
+        torch.cuda.synchronize()
+    with open(os.path.join(ROOT, "gpurun_out", "costmodel_order.json"), "w") as f:
+        json.dump({"sdf": names, "meshes": [n for n, _ in ms], "npts": NPTS, "npairs": 4096}, f)
+
+
+def parse(csv_path):
+    import csv
+    order = json.load(open(os.path.join(os.path.dirname(csv_path), "costmodel_order.json")))
+    rows = [r for r in csv.reader(open(csv_path)) if r]
+    hdr = None
+    launches = {}
+    for r in rows:
+        if r[0] == "ID":
+            hdr = r
+            continue
+        if hdr is None or len(r) != len(hdr):
+            continue
+        d = dict(zip(hdr, r))
+        lid = int(d["ID"])
+        L = launches.setdefault(lid, {"name": d["Kernel Name"]})
+        L[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
+
+    def flops(L):
+        g = lambda k: L.get("smsp__sass_thread_inst_executed_op_%s_pred_on.sum" % k, 0.0)
+        mufu = L.get("smsp__inst_executed_pipe_xu.sum", 0.0) * 32.0
+        return 2 * g("ffma") + g("fadd") + g("fmul") + 4 * g("ffma2") + 2 * g("fadd2") + 2 * g("fmul2"), mufu
+
+    sdf_l = [L for _, L in sorted(launches.items()) if "k_sdf_eval" in L["name"]]
+    man_l = [L for _, L in sorted(launches.items()) if "k_contact_manifold" in L["name"]]
+    # with several SDF classes a call may launch one kernel per class; the
+    # sdf table is built from the per-call sums
+    names = order["sdf"]
+    n_sdf_calls = 2 * len(names)
+    per_call = len(sdf_l) // n_sdf_calls
+    table = {}
+    for i, n in enumerate(names):
+        for j, o in enumerate((1, 2)):
+            ls = sdf_l[(2 * i + j) * per_call:(2 * i + j + 1) * per_call]
+            f = sum(flops(L)[0] for L in ls) / order["npts"]
+            m = sum(flops(L)[1] for L in ls) / order["npts"]
+            table.setdefault(n, {})["order%d" % o] = {"flop": round(f, 1), "mufu": round(m, 2)}
+    hs1 = table["C1:ground"]["order1"]["flop"]
+    hs2 = table["C1:ground"]["order2"]["flop"]
+    from paper_2604_17538_b200 import synth  # noqa
+    over = {}
+    mnames = order["meshes"]
+    per_m = len(man_l) // len(mnames)
+    import paper_2604_17538_b200.binding  # noqa
+    for k, n in enumerate(mnames):
+        ls = man_l[k * per_m:(k + 1) * per_m]
+        f = sum(flops(L)[0] for L in ls) / order["npairs"]
+        over[n] = {"flop_per_pair_total_with_halfspace": round(f, 1)}
+    out = {"provenance": "ncu FP32 op counts (2 FFMA + FADD + FMUL per thread instr) of k_sdf_eval over %d points "
+                         "per shape and order, and of k_contact_manifold (tier 2) with a half-space SDF per mesh; "
+                         "tools/costmodel.py" % order["npts"],
+           "sdf": table, "halfspace_eval": {"order1": hs1, "order2": hs2}, "manifold_with_halfspace": over}
+    path = os.path.join(ROOT, "paper_2604_17538_b200", "costmodel.json")
+    json.dump(out, open(path, "w"), indent=1)
+    print(json.dumps(out, indent=1)[:3000])
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "run":
+        run()
+    else:
+        parse(sys.argv[2])
