@@ -158,7 +158,8 @@ def oracle_rate(scene, budget_s=15.0, threads=0, max_pairs=None):
     from oracle import oracle as O
     osc = O.OracleScene(scene)
     cores = O.max_threads() if threads == 0 else threads
-    n = min(len(scene.pairs), max(cores, 8))
+    # pilot large enough to keep every core busy, then scale to the budget
+    n = min(len(scene.pairs), 16 * max(cores, 8))
     t0 = time.perf_counter()
     osc.contact_manifold(pairs=scene.pairs[:n], n_threads=threads)
     dt = time.perf_counter() - t0
@@ -320,8 +321,15 @@ def main():
     fpp = flop_launch / n_pairs if flop_launch else None
     if fpp:
         achieved = flop_launch / kern_s / 1e12
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "r01_traffic_%s.json" % args.workload.lower())
+        if os.path.exists(tpath) and args.tier == 2:
+            with open(tpath) as f:
+                traffic = json.load(f)["bytes_per_pair"] * n_pairs   # measured DRAM bytes per launch
         roof = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP32_PEAK_TFLOPS, "traffic": None,
+                "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,
+                "traffic_unit": "bytes per step (ncu dram read + write, scaled per pair)",
+                "bytes_alg": bytes_alg,
                 "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
                 "flop_per_pair": fpp, "flop_source": "costmodel.json (ncu-measured per-shape/order table, DESIGN.md §7)",
                 "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks["hbm_gbs"],
@@ -333,7 +341,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, m, cores, dt = oracle_rate(scene, budget_s=15.0)
+        rate, m, cores, dt = oracle_rate(scene, budget_s=20.0)
         cpu = {"value": rate, "unit": "pairs/s", "cores": cores, "kind": "oracle",
                "sample": "first %d pairs of the %s shard, FP64 jet oracle, OpenMP over pairs, %.1f s" % (m, args.workload, dt)}
 

@@ -45,7 +45,8 @@ def compare(name, got, ref, ref_pert, tol, report):
     got = np.asarray(got, dtype=np.float64)
     sens = np.abs(ref - ref_pert)
     excl = sens > tol / 10.0
-    bad = (np.abs(got - ref) > tol) & ~excl
+    # non-finite values on either side are failures, never exclusions
+    bad = ((np.abs(got - ref) > tol) & ~excl) | ~np.isfinite(got) | ~np.isfinite(ref)
     nb = int(bad.sum())
     report.append(dict(field=name, n=int(ref.size), excluded=int(excl.sum()), failures=nb,
                        max_err_over_tol=float(np.nanmax(np.where(excl, 0, np.abs(got - ref) / tol)))
