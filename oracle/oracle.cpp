@@ -353,16 +353,29 @@ template <class T> void xpsq_roots(const Node& n, const T* y, const Smooth& sp, 
   if (delta_out) *delta_out = val(Delta);
   if (wneg_out) *wneg_out = val(wneg);
   T tm = T(0.0), tp[3] = {T(0.0), T(0.0), T(0.0)};
-  // A branch whose weight underflows to exactly 0 contributes exactly 0; it is
-  // skipped so that 0 * (non-finite derivative of a degenerate branch) cannot
-  // poison the jets (reading #34).
-  if (val(wneg) > 0.0) {
+  // A branch whose weight is below 1e-200 is skipped (reading #34):
+  // its value contribution is < 1e-200 and its derivative contributions are
+  // O(sqrt(weight)) (the branch's degenerate square / cube roots scale like
+  // the projected discriminant s+(-|Delta|) ~ tau * weight), i.e. zero at FP64
+  // resolution, while evaluating it literally would form 0 * inf in the jets
+  // once s+ underflows (|Delta|/tau > ~740).
+  const double W_SKIP = 1e-200;
+  if (val(wneg) > W_SKIP) {
     T D = -Dm / 108.0;
     T sD = sqrt(D);
-    T s = cbrt(-Q / 2.0 + sD) + cbrt(-Q / 2.0 - sD);
+    // Cardano s = cbrt(-Q/2 + sqrt(D)) + cbrt(-Q/2 - sqrt(D)), evaluated in
+    // its cancellation-free form (reading #37): u = the term whose
+    // radicand does not cancel, v = cbrt(Q^2/4 - D) / u (the product of the two
+    // cube roots), with Q^2/4 - D = -(P^3 + s+(Delta)/4)/27 (exact identity,
+    // since -Delta- = s+(-Delta) = -Delta + s+(Delta) and -Delta = 4P^3 + 27Q^2).
+    // Term-by-term evaluation loses every digit of the smaller radicand when
+    // |P|^3 << Q^2 and returns non-finite derivatives (radicand rounded to 0).
+    T u = val(Q) >= 0.0 ? cbrt(-Q / 2.0 - sD) : cbrt(-Q / 2.0 + sD);
+    T prod = cbrt(-(P * P * P + softplus(Delta, sp.tau_delta) / 4.0) / 27.0);
+    T s = val(u) != 0.0 ? u + prod / u : u;
     tm = softclip(s - b / 3.0, 0.0, 1.0, sp.tau_clip_t);
   }
-  if (val(wpos) > 0.0) {
+  if (val(wpos) > W_SKIP) {
     T rho = exp(log(Q * Q / 4.0 + Dp / 108.0) / 6.0);
     T th = atan2(sqrt(Dp / 108.0), -Q / 2.0);
     for (int k = 0; k < 3; ++k) {
@@ -371,8 +384,8 @@ template <class T> void xpsq_roots(const Node& n, const T* y, const Smooth& sp, 
     }
   }
   for (int k = 0; k < 3; ++k) {
-    if (val(wneg) > 0.0 && val(wpos) > 0.0) tk[k] = wneg * tm + wpos * tp[k];
-    else if (val(wneg) > 0.0) tk[k] = wneg * tm;
+    if (val(wneg) > W_SKIP && val(wpos) > W_SKIP) tk[k] = wneg * tm + wpos * tp[k];
+    else if (val(wneg) > W_SKIP) tk[k] = wneg * tm;
     else tk[k] = wpos * tp[k];
   }
 }

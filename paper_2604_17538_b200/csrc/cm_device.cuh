@@ -540,7 +540,9 @@ __device__ __forceinline__ bool soft_cardano(const J2<O>& P, const J2<O>& Q, flo
   J2<O> tm = jconst<2, O>(0.f), tp[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) tp[k] = jconst<2, O>(0.f);
-  if (wneg.v > 0.f) {
+  // branches whose weight is below 1e-20 are skipped (reading #34)
+  constexpr float W_SKIP = 1e-20f;
+  if (wneg.v > W_SKIP) {
     J2<O> spD = jsoftplus(Delta, td, itd);          // s+(Delta)
     J2<O> Pm = jcbrt(P3 + spD * 0.25f);
     J2<O> D = jsoftplus(-Delta, td, itd) * (1.f / 108.f);
@@ -552,7 +554,7 @@ __device__ __forceinline__ bool soft_cardano(const J2<O>& P, const J2<O>& Q, flo
     else s = u;
     tm = jsoftclip(s - b3, 0.f, 1.f, tc, itc);
   }
-  if (wpos.v > 0.f) {
+  if (wpos.v > W_SKIP) {
     J2<O> Dp = jsoftplus(Delta, td, itd) * (1.f / 108.f);   // Delta+ / 108
     J2<O> r6 = Q * Q * 0.25f + Dp;
     J2<O> rho = jex2(jlg2(r6) * (1.f / 6.f));
@@ -565,11 +567,11 @@ __device__ __forceinline__ bool soft_cardano(const J2<O>& P, const J2<O>& Q, flo
   }
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    if (wneg.v > 0.f && wpos.v > 0.f) t[k] = wneg * tm + wpos * tp[k];
-    else if (wneg.v > 0.f) t[k] = wneg * tm;
+    if (wneg.v > W_SKIP && wpos.v > W_SKIP) t[k] = wneg * tm + wpos * tp[k];
+    else if (wneg.v > W_SKIP) t[k] = wneg * tm;
     else t[k] = wpos * tp[k];
   }
-  return !(wpos.v > 0.f);
+  return !(wpos.v > W_SKIP);
 }
 
 // XPSQ leaf in its local frame
@@ -699,6 +701,148 @@ struct XsqParams {
   float p1, p2, m, k;
 };
 
+// Soft Cardano with implicit derivatives (same function as soft_cardano; far
+// less code than the jets).  Each branch returns roots of a modified
+// depressed cubic F(s) = s^3 + Pt s + Q = 0 whose discriminant is the
+// projected one (reading #10):
+//   negative:  Pt = cbrt(W),       W = P^3 + s+(Delta)/4            (one root)
+//   positive:  Pt = -3 cbrt(V),    V = Q^2/4 + s+(Delta)/108        (three roots)
+// so with a, b in {P, Q}:  s_a = -(Pt_a s + Q_a)/F_s,  F_s = 3 s^2 + Pt,
+//   s_ab = -(6 s s_a s_b + Pt_b s_a + Pt_a s_b + Pt_ab s)/F_s.
+// The values use the cancellation-free forms of soft_cardano.
+template <int O>
+__device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3, const SmoothDev& sp, J2<O>* t) {
+  const float td = sp.tau_delta, itd = 1.f / td;
+  const float tc = sp.tau_clip_t, itc = 1.f / tc;
+  const float P2 = P * P, P3 = P2 * P;
+  const float Delta = -(4.f * P3 + 27.f * Q * Q);
+  const float Dl[2] = {-12.f * P2, -54.f * Q};          // dDelta/d(P, Q)
+  const float Dll[3] = {-24.f * P, 0.f, -54.f};         // PP, PQ, QQ
+  const float wn = sigm(-Delta * itd), wp = sigm(Delta * itd);
+  const float sp1 = sigm(Delta * itd);                  // s+'(Delta)
+  const float sp2 = sp1 * (1.f - sp1) * itd;            // s+''(Delta)
+  const float spD = softplus(Delta, td, itd);           // s+(Delta)
+  // blend weights and their derivatives
+  const float dwn = -wn * (1.f - wn) * itd, dwp = wp * (1.f - wp) * itd;
+  const float ddwn = wn * (1.f - wn) * (1.f - 2.f * wn) * itd * itd;
+  const float ddwp = wp * (1.f - wp) * (1.f - 2.f * wp) * itd * itd;
+  // derivatives of the modified coefficient and of the root
+  auto root_derivs = [&](float s, float Pt, const float* Pa, const float* Pab, float* sa, float* sab) {
+    const float Fs = fmaf(3.f * s, s, Pt);
+    const float iF = 1.f / Fs;
+    sa[0] = -(Pa[0] * s) * iF;
+    sa[1] = -(fmaf(Pa[1], s, 1.f)) * iF;
+    if constexpr (O >= 2) {
+      sab[0] = -(6.f * s * sa[0] * sa[0] + 2.f * Pa[0] * sa[0] + Pab[0] * s) * iF;
+      sab[1] = -(6.f * s * sa[0] * sa[1] + Pa[1] * sa[0] + Pa[0] * sa[1] + Pab[1] * s) * iF;
+      sab[2] = -(6.f * s * sa[1] * sa[1] + 2.f * Pa[1] * sa[1] + Pab[2] * s) * iF;
+    }
+  };
+  // soft clip of s - b/3 into (0, 1) with derivatives
+  auto clip = [&](float s, const float* sa, const float* sab, float& v, float* va, float* vab) {
+    const float x = s - b3;
+    v = softclip(x, 0.f, 1.f, tc, itc);
+    const float s1 = sigm(x * itc), s2 = sigm((x - 1.f) * itc);
+    const float c1 = s1 - s2, c2 = (s1 * (1.f - s1) - s2 * (1.f - s2)) * itc;
+    va[0] = c1 * sa[0];
+    va[1] = c1 * sa[1];
+    if constexpr (O >= 2) {
+      vab[0] = fmaf(c2 * sa[0], sa[0], c1 * sab[0]);
+      vab[1] = fmaf(c2 * sa[0], sa[1], c1 * sab[1]);
+      vab[2] = fmaf(c2 * sa[1], sa[1], c1 * sab[2]);
+    }
+  };
+  float tm = 0.f, tma[2] = {0.f, 0.f}, tmab[3] = {0.f, 0.f, 0.f};
+  float tp[3] = {0.f, 0.f, 0.f}, tpa[3][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}}, tpab[3][3] = {};
+  constexpr float W_SKIP = 1e-20f;   // negligible branches are skipped (reading #34)
+  const bool use_n = wn > W_SKIP, use_p = wp > W_SKIP;
+  if (use_n) {
+    const float W = fmaf(0.25f, spD, P3);
+    const float Pm = cbrtf(W);
+    // Cardano's cancellation-free form: u = cbrt(-Q/2 - sign(Q) sqrt(D)), v = -Pm/(3u)
+    const float D = softplus(-Delta, td, itd) * (1.f / 108.f);
+    const float sD = sqrtf(D);
+    const float u = cbrtf(Q >= 0.f ? -0.5f * Q - sD : -0.5f * Q + sD);
+    const float s = fabsf(u) > 1e-30f ? u - Pm / (3.f * u) : u;
+    float sa[2] = {0.f, 0.f}, sab[3] = {0.f, 0.f, 0.f};
+    if constexpr (O >= 1) {
+      const float Wa[2] = {fmaf(3.f, P2, 0.25f * sp1 * Dl[0]), 0.25f * sp1 * Dl[1]};
+      const float ip2 = 1.f / fmaxf(3.f * Pm * Pm, 1e-30f);   // guarded at the cusp (reading #15)
+      const float Pa[2] = {Wa[0] * ip2, Wa[1] * ip2};
+      float Pab[3] = {0.f, 0.f, 0.f};
+      if constexpr (O >= 2) {
+        const float Wab[3] = {fmaf(6.f, P, 0.25f * fmaf(sp2 * Dl[0], Dl[0], sp1 * Dll[0])),
+                              0.25f * sp2 * Dl[0] * Dl[1], 0.25f * fmaf(sp2 * Dl[1], Dl[1], sp1 * Dll[2])};
+        const float den = 3.f * Pm * Pm * Pm;
+        const float c = 2.f * ip2 / (fabsf(den) > 1e-30f ? den : copysignf(1e-30f, den));
+        Pab[0] = fmaf(-c, Wa[0] * Wa[0], Wab[0] * ip2);
+        Pab[1] = fmaf(-c, Wa[0] * Wa[1], Wab[1] * ip2);
+        Pab[2] = fmaf(-c, Wa[1] * Wa[1], Wab[2] * ip2);
+      }
+      root_derivs(s, Pm, Pa, Pab, sa, sab);
+    }
+    clip(s, sa, sab, tm, tma, tmab);
+  }
+  if (use_p) {
+    const float V = fmaf(0.25f * Q, Q, spD * (1.f / 108.f));
+    const float rho = ex2(lg2(V) * (1.f / 6.f));
+    const float th = atan2f(sqrtf(spD * (1.f / 108.f)), -0.5f * Q);
+    float Pa[2] = {0.f, 0.f}, Pab[3] = {0.f, 0.f, 0.f};
+    const float Pt = -3.f * rho * rho;
+    if constexpr (O >= 1) {
+      const float Va[2] = {sp1 * Dl[0] * (1.f / 108.f), fmaf(0.5f, Q, sp1 * Dl[1] * (1.f / 108.f))};
+      const float iV23 = 1.f / fmaxf(rho * rho * rho * rho, 1e-30f);   // V^(-2/3)
+      Pa[0] = -Va[0] * iV23;
+      Pa[1] = -Va[1] * iV23;
+      if constexpr (O >= 2) {
+        const float Vab[3] = {fmaf(sp2 * Dl[0], Dl[0], sp1 * Dll[0]) * (1.f / 108.f),
+                              sp2 * Dl[0] * Dl[1] * (1.f / 108.f),
+                              fmaf(fmaf(sp2 * Dl[1], Dl[1], sp1 * Dll[2]), 1.f / 108.f, 0.5f)};
+        const float c = (2.f / 3.f) * iV23 / fmaxf(V, 1e-30f);
+        Pab[0] = fmaf(c, Va[0] * Va[0], -Vab[0] * iV23);
+        Pab[1] = fmaf(c, Va[0] * Va[1], -Vab[1] * iV23);
+        Pab[2] = fmaf(c, Va[1] * Va[1], -Vab[2] * iV23);
+      }
+    }
+#pragma unroll 1
+    for (int k = 0; k < 3; ++k) {
+      float sn, cs;
+      sincosf((th + 6.283185307179586f * (float)k) * (1.f / 3.f), &sn, &cs);
+      const float s = 2.f * rho * cs;
+      float sa[2] = {0.f, 0.f}, sab[3] = {0.f, 0.f, 0.f};
+      if constexpr (O >= 1) root_derivs(s, Pt, Pa, Pab, sa, sab);
+      float v, va[2], vab[3];
+      clip(s, sa, sab, v, va, vab);
+      tp[k] = v;
+      tpa[k][0] = va[0]; tpa[k][1] = va[1];
+      if constexpr (O >= 2) { tpab[k][0] = vab[0]; tpab[k][1] = vab[1]; tpab[k][2] = vab[2]; }
+    }
+  }
+  // blend t_k = wn t- + wp t+_k (product rule)
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float a = use_n ? 1.f : 0.f, b = use_p ? 1.f : 0.f;
+    t[k].v = a * wn * tm + b * wp * tp[k];
+    if constexpr (O >= 1) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        t[k].g[i] = a * fmaf(dwn * Dl[i], tm, wn * tma[i]) + b * fmaf(dwp * Dl[i], tp[k], wp * tpa[k][i]);
+    }
+    if constexpr (O >= 2) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int i = q == 2 ? 1 : 0, j = q == 0 ? 0 : 1;
+        const float wnab = fmaf(ddwn * Dl[i], Dl[j], dwn * Dll[q]);
+        const float wpab = fmaf(ddwp * Dl[i], Dl[j], dwp * Dll[q]);
+        const float hn = wnab * tm + dwn * Dl[i] * tma[j] + dwn * Dl[j] * tma[i] + wn * tmab[q];
+        const float hp = wpab * tp[k] + dwp * Dl[i] * tpa[k][j] + dwp * Dl[j] * tpa[k][i] + wp * tpab[k][q];
+        t[k].h[q] = a * hn + b * hp;
+      }
+    }
+  }
+  return !use_p;
+}
+
 // returns true when the three roots are bitwise identical (point / straight
 // splines, or the curved case when the positive-branch weight is exactly 0 in
 // FP32): then the three PSQ terms coincide and -LSE(-phi, -phi, -phi) =
@@ -733,7 +877,7 @@ __device__ __forceinline__ bool xpsq_root_t(const Xpsq& X, const SmoothDev& sp, 
     const float Qv = X.gQ[0] * w[0] + X.gQ[1] * w[1] + X.gQ[2] * w[2] + X.Q0;
     constexpr int OC = O;
     J2<OC> t2[3];
-    const bool single = soft_cardano<OC>(jvar<2, OC>(Pv, 0), jvar<2, OC>(Qv, 1), X.b3, sp, t2);
+    const bool single = soft_cardano_implicit<OC>(Pv, Qv, X.b3, sp, t2);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       tv[k] = t2[k].v;

@@ -295,3 +295,16 @@ def test_sliding_box_stack_continuity(oracle_mod):
             active = out["W"] > 1e-3
             assert np.abs(out["point"] - prev)[active].max() <= 50 * 1e-3
         prev = out["point"]
+
+
+@pytest.mark.parametrize("cfg", ["C4", "C5"])
+def test_oracle_outputs_finite_on_workloads(oracle_mod, cfg):
+    """Every oracle output is finite on seeded samples of the benchmark
+    workloads (guards readings #34 and #37: negligible soft-Cardano branches
+    and the cancellation-free Cardano evaluation)."""
+    O = oracle_mod
+    sc = synth.c4_scene(48) if cfg == "C4" else synth.c5_scene(3000)
+    osc = O.OracleScene(sc)
+    r = osc.contact_manifold(pairs=sc.pairs[:900])
+    for k in ("point", "normal", "depth", "W", "q", "ddepth", "dnormal"):
+        assert np.isfinite(r[k]).all(), k
