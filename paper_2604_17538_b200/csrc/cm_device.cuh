@@ -519,60 +519,9 @@ template <int O> __device__ __forceinline__ J3<O> lse_jets(const J3<O>* x, int n
   return L * s;
 }
 
-// soft Cardano on a 2-variable jet in (P, Q) (Eq. (6); DESIGN.md
-// readings #9-#13).  Negative branch: real root of s^3 + P- s + Q = 0 with
-// P-^3 = P^3 + s+(Delta)/4 (the cubic whose discriminant is Delta- =
-// -s+(-Delta)), computed in Cardano's cancellation-free form u + v,
-// u = cbrt(-Q/2 - sign(Q) sqrt(D)), v = -P-/(3u), D = -Delta-/108.  Positive
-// branch: trigonometric form with Delta+ = s+(Delta):
-// rho^6 = Q^2/4 + Delta+/108, theta = atan2(sqrt(Delta+/108), -Q/2),
-// s_k = 2 rho cos((theta + 2 pi k)/3).  Both soft-clipped to (0,1), blended by
-// sigma(-Delta/tau), sigma(Delta/tau).
+// soft Cardano (Eq. (6)) with implicit derivatives, defined below
 template <int O>
-__device__ __forceinline__ bool soft_cardano(const J2<O>& P, const J2<O>& Q, float b3, const SmoothDev& sp,
-                                             J2<O>* t) {
-  const float td = sp.tau_delta, itd = 1.f / td;
-  const float tc = sp.tau_clip_t, itc = 1.f / tc;
-  J2<O> P3 = P * P * P;
-  J2<O> Delta = -(P3 * 4.f + Q * Q * 27.f);
-  J2<O> wneg = jsigm(-Delta * itd);
-  J2<O> wpos = jsigm(Delta * itd);
-  J2<O> tm = jconst<2, O>(0.f), tp[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) tp[k] = jconst<2, O>(0.f);
-  // branches whose weight is below 1e-20 are skipped (reading #34)
-  constexpr float W_SKIP = 1e-20f;
-  if (wneg.v > W_SKIP) {
-    J2<O> spD = jsoftplus(Delta, td, itd);          // s+(Delta)
-    J2<O> Pm = jcbrt(P3 + spD * 0.25f);
-    J2<O> D = jsoftplus(-Delta, td, itd) * (1.f / 108.f);
-    J2<O> sD = jsqrt(D);
-    J2<O> arg = (Q.v >= 0.f) ? (-Q * 0.5f - sD) : (-Q * 0.5f + sD);
-    J2<O> u = jcbrt(arg);
-    J2<O> s;
-    if (fabsf(u.v) > 1e-30f) s = u - Pm * jinv(u) * (1.f / 3.f);
-    else s = u;
-    tm = jsoftclip(s - b3, 0.f, 1.f, tc, itc);
-  }
-  if (wpos.v > W_SKIP) {
-    J2<O> Dp = jsoftplus(Delta, td, itd) * (1.f / 108.f);   // Delta+ / 108
-    J2<O> r6 = Q * Q * 0.25f + Dp;
-    J2<O> rho = jex2(jlg2(r6) * (1.f / 6.f));
-    J2<O> th = jatan2(jsqrt(Dp), -Q * 0.5f);
-#pragma unroll 1
-    for (int k = 0; k < 3; ++k) {
-      J2<O> sk = rho * jcos((th + 6.283185307179586f * (float)k) * (1.f / 3.f)) * 2.f;
-      tp[k] = jsoftclip(sk - b3, 0.f, 1.f, tc, itc);
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    if (wneg.v > W_SKIP && wpos.v > W_SKIP) t[k] = wneg * tm + wpos * tp[k];
-    else if (wneg.v > W_SKIP) t[k] = wneg * tm;
-    else t[k] = wpos * tp[k];
-  }
-  return !(wpos.v > W_SKIP);
-}
+__device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3, const SmoothDev& sp, J2<O>* t);
 
 // XPSQ leaf in its local frame
 template <int O> __device__ CM_XINL void xpsq_eval(const Xpsq& X, const SmoothDev& sp, const float* y, Res<O>& out) {
@@ -595,9 +544,8 @@ template <int O> __device__ CM_XINL void xpsq_eval(const Xpsq& X, const SmoothDe
   } else {
     float Pv = X.gP[0] * w[0] + X.gP[1] * w[1] + X.gP[2] * w[2] + X.P0;
     float Qv = X.gQ[0] * w[0] + X.gQ[1] * w[1] + X.gQ[2] * w[2] + X.Q0;
-    J2<O> P = jvar<2, O>(Pv, 0), Q = jvar<2, O>(Qv, 1);
     J2<O> t2[3];
-    soft_cardano<O>(P, Q, X.b3, sp, t2);
+    soft_cardano_implicit<O>(Pv, Qv, X.b3, sp, t2);
     // chain (P, Q) -> y: grad t = tP gP + tQ gQ; hess = [gP gQ] H [gP gQ]^T
 #pragma unroll
     for (int k = 0; k < 3; ++k) {

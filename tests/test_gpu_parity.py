@@ -164,7 +164,9 @@ def test_manifold_edge_cases(cuda, oracle_mod):
     closed) and tier-dependent NULL outputs."""
     import torch
     from paper_2604_17538_b200 import binding
-    tri = synth.make_shape("tri", None, (np.array([[0, 0, 0], [0.1, 0, 0], [0, 0.1, 0]], np.float32),
+    # (no vertex at the sphere centre: the radial SQ distance is not
+    # differentiable there, DESIGN.md reading #2)
+    tri = synth.make_shape("tri", None, (np.array([[0.01, 0.02, 0.005], [0.1, 0, 0], [0, 0.1, 0]], np.float32),
                                          np.array([[0, 1, 2]], np.int32)))
     sph = synth.make_shape("sph", synth.sq((0.05,) * 3, (1, 1)), None)
     poses = np.zeros((2, 2, 8), np.float32)
