@@ -437,16 +437,19 @@ def c4_scene(n_env: int = 65536, seed: int = 4, n_links: int = 20) -> Scene:
     clr = rng.uniform(-0.004, 0.006, (n_env, n_links))
     lq = random_quats(rng, n_env * n_links).reshape(n_env, n_links, 4)
     poses = np.zeros((n_env, n_links + 1, 8))
-    # object surface support distance along each direction (from samples)
-    for e in range(n_env):
-        qo = quat_from_axis_angle((0, 0, 1), yaw[e])
-        poses[e, 0] = pose_row((0, 0, 0), qo)
-        S = surf @ quat_to_mat(qo).T
-        proj = dirs[e] @ S.T                              # [links, samples]
-        sup = proj.max(axis=1)
-        for i in range(n_links):
-            r = sup[i] + clr[e, i] + link_a[i][0]
-            poses[e, 1 + i] = pose_row(dirs[e, i] * r, lq[e, i])
+    # object surface support distance along each direction (from samples):
+    # support of the yawed cup along u = support of the cup along R(yaw)^T u
+    cy, sy = np.cos(yaw), np.sin(yaw)
+    qo = np.stack([np.cos(yaw / 2), np.zeros(n_env), np.zeros(n_env), np.sin(yaw / 2)], 1)
+    ul = np.stack([cy[:, None] * dirs[..., 0] + sy[:, None] * dirs[..., 1],
+                   -sy[:, None] * dirs[..., 0] + cy[:, None] * dirs[..., 1], dirs[..., 2]], axis=-1)
+    sup = np.empty((n_env, n_links))
+    for lo in range(0, n_env, 4096):
+        sup[lo:lo + 4096] = (ul[lo:lo + 4096] @ surf.T).max(axis=2)
+    r = sup + clr + np.array([a[0] for a in link_a])[None, :]
+    poses[:, 0, 3:7] = qo
+    poses[:, 1:, :3] = dirs * r[..., None]
+    poses[:, 1:, 3:7] = lq
     pairs = np.stack([np.repeat(np.arange(n_env), n_links), np.tile(np.arange(1, n_links + 1), n_env),
                       np.zeros(n_env * n_links), np.tile(np.arange(1, n_links + 1), n_env),
                       np.zeros(n_env * n_links)], axis=1).astype(np.int32)

@@ -140,3 +140,31 @@ def excluded_fraction(rep):
     n = sum(r["n"] for r in rep)
     e = sum(r["excluded"] for r in rep)
     return e / max(n, 1)
+
+
+def gpu_manifold_sampled(scene, pair_idx, tier=2):
+    """Runs the whole scene on the GPU (bench launch configuration) and
+    returns only the rows of pairs `pair_idx`, gathered on the device, in the
+    layout of gpu_manifold (offsets re-based to the gathered rows)."""
+    import torch
+    from paper_2604_17538_b200 import binding
+    S = binding.Scene(scene.shapes, scene.smooth)
+    pairs_t = torch.from_numpy(np.ascontiguousarray(scene.pairs, dtype=np.int32)).cuda()
+    poses_t = torch.from_numpy(np.ascontiguousarray(scene.poses, dtype=np.float32)).cuda()
+    offs = S.manifold_offsets(pairs_t)
+    C = S.manifold_size(scene.pairs)
+    out = S.contact_manifold(pairs_t, offs, C, poses_t, tier)
+    torch.cuda.synchronize()
+    offs_h = offs.cpu().numpy()
+    F = np.array([S.counts(int(a))[2] for a in scene.pairs[pair_idx, 3]])
+    rows = np.concatenate([np.arange(offs_h[i], offs_h[i] + f) for i, f in zip(pair_idx, F)])
+    rows_t = torch.from_numpy(rows).cuda()
+    res = {k: v.index_select(v.dim() - 1, rows_t).cpu().numpy() for k, v in out.items()}
+    del out
+    torch.cuda.empty_cache()
+    # re-based offsets: gathered pair k occupies [new_off[k], new_off[k] + F_k)
+    full_offs = np.zeros(len(scene.pairs), np.int64)
+    full_offs[pair_idx] = np.concatenate([[0], np.cumsum(F)[:-1]])
+    res["offsets"] = full_offs
+    res["C"] = int(len(rows))
+    return res

@@ -218,3 +218,18 @@ def test_expand_jacobian(cuda, oracle_mod):
     ref = osc.contact_manifold()
     Jr = ref["J"].reshape(-1, 36).T
     assert np.allclose(J, Jr, atol=1e-5 * max(1.0, np.abs(Jr).max()))
+
+
+@pytest.mark.parametrize("cfg", ["C4", "C5"])
+def test_manifold_full_size_sampled(cuda, oracle_mod, cfg):
+    """BASELINE.json full sizes in bench.py's launch configuration: C4 (64k
+    envs x 20 links) and C5 (1M envs, all SDF classes in one call); 48 pairs
+    sampled with a seeded generator and compared with the oracle."""
+    sc = synth.c4_scene(65536) if cfg == "C4" else synth.c5_scene(1 << 20)
+    idx = np.sort(np.random.default_rng(8).choice(len(sc.pairs), 48, replace=False))
+    gpu = PT.gpu_manifold_sampled(sc, idx, 2)
+    osc = oracle_mod.OracleScene(sc)
+    nf, rep = PT.manifold_parity(sc, osc, gpu, 2, idx, np.random.default_rng(9), sc.ell)
+    _report("manifold_full_%s" % cfg, rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+    assert PT.excluded_fraction(rep) < 0.01
