@@ -349,99 +349,119 @@ __global__ void __launch_bounds__(CM_MANIFOLD_THREADS, CM_MANIFOLD_MINBLOCKS) k_
         for (int a = 0; a < 3; ++a) out.q[a * C + c] = qv[a];
       }
       if constexpr (TIER >= 2) {
-        // d d_i = g^T J(p_i) (+ (g.e_t) d alpha_bar for edge points); computed
-        // on the fly in both passes (recomputing is cheaper than holding 6x9
-        // values live)
-        auto cand_dd = [&](int i, float* o, float* ew /*unit e_t, edges*/) {
-          const bool isv = i < 3;
-          const int id = isv ? cv[i] : ce[i - 3];
-          const float* bp = isv ? sv + VP * V + id : se + EP * E + id;
-          const float* bn = isv ? sv + VN * V + id : se + EN * E + id;
-          const int sd = isv ? V : E;
-          const float p[3] = {bp[0], bp[sd], bp[2 * sd]};
-          const float g[3] = {bn[0], bn[sd], bn[2 * sd]};
-          gJ(g, p, F, o);
-          if (!isv) {
-            const int vI = __ldg(ed + 2 * id), vII = __ldg(ed + 2 * id + 1);
+        // Tier-2 derivatives in one pass over the 6 candidates.
+        // With g_i = n_i, r = p - t:  d d_i = [g, p x g - tA x g, -(p x g) + tB x g]
+        //   (+ (g.e_t) d alpha_bar for edge points),
+        //   d depth = sum z_i d d_i,
+        //   d n = sum_i c_i n_i (x) d d_i + itmin nbar (x) d depth + sum_i zg_i d n_i,
+        //   c_i = zg_i (-1/tau_min - (1 - gamma_i)/tau_cmp),
+        //   d n_i = [H, -H[p - tA]x, H[p - tB]x - [n]x] (+ H e_t (x) d alpha_bar).
+        // The sums collapse to a few moments of the candidates:
+        //   K = sum c n n^T, L = sum c n (p x n)^T, Hb = sum zg H, M = sum zg H[p]x
+        //   -> d n = [K + Hb, L + K[tA]x + Hb[tA]x - M, -L - K[tB]x + M - Hb[tB]x - [nbar]x]
+        //          + itmin nbar (x) d depth + sum_edges (c ge n + zg H e_t) (x) d alpha_bar
+        float Sg[3] = {0.f, 0.f, 0.f}, Spg[3] = {0.f, 0.f, 0.f}, Se[NDQ];
+        float K[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, Hb[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        float Lm[9], Mm[9], dnE[3][NDQ];
 #pragma unroll
-            for (int a = 0; a < 3; ++a) ew[a] = sv[(VP + a) * V + vII] - sv[(VP + a) * V + vI];
-            const float il = rsqrtf(ew[0] * ew[0] + ew[1] * ew[1] + ew[2] * ew[2]);
-#pragma unroll
-            for (int a = 0; a < 3; ++a) ew[a] *= il;
-            const float ge = g[0] * ew[0] + g[1] * ew[1] + g[2] * ew[2];
-#pragma unroll
-            for (int k = 0; k < NDQ; ++k) o[k] = fmaf(ge, se[(EDAB + k) * E + id], o[k]);
-          }
-        };
-        // d depth = sum z_i d d_i
-        float dd[NDQ];
-#pragma unroll
-        for (int k = 0; k < NDQ; ++k) dd[k] = 0.f;
-#pragma unroll 1
-        for (int i = 0; i < 6; ++i) {
-          float o[NDQ], ew[3];
-          cand_dd(i, o, ew);
-#pragma unroll
-          for (int k = 0; k < NDQ; ++k) dd[k] = fmaf(z[i], o[k], dd[k]);
-        }
-        // d n = sum_i [d(z_i gamma_i) n_i + z_i gamma_i d n_i]
-        //   d(z gamma)_i = z_i gamma_i [-(d d_i - d depth)/tau_min - (1 - gamma_i) d d_i / tau_cmp]
-        //   d n_i = [H, -H[p - tA]x, (-H), H[p - tB]x - [n]x] (+ H e_t d alpha_bar)
-        float dn[3][NDQ];
+        for (int k = 0; k < 9; ++k) { Se[k] = 0.f; Lm[k] = 0.f; Mm[k] = 0.f; }
 #pragma unroll
         for (int a = 0; a < 3; ++a)
 #pragma unroll
-          for (int k = 0; k < NDQ; ++k) dn[a][k] = 0.f;
-#pragma unroll 1
+          for (int k = 0; k < NDQ; ++k) dnE[a][k] = 0.f;
+#pragma unroll
         for (int i = 0; i < 6; ++i) {
           const bool isv = i < 3;
           const int id = isv ? cv[i] : ce[i - 3];
-          float cz[NDQ], ew[3];
-          cand_dd(i, cz, ew);
-          const float zgi = isv ? (i == 0 ? zg[0] : (i == 1 ? zg[1] : zg[2])) : (i == 3 ? zg[3] : (i == 4 ? zg[4] : zg[5]));
-          const float dci = isv ? sv[VD * V + id] : se[ED * E + id];
-          const float gam = sigm(-dci * itcmp);
-          const float c1 = -itmin, c2 = -(1.f - gam) * itcmp;
-#pragma unroll
-          for (int k = 0; k < NDQ; ++k) cz[k] = zgi * fmaf(c1 + c2, cz[k], itmin * dd[k]);
           const float* bp = isv ? sv + VP * V + id : se + EP * E + id;
           const float* bn = isv ? sv + VN * V + id : se + EN * E + id;
           const float* bh = isv ? sv + VH * V + id : se + EH * E + id;
           const int sd = isv ? V : E;
           const float p[3] = {bp[0], bp[sd], bp[2 * sd]};
-          const float nn[3] = {bn[0], bn[sd], bn[2 * sd]};
-          const float h6[6] = {bh[0], bh[sd], bh[2 * sd], bh[3 * sd], bh[4 * sd], bh[5 * sd]};
-          const float H[3][3] = {{h6[0], h6[1], h6[2]}, {h6[1], h6[3], h6[4]}, {h6[2], h6[4], h6[5]}};
-          const float ra[3] = {p[0] - F.tA[0], p[1] - F.tA[1], p[2] - F.tA[2]};
-          const float rb[3] = {p[0] - F.tB[0], p[1] - F.tB[1], p[2] - F.tB[2]};
-          const float w = zgi;
+          const float n[3] = {bn[0], bn[sd], bn[2 * sd]};
+          const float h[6] = {bh[0], bh[sd], bh[2 * sd], bh[3 * sd], bh[4 * sd], bh[5 * sd]};
+          const float gam = sigm(-dc[i] * itcmp);
+          const float w = zg[i];
+          const float ci = w * (-itmin - (1.f - gam) * itcmp);
+          const float pxn[3] = {p[1] * n[2] - p[2] * n[1], p[2] * n[0] - p[0] * n[2], p[0] * n[1] - p[1] * n[0]};
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
-            // H [r]x row a: (H_a1 r2 - H_a2 r1, H_a2 r0 - H_a0 r2, H_a0 r1 - H_a1 r0)
-            const float hka0 = H[a][1] * ra[2] - H[a][2] * ra[1];
-            const float hka1 = H[a][2] * ra[0] - H[a][0] * ra[2];
-            const float hka2 = H[a][0] * ra[1] - H[a][1] * ra[0];
-            const float hkb0 = H[a][1] * rb[2] - H[a][2] * rb[1];
-            const float hkb1 = H[a][2] * rb[0] - H[a][0] * rb[2];
-            const float hkb2 = H[a][0] * rb[1] - H[a][1] * rb[0];
-            // [n]x row a
-            const float nk0 = a == 0 ? 0.f : (a == 1 ? nn[2] : -nn[1]);
-            const float nk1 = a == 0 ? -nn[2] : (a == 1 ? 0.f : nn[0]);
-            const float nk2 = a == 0 ? nn[1] : (a == 1 ? -nn[0] : 0.f);
-            const float dni[NDQ] = {H[a][0], H[a][1], H[a][2], -hka0, -hka1, -hka2, hkb0 - nk0, hkb1 - nk1, hkb2 - nk2};
+            Sg[a] = fmaf(z[i], n[a], Sg[a]);
+            Spg[a] = fmaf(z[i], pxn[a], Spg[a]);
+          }
+          const float cn[3] = {ci * n[0], ci * n[1], ci * n[2]};
+          K[0] = fmaf(cn[0], n[0], K[0]); K[1] = fmaf(cn[0], n[1], K[1]); K[2] = fmaf(cn[0], n[2], K[2]);
+          K[3] = fmaf(cn[1], n[1], K[3]); K[4] = fmaf(cn[1], n[2], K[4]); K[5] = fmaf(cn[2], n[2], K[5]);
 #pragma unroll
-            for (int k = 0; k < NDQ; ++k) dn[a][k] = fmaf(nn[a], cz[k], fmaf(w, dni[k], dn[a][k]));
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) Lm[a * 3 + b] = fmaf(cn[a], pxn[b], Lm[a * 3 + b]);
+#pragma unroll
+          for (int k = 0; k < 6; ++k) Hb[k] = fmaf(w, h[k], Hb[k]);
+          const float H[3][3] = {{h[0], h[1], h[2]}, {h[1], h[3], h[4]}, {h[2], h[4], h[5]}};
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            // (H [p]x) row a
+            Mm[a * 3 + 0] = fmaf(w, H[a][1] * p[2] - H[a][2] * p[1], Mm[a * 3 + 0]);
+            Mm[a * 3 + 1] = fmaf(w, H[a][2] * p[0] - H[a][0] * p[2], Mm[a * 3 + 1]);
+            Mm[a * 3 + 2] = fmaf(w, H[a][0] * p[1] - H[a][1] * p[0], Mm[a * 3 + 2]);
           }
           if (!isv) {
-            float he[3];
+            // sliding along the edge: e_t (world, unit) and d alpha_bar
+            const int vI = __ldg(ed + 2 * id), vII = __ldg(ed + 2 * id + 1);
+            float ew[3];
 #pragma unroll
-            for (int a = 0; a < 3; ++a) he[a] = (H[a][0] * ew[0] + H[a][1] * ew[1] + H[a][2] * ew[2]) * w;
+            for (int a = 0; a < 3; ++a) ew[a] = sv[(VP + a) * V + vII] - sv[(VP + a) * V + vI];
+            const float il = rsqrtf(ew[0] * ew[0] + ew[1] * ew[1] + ew[2] * ew[2]);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) ew[a] *= il;
+            const float ge = n[0] * ew[0] + n[1] * ew[1] + n[2] * ew[2];
+            float u[3];   // c ge n + zg H e_t
+#pragma unroll
+            for (int a = 0; a < 3; ++a) u[a] = fmaf(ci * ge, n[a], w * (H[a][0] * ew[0] + H[a][1] * ew[1] + H[a][2] * ew[2]));
+            const float zge = z[i] * ge;
 #pragma unroll
             for (int k = 0; k < NDQ; ++k) {
               const float dk = se[(EDAB + k) * E + id];
+              Se[k] = fmaf(zge, dk, Se[k]);
 #pragma unroll
-              for (int a = 0; a < 3; ++a) dn[a][k] = fmaf(he[a], dk, dn[a][k]);
+              for (int a = 0; a < 3; ++a) dnE[a][k] = fmaf(u[a], dk, dnE[a][k]);
             }
+          }
+        }
+        // d depth = [Sg, Spg - tA x Sg, -Spg + tB x Sg] + Se
+        const float* tA = F.tA;
+        const float* tB = F.tB;
+        float dd[NDQ];
+        dd[0] = Sg[0] + Se[0]; dd[1] = Sg[1] + Se[1]; dd[2] = Sg[2] + Se[2];
+        dd[3] = Spg[0] - (tA[1] * Sg[2] - tA[2] * Sg[1]) + Se[3];
+        dd[4] = Spg[1] - (tA[2] * Sg[0] - tA[0] * Sg[2]) + Se[4];
+        dd[5] = Spg[2] - (tA[0] * Sg[1] - tA[1] * Sg[0]) + Se[5];
+        dd[6] = -Spg[0] + (tB[1] * Sg[2] - tB[2] * Sg[1]) + Se[6];
+        dd[7] = -Spg[1] + (tB[2] * Sg[0] - tB[0] * Sg[2]) + Se[7];
+        dd[8] = -Spg[2] + (tB[0] * Sg[1] - tB[1] * Sg[0]) + Se[8];
+        // d n rows
+        const float Ks[3][3] = {{K[0], K[1], K[2]}, {K[1], K[3], K[4]}, {K[2], K[4], K[5]}};
+        const float Hs[3][3] = {{Hb[0], Hb[1], Hb[2]}, {Hb[1], Hb[3], Hb[4]}, {Hb[2], Hb[4], Hb[5]}};
+        float dn[3][NDQ];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const float KH[3] = {Ks[a][0] + Hs[a][0], Ks[a][1] + Hs[a][1], Ks[a][2] + Hs[a][2]};
+          // (X [t]x) row a for X = K + Hb, t = tA and tB
+          const float xA[3] = {KH[1] * tA[2] - KH[2] * tA[1], KH[2] * tA[0] - KH[0] * tA[2], KH[0] * tA[1] - KH[1] * tA[0]};
+          const float KtB[3] = {Ks[a][1] * tB[2] - Ks[a][2] * tB[1], Ks[a][2] * tB[0] - Ks[a][0] * tB[2],
+                                Ks[a][0] * tB[1] - Ks[a][1] * tB[0]};
+          const float HtB[3] = {Hs[a][1] * tB[2] - Hs[a][2] * tB[1], Hs[a][2] * tB[0] - Hs[a][0] * tB[2],
+                                Hs[a][0] * tB[1] - Hs[a][1] * tB[0]};
+          // [nbar]x row a
+          const float nk[3] = {a == 0 ? 0.f : (a == 1 ? nrm[2] : -nrm[1]), a == 0 ? -nrm[2] : (a == 1 ? 0.f : nrm[0]),
+                               a == 0 ? nrm[1] : (a == 1 ? -nrm[0] : 0.f)};
+          const float nb = nrm[a] * itmin;
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            dn[a][b] = KH[b] + nb * dd[b] + dnE[a][b];
+            dn[a][3 + b] = Lm[a * 3 + b] + xA[b] - Mm[a * 3 + b] + nb * dd[3 + b] + dnE[a][3 + b];
+            dn[a][6 + b] = -Lm[a * 3 + b] - KtB[b] + Mm[a * 3 + b] - HtB[b] - nk[b] + nb * dd[6 + b] + dnE[a][6 + b];
           }
         }
         // store: q order (tA 0-2, thetaA 3-5, tB 6-8 = -tA, thetaB 9-11)
