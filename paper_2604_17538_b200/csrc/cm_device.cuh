@@ -1046,7 +1046,10 @@ __device__ __forceinline__ void fold_level(Acc<O>& a0, Acc<O>& a1, Acc<O>& a2, i
 }
 
 // phi, grad, hess of shape `sh` at the body-frame point x
-template <int O, int XP> __device__ CM_SINL void eval_shape(const SceneDev& S, const ShapeRec& sh, const float* x, Res<O>& out) {
+// FLAT: every boolean node of the shape sits at the root (nesting depth <= 1),
+// so one accumulator level suffices (fewer live registers)
+template <int O, int XP, bool FLAT = false>
+__device__ CM_SINL void eval_shape(const SceneDev& S, const ShapeRec& sh, const float* x, Res<O>& out) {
   const float tau = S.sp.tau_min, itau = 1.f / tau, itl = LOG2E * itau;
   if (sh.prog_len == 1) {  // single leaf: no accumulator needed
     leaf_eval<O, XP>(S, S.prog[sh.prog_begin].idx, x, out);
@@ -1059,7 +1062,7 @@ template <int O, int XP> __device__ CM_SINL void eval_shape(const SceneDev& S, c
     const Instr in = prog[pc];
     if (in.op == OP_BEGIN) {
       ++lvl;
-      if (lvl == 0) acc_init(a0);
+      if (FLAT || lvl == 0) acc_init(a0);
       else if (lvl == 1) acc_init(a1);
       else acc_init(a2);
       continue;
@@ -1068,12 +1071,13 @@ template <int O, int XP> __device__ CM_SINL void eval_shape(const SceneDev& S, c
     if (in.op == OP_LEAF) {
       leaf_eval<O, XP>(S, in.idx, x, r);
     } else {
-      if (lvl == 0) acc_final(a0, in.out_sign, tau, itau, r);
+      if (FLAT || lvl == 0) acc_final(a0, in.out_sign, tau, itau, r);
       else if (lvl == 1) acc_final(a1, in.out_sign, tau, itau, r);
       else acc_final(a2, in.out_sign, tau, itau, r);
       --lvl;
     }
     if (lvl < 0) out = r;
+    else if (FLAT) acc_fold(a0, in.child_sign, r, itl, itau);
     else fold_level(a0, a1, a2, lvl, in.child_sign, r, itl, itau);
   }
 }

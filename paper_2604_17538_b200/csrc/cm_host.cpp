@@ -331,8 +331,8 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
       id.t[0] = id.t[1] = id.t[2] = 0.0;
       if (!emit(0, 1.f, id, 0)) { delete sc; return fail(CM_ERR_UNSUPPORTED, "shape " + std::to_string(s) + ": " + err); }
       r.has_sdf = 1;
-      r.uses_xpsq = xclass;
-      sc->class_mask |= 1 << xclass;
+      r.uses_xpsq = (xclass == 0 && max_depth > 1) ? 3 : xclass;
+      sc->class_mask |= 1 << r.uses_xpsq;
     }
     r.prog_len = (int32_t)prog.size() - r.prog_begin;
 

@@ -60,7 +60,10 @@ struct Xpsq {
 
 struct ShapeRec {
   int32_t prog_begin, prog_len;
-  int32_t has_sdf, uses_xpsq;   // uses_xpsq: SDF class 0 / 1 / 2 (see cm_device.cuh leaf_eval)
+  // SDF class (one kernel instantiation each): 0 SQ family with nesting depth
+  // <= 1, 1 constant-schedule XPSQ, 2 varying-schedule XPSQ, 3 SQ family
+  // with nested booleans
+  int32_t has_sdf, uses_xpsq;
   int32_t V, E, F;
   int32_t v_off, e_off, f_off;   // into verts (x3), edges (x2), faces / face_edges (x3)
   int32_t pad;

@@ -83,20 +83,29 @@ constexpr int NDQ = 9;
 #define CM_PHASE_TIMING 0
 #endif
 #if CM_PHASE_TIMING
-__device__ unsigned long long g_phase_cycles[3][4];
+__device__ unsigned long long g_phase_cycles[4][5];
 extern "C" int cm_debug_phase_cycles(unsigned long long* out) {
   return (int)cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles));
 }
 #endif
 
-template <int TIER, int XP>
 #ifndef CM_MANIFOLD_THREADS
 #define CM_MANIFOLD_THREADS 128
+#endif
+#ifndef CM_MANIFOLD_MINBLOCKS_FLAT
+#define CM_MANIFOLD_MINBLOCKS_FLAT 3
 #endif
 #ifndef CM_MANIFOLD_MINBLOCKS
 #define CM_MANIFOLD_MINBLOCKS 2
 #endif
-__global__ void __launch_bounds__(CM_MANIFOLD_THREADS, CM_MANIFOLD_MINBLOCKS) k_contact_manifold(SceneDev S, const int32_t* __restrict__ pairs,
+// CLS: SDF class (cm_internal.h ShapeRec); XPM: XPSQ mode of leaf_eval;
+// flat SQ-family shapes get a tighter register budget (3 CTAs / SM)
+template <int CLS> struct ClsTraits {
+  static constexpr int XPM = CLS == 3 ? 0 : CLS;
+  static constexpr bool FLAT = CLS == 0;
+};
+template <int TIER, int XP, int MB>
+__global__ void __launch_bounds__(CM_MANIFOLD_THREADS, MB) k_contact_manifold(SceneDev S, const int32_t* __restrict__ pairs,
                                                           int64_t n_pairs, const int64_t* __restrict__ offsets,
                                                           const float* __restrict__ poses, int32_t n_slot,
                                                           cm_manifold_out out, int64_t C, int xp_filter,
@@ -117,7 +126,7 @@ __global__ void __launch_bounds__(CM_MANIFOLD_THREADS, CM_MANIFOLD_MINBLOCKS) k_
 #define CM_PT(k)                                                                             \
   if (threadIdx.x == 0) {                                                                    \
     long long t_now = clock64();                                                             \
-    if (k > 0) atomicAdd(&g_phase_cycles[XP][k - 1], (unsigned long long)(t_now - t_mark)); \
+    if (k > 0 || t_mark) atomicAdd(&g_phase_cycles[XP][k > 0 ? k - 1 : 4], (unsigned long long)(t_now - t_mark)); \
     t_mark = t_now;                                                                          \
   }
 #else
@@ -160,7 +169,7 @@ __global__ void __launch_bounds__(CM_MANIFOLD_THREADS, CM_MANIFOLD_MINBLOCKS) k_
         pw[i] = F.RA[i * 3] * x[0] + F.RA[i * 3 + 1] * x[1] + F.RA[i * 3 + 2] * x[2] + F.tA[i];
       }
       Res<OV> r;
-      eval_shape<OV, XP>(S, SB, xb, r);
+      eval_shape<OV, ClsTraits<XP>::XPM, ClsTraits<XP>::FLAT>(S, SB, xb, r);
       float n[3];
       rot_vec(F.RB, r.g, n);
 #pragma unroll
@@ -209,7 +218,7 @@ __global__ void __launch_bounds__(CM_MANIFOLD_THREADS, CM_MANIFOLD_MINBLOCKS) k_
         } else {
           const float xb[3] = {fmaf(al, eb[0], xI[0]), fmaf(al, eb[1], xI[1]), fmaf(al, eb[2], xI[2])};
           Res<OT> r;
-          eval_shape<OT, XP>(S, SB, xb, r);
+          eval_shape<OT, ClsTraits<XP>::XPM, ClsTraits<XP>::FLAT>(S, SB, xb, r);
           phi = r.v;
           if constexpr (TIER >= 2) rot_vec(F.RB, r.g, g);
         }
@@ -264,7 +273,7 @@ __global__ void __launch_bounds__(CM_MANIFOLD_THREADS, CM_MANIFOLD_MINBLOCKS) k_
         pw[i] = fmaf(ab, ew[i], sv[(VP + i) * V + vI]);
       }
       Res<OV> r;
-      eval_shape<OV, XP>(S, SB, xb, r);
+      eval_shape<OV, ClsTraits<XP>::XPM, ClsTraits<XP>::FLAT>(S, SB, xb, r);
       float n[3];
       rot_vec(F.RB, r.g, n);
 #pragma unroll
@@ -507,17 +516,14 @@ int manifold_max_smem_bytes() {
   return m;
 }
 
-template <int TIER, int XP>
-static int launch_manifold_t(const SceneDev& s, int xp_filter, int max_V, int max_E, const int32_t* pairs,
+template <int TIER, int XP, int MB>
+static int launch_manifold_v(const SceneDev& s, int xp_filter, bool use_smem, int64_t need, const int32_t* pairs,
                              int64_t n_pairs, const int64_t* offsets, const float* poses, int32_t n_slot,
                              const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats,
                              cudaStream_t st) {
   const int threads = CM_MANIFOLD_THREADS;
-  const int64_t need = manifold_smem_floats(max_V, max_E, TIER) * 4;
-  const int static_smem = (int)(sizeof(PairFrame) + 2 * sizeof(ShapeRec));
-  const bool use_smem = need <= kSmemBudget && need + static_smem + 1024 <= manifold_max_smem_bytes();
   int smem = use_smem ? (int)need : 0;
-  auto kern = k_contact_manifold<TIER, XP>;
+  auto kern = k_contact_manifold<TIER, XP, MB>;
   static int configured = 0;
   if (smem > configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -546,6 +552,27 @@ static int launch_manifold_t(const SceneDev& s, int xp_filter, int max_V, int ma
   return check_launch("k_contact_manifold");
 }
 
+template <int TIER, int XP>
+static int launch_manifold_t(const SceneDev& s, int xp_filter, int max_V, int max_E, const int32_t* pairs,
+                             int64_t n_pairs, const int64_t* offsets, const float* poses, int32_t n_slot,
+                             const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats,
+                             cudaStream_t st) {
+  const int64_t need = manifold_smem_floats(max_V, max_E, TIER) * 4;
+  const int static_smem = (int)(sizeof(PairFrame) + 2 * sizeof(ShapeRec));
+  const bool use_smem = need <= kSmemBudget && need + static_smem + 1024 <= manifold_max_smem_bytes();
+  // flat SQ-family SDFs: a 3-CTA/SM register budget pays off only when three
+  // pairs' state also fits in shared memory (else the tighter budget just spills)
+  if constexpr (XP == 0) {
+    const bool hi = !use_smem || 3 * (need + static_smem + 1024) <= 228 * 1024;
+    if (hi)
+      return launch_manifold_v<TIER, XP, CM_MANIFOLD_MINBLOCKS_FLAT>(s, xp_filter, use_smem, need, pairs, n_pairs,
+                                                                     offsets, poses, n_slot, out, C, scratch,
+                                                                     scratch_floats, st);
+  }
+  return launch_manifold_v<TIER, XP, CM_MANIFOLD_MINBLOCKS>(s, xp_filter, use_smem, need, pairs, n_pairs, offsets,
+                                                            poses, n_slot, out, C, scratch, scratch_floats, st);
+}
+
 int launch_manifold(const SceneDev& s, int class_mask, int max_V, int max_E, const int32_t* pairs,
                     int64_t n_pairs, const int64_t* offsets, const float* poses, int32_t n_slot, uint32_t flags,
                     const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats, void* stream) {
@@ -562,6 +589,7 @@ int launch_manifold(const SceneDev& s, int class_mask, int max_V, int max_E, con
   if (class_mask & 1) rc = CM_T(0);
   if (!rc && (class_mask & 2)) rc = CM_T(1);
   if (!rc && (class_mask & 4)) rc = CM_T(2);
+  if (!rc && (class_mask & 8)) rc = CM_T(3);
 #undef CM_T
 #undef CM_L
   return rc;

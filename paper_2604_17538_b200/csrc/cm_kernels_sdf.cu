@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(256) k_sdf_eval(SceneDev S, const int32_t* __r
     float y[3];
     to_local(R, t, x, y);
     Res<O> r;
-    eval_shape<O, XP>(S, sh, y, r);
+    eval_shape<O, XP == 3 ? 0 : XP, XP == 0>(S, sh, y, r);
     d[n] = r.v;
     if constexpr (O >= 1) {
       float g[3];
@@ -165,6 +165,9 @@ int launch_sdf_eval(const SceneDev& s, int class_mask, const int32_t* ids, const
     rc = dispatch_sdf<1>(s, multi ? 1 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, st);
   if (!rc && (class_mask & 4))
     rc = dispatch_sdf<2>(s, multi ? 2 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, st);
+  // nested SQ-family shapes: general interpreter, no XPSQ code
+  if (!rc && (class_mask & 8))
+    rc = dispatch_sdf<3>(s, multi ? 3 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, st);
   return rc;
 }
 

@@ -15,14 +15,14 @@ pairs = torch.from_numpy(sc.pairs).cuda(); poses = torch.from_numpy(sc.poses).cu
 offs = S.manifold_offsets(pairs); Cn = S.manifold_size(sc.pairs)
 out = S.alloc_manifold(Cn, 2, pairs.device)
 L = binding.lib()
-buf = (C.c_ulonglong * 12)()
+buf = (C.c_ulonglong * 20)()
 L.cm_debug_phase_cycles(buf)
-base = np.array(buf[:]).reshape(3, 4)
+base = np.array(buf[:]).reshape(4, 5)
 S.contact_manifold(pairs, offs, Cn, poses, 2, out); torch.cuda.synchronize()
 L.cm_debug_phase_cycles(buf)
-cyc = np.array(buf[:]).reshape(3, 4) - base
-names = ["vertices", "traces", "midpoints", "faces"]
-for k, nm in enumerate(["SQ-family", "XPSQ", "XPSQ-vary"]):
+cyc = np.array(buf[:]).reshape(4, 5) - base
+names = ["vertices", "traces", "midpoints", "faces", "prologue"]
+for k, nm in enumerate(["SQ-flat", "XPSQ", "XPSQ-vary", "SQ-nested"]):
     t = cyc[k].sum()
     if t:
-        print(wl, nm, " ".join("%s %.1f%%" % (names[i], 100 * cyc[k][i] / t) for i in range(4)), "total Gcyc %.2f" % (t / 1e9))
+        print(wl, nm, " ".join("%s %.1f%%" % (names[i], 100 * cyc[k][i] / t) for i in range(5)), "total Gcyc %.2f" % (t / 1e9))
