@@ -184,6 +184,18 @@ int cm_sdf_eval(const cm_scene* scene, const int32_t* shape_ids, const float* po
 #define CM_TIER1 1u
 #define CM_TIER2 2u
 #define CM_TIER_MASK 3u
+/* CM_FULL_MODE: one contact per vertex and per edge of the sampled
+ * surface (V + E rows, vertices first, then edges in cm_shape_topology order)
+ * instead of one fused contact per face.  Row i is candidate i itself: point,
+ * raw normal grad phi, depth phi, W = gamma = sigma(-phi/tau_cmp), q = gamma p
+ * (J = gamma J_i), dom = 0 vertex / 1 edge point; tier-2 derivatives of
+ * phi and grad phi.
+ * CM_TWO_SIDED: the manifold of A sampled against B's SDF followed by
+ * the manifold of B sampled against A's SDF (both shapes of every pair need an
+ * SDF and a sampled surface); derivative columns of both halves are in the
+ * pair's own order (t_A, theta_A, t_B, theta_B). */
+#define CM_FULL_MODE 4u
+#define CM_TWO_SIDED 8u
 
 typedef struct cm_manifold_out {
   float* point;
@@ -196,25 +208,29 @@ typedef struct cm_manifold_out {
   int8_t* dom;
 } cm_manifold_out;
 
-/* Number of contacts for a pair list given on the HOST (shapeA of each pair,
- * stride `stride` int32 between entries). */
-int cm_manifold_size(const cm_scene* scene, const int32_t* shapeA_host, int64_t n_pairs, int64_t stride,
+/* Number of contacts of a pair list given on the HOST (pairs_host [n,5]) for
+ * the mode bits of `flags` (CM_FULL_MODE, CM_TWO_SIDED); also validates that
+ * every pair's sampled shape has a surface and its SDF shape an SDF (both, on
+ * both shapes, with CM_TWO_SIDED) -> CM_ERR_INVALID otherwise. */
+int cm_manifold_size(const cm_scene* scene, const int32_t* pairs_host, int64_t n_pairs, uint32_t flags,
                      int64_t* n_contacts);
-/* Device exclusive scan of F(shapeA_i) over the pairs -> offsets[n_pairs]
- * (device int64).  Uses `workspace` of cm_manifold_offsets_workspace() bytes
- * (device, caller-owned). */
+/* Device exclusive scan of the per-pair contact counts (same mode bits) ->
+ * offsets[n_pairs] (device int64).  Uses `workspace` of
+ * cm_manifold_offsets_workspace() bytes (device, caller-owned). */
 int64_t cm_manifold_offsets_workspace(int64_t n_pairs);
-int cm_manifold_offsets(const cm_scene* scene, const int32_t* pairs, int64_t n_pairs, int64_t* offsets,
+int cm_manifold_offsets(const cm_scene* scene, const int32_t* pairs, int64_t n_pairs, uint32_t flags, int64_t* offsets,
                         void* workspace, int64_t workspace_bytes, void* stream);
 int cm_contact_manifold(const cm_scene* scene, const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,
                         const float* poses, int64_t n_env, int32_t n_slot, uint32_t flags,
                         const cm_manifold_out* out, int64_t n_contacts, void* stream);
 
 /* Expands the compact Jacobian: J[36*C] ([r*12+c], device) from W, q and the
- * pairs' poses. */
+ * pairs' poses, for the layout of the same mode bits (`flags`).  Rows of the
+ * transposed half of CM_TWO_SIDED carry the opposite sign (their contact
+ * velocity is v_B - v_A). */
 int cm_expand_jacobian(const cm_scene* scene, const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,
-                       const float* poses, int64_t n_env, int32_t n_slot, const float* W, const float* q,
-                       int64_t n_contacts, float* J, void* stream);
+                       const float* poses, int64_t n_env, int32_t n_slot, uint32_t flags, const float* W,
+                       const float* q, int64_t n_contacts, float* J, void* stream);
 
 /* Number of kernel launches the library issued since scene creation (all
  * scenes, this process) — instrumentation for bench.py's gpu_launches. */

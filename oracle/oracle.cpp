@@ -689,8 +689,12 @@ int ora_sdf_eval(void* s, const int* shape_ids, const double* poses, const doubl
 }
 
 // ---- contact manifold -------------------------------------------
-// One-sided reduced manifold: shape A (pairs[5i+3]) is the sampled mesh, shape
-// B (pairs[5i+4]) the SDF.  pairs[i] = {env, slotA, slotB, shapeA,
+// Reduced manifold: shape A (pairs[5i+3]) is the sampled mesh, shape B
+// (pairs[5i+4]) the SDF.  mode bit 4: full mode (one contact
+// per vertex, then per edge in sorted-(lo,hi) order: point, raw normal, depth
+// phi, W = gamma, q = gamma p, dom = 0 vertex / 1 edge); mode bit 8:
+// two-sided (then B sampled against A's SDF; derivative columns stay in
+// the pair's (A, B) order, J rows of that half are v_B - v_A).  pairs[i] = {env, slotA, slotB, shapeA,
 // shapeB}; poses[(env*n_slot + slot)*8 + ...] = t(3), q(w,x,y,z), pad.
 // Contacts of pair i occupy rows [off_i, off_i + F_A) in input pair order.
 // Per contact c (row-major arrays):
@@ -701,35 +705,47 @@ int ora_sdf_eval(void* s, const int* shape_ids, const double* poses, const doubl
 int ora_contact_manifold(void* s, const int* pairs, long n_pairs, const double* poses, long n_env, int n_slot,
                          double* point, double* normal, double* depth, double* W, double* qv, double* ddepth,
                          double* dnormal, int* dom, double* J, double* zout, double* dcand, double* gout,
-                         int n_threads) {
+                         int mode, int n_threads) {
   Scene* sc = (Scene*)s;
   const Smooth sp = sc->sp;
   (void)n_env;
+  const bool full = (mode & 4) != 0, two = (mode & 8) != 0;
+  auto count = [&](int shape) { const Mesh& m = sc->shapes[shape].mesh; return full ? (long)m.V + m.E : (long)m.F; };
   std::vector<long> off(n_pairs + 1, 0);
-  for (long i = 0; i < n_pairs; ++i) off[i + 1] = off[i] + sc->shapes[pairs[5 * i + 3]].mesh.F;
+  for (long i = 0; i < n_pairs; ++i)
+    off[i + 1] = off[i] + count(pairs[5 * i + 3]) + (two ? count(pairs[5 * i + 4]) : 0);
 #ifdef _OPENMP
   if (n_threads > 0) omp_set_num_threads(n_threads);
 #endif
 #pragma omp parallel for schedule(dynamic, 1)
   for (long pi = 0; pi < n_pairs; ++pi) {
+   long row0 = off[pi];
+   for (int side = 0; side < (two ? 2 : 1); ++side) {
+    // "A" below is the sampled body of this side, "B" the SDF body
     const int* pr = pairs + 5 * pi;
-    const Shape& SA = sc->shapes[pr[3]];
-    const Shape& SB = sc->shapes[pr[4]];
+    const Shape& SA = sc->shapes[pr[3 + side]];
+    const Shape& SB = sc->shapes[pr[4 - side]];
     const Mesh& m = SA.mesh;
-    const double* pa = poses + 8 * ((long)pr[0] * n_slot + pr[1]);
-    const double* pb = poses + 8 * ((long)pr[0] * n_slot + pr[2]);
+    const double* pa = poses + 8 * ((long)pr[0] * n_slot + pr[1 + side]);
+    const double* pb = poses + 8 * ((long)pr[0] * n_slot + pr[2 - side]);
     double RA[9], RB[9], tA[3] = {pa[0], pa[1], pa[2]}, tB[3] = {pb[0], pb[1], pb[2]};
     double qa[4] = {pa[3], pa[4], pa[5], pa[6]}, qb[4] = {pb[3], pb[4], pb[5], pb[6]};
     quat_to_R(qa, RA); quat_to_R(qb, RB);
 
-    // q-jet poses (first order, 12 seeds)
+    // q-jet poses (first order, 12 seeds): q = (dt, dtheta) of the pair's
+    // first body, then of its second body, whichever plays the sampled role
+    const int sA = side ? 6 : 0, sB = side ? 0 : 6;
     D12 dtA[3], wA[3], dtB[3], wB[3];
     for (int i = 0; i < 3; ++i) {
-      dtA[i] = D12(0.0); dtA[i].d[i] = 1.0;
-      wA[i] = D12(0.0); wA[i].d[3 + i] = 1.0;
-      dtB[i] = D12(0.0); dtB[i].d[6 + i] = 1.0;
-      wB[i] = D12(0.0); wB[i].d[9 + i] = 1.0;
+      dtA[i] = D12(0.0); dtA[i].d[sA + i] = 1.0;
+      wA[i] = D12(0.0); wA[i].d[sA + 3 + i] = 1.0;
+      dtB[i] = D12(0.0); dtB[i].d[sB + i] = 1.0;
+      wB[i] = D12(0.0); wB[i].d[sB + 3 + i] = 1.0;
     }
+    // J_i rows are v_sampled - v_sdf; written in the pair's (A, B) columns
+    const double sg = side ? -1.0 : 1.0;
+    const double* tP = side ? tB : tA;   // the pair's first body translation
+    const double* tQ = side ? tA : tB;   // the pair's second body translation
     D12 RAq[9], tAq[3], RBq[9], tBq[3];
     perturbed_pose(RA, tA, dtA, wA, RAq, tAq);
     perturbed_pose(RB, tB, dtB, wB, RBq, tBq);
@@ -798,9 +814,49 @@ int ora_contact_manifold(void* s, const int* pairs, long n_pairs, const double* 
       for (int i = 0; i < 3; ++i) ep[3 * e + i] = pI[i] + ab * et[i];
       cand(&ep[3 * e], ed[e], &en[3 * e]);
     }
+    if (full) {
+      // one contact per vertex, then per edge in sorted (lo, hi) order
+      std::vector<int> eo(m.E);
+      for (int e = 0; e < m.E; ++e) eo[e] = e;
+      std::sort(eo.begin(), eo.end(), [&](int a, int b) {
+        return std::make_pair(m.e[2 * a], m.e[2 * a + 1]) < std::make_pair(m.e[2 * b], m.e[2 * b + 1]); });
+      for (int k = 0; k < m.V + m.E; ++k) {
+        const bool isv = k < m.V;
+        const int id = isv ? k : eo[k - m.V];
+        const D12* P = isv ? &vp[3 * id] : &ep[3 * id];
+        const D12* N = isv ? &vn[3 * id] : &en[3 * id];
+        const D12& dk = isv ? vd[id] : ed[id];
+        const long c = row0 + k;
+        const double gam = val(sigmoid(-dk / sp.tau_cmp));
+        for (int a = 0; a < 3; ++a) {
+          point[3 * c + a] = P[a].v;
+          normal[3 * c + a] = N[a].v;
+          qv[3 * c + a] = gam * P[a].v;
+          for (int j = 0; j < 12; ++j) dnormal[36 * c + a * 12 + j] = N[a].d[j];
+        }
+        depth[c] = dk.v; W[c] = gam; dom[c] = isv ? 0 : 1;
+        for (int j = 0; j < 12; ++j) ddepth[12 * c + j] = dk.d[j];
+        double ra[3], rb[3];
+        for (int a = 0; a < 3; ++a) { ra[a] = P[a].v - tP[a]; rb[a] = P[a].v - tQ[a]; }
+        double Ka[9] = {0, -ra[2], ra[1], ra[2], 0, -ra[0], -ra[1], ra[0], 0};
+        double Kb[9] = {0, -rb[2], rb[1], rb[2], 0, -rb[0], -rb[1], rb[0], 0};
+        for (int a = 0; a < 36; ++a) J[36 * c + a] = 0.0;
+        for (int r = 0; r < 3; ++r) {
+          J[36 * c + r * 12 + r] += sg * gam;
+          J[36 * c + r * 12 + 6 + r] -= sg * gam;
+          for (int k2 = 0; k2 < 3; ++k2) {
+            J[36 * c + r * 12 + 3 + k2] -= sg * gam * Ka[r * 3 + k2];
+            J[36 * c + r * 12 + 9 + k2] += sg * gam * Kb[r * 3 + k2];
+          }
+        }
+        for (int i = 0; i < 6; ++i) { zout[6 * c + i] = 0.0; dcand[6 * c + i] = dk.v; gout[6 * c + i] = gam; }
+      }
+      row0 += m.V + m.E;
+      continue;
+    }
     // per-face fusion
     for (int f = 0; f < m.F; ++f) {
-      long c = off[pi] + f;
+      long c = row0 + f;
       const D12* P6[6]; D12 dd[6]; const D12* N6[6];
       for (int k = 0; k < 3; ++k) {
         int vi = m.f[3 * f + k];
@@ -830,11 +886,12 @@ int ora_contact_manifold(void* s, const int* pairs, long n_pairs, const double* 
       int im = 0;
       for (int i = 1; i < 6; ++i) if (val(dd[i]) < val(dd[im])) im = i;
       // literal fused contact Jacobian J = sum z_i gamma_i J_i, J_i = [I, -[p-tA]x, -I, [p-tB]x]
+      // (in the pair's (A, B) columns; the transposed side has the opposite sign)
       double Jc[36] = {0};
       for (int i = 0; i < 6; ++i) {
-        double zg = val(z[i]) * val(gam[i]);
+        double zg = sg * val(z[i]) * val(gam[i]);
         double ra[3], rb[3];
-        for (int k = 0; k < 3; ++k) { ra[k] = P6[i][k].v - tA[k]; rb[k] = P6[i][k].v - tB[k]; }
+        for (int k = 0; k < 3; ++k) { ra[k] = P6[i][k].v - tP[k]; rb[k] = P6[i][k].v - tQ[k]; }
         double Ka[9] = {0, -ra[2], ra[1], ra[2], 0, -ra[0], -ra[1], ra[0], 0};
         double Kb[9] = {0, -rb[2], rb[1], rb[2], 0, -rb[0], -rb[1], rb[0], 0};
         for (int r = 0; r < 3; ++r) {
@@ -857,6 +914,8 @@ int ora_contact_manifold(void* s, const int* pairs, long n_pairs, const double* 
       for (int k = 0; k < 36; ++k) J[36 * c + k] = Jc[k];
       for (int i = 0; i < 6; ++i) { zout[6 * c + i] = z[i].v; dcand[6 * c + i] = dd[i].v; gout[6 * c + i] = gam[i].v; }
     }
+    row0 += m.F;
+   }
   }
   return 0;
 }

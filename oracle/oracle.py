@@ -52,7 +52,7 @@ def lib():
         L.ora_mesh_counts.argtypes = [p, i, p, p, p]
         L.ora_mesh_topology.argtypes = [p, i, p, p]
         L.ora_sdf_eval.argtypes = [p, p, p, p, l, l, i, p, p, p, p, p, p]
-        L.ora_contact_manifold.argtypes = [p, p, l, p, l, i] + [p] * 12 + [i]
+        L.ora_contact_manifold.argtypes = [p, p, l, p, l, i] + [p] * 12 + [i, i]
         L.ora_max_threads.restype = i
         _lib = L
     return _lib
@@ -202,12 +202,16 @@ class OracleScene:
                            *[_ptr(out[k]) for k in ("d", "grad", "hess", "dpose", "d2pose", "dxdpose")])
         return out
 
-    def contact_manifold(self, pairs=None, poses=None, n_threads=0):
+    def contact_manifold(self, pairs=None, poses=None, n_threads=0, mode=0):
+        """mode bits: 4 full mode (V + E contacts), 8 two-sided."""
         sc = self.scene
         pairs = np.ascontiguousarray(sc.pairs if pairs is None else pairs, dtype=np.int32)
         poses = np.ascontiguousarray(sc.poses if poses is None else poses, dtype=np.float64)
         n_env, n_slot = poses.shape[0], poses.shape[1]
-        F = [self.mesh_counts(int(a))[2] for a in pairs[:, 3]]
+        def cnt(s):
+            V, E, F_ = self.mesh_counts(int(s))
+            return V + E if mode & 4 else F_
+        F = [cnt(a) + (cnt(b) if mode & 8 else 0) for a, b in zip(pairs[:, 3], pairs[:, 4])]
         Ct = int(sum(F))
         out = dict(point=np.zeros((Ct, 3)), normal=np.zeros((Ct, 3)), depth=np.zeros(Ct), W=np.zeros(Ct),
                    q=np.zeros((Ct, 3)), ddepth=np.zeros((Ct, 12)), dnormal=np.zeros((Ct, 3, 12)),
@@ -216,7 +220,7 @@ class OracleScene:
         lib().ora_contact_manifold(self.h, _ptr(pairs), len(pairs), _ptr(poses), n_env, n_slot,
                                    *[_ptr(out[k]) for k in ("point", "normal", "depth", "W", "q", "ddepth",
                                                             "dnormal", "dom", "J", "z", "dcand", "gamma")],
-                                   int(n_threads))
+                                   int(mode), int(n_threads))
         out["offsets"] = np.concatenate([[0], np.cumsum(F)]).astype(np.int64)
         return out
 

@@ -20,6 +20,7 @@ CM_MAX_CHILDREN = 32
 NODE_TYPES = {"halfspace": 0, "sq": 1, "psq": 2, "xpsq": 3, "union": 10, "intersection": 11, "subtraction": 12}
 
 SDF_VALUE, SDF_GRAD, SDF_HESS, SDF_POSE_GRAD, SDF_POSE_HESS = 1, 2, 4, 8, 16
+FULL_MODE, TWO_SIDED = 4, 8   # manifold mode bits (include/xpsq_cm.h)
 
 EXPORTS = ["cm_version", "cm_last_error", "cm_scene_create", "cm_scene_destroy", "cm_shape_counts",
            "cm_shape_topology", "cm_sdf_eval", "cm_manifold_size", "cm_manifold_offsets_workspace",
@@ -71,12 +72,12 @@ def lib():
         L.cm_shape_counts.argtypes = [p, i32, p, p, p]
         L.cm_shape_topology.argtypes = [p, i32, p, p]
         L.cm_sdf_eval.argtypes = [p, p, p, p, i64, i64, u32, p, p, p, p, p, p, p]
-        L.cm_manifold_size.argtypes = [p, p, i64, i64, p]
+        L.cm_manifold_size.argtypes = [p, p, i64, u32, p]
         L.cm_manifold_offsets_workspace.argtypes = [i64]
         L.cm_manifold_offsets_workspace.restype = i64
-        L.cm_manifold_offsets.argtypes = [p, p, i64, p, p, i64, p]
+        L.cm_manifold_offsets.argtypes = [p, p, i64, u32, p, p, i64, p]
         L.cm_contact_manifold.argtypes = [p, p, i64, p, p, i64, i32, u32, p, i64, p]
-        L.cm_expand_jacobian.argtypes = [p, p, i64, p, p, i64, i32, p, p, i64, p, p]
+        L.cm_expand_jacobian.argtypes = [p, p, i64, p, p, i64, i32, u32, p, p, i64, p, p]
         L.cm_launch_count.restype = i64
         _lib = L
     return _lib
@@ -218,21 +219,24 @@ class Scene:
         return out
 
     # ---- contact manifold ---------------------------------------------------
-    def manifold_size(self, pairs_host: np.ndarray) -> int:
+    def manifold_size(self, pairs_host: np.ndarray, mode: int = 0) -> int:
+        """Contact count of a host pair list for the mode bits (FULL_MODE,
+        TWO_SIDED)."""
         pairs_host = np.ascontiguousarray(pairs_host, dtype=np.int32)
         n = C.c_int64()
-        _check(lib().cm_manifold_size(self.h, pairs_host[:, 3:].ctypes.data_as(C.c_void_p), len(pairs_host), 5,
+        _check(lib().cm_manifold_size(self.h, pairs_host.ctypes.data_as(C.c_void_p), len(pairs_host), mode,
                                       C.byref(n)), "cm_manifold_size")
         return n.value
 
-    def manifold_offsets(self, pairs):
-        """Device exclusive scan of F(shapeA) -> int64 offsets [n_pairs]."""
+    def manifold_offsets(self, pairs, mode: int = 0):
+        """Device exclusive scan of the per-pair contact counts -> int64
+        offsets [n_pairs]."""
         import torch
         n = pairs.shape[0]
         offs = torch.empty(n, dtype=torch.int64, device=pairs.device)
         ws_bytes = int(lib().cm_manifold_offsets_workspace(n))
         ws = torch.empty(ws_bytes, dtype=torch.uint8, device=pairs.device)
-        _check(lib().cm_manifold_offsets(self.h, _ptr(pairs), n, _ptr(offs), _ptr(ws), ws_bytes, _stream()),
+        _check(lib().cm_manifold_offsets(self.h, _ptr(pairs), n, mode, _ptr(offs), _ptr(ws), ws_bytes, _stream()),
                "cm_manifold_offsets")
         return offs
 
@@ -249,9 +253,10 @@ class Scene:
             out["dnormal"] = e(36, C_)
         return out
 
-    def contact_manifold(self, pairs, offsets, n_contacts: int, poses, tier: int = 2, out=None):
+    def contact_manifold(self, pairs, offsets, n_contacts: int, poses, tier: int = 2, out=None, mode: int = 0):
         """pairs int32 [NP,5] (env, slotA, slotB, shapeA, shapeB), offsets
-        int64 [NP], poses float32 [n_env, n_slot, 8] (CUDA tensors)."""
+        int64 [NP] (manifold_offsets with the same mode), poses float32
+        [n_env, n_slot, 8] (CUDA tensors); mode = FULL_MODE | TWO_SIDED bits."""
         for t in (pairs, offsets, poses):
             if not t.is_cuda or not t.is_contiguous():
                 raise CMError("contact_manifold: inputs must be contiguous CUDA tensors")
@@ -260,15 +265,15 @@ class Scene:
         o = cm_manifold_out(*[out[k].data_ptr() if k in out else None
                               for k in ("point", "normal", "depth", "W", "q", "ddepth", "dnormal", "dom")])
         _check(lib().cm_contact_manifold(self.h, _ptr(pairs), pairs.shape[0], _ptr(offsets), _ptr(poses),
-                                         poses.shape[0], poses.shape[1], tier, C.byref(o), n_contacts, _stream()),
-               "cm_contact_manifold")
+                                         poses.shape[0], poses.shape[1], tier | mode, C.byref(o), n_contacts,
+                                         _stream()), "cm_contact_manifold")
         return out
 
-    def expand_jacobian(self, pairs, offsets, poses, W, q, n_contacts: int):
+    def expand_jacobian(self, pairs, offsets, poses, W, q, n_contacts: int, mode: int = 0):
         import torch
         J = torch.empty(36, n_contacts, device=poses.device, dtype=torch.float32)
         _check(lib().cm_expand_jacobian(self.h, _ptr(pairs), pairs.shape[0], _ptr(offsets), _ptr(poses),
-                                        poses.shape[0], poses.shape[1], _ptr(W), _ptr(q), n_contacts, _ptr(J),
+                                        poses.shape[0], poses.shape[1], mode, _ptr(W), _ptr(q), n_contacts, _ptr(J),
                                         _stream()), "cm_expand_jacobian")
         return J
 
@@ -277,5 +282,5 @@ def sdf_eval(scene: Scene, shape_ids, poses, points, P: int, flags: int = SDF_VA
     return scene.sdf_eval(shape_ids, poses, points, P, flags)
 
 
-def contact_manifold(scene: Scene, pairs, offsets, n_contacts, poses, tier: int = 2, out=None):
-    return scene.contact_manifold(pairs, offsets, n_contacts, poses, tier, out)
+def contact_manifold(scene: Scene, pairs, offsets, n_contacts, poses, tier: int = 2, out=None, mode: int = 0):
+    return scene.contact_manifold(pairs, offsets, n_contacts, poses, tier, out, mode)

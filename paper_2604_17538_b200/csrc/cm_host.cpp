@@ -469,13 +469,21 @@ int cm_sdf_eval(const cm_scene* sc, const int32_t* ids, const float* poses, cons
   return CM_OK;
 }
 
-int cm_manifold_size(const cm_scene* sc, const int32_t* shapeA, int64_t n_pairs, int64_t stride, int64_t* n) {
-  if (!sc || (!shapeA && n_pairs > 0) || !n) return fail(CM_ERR_INVALID, "cm_manifold_size");
+int cm_manifold_size(const cm_scene* sc, const int32_t* pairs, int64_t n_pairs, uint32_t flags, int64_t* n) {
+  if (!sc || (!pairs && n_pairs > 0) || !n) return fail(CM_ERR_INVALID, "cm_manifold_size");
+  const bool full = flags & CM_FULL_MODE, two = flags & CM_TWO_SIDED;
+  const int ns = (int)sc->shapes.size();
   int64_t c = 0;
   for (int64_t i = 0; i < n_pairs; ++i) {
-    int s = shapeA[i * stride];
-    if (s < 0 || s >= (int)sc->shapes.size()) return fail(CM_ERR_INVALID, "cm_manifold_size: bad shape id");
-    c += sc->shapes[s].F;
+    const int a = pairs[5 * i + 3], b = pairs[5 * i + 4];
+    if (a < 0 || a >= ns || b < 0 || b >= ns) return fail(CM_ERR_INVALID, "cm_manifold_size: bad shape id");
+    for (int side = 0; side < (two ? 2 : 1); ++side) {
+      const ShapeRec& sa = sc->shapes[side ? b : a];
+      const ShapeRec& sb = sc->shapes[side ? a : b];
+      if (sa.F == 0) return fail(CM_ERR_INVALID, "cm_manifold_size: sampled shape has no surface");
+      if (!sb.has_sdf) return fail(CM_ERR_INVALID, "cm_manifold_size: SDF shape has no SDF");
+      c += full ? (int64_t)sa.V + sa.E : (int64_t)sa.F;
+    }
   }
   *n = c;
   return CM_OK;
@@ -483,14 +491,14 @@ int cm_manifold_size(const cm_scene* sc, const int32_t* shapeA, int64_t n_pairs,
 
 int64_t cm_manifold_offsets_workspace(int64_t n_pairs) { return cml::offsets_workspace(n_pairs); }
 
-int cm_manifold_offsets(const cm_scene* sc, const int32_t* pairs, int64_t n_pairs, int64_t* offsets, void* ws,
-                        int64_t ws_bytes, void* stream) {
+int cm_manifold_offsets(const cm_scene* sc, const int32_t* pairs, int64_t n_pairs, uint32_t flags, int64_t* offsets,
+                        void* ws, int64_t ws_bytes, void* stream) {
   if (!sc) return fail(CM_ERR_INVALID, "cm_manifold_offsets: NULL scene");
   if (n_pairs == 0) return CM_OK;
   if (!pairs || !offsets || !ws) return fail(CM_ERR_INVALID, "cm_manifold_offsets: NULL argument");
   if (n_pairs > (int64_t)0x7fffffff) return fail(CM_ERR_UNSUPPORTED, "cm_manifold_offsets: too many pairs");
   if (ws_bytes < cml::offsets_workspace(n_pairs)) return fail(CM_ERR_INVALID, "cm_manifold_offsets: workspace too small");
-  int rc = cml::launch_offsets(sc->dev, pairs, n_pairs, offsets, ws, ws_bytes, stream);
+  int rc = cml::launch_offsets(sc->dev, pairs, n_pairs, flags, offsets, ws, ws_bytes, stream);
   if (rc) return fail(rc, cml::last_cuda_error());
   return CM_OK;
 }
@@ -515,11 +523,11 @@ int cm_contact_manifold(const cm_scene* sc, const int32_t* pairs, int64_t n_pair
 }
 
 int cm_expand_jacobian(const cm_scene* sc, const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,
-                       const float* poses, int64_t n_env, int32_t n_slot, const float* W, const float* q,
-                       int64_t n_contacts, float* J, void* stream) {
+                       const float* poses, int64_t n_env, int32_t n_slot, uint32_t flags, const float* W,
+                       const float* q, int64_t n_contacts, float* J, void* stream) {
   (void)n_env;
   if (!sc || !pairs || !offsets || !poses || !W || !q || !J) return fail(CM_ERR_INVALID, "cm_expand_jacobian");
-  int rc = cml::launch_expand(pairs, n_pairs, offsets, sc->dev, poses, n_slot, W, q, n_contacts, J, stream);
+  int rc = cml::launch_expand(pairs, n_pairs, offsets, sc->dev, poses, n_slot, W, q, n_contacts, J, flags, stream);
   if (rc) return fail(rc, cml::last_cuda_error());
   return CM_OK;
 }

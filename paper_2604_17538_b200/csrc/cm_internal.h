@@ -102,12 +102,12 @@ int launch_sdf_eval(const cmi::SceneDev& s, int class_mask, const int32_t* shape
 int launch_manifold(const cmi::SceneDev& s, int class_mask, int max_V, int max_E, const int32_t* pairs,
                     int64_t n_pairs, const int64_t* offsets, const float* poses, int32_t n_slot, uint32_t flags,
                     const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats, void* stream);
-int launch_offsets(const cmi::SceneDev& s, const int32_t* pairs, int64_t n_pairs, int64_t* offsets, void* ws,
-                   int64_t ws_bytes, void* stream);
+int launch_offsets(const cmi::SceneDev& s, const int32_t* pairs, int64_t n_pairs, uint32_t flags, int64_t* offsets,
+                   void* ws, int64_t ws_bytes, void* stream);
 int64_t offsets_workspace(int64_t n_pairs);
 int launch_expand(const int32_t* pairs, int64_t n_pairs, const int64_t* offsets, const cmi::SceneDev& s,
                   const float* poses, int32_t n_slot, const float* W, const float* q, int64_t C, float* J,
-                  void* stream);
+                  uint32_t flags, void* stream);
 int64_t manifold_smem_floats(int V, int E, int tier);
 int manifold_max_smem_bytes();
 const char* last_cuda_error();

@@ -78,6 +78,74 @@ __device__ __forceinline__ void gJ(const float* g, const float* p, const PairFra
 // derivative slots: 9 independent components (tA, thetaA, thetaB); tB = -tA
 constexpr int NDQ = 9;
 
+// Full mode (V + E contacts): candidate i is its own contact.
+//   point p, normal n = grad phi (raw), depth d, W = gamma, q = gamma p (so the
+//   compact J = gamma J_i, the single-candidate case of P:161), dom = kind
+//   (0 vertex, 1 edge point); tier 2: d d / dq = g^T J(p) (+ (g.e_t) d alpha_bar),
+//   d n / dq = [H, -H[p - tA]x, (-H), H[p - tB]x - [n]x] (+ H e_t d alpha_bar^T).
+template <int TIER>
+__device__ __forceinline__ void store_candidate(const cm_manifold_out& out, int64_t C, int64_t c, const float* p,
+                                                const float* n, float d, const float* h, const float* ew,
+                                                const float* dab, const PairFrame& F, int kind, float itcmp, int cTA,
+                                                int cRA, int cTB, int cRB) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    out.point[a * C + c] = p[a];
+    out.normal[a * C + c] = n[a];
+  }
+  out.depth[c] = d;
+  out.dom[c] = (int8_t)kind;
+  if constexpr (TIER >= 1) {
+    const float gam = sigm(-d * itcmp);
+    out.W[c] = gam;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) out.q[a * C + c] = gam * p[a];
+  }
+  if constexpr (TIER >= 2) {
+    float dd[NDQ];
+    gJ(n, p, F, dd);
+    const float H[3][3] = {{h[0], h[1], h[2]}, {h[1], h[3], h[4]}, {h[2], h[4], h[5]}};
+    float he[3] = {0.f, 0.f, 0.f};
+    if (ew) {
+      const float ge = n[0] * ew[0] + n[1] * ew[1] + n[2] * ew[2];
+#pragma unroll
+      for (int k = 0; k < NDQ; ++k) dd[k] = fmaf(ge, dab[k], dd[k]);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) he[a] = H[a][0] * ew[0] + H[a][1] * ew[1] + H[a][2] * ew[2];
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      out.ddepth[(cTA + k) * C + c] = dd[k];
+      out.ddepth[(cRA + k) * C + c] = dd[3 + k];
+      out.ddepth[(cTB + k) * C + c] = -dd[k];
+      out.ddepth[(cRB + k) * C + c] = dd[6 + k];
+    }
+    const float ra[3] = {p[0] - F.tA[0], p[1] - F.tA[1], p[2] - F.tA[2]};
+    const float rb[3] = {p[0] - F.tB[0], p[1] - F.tB[1], p[2] - F.tB[2]};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float nk[3] = {a == 0 ? 0.f : (a == 1 ? n[2] : -n[1]), a == 0 ? -n[2] : (a == 1 ? 0.f : n[0]),
+                           a == 0 ? n[1] : (a == 1 ? -n[0] : 0.f)};
+      float row[NDQ] = {H[a][0], H[a][1], H[a][2],
+                        -(H[a][1] * ra[2] - H[a][2] * ra[1]), -(H[a][2] * ra[0] - H[a][0] * ra[2]),
+                        -(H[a][0] * ra[1] - H[a][1] * ra[0]),
+                        (H[a][1] * rb[2] - H[a][2] * rb[1]) - nk[0], (H[a][2] * rb[0] - H[a][0] * rb[2]) - nk[1],
+                        (H[a][0] * rb[1] - H[a][1] * rb[0]) - nk[2]};
+      if (ew) {
+#pragma unroll
+        for (int k = 0; k < NDQ; ++k) row[k] = fmaf(he[a], dab[k], row[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        out.dnormal[(a * 12 + cTA + k) * C + c] = row[k];
+        out.dnormal[(a * 12 + cRA + k) * C + c] = row[3 + k];
+        out.dnormal[(a * 12 + cTB + k) * C + c] = -row[k];
+        out.dnormal[(a * 12 + cRB + k) * C + c] = row[6 + k];
+      }
+    }
+  }
+}
+
 // optional per-phase cycle accounting (tools/phase_timing.py; off in the product build)
 #ifndef CM_PHASE_TIMING
 #define CM_PHASE_TIMING 0
@@ -109,8 +177,11 @@ __global__ void __launch_bounds__(CM_MANIFOLD_THREADS, MB) k_contact_manifold(Sc
                                                           int64_t n_pairs, const int64_t* __restrict__ offsets,
                                                           const float* __restrict__ poses, int32_t n_slot,
                                                           cm_manifold_out out, int64_t C, int xp_filter,
-                                                          float* __restrict__ scratch, int64_t scratch_floats) {
+                                                          float* __restrict__ scratch, int64_t scratch_floats,
+                                                          uint32_t mode) {
   extern __shared__ float smem[];
+  const bool full = (mode & CM_FULL_MODE) != 0;        // one contact per vertex and per edge
+  const bool two = (mode & CM_TWO_SIDED) != 0;         // roles transposed as a second manifold
   constexpr int OV = TIER >= 2 ? 2 : 1;   // order at vertices / midpoints
   constexpr int OT = TIER >= 2 ? 1 : 0;   // order inside the trace
   const SmoothDev sp = S.sp;
@@ -120,6 +191,7 @@ __global__ void __launch_bounds__(CM_MANIFOLD_THREADS, MB) k_contact_manifold(Sc
   float* st = scratch ? scratch + (int64_t)blockIdx.x * scratch_floats : smem;
   __shared__ PairFrame Fs;
   __shared__ ShapeRec SA, SB;
+  __shared__ int64_t s_off;
 
 #if CM_PHASE_TIMING
   long long t_mark = 0;
@@ -132,13 +204,21 @@ __global__ void __launch_bounds__(CM_MANIFOLD_THREADS, MB) k_contact_manifold(Sc
 #else
 #define CM_PT(k)
 #endif
-  for (int64_t pi = blockIdx.x; pi < n_pairs; pi += gridDim.x) {
+  const int64_t n_units = two ? 2 * n_pairs : n_pairs;
+  for (int64_t un = blockIdx.x; un < n_units; un += gridDim.x) {
+    const int64_t pi = two ? un >> 1 : un;
+    const int side = two ? (int)(un & 1) : 0;         // 1: B sampled against A's SDF
     const int32_t* pr = pairs + 5 * pi;
-    const int env = __ldg(pr + 0), slA = __ldg(pr + 1), slB = __ldg(pr + 2);
-    const int shA = __ldg(pr + 3), shB = __ldg(pr + 4);
+    const int env = __ldg(pr + 0);
+    const int slA = __ldg(pr + 1 + side), slB = __ldg(pr + 2 - side);
+    const int shA = __ldg(pr + 3 + side), shB = __ldg(pr + 4 - side);
     const ShapeRec sa = S.shapes[shA];
     const ShapeRec sb = S.shapes[shB];
     if (xp_filter >= 0 && sb.uses_xpsq != xp_filter) continue;   // uniform across the CTA
+    if (!sb.has_sdf || sa.F == 0) continue;                      // rejected by cm_manifold_size
+    // output columns of the (t_A, theta_A, t_B, theta_B) blocks in the pair's
+    // own (A, B) order: the transposed side writes its blocks swapped
+    const int cTA = side ? 6 : 0, cRA = side ? 9 : 3, cTB = side ? 0 : 6, cRB = side ? 3 : 9;
     __syncthreads();   // previous pair's readers of Fs / st are done
     if (threadIdx.x == 0) {
       float pa[8], pb[8];
@@ -149,6 +229,12 @@ __global__ void __launch_bounds__(CM_MANIFOLD_THREADS, MB) k_contact_manifold(Sc
       pair_frame(pa, pb, Fs);
       SA = sa;
       SB = sb;
+      int64_t o = __ldg(offsets + pi);
+      if (side) {
+        const ShapeRec s0 = S.shapes[__ldg(pr + 3)];
+        o += full ? (int64_t)s0.V + s0.E : (int64_t)s0.F;
+      }
+      s_off = o;
     }
     __syncthreads();
     CM_PT(0);
@@ -179,12 +265,14 @@ __global__ void __launch_bounds__(CM_MANIFOLD_THREADS, MB) k_contact_manifold(Sc
         sv[(VN + i) * V + v] = n[i];
       }
       sv[VD * V + v] = r.v;
+      float h[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       if constexpr (TIER >= 2) {
-        float h[6];
         rot_sym(F.RB, r.h, h);
 #pragma unroll
         for (int k = 0; k < 6; ++k) sv[(VH + k) * V + v] = h[k];
       }
+      if (full)
+        store_candidate<TIER>(out, C, s_off + v, pw, n, r.v, h, nullptr, nullptr, F, 0, itcmp, cTA, cRA, cTB, cRB);
     }
     __syncthreads();
     CM_PT(1);
@@ -282,20 +370,23 @@ __global__ void __launch_bounds__(CM_MANIFOLD_THREADS, MB) k_contact_manifold(Sc
         se[(EN + i) * E + e] = n[i];
       }
       se[ED * E + e] = r.v;
+      float h[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       if constexpr (TIER >= 2) {
-        float h[6];
         rot_sym(F.RB, r.h, h);
 #pragma unroll
         for (int k = 0; k < 6; ++k) se[(EH + k) * E + e] = h[k];
 #pragma unroll
         for (int k = 0; k < NDQ; ++k) se[(EDAB + k) * E + e] = dab[k];
       }
+      if (full)
+        store_candidate<TIER>(out, C, s_off + V + e, pw, n, r.v, h, ew, dab, F, 1, itcmp, cTA, cRA, cTB, cRB);
     }
     __syncthreads();
     CM_PT(3);
+    if (full) continue;   // full mode: every candidate was written above
 
     // ---- phase 4: per-face fusion -------------------------------
-    const int64_t off = __ldg(offsets + pi);
+    const int64_t off = s_off;
     const int32_t* fv = S.faces + 3 * (int64_t)sa.f_off;
     const int32_t* fe = S.face_edges + 3 * (int64_t)sa.f_off;
     const float itlm = LOG2E * itmin;
@@ -476,19 +567,19 @@ __global__ void __launch_bounds__(CM_MANIFOLD_THREADS, MB) k_contact_manifold(Sc
         // store: q order (tA 0-2, thetaA 3-5, tB 6-8 = -tA, thetaB 9-11)
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-          out.ddepth[k * C + c] = dd[k];
-          out.ddepth[(3 + k) * C + c] = dd[3 + k];
-          out.ddepth[(6 + k) * C + c] = -dd[k];
-          out.ddepth[(9 + k) * C + c] = dd[6 + k];
+          out.ddepth[(cTA + k) * C + c] = dd[k];
+          out.ddepth[(cRA + k) * C + c] = dd[3 + k];
+          out.ddepth[(cTB + k) * C + c] = -dd[k];
+          out.ddepth[(cRB + k) * C + c] = dd[6 + k];
         }
 #pragma unroll
         for (int a = 0; a < 3; ++a)
 #pragma unroll
           for (int k = 0; k < 3; ++k) {
-            out.dnormal[(a * 12 + k) * C + c] = dn[a][k];
-            out.dnormal[(a * 12 + 3 + k) * C + c] = dn[a][3 + k];
-            out.dnormal[(a * 12 + 6 + k) * C + c] = -dn[a][k];
-            out.dnormal[(a * 12 + 9 + k) * C + c] = dn[a][6 + k];
+            out.dnormal[(a * 12 + cTA + k) * C + c] = dn[a][k];
+            out.dnormal[(a * 12 + cRA + k) * C + c] = dn[a][3 + k];
+            out.dnormal[(a * 12 + cTB + k) * C + c] = -dn[a][k];
+            out.dnormal[(a * 12 + cRB + k) * C + c] = dn[a][6 + k];
           }
       }
     }
@@ -520,7 +611,7 @@ template <int TIER, int XP, int MB>
 static int launch_manifold_v(const SceneDev& s, int xp_filter, bool use_smem, int64_t need, const int32_t* pairs,
                              int64_t n_pairs, const int64_t* offsets, const float* poses, int32_t n_slot,
                              const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats,
-                             cudaStream_t st) {
+                             cudaStream_t st, uint32_t mode) {
   const int threads = CM_MANIFOLD_THREADS;
   int smem = use_smem ? (int)need : 0;
   auto kern = k_contact_manifold<TIER, XP, MB>;
@@ -545,10 +636,11 @@ static int launch_manifold_v(const SceneDev& s, int xp_filter, bool use_smem, in
       return CM_ERR_UNSUPPORTED;
     }
   }
-  if (grid > n_pairs) grid = n_pairs;
+  const int64_t n_units = (mode & CM_TWO_SIDED) ? 2 * n_pairs : n_pairs;
+  if (grid > n_units) grid = n_units;
   if (grid < 1) return CM_OK;
   kern<<<(unsigned)grid, threads, smem, st>>>(s, pairs, n_pairs, offsets, poses, n_slot, *out, C, xp_filter,
-                                              use_smem ? nullptr : scratch, use_smem ? 0 : need / 4);
+                                              use_smem ? nullptr : scratch, use_smem ? 0 : need / 4, mode);
   return check_launch("k_contact_manifold");
 }
 
@@ -556,7 +648,7 @@ template <int TIER, int XP>
 static int launch_manifold_t(const SceneDev& s, int xp_filter, int max_V, int max_E, const int32_t* pairs,
                              int64_t n_pairs, const int64_t* offsets, const float* poses, int32_t n_slot,
                              const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats,
-                             cudaStream_t st) {
+                             cudaStream_t st, uint32_t mode) {
   const int64_t need = manifold_smem_floats(max_V, max_E, TIER) * 4;
   const int static_smem = (int)(sizeof(PairFrame) + 2 * sizeof(ShapeRec));
   const bool use_smem = need <= kSmemBudget && need + static_smem + 1024 <= manifold_max_smem_bytes();
@@ -567,10 +659,10 @@ static int launch_manifold_t(const SceneDev& s, int xp_filter, int max_V, int ma
     if (hi)
       return launch_manifold_v<TIER, XP, CM_MANIFOLD_MINBLOCKS_FLAT>(s, xp_filter, use_smem, need, pairs, n_pairs,
                                                                      offsets, poses, n_slot, out, C, scratch,
-                                                                     scratch_floats, st);
+                                                                     scratch_floats, st, mode);
   }
   return launch_manifold_v<TIER, XP, CM_MANIFOLD_MINBLOCKS>(s, xp_filter, use_smem, need, pairs, n_pairs, offsets,
-                                                            poses, n_slot, out, C, scratch, scratch_floats, st);
+                                                            poses, n_slot, out, C, scratch, scratch_floats, st, mode);
 }
 
 int launch_manifold(const SceneDev& s, int class_mask, int max_V, int max_E, const int32_t* pairs,
@@ -583,7 +675,7 @@ int launch_manifold(const SceneDev& s, int class_mask, int max_V, int max_E, con
   const int tier = (int)(flags & CM_TIER_MASK);
   const bool multi = (class_mask & (class_mask - 1)) != 0;
 #define CM_L(T, X) launch_manifold_t<T, X>(s, multi ? X : -1, max_V, max_E, pairs, n_pairs, offsets, poses, n_slot, \
-                                           out, C, scratch, scratch_floats, st)
+                                           out, C, scratch, scratch_floats, st, flags & (CM_FULL_MODE | CM_TWO_SIDED))
 #define CM_T(X) (tier >= 2 ? CM_L(2, X) : (tier == 1 ? CM_L(1, X) : CM_L(0, X)))
   int rc = CM_OK;
   if (class_mask & 1) rc = CM_T(0);

@@ -51,9 +51,17 @@ int num_sms() {
 
 // ---- offsets: exclusive scan of F(shapeA) over the pairs ---------------------
 __global__ void k_face_counts(const ShapeRec* __restrict__ shapes, const int32_t* __restrict__ pairs, int64_t n,
-                              int64_t* __restrict__ cnt) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    cnt[i] = shapes[__ldg(pairs + 5 * i + 3)].F;
+                              uint32_t flags, int64_t* __restrict__ cnt) {
+  const bool full = flags & CM_FULL_MODE, two = flags & CM_TWO_SIDED;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const ShapeRec a = shapes[__ldg(pairs + 5 * i + 3)];
+    int64_t c = full ? (int64_t)a.V + a.E : (int64_t)a.F;
+    if (two) {
+      const ShapeRec b = shapes[__ldg(pairs + 5 * i + 4)];
+      c += full ? (int64_t)b.V + b.E : (int64_t)b.F;
+    }
+    cnt[i] = c;
+  }
 }
 
 int64_t offsets_workspace(int64_t n_pairs) {
@@ -62,13 +70,13 @@ int64_t offsets_workspace(int64_t n_pairs) {
   return (int64_t)bytes + 256;
 }
 
-int launch_offsets(const SceneDev& s, const int32_t* pairs, int64_t n_pairs, int64_t* offsets, void* ws,
-                   int64_t ws_bytes, void* stream) {
+int launch_offsets(const SceneDev& s, const int32_t* pairs, int64_t n_pairs, uint32_t flags, int64_t* offsets,
+                   void* ws, int64_t ws_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   int64_t blocks = (n_pairs + 255) / 256;
   if (blocks > 4096) blocks = 4096;
   if (blocks < 1) return CM_OK;
-  k_face_counts<<<(unsigned)blocks, 256, 0, st>>>(s.shapes, pairs, n_pairs, offsets);
+  k_face_counts<<<(unsigned)blocks, 256, 0, st>>>(s.shapes, pairs, n_pairs, flags, offsets);
   int rc = check_launch("k_face_counts");
   if (rc) return rc;
   size_t bytes = (size_t)ws_bytes;
@@ -85,40 +93,48 @@ int launch_offsets(const SceneDev& s, const int32_t* pairs, int64_t n_pairs, int
 __global__ void k_expand_jacobian(const ShapeRec* __restrict__ shapes, const int32_t* __restrict__ pairs,
                                   int64_t n_pairs, const int64_t* __restrict__ offsets,
                                   const float* __restrict__ poses, int32_t n_slot, const float* __restrict__ W,
-                                  const float* __restrict__ q, int64_t C, float* __restrict__ J) {
+                                  const float* __restrict__ q, int64_t C, float* __restrict__ J, uint32_t flags) {
+  const bool full = flags & CM_FULL_MODE, two = flags & CM_TWO_SIDED;
   for (int64_t pi = blockIdx.x; pi < n_pairs; pi += gridDim.x) {
     const int32_t* pr = pairs + 5 * pi;
     const float* pa = poses + 8 * ((int64_t)pr[0] * n_slot + pr[1]);
     const float* pb = poses + 8 * ((int64_t)pr[0] * n_slot + pr[2]);
-    const int nf = shapes[pr[3]].F;
-    const int64_t off = offsets[pi];
-    for (int f = threadIdx.x; f < nf; f += blockDim.x) {
-      const int64_t c = off + f;
-      const float w = W[c];
-      const float qa[3] = {q[c] - w * pa[0], q[C + c] - w * pa[1], q[2 * C + c] - w * pa[2]};
-      const float qb[3] = {q[c] - w * pb[0], q[C + c] - w * pb[1], q[2 * C + c] - w * pb[2]};
-      const float Ka[3][3] = {{0.f, -qa[2], qa[1]}, {qa[2], 0.f, -qa[0]}, {-qa[1], qa[0], 0.f}};
-      const float Kb[3][3] = {{0.f, -qb[2], qb[1]}, {qb[2], 0.f, -qb[0]}, {-qb[1], qb[0], 0.f}};
+    int64_t off = offsets[pi];
+    for (int side = 0; side < (two ? 2 : 1); ++side) {
+      const ShapeRec sh = shapes[pr[3 + side]];
+      const int nf = full ? sh.V + sh.E : sh.F;
+      // side 1 samples B against A: its contact velocity is v_B - v_A, i.e.
+      // J = -[W I, -[q - W tA]x, -W I, [q - W tB]x] in the pair's (A, B) order
+      const float sg = side ? -1.f : 1.f;
+      for (int f = threadIdx.x; f < nf; f += blockDim.x) {
+        const int64_t c = off + f;
+        const float w = W[c];
+        const float qa[3] = {q[c] - w * pa[0], q[C + c] - w * pa[1], q[2 * C + c] - w * pa[2]};
+        const float qb[3] = {q[c] - w * pb[0], q[C + c] - w * pb[1], q[2 * C + c] - w * pb[2]};
+        const float Ka[3][3] = {{0.f, -qa[2], qa[1]}, {qa[2], 0.f, -qa[0]}, {-qa[1], qa[0], 0.f}};
+        const float Kb[3][3] = {{0.f, -qb[2], qb[1]}, {qb[2], 0.f, -qb[0]}, {-qb[1], qb[0], 0.f}};
 #pragma unroll
-      for (int r = 0; r < 3; ++r)
+        for (int r = 0; r < 3; ++r)
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          J[(r * 12 + k) * C + c] = r == k ? w : 0.f;
-          J[(r * 12 + 3 + k) * C + c] = -Ka[r][k];
-          J[(r * 12 + 6 + k) * C + c] = r == k ? -w : 0.f;
-          J[(r * 12 + 9 + k) * C + c] = Kb[r][k];
-        }
+          for (int k = 0; k < 3; ++k) {
+            J[(r * 12 + k) * C + c] = sg * (r == k ? w : 0.f);
+            J[(r * 12 + 3 + k) * C + c] = -sg * Ka[r][k];
+            J[(r * 12 + 6 + k) * C + c] = sg * (r == k ? -w : 0.f);
+            J[(r * 12 + 9 + k) * C + c] = sg * Kb[r][k];
+          }
+      }
+      off += nf;
     }
   }
 }
 
 int launch_expand(const int32_t* pairs, int64_t n_pairs, const int64_t* offsets, const SceneDev& s,
                   const float* poses, int32_t n_slot, const float* W, const float* q, int64_t C, float* J,
-                  void* stream) {
+                  uint32_t flags, void* stream) {
   int64_t grid = n_pairs < 65535 ? n_pairs : 65535;
   if (grid < 1) return CM_OK;
   k_expand_jacobian<<<(unsigned)grid, 128, 0, (cudaStream_t)stream>>>(s.shapes, pairs, n_pairs, offsets, poses,
-                                                                       n_slot, W, q, C, J);
+                                                                       n_slot, W, q, C, J, flags);
   return check_launch("k_expand_jacobian");
 }
 

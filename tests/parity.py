@@ -58,7 +58,7 @@ def compare(name, got, ref, ref_pert, tol, report):
     return nb
 
 
-def gpu_manifold(scene, tier=2, pairs=None, poses=None, S=None):
+def gpu_manifold(scene, tier=2, pairs=None, poses=None, S=None, mode=0):
     import torch
     from paper_2604_17538_b200 import binding
     S = S or binding.Scene(scene.shapes, scene.smooth)
@@ -66,9 +66,9 @@ def gpu_manifold(scene, tier=2, pairs=None, poses=None, S=None):
     poses_np = scene.poses if poses is None else poses
     pairs_t = torch.from_numpy(np.ascontiguousarray(pairs_np, dtype=np.int32)).cuda()
     poses_t = torch.from_numpy(np.ascontiguousarray(poses_np, dtype=np.float32)).cuda()
-    offs = S.manifold_offsets(pairs_t)
-    C = S.manifold_size(pairs_np)
-    out = S.contact_manifold(pairs_t, offs, C, poses_t, tier)
+    offs = S.manifold_offsets(pairs_t, mode)
+    C = S.manifold_size(pairs_np, mode)
+    out = S.contact_manifold(pairs_t, offs, C, poses_t, tier, mode=mode)
     torch.cuda.synchronize()
     res = {k: v.cpu().numpy() for k, v in out.items()}
     res["offsets"] = offs.cpu().numpy()
@@ -76,12 +76,12 @@ def gpu_manifold(scene, tier=2, pairs=None, poses=None, S=None):
     return res, S
 
 
-def manifold_parity(scene, osc, gpu, tier, pair_idx, rng, ell):
+def manifold_parity(scene, osc, gpu, tier, pair_idx, rng, ell, mode=0):
     """Compares the GPU manifold rows of pairs `pair_idx` (GPU ran the whole
     scene.pairs) with the oracle on those pairs.  Returns (failures, report)."""
     pairs = scene.pairs[pair_idx]
-    ref = osc.contact_manifold(pairs=pairs, poses=scene.poses)
-    refp = osc.contact_manifold(pairs=pairs, poses=perturb_inputs(rng, scene.poses))
+    ref = osc.contact_manifold(pairs=pairs, poses=scene.poses, mode=mode)
+    refp = osc.contact_manifold(pairs=pairs, poses=perturb_inputs(rng, scene.poses), mode=mode)
     rows = np.concatenate([np.arange(gpu["offsets"][i], gpu["offsets"][i] + (ref["offsets"][k + 1] - ref["offsets"][k]))
                            for k, i in enumerate(pair_idx)]).astype(np.int64)
     rep = []
@@ -98,8 +98,9 @@ def manifold_parity(scene, osc, gpu, tier, pair_idx, rng, ell):
         dn = g("dnormal").reshape(3, 12, -1).transpose(2, 0, 1)
         nf += compare("dnormal", dn, ref["dnormal"], refp["dnormal"], tol_hess(ref["dnormal"], (1, 2), ell), rep)
     # dominant candidate, outside near ties of the two deepest candidates
+    # (full mode: the candidate kind, compared exactly)
     ds = np.sort(ref["dcand"], axis=1)
-    clear = (ds[:, 1] - ds[:, 0]) > 1e-4 * ell
+    clear = (ds[:, 1] - ds[:, 0]) > 1e-4 * ell if not (mode & 4) else np.ones(len(ds), bool)
     dom_bad = int(((g("dom").astype(np.int64) != ref["dom"]) & clear).sum())
     rep.append(dict(field="dom", n=int(len(clear)), excluded=int((~clear).sum()), failures=dom_bad))
     nf += dom_bad

@@ -233,3 +233,40 @@ def test_manifold_full_size_sampled(cuda, oracle_mod, cfg):
     _report("manifold_full_%s" % cfg, rep)
     assert nf == 0, json.dumps(rep, indent=1)
     assert PT.excluded_fraction(rep) < 0.01
+
+
+@pytest.mark.parametrize("mode,tier", [(4, 2), (8, 2), (12, 2), (4, 1), (8, 0)])
+def test_manifold_modes_c1(cuda, oracle_mod, mode, tier):
+    """Full mode (V + E contacts), two-sided (roles transposed)
+    and both, on C1 (the box and the ground both carry an SDF and a mesh)."""
+    sc = synth.c1_scene()
+    osc = oracle_mod.OracleScene(sc)
+    gpu, _ = PT.gpu_manifold(sc, tier, mode=mode)
+    nf, rep = PT.manifold_parity(sc, osc, gpu, tier, np.arange(len(sc.pairs)), np.random.default_rng(11), sc.ell,
+                                 mode=mode)
+    _report("manifold_c1_mode%d_t%d" % (mode, tier), rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+    assert PT.excluded_fraction(rep) < 0.01
+
+
+def test_manifold_full_mode_c4(cuda, oracle_mod):
+    sc = synth.c4_scene(64)
+    osc = oracle_mod.OracleScene(sc)
+    gpu, _ = PT.gpu_manifold(sc, 2, mode=4)
+    idx = np.sort(np.random.default_rng(12).choice(len(sc.pairs), 24, replace=False))
+    nf, rep = PT.manifold_parity(sc, osc, gpu, 2, idx, np.random.default_rng(13), sc.ell, mode=4)
+    _report("manifold_c4_full", rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+
+
+def test_expand_jacobian_two_sided(cuda, oracle_mod):
+    import torch
+    sc = synth.c1_scene()
+    osc = oracle_mod.OracleScene(sc)
+    for mode in (8, 12):
+        gpu, S = PT.gpu_manifold(sc, 1, mode=mode)
+        J = S.expand_jacobian(torch.from_numpy(sc.pairs).cuda(), torch.from_numpy(gpu["offsets"]).cuda(),
+                              torch.from_numpy(sc.poses).cuda(), torch.from_numpy(gpu["W"]).cuda(),
+                              torch.from_numpy(gpu["q"]).cuda(), gpu["C"], mode=mode).cpu().numpy()
+        Jr = osc.contact_manifold(mode=mode)["J"].reshape(-1, 36).T
+        assert np.allclose(J, Jr, atol=1e-5 * max(1.0, np.abs(Jr).max()))

@@ -308,3 +308,101 @@ def test_oracle_outputs_finite_on_workloads(oracle_mod, cfg):
     r = osc.contact_manifold(pairs=sc.pairs[:900])
     for k in ("point", "normal", "depth", "W", "q", "ddepth", "dnormal"):
         assert np.isfinite(r[k]).all(), k
+
+
+def test_full_mode_box_on_plane_and_consistency(oracle_mod):
+    """Full mode: V + E rows, vertices first; every row is the
+    candidate itself.  Box flat on a plane: bottom vertices have depth
+    exactly -delta, W = sigma(delta/tau); each row equals the reduced mode's
+    candidate of the same vertex / edge."""
+    O = oracle_mod
+    delta = 2e-3
+    box = synth.make_shape("b", None, synth.box_mesh((0.1, 0.1, 0.1), 2))
+    ground = synth.make_shape("g", synth.halfspace((0, 0, 1), 0.0), None)
+    poses = np.zeros((1, 2, 8))
+    poses[0, 0] = synth.pose_row((0.01, -0.02, 0.1 - delta), synth.quat_from_axis_angle((0, 0, 1), 0.3))
+    poses[0, 1] = synth.pose_row((0, 0, 0), (1, 0, 0, 0))
+    sc = scene_of([box, ground], pairs=np.array([[0, 0, 1, 0, 1]], np.int32), poses=poses)
+    osc = O.OracleScene(sc)
+    full = osc.contact_manifold(mode=4)
+    red = osc.contact_manifold()
+    V, E, F = osc.mesh_counts(0)
+    assert len(full["depth"]) == V + E
+    assert np.all(full["dom"][:V] == 0) and np.all(full["dom"][V:] == 1)
+    d32 = float(np.float32(0.1)) - float(np.float32(0.1 - delta))
+    zb = box.vertices[:, 2] < 0
+    assert np.allclose(full["depth"][:V][zb], -d32, atol=1e-12)
+    assert np.allclose(full["W"][:V][zb], 1.0 / (1.0 + math.exp(-d32 / TAU_CMP)), atol=1e-12)
+    assert np.allclose(full["q"], full["W"][:, None] * full["point"], atol=1e-15)
+    # consistency with the reduced mode's candidates
+    e, fe = osc.mesh_topology(0)
+    order = np.lexsort((e[:, 1], e[:, 0]))          # sorted (lo, hi) edge order
+    rank = np.empty(E, int)
+    rank[order] = np.arange(E)
+    for f in range(F):
+        for k in range(3):
+            assert red["dcand"][f, k] == full["depth"][box.faces[f, k]]
+            assert red["dcand"][f, 3 + k] == full["depth"][V + rank[fe[f, k]]]
+
+
+def test_full_mode_derivatives_fd(oracle_mod):
+    """Full-mode d depth/dq and d normal/dq vs central finite differences."""
+    O = oracle_mod
+    shapes, poses, ell = _random_pair_scene(O, 2, "sq")
+    poses = poses.astype(np.float32).astype(np.float64)
+    base, osc = _manifold(O, shapes, poses, np.array([[0, 0, 1, 0, 1]], np.int32), ell)
+    base = osc.contact_manifold(mode=4)
+    h = 1e-6
+    for j in range(12):
+        e = np.zeros(6)
+        e[j % 6] = h
+        pp, pm = poses.copy(), poses.copy()
+        pp[0, j // 6] = perturb(poses[0, j // 6], e)
+        pm[0, j // 6] = perturb(poses[0, j // 6], -e)
+        op_, om_ = osc.contact_manifold(poses=pp, mode=4), osc.contact_manifold(poses=pm, mode=4)
+        assert np.allclose((op_["depth"] - om_["depth"]) / (2 * h), base["ddepth"][:, j], atol=1e-5)
+        assert np.allclose((op_["normal"] - om_["normal"]) / (2 * h), base["dnormal"][:, :, j], atol=1e-4)
+
+
+def test_two_sided_equals_transposed_pair(oracle_mod):
+    """Two-sided: the second half is the one-sided manifold of the
+    transposed pair, with its derivative and Jacobian column blocks
+    expressed in the pair's (A, B) order (its J rows are v_B - v_A, i.e. the
+    negated side-0 formula [I, -[p - tA]x, -I, [p - tB]x])."""
+    O = oracle_mod
+    sc = synth.c1_scene()
+    osc = O.OracleScene(sc)
+    pair = sc.pairs[:1]                                  # box (sampled) on ground (SDF)
+    two = osc.contact_manifold(pairs=pair, mode=8)
+    one = osc.contact_manifold(pairs=pair)
+    swp = osc.contact_manifold(pairs=pair[:, [0, 2, 1, 4, 3]])
+    n0 = len(one["depth"])
+    assert len(two["depth"]) == n0 + len(swp["depth"])
+    for k in ("depth", "point", "normal", "W", "q", "dom"):
+        assert np.array_equal(two[k][:n0], one[k])
+        assert np.allclose(two[k][n0:], swp[k], atol=1e-15)
+    perm = np.r_[6:12, 0:6]
+    assert np.allclose(two["ddepth"][n0:], swp["ddepth"][:, perm], atol=1e-13)
+    assert np.allclose(two["dnormal"][n0:], swp["dnormal"][:, :, perm], atol=1e-11)
+    assert np.allclose(two["J"][n0:], swp["J"][:, :, perm], atol=1e-13)
+    W, q = two["W"][n0:], two["q"][n0:]
+    tA, tB = sc.poses[0, 0, :3].astype(np.float64), sc.poses[0, 1, :3].astype(np.float64)
+    for c in range(len(W)):
+        Jc = np.concatenate([W[c] * np.eye(3), -skew(q[c] - W[c] * tA), -W[c] * np.eye(3), skew(q[c] - W[c] * tB)], 1)
+        assert np.allclose(two["J"][n0 + c], -Jc, atol=1e-12)
+
+
+def test_two_sided_mirror_symmetry(oracle_mod):
+    """Two identical spheres placed symmetrically: the two halves have equal
+    depth multisets and opposite normals (SURVEY §8c.3 role swap)."""
+    O = oracle_mod
+    r = 0.1
+    sph = synth.make_shape("s", synth.sq((r, r, r), (1, 1)), synth.sq_mesh((r, r, r), (1, 1), 3))
+    poses = np.zeros((1, 2, 8))
+    poses[0, 0] = synth.pose_row((-0.095, 0, 0), (1, 0, 0, 0))
+    poses[0, 1] = synth.pose_row((0.095, 0, 0), (0, 0, 0, 1))   # rotated 180 deg about z: mirror image
+    sc = scene_of([sph], pairs=np.array([[0, 0, 1, 0, 0]], np.int32), poses=poses)
+    out = O.OracleScene(sc).contact_manifold(mode=8)
+    n = len(out["depth"]) // 2
+    assert np.allclose(np.sort(out["depth"][:n]), np.sort(out["depth"][n:]), atol=1e-12)
+    assert np.allclose(out["normal"][:n].sum(0), -out["normal"][n:].sum(0), atol=1e-12)
