@@ -94,10 +94,15 @@ def make_scene(workload, n_env, env_lo):
         return synth.c3_scene(n_env, seed=3 + 1000 * (env_lo // max(n_env, 1)))
     if workload == "C2":
         return synth.c2_scene(n_env, seed=2 + 1000 * (env_lo // max(n_env, 1)))
+    if workload == "SDF":
+        return synth.sdf_scene(n_env, SDF_P, env_lo=env_lo)
     raise SystemExit("unknown workload " + workload)
 
 
-DEFAULT_NENV = {"C5": 1 << 20, "C4": 1 << 16, "C3": 1 << 14, "C2": 1000}
+DEFAULT_NENV = {"C5": 1 << 20, "C4": 1 << 16, "C3": 1 << 14, "C2": 1000, "SDF": 1 << 18}
+SDF_P = 64            # query points per body (SDF workload)
+SDF_METRIC = "sdf_eval point-evaluations/sec (value + gradient + Hessian + pose gradient)"
+SDF_BYTES_PER_POINT = 12 + 4 + 12 + 24 + 24   # point in; d, grad, hess (6), dpose (6) out
 
 
 class ClockSampler:
@@ -173,10 +178,44 @@ def oracle_rate(scene, budget_s=15.0, threads=0, max_pairs=None):
     return m / dt, m, cores, dt
 
 
+def run_reference_sdf(args):
+    n_body = args.n_env or DEFAULT_NENV["SDF"]
+    sc = make_scene("SDF", min(n_body, 65536), 0)
+    from oracle import oracle as O
+    osc = O.OracleScene(sc)
+    P = sc.P
+
+    def run(m):
+        osc.sdf_eval(sc.point_shapes[:m], sc.point_poses[:m], sc.points[:m * P], P, want_pose=True)
+
+    n = 64
+    t0 = time.perf_counter()
+    run(n)
+    per = (time.perf_counter() - t0) / n
+    m = int(max(n, min(len(sc.point_shapes), 150.0 / max(args.steps + args.warmup, 1) / max(per, 1e-9))))
+    for _ in range(args.warmup):
+        run(m)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run(m)
+    dt = (time.perf_counter() - t0) / args.steps
+    val = m * P / dt
+    line = {"impl": "reference", "metric": SDF_METRIC, "value": val, "unit": "points/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "SDF", "bodies_per_gpu": n_body, "points_per_body": P},
+            "cpu_baseline": {"value": val, "unit": "points/s", "cores": O.max_threads(), "kind": "oracle",
+                             "sample": "first %d bodies x %d points per step (FP64 jet oracle, OpenMP)" % (m, P)},
+            "e2e": {"value": val, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    if args.workload == "SDF":
+        return run_reference_sdf(args)
     n_env = args.n_env or DEFAULT_NENV[args.workload]
     scene = make_scene(args.workload, min(n_env, 65536), 0)
     from oracle import oracle as O
@@ -209,13 +248,144 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _timed(step, args, stream, flush, world, local):
+    """W warm-up steps, then K steps timed with CUDA events on the launching
+    stream (L2 flushed before each), barrier + synchronize on both sides,
+    clocks sampled during the timed region; returns (max-over-ranks ms per
+    step, own kernel launches, clocks)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2604_17538_b200 import binding
+    dev = torch.device("cuda", local)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = binding.launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    launches = binding.launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = float(np.sum([a.elapsed_time(b) for a, b in ev]))
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()) / args.steps, launches, clk
+
+
+def run_sdf(args, sc, n_body, gen_s, world, rank, local):
+    """Secondary metric: cm_sdf_eval of the 32 C5 SDF prototypes
+    with value, gradient, Hessian and pose gradient at P points per body."""
+    import torch
+    import torch.distributed as dist
+    from paper_2604_17538_b200 import binding
+    dev = torch.device("cuda", local)
+    S = binding.Scene(sc.shapes, sc.smooth, device=local)
+    P = sc.P
+    flags = binding.SDF_VALUE | binding.SDF_GRAD | binding.SDF_HESS | binding.SDF_POSE_GRAD
+    ids = torch.from_numpy(sc.point_shapes).to(dev)
+    poses = torch.from_numpy(sc.point_poses).to(dev)
+    pts = torch.from_numpy(sc.points).to(dev)
+    out = S.sdf_eval(ids, poses, pts, P, flags)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    ms, launches, clk = _timed(lambda: S.sdf_eval(ids, poses, pts, P, flags, out=out), args, stream, flush, world,
+                               local)
+    n_pts = len(sc.point_shapes) * P
+    value = n_pts * world / (ms / 1e3)
+    e2e = None
+    if not args.no_e2e:
+        pts_h = torch.from_numpy(sc.points).pin_memory()
+        d_h = torch.empty(n_pts, dtype=torch.float32).pin_memory()
+        pts_d = torch.empty_like(pts)
+
+        def e2e_step():
+            pts_d.copy_(pts_h, non_blocking=True)
+            o = S.sdf_eval(ids, poses, pts_d, P, flags, out=out)
+            d_h.copy_(o["d"], non_blocking=True)
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": n_pts * world / (float(te.item()) / 1e3), "unit": "points/s",
+               "h2d_bytes_per_step": int(pts_h.numel() * 4), "d2h_bytes_per_step": int(n_pts * 4)}
+    with open(os.path.join(ROOT, "paper_2604_17538_b200", "costmodel.json")) as f:
+        cm = json.load(f)
+    names = [sc.shapes[i].name for i in range(len(sc.shapes))]
+    cnt = np.bincount(sc.point_shapes, minlength=len(names))
+    flop = float(sum(cnt[i] * P * cm["sdf"][names[i]]["order2"]["flop"] for i in range(len(names))))
+    kern_s = ms / 1e3
+    bytes_alg = n_pts * SDF_BYTES_PER_POINT + len(sc.point_shapes) * 36
+    peaks, peak_src = load_peaks()
+    achieved = flop / kern_s / 1e12
+    hbm = bytes_alg / kern_s / 1e9
+    roof = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": achieved / FP32_PEAK_TFLOPS, "traffic": None,
+            "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
+            "flop_per_point": flop / n_pts, "flop_source": "costmodel.json order-2 evaluation FLOPs per shape",
+            "hbm": {"achieved_gbs": hbm, "peak_gbs": peaks["hbm_gbs"], "frac": hbm / peaks["hbm_gbs"],
+                    "bytes_alg": bytes_alg, "peak_source": peak_src}}
+    if hbm / peaks["hbm_gbs"] > achieved / FP32_PEAK_TFLOPS:
+        roof.update({"bound": "hbm", "achieved": hbm, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": hbm / peaks["hbm_gbs"]})
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+        osc = O.OracleScene(sc)
+        m = 256
+        t0 = time.perf_counter()
+        osc.sdf_eval(sc.point_shapes[:m], sc.point_poses[:m], sc.points[:m * P], P, want_pose=True)
+        per = (time.perf_counter() - t0) / m
+        m = int(max(m, min(len(sc.point_shapes), 15.0 / max(per, 1e-9))))
+        t0 = time.perf_counter()
+        osc.sdf_eval(sc.point_shapes[:m], sc.point_poses[:m], sc.points[:m * P], P, want_pose=True)
+        dt = time.perf_counter() - t0
+        cpu = {"value": m * P / dt, "unit": "points/s", "cores": O.max_threads(), "kind": "oracle",
+               "sample": "first %d bodies x %d points of the SDF shard, FP64 jet oracle (with pose Hessians), "
+                         "OpenMP, %.1f s" % (m, P, dt)}
+    if rank == 0:
+        line = {"metric": SDF_METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": "SDF", "bodies_per_gpu": n_body, "points_per_body": P,
+                           "l2": "flushed (256 MiB write) between steps",
+                           "parallelism": "body-sharded dp%d, no data-path collective" % world,
+                           "input_gen_s": round(gen_s, 1)},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C5", choices=["C5", "C4", "C3", "C2"])
+    ap.add_argument("--workload", default="C5", choices=["C5", "C4", "C3", "C2", "SDF"])
     ap.add_argument("--n-env", type=int, default=0)
     ap.add_argument("--tier", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -238,6 +408,8 @@ def main():
     t0 = time.time()
     scene = make_scene(args.workload, n_env, rank * n_env)
     gen_s = time.time() - t0
+    if args.workload == "SDF":
+        return run_sdf(args, scene, n_env, gen_s, world, rank, local)
     S = binding.Scene(scene.shapes, scene.smooth, device=local)
     dev = torch.device("cuda", local)
     pairs = torch.from_numpy(scene.pairs).to(dev)
@@ -251,34 +423,7 @@ def main():
     def step():
         S.contact_manifold(pairs, offs, C, poses, args.tier, out)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
-    l0 = binding.launch_count()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    for i in range(args.steps):
-        flush.fill_(float(i))
-        ev[i][0].record(stream)
-        step()
-        ev[i][1].record(stream)
-    torch.cuda.synchronize()
-    launches = binding.launch_count() - l0
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clk = clocks.stop()
-    times = [a.elapsed_time(b) for a, b in ev]
-    total_ms = float(np.sum(times))
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
+    ms_per_step, launches, clk = _timed(step, args, stream, flush, world, local)
     n_pairs_all = len(scene.pairs) * world
     value = n_pairs_all / (ms_per_step / 1e3)
 

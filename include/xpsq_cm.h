@@ -33,6 +33,12 @@
  *     ordered (dt_x, dt_y, dt_z, dtheta_x, dtheta_y, dtheta_z).
  *   - Sign convention: phi < 0 inside, > 0 outside ("gamma = [[d < 0]]").
  *   - Thread safety: calls on distinct streams may run concurrently.
+ *     cm_contact_manifold uses the scene's chunk scratch (allocated at scene
+ *     creation): concurrent manifold calls on ONE scene are enqueued under a
+ *     per-scene lock and serialised on the device through the scene's two
+ *     internal streams (forked from and joined back into the caller's stream
+ *     with events, so stream capture into a CUDA graph works); calls on
+ *     distinct scenes run concurrently.
  */
 #ifndef XPSQ_CM_H
 #define XPSQ_CM_H

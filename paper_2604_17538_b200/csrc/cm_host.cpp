@@ -7,8 +7,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <mutex>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -189,6 +191,11 @@ struct cm_scene {
   std::vector<void*> allocs;
   float* scratch = nullptr;
   int64_t scratch_floats = 0;
+  // manifold calls share the scratch: a call enqueues under `mu` and forks
+  // onto the scene's aux streams, which serialise calls on the device
+  std::mutex mu;
+  cudaStream_t aux[cmi::kManifoldStreams] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[cmi::kManifoldStreams] = {};
 };
 
 extern "C" {
@@ -409,17 +416,25 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
     if (p) sc->allocs.push_back(const_cast<void*>(p));
   D.sp = SmoothDev{sp->tau_cmp, sp->tau_min, sp->tau_clip_alpha, sp->tau_clip_t, sp->tau_delta, sp->trace_iters};
   D.n_shapes = n_shapes;
-  // global scratch for sampled surfaces whose pair state exceeds the shared
-  // memory budget of two resident CTAs per SM (e.g. C3's 16x32 patch at tier 2)
+  // chunk scratch of the manifold kernels (one candidate-state slot per unit)
   if (rc == CM_OK && sc->max_F > 0) {
-    int64_t need = cml::manifold_smem_floats(sc->max_V, sc->max_E, 2);
-    if (need * 4 > cmi::kSmemBudget) {
-      int sms = 148;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-      sc->scratch_floats = need * (int64_t)sms * 4;
-      e = cudaMalloc(&sc->scratch, sc->scratch_floats * sizeof(float));
-      if (e != cudaSuccess) { rc = CM_ERR_OOM; g_err = "scratch allocation failed"; }
-      else sc->allocs.push_back(sc->scratch);
+    const int64_t slot = cml::manifold_slot_floats(sc->max_V, sc->max_E, 2);
+    int64_t units = cmi::kChunkUnits;
+    if (const char* env = std::getenv("CM_CHUNK_UNITS")) units = std::max<int64_t>(1, std::atoll(env));
+    units = std::min<int64_t>(units, std::max<int64_t>(1, cmi::kScratchCapBytes / (slot * 4)));
+    units = std::max<int64_t>(units, cmi::kManifoldStreams);
+    sc->scratch_floats = slot * units;
+    e = cudaMalloc(&sc->scratch, sc->scratch_floats * sizeof(float));
+    if (e != cudaSuccess) { rc = CM_ERR_OOM; g_err = "scratch allocation failed"; }
+    else sc->allocs.push_back(sc->scratch);
+    for (int i = 0; rc == CM_OK && i < cmi::kManifoldStreams; ++i) {
+      if (cudaStreamCreateWithFlags(&sc->aux[i], cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&sc->ev_join[i], cudaEventDisableTiming) != cudaSuccess) {
+        rc = CM_ERR_CUDA; g_err = "aux stream creation failed";
+      }
+    }
+    if (rc == CM_OK && cudaEventCreateWithFlags(&sc->ev_fork, cudaEventDisableTiming) != cudaSuccess) {
+      rc = CM_ERR_CUDA; g_err = "aux event creation failed";
     }
   }
   if (rc != CM_OK) {
@@ -432,6 +447,11 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
 
 int cm_scene_destroy(cm_scene* sc) {
   if (!sc) return CM_OK;
+  for (int i = 0; i < cmi::kManifoldStreams; ++i) {
+    if (sc->aux[i]) cudaStreamDestroy(sc->aux[i]);
+    if (sc->ev_join[i]) cudaEventDestroy(sc->ev_join[i]);
+  }
+  if (sc->ev_fork) cudaEventDestroy(sc->ev_fork);
   for (void* p : sc->allocs) cudaFree(p);
   delete sc;
   return CM_OK;
@@ -516,8 +536,23 @@ int cm_contact_manifold(const cm_scene* sc, const int32_t* pairs, int64_t n_pair
   if (tier >= 1 && (!out->W || !out->q)) return fail(CM_ERR_INVALID, "tier-1 outputs are NULL");
   if (tier >= 2 && (!out->ddepth || !out->dnormal)) return fail(CM_ERR_INVALID, "tier-2 outputs are NULL");
   if (sc->max_F == 0) return fail(CM_ERR_INVALID, "scene has no sampled surface");
+  cm_scene* ms = const_cast<cm_scene*>(sc);   // internal scheduling state only
+  std::lock_guard<std::mutex> lock(ms->mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  // fork: the aux streams wait for the caller's prior work; join: the
+  // caller's stream waits for every chunk
+  if (cudaEventRecord(ms->ev_fork, st) != cudaSuccess) return fail(CM_ERR_CUDA, "cm_contact_manifold: event record");
+  void* aux[cmi::kManifoldStreams];
+  for (int i = 0; i < cmi::kManifoldStreams; ++i) {
+    cudaStreamWaitEvent(ms->aux[i], ms->ev_fork, 0);
+    aux[i] = ms->aux[i];
+  }
   int rc = cml::launch_manifold(sc->dev, sc->class_mask, sc->max_V, sc->max_E, pairs, n_pairs, offsets, poses, n_slot,
-                                flags, out, n_contacts, sc->scratch, sc->scratch_floats, stream);
+                                flags, out, n_contacts, sc->scratch, sc->scratch_floats, aux, cmi::kManifoldStreams);
+  for (int i = 0; i < cmi::kManifoldStreams; ++i) {
+    cudaEventRecord(ms->ev_join[i], ms->aux[i]);
+    cudaStreamWaitEvent(st, ms->ev_join[i], 0);
+  }
   if (rc) return fail(rc, cml::last_cuda_error());
   return CM_OK;
 }

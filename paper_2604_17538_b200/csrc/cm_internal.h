@@ -88,9 +88,12 @@ struct SceneDev {
   int32_t n_shapes;
 };
 
-// per-pair candidate state above this many bytes goes to a global (L2
-// resident) scratch instead of shared memory, so that >= 2 CTAs fit per SM
-constexpr int64_t kSmemBudget = 110 * 1024;
+// manifold chunk scratch: the units of one chunk keep their candidate state
+// in a global slot each; the scene allocates kChunkUnits slots (capped at
+// kScratchCapBytes) at creation (CM_CHUNK_UNITS overrides the unit count)
+constexpr int64_t kChunkUnits = 16384;
+constexpr int kManifoldStreams = 2;     // chunks alternate between the scene's aux streams
+constexpr int64_t kScratchCapBytes = 1024ll << 20;
 
 }  // namespace cmi
 
@@ -101,15 +104,15 @@ int launch_sdf_eval(const cmi::SceneDev& s, int class_mask, const int32_t* shape
                     float* dpose, float* d2pose, float* dxdpose, void* stream);
 int launch_manifold(const cmi::SceneDev& s, int class_mask, int max_V, int max_E, const int32_t* pairs,
                     int64_t n_pairs, const int64_t* offsets, const float* poses, int32_t n_slot, uint32_t flags,
-                    const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats, void* stream);
+                    const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats,
+                    void* const* streams, int n_streams);
 int launch_offsets(const cmi::SceneDev& s, const int32_t* pairs, int64_t n_pairs, uint32_t flags, int64_t* offsets,
                    void* ws, int64_t ws_bytes, void* stream);
 int64_t offsets_workspace(int64_t n_pairs);
 int launch_expand(const int32_t* pairs, int64_t n_pairs, const int64_t* offsets, const cmi::SceneDev& s,
                   const float* poses, int32_t n_slot, const float* W, const float* q, int64_t C, float* J,
                   uint32_t flags, void* stream);
-int64_t manifold_smem_floats(int V, int E, int tier);
-int manifold_max_smem_bytes();
+int64_t manifold_slot_floats(int V, int E, int tier);
 const char* last_cuda_error();
 int64_t launch_count();
 }  // namespace cml

@@ -1,14 +1,16 @@
-// sm_100a kernels of the hot path (arXiv 2604.17538):
-//   k_sdf_eval          batched SDF value / gradient / Hessian (+ pose
-//                       derivatives) — §II-B, Eq. (1)-(6)
-//   k_contact_manifold  one CTA per (env, pair): sampled-surface vertices ->
-//                       sphere-traced edge points -> 6 candidates per face ->
-//                       softmax fusion -> SoA stores — §II-C
-//   k_face_counts / cub scan, k_expand_jacobian   (offsets, J expansion)
-//
-// Hot-path design: FP32 CUDA-core math (no tensor cores: the
-// path is not a dense contraction), MUFU ex2/lg2/rcp in the log domain,
-// pair-local candidate state in shared memory, field-major coalesced stores.
+// sm_100a kernels of the contact-manifold hot path (arXiv 2604.17538 §II-C,
+// P:129-163).  One unit = one (env, pair[, side]) manifold.  A call runs over
+// chunks of units; per chunk and per SDF class four kernels run in stream
+// order, each one CTA per unit:
+//   k_mf_vertices  phi, n (, H) of B at A's sampled vertices
+//   k_mf_traces    2 gated sphere traces per edge (+ d alpha / dq)
+//   k_mf_midpoints phi, n (, H) of B at the edge points p_e
+//   k_mf_faces     per-face softmax fusion of the 6 candidates
+// Candidate state lives in a per-chunk global scratch slot (L2 resident for
+// the chunk sizes used).  Splitting the phases into kernels removes the
+// per-pair CTA barriers and keeps a single SDF-evaluation instance per kernel
+// in the instruction cache (the fused one-CTA-per-pair kernel
+// was instruction-fetch and barrier bound).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -25,18 +27,16 @@ using cml::check_launch;
 using cml::num_sms;
 
 // ============================================================================
-// contact manifold
+// per-unit scratch slot (field-major, stride = V or E)
+//   vertex fields:              d, n[3] (world grad phi), H[6] (world, tier 2)
+//   edge fields after traces:   a_I, a_II (soft-clipped), da_I[9], da_II[9] (tier 2)
+//   edge fields after midpoint: a_bar, d, n[3], H[6] (tier 2), da_bar[9] (tier 2)
 // ============================================================================
-// Per-pair candidate storage (field-major, stride = V or E):
-//   vertex fields: xb[3] (B-local), pw[3] (world), d, n[3] (world grad phi),
-//                  H[6] (world, tier 2)
-//   edge fields during the trace: aI, aII, daI[12], daII[12] (tier 2);
-//   after the midpoint phase:     pw[3], d, n[3], H[6], dab[12] (tier 2)
-__host__ __device__ constexpr int vfields(int tier) { return tier >= 2 ? 16 : 10; }
-__host__ __device__ constexpr int efields(int tier) { return tier >= 2 ? 26 : 7; }
-enum { VX = 0, VP = 3, VD = 6, VN = 7, VH = 10 };
-enum { EA = 0, EB = 1, EDA = 2, EDB = 14 };             // trace layout
-enum { EP = 0, ED = 3, EN = 4, EH = 7, EDAB = 13 };     // midpoint layout
+__host__ __device__ constexpr int vfields(int tier) { return tier >= 2 ? 10 : 4; }
+__host__ __device__ constexpr int efields(int tier) { return tier >= 2 ? 20 : 5; }
+enum { VD = 0, VN = 1, VH = 4 };
+enum { TA = 0, TB = 1, TDA = 2, TDB = 11 };                // trace layout
+enum { MAB = 0, MD = 1, MN = 2, MH = 5, MDAB = 11 };       // midpoint layout
 
 struct PairFrame {
   float RA[9], tA[3], RB[9], tB[3];
@@ -146,545 +146,691 @@ __device__ __forceinline__ void store_candidate(const cm_manifold_out& out, int6
   }
 }
 
-// optional per-phase cycle accounting (tools/phase_timing.py; off in the product build)
-#ifndef CM_PHASE_TIMING
-#define CM_PHASE_TIMING 0
+// ============================================================================
+// unit set-up shared by the four kernels
+// ============================================================================
+struct MfArgs {
+  SceneDev S;
+  const int32_t* pairs;
+  int64_t n_pairs;
+  int64_t unit0;             // first unit of this chunk
+  const int64_t* offsets;
+  const float* poses;
+  int32_t n_slot;
+  cm_manifold_out out;
+  int64_t C;
+  int32_t xp_filter;         // SDF class handled by this launch (-1: all)
+  float* scratch;            // chunk scratch, one slot of `slot` floats per unit
+  int64_t slot;
+  uint32_t mode;
+};
+
+struct UnitCtx {
+  PairFrame F;
+  ShapeRec SA, SB;
+  int64_t off;               // first output row of this unit
+  int side;
+  int valid;
+};
+
+// threads per unit CTA: 64 for large batches (lane use on V = 56..98 meshes);
+// small batches get up to CM_MF_MAX_THREADS so the SMs still fill
+#ifndef CM_MF_THREADS
+#define CM_MF_THREADS 64
 #endif
-#if CM_PHASE_TIMING
-__device__ unsigned long long g_phase_cycles[4][5];
-extern "C" int cm_debug_phase_cycles(unsigned long long* out) {
-  return (int)cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles));
-}
+#define CM_MF_MAX_THREADS 256
+#ifndef CM_MF_FACE_MINB
+#define CM_MF_FACE_MINB 2   // face kernel: <= 128 registers
 #endif
 
-#ifndef CM_MANIFOLD_THREADS
-#define CM_MANIFOLD_THREADS 128
-#endif
-#ifndef CM_MANIFOLD_MINBLOCKS_FLAT
-#define CM_MANIFOLD_MINBLOCKS_FLAT 3
-#endif
-#ifndef CM_MANIFOLD_MINBLOCKS
-#define CM_MANIFOLD_MINBLOCKS 2
-#endif
-// CLS: SDF class (cm_internal.h ShapeRec); XPM: XPSQ mode of leaf_eval;
-// flat SQ-family shapes get a tighter register budget (3 CTAs / SM)
+// Thread 0 resolves the unit (pair, side), its shapes, frame and output
+// offset into shared memory; returns false (uniformly) when another launch
+// owns the unit's SDF class or the unit has no manifold.
+__device__ __forceinline__ bool unit_setup(const MfArgs& a, UnitCtx& U) {
+  if (threadIdx.x == 0) {
+    const bool full = (a.mode & CM_FULL_MODE) != 0;
+    const bool two = (a.mode & CM_TWO_SIDED) != 0;
+    const int64_t un = a.unit0 + blockIdx.x;
+    const int64_t pi = two ? un >> 1 : un;
+    const int side = two ? (int)(un & 1) : 0;          // 1: B sampled against A's SDF
+    const int32_t* pr = a.pairs + 5 * pi;
+    const int env = __ldg(pr + 0);
+    const int slA = __ldg(pr + 1 + side), slB = __ldg(pr + 2 - side);
+    const int shA = __ldg(pr + 3 + side), shB = __ldg(pr + 4 - side);
+    const ShapeRec sa = a.S.shapes[shA];
+    const ShapeRec sb = a.S.shapes[shB];
+    int ok = (a.xp_filter < 0 || sb.uses_xpsq == a.xp_filter) && sb.has_sdf && sa.F > 0;
+    if (ok) {
+      float pa[8], pb[8];
+      const float* A = a.poses + 8 * ((int64_t)env * a.n_slot + slA);
+      const float* B = a.poses + 8 * ((int64_t)env * a.n_slot + slB);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { pa[i] = __ldg(A + i); pb[i] = __ldg(B + i); }
+      pair_frame(pa, pb, U.F);
+      U.SA = sa;
+      U.SB = sb;
+      int64_t o = __ldg(a.offsets + pi);
+      if (side) {
+        const ShapeRec s0 = a.S.shapes[__ldg(pr + 3)];
+        o += full ? (int64_t)s0.V + s0.E : (int64_t)s0.F;
+      }
+      U.off = o;
+      U.side = side;
+    }
+    U.valid = ok;
+  }
+  __syncthreads();
+  return U.valid != 0;
+}
+
+// CLS: SDF class (cm_internal.h ShapeRec); XPM: XPSQ mode of leaf_eval
 template <int CLS> struct ClsTraits {
   static constexpr int XPM = CLS == 3 ? 0 : CLS;
   static constexpr bool FLAT = CLS == 0;
 };
-template <int TIER, int XP, int MB>
-__global__ void __launch_bounds__(CM_MANIFOLD_THREADS, MB) k_contact_manifold(SceneDev S, const int32_t* __restrict__ pairs,
-                                                          int64_t n_pairs, const int64_t* __restrict__ offsets,
-                                                          const float* __restrict__ poses, int32_t n_slot,
-                                                          cm_manifold_out out, int64_t C, int xp_filter,
-                                                          float* __restrict__ scratch, int64_t scratch_floats,
-                                                          uint32_t mode) {
-  extern __shared__ float smem[];
-  const bool full = (mode & CM_FULL_MODE) != 0;        // one contact per vertex and per edge
-  const bool two = (mode & CM_TWO_SIDED) != 0;         // roles transposed as a second manifold
-  constexpr int OV = TIER >= 2 ? 2 : 1;   // order at vertices / midpoints
-  constexpr int OT = TIER >= 2 ? 1 : 0;   // order inside the trace
-  const SmoothDev sp = S.sp;
-  const float tcmp = sp.tau_cmp, itcmp = 1.f / tcmp;
-  const float tmin = sp.tau_min, itmin = 1.f / tmin;
-  const float tca = sp.tau_clip_alpha, itca = 1.f / tca;
-  float* st = scratch ? scratch + (int64_t)blockIdx.x * scratch_floats : smem;
-  __shared__ PairFrame Fs;
-  __shared__ ShapeRec SA, SB;
-  __shared__ int64_t s_off;
 
-#if CM_PHASE_TIMING
-  long long t_mark = 0;
-#define CM_PT(k)                                                                             \
-  if (threadIdx.x == 0) {                                                                    \
-    long long t_now = clock64();                                                             \
-    if (k > 0 || t_mark) atomicAdd(&g_phase_cycles[XP][k > 0 ? k - 1 : 4], (unsigned long long)(t_now - t_mark)); \
-    t_mark = t_now;                                                                          \
+// output columns of the (t_A, theta_A, t_B, theta_B) blocks in the pair's own
+// (A, B) order: the transposed side writes its blocks swapped
+#define CM_COLS(side) \
+  const int cTA = (side) ? 6 : 0, cRA = (side) ? 9 : 3, cTB = (side) ? 0 : 6, cRB = (side) ? 3 : 9
+
+__device__ __forceinline__ void edge_dir(const float* lv, const int32_t* ed, int e, int& vI, int& vII, float* el,
+                                         float& L) {
+  vI = __ldg(ed + 2 * e);
+  vII = __ldg(ed + 2 * e + 1);
+  const float dl[3] = {__ldg(lv + 3 * vII) - __ldg(lv + 3 * vI), __ldg(lv + 3 * vII + 1) - __ldg(lv + 3 * vI + 1),
+                       __ldg(lv + 3 * vII + 2) - __ldg(lv + 3 * vI + 2)};
+  L = sqrtf(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
+  const float iL = 1.f / L;
+  el[0] = dl[0] * iL; el[1] = dl[1] * iL; el[2] = dl[2] * iL;
+}
+
+// x_B = Rrel x + trel (B frame) and p = RA x + tA (world) of a local vertex
+__device__ __forceinline__ void vertex_frames(const PairFrame& F, const float* lv, int v, float* xb, float* pw) {
+  const float x[3] = {__ldg(lv + 3 * v), __ldg(lv + 3 * v + 1), __ldg(lv + 3 * v + 2)};
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    xb[i] = F.Rrel[i * 3] * x[0] + F.Rrel[i * 3 + 1] * x[1] + F.Rrel[i * 3 + 2] * x[2] + F.trel[i];
+    pw[i] = F.RA[i * 3] * x[0] + F.RA[i * 3 + 1] * x[1] + F.RA[i * 3 + 2] * x[2] + F.tA[i];
   }
-#else
-#define CM_PT(k)
-#endif
-  const int64_t n_units = two ? 2 * n_pairs : n_pairs;
-  for (int64_t un = blockIdx.x; un < n_units; un += gridDim.x) {
-    const int64_t pi = two ? un >> 1 : un;
-    const int side = two ? (int)(un & 1) : 0;         // 1: B sampled against A's SDF
-    const int32_t* pr = pairs + 5 * pi;
-    const int env = __ldg(pr + 0);
-    const int slA = __ldg(pr + 1 + side), slB = __ldg(pr + 2 - side);
-    const int shA = __ldg(pr + 3 + side), shB = __ldg(pr + 4 - side);
-    const ShapeRec sa = S.shapes[shA];
-    const ShapeRec sb = S.shapes[shB];
-    if (xp_filter >= 0 && sb.uses_xpsq != xp_filter) continue;   // uniform across the CTA
-    if (!sb.has_sdf || sa.F == 0) continue;                      // rejected by cm_manifold_size
-    // output columns of the (t_A, theta_A, t_B, theta_B) blocks in the pair's
-    // own (A, B) order: the transposed side writes its blocks swapped
-    const int cTA = side ? 6 : 0, cRA = side ? 9 : 3, cTB = side ? 0 : 6, cRB = side ? 3 : 9;
-    __syncthreads();   // previous pair's readers of Fs / st are done
-    if (threadIdx.x == 0) {
-      float pa[8], pb[8];
-      const float* a = poses + 8 * ((int64_t)env * n_slot + slA);
-      const float* b = poses + 8 * ((int64_t)env * n_slot + slB);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) { pa[i] = __ldg(a + i); pb[i] = __ldg(b + i); }
-      pair_frame(pa, pb, Fs);
-      SA = sa;
-      SB = sb;
-      int64_t o = __ldg(offsets + pi);
-      if (side) {
-        const ShapeRec s0 = S.shapes[__ldg(pr + 3)];
-        o += full ? (int64_t)s0.V + s0.E : (int64_t)s0.F;
-      }
-      s_off = o;
-    }
-    __syncthreads();
-    CM_PT(0);
-    const PairFrame& F = Fs;
-    const int V = sa.V, E = sa.E, NF = sa.F;
-    float* sv = st;                                   // vertex block
-    float* se = st + (int64_t)vfields(TIER) * V;      // edge block
-    const float* lv = S.verts + 3 * (int64_t)sa.v_off;
-    const int32_t* ed = S.edges + 2 * (int64_t)sa.e_off;
+}
 
-    // ---- phase 1: vertices: phi, n (and H) of B -------------
+// ---- phase 1: vertices: phi, n (and H) of B ----------------
+template <int TIER, int XP>
+__global__ void __launch_bounds__(CM_MF_MAX_THREADS) k_mf_vertices(const MfArgs a) {
+  __shared__ UnitCtx U;
+  if (!unit_setup(a, U)) return;
+  constexpr int OV = TIER >= 2 ? 2 : 1;
+  const PairFrame& F = U.F;
+  const int V = U.SA.V;
+  float* sv = a.scratch + (int64_t)blockIdx.x * a.slot;
+  const float* lv = a.S.verts + 3 * (int64_t)U.SA.v_off;
+  const bool full = (a.mode & CM_FULL_MODE) != 0;
+  const float itcmp = 1.f / a.S.sp.tau_cmp;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    float xb[3], pw[3];
+    vertex_frames(F, lv, v, xb, pw);
+    Res<OV> r;
+    eval_shape<OV, ClsTraits<XP>::XPM, ClsTraits<XP>::FLAT>(a.S, U.SB, xb, r);
+    float n[3];
+    rot_vec(F.RB, r.g, n);
+    sv[VD * V + v] = r.v;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) sv[(VN + i) * V + v] = n[i];
+    float h[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if constexpr (TIER >= 2) {
+      rot_sym(F.RB, r.h, h);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) sv[(VH + k) * V + v] = h[k];
+    }
+    if (full) {
+      CM_COLS(U.side);
+      store_candidate<TIER>(a.out, a.C, U.off + v, pw, n, r.v, h, nullptr, nullptr, F, 0, itcmp, cTA, cRA, cTB, cRB);
+    }
+  }
+}
+
+// ---- phase 2: sphere traces (Fig. 2), 2 per edge ----------------
+template <int TIER, int XP>
+__global__ void __launch_bounds__(CM_MF_MAX_THREADS) k_mf_traces(const MfArgs a) {
+  __shared__ UnitCtx U;
+  if (!unit_setup(a, U)) return;
+  constexpr int OT = TIER >= 2 ? 1 : 0;   // order inside the trace
+  const SmoothDev sp = a.S.sp;
+  const float itcmp = 1.f / sp.tau_cmp;
+  const float tca = sp.tau_clip_alpha, itca = 1.f / tca;
+  const PairFrame& F = U.F;
+  const int V = U.SA.V, E = U.SA.E;
+  const float* sv = a.scratch + (int64_t)blockIdx.x * a.slot;
+  float* se = a.scratch + (int64_t)blockIdx.x * a.slot + (int64_t)vfields(TIER) * V;
+  const float* lv = a.S.verts + 3 * (int64_t)U.SA.v_off;
+  const int32_t* ed = a.S.edges + 2 * (int64_t)U.SA.e_off;
+  for (int j = threadIdx.x; j < 2 * E; j += blockDim.x) {
+    const int e = j < E ? j : j - E;
+    const int dir = j < E ? 0 : 1;     // 0: from v_I along +e_t; 1: from v_II along -e_t
+    int vI, vII;
+    float el[3], L;
+    edge_dir(lv, ed, e, vI, vII, el, L);
+    float eb[3], ew[3];
+    rot_vec(F.Rrel, el, eb);
+    rot_vec(F.RA, el, ew);
+    float xI[3], pI[3];
+    vertex_frames(F, lv, vI, xI, pI);
+    const int v0 = dir ? vII : vI;
+    float al = dir ? L : 0.f;
+    const float sgn = dir ? -1.f : 1.f;
+    float da[NDQ];
+#pragma unroll
+    for (int k = 0; k < NDQ; ++k) da[k] = 0.f;
+    for (int it = 0; it < sp.iters; ++it) {
+      float phi, g[3];
+      if (it == 0) {   // the corner itself: reuse the vertex evaluation (reading #22)
+        phi = sv[VD * V + v0];
+        g[0] = sv[(VN + 0) * V + v0]; g[1] = sv[(VN + 1) * V + v0]; g[2] = sv[(VN + 2) * V + v0];
+      } else {
+        const float xb[3] = {fmaf(al, eb[0], xI[0]), fmaf(al, eb[1], xI[1]), fmaf(al, eb[2], xI[2])};
+        Res<OT> r;
+        eval_shape<OT, ClsTraits<XP>::XPM, ClsTraits<XP>::FLAT>(a.S, U.SB, xb, r);
+        phi = r.v;
+        if constexpr (TIER >= 2) rot_vec(F.RB, r.g, g);
+      }
+      // gated step G(phi) = sigma(phi / tau) phi  (reading #20)
+      const float s = sigm(phi * itcmp);
+      if constexpr (TIER >= 2) {
+        // d alpha_{k+1} = d alpha_k + sgn G'(phi) [g^T J(p) dq + (g.e_t) d alpha_k]
+        const float Gp = fmaf(phi * s * (1.f - s), itcmp, s);
+        const float p[3] = {fmaf(al, ew[0], pI[0]), fmaf(al, ew[1], pI[1]), fmaf(al, ew[2], pI[2])};
+        float gj[NDQ];
+        gJ(g, p, F, gj);
+        const float ge = g[0] * ew[0] + g[1] * ew[1] + g[2] * ew[2];
+        const float c = sgn * Gp;
+#pragma unroll
+        for (int k = 0; k < NDQ; ++k) da[k] = fmaf(c, fmaf(ge, da[k], gj[k]), da[k]);
+      }
+      al = fmaf(sgn * s, phi, al);
+    }
+    // soft clip to the edge (reading #21)
+    se[(dir ? TB : TA) * E + e] = softclip(al, 0.f, L, tca, itca);
+    if constexpr (TIER >= 2) {
+      const float cd = softclip_d(al, 0.f, L, itca);
+      const int base = dir ? TDB : TDA;
+#pragma unroll
+      for (int k = 0; k < NDQ; ++k) se[(base + k) * E + e] = cd * da[k];
+    }
+  }
+}
+
+// ---- phase 3: edge points p_e = v_I + a_bar e_t, a_bar = (a_I + a_II)/2
+template <int TIER, int XP>
+__global__ void __launch_bounds__(CM_MF_MAX_THREADS) k_mf_midpoints(const MfArgs a) {
+  __shared__ UnitCtx U;
+  if (!unit_setup(a, U)) return;
+  constexpr int OV = TIER >= 2 ? 2 : 1;
+  const PairFrame& F = U.F;
+  const int V = U.SA.V, E = U.SA.E;
+  float* se = a.scratch + (int64_t)blockIdx.x * a.slot + (int64_t)vfields(TIER) * V;
+  const float* lv = a.S.verts + 3 * (int64_t)U.SA.v_off;
+  const int32_t* ed = a.S.edges + 2 * (int64_t)U.SA.e_off;
+  const bool full = (a.mode & CM_FULL_MODE) != 0;
+  const float itcmp = 1.f / a.S.sp.tau_cmp;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int vI, vII;
+    float el[3], L;
+    edge_dir(lv, ed, e, vI, vII, el, L);
+    float eb[3], ew[3];
+    rot_vec(F.Rrel, el, eb);
+    rot_vec(F.RA, el, ew);
+    const float ab = 0.5f * (se[TA * E + e] + se[TB * E + e]);
+    float dab[NDQ];
+    if constexpr (TIER >= 2) {
+#pragma unroll
+      for (int k = 0; k < NDQ; ++k) dab[k] = 0.5f * (se[(TDA + k) * E + e] + se[(TDB + k) * E + e]);
+    }
+    float xI[3], pI[3];
+    vertex_frames(F, lv, vI, xI, pI);
+    float xb[3], pw[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      xb[i] = fmaf(ab, eb[i], xI[i]);
+      pw[i] = fmaf(ab, ew[i], pI[i]);
+    }
+    Res<OV> r;
+    eval_shape<OV, ClsTraits<XP>::XPM, ClsTraits<XP>::FLAT>(a.S, U.SB, xb, r);
+    float n[3];
+    rot_vec(F.RB, r.g, n);
+    se[MAB * E + e] = ab;
+    se[MD * E + e] = r.v;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) se[(MN + i) * E + e] = n[i];
+    float h[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if constexpr (TIER >= 2) {
+      rot_sym(F.RB, r.h, h);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) se[(MH + k) * E + e] = h[k];
+#pragma unroll
+      for (int k = 0; k < NDQ; ++k) se[(MDAB + k) * E + e] = dab[k];
+    }
+    if (full) {
+      CM_COLS(U.side);
+      store_candidate<TIER>(a.out, a.C, U.off + V + e, pw, n, r.v, h, ew, dab, F, 1, itcmp, cTA, cRA, cTB, cRB);
+    }
+  }
+}
+
+// ---- phase 4: per-face fusion ---------------------------------
+// STAGED: the unit's candidate state is first copied (coalesced) into shared
+// memory together with the candidates' world points p and the edges' world
+// directions e_t, computed once per vertex / edge instead of once per face;
+// the face loop then gathers from shared memory.  Units too large for shared
+// memory gather from the scratch slot and recompute p, e_t per face.
+// Staged layout: the slot's used region [vfields x V | efields x E] copied
+// by one TMA bulk copy (cp.async.bulk, completion on an mbarrier), then
+// p[3][V] of the vertices and p_I[3][E], e_t[3][E] of the edges (the edge
+// point is p_I + a_bar e_t).
+__host__ __device__ constexpr int round4(int x) { return (x + 3) & ~3; }
+__host__ __device__ constexpr int face_stage_floats(int V, int E, int tier) {
+  return round4(vfields(tier) * V + efields(tier) * E) + 3 * V + 6 * E;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// global -> shared bulk copy of `bytes` (multiple of 16, 16-B aligned ends)
+// by the calling thread; completion is counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n"
+      ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+
+template <int TIER, bool STAGED>
+__global__ void __launch_bounds__(CM_MF_MAX_THREADS, CM_MF_FACE_MINB) k_mf_faces(const MfArgs a) {
+  extern __shared__ __align__(16) float fsm[];
+  __shared__ UnitCtx U;
+  __shared__ uint64_t bar;
+  if (STAGED && threadIdx.x == 0) mbar_init(&bar, 1);   // published by unit_setup's barrier
+  if (!unit_setup(a, U)) return;
+  const SmoothDev sp = a.S.sp;
+  const float itcmp = 1.f / sp.tau_cmp;
+  const float tmin = sp.tau_min, itmin = 1.f / tmin;
+  const PairFrame& F = U.F;
+  const int V = U.SA.V, E = U.SA.E, NF = U.SA.F;
+  constexpr int VF = vfields(TIER), EF = efields(TIER);
+  const float* gv = a.scratch + (int64_t)blockIdx.x * a.slot;
+  const float* ge = gv + (int64_t)VF * V;
+  const float* lv = a.S.verts + 3 * (int64_t)U.SA.v_off;
+  const int32_t* ed = a.S.edges + 2 * (int64_t)U.SA.e_off;
+  const int32_t* fv = a.S.faces + 3 * (int64_t)U.SA.f_off;
+  const int32_t* fe = a.S.face_edges + 3 * (int64_t)U.SA.f_off;
+  const cm_manifold_out& out = a.out;
+  const int64_t C = a.C;
+  const float* sv = gv;
+  const float* se = ge;
+  float* s_pv = nullptr;   // staged vertex points p[3][V]
+  float* s_pe = nullptr;   // staged edge p_I[3][E], e_t[3][E]
+  if constexpr (STAGED) {
+    const int used = round4(VF * V + EF * E);
+    if (threadIdx.x == 0) bulk_g2s(fsm, gv, (uint32_t)used * 4u, &bar);
+    s_pv = fsm + used;
+    s_pe = s_pv + 3 * V;
+    // overlapped with the copy: the candidates' world geometry
     for (int v = threadIdx.x; v < V; v += blockDim.x) {
-      const float x[3] = {__ldg(lv + 3 * v), __ldg(lv + 3 * v + 1), __ldg(lv + 3 * v + 2)};
       float xb[3], pw[3];
+      vertex_frames(F, lv, v, xb, pw);
 #pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        xb[i] = F.Rrel[i * 3] * x[0] + F.Rrel[i * 3 + 1] * x[1] + F.Rrel[i * 3 + 2] * x[2] + F.trel[i];
-        pw[i] = F.RA[i * 3] * x[0] + F.RA[i * 3 + 1] * x[1] + F.RA[i * 3 + 2] * x[2] + F.tA[i];
-      }
-      Res<OV> r;
-      eval_shape<OV, ClsTraits<XP>::XPM, ClsTraits<XP>::FLAT>(S, SB, xb, r);
-      float n[3];
-      rot_vec(F.RB, r.g, n);
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        sv[(VX + i) * V + v] = xb[i];
-        sv[(VP + i) * V + v] = pw[i];
-        sv[(VN + i) * V + v] = n[i];
-      }
-      sv[VD * V + v] = r.v;
-      float h[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      if constexpr (TIER >= 2) {
-        rot_sym(F.RB, r.h, h);
-#pragma unroll
-        for (int k = 0; k < 6; ++k) sv[(VH + k) * V + v] = h[k];
-      }
-      if (full)
-        store_candidate<TIER>(out, C, s_off + v, pw, n, r.v, h, nullptr, nullptr, F, 0, itcmp, cTA, cRA, cTB, cRB);
+      for (int k = 0; k < 3; ++k) s_pv[k * V + v] = pw[k];
     }
-    __syncthreads();
-    CM_PT(1);
-
-    // ---- phase 2: sphere traces (Fig. 2), 2 per edge -------------
-    for (int j = threadIdx.x; j < 2 * E; j += blockDim.x) {
-      const int e = j < E ? j : j - E;
-      const int dir = j < E ? 0 : 1;     // 0: from v_I along +e_t; 1: from v_II along -e_t
-      const int vI = __ldg(ed + 2 * e), vII = __ldg(ed + 2 * e + 1);
-      const float dl[3] = {__ldg(lv + 3 * vII) - __ldg(lv + 3 * vI), __ldg(lv + 3 * vII + 1) - __ldg(lv + 3 * vI + 1),
-                           __ldg(lv + 3 * vII + 2) - __ldg(lv + 3 * vI + 2)};
-      const float L = sqrtf(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
-      const float iL = 1.f / L;
-      const float el[3] = {dl[0] * iL, dl[1] * iL, dl[2] * iL};
-      float eb[3], ew[3];
-      rot_vec(F.Rrel, el, eb);
-      rot_vec(F.RA, el, ew);
-      const float xI[3] = {sv[(VX + 0) * V + vI], sv[(VX + 1) * V + vI], sv[(VX + 2) * V + vI]};
-      const float pI[3] = {sv[(VP + 0) * V + vI], sv[(VP + 1) * V + vI], sv[(VP + 2) * V + vI]};
-      const int v0 = dir ? vII : vI;
-      float al = dir ? L : 0.f;
-      const float sgn = dir ? -1.f : 1.f;
-      float da[NDQ];
-#pragma unroll
-      for (int k = 0; k < NDQ; ++k) da[k] = 0.f;
-      for (int it = 0; it < sp.iters; ++it) {
-        float phi, g[3];
-        if (it == 0) {   // the corner itself: reuse the vertex evaluation (reading #22)
-          phi = sv[VD * V + v0];
-          g[0] = sv[(VN + 0) * V + v0]; g[1] = sv[(VN + 1) * V + v0]; g[2] = sv[(VN + 2) * V + v0];
-        } else {
-          const float xb[3] = {fmaf(al, eb[0], xI[0]), fmaf(al, eb[1], xI[1]), fmaf(al, eb[2], xI[2])};
-          Res<OT> r;
-          eval_shape<OT, ClsTraits<XP>::XPM, ClsTraits<XP>::FLAT>(S, SB, xb, r);
-          phi = r.v;
-          if constexpr (TIER >= 2) rot_vec(F.RB, r.g, g);
-        }
-        // gated step G(phi) = sigma(phi / tau) phi  (reading #20)
-        const float s = sigm(phi * itcmp);
-        if constexpr (TIER >= 2) {
-          // d alpha_{k+1} = d alpha_k + sgn G'(phi) [g^T J(p) dq + (g.e_t) d alpha_k]
-          const float Gp = fmaf(phi * s * (1.f - s), itcmp, s);
-          const float p[3] = {fmaf(al, ew[0], pI[0]), fmaf(al, ew[1], pI[1]), fmaf(al, ew[2], pI[2])};
-          float gj[NDQ];
-          gJ(g, p, F, gj);
-          const float ge = g[0] * ew[0] + g[1] * ew[1] + g[2] * ew[2];
-          const float c = sgn * Gp;
-#pragma unroll
-          for (int k = 0; k < NDQ; ++k) da[k] = fmaf(c, fmaf(ge, da[k], gj[k]), da[k]);
-        }
-        al = fmaf(sgn * s, phi, al);
-      }
-      // soft clip to the edge (reading #21)
-      const float at = softclip(al, 0.f, L, tca, itca);
-      se[(dir ? EB : EA) * E + e] = at;
-      if constexpr (TIER >= 2) {
-        const float cd = softclip_d(al, 0.f, L, itca);
-        const int base = dir ? EDB : EDA;
-#pragma unroll
-        for (int k = 0; k < NDQ; ++k) se[(base + k) * E + e] = cd * da[k];
-      }
-    }
-    __syncthreads();
-    CM_PT(2);
-
-    // ---- phase 3: edge midpoints p_e = (p_I + p_II)/2 ----------------
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
-      const int vI = __ldg(ed + 2 * e), vII = __ldg(ed + 2 * e + 1);
-      const float dl[3] = {__ldg(lv + 3 * vII) - __ldg(lv + 3 * vI), __ldg(lv + 3 * vII + 1) - __ldg(lv + 3 * vI + 1),
-                           __ldg(lv + 3 * vII + 2) - __ldg(lv + 3 * vI + 2)};
-      const float iL = rsqrtf(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
-      const float el[3] = {dl[0] * iL, dl[1] * iL, dl[2] * iL};
-      float eb[3], ew[3];
-      rot_vec(F.Rrel, el, eb);
+      int vI, vII;
+      float el[3], L, ew[3], xb[3], pI[3];
+      edge_dir(lv, ed, e, vI, vII, el, L);
       rot_vec(F.RA, el, ew);
-      const float ab = 0.5f * (se[EA * E + e] + se[EB * E + e]);
-      float dab[NDQ];
-      if constexpr (TIER >= 2) {
+      vertex_frames(F, lv, vI, xb, pI);
 #pragma unroll
-        for (int k = 0; k < NDQ; ++k) dab[k] = 0.5f * (se[(EDA + k) * E + e] + se[(EDB + k) * E + e]);
+      for (int k = 0; k < 3; ++k) {
+        s_pe[k * E + e] = pI[k];
+        s_pe[(3 + k) * E + e] = ew[k];
       }
-      float xb[3], pw[3];
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        xb[i] = fmaf(ab, eb[i], sv[(VX + i) * V + vI]);
-        pw[i] = fmaf(ab, ew[i], sv[(VP + i) * V + vI]);
-      }
-      Res<OV> r;
-      eval_shape<OV, ClsTraits<XP>::XPM, ClsTraits<XP>::FLAT>(S, SB, xb, r);
-      float n[3];
-      rot_vec(F.RB, r.g, n);
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        se[(EP + i) * E + e] = pw[i];
-        se[(EN + i) * E + e] = n[i];
-      }
-      se[ED * E + e] = r.v;
-      float h[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      if constexpr (TIER >= 2) {
-        rot_sym(F.RB, r.h, h);
-#pragma unroll
-        for (int k = 0; k < 6; ++k) se[(EH + k) * E + e] = h[k];
-#pragma unroll
-        for (int k = 0; k < NDQ; ++k) se[(EDAB + k) * E + e] = dab[k];
-      }
-      if (full)
-        store_candidate<TIER>(out, C, s_off + V + e, pw, n, r.v, h, ew, dab, F, 1, itcmp, cTA, cRA, cTB, cRB);
     }
+    mbar_wait(&bar, 0);
     __syncthreads();
-    CM_PT(3);
-    if (full) continue;   // full mode: every candidate was written above
-
-    // ---- phase 4: per-face fusion -------------------------------
-    const int64_t off = s_off;
-    const int32_t* fv = S.faces + 3 * (int64_t)sa.f_off;
-    const int32_t* fe = S.face_edges + 3 * (int64_t)sa.f_off;
-    const float itlm = LOG2E * itmin;
-    for (int f = threadIdx.x; f < NF; f += blockDim.x) {
-      int cv[3], ce[3];
+    sv = fsm;
+    se = fsm + VF * V;
+  }
+  CM_COLS(U.side);
+  const float itlm = LOG2E * itmin;
+  for (int f = threadIdx.x; f < NF; f += blockDim.x) {
+    int cv[3], ce[3];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) { cv[k] = __ldg(fv + 3 * f + k); ce[k] = __ldg(fe + 3 * f + k); }
-      // candidate depths d_i; order [v_i0, v_i1, v_i2, e(i0,i1), e(i1,i2), e(i2,i0)]
-      float dc[6];
+    for (int k = 0; k < 3; ++k) { cv[k] = __ldg(fv + 3 * f + k); ce[k] = __ldg(fe + 3 * f + k); }
+    // candidate depths d_i; order [v_i0, v_i1, v_i2, e(i0,i1), e(i1,i2), e(i2,i0)]
+    float dc[6];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) { dc[k] = sv[VD * V + cv[k]]; dc[3 + k] = se[ED * E + ce[k]]; }
-      float dm = dc[0];
+    for (int k = 0; k < 3; ++k) { dc[k] = sv[VD * V + cv[k]]; dc[3 + k] = se[MD * E + ce[k]]; }
+    // candidate points (world): vertices RA x + tA, edge points p_I + a_bar e_t
+    // (the same arithmetic as the vertex / midpoint kernels), and the edges'
+    // world directions e_t for the sliding terms
+    float pc[6][3], ewc[3][3];
 #pragma unroll
-      for (int i = 1; i < 6; ++i) dm = fminf(dm, dc[i]);
-      float z[6], Z = 0.f;
+    for (int k = 0; k < 3; ++k) {
+      if constexpr (STAGED) {
+        const float ab = se[MAB * E + ce[k]];
 #pragma unroll
-      for (int i = 0; i < 6; ++i) { z[i] = ex2((dm - dc[i]) * itlm); Z += z[i]; }
-      const float iZ = 1.f / Z;
-      float zg[6];
-      float Wf = 0.f;
-      int dom = 0;
+        for (int i = 0; i < 3; ++i) {
+          pc[k][i] = s_pv[i * V + cv[k]];
+          ewc[k][i] = s_pe[(3 + i) * E + ce[k]];
+          pc[3 + k][i] = fmaf(ab, ewc[k][i], s_pe[i * E + ce[k]]);
+        }
+      } else {
+        float xb[3];
+        vertex_frames(F, lv, cv[k], xb, pc[k]);
+        int vI, vII;
+        float el[3], L;
+        edge_dir(lv, ed, ce[k], vI, vII, el, L);
+        rot_vec(F.RA, el, ewc[k]);
+        float pI[3];
+        vertex_frames(F, lv, vI, xb, pI);
+        const float ab = se[MAB * E + ce[k]];
 #pragma unroll
-      for (int i = 0; i < 6; ++i) {
-        z[i] *= iZ;                                   // z = s_argmax(-d)
-        const float gam = sigm(-dc[i] * itcmp);        // gamma = [[d < 0]]
-        zg[i] = z[i] * gam;
-        Wf += zg[i];
-        // dominant candidate argmax z_i gamma_i = argmin d_i (both factors
-        // decrease with d_i); taken on d so it survives weight underflow
-        if (dc[i] < dc[dom]) dom = i;
+        for (int i = 0; i < 3; ++i) pc[3 + k][i] = fmaf(ab, ewc[k][i], pI[i]);
       }
-      const float depth = fmaf(-tmin * LN2, lg2(Z), dm);   // smooth min (reading #25)
-      float nrm[3] = {0.f, 0.f, 0.f}, qv[3] = {0.f, 0.f, 0.f}, pt[3] = {0.f, 0.f, 0.f};
+    }
+    float dm = dc[0];
+#pragma unroll
+    for (int i = 1; i < 6; ++i) dm = fminf(dm, dc[i]);
+    float z[6], Z = 0.f;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) { z[i] = ex2((dm - dc[i]) * itlm); Z += z[i]; }
+    const float iZ = 1.f / Z;
+    float zg[6];
+    float Wf = 0.f;
+    int dom = 0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      z[i] *= iZ;                                   // z = s_argmax(-d)
+      const float gam = sigm(-dc[i] * itcmp);        // gamma = [[d < 0]]
+      zg[i] = z[i] * gam;
+      Wf += zg[i];
+      // dominant candidate argmax z_i gamma_i = argmin d_i (both factors
+      // decrease with d_i); taken on d so it survives weight underflow
+      if (dc[i] < dc[dom]) dom = i;
+    }
+    const float depth = fmaf(-tmin * LN2, lg2(Z), dm);   // smooth min (reading #25)
+    float nrm[3] = {0.f, 0.f, 0.f}, qv[3] = {0.f, 0.f, 0.f}, pt[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      const bool isv = i < 3;
+      const int id = isv ? cv[i] : ce[i - 3];
+      const float* bn = isv ? sv + VN * V + id : se + MN * E + id;
+      const int sd = isv ? V : E;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float p = pc[i][k], nn = bn[k * sd];
+        nrm[k] = fmaf(zg[i], nn, nrm[k]);
+        qv[k] = fmaf(zg[i], p, qv[k]);
+        pt[k] = fmaf(z[i], p, pt[k]);
+      }
+    }
+    const int64_t c = U.off + f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      out.point[k * C + c] = pt[k];
+      out.normal[k * C + c] = nrm[k];
+    }
+    out.depth[c] = depth;
+    out.dom[c] = (int8_t)dom;
+    if constexpr (TIER >= 1) {
+      out.W[c] = Wf;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) out.q[k * C + c] = qv[k];
+    }
+    if constexpr (TIER >= 2) {
+      // Tier-2 derivatives in one pass over the 6 candidates.
+      // With g_i = n_i, r = p - t:  d d_i = [g, p x g - tA x g, -(p x g) + tB x g]
+      //   (+ (g.e_t) d alpha_bar for edge points),
+      //   d depth = sum z_i d d_i,
+      //   d n = sum_i c_i n_i (x) d d_i + itmin nbar (x) d depth + sum_i zg_i d n_i,
+      //   c_i = zg_i (-1/tau_min - (1 - gamma_i)/tau_cmp),
+      //   d n_i = [H, -H[p - tA]x, H[p - tB]x - [n]x] (+ H e_t (x) d alpha_bar).
+      // The sums collapse to a few moments of the candidates:
+      //   K = sum c n n^T, L = sum c n (p x n)^T, Hb = sum zg H, M = sum zg H[p]x
+      //   -> d n = [K + Hb, L + K[tA]x + Hb[tA]x - M, -L - K[tB]x + M - Hb[tB]x - [nbar]x]
+      //          + itmin nbar (x) d depth + sum_edges (c ge n + zg H e_t) (x) d alpha_bar
+      float Sg[3] = {0.f, 0.f, 0.f}, Spg[3] = {0.f, 0.f, 0.f}, Se[NDQ];
+      float K[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, Hb[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      float Lm[9], Mm[9], dnE[3][NDQ];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) { Se[k] = 0.f; Lm[k] = 0.f; Mm[k] = 0.f; }
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int k = 0; k < NDQ; ++k) dnE[q][k] = 0.f;
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
         const bool isv = i < 3;
         const int id = isv ? cv[i] : ce[i - 3];
-        const float* bp = isv ? sv + VP * V + id : se + EP * E + id;
-        const float* bn = isv ? sv + VN * V + id : se + EN * E + id;
+        const float* bn = isv ? sv + VN * V + id : se + MN * E + id;
+        const float* bh = isv ? sv + VH * V + id : se + MH * E + id;
         const int sd = isv ? V : E;
+        const float* p = pc[i];
+        const float n[3] = {bn[0], bn[sd], bn[2 * sd]};
+        const float h[6] = {bh[0], bh[sd], bh[2 * sd], bh[3 * sd], bh[4 * sd], bh[5 * sd]};
+        const float gam = sigm(-dc[i] * itcmp);
+        const float w = zg[i];
+        const float ci = w * (-itmin - (1.f - gam) * itcmp);
+        const float pxn[3] = {p[1] * n[2] - p[2] * n[1], p[2] * n[0] - p[0] * n[2], p[0] * n[1] - p[1] * n[0]};
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          const float p = bp[a * sd], nn = bn[a * sd];
-          nrm[a] = fmaf(zg[i], nn, nrm[a]);
-          qv[a] = fmaf(zg[i], p, qv[a]);
-          pt[a] = fmaf(z[i], p, pt[a]);
+        for (int q = 0; q < 3; ++q) {
+          Sg[q] = fmaf(z[i], n[q], Sg[q]);
+          Spg[q] = fmaf(z[i], pxn[q], Spg[q]);
+        }
+        const float cn[3] = {ci * n[0], ci * n[1], ci * n[2]};
+        K[0] = fmaf(cn[0], n[0], K[0]); K[1] = fmaf(cn[0], n[1], K[1]); K[2] = fmaf(cn[0], n[2], K[2]);
+        K[3] = fmaf(cn[1], n[1], K[3]); K[4] = fmaf(cn[1], n[2], K[4]); K[5] = fmaf(cn[2], n[2], K[5]);
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) Lm[q * 3 + b] = fmaf(cn[q], pxn[b], Lm[q * 3 + b]);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) Hb[k] = fmaf(w, h[k], Hb[k]);
+        const float H[3][3] = {{h[0], h[1], h[2]}, {h[1], h[3], h[4]}, {h[2], h[4], h[5]}};
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          // (H [p]x) row q
+          Mm[q * 3 + 0] = fmaf(w, H[q][1] * p[2] - H[q][2] * p[1], Mm[q * 3 + 0]);
+          Mm[q * 3 + 1] = fmaf(w, H[q][2] * p[0] - H[q][0] * p[2], Mm[q * 3 + 1]);
+          Mm[q * 3 + 2] = fmaf(w, H[q][0] * p[1] - H[q][1] * p[0], Mm[q * 3 + 2]);
+        }
+        if (!isv) {
+          // sliding along the edge: e_t (world, unit) and d alpha_bar
+          const float* ew = ewc[i - 3];
+          const float ge = n[0] * ew[0] + n[1] * ew[1] + n[2] * ew[2];
+          float u[3];   // c ge n + zg H e_t
+#pragma unroll
+          for (int q = 0; q < 3; ++q) u[q] = fmaf(ci * ge, n[q], w * (H[q][0] * ew[0] + H[q][1] * ew[1] + H[q][2] * ew[2]));
+          const float zge = z[i] * ge;
+#pragma unroll
+          for (int k = 0; k < NDQ; ++k) {
+            const float dk = se[(MDAB + k) * E + id];
+            Se[k] = fmaf(zge, dk, Se[k]);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) dnE[q][k] = fmaf(u[q], dk, dnE[q][k]);
+          }
         }
       }
-      const int64_t c = off + f;
+      // d depth = [Sg, Spg - tA x Sg, -Spg + tB x Sg] + Se
+      const float* tA = F.tA;
+      const float* tB = F.tB;
+      float dd[NDQ];
+      dd[0] = Sg[0] + Se[0]; dd[1] = Sg[1] + Se[1]; dd[2] = Sg[2] + Se[2];
+      dd[3] = Spg[0] - (tA[1] * Sg[2] - tA[2] * Sg[1]) + Se[3];
+      dd[4] = Spg[1] - (tA[2] * Sg[0] - tA[0] * Sg[2]) + Se[4];
+      dd[5] = Spg[2] - (tA[0] * Sg[1] - tA[1] * Sg[0]) + Se[5];
+      dd[6] = -Spg[0] + (tB[1] * Sg[2] - tB[2] * Sg[1]) + Se[6];
+      dd[7] = -Spg[1] + (tB[2] * Sg[0] - tB[0] * Sg[2]) + Se[7];
+      dd[8] = -Spg[2] + (tB[0] * Sg[1] - tB[1] * Sg[0]) + Se[8];
+      // d n rows
+      const float Ks[3][3] = {{K[0], K[1], K[2]}, {K[1], K[3], K[4]}, {K[2], K[4], K[5]}};
+      const float Hs[3][3] = {{Hb[0], Hb[1], Hb[2]}, {Hb[1], Hb[3], Hb[4]}, {Hb[2], Hb[4], Hb[5]}};
+      float dn[3][NDQ];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        out.point[a * C + c] = pt[a];
-        out.normal[a * C + c] = nrm[a];
-      }
-      out.depth[c] = depth;
-      out.dom[c] = (int8_t)dom;
-      if constexpr (TIER >= 1) {
-        out.W[c] = Wf;
+      for (int q = 0; q < 3; ++q) {
+        const float KH[3] = {Ks[q][0] + Hs[q][0], Ks[q][1] + Hs[q][1], Ks[q][2] + Hs[q][2]};
+        // (X [t]x) row q for X = K + Hb, t = tA and tB
+        const float xA[3] = {KH[1] * tA[2] - KH[2] * tA[1], KH[2] * tA[0] - KH[0] * tA[2], KH[0] * tA[1] - KH[1] * tA[0]};
+        const float KtB[3] = {Ks[q][1] * tB[2] - Ks[q][2] * tB[1], Ks[q][2] * tB[0] - Ks[q][0] * tB[2],
+                              Ks[q][0] * tB[1] - Ks[q][1] * tB[0]};
+        const float HtB[3] = {Hs[q][1] * tB[2] - Hs[q][2] * tB[1], Hs[q][2] * tB[0] - Hs[q][0] * tB[2],
+                              Hs[q][0] * tB[1] - Hs[q][1] * tB[0]};
+        // [nbar]x row q
+        const float nk[3] = {q == 0 ? 0.f : (q == 1 ? nrm[2] : -nrm[1]), q == 0 ? -nrm[2] : (q == 1 ? 0.f : nrm[0]),
+                             q == 0 ? nrm[1] : (q == 1 ? -nrm[0] : 0.f)};
+        const float nb = nrm[q] * itmin;
 #pragma unroll
-        for (int a = 0; a < 3; ++a) out.q[a * C + c] = qv[a];
-      }
-      if constexpr (TIER >= 2) {
-        // Tier-2 derivatives in one pass over the 6 candidates.
-        // With g_i = n_i, r = p - t:  d d_i = [g, p x g - tA x g, -(p x g) + tB x g]
-        //   (+ (g.e_t) d alpha_bar for edge points),
-        //   d depth = sum z_i d d_i,
-        //   d n = sum_i c_i n_i (x) d d_i + itmin nbar (x) d depth + sum_i zg_i d n_i,
-        //   c_i = zg_i (-1/tau_min - (1 - gamma_i)/tau_cmp),
-        //   d n_i = [H, -H[p - tA]x, H[p - tB]x - [n]x] (+ H e_t (x) d alpha_bar).
-        // The sums collapse to a few moments of the candidates:
-        //   K = sum c n n^T, L = sum c n (p x n)^T, Hb = sum zg H, M = sum zg H[p]x
-        //   -> d n = [K + Hb, L + K[tA]x + Hb[tA]x - M, -L - K[tB]x + M - Hb[tB]x - [nbar]x]
-        //          + itmin nbar (x) d depth + sum_edges (c ge n + zg H e_t) (x) d alpha_bar
-        float Sg[3] = {0.f, 0.f, 0.f}, Spg[3] = {0.f, 0.f, 0.f}, Se[NDQ];
-        float K[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, Hb[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        float Lm[9], Mm[9], dnE[3][NDQ];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) { Se[k] = 0.f; Lm[k] = 0.f; Mm[k] = 0.f; }
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-          for (int k = 0; k < NDQ; ++k) dnE[a][k] = 0.f;
-#pragma unroll
-        for (int i = 0; i < 6; ++i) {
-          const bool isv = i < 3;
-          const int id = isv ? cv[i] : ce[i - 3];
-          const float* bp = isv ? sv + VP * V + id : se + EP * E + id;
-          const float* bn = isv ? sv + VN * V + id : se + EN * E + id;
-          const float* bh = isv ? sv + VH * V + id : se + EH * E + id;
-          const int sd = isv ? V : E;
-          const float p[3] = {bp[0], bp[sd], bp[2 * sd]};
-          const float n[3] = {bn[0], bn[sd], bn[2 * sd]};
-          const float h[6] = {bh[0], bh[sd], bh[2 * sd], bh[3 * sd], bh[4 * sd], bh[5 * sd]};
-          const float gam = sigm(-dc[i] * itcmp);
-          const float w = zg[i];
-          const float ci = w * (-itmin - (1.f - gam) * itcmp);
-          const float pxn[3] = {p[1] * n[2] - p[2] * n[1], p[2] * n[0] - p[0] * n[2], p[0] * n[1] - p[1] * n[0]};
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            Sg[a] = fmaf(z[i], n[a], Sg[a]);
-            Spg[a] = fmaf(z[i], pxn[a], Spg[a]);
-          }
-          const float cn[3] = {ci * n[0], ci * n[1], ci * n[2]};
-          K[0] = fmaf(cn[0], n[0], K[0]); K[1] = fmaf(cn[0], n[1], K[1]); K[2] = fmaf(cn[0], n[2], K[2]);
-          K[3] = fmaf(cn[1], n[1], K[3]); K[4] = fmaf(cn[1], n[2], K[4]); K[5] = fmaf(cn[2], n[2], K[5]);
-#pragma unroll
-          for (int a = 0; a < 3; ++a)
-#pragma unroll
-            for (int b = 0; b < 3; ++b) Lm[a * 3 + b] = fmaf(cn[a], pxn[b], Lm[a * 3 + b]);
-#pragma unroll
-          for (int k = 0; k < 6; ++k) Hb[k] = fmaf(w, h[k], Hb[k]);
-          const float H[3][3] = {{h[0], h[1], h[2]}, {h[1], h[3], h[4]}, {h[2], h[4], h[5]}};
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            // (H [p]x) row a
-            Mm[a * 3 + 0] = fmaf(w, H[a][1] * p[2] - H[a][2] * p[1], Mm[a * 3 + 0]);
-            Mm[a * 3 + 1] = fmaf(w, H[a][2] * p[0] - H[a][0] * p[2], Mm[a * 3 + 1]);
-            Mm[a * 3 + 2] = fmaf(w, H[a][0] * p[1] - H[a][1] * p[0], Mm[a * 3 + 2]);
-          }
-          if (!isv) {
-            // sliding along the edge: e_t (world, unit) and d alpha_bar
-            const int vI = __ldg(ed + 2 * id), vII = __ldg(ed + 2 * id + 1);
-            float ew[3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) ew[a] = sv[(VP + a) * V + vII] - sv[(VP + a) * V + vI];
-            const float il = rsqrtf(ew[0] * ew[0] + ew[1] * ew[1] + ew[2] * ew[2]);
-#pragma unroll
-            for (int a = 0; a < 3; ++a) ew[a] *= il;
-            const float ge = n[0] * ew[0] + n[1] * ew[1] + n[2] * ew[2];
-            float u[3];   // c ge n + zg H e_t
-#pragma unroll
-            for (int a = 0; a < 3; ++a) u[a] = fmaf(ci * ge, n[a], w * (H[a][0] * ew[0] + H[a][1] * ew[1] + H[a][2] * ew[2]));
-            const float zge = z[i] * ge;
-#pragma unroll
-            for (int k = 0; k < NDQ; ++k) {
-              const float dk = se[(EDAB + k) * E + id];
-              Se[k] = fmaf(zge, dk, Se[k]);
-#pragma unroll
-              for (int a = 0; a < 3; ++a) dnE[a][k] = fmaf(u[a], dk, dnE[a][k]);
-            }
-          }
+        for (int b = 0; b < 3; ++b) {
+          dn[q][b] = KH[b] + nb * dd[b] + dnE[q][b];
+          dn[q][3 + b] = Lm[q * 3 + b] + xA[b] - Mm[q * 3 + b] + nb * dd[3 + b] + dnE[q][3 + b];
+          dn[q][6 + b] = -Lm[q * 3 + b] - KtB[b] + Mm[q * 3 + b] - HtB[b] - nk[b] + nb * dd[6 + b] + dnE[q][6 + b];
         }
-        // d depth = [Sg, Spg - tA x Sg, -Spg + tB x Sg] + Se
-        const float* tA = F.tA;
-        const float* tB = F.tB;
-        float dd[NDQ];
-        dd[0] = Sg[0] + Se[0]; dd[1] = Sg[1] + Se[1]; dd[2] = Sg[2] + Se[2];
-        dd[3] = Spg[0] - (tA[1] * Sg[2] - tA[2] * Sg[1]) + Se[3];
-        dd[4] = Spg[1] - (tA[2] * Sg[0] - tA[0] * Sg[2]) + Se[4];
-        dd[5] = Spg[2] - (tA[0] * Sg[1] - tA[1] * Sg[0]) + Se[5];
-        dd[6] = -Spg[0] + (tB[1] * Sg[2] - tB[2] * Sg[1]) + Se[6];
-        dd[7] = -Spg[1] + (tB[2] * Sg[0] - tB[0] * Sg[2]) + Se[7];
-        dd[8] = -Spg[2] + (tB[0] * Sg[1] - tB[1] * Sg[0]) + Se[8];
-        // d n rows
-        const float Ks[3][3] = {{K[0], K[1], K[2]}, {K[1], K[3], K[4]}, {K[2], K[4], K[5]}};
-        const float Hs[3][3] = {{Hb[0], Hb[1], Hb[2]}, {Hb[1], Hb[3], Hb[4]}, {Hb[2], Hb[4], Hb[5]}};
-        float dn[3][NDQ];
+      }
+      // store: q order (tA 0-2, thetaA 3-5, tB 6-8 = -tA, thetaB 9-11)
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          const float KH[3] = {Ks[a][0] + Hs[a][0], Ks[a][1] + Hs[a][1], Ks[a][2] + Hs[a][2]};
-          // (X [t]x) row a for X = K + Hb, t = tA and tB
-          const float xA[3] = {KH[1] * tA[2] - KH[2] * tA[1], KH[2] * tA[0] - KH[0] * tA[2], KH[0] * tA[1] - KH[1] * tA[0]};
-          const float KtB[3] = {Ks[a][1] * tB[2] - Ks[a][2] * tB[1], Ks[a][2] * tB[0] - Ks[a][0] * tB[2],
-                                Ks[a][0] * tB[1] - Ks[a][1] * tB[0]};
-          const float HtB[3] = {Hs[a][1] * tB[2] - Hs[a][2] * tB[1], Hs[a][2] * tB[0] - Hs[a][0] * tB[2],
-                                Hs[a][0] * tB[1] - Hs[a][1] * tB[0]};
-          // [nbar]x row a
-          const float nk[3] = {a == 0 ? 0.f : (a == 1 ? nrm[2] : -nrm[1]), a == 0 ? -nrm[2] : (a == 1 ? 0.f : nrm[0]),
-                               a == 0 ? nrm[1] : (a == 1 ? -nrm[0] : 0.f)};
-          const float nb = nrm[a] * itmin;
+      for (int k = 0; k < 3; ++k) {
+        out.ddepth[(cTA + k) * C + c] = dd[k];
+        out.ddepth[(cRA + k) * C + c] = dd[3 + k];
+        out.ddepth[(cTB + k) * C + c] = -dd[k];
+        out.ddepth[(cRB + k) * C + c] = dd[6 + k];
+      }
 #pragma unroll
-          for (int b = 0; b < 3; ++b) {
-            dn[a][b] = KH[b] + nb * dd[b] + dnE[a][b];
-            dn[a][3 + b] = Lm[a * 3 + b] + xA[b] - Mm[a * 3 + b] + nb * dd[3 + b] + dnE[a][3 + b];
-            dn[a][6 + b] = -Lm[a * 3 + b] - KtB[b] + Mm[a * 3 + b] - HtB[b] - nk[b] + nb * dd[6 + b] + dnE[a][6 + b];
-          }
-        }
-        // store: q order (tA 0-2, thetaA 3-5, tB 6-8 = -tA, thetaB 9-11)
+      for (int q = 0; q < 3; ++q)
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-          out.ddepth[(cTA + k) * C + c] = dd[k];
-          out.ddepth[(cRA + k) * C + c] = dd[3 + k];
-          out.ddepth[(cTB + k) * C + c] = -dd[k];
-          out.ddepth[(cRB + k) * C + c] = dd[6 + k];
+          out.dnormal[(q * 12 + cTA + k) * C + c] = dn[q][k];
+          out.dnormal[(q * 12 + cRA + k) * C + c] = dn[q][3 + k];
+          out.dnormal[(q * 12 + cTB + k) * C + c] = -dn[q][k];
+          out.dnormal[(q * 12 + cRB + k) * C + c] = dn[q][6 + k];
         }
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            out.dnormal[(a * 12 + cTA + k) * C + c] = dn[a][k];
-            out.dnormal[(a * 12 + cRA + k) * C + c] = dn[a][3 + k];
-            out.dnormal[(a * 12 + cTB + k) * C + c] = -dn[a][k];
-            out.dnormal[(a * 12 + cRB + k) * C + c] = dn[a][6 + k];
-          }
-      }
     }
-#if CM_PHASE_TIMING
-    __syncthreads();
-#endif
-    CM_PT(4);
   }
 }
 
 namespace cml {
 
-int64_t manifold_smem_floats(int V, int E, int tier) {
-  return (int64_t)vfields(tier) * V + (int64_t)efields(tier) * E;
-}
-
-int manifold_max_smem_bytes() {
-  static int m = 0;
-  if (!m) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&m, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (m <= 0) m = 227 * 1024;
-  }
-  return m;
-}
-
-template <int TIER, int XP, int MB>
-static int launch_manifold_v(const SceneDev& s, int xp_filter, bool use_smem, int64_t need, const int32_t* pairs,
-                             int64_t n_pairs, const int64_t* offsets, const float* poses, int32_t n_slot,
-                             const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats,
-                             cudaStream_t st, uint32_t mode) {
-  const int threads = CM_MANIFOLD_THREADS;
-  int smem = use_smem ? (int)need : 0;
-  auto kern = k_contact_manifold<TIER, XP, MB>;
-  static int configured = 0;
-  if (smem > configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    configured = smem;
-  }
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
-  if (per_sm < 1) per_sm = 1;
-  int64_t grid = (int64_t)num_sms() * per_sm;
-  if (!use_smem) {
-    if (scratch == nullptr) {
-      set_error("manifold: surface too large for shared memory and no scratch");
-      return CM_ERR_UNSUPPORTED;
-    }
-    int64_t slots = scratch_floats / (need / 4);
-    if (grid > slots) grid = slots;
-    if (grid < 1) {
-      set_error("manifold: scratch too small");
-      return CM_ERR_UNSUPPORTED;
-    }
-  }
-  const int64_t n_units = (mode & CM_TWO_SIDED) ? 2 * n_pairs : n_pairs;
-  if (grid > n_units) grid = n_units;
-  if (grid < 1) return CM_OK;
-  kern<<<(unsigned)grid, threads, smem, st>>>(s, pairs, n_pairs, offsets, poses, n_slot, *out, C, xp_filter,
-                                              use_smem ? nullptr : scratch, use_smem ? 0 : need / 4, mode);
-  return check_launch("k_contact_manifold");
+// floats of one unit's scratch slot
+int64_t manifold_slot_floats(int V, int E, int tier) {
+  // multiple of 4 floats: every slot starts 16-B aligned (bulk copies)
+  return ((int64_t)vfields(tier) * V + (int64_t)efields(tier) * E + 3) & ~(int64_t)3;
 }
 
 template <int TIER, int XP>
-static int launch_manifold_t(const SceneDev& s, int xp_filter, int max_V, int max_E, const int32_t* pairs,
-                             int64_t n_pairs, const int64_t* offsets, const float* poses, int32_t n_slot,
-                             const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats,
-                             cudaStream_t st, uint32_t mode) {
-  const int64_t need = manifold_smem_floats(max_V, max_E, TIER) * 4;
-  const int static_smem = (int)(sizeof(PairFrame) + 2 * sizeof(ShapeRec));
-  const bool use_smem = need <= kSmemBudget && need + static_smem + 1024 <= manifold_max_smem_bytes();
-  // flat SQ-family SDFs: a 3-CTA/SM register budget pays off only when three
-  // pairs' state also fits in shared memory (else the tighter budget just spills)
-  if constexpr (XP == 0) {
-    const bool hi = !use_smem || 3 * (need + static_smem + 1024) <= 228 * 1024;
-    if (hi)
-      return launch_manifold_v<TIER, XP, CM_MANIFOLD_MINBLOCKS_FLAT>(s, xp_filter, use_smem, need, pairs, n_pairs,
-                                                                     offsets, poses, n_slot, out, C, scratch,
-                                                                     scratch_floats, st, mode);
+static int launch_sdf_phases(MfArgs& a, int64_t nb, int T, cudaStream_t st) {
+  k_mf_vertices<TIER, XP><<<(unsigned)nb, T, 0, st>>>(a);
+  int rc = check_launch("k_mf_vertices");
+  if (rc) return rc;
+  k_mf_traces<TIER, XP><<<(unsigned)nb, T, 0, st>>>(a);
+  if ((rc = check_launch("k_mf_traces"))) return rc;
+  k_mf_midpoints<TIER, XP><<<(unsigned)nb, T, 0, st>>>(a);
+  return check_launch("k_mf_midpoints");
+}
+
+constexpr int kStageSmallBytes = 24 * 1024;
+
+template <int TIER>
+static int launch_tier(MfArgs a, int class_mask, int max_V, int max_E, int64_t n_units, int64_t chunk,
+                       cudaStream_t const* streams, int n_streams) {
+  const bool full = (a.mode & CM_FULL_MODE) != 0;
+  const bool multi = (class_mask & (class_mask - 1)) != 0;
+  float* scratch0 = a.scratch;
+  // face-kernel staging in shared memory when the largest unit fits; used
+  // for small staged footprints and for chunks too small to fill the SMs
+  // anyway (measured: C4 / C2 gain 3-25%, C5 / C3 lose 8-10% to the lower
+  // occupancy)
+  int stage_bytes = (int)(face_stage_floats(max_V, max_E, TIER) * 4);
+  {
+    static int configured = 0;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (stage_bytes + (int)sizeof(UnitCtx) + 1024 > optin) {
+      stage_bytes = 0;
+    } else if (stage_bytes > configured) {
+      cudaFuncSetAttribute(k_mf_faces<TIER, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
+      configured = stage_bytes;
+    }
   }
-  return launch_manifold_v<TIER, XP, CM_MANIFOLD_MINBLOCKS>(s, xp_filter, use_smem, need, pairs, n_pairs, offsets,
-                                                            poses, n_slot, out, C, scratch, scratch_floats, st, mode);
+  // chunk k runs on stream k % n_streams in that stream's scratch region, so
+  // one chunk's kernel tails overlap the next chunk's kernels
+  for (int64_t u0 = 0, k = 0; u0 < n_units; u0 += chunk, ++k) {
+    const int64_t nb = n_units - u0 < chunk ? n_units - u0 : chunk;
+    cudaStream_t st = streams[k % n_streams];
+    a.unit0 = u0;
+    a.scratch = scratch0 + (k % n_streams) * chunk * a.slot;
+    // >= 32 resident warps per SM over the chunk's units (small batches)
+    int T = CM_MF_THREADS;
+    while (T < CM_MF_MAX_THREADS && nb * (T / 32) < (int64_t)num_sms() * 32) T *= 2;
+    int rc = CM_OK;
+    // SDF phases: one instantiation per SDF class present (0 SQ family flat,
+    // 1 constant-schedule XPSQ, 2 varying-schedule XPSQ, 3 nested SQ family);
+    // with several classes each launch skips the other classes' units
+    if (class_mask & 1) { a.xp_filter = multi ? 0 : -1; rc = launch_sdf_phases<TIER, 0>(a, nb, T, st); }
+    if (!rc && (class_mask & 2)) { a.xp_filter = multi ? 1 : -1; rc = launch_sdf_phases<TIER, 1>(a, nb, T, st); }
+    if (!rc && (class_mask & 4)) { a.xp_filter = multi ? 2 : -1; rc = launch_sdf_phases<TIER, 2>(a, nb, T, st); }
+    if (!rc && (class_mask & 8)) { a.xp_filter = multi ? 3 : -1; rc = launch_sdf_phases<TIER, 3>(a, nb, T, st); }
+    if (rc) return rc;
+    if (!full) {   // the fusion does not depend on the SDF class: one launch
+      a.xp_filter = -1;
+      if (stage_bytes > 0 && (stage_bytes <= kStageSmallBytes || nb < 8 * (int64_t)num_sms()))
+        k_mf_faces<TIER, true><<<(unsigned)nb, T, stage_bytes, st>>>(a);
+      else
+        k_mf_faces<TIER, false><<<(unsigned)nb, T, 0, st>>>(a);
+      if ((rc = check_launch("k_mf_faces"))) return rc;
+    }
+  }
+  return CM_OK;
 }
 
 int launch_manifold(const SceneDev& s, int class_mask, int max_V, int max_E, const int32_t* pairs,
                     int64_t n_pairs, const int64_t* offsets, const float* poses, int32_t n_slot, uint32_t flags,
-                    const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats, void* stream) {
-  // class_mask bit c: SDF shapes of class c present (0 SQ family, 1 constant
-  // schedule XPSQ, 2 varying-schedule XPSQ).  One instantiation per present
-  // class; with several classes each kernel skips the other classes' pairs.
-  cudaStream_t st = (cudaStream_t)stream;
+                    const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats,
+                    void* const* streams, int n_streams) {
   const int tier = (int)(flags & CM_TIER_MASK);
-  const bool multi = (class_mask & (class_mask - 1)) != 0;
-#define CM_L(T, X) launch_manifold_t<T, X>(s, multi ? X : -1, max_V, max_E, pairs, n_pairs, offsets, poses, n_slot, \
-                                           out, C, scratch, scratch_floats, st, flags & (CM_FULL_MODE | CM_TWO_SIDED))
-#define CM_T(X) (tier >= 2 ? CM_L(2, X) : (tier == 1 ? CM_L(1, X) : CM_L(0, X)))
-  int rc = CM_OK;
-  if (class_mask & 1) rc = CM_T(0);
-  if (!rc && (class_mask & 2)) rc = CM_T(1);
-  if (!rc && (class_mask & 4)) rc = CM_T(2);
-  if (!rc && (class_mask & 8)) rc = CM_T(3);
-#undef CM_T
-#undef CM_L
-  return rc;
+  const uint32_t mode = flags & (CM_FULL_MODE | CM_TWO_SIDED);
+  const int64_t n_units = (mode & CM_TWO_SIDED) ? 2 * n_pairs : n_pairs;
+  const int64_t slot = manifold_slot_floats(max_V, max_E, tier);
+  if (n_streams < 1) n_streams = 1;
+  int64_t chunk = slot > 0 ? scratch_floats / n_streams / slot : 0;
+  if (scratch == nullptr || chunk < 1) {
+    set_error("manifold: scene scratch missing or too small");
+    return CM_ERR_UNSUPPORTED;
+  }
+  if (chunk > 0x7fffffff) chunk = 0x7fffffff;
+  MfArgs a;
+  a.S = s;
+  a.pairs = pairs;
+  a.n_pairs = n_pairs;
+  a.unit0 = 0;
+  a.offsets = offsets;
+  a.poses = poses;
+  a.n_slot = n_slot;
+  a.out = *out;
+  a.C = C;
+  a.xp_filter = -1;
+  a.scratch = scratch;
+  a.slot = slot;
+  a.mode = mode;
+  cudaStream_t const* sts = (cudaStream_t const*)streams;
+  if (tier >= 2) return launch_tier<2>(a, class_mask, max_V, max_E, n_units, chunk, sts, n_streams);
+  if (tier == 1) return launch_tier<1>(a, class_mask, max_V, max_E, n_units, chunk, sts, n_streams);
+  return launch_tier<0>(a, class_mask, max_V, max_E, n_units, chunk, sts, n_streams);
 }
 
 }  // namespace cml

@@ -654,3 +654,50 @@ def c5_scene(n_env: int = 1 << 20, env_lo: int = 0, seed: int = 5) -> Scene:
         e = t
     return Scene("C5", shapes, smooth_params(0.1), pairs, poses.astype(F32), ell=0.1,
                  meta=dict(env_lo=env_lo, n_sampled=n_s, n_sdf=len(sdf)))
+
+
+def sdf_scene(n_body: int = 1 << 16, P: int = 64, env_lo: int = 0, seed: int = 6) -> Scene:
+    """sdf_eval workload (SURVEY §8d secondary metric): the 32 C5 SDF
+    prototypes, one body per batch item with a uniform rotation and a
+    translation U[-0.1, 0.1]^3, and P query points per body: samples of the
+    body's constituent surfaces (_sdf_surface_samples) jittered by N(0, 0.01^2)
+    per axis in the body frame, then moved to world.  Bodies
+    [env_lo, env_lo + n_body) of a global sequence keyed per block of 65536
+    bodies (rank shards, as c5_scene)."""
+    _, sdf = c5_library(5)
+    surf = [_sdf_surface_samples(s) for s in sdf]
+    shape_ids = np.zeros(n_body, np.int32)
+    poses = np.zeros((n_body, 8))
+    pts = np.zeros((n_body, P, 3))
+    e = env_lo
+    while e < env_lo + n_body:
+        blk = e // C5_BLOCK
+        lo, hi = blk * C5_BLOCK, (blk + 1) * C5_BLOCK
+        rng = np.random.Generator(np.random.Philox(key=[seed, blk]))
+        ib = rng.integers(0, len(sdf), C5_BLOCK)
+        q = random_quats(rng, C5_BLOCK)
+        t = rng.uniform(-0.1, 0.1, (C5_BLOCK, 3))
+        u = rng.random((C5_BLOCK, P))
+        jit = rng.normal(0.0, 0.01, (C5_BLOCK, P, 3))
+        s, t_ = max(e, lo), min(env_lo + n_body, hi)
+        sl, o = slice(s - lo, t_ - lo), slice(s - env_lo, t_ - env_lo)
+        shape_ids[o] = ib[sl]
+        poses[o, :3] = t[sl]
+        poses[o, 3:7] = q[sl]
+        loc = np.zeros((t_ - s, P, 3))
+        for k in range(len(sdf)):
+            m = ib[sl] == k
+            if m.any():
+                idx = np.minimum((u[sl][m] * len(surf[k])).astype(np.int64), len(surf[k]) - 1)
+                loc[m] = surf[k][idx]
+        loc += jit[sl]
+        R = quats_to_mats(q[sl])
+        pts[o] = np.einsum("nij,npj->npi", R, loc) + t[sl][:, None, :]
+        e = t_
+    sc = Scene("SDF", sdf, smooth_params(0.1), np.zeros((0, 5), np.int32), poses[:, None, :].astype(F32), ell=0.1,
+               meta=dict(env_lo=env_lo))
+    sc.points = pts.reshape(-1, 3).astype(F32)
+    sc.point_shapes = shape_ids
+    sc.point_poses = poses.astype(F32)
+    sc.P = P
+    return sc

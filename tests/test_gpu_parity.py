@@ -270,3 +270,55 @@ def test_expand_jacobian_two_sided(cuda, oracle_mod):
                               torch.from_numpy(gpu["q"]).cuda(), gpu["C"], mode=mode).cpu().numpy()
         Jr = osc.contact_manifold(mode=mode)["J"].reshape(-1, 36).T
         assert np.allclose(J, Jr, atol=1e-5 * max(1.0, np.abs(Jr).max()))
+
+
+def test_sdf_workload_full_size_sampled(cuda, oracle_mod):
+    """bench.py's SDF workload at its default size (262144 bodies x 64 points
+    of the 32 C5 SDF prototypes, value + gradient + Hessian + pose gradient) in
+    one launch; 256 bodies sampled with a seeded generator against the oracle."""
+    import torch
+    from paper_2604_17538_b200 import binding
+    sc = synth.sdf_scene(1 << 18, 64)
+    P = sc.P
+    S = binding.Scene(sc.shapes, sc.smooth)
+    flags = binding.SDF_VALUE | binding.SDF_GRAD | binding.SDF_HESS | binding.SDF_POSE_GRAD
+    out = S.sdf_eval(torch.from_numpy(sc.point_shapes).cuda(), torch.from_numpy(sc.point_poses).cuda(),
+                     torch.from_numpy(sc.points).cuda(), P, flags)
+    torch.cuda.synchronize()
+    bi = np.sort(np.random.default_rng(21).choice(len(sc.point_shapes), 256, replace=False))
+    rows = torch.from_numpy((bi[:, None] * P + np.arange(P)[None, :]).reshape(-1)).cuda()
+    gpu = {k: (v[..., rows] if v.dim() > 1 else v[rows]).cpu().numpy() for k, v in out.items()}
+    osc = oracle_mod.OracleScene(sc)
+    pts = sc.points.reshape(-1, P, 3)[bi].reshape(-1, 3)
+    nf, rep = PT.sdf_parity(osc, gpu, sc.point_shapes[bi], sc.point_poses[bi], pts, P,
+                            np.random.default_rng(22), sc.ell)
+    _report("sdf_workload_full", rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+    assert PT.excluded_fraction(rep) < 0.01
+
+
+def test_manifold_large_patch_unstaged(cuda, oracle_mod):
+    """A 40x40 plane patch (V = 1600, E = 4641, F = 3042): the unit's staged
+    face state (~566 KB) exceeds shared memory, so the face kernel gathers from
+    the scratch slot and recomputes the candidate points per face; sampled
+    against a sphere and a PSQ at three poses."""
+    patch = synth.make_shape("patch40", None, synth.plane_patch(40, 40, 0.6, 0.6))
+    sph = synth.make_shape("sph", synth.sq((0.08,) * 3, (1, 1)), None)
+    psq = synth.make_shape("psq", synth.psq((0.1, 0.07, 0.06), (0.6, 0.9), [[0.3, 0.2, 0.9, -0.02]]), None)
+    n_env = 3
+    poses = np.zeros((n_env, 3, 8), np.float32)
+    poses[:, :, 3] = 1
+    rng = np.random.default_rng(31)
+    for e in range(n_env):
+        poses[e, 1, :3] = (rng.uniform(-0.1, 0.1), rng.uniform(-0.1, 0.1), 0.07 - 0.01 * e)
+        poses[e, 2, :3] = (rng.uniform(-0.1, 0.1), rng.uniform(-0.1, 0.1), 0.05 - 0.01 * e)
+        poses[e, 1, 3:7] = synth.random_quats(rng, 1)[0]
+        poses[e, 2, 3:7] = synth.random_quats(rng, 1)[0]
+    pairs = np.array([[e, 0, 1 + k, 0, 1 + k] for e in range(n_env) for k in range(2)], np.int32)
+    sc = scene_of([patch, sph, psq], ell=1.0, pairs=pairs, poses=poses)
+    osc = oracle_mod.OracleScene(sc)
+    gpu, _ = PT.gpu_manifold(sc, 2)
+    nf, rep = PT.manifold_parity(sc, osc, gpu, 2, np.arange(len(pairs)), np.random.default_rng(32), sc.ell)
+    _report("manifold_patch40", rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+    assert PT.excluded_fraction(rep) < 0.01

@@ -90,3 +90,26 @@ def test_slice_envs_renumbers():
     sh = sc.slice_envs(3, 6)
     assert sh.n_env == 3 and sh.pairs[:, 0].min() == 0 and sh.pairs[:, 0].max() == 2
     assert np.array_equal(sh.poses, sc.poses[3:6])
+
+
+def test_sdf_workload_shards_match_single_generation():
+    # sdf_eval workload: a rank's body range equals the same bodies cut from
+    # one generation of the whole range (per-65536-block keys), points stay
+    # near the bodies' surfaces, and the oracle values agree shard vs whole
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    from oracle import oracle as O
+    full = bench.make_scene("SDF", 70000, 0)
+    sh = bench.make_scene("SDF", 100, 65500)
+    P = sh.P
+    assert np.array_equal(sh.point_shapes, full.point_shapes[65500:65600])
+    assert np.array_equal(sh.point_poses, full.point_poses[65500:65600])
+    assert np.array_equal(sh.points, full.points[65500 * P:65600 * P])
+    o1 = O.OracleScene(sh).sdf_eval(sh.point_shapes[:4], sh.point_poses[:4], sh.points[:4 * P], P)
+    o2 = O.OracleScene(full).sdf_eval(full.point_shapes[65500:65504], full.point_poses[65500:65504],
+                                      full.points[65500 * P:65504 * P], P)
+    assert np.array_equal(o1["d"], o2["d"]) and np.array_equal(o1["hess"], o2["hess"])
+    # the query points straddle the surfaces: both signs, most within 0.05
+    d = O.OracleScene(sh).sdf_eval(sh.point_shapes, sh.point_poses, sh.points, P, want_pose=False)["d"]
+    assert (d < 0).mean() > 0.2 and (d > 0).mean() > 0.2 and (np.abs(d) < 0.05).mean() > 0.9
