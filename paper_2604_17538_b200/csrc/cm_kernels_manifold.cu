@@ -179,6 +179,26 @@ struct UnitCtx {
 #define CM_MF_THREADS 64
 #endif
 #define CM_MF_MAX_THREADS 256
+// minimum resident 256-thread blocks per SM, i.e. register budgets of
+// 65536 / (256 MINB): 128 registers except the order-2 XPSQ evaluations
+// (measured on C5 / C4 / C3)
+#ifndef CM_MF_MINB_V
+#define CM_MF_MINB_V 2
+#endif
+#ifndef CM_MF_MINB_T
+#define CM_MF_MINB_T 2
+#endif
+#ifndef CM_MF_MINB_M
+#define CM_MF_MINB_M 2
+#endif
+#ifndef CM_MF_MINB_VM_XP1
+#define CM_MF_MINB_VM_XP1 1
+#endif
+template <int TIER, int XP> struct MinB {
+  static constexpr int VERTICES = XP == 1 ? CM_MF_MINB_VM_XP1 : CM_MF_MINB_V;
+  static constexpr int TRACES = CM_MF_MINB_T;
+  static constexpr int MIDPOINTS = XP == 1 ? CM_MF_MINB_VM_XP1 : CM_MF_MINB_M;
+};
 #ifndef CM_MF_FACE_MINB
 #define CM_MF_FACE_MINB 2   // face kernel: <= 128 registers
 #endif
@@ -257,7 +277,7 @@ __device__ __forceinline__ void vertex_frames(const PairFrame& F, const float* l
 
 // ---- phase 1: vertices: phi, n (and H) of B ----------------
 template <int TIER, int XP>
-__global__ void __launch_bounds__(CM_MF_MAX_THREADS) k_mf_vertices(const MfArgs a) {
+__global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::VERTICES) k_mf_vertices(const MfArgs a) {
   __shared__ UnitCtx U;
   if (!unit_setup(a, U)) return;
   constexpr int OV = TIER >= 2 ? 2 : 1;
@@ -292,7 +312,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS) k_mf_vertices(const MfArgs 
 
 // ---- phase 2: sphere traces (Fig. 2), 2 per edge ----------------
 template <int TIER, int XP>
-__global__ void __launch_bounds__(CM_MF_MAX_THREADS) k_mf_traces(const MfArgs a) {
+__global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::TRACES) k_mf_traces(const MfArgs a) {
   __shared__ UnitCtx U;
   if (!unit_setup(a, U)) return;
   constexpr int OT = TIER >= 2 ? 1 : 0;   // order inside the trace
@@ -362,7 +382,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS) k_mf_traces(const MfArgs a)
 
 // ---- phase 3: edge points p_e = v_I + a_bar e_t, a_bar = (a_I + a_II)/2
 template <int TIER, int XP>
-__global__ void __launch_bounds__(CM_MF_MAX_THREADS) k_mf_midpoints(const MfArgs a) {
+__global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::MIDPOINTS) k_mf_midpoints(const MfArgs a) {
   __shared__ UnitCtx U;
   if (!unit_setup(a, U)) return;
   constexpr int OV = TIER >= 2 ? 2 : 1;
