@@ -72,6 +72,34 @@ __device__ __forceinline__ float softclip_d(float x, float lo, float hi, float i
   return sigm((x - lo) * itau) - sigm((x - hi) * itau);
 }
 
+// cube root from the MUFU log / exp plus one Newton step (rel. error ~1e-7)
+__device__ __forceinline__ float cbrt_fast(float x) {
+  const float ax = fabsf(x);
+  float y = ex2(lg2(ax) * (1.f / 3.f));          // ax = 0 -> 0
+  if (y > 0.f && y < INFINITY) y = fmaf(1.f / 3.f, fmaf(ax, rcpa(y * y), -y), y);
+  return copysignf(y, x);
+}
+// atan2(y, x) for y >= 0 (result in [0, pi]): octant reduction and an odd
+// degree-15 polynomial on [0, 1] (abs. error ~1.2e-7)
+__device__ __forceinline__ float atan2_pos(float y, float x) {
+  const float ax = fabsf(x);
+  const float mx = fmaxf(ax, y), mn = fminf(ax, y);
+  const float a = mx > 0.f ? mn * rcpa(mx) : 0.f;
+  const float t = a * a;
+  float r = -0.004054551012814045f;
+  r = fmaf(r, t, 0.02186291106045246f);
+  r = fmaf(r, t, -0.055912282317876816f);
+  r = fmaf(r, t, 0.09642196446657181f);
+  r = fmaf(r, t, -0.1390863060951233f);
+  r = fmaf(r, t, 0.19946566224098206f);
+  r = fmaf(r, t, -0.33329862356185913f);
+  r = fmaf(r, t, 0.9999993443489075f);
+  r *= a;
+  if (y > ax) r = 1.5707963267948966f - r;
+  if (x < 0.f) r = 3.141592653589793f - r;
+  return r;
+}
+
 // ---- results ---------------------------------------------------------------
 // packed symmetric 3x3: xx, xy, xz, yy, yz, zz
 template <int O> struct Res {
@@ -525,7 +553,7 @@ __device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3
 
 // XPSQ leaf in its local frame
 template <int O> __device__ CM_XINL void xpsq_eval(const Xpsq& X, const SmoothDev& sp, const float* y, Res<O>& out) {
-  const float tc = sp.tau_clip_t, itc = 1.f / tc;
+  const float tc = sp.tau_clip_t, itc = sp.i_clip_t;
   float w[3] = {y[0] - X.p1[0], y[1] - X.p1[1], y[2] - X.p1[2]};
   J3<O> tk[3];
   if (X.cls == 0) {
@@ -660,8 +688,8 @@ struct XsqParams {
 // The values use the cancellation-free forms of soft_cardano.
 template <int O>
 __device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3, const SmoothDev& sp, J2<O>* t) {
-  const float td = sp.tau_delta, itd = 1.f / td;
-  const float tc = sp.tau_clip_t, itc = 1.f / tc;
+  const float td = sp.tau_delta, itd = sp.i_delta;
+  const float tc = sp.tau_clip_t, itc = sp.i_clip_t;
   const float P2 = P * P, P3 = P2 * P;
   const float Delta = -(4.f * P3 + 27.f * Q * Q);
   const float Dl[2] = {-12.f * P2, -54.f * Q};          // dDelta/d(P, Q)
@@ -677,7 +705,7 @@ __device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3
   // derivatives of the modified coefficient and of the root
   auto root_derivs = [&](float s, float Pt, const float* Pa, const float* Pab, float* sa, float* sab) {
     const float Fs = fmaf(3.f * s, s, Pt);
-    const float iF = 1.f / Fs;
+    const float iF = rcpa(Fs);
     sa[0] = -(Pa[0] * s) * iF;
     sa[1] = -(fmaf(Pa[1], s, 1.f)) * iF;
     if constexpr (O >= 2) {
@@ -706,23 +734,23 @@ __device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3
   const bool use_n = wn > W_SKIP, use_p = wp > W_SKIP;
   if (use_n) {
     const float W = fmaf(0.25f, spD, P3);
-    const float Pm = cbrtf(W);
+    const float Pm = cbrt_fast(W);
     // Cardano's cancellation-free form: u = cbrt(-Q/2 - sign(Q) sqrt(D)), v = -Pm/(3u)
     const float D = softplus(-Delta, td, itd) * (1.f / 108.f);
     const float sD = sqrtf(D);
-    const float u = cbrtf(Q >= 0.f ? -0.5f * Q - sD : -0.5f * Q + sD);
-    const float s = fabsf(u) > 1e-30f ? u - Pm / (3.f * u) : u;
+    const float u = cbrt_fast(Q >= 0.f ? -0.5f * Q - sD : -0.5f * Q + sD);
+    const float s = fabsf(u) > 1e-30f ? u - Pm * rcpa(3.f * u) : u;
     float sa[2] = {0.f, 0.f}, sab[3] = {0.f, 0.f, 0.f};
     if constexpr (O >= 1) {
       const float Wa[2] = {fmaf(3.f, P2, 0.25f * sp1 * Dl[0]), 0.25f * sp1 * Dl[1]};
-      const float ip2 = 1.f / fmaxf(3.f * Pm * Pm, 1e-30f);   // guarded at the cusp (reading #15)
+      const float ip2 = rcpa(fmaxf(3.f * Pm * Pm, 1e-30f));   // guarded at the cusp (reading #15)
       const float Pa[2] = {Wa[0] * ip2, Wa[1] * ip2};
       float Pab[3] = {0.f, 0.f, 0.f};
       if constexpr (O >= 2) {
         const float Wab[3] = {fmaf(6.f, P, 0.25f * fmaf(sp2 * Dl[0], Dl[0], sp1 * Dll[0])),
                               0.25f * sp2 * Dl[0] * Dl[1], 0.25f * fmaf(sp2 * Dl[1], Dl[1], sp1 * Dll[2])};
         const float den = 3.f * Pm * Pm * Pm;
-        const float c = 2.f * ip2 / (fabsf(den) > 1e-30f ? den : copysignf(1e-30f, den));
+        const float c = 2.f * ip2 * rcpa(fabsf(den) > 1e-30f ? den : copysignf(1e-30f, den));
         Pab[0] = fmaf(-c, Wa[0] * Wa[0], Wab[0] * ip2);
         Pab[1] = fmaf(-c, Wa[0] * Wa[1], Wab[1] * ip2);
         Pab[2] = fmaf(-c, Wa[1] * Wa[1], Wab[2] * ip2);
@@ -734,19 +762,23 @@ __device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3
   if (use_p) {
     const float V = fmaf(0.25f * Q, Q, spD * (1.f / 108.f));
     const float rho = ex2(lg2(V) * (1.f / 6.f));
-    const float th = atan2f(sqrtf(spD * (1.f / 108.f)), -0.5f * Q);
+    // roots 2 rho cos((th + 2 pi k)/3) from one sincos of th/3 (angle addition)
+    const float th3 = atan2_pos(sqrtf(spD * (1.f / 108.f)), -0.5f * Q) * (1.f / 3.f);
+    float sn3, cs3;
+    __sincosf(th3, &sn3, &cs3);
+    const float ck1 = fmaf(-0.8660254037844386f, sn3, -0.5f * cs3), ck2 = fmaf(0.8660254037844386f, sn3, -0.5f * cs3);
     float Pa[2] = {0.f, 0.f}, Pab[3] = {0.f, 0.f, 0.f};
     const float Pt = -3.f * rho * rho;
     if constexpr (O >= 1) {
       const float Va[2] = {sp1 * Dl[0] * (1.f / 108.f), fmaf(0.5f, Q, sp1 * Dl[1] * (1.f / 108.f))};
-      const float iV23 = 1.f / fmaxf(rho * rho * rho * rho, 1e-30f);   // V^(-2/3)
+      const float iV23 = rcpa(fmaxf(rho * rho * rho * rho, 1e-30f));   // V^(-2/3)
       Pa[0] = -Va[0] * iV23;
       Pa[1] = -Va[1] * iV23;
       if constexpr (O >= 2) {
         const float Vab[3] = {fmaf(sp2 * Dl[0], Dl[0], sp1 * Dll[0]) * (1.f / 108.f),
                               sp2 * Dl[0] * Dl[1] * (1.f / 108.f),
                               fmaf(fmaf(sp2 * Dl[1], Dl[1], sp1 * Dll[2]), 1.f / 108.f, 0.5f)};
-        const float c = (2.f / 3.f) * iV23 / fmaxf(V, 1e-30f);
+        const float c = (2.f / 3.f) * iV23 * rcpa(fmaxf(V, 1e-30f));
         Pab[0] = fmaf(c, Va[0] * Va[0], -Vab[0] * iV23);
         Pab[1] = fmaf(c, Va[0] * Va[1], -Vab[1] * iV23);
         Pab[2] = fmaf(c, Va[1] * Va[1], -Vab[2] * iV23);
@@ -754,9 +786,7 @@ __device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3
     }
 #pragma unroll 1
     for (int k = 0; k < 3; ++k) {
-      float sn, cs;
-      sincosf((th + 6.283185307179586f * (float)k) * (1.f / 3.f), &sn, &cs);
-      const float s = 2.f * rho * cs;
+      const float s = 2.f * rho * (k == 0 ? cs3 : (k == 1 ? ck1 : ck2));
       float sa[2] = {0.f, 0.f}, sab[3] = {0.f, 0.f, 0.f};
       if constexpr (O >= 1) root_derivs(s, Pt, Pa, Pab, sa, sab);
       float v, va[2], vab[3];
@@ -798,7 +828,7 @@ __device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3
 template <int O>
 __device__ __forceinline__ bool xpsq_root_t(const Xpsq& X, const SmoothDev& sp, const float* w, float* tv, float (*tg)[3],
                                             float (*th)[6]) {
-  const float tc = sp.tau_clip_t, itc = 1.f / tc;
+  const float tc = sp.tau_clip_t, itc = sp.i_clip_t;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     tv[k] = 0.5f;
@@ -849,17 +879,17 @@ __device__ __forceinline__ bool xpsq_root_t(const Xpsq& X, const SmoothDev& sp, 
 }
 
 template <int O> __device__ CM_XINL void xpsq_eval_fast(const Xpsq& X, const SmoothDev& sp, const float* y, Res<O>& out) {
-  const float tau = sp.tau_min, itau = 1.f / tau, itl = LOG2E * itau;
+  const float tau = sp.tau_min, itau = sp.i_min, itl = LOG2E * itau;
   const float w[3] = {y[0] - X.p1[0], y[1] - X.p1[1], y[2] - X.p1[2]};
   float tv[3], tg[3][3], th[3][6];
   const bool single = xpsq_root_t<O>(X, sp, w, tv, tg, th);
   XsqParams sq;
 #pragma unroll
-  for (int i = 0; i < 3; ++i) sq.ia[i] = 1.f / X.a0[i];
-  sq.p1 = 1.f / X.eps0[0];
-  sq.p2 = 1.f / X.eps0[1];
-  sq.m = X.eps0[1] * sq.p1;
-  sq.k = 0.5f * X.eps0[0];
+  for (int i = 0; i < 3; ++i) sq.ia[i] = X.sq_ia[i];
+  sq.p1 = X.sq_p1;
+  sq.p2 = X.sq_p2;
+  sq.m = X.sq_m;
+  sq.k = X.sq_k;
   const float* b = X.frenet ? X.bhat : nullptr;
   Acc<O> acc;
   acc_init(acc);
@@ -995,7 +1025,7 @@ __device__ __forceinline__ void leaf_eval(const SceneDev& S, int li, const float
     const int np = L.n_planes;
     if (np > 0) {
       // PSQ: smooth intersection Eq. (3) with the half-spaces
-      const float tau = S.sp.tau_min, itau = 1.f / tau, itl = LOG2E * itau;
+      const float tau = S.sp.tau_min, itau = S.sp.i_min, itl = LOG2E * itau;
       Acc<O> a;
       acc_init(a);
       acc_fold(a, 1.f, l, itl, itau);
@@ -1050,7 +1080,7 @@ __device__ __forceinline__ void fold_level(Acc<O>& a0, Acc<O>& a1, Acc<O>& a2, i
 // so one accumulator level suffices (fewer live registers)
 template <int O, int XP, bool FLAT = false>
 __device__ CM_SINL void eval_shape(const SceneDev& S, const ShapeRec& sh, const float* x, Res<O>& out) {
-  const float tau = S.sp.tau_min, itau = 1.f / tau, itl = LOG2E * itau;
+  const float tau = S.sp.tau_min, itau = S.sp.i_min, itl = LOG2E * itau;
   if (sh.prog_len == 1) {  // single leaf: no accumulator needed
     leaf_eval<O, XP>(S, S.prog[sh.prog_begin].idx, x, out);
     return;

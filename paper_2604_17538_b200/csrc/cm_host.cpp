@@ -153,6 +153,11 @@ Xpsq pack_xpsq(const cm_node& n) {
     X.da[i] = n.a[1][i] - n.a[0][i];
     varying |= X.da[i] != 0.f;
   }
+  for (int i = 0; i < 3; ++i) X.sq_ia[i] = (float)(1.0 / n.a[0][i]);
+  X.sq_p1 = (float)(1.0 / n.eps[0][0]);
+  X.sq_p2 = (float)(1.0 / n.eps[0][1]);
+  X.sq_m = (float)((double)n.eps[0][1] / n.eps[0][0]);
+  X.sq_k = (float)(0.5 * n.eps[0][0]);
   for (int j = 0; j < n.n_planes; ++j)
     for (int i = 0; i < 4; ++i) {
       X.pl0[j][i] = n.planes[0][j][i];
@@ -414,7 +419,9 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
   for (const void* p : {(const void*)D.prog, (const void*)D.leaves, (const void*)D.xpsq, (const void*)D.shapes,
                         (const void*)D.verts, (const void*)D.edges, (const void*)D.faces, (const void*)D.face_edges})
     if (p) sc->allocs.push_back(const_cast<void*>(p));
-  D.sp = SmoothDev{sp->tau_cmp, sp->tau_min, sp->tau_clip_alpha, sp->tau_clip_t, sp->tau_delta, sp->trace_iters};
+  D.sp = SmoothDev{sp->tau_cmp, sp->tau_min, sp->tau_clip_alpha, sp->tau_clip_t, sp->tau_delta, sp->trace_iters,
+                   (float)(1.0 / sp->tau_cmp), (float)(1.0 / sp->tau_min), (float)(1.0 / sp->tau_clip_alpha),
+                   (float)(1.0 / sp->tau_clip_t), (float)(1.0 / sp->tau_delta)};
   D.n_shapes = n_shapes;
   // chunk scratch of the manifold kernels (one candidate-state slot per unit)
   if (rc == CM_OK && sc->max_F > 0) {

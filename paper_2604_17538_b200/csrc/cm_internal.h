@@ -55,6 +55,7 @@ struct Xpsq {
   int32_t n_planes;
   float eps0[2], deps[2];
   float a0[3], da[3];
+  float sq_ia[3], sq_p1, sq_p2, sq_m, sq_k;   // SQ constants of the t = 0 schedule
   float pl0[CM_MAX_PLANES][4], dpl[CM_MAX_PLANES][4];
 };
 
@@ -72,6 +73,7 @@ struct ShapeRec {
 struct SmoothDev {
   float tau_cmp, tau_min, tau_clip_alpha, tau_clip_t, tau_delta;
   int32_t iters;
+  float i_cmp, i_min, i_clip_alpha, i_clip_t, i_delta;   // reciprocals (host-computed)
 };
 
 // everything a kernel needs to evaluate any shape of the scene

@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::VERTICES) k
   float* sv = a.scratch + (int64_t)blockIdx.x * a.slot;
   const float* lv = a.S.verts + 3 * (int64_t)U.SA.v_off;
   const bool full = (a.mode & CM_FULL_MODE) != 0;
-  const float itcmp = 1.f / a.S.sp.tau_cmp;
+  const float itcmp = a.S.sp.i_cmp;
   for (int v = threadIdx.x; v < V; v += blockDim.x) {
     float xb[3], pw[3];
     vertex_frames(F, lv, v, xb, pw);
@@ -317,8 +317,8 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::TRACES) k_m
   if (!unit_setup(a, U)) return;
   constexpr int OT = TIER >= 2 ? 1 : 0;   // order inside the trace
   const SmoothDev sp = a.S.sp;
-  const float itcmp = 1.f / sp.tau_cmp;
-  const float tca = sp.tau_clip_alpha, itca = 1.f / tca;
+  const float itcmp = sp.i_cmp;
+  const float tca = sp.tau_clip_alpha, itca = sp.i_clip_alpha;
   const PairFrame& F = U.F;
   const int V = U.SA.V, E = U.SA.E;
   const float* sv = a.scratch + (int64_t)blockIdx.x * a.slot;
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::MIDPOINTS) 
   const float* lv = a.S.verts + 3 * (int64_t)U.SA.v_off;
   const int32_t* ed = a.S.edges + 2 * (int64_t)U.SA.e_off;
   const bool full = (a.mode & CM_FULL_MODE) != 0;
-  const float itcmp = 1.f / a.S.sp.tau_cmp;
+  const float itcmp = a.S.sp.i_cmp;
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int vI, vII;
     float el[3], L;
@@ -480,8 +480,8 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, CM_MF_FACE_MINB) k_mf_faces
   if (STAGED && threadIdx.x == 0) mbar_init(&bar, 1);   // published by unit_setup's barrier
   if (!unit_setup(a, U)) return;
   const SmoothDev sp = a.S.sp;
-  const float itcmp = 1.f / sp.tau_cmp;
-  const float tmin = sp.tau_min, itmin = 1.f / tmin;
+  const float itcmp = sp.i_cmp;
+  const float tmin = sp.tau_min, itmin = sp.i_min;
   const PairFrame& F = U.F;
   const int V = U.SA.V, E = U.SA.E, NF = U.SA.F;
   constexpr int VF = vfields(TIER), EF = efields(TIER);
