@@ -203,6 +203,17 @@ struct cm_scene {
   cudaEvent_t ev_fork = nullptr, ev_join[cmi::kManifoldStreams] = {};
 };
 
+// aux streams used per manifold call (CM_MANIFOLD_STREAMS=1 serialises the
+// chunks on one stream; experiments only)
+static int n_aux_streams() {
+  static const int n = [] {
+    const char* e = std::getenv("CM_MANIFOLD_STREAMS");
+    int v = e ? std::atoi(e) : cmi::kManifoldStreams;
+    return std::min(std::max(v, 1), cmi::kManifoldStreams);
+  }();
+  return n;
+}
+
 extern "C" {
 
 int cm_version(void) { return CM_ABI_VERSION; }
@@ -555,7 +566,7 @@ int cm_contact_manifold(const cm_scene* sc, const int32_t* pairs, int64_t n_pair
     aux[i] = ms->aux[i];
   }
   int rc = cml::launch_manifold(sc->dev, sc->class_mask, sc->max_V, sc->max_E, pairs, n_pairs, offsets, poses, n_slot,
-                                flags, out, n_contacts, sc->scratch, sc->scratch_floats, aux, cmi::kManifoldStreams);
+                                flags, out, n_contacts, sc->scratch, sc->scratch_floats, aux, n_aux_streams());
   for (int i = 0; i < cmi::kManifoldStreams; ++i) {
     cudaEventRecord(ms->ev_join[i], ms->aux[i]);
     cudaStreamWaitEvent(st, ms->ev_join[i], 0);
