@@ -454,12 +454,15 @@ def main():
         e2e = {"value": n_pairs_all / (float(te.item()) / 1e3), "unit": "pairs/s",
                "h2d_bytes_per_step": int(poses_h.numel() * 4), "d2h_bytes_per_step": int(C * 4)}
 
-    # ---- roofline of the dominant kernel (k_contact_manifold) -------------
+    # ---- roofline of the manifold kernels ---------------------------------
     peaks, peak_src = load_peaks()
     n_pairs = len(scene.pairs)
     bytes_alg = n_pairs * IN_BYTES_PER_PAIR + C * OUT_BYTES_PER_CONTACT[args.tier]
-    # the step is exactly the k_contact_manifold launch(es) of one call (one
-    # lean + one XPSQ instantiation for scenes mixing both SDF classes)
+    # the step is exactly the k_mf_* launches of one cm_contact_manifold call
+    # (per chunk of units: vertices, traces, midpoints per SDF class, then
+    # faces), timed together with CUDA events on the caller's stream; the
+    # algorithmic FLOPs are those of the whole method, so the roofline covers
+    # the kernels of the step together (per-kernel shares: profiles/traffic_*.json)
     kern_s = ms_per_step / 1e3
     hbm_gbs = bytes_alg / kern_s / 1e9
     flop_launch = flop_per_launch(args.workload, scene, S) if args.tier == 2 else None
@@ -467,13 +470,21 @@ def main():
     if fpp:
         achieved = flop_launch / kern_s / 1e12
         traffic = None
-        tpath = os.path.join(ROOT, "profiles", "r01_traffic_%s.json" % args.workload.lower())
+        dominant = None
+        tpath = os.path.join(ROOT, "profiles", "traffic_%s.json" % args.workload.lower())
         if os.path.exists(tpath) and args.tier == 2:
             with open(tpath) as f:
-                traffic = json.load(f)["bytes_per_pair"] * n_pairs   # measured DRAM bytes per launch
+                tj = json.load(f)
+            traffic = tj["bytes_per_pair"] * n_pairs   # measured DRAM bytes per step
+            top = max(tj["kernels"], key=lambda k: k["share_of_chunk_time"])
+            dominant = {"kernel": top["kernel"], "share_of_step": round(top["share_of_chunk_time"], 3),
+                        "source": "ncu launch durations of one chunk (%s)" % os.path.basename(tpath)}
         roof = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,
-                "traffic_unit": "bytes per step (ncu dram read + write, scaled per pair)",
+                "scope": "all k_mf_* kernels of the step (the step is exactly these launches)",
+                "dominant_kernel": dominant,
+                "traffic_unit": "bytes per step (ncu dram read + write of one chunk's kernels, cold-cache replays, "
+                                "scaled per pair)",
                 "bytes_alg": bytes_alg,
                 "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
                 "flop_per_pair": fpp, "flop_source": "costmodel.json (ncu-measured per-shape/order table, DESIGN.md §7)",
