@@ -181,7 +181,7 @@ struct UnitCtx {
 #define CM_MF_MAX_THREADS 256
 // minimum resident 256-thread blocks per SM, i.e. register budgets of
 // 65536 / (256 MINB): 128 registers except the order-2 XPSQ evaluations
-// (measured on C5 / C4 / C3)
+// (measured on C5 / C4 / C3); flat SQ-family class: 80
 #ifndef CM_MF_MINB_V
 #define CM_MF_MINB_V 2
 #endif
@@ -191,13 +191,22 @@ struct UnitCtx {
 #ifndef CM_MF_MINB_M
 #define CM_MF_MINB_M 2
 #endif
+#ifndef CM_MF_MINB_V_XP0
+#define CM_MF_MINB_V_XP0 3
+#endif
+#ifndef CM_MF_MINB_M_XP0
+#define CM_MF_MINB_M_XP0 3
+#endif
+#ifndef CM_MF_MINB_T_XP0
+#define CM_MF_MINB_T_XP0 3
+#endif
 #ifndef CM_MF_MINB_VM_XP1
 #define CM_MF_MINB_VM_XP1 1
 #endif
 template <int TIER, int XP> struct MinB {
-  static constexpr int VERTICES = XP == 1 ? CM_MF_MINB_VM_XP1 : CM_MF_MINB_V;
-  static constexpr int TRACES = CM_MF_MINB_T;
-  static constexpr int MIDPOINTS = XP == 1 ? CM_MF_MINB_VM_XP1 : CM_MF_MINB_M;
+  static constexpr int VERTICES = XP == 1 ? CM_MF_MINB_VM_XP1 : (XP == 0 ? CM_MF_MINB_V_XP0 : CM_MF_MINB_V);
+  static constexpr int TRACES = XP == 0 ? CM_MF_MINB_T_XP0 : CM_MF_MINB_T;
+  static constexpr int MIDPOINTS = XP == 1 ? CM_MF_MINB_VM_XP1 : (XP == 0 ? CM_MF_MINB_M_XP0 : CM_MF_MINB_M);
 };
 #ifndef CM_MF_FACE_MINB
 #define CM_MF_FACE_MINB 2   // face kernel: <= 128 registers
