@@ -200,13 +200,16 @@ struct UnitCtx {
 #ifndef CM_MF_MINB_T_XP0
 #define CM_MF_MINB_T_XP0 3
 #endif
-#ifndef CM_MF_MINB_VM_XP1
-#define CM_MF_MINB_VM_XP1 1
+#ifndef CM_MF_MINB_V_XP1
+#define CM_MF_MINB_V_XP1 1
+#endif
+#ifndef CM_MF_MINB_M_XP1
+#define CM_MF_MINB_M_XP1 1
 #endif
 template <int TIER, int XP> struct MinB {
-  static constexpr int VERTICES = XP == 1 ? CM_MF_MINB_VM_XP1 : (XP == 0 ? CM_MF_MINB_V_XP0 : CM_MF_MINB_V);
+  static constexpr int VERTICES = XP == 1 ? CM_MF_MINB_V_XP1 : (XP == 0 ? CM_MF_MINB_V_XP0 : CM_MF_MINB_V);
   static constexpr int TRACES = XP == 0 ? CM_MF_MINB_T_XP0 : CM_MF_MINB_T;
-  static constexpr int MIDPOINTS = XP == 1 ? CM_MF_MINB_VM_XP1 : (XP == 0 ? CM_MF_MINB_M_XP0 : CM_MF_MINB_M);
+  static constexpr int MIDPOINTS = XP == 1 ? CM_MF_MINB_M_XP1 : (XP == 0 ? CM_MF_MINB_M_XP0 : CM_MF_MINB_M);
 };
 #ifndef CM_MF_FACE_MINB
 #define CM_MF_FACE_MINB 2   // face kernel: <= 128 registers
