@@ -27,16 +27,24 @@ using cml::check_launch;
 using cml::num_sms;
 
 // ============================================================================
-// per-unit scratch slot (field-major, stride = V or E)
-//   vertex fields:              d, n[3] (world grad phi), H[6] (world, tier 2)
-//   edge fields after traces:   a_I, a_II (soft-clipped), da_I[9], da_II[9] (tier 2)
-//   edge fields after midpoint: a_bar, d, n[3], H[6] (tier 2), da_bar[9] (tier 2)
+// per-unit scratch slot: one 16-B aligned record per candidate (vertex records
+// first, then edge records), loaded and stored with 128-bit accesses
+//   vertex record:               d, n[3] (world grad phi) | H[6] (world), pad[2]
+//                                (tier 2: 12 floats, else 4)
+//   edge record after traces:    a_I, da_I[9], a_II, da_II[9] (tier 2: 20 floats;
+//                                else a_I, a_II in 8)
+//   edge record after midpoint:  a_bar, d, n[3], H[6], da_bar[9] (else a_bar, d, n[3])
 // ============================================================================
-__host__ __device__ constexpr int vfields(int tier) { return tier >= 2 ? 10 : 4; }
-__host__ __device__ constexpr int efields(int tier) { return tier >= 2 ? 20 : 5; }
+__host__ __device__ constexpr int vrec(int tier) { return tier >= 2 ? 12 : 4; }
+__host__ __device__ constexpr int erec(int tier) { return tier >= 2 ? 20 : 8; }
+__host__ __device__ constexpr int trace_b(int tier) { return tier >= 2 ? 10 : 1; }   // a_II offset
 enum { VD = 0, VN = 1, VH = 4 };
-enum { TA = 0, TB = 1, TDA = 2, TDB = 11 };                // trace layout
 enum { MAB = 0, MD = 1, MN = 2, MH = 5, MDAB = 11 };       // midpoint layout
+
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
 
 struct PairFrame {
   float RA[9], tA[3], RB[9], tB[3];
@@ -306,14 +314,13 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::VERTICES) k
     eval_shape<OV, ClsTraits<XP>::XPM, ClsTraits<XP>::FLAT>(a.S, U.SB, xb, r);
     float n[3];
     rot_vec(F.RB, r.g, n);
-    sv[VD * V + v] = r.v;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) sv[(VN + i) * V + v] = n[i];
+    float* rec = sv + v * vrec(TIER);
+    st4(rec, r.v, n[0], n[1], n[2]);
     float h[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if constexpr (TIER >= 2) {
       rot_sym(F.RB, r.h, h);
-#pragma unroll
-      for (int k = 0; k < 6; ++k) sv[(VH + k) * V + v] = h[k];
+      st4(rec + 4, h[0], h[1], h[2], h[3]);
+      st4(rec + 8, h[4], h[5], 0.f, 0.f);
     }
     if (full) {
       CM_COLS(U.side);
@@ -334,7 +341,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::TRACES) k_m
   const PairFrame& F = U.F;
   const int V = U.SA.V, E = U.SA.E;
   const float* sv = a.scratch + (int64_t)blockIdx.x * a.slot;
-  float* se = a.scratch + (int64_t)blockIdx.x * a.slot + (int64_t)vfields(TIER) * V;
+  float* se = a.scratch + (int64_t)blockIdx.x * a.slot + (int64_t)vrec(TIER) * V;
   const float* lv = a.S.verts + 3 * (int64_t)U.SA.v_off;
   const int32_t* ed = a.S.edges + 2 * (int64_t)U.SA.e_off;
   for (int j = threadIdx.x; j < 2 * E; j += blockDim.x) {
@@ -357,8 +364,9 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::TRACES) k_m
     for (int it = 0; it < sp.iters; ++it) {
       float phi, g[3];
       if (it == 0) {   // the corner itself: reuse the vertex evaluation (reading #22)
-        phi = sv[VD * V + v0];
-        g[0] = sv[(VN + 0) * V + v0]; g[1] = sv[(VN + 1) * V + v0]; g[2] = sv[(VN + 2) * V + v0];
+        const float4 dn = ld4(sv + v0 * vrec(TIER));
+        phi = dn.x;
+        g[0] = dn.y; g[1] = dn.z; g[2] = dn.w;
       } else {
         const float xb[3] = {fmaf(al, eb[0], xI[0]), fmaf(al, eb[1], xI[1]), fmaf(al, eb[2], xI[2])};
         Res<OT> r;
@@ -382,12 +390,24 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::TRACES) k_m
       al = fmaf(sgn * s, phi, al);
     }
     // soft clip to the edge (reading #21)
-    se[(dir ? TB : TA) * E + e] = softclip(al, 0.f, L, tca, itca);
+    float* rec = se + e * erec(TIER) + (dir ? trace_b(TIER) : 0);
+    const float at = softclip(al, 0.f, L, tca, itca);
     if constexpr (TIER >= 2) {
       const float cd = softclip_d(al, 0.f, L, itca);
-      const int base = dir ? TDB : TDA;
+      float o[10] = {at};
 #pragma unroll
-      for (int k = 0; k < NDQ; ++k) se[(base + k) * E + e] = cd * da[k];
+      for (int k = 0; k < NDQ; ++k) o[1 + k] = cd * da[k];
+      if (dir == 0) {   // record floats 0-9: two float4 + one float2
+        st4(rec, o[0], o[1], o[2], o[3]);
+        st4(rec + 4, o[4], o[5], o[6], o[7]);
+        *reinterpret_cast<float2*>(rec + 8) = make_float2(o[8], o[9]);
+      } else {          // record floats 10-19: one float2 + two float4
+        *reinterpret_cast<float2*>(rec) = make_float2(o[0], o[1]);
+        st4(rec + 2, o[2], o[3], o[4], o[5]);
+        st4(rec + 6, o[6], o[7], o[8], o[9]);
+      }
+    } else {
+      *rec = at;
     }
   }
 }
@@ -400,7 +420,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::MIDPOINTS) 
   constexpr int OV = TIER >= 2 ? 2 : 1;
   const PairFrame& F = U.F;
   const int V = U.SA.V, E = U.SA.E;
-  float* se = a.scratch + (int64_t)blockIdx.x * a.slot + (int64_t)vfields(TIER) * V;
+  float* se = a.scratch + (int64_t)blockIdx.x * a.slot + (int64_t)vrec(TIER) * V;
   const float* lv = a.S.verts + 3 * (int64_t)U.SA.v_off;
   const int32_t* ed = a.S.edges + 2 * (int64_t)U.SA.e_off;
   const bool full = (a.mode & CM_FULL_MODE) != 0;
@@ -412,11 +432,20 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::MIDPOINTS) 
     float eb[3], ew[3];
     rot_vec(F.Rrel, el, eb);
     rot_vec(F.RA, el, ew);
-    const float ab = 0.5f * (se[TA * E + e] + se[TB * E + e]);
-    float dab[NDQ];
+    float* rec = se + e * erec(TIER);
+    float ab, dab[NDQ];
     if constexpr (TIER >= 2) {
+      float t[20];
 #pragma unroll
-      for (int k = 0; k < NDQ; ++k) dab[k] = 0.5f * (se[(TDA + k) * E + e] + se[(TDB + k) * E + e]);
+      for (int q = 0; q < 5; ++q) {
+        const float4 v4 = ld4(rec + 4 * q);
+        t[4 * q] = v4.x; t[4 * q + 1] = v4.y; t[4 * q + 2] = v4.z; t[4 * q + 3] = v4.w;
+      }
+      ab = 0.5f * (t[0] + t[10]);
+#pragma unroll
+      for (int k = 0; k < NDQ; ++k) dab[k] = 0.5f * (t[1 + k] + t[11 + k]);
+    } else {
+      ab = 0.5f * (rec[0] + rec[1]);
     }
     float xI[3], pI[3];
     vertex_frames(F, lv, vI, xI, pI);
@@ -430,17 +459,17 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::MIDPOINTS) 
     eval_shape<OV, ClsTraits<XP>::XPM, ClsTraits<XP>::FLAT>(a.S, U.SB, xb, r);
     float n[3];
     rot_vec(F.RB, r.g, n);
-    se[MAB * E + e] = ab;
-    se[MD * E + e] = r.v;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) se[(MN + i) * E + e] = n[i];
     float h[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if constexpr (TIER >= 2) {
       rot_sym(F.RB, r.h, h);
-#pragma unroll
-      for (int k = 0; k < 6; ++k) se[(MH + k) * E + e] = h[k];
-#pragma unroll
-      for (int k = 0; k < NDQ; ++k) se[(MDAB + k) * E + e] = dab[k];
+      st4(rec, ab, r.v, n[0], n[1]);
+      st4(rec + 4, n[2], h[0], h[1], h[2]);
+      st4(rec + 8, h[3], h[4], h[5], dab[0]);
+      st4(rec + 12, dab[1], dab[2], dab[3], dab[4]);
+      st4(rec + 16, dab[5], dab[6], dab[7], dab[8]);
+    } else {
+      st4(rec, ab, r.v, n[0], n[1]);
+      rec[4] = n[2];
     }
     if (full) {
       CM_COLS(U.side);
@@ -455,13 +484,12 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::MIDPOINTS) 
 // directions e_t, computed once per vertex / edge instead of once per face;
 // the face loop then gathers from shared memory.  Units too large for shared
 // memory gather from the scratch slot and recompute p, e_t per face.
-// Staged layout: the slot's used region [vfields x V | efields x E] copied
-// by one TMA bulk copy (cp.async.bulk, completion on an mbarrier), then
-// p[3][V] of the vertices and p_I[3][E], e_t[3][E] of the edges (the edge
-// point is p_I + a_bar e_t).
-__host__ __device__ constexpr int round4(int x) { return (x + 3) & ~3; }
+// Staged layout: the slot's used records [V vertex | E edge] copied by one
+// TMA bulk copy (cp.async.bulk, completion on an mbarrier), then p[3][V] of
+// the vertices and p_I[3][E], e_t[3][E] of the edges (the edge point is
+// p_I + a_bar e_t).
 __host__ __device__ constexpr int face_stage_floats(int V, int E, int tier) {
-  return round4(vfields(tier) * V + efields(tier) * E) + 3 * V + 6 * E;
+  return vrec(tier) * V + erec(tier) * E + 3 * V + 6 * E;
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -496,9 +524,9 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, CM_MF_FACE_MINB) k_mf_faces
   const float tmin = sp.tau_min, itmin = sp.i_min;
   const PairFrame& F = U.F;
   const int V = U.SA.V, E = U.SA.E, NF = U.SA.F;
-  constexpr int VF = vfields(TIER), EF = efields(TIER);
+  constexpr int VR = vrec(TIER), ER = erec(TIER);
   const float* gv = a.scratch + (int64_t)blockIdx.x * a.slot;
-  const float* ge = gv + (int64_t)VF * V;
+  const float* ge = gv + (int64_t)VR * V;
   const float* lv = a.S.verts + 3 * (int64_t)U.SA.v_off;
   const int32_t* ed = a.S.edges + 2 * (int64_t)U.SA.e_off;
   const int32_t* fv = a.S.faces + 3 * (int64_t)U.SA.f_off;
@@ -510,7 +538,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, CM_MF_FACE_MINB) k_mf_faces
   float* s_pv = nullptr;   // staged vertex points p[3][V]
   float* s_pe = nullptr;   // staged edge p_I[3][E], e_t[3][E]
   if constexpr (STAGED) {
-    const int used = round4(VF * V + EF * E);
+    const int used = VR * V + ER * E;
     if (threadIdx.x == 0) bulk_g2s(fsm, gv, (uint32_t)used * 4u, &bar);
     s_pv = fsm + used;
     s_pe = s_pv + 3 * V;
@@ -536,7 +564,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, CM_MF_FACE_MINB) k_mf_faces
     mbar_wait(&bar, 0);
     __syncthreads();
     sv = fsm;
-    se = fsm + VF * V;
+    se = fsm + VR * V;
   }
   CM_COLS(U.side);
   const float itlm = LOG2E * itmin;
@@ -547,7 +575,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, CM_MF_FACE_MINB) k_mf_faces
     // candidate depths d_i; order [v_i0, v_i1, v_i2, e(i0,i1), e(i1,i2), e(i2,i0)]
     float dc[6];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) { dc[k] = sv[VD * V + cv[k]]; dc[3 + k] = se[MD * E + ce[k]]; }
+    for (int k = 0; k < 3; ++k) { dc[k] = sv[cv[k] * VR + VD]; dc[3 + k] = se[ce[k] * ER + MD]; }
     // candidate points (world): vertices RA x + tA, edge points p_I + a_bar e_t
     // (the same arithmetic as the vertex / midpoint kernels), and the edges'
     // world directions e_t for the sliding terms
@@ -555,7 +583,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, CM_MF_FACE_MINB) k_mf_faces
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       if constexpr (STAGED) {
-        const float ab = se[MAB * E + ce[k]];
+        const float ab = se[ce[k] * ER + MAB];
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
           pc[k][i] = s_pv[i * V + cv[k]];
@@ -571,7 +599,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, CM_MF_FACE_MINB) k_mf_faces
         rot_vec(F.RA, el, ewc[k]);
         float pI[3];
         vertex_frames(F, lv, vI, xb, pI);
-        const float ab = se[MAB * E + ce[k]];
+        const float ab = se[ce[k] * ER + MAB];
 #pragma unroll
         for (int i = 0; i < 3; ++i) pc[3 + k][i] = fmaf(ab, ewc[k][i], pI[i]);
       }
@@ -602,11 +630,10 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, CM_MF_FACE_MINB) k_mf_faces
     for (int i = 0; i < 6; ++i) {
       const bool isv = i < 3;
       const int id = isv ? cv[i] : ce[i - 3];
-      const float* bn = isv ? sv + VN * V + id : se + MN * E + id;
-      const int sd = isv ? V : E;
+      const float* bn = isv ? sv + id * VR + VN : se + id * ER + MN;
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        const float p = pc[i][k], nn = bn[k * sd];
+        const float p = pc[i][k], nn = bn[k];
         nrm[k] = fmaf(zg[i], nn, nrm[k]);
         qv[k] = fmaf(zg[i], p, qv[k]);
         pt[k] = fmaf(z[i], p, pt[k]);
@@ -650,12 +677,21 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, CM_MF_FACE_MINB) k_mf_faces
       for (int i = 0; i < 6; ++i) {
         const bool isv = i < 3;
         const int id = isv ? cv[i] : ce[i - 3];
-        const float* bn = isv ? sv + VN * V + id : se + MN * E + id;
-        const float* bh = isv ? sv + VH * V + id : se + MH * E + id;
-        const int sd = isv ? V : E;
         const float* p = pc[i];
-        const float n[3] = {bn[0], bn[sd], bn[2 * sd]};
-        const float h[6] = {bh[0], bh[sd], bh[2 * sd], bh[3 * sd], bh[4 * sd], bh[5 * sd]};
+        float n[3], h[6], dab[NDQ];
+        if (isv) {   // d, n[3] | H[6], pad
+          const float* rv = sv + id * VR;
+          const float4 a0 = ld4(rv), a1 = ld4(rv + 4), a2 = ld4(rv + 8);
+          n[0] = a0.y; n[1] = a0.z; n[2] = a0.w;
+          h[0] = a1.x; h[1] = a1.y; h[2] = a1.z; h[3] = a1.w; h[4] = a2.x; h[5] = a2.y;
+        } else {     // a_bar, d, n[3], H[6], da_bar[9]
+          const float* re = se + id * ER;
+          const float4 a0 = ld4(re), a1 = ld4(re + 4), a2 = ld4(re + 8), a3 = ld4(re + 12), a4 = ld4(re + 16);
+          n[0] = a0.z; n[1] = a0.w; n[2] = a1.x;
+          h[0] = a1.y; h[1] = a1.z; h[2] = a1.w; h[3] = a2.x; h[4] = a2.y; h[5] = a2.z;
+          dab[0] = a2.w; dab[1] = a3.x; dab[2] = a3.y; dab[3] = a3.z; dab[4] = a3.w;
+          dab[5] = a4.x; dab[6] = a4.y; dab[7] = a4.z; dab[8] = a4.w;
+        }
         const float gam = sigm(-dc[i] * itcmp);
         const float w = zg[i];
         const float ci = w * (-itmin - (1.f - gam) * itcmp);
@@ -692,7 +728,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, CM_MF_FACE_MINB) k_mf_faces
           const float zge = z[i] * ge;
 #pragma unroll
           for (int k = 0; k < NDQ; ++k) {
-            const float dk = se[(MDAB + k) * E + id];
+            const float dk = dab[k];
             Se[k] = fmaf(zge, dk, Se[k]);
 #pragma unroll
             for (int q = 0; q < 3; ++q) dnE[q][k] = fmaf(u[q], dk, dnE[q][k]);
@@ -759,8 +795,8 @@ namespace cml {
 
 // floats of one unit's scratch slot
 int64_t manifold_slot_floats(int V, int E, int tier) {
-  // multiple of 4 floats: every slot starts 16-B aligned (bulk copies)
-  return ((int64_t)vfields(tier) * V + (int64_t)efields(tier) * E + 3) & ~(int64_t)3;
+  // records are multiples of 4 floats: every slot and record is 16-B aligned
+  return (int64_t)vrec(tier) * V + (int64_t)erec(tier) * E;
 }
 
 template <int TIER, int XP>
