@@ -234,6 +234,7 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
   std::vector<ShapeRec> recs(n_shapes);
   std::vector<float> verts;
   std::vector<int32_t> edges_all, faces_all, fe_all;
+  std::vector<float> edge_geom;   // x_I, L, e_t (computed in FP64 from the FP32 vertices)
   cm_scene* sc = new cm_scene;
   sc->device = device;
   sc->edges.resize(n_shapes);
@@ -405,6 +406,14 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
       r.f_off = (int32_t)(faces_all.size() / 3);
       verts.insert(verts.end(), d.vertices, d.vertices + 3 * V);
       edges_all.insert(edges_all.end(), eg.begin(), eg.end());
+      for (int k = 0; k < E; ++k) {
+        const float* xa = d.vertices + 3 * eg[2 * k];
+        const float* xb = d.vertices + 3 * eg[2 * k + 1];
+        const double dl[3] = {(double)xb[0] - xa[0], (double)xb[1] - xa[1], (double)xb[2] - xa[2]};
+        const double L = std::sqrt(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
+        const float g8[8] = {xa[0], xa[1], xa[2], (float)L, (float)(dl[0] / L), (float)(dl[1] / L), (float)(dl[2] / L), 0.f};
+        edge_geom.insert(edge_geom.end(), g8, g8 + 8);
+      }
       faces_all.insert(faces_all.end(), d.faces, d.faces + 3 * F);
       fe_all.insert(fe_all.end(), fe.begin(), fe.end());
       sc->max_V = std::max(sc->max_V, V);
@@ -425,10 +434,12 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
   D.shapes = dev_copy(recs, rc);
   D.verts = dev_copy(verts, rc);
   D.edges = dev_copy(edges_all, rc);
+  D.edge_geom = dev_copy(edge_geom, rc);
   D.faces = dev_copy(faces_all, rc);
   D.face_edges = dev_copy(fe_all, rc);
   for (const void* p : {(const void*)D.prog, (const void*)D.leaves, (const void*)D.xpsq, (const void*)D.shapes,
-                        (const void*)D.verts, (const void*)D.edges, (const void*)D.faces, (const void*)D.face_edges})
+                        (const void*)D.verts, (const void*)D.edges, (const void*)D.faces, (const void*)D.face_edges,
+                        (const void*)D.edge_geom})
     if (p) sc->allocs.push_back(const_cast<void*>(p));
   D.sp = SmoothDev{sp->tau_cmp, sp->tau_min, sp->tau_clip_alpha, sp->tau_clip_t, sp->tau_delta, sp->trace_iters,
                    (float)(1.0 / sp->tau_cmp), (float)(1.0 / sp->tau_min), (float)(1.0 / sp->tau_clip_alpha),

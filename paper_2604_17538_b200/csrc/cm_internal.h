@@ -84,6 +84,7 @@ struct SceneDev {
   const ShapeRec* shapes;
   const float* verts;
   const int32_t* edges;
+  const float* edge_geom;     // per edge 8 floats: x_I[3], L, e_t[3] (unit, local), 0
   const int32_t* faces;
   const int32_t* face_edges;
   SmoothDev sp;

@@ -274,25 +274,26 @@ template <int CLS> struct ClsTraits {
 #define CM_COLS(side) \
   const int cTA = (side) ? 6 : 0, cRA = (side) ? 9 : 3, cTB = (side) ? 0 : 6, cRB = (side) ? 3 : 9
 
-__device__ __forceinline__ void edge_dir(const float* lv, const int32_t* ed, int e, int& vI, int& vII, float* el,
-                                         float& L) {
-  vI = __ldg(ed + 2 * e);
-  vII = __ldg(ed + 2 * e + 1);
-  const float dl[3] = {__ldg(lv + 3 * vII) - __ldg(lv + 3 * vI), __ldg(lv + 3 * vII + 1) - __ldg(lv + 3 * vI + 1),
-                       __ldg(lv + 3 * vII + 2) - __ldg(lv + 3 * vI + 2)};
-  L = sqrtf(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
-  const float iL = 1.f / L;
-  el[0] = dl[0] * iL; el[1] = dl[1] * iL; el[2] = dl[2] * iL;
+// static edge geometry of the sampled surface (scene creation, FP64 from the
+// FP32 vertices): x_I (local), L, unit direction e_t (local) in two float4
+__device__ __forceinline__ void edge_geom(const float* eg, int e, float* xI, float& L, float* el) {
+  const float4 g0 = __ldg(reinterpret_cast<const float4*>(eg) + 2 * e);
+  const float4 g1 = __ldg(reinterpret_cast<const float4*>(eg) + 2 * e + 1);
+  xI[0] = g0.x; xI[1] = g0.y; xI[2] = g0.z; L = g0.w;
+  el[0] = g1.x; el[1] = g1.y; el[2] = g1.z;
 }
 
-// x_B = Rrel x + trel (B frame) and p = RA x + tA (world) of a local vertex
-__device__ __forceinline__ void vertex_frames(const PairFrame& F, const float* lv, int v, float* xb, float* pw) {
-  const float x[3] = {__ldg(lv + 3 * v), __ldg(lv + 3 * v + 1), __ldg(lv + 3 * v + 2)};
+// x_B = Rrel x + trel (B frame) and p = RA x + tA (world) of a local point
+__device__ __forceinline__ void to_frames(const PairFrame& F, const float* x, float* xb, float* pw) {
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     xb[i] = F.Rrel[i * 3] * x[0] + F.Rrel[i * 3 + 1] * x[1] + F.Rrel[i * 3 + 2] * x[2] + F.trel[i];
     pw[i] = F.RA[i * 3] * x[0] + F.RA[i * 3 + 1] * x[1] + F.RA[i * 3 + 2] * x[2] + F.tA[i];
   }
+}
+__device__ __forceinline__ void vertex_frames(const PairFrame& F, const float* lv, int v, float* xb, float* pw) {
+  const float x[3] = {__ldg(lv + 3 * v), __ldg(lv + 3 * v + 1), __ldg(lv + 3 * v + 2)};
+  to_frames(F, x, xb, pw);
 }
 
 // ---- phase 1: vertices: phi, n (and H) of B ----------------
@@ -347,15 +348,25 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::TRACES) k_m
   for (int j = threadIdx.x; j < 2 * E; j += blockDim.x) {
     const int e = j < E ? j : j - E;
     const int dir = j < E ? 0 : 1;     // 0: from v_I along +e_t; 1: from v_II along -e_t
-    int vI, vII;
-    float el[3], L;
-    edge_dir(lv, ed, e, vI, vII, el, L);
+    const int v0 = __ldg(ed + 2 * e + dir);
+    const float4 corner = ld4(sv + v0 * vrec(TIER));   // d, n of the start vertex (issued early)
+    // edge geometry from the vertex buffer here (the static edge table of
+    // the other kernels measured 3% slower in this one)
+    float xl[3], el[3], L;
+    {
+      const int vI = __ldg(ed + 2 * e), vII = __ldg(ed + 2 * e + 1);
+      const float dl[3] = {__ldg(lv + 3 * vII) - __ldg(lv + 3 * vI), __ldg(lv + 3 * vII + 1) - __ldg(lv + 3 * vI + 1),
+                           __ldg(lv + 3 * vII + 2) - __ldg(lv + 3 * vI + 2)};
+      L = sqrtf(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
+      const float iL = 1.f / L;
+      el[0] = dl[0] * iL; el[1] = dl[1] * iL; el[2] = dl[2] * iL;
+      xl[0] = __ldg(lv + 3 * vI); xl[1] = __ldg(lv + 3 * vI + 1); xl[2] = __ldg(lv + 3 * vI + 2);
+    }
     float eb[3], ew[3];
     rot_vec(F.Rrel, el, eb);
     rot_vec(F.RA, el, ew);
     float xI[3], pI[3];
-    vertex_frames(F, lv, vI, xI, pI);
-    const int v0 = dir ? vII : vI;
+    to_frames(F, xl, xI, pI);
     float al = dir ? L : 0.f;
     const float sgn = dir ? -1.f : 1.f;
     float da[NDQ];
@@ -364,9 +375,8 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::TRACES) k_m
     for (int it = 0; it < sp.iters; ++it) {
       float phi, g[3];
       if (it == 0) {   // the corner itself: reuse the vertex evaluation (reading #22)
-        const float4 dn = ld4(sv + v0 * vrec(TIER));
-        phi = dn.x;
-        g[0] = dn.y; g[1] = dn.z; g[2] = dn.w;
+        phi = corner.x;
+        g[0] = corner.y; g[1] = corner.z; g[2] = corner.w;
       } else {
         const float xb[3] = {fmaf(al, eb[0], xI[0]), fmaf(al, eb[1], xI[1]), fmaf(al, eb[2], xI[2])};
         Res<OT> r;
@@ -421,14 +431,12 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::MIDPOINTS) 
   const PairFrame& F = U.F;
   const int V = U.SA.V, E = U.SA.E;
   float* se = a.scratch + (int64_t)blockIdx.x * a.slot + (int64_t)vrec(TIER) * V;
-  const float* lv = a.S.verts + 3 * (int64_t)U.SA.v_off;
-  const int32_t* ed = a.S.edges + 2 * (int64_t)U.SA.e_off;
+  const float* eg = a.S.edge_geom + 8 * (int64_t)U.SA.e_off;
   const bool full = (a.mode & CM_FULL_MODE) != 0;
   const float itcmp = a.S.sp.i_cmp;
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    int vI, vII;
-    float el[3], L;
-    edge_dir(lv, ed, e, vI, vII, el, L);
+    float xl[3], el[3], L;
+    edge_geom(eg, e, xl, L, el);
     float eb[3], ew[3];
     rot_vec(F.Rrel, el, eb);
     rot_vec(F.RA, el, ew);
@@ -448,7 +456,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::MIDPOINTS) 
       ab = 0.5f * (rec[0] + rec[1]);
     }
     float xI[3], pI[3];
-    vertex_frames(F, lv, vI, xI, pI);
+    to_frames(F, xl, xI, pI);
     float xb[3], pw[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
@@ -528,7 +536,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, CM_MF_FACE_MINB) k_mf_faces
   const float* gv = a.scratch + (int64_t)blockIdx.x * a.slot;
   const float* ge = gv + (int64_t)VR * V;
   const float* lv = a.S.verts + 3 * (int64_t)U.SA.v_off;
-  const int32_t* ed = a.S.edges + 2 * (int64_t)U.SA.e_off;
+  const float* eg = a.S.edge_geom + 8 * (int64_t)U.SA.e_off;
   const int32_t* fv = a.S.faces + 3 * (int64_t)U.SA.f_off;
   const int32_t* fe = a.S.face_edges + 3 * (int64_t)U.SA.f_off;
   const cm_manifold_out& out = a.out;
@@ -550,11 +558,10 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, CM_MF_FACE_MINB) k_mf_faces
       for (int k = 0; k < 3; ++k) s_pv[k * V + v] = pw[k];
     }
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
-      int vI, vII;
-      float el[3], L, ew[3], xb[3], pI[3];
-      edge_dir(lv, ed, e, vI, vII, el, L);
+      float xl[3], el[3], L, ew[3], xb[3], pI[3];
+      edge_geom(eg, e, xl, L, el);
       rot_vec(F.RA, el, ew);
-      vertex_frames(F, lv, vI, xb, pI);
+      to_frames(F, xl, xb, pI);
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         s_pe[k * E + e] = pI[k];
@@ -593,12 +600,11 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, CM_MF_FACE_MINB) k_mf_faces
       } else {
         float xb[3];
         vertex_frames(F, lv, cv[k], xb, pc[k]);
-        int vI, vII;
-        float el[3], L;
-        edge_dir(lv, ed, ce[k], vI, vII, el, L);
+        float xl[3], el[3], L;
+        edge_geom(eg, ce[k], xl, L, el);
         rot_vec(F.RA, el, ewc[k]);
         float pI[3];
-        vertex_frames(F, lv, vI, xb, pI);
+        to_frames(F, xl, xb, pI);
         const float ab = se[ce[k] * ER + MAB];
 #pragma unroll
         for (int i = 0; i < 3; ++i) pc[3 + k][i] = fmaf(ab, ewc[k][i], pI[i]);
