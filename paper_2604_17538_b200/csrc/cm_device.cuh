@@ -14,12 +14,17 @@
 namespace cmd {
 using namespace cmi;
 
-// Code-size control: the XPSQ evaluators (and optionally the whole shape
-// interpreter) are kept out of line so that each exists once per derivative
-// order instead of once per call site; inlined, the XPSQ kernels exceed the
-// instruction cache (ncu: stalls on "no instructions").
+// Code-size control.  In the fused one-kernel manifold design the XPSQ
+// evaluators had to stay out of line (inlined, its four phases overflowed the
+// instruction cache).  The per-phase kernels hold one evaluation instance
+// each, so the constant-schedule evaluator is inlined there (the call ABI
+// spilled ~10% of the trace kernel's instructions to local memory; inlining:
+// C5 +6%, C4 +23%); the varying-schedule jets stay out of line.
 #ifndef CM_XPSQ_NOINLINE
 #define CM_XPSQ_NOINLINE 1
+#endif
+#ifndef CM_XPSQ_INLINE_MAX_O
+#define CM_XPSQ_INLINE_MAX_O 2   // constant-schedule XPSQ inlined up to this order
 #endif
 #ifndef CM_SHAPE_NOINLINE
 #define CM_SHAPE_NOINLINE 0
@@ -878,7 +883,8 @@ __device__ __forceinline__ bool xpsq_root_t(const Xpsq& X, const SmoothDev& sp, 
   return true;
 }
 
-template <int O> __device__ CM_XINL void xpsq_eval_fast(const Xpsq& X, const SmoothDev& sp, const float* y, Res<O>& out) {
+template <int O>
+__device__ __forceinline__ void xpsq_eval_fast_body(const Xpsq& X, const SmoothDev& sp, const float* y, Res<O>& out) {
   const float tau = sp.tau_min, itau = sp.i_min, itl = LOG2E * itau;
   const float w[3] = {y[0] - X.p1[0], y[1] - X.p1[1], y[2] - X.p1[2]};
   float tv[3], tg[3][3], th[3][6];
@@ -1000,6 +1006,10 @@ template <int O> __device__ CM_XINL void xpsq_eval_fast(const Xpsq& X, const Smo
   }
   acc_final(acc, -1.f, tau, itau, out);
 }
+// out-of-line instance, used above CM_XPSQ_INLINE_MAX_O
+template <int O> __device__ CM_XINL void xpsq_eval_fast(const Xpsq& X, const SmoothDev& sp, const float* y, Res<O>& out) {
+  xpsq_eval_fast_body<O>(X, sp, y, out);
+}
 
 // ---- leaf dispatch ---------------------------------------------------------
 // XP: 0 no XPSQ leaves, 1 constant-schedule XPSQ (analytic fast path),
@@ -1041,6 +1051,8 @@ __device__ __forceinline__ void leaf_eval(const SceneDev& S, int li, const float
     if constexpr (XP == 2) {
       if (X.varying) xpsq_eval<O>(X, S.sp, y, l);   // schedules vary along t: jets
       else xpsq_eval_fast<O>(X, S.sp, y, l);
+    } else if constexpr (O <= CM_XPSQ_INLINE_MAX_O) {
+      xpsq_eval_fast_body<O>(X, S.sp, y, l);
     } else {
       xpsq_eval_fast<O>(X, S.sp, y, l);
     }
