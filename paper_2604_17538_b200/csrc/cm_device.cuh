@@ -1013,8 +1013,10 @@ template <int O> __device__ CM_XINL void xpsq_eval_fast(const Xpsq& X, const Smo
 
 // ---- leaf dispatch ---------------------------------------------------------
 // XP: 0 no XPSQ leaves, 1 constant-schedule XPSQ (analytic fast path),
-// 2 any XPSQ (jets when the schedules vary along t)
-template <int O, int XP>
+// 2 any XPSQ (jets when the schedules vary along t); XINL: constant-schedule
+// XPSQ inlined up to order CM_XPSQ_INLINE_MAX_O (manifold kernels) or always
+// out of line (sdf_eval: one kernel for all leaf kinds, measured faster so)
+template <int O, int XP, bool XINL = true>
 __device__ __forceinline__ void leaf_eval(const SceneDev& S, int li, const float* x, Res<O>& r) {
   const Leaf& L = S.leaves[li];
   float y[3];
@@ -1051,7 +1053,7 @@ __device__ __forceinline__ void leaf_eval(const SceneDev& S, int li, const float
     if constexpr (XP == 2) {
       if (X.varying) xpsq_eval<O>(X, S.sp, y, l);   // schedules vary along t: jets
       else xpsq_eval_fast<O>(X, S.sp, y, l);
-    } else if constexpr (O <= CM_XPSQ_INLINE_MAX_O) {
+    } else if constexpr (XINL && O <= CM_XPSQ_INLINE_MAX_O) {
       xpsq_eval_fast_body<O>(X, S.sp, y, l);
     } else {
       xpsq_eval_fast<O>(X, S.sp, y, l);
@@ -1090,11 +1092,11 @@ __device__ __forceinline__ void fold_level(Acc<O>& a0, Acc<O>& a1, Acc<O>& a2, i
 // phi, grad, hess of shape `sh` at the body-frame point x
 // FLAT: every boolean node of the shape sits at the root (nesting depth <= 1),
 // so one accumulator level suffices (fewer live registers)
-template <int O, int XP, bool FLAT = false>
+template <int O, int XP, bool FLAT = false, bool XINL = true>
 __device__ CM_SINL void eval_shape(const SceneDev& S, const ShapeRec& sh, const float* x, Res<O>& out) {
   const float tau = S.sp.tau_min, itau = S.sp.i_min, itl = LOG2E * itau;
   if (sh.prog_len == 1) {  // single leaf: no accumulator needed
-    leaf_eval<O, XP>(S, S.prog[sh.prog_begin].idx, x, out);
+    leaf_eval<O, XP, XINL>(S, S.prog[sh.prog_begin].idx, x, out);
     return;
   }
   Acc<O> a0, a1, a2;
@@ -1111,7 +1113,7 @@ __device__ CM_SINL void eval_shape(const SceneDev& S, const ShapeRec& sh, const 
     }
     Res<O> r;
     if (in.op == OP_LEAF) {
-      leaf_eval<O, XP>(S, in.idx, x, r);
+      leaf_eval<O, XP, XINL>(S, in.idx, x, r);
     } else {
       if (FLAT || lvl == 0) acc_final(a0, in.out_sign, tau, itau, r);
       else if (lvl == 1) acc_final(a1, in.out_sign, tau, itau, r);

@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(256) k_sdf_eval(SceneDev S, const int32_t* __r
     float y[3];
     to_local(R, t, x, y);
     Res<O> r;
-    eval_shape<O, XP == 3 ? 0 : XP, XP == 0>(S, sh, y, r);
+    eval_shape<O, XP == 3 ? 0 : XP, XP == 0, false>(S, sh, y, r);
     d[n] = r.v;
     if constexpr (O >= 1) {
       float g[3];
