@@ -1,14 +1,9 @@
-// sm_100a kernels of the hot path (arXiv 2604.17538):
-//   k_sdf_eval          batched SDF value / gradient / Hessian (+ pose
-//                       derivatives) — §II-B, Eq. (1)-(6)
-//   k_contact_manifold  one CTA per (env, pair): sampled-surface vertices ->
-//                       sphere-traced edge points -> 6 candidates per face ->
-//                       softmax fusion -> SoA stores — §II-C
-//   k_face_counts / cub scan, k_expand_jacobian   (offsets, J expansion)
-//
-// Hot-path design: FP32 CUDA-core math (no tensor cores: the
-// path is not a dense contraction), MUFU ex2/lg2/rcp in the log domain,
-// pair-local candidate state in shared memory, field-major coalesced stores.
+// sm_100a kernel of the sdf_eval path (arXiv 2604.17538 §II-B, Eq. (1)-(6)):
+//   k_sdf_eval  batched SDF value / gradient / Hessian (+ pose derivatives),
+//               one thread per point, one instantiation per SDF class.
+// FP32 CUDA-core math (not a dense contraction: no tensor cores), MUFU
+// ex2/lg2/rcp in the log domain, field-major coalesced stores.
+// The manifold kernels are in cm_kernels_manifold.cu.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
