@@ -84,14 +84,16 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
-def make_scene(workload, n_env, env_lo):
+def make_scene(workload, n_env, env_lo, K=18):
     from paper_2604_17538_b200 import synth
+    if workload == "C1":
+        return synth.c1_scene()
     if workload == "C5":
         return synth.c5_scene(n_env, env_lo=env_lo)
     if workload == "C4":
         return synth.c4_scene(n_env, seed=4 + 1000 * (env_lo // max(n_env, 1)))
     if workload == "C3":
-        return synth.c3_scene(n_env, seed=3 + 1000 * (env_lo // max(n_env, 1)))
+        return synth.c3_scene(n_env, seed=3 + 1000 * (env_lo // max(n_env, 1)), K=K)
     if workload == "C2":
         return synth.c2_scene(n_env, seed=2 + 1000 * (env_lo // max(n_env, 1)))
     if workload == "SDF":
@@ -99,7 +101,7 @@ def make_scene(workload, n_env, env_lo):
     raise SystemExit("unknown workload " + workload)
 
 
-DEFAULT_NENV = {"C5": 1 << 20, "C4": 1 << 16, "C3": 1 << 14, "C2": 1000, "SDF": 1 << 18}
+DEFAULT_NENV = {"C5": 1 << 20, "C4": 1 << 16, "C3": 1 << 14, "C2": 1000, "SDF": 1 << 18, "C1": 1}
 SDF_P = 64            # query points per body (SDF workload)
 SDF_METRIC = "sdf_eval point-evaluations/sec (value + gradient + Hessian + pose gradient)"
 SDF_BYTES_PER_POINT = 12 + 4 + 12 + 24 + 24   # point in; d, grad, hess (6), dpose (6) out
@@ -385,7 +387,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C5", choices=["C5", "C4", "C3", "C2", "SDF"])
+    ap.add_argument("--workload", default="C5", choices=["C5", "C4", "C3", "C2", "SDF", "C1"])
+    ap.add_argument("--k", type=int, default=18, help="C3: number of SQs in the smooth union (P:200 sweep)")
     ap.add_argument("--n-env", type=int, default=0)
     ap.add_argument("--tier", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -406,7 +409,7 @@ def main():
 
     n_env = args.n_env or DEFAULT_NENV[args.workload]
     t0 = time.time()
-    scene = make_scene(args.workload, n_env, rank * n_env)
+    scene = make_scene(args.workload, n_env, rank * n_env, K=args.k)
     gen_s = time.time() - t0
     if args.workload == "SDF":
         return run_sdf(args, scene, n_env, gen_s, world, rank, local)
@@ -512,6 +515,10 @@ def main():
                            "input_gen_s": round(gen_s, 1)},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk}
+        if args.workload == "C3" and args.k != 18:
+            line["config"]["sqs_in_union"] = args.k
+        if args.workload == "C1":   # latency-bound: report the per-call latency
+            line["config"]["latency_us_per_call"] = ms_per_step * 1e3
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
