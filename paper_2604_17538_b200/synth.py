@@ -358,7 +358,7 @@ def blob18(seed: int = 3, K: int = 18):
         c = rng.uniform(-0.15, 0.15, 3)
         q = random_quats(rng, 1)[0]
         kids.append(sq(a, eps, pose=[*c, *q]))
-    return op("union", kids)
+    return kids[0] if K == 1 else op("union", kids)   # a union needs >= 2 operands
 
 
 def _node_surface_points(node: Node, n=400):
