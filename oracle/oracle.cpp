@@ -920,6 +920,118 @@ int ora_contact_manifold(void* s, const int* pairs, long n_pairs, const double* 
   return 0;
 }
 
+// ---- second-order manifold derivatives (P:8 motivates
+// Hessians for second-order control) ----------------------------------------
+// The same manifold as ora_contact_manifold (reduced or full mode, one- or
+// two-sided), recomputed with second-order q-jets Dual<Dual<double,12>,12>:
+// d2depth[78 c + k] = d^2 depth / dq_i dq_j for the packed upper triangle
+// i <= j of the pair-ordered q = (dt_A, dtheta_A, dt_B, dtheta_B) (k runs over
+// (0,0), (0,1), .., (0,11), (1,1), ..).  In full mode the depth of a row is
+// the candidate's phi.  Every step is the literal one of ora_contact_manifold
+// on the second-order jet type (no derivative is hand-derived here).
+using Q2 = Dual<D12, 12>;
+int ora_manifold_d2depth(void* s, const int* pairs, long n_pairs, const double* poses, long n_env, int n_slot,
+                         double* d2depth, int mode, int n_threads) {
+  Scene* sc = (Scene*)s;
+  const Smooth sp = sc->sp;
+  (void)n_env;
+  const bool full = (mode & 4) != 0, two = (mode & 8) != 0;
+  auto count = [&](int shape) { const Mesh& m = sc->shapes[shape].mesh; return full ? (long)m.V + m.E : (long)m.F; };
+  std::vector<long> off(n_pairs + 1, 0);
+  for (long i = 0; i < n_pairs; ++i)
+    off[i + 1] = off[i] + count(pairs[5 * i + 3]) + (two ? count(pairs[5 * i + 4]) : 0);
+  auto store = [&](long c, const Q2& x) {
+    int k = 0;
+    for (int i = 0; i < 12; ++i)
+      for (int j = i; j < 12; ++j) d2depth[78 * c + (k++)] = x.d[i].d[j];
+  };
+#ifdef _OPENMP
+  if (n_threads > 0) omp_set_num_threads(n_threads);
+#endif
+#pragma omp parallel for schedule(dynamic, 1)
+  for (long pi = 0; pi < n_pairs; ++pi) {
+   long row0 = off[pi];
+   for (int side = 0; side < (two ? 2 : 1); ++side) {
+    const int* pr = pairs + 5 * pi;
+    const Shape& SA = sc->shapes[pr[3 + side]];
+    const Shape& SB = sc->shapes[pr[4 - side]];
+    const Mesh& m = SA.mesh;
+    const double* pa = poses + 8 * ((long)pr[0] * n_slot + pr[1 + side]);
+    const double* pb = poses + 8 * ((long)pr[0] * n_slot + pr[2 - side]);
+    double RA[9], RB[9], tA[3] = {pa[0], pa[1], pa[2]}, tB[3] = {pb[0], pb[1], pb[2]};
+    double qa[4] = {pa[3], pa[4], pa[5], pa[6]}, qb[4] = {pb[3], pb[4], pb[5], pb[6]};
+    quat_to_R(qa, RA); quat_to_R(qb, RB);
+    // second-order seeds: q_k carries d/dq_k at both jet levels
+    const int sA = side ? 6 : 0, sB = side ? 0 : 6;
+    auto seed = [](int k) { Q2 x(0.0); x.v.d[k] = 1.0; x.d[k].v = 1.0; return x; };
+    Q2 dtA[3], wA[3], dtB[3], wB[3];
+    for (int i = 0; i < 3; ++i) {
+      dtA[i] = seed(sA + i); wA[i] = seed(sA + 3 + i);
+      dtB[i] = seed(sB + i); wB[i] = seed(sB + 3 + i);
+    }
+    Q2 RAq[9], tAq[3], RBq[9], tBq[3];
+    perturbed_pose(RA, tA, dtA, wA, RAq, tAq);
+    perturbed_pose(RB, tB, dtB, wB, RBq, tBq);
+    auto world_of = [&](const double* v, Q2* p) {
+      for (int i = 0; i < 3; ++i) p[i] = RAq[i * 3 + 0] * v[0] + RAq[i * 3 + 1] * v[1] + RAq[i * 3 + 2] * v[2] + tAq[i];
+    };
+    auto phi = [&](const Q2* p) { return shape_phi_world(SB, RBq, tBq, p, sp); };
+    std::vector<Q2> vd(m.V), ed(m.E);
+    for (int k = 0; k < m.V; ++k) {
+      Q2 p[3];
+      world_of(&m.v[3 * k], p);
+      vd[k] = phi(p);
+    }
+    for (int e = 0; e < m.E; ++e) {   // trace both corners, clip, midpoint
+      const double* vI = &m.v[3 * m.e[2 * e]];
+      const double* vII = &m.v[3 * m.e[2 * e + 1]];
+      double dl[3] = {vII[0] - vI[0], vII[1] - vI[1], vII[2] - vI[2]};
+      double L = std::sqrt(dot3(dl, dl));
+      double etl[3] = {dl[0] / L, dl[1] / L, dl[2] / L};
+      Q2 pI[3], et[3];
+      world_of(vI, pI);
+      for (int i = 0; i < 3; ++i) et[i] = RAq[i * 3 + 0] * etl[0] + RAq[i * 3 + 1] * etl[1] + RAq[i * 3 + 2] * etl[2];
+      Q2 alpha(0.0), beta(L);
+      for (int it = 0; it < sp.trace_iters; ++it) {
+        Q2 x[3];
+        for (int i = 0; i < 3; ++i) x[i] = pI[i] + alpha * et[i];
+        Q2 ph = phi(x);
+        alpha = alpha + sigmoid(ph / sp.tau_cmp) * ph;
+      }
+      for (int it = 0; it < sp.trace_iters; ++it) {
+        Q2 x[3];
+        for (int i = 0; i < 3; ++i) x[i] = pI[i] + beta * et[i];
+        Q2 ph = phi(x);
+        beta = beta - sigmoid(ph / sp.tau_cmp) * ph;
+      }
+      Q2 ab = 0.5 * (softclip(alpha, 0.0, L, sp.tau_clip_alpha) + softclip(beta, 0.0, L, sp.tau_clip_alpha));
+      Q2 x[3];
+      for (int i = 0; i < 3; ++i) x[i] = pI[i] + ab * et[i];
+      ed[e] = phi(x);
+    }
+    if (full) {
+      std::vector<int> eo(m.E);
+      for (int e = 0; e < m.E; ++e) eo[e] = e;
+      std::sort(eo.begin(), eo.end(), [&](int a, int b) {
+        return std::make_pair(m.e[2 * a], m.e[2 * a + 1]) < std::make_pair(m.e[2 * b], m.e[2 * b + 1]); });
+      for (int k = 0; k < m.V + m.E; ++k) store(row0 + k, k < m.V ? vd[k] : ed[eo[k - m.V]]);
+      row0 += m.V + m.E;
+      continue;
+    }
+    for (int f = 0; f < m.F; ++f) {   // smooth-min depth of the face's 6 candidates
+      Q2 negd[6];
+      for (int k = 0; k < 3; ++k) {
+        negd[k] = -vd[m.f[3 * f + k]];
+        negd[3 + k] = -ed[m.fe[3 * f + k]];
+      }
+      store(row0 + f, -lse(negd, 6, sp.tau_min));
+    }
+    row0 += m.F;
+   }
+  }
+  return 0;
+}
+
 int ora_max_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

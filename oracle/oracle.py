@@ -53,6 +53,7 @@ def lib():
         L.ora_mesh_topology.argtypes = [p, i, p, p]
         L.ora_sdf_eval.argtypes = [p, p, p, p, l, l, i, p, p, p, p, p, p]
         L.ora_contact_manifold.argtypes = [p, p, l, p, l, i] + [p] * 12 + [i, i]
+        L.ora_manifold_d2depth.argtypes = [p, p, l, p, l, i, p, i, i]
         L.ora_max_threads.restype = i
         _lib = L
     return _lib
@@ -222,6 +223,23 @@ class OracleScene:
                                                             "dnormal", "dom", "J", "z", "dcand", "gamma")],
                                    int(mode), int(n_threads))
         out["offsets"] = np.concatenate([[0], np.cumsum(F)]).astype(np.int64)
+        return out
+
+    def manifold_d2depth(self, pairs=None, poses=None, n_threads=0, mode=0):
+        """d^2 depth / dq^2 per contact (packed upper triangle, 78 per row, q in
+        the pair's (t_A, theta_A, t_B, theta_B) order) for the same rows as
+        contact_manifold(pairs, poses, mode=mode)."""
+        sc = self.scene
+        pairs = np.ascontiguousarray(sc.pairs if pairs is None else pairs, dtype=np.int32)
+        poses = np.ascontiguousarray(sc.poses if poses is None else poses, dtype=np.float64)
+        n_env, n_slot = poses.shape[0], poses.shape[1]
+        def cnt(s):
+            V, E, F_ = self.mesh_counts(int(s))
+            return V + E if mode & 4 else F_
+        Ct = int(sum(cnt(a) + (cnt(b) if mode & 8 else 0) for a, b in zip(pairs[:, 3], pairs[:, 4])))
+        out = np.zeros((Ct, 78))
+        lib().ora_manifold_d2depth(self.h, _ptr(pairs), len(pairs), _ptr(poses), n_env, n_slot, _ptr(out),
+                                   int(mode), int(n_threads))
         return out
 
 

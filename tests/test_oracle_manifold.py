@@ -406,3 +406,99 @@ def test_two_sided_mirror_symmetry(oracle_mod):
     n = len(out["depth"]) // 2
     assert np.allclose(np.sort(out["depth"][:n]), np.sort(out["depth"][n:]), atol=1e-12)
     assert np.allclose(out["normal"][:n].sum(0), -out["normal"][n:].sum(0), atol=1e-12)
+
+
+# ---- second-order manifold derivatives -------------------
+def _unpack78(h):
+    iu = np.triu_indices(12)
+    H = np.zeros(h.shape[:-1] + (12, 12))
+    H[..., iu[0], iu[1]] = h
+    H[..., iu[1], iu[0]] = h
+    return H
+
+
+def _d2_value_fd(osc, poses, mode, h):
+    """Second central differences of the oracle's depth VALUES in the
+    exp-map chart of each body (one exponential per body, so the chart's
+    Hessian is symmetric): independent of the jets."""
+    def f(dq):
+        pp = poses.copy()
+        pp[0, 0] = perturb(poses[0, 0], dq[:6])
+        pp[0, 1] = perturb(poses[0, 1], dq[6:])
+        return osc.contact_manifold(poses=pp, mode=mode)["depth"]
+    iu = np.triu_indices(12)
+    cols = []
+    for i, j in zip(*iu):
+        ei = np.zeros(12); ei[i] = h
+        ej = np.zeros(12); ej[j] = h
+        cols.append((f(ei + ej) - f(ei - ej) - f(-ei + ej) + f(-ei - ej)) / (4 * h * h))
+    return np.stack(cols, 1)
+
+
+@pytest.mark.parametrize("kind,seed,mode", [("sq", 1, 0), ("cup", 4, 0), ("blob", 3, 0), ("sq", 2, 4)])
+def test_manifold_d2depth_fd(oracle_mod, kind, seed, mode):
+    """d^2 depth / dq^2 (second-order q-jets through the whole manifold) vs
+    second differences of the oracle's depth values (reduced and full mode)."""
+    O = oracle_mod
+    shapes, poses, ell = _random_pair_scene(O, seed, kind)
+    poses = poses.astype(np.float32).astype(np.float64)
+    pairs = np.array([[0, 0, 1, 0, 1]], np.int32)
+    _, osc = _manifold(O, shapes, poses, pairs, ell)
+    H = osc.manifold_d2depth(poses=poses, mode=mode)
+    Hfd = _d2_value_fd(osc, poses, mode, 3e-5 * ell)
+    scale = np.maximum(1.0 / ell, np.abs(H).max(1))
+    err = np.abs(H - Hfd).max(1) / scale
+    assert err.max() < 5e-3 and np.median(err) < 1e-4, (err.max(), np.median(err))
+
+
+def test_manifold_d2depth_gradient_consistency_and_invariance(oracle_mod):
+    """C1: the Hessian equals the symmetrised central difference of the
+    first-order ddepth (the antisymmetric part of that difference is the
+    Baker-Campbell-Hausdorff term of composing two left twists; pair 0, whose
+    columns are slots 0 then 1), and on both pairs it inherits translation
+    invariance: rows / columns of t_B are minus those of t_A."""
+    O = oracle_mod
+    sc = synth.c1_scene()
+    osc = O.OracleScene(sc)
+    poses = sc.poses.astype(np.float64)
+    assert tuple(sc.pairs[0, 1:3]) == (0, 1)
+    H = _unpack78(osc.manifold_d2depth(poses=poses))
+    F0 = osc.mesh_counts(int(sc.pairs[0, 3]))[2]
+    rows = np.arange(0, F0, 7)
+    h = 1e-5
+    cols = []
+    for j in range(12):
+        e = np.zeros(6); e[j % 6] = h
+        pp, pm = poses.copy(), poses.copy()
+        pp[0, j // 6] = perturb(poses[0, j // 6], e)
+        pm[0, j // 6] = perturb(poses[0, j // 6], -e)
+        cols.append((osc.contact_manifold(poses=pp)["ddepth"][rows] - osc.contact_manifold(poses=pm)["ddepth"][rows]) / (2 * h))
+    Hfd = np.stack(cols, 2)                       # [row, i, j]
+    Hs = 0.5 * (Hfd + np.swapaxes(Hfd, 1, 2))
+    scale = np.maximum(1.0, np.abs(H[rows]).max((1, 2)))
+    assert np.all(np.abs(H[rows] - Hs).max((1, 2)) <= 1e-3 * scale)
+    tol = 1e-9 * np.abs(H).max()
+    tA, tB = slice(0, 3), slice(6, 9)
+    assert np.allclose(H[:, tB, 3:6], -H[:, tA, 3:6], atol=tol)
+    assert np.allclose(H[:, tB, 9:12], -H[:, tA, 9:12], atol=tol)
+    assert np.allclose(H[:, tB, tB], H[:, tA, tA], atol=tol)
+    assert np.allclose(H[:, tA, tB], -H[:, tA, tA], atol=tol)
+
+
+def test_manifold_d2depth_two_sided(oracle_mod):
+    """Two-sided rows: the first half equals the one-sided Hessian; the second
+    half equals the transposed pair's Hessian with the body blocks swapped."""
+    O = oracle_mod
+    sc = synth.c1_scene()
+    osc = O.OracleScene(sc)
+    pr = sc.pairs[:1]
+    one = osc.manifold_d2depth(pairs=pr)
+    two = osc.manifold_d2depth(pairs=pr, mode=8)
+    n = len(one)
+    assert np.allclose(two[:n], one, rtol=0, atol=1e-12 * np.abs(one).max())
+    trp = pr[:, [0, 2, 1, 4, 3]]
+    Ht = _unpack78(osc.manifold_d2depth(pairs=trp))
+    perm = np.r_[6:12, 0:6]
+    Hs = Ht[:, perm][:, :, perm]
+    H2 = _unpack78(two[n:])
+    assert np.allclose(H2, Hs, rtol=0, atol=1e-12 * np.abs(Hs).max())
