@@ -40,7 +40,7 @@ sys.path.insert(0, ROOT)
 # with M(mesh_A) the tier-2 manifold FLOPs of the mesh against a half-space.
 # Bytes per pair are algorithmic too (inputs: two poses + the pair record;
 # outputs: F contacts x 237 B at tier 2).
-OUT_BYTES_PER_CONTACT = {0: 33, 1: 45, 2: 237}
+OUT_BYTES_PER_CONTACT = {0: 33, 1: 45, 2: 237, 3: 237 + 78 * 4}
 IN_BYTES_PER_PAIR = 2 * 32 + 20
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4 at the 1965 MHz max SM clock
 
@@ -505,7 +505,8 @@ def main():
                "sample": "first %d pairs of the %s shard, FP64 jet oracle, OpenMP over pairs, %.1f s" % (m, args.workload, dt)}
 
     if rank == 0:
-        line = {"metric": "contact-manifold evals/sec with derivatives (tier 2)", "value": value, "unit": "pairs/s",
+        line = {"metric": "contact-manifold evals/sec with derivatives (tier %d)" % args.tier, "value": value,
+                "unit": "pairs/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic",

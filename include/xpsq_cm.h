@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define CM_ABI_VERSION 1
+#define CM_ABI_VERSION 2
 #define CM_MAX_PLANES 8      /* half-spaces per PSQ / XPSQ cross-section      */
 #define CM_MAX_CHILDREN 32   /* children per boolean node                     */
 #define CM_MAX_DEPTH 3       /* nesting of boolean nodes in one shape         */
@@ -185,10 +185,16 @@ int cm_sdf_eval(const cm_scene* scene, const int32_t* shape_ids, const float* po
  *           3x12 contact Jacobian sum z_i gamma_i J_i is exactly
  *           [W I, -[q - W tA]x, -W I, [q - W tB]x] (cm_expand_jacobian)
  *   tier 2: ddepth[12C] and dnormal[36C] ([i*12+j] = d n_i / d q_j): the
- *           derivatives with respect to q = (dt_A, dtheta_A, dt_B, dtheta_B). */
+ *           derivatives with respect to q = (dt_A, dtheta_A, dt_B, dtheta_B)
+ *   tier 3: d2depth[78C]: the second derivatives d^2 depth / dq_i dq_j, packed
+ *           upper triangle i <= j in row order ((0,0), (0,1), .., (0,11),
+ *           (1,1), ..), field k at d2depth[k*C + row] (
+ *           P:8 motivates Hessians for second-order control).  Full mode:
+ *           of the candidate's phi. */
 #define CM_TIER0 0u
 #define CM_TIER1 1u
 #define CM_TIER2 2u
+#define CM_TIER3 3u
 #define CM_TIER_MASK 3u
 /* CM_FULL_MODE: one contact per vertex and per edge of the sampled
  * surface (V + E rows, vertices first, then edges in cm_shape_topology order)
@@ -212,6 +218,7 @@ typedef struct cm_manifold_out {
   float* ddepth;
   float* dnormal;
   int8_t* dom;
+  float* d2depth;   /* tier 3 only (may be NULL below tier 3) */
 } cm_manifold_out;
 
 /* Number of contacts of a pair list given on the HOST (pairs_host [n,5]) for

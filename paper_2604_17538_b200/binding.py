@@ -45,7 +45,7 @@ class cm_smooth_params(C.Structure):
 
 
 class cm_manifold_out(C.Structure):
-    _fields_ = [(k, C.c_void_p) for k in ("point", "normal", "depth", "W", "q", "ddepth", "dnormal", "dom")]
+    _fields_ = [(k, C.c_void_p) for k in ("point", "normal", "depth", "W", "q", "ddepth", "dnormal", "dom", "d2depth")]
 
 
 class CMError(RuntimeError):
@@ -251,6 +251,8 @@ class Scene:
         if tier >= 2:
             out["ddepth"] = e(12, C_)
             out["dnormal"] = e(36, C_)
+        if tier >= 3:
+            out["d2depth"] = e(78, C_)
         return out
 
     def contact_manifold(self, pairs, offsets, n_contacts: int, poses, tier: int = 2, out=None, mode: int = 0):
@@ -263,7 +265,7 @@ class Scene:
         if out is None:
             out = self.alloc_manifold(n_contacts, tier, poses.device)
         o = cm_manifold_out(*[out[k].data_ptr() if k in out else None
-                              for k in ("point", "normal", "depth", "W", "q", "ddepth", "dnormal", "dom")])
+                              for k in ("point", "normal", "depth", "W", "q", "ddepth", "dnormal", "dom", "d2depth")])
         _check(lib().cm_contact_manifold(self.h, _ptr(pairs), pairs.shape[0], _ptr(offsets), _ptr(poses),
                                          poses.shape[0], poses.shape[1], tier | mode, C.byref(o), n_contacts,
                                          _stream()), "cm_contact_manifold")

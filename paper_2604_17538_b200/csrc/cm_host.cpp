@@ -560,10 +560,11 @@ int cm_contact_manifold(const cm_scene* sc, const int32_t* pairs, int64_t n_pair
   if (n_pairs == 0) return CM_OK;   // empty batch: nothing to launch
   if (!pairs || !offsets || !poses) return fail(CM_ERR_INVALID, "cm_contact_manifold: NULL argument");
   const unsigned tier = flags & CM_TIER_MASK;
-  if (tier > 2) return fail(CM_ERR_INVALID, "cm_contact_manifold: tier");
+  if (tier > 3) return fail(CM_ERR_INVALID, "cm_contact_manifold: tier");
   if (!out->point || !out->normal || !out->depth || !out->dom) return fail(CM_ERR_INVALID, "tier-0 outputs are NULL");
   if (tier >= 1 && (!out->W || !out->q)) return fail(CM_ERR_INVALID, "tier-1 outputs are NULL");
   if (tier >= 2 && (!out->ddepth || !out->dnormal)) return fail(CM_ERR_INVALID, "tier-2 outputs are NULL");
+  if (tier >= 3 && !out->d2depth) return fail(CM_ERR_INVALID, "tier-3 output d2depth is NULL");
   if (sc->max_F == 0) return fail(CM_ERR_INVALID, "scene has no sampled surface");
   cm_scene* ms = const_cast<cm_scene*>(sc);   // internal scheduling state only
   std::lock_guard<std::mutex> lock(ms->mu);

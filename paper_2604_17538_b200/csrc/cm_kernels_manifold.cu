@@ -34,10 +34,16 @@ using cml::num_sms;
 //   edge record after traces:    a_I, da_I[9], a_II, da_II[9] (tier 2: 20 floats;
 //                                else a_I, a_II in 8)
 //   edge record after midpoint:  a_bar, d, n[3], H[6], da_bar[9] (else a_bar, d, n[3])
+// tier 3 adds the second derivatives over the 9 independent coordinates
+// z = (t_A, theta_A, theta_B) (t_B = -t_A by translation invariance), packed
+// upper 9x9 (45): vertex record + d2d[45] at 12 (60 floats); per trace
+// direction a, da[9], d2a[45] (56 floats each, a_II record at 56); after the
+// midpoint d2d[45] at 20 (edge record 112 floats).
 // ============================================================================
-__host__ __device__ constexpr int vrec(int tier) { return tier >= 2 ? 12 : 4; }
-__host__ __device__ constexpr int erec(int tier) { return tier >= 2 ? 20 : 8; }
-__host__ __device__ constexpr int trace_b(int tier) { return tier >= 2 ? 10 : 1; }   // a_II offset
+__host__ __device__ constexpr int vrec(int tier) { return tier >= 3 ? 60 : (tier >= 2 ? 12 : 4); }
+__host__ __device__ constexpr int erec(int tier) { return tier >= 3 ? 112 : (tier >= 2 ? 20 : 8); }
+__host__ __device__ constexpr int trace_b(int tier) { return tier >= 3 ? 56 : (tier >= 2 ? 10 : 1); }   // a_II offset
+enum { VD2 = 12, TD2 = 10, MD2 = 20 };                    // tier-3 offsets of the 45 second derivatives
 enum { VD = 0, VN = 1, VH = 4 };
 enum { MAB = 0, MD = 1, MN = 2, MH = 5, MDAB = 11 };       // midpoint layout
 
@@ -85,6 +91,105 @@ __device__ __forceinline__ void gJ(const float* g, const float* p, const PairFra
 
 // derivative slots: 9 independent components (tA, thetaA, thetaB); tB = -tA
 constexpr int NDQ = 9;
+constexpr int N45 = 45;   // packed upper 9x9
+__host__ __device__ constexpr int p9(int i, int j) { return i * 9 - i * (i - 1) / 2 + (j - i); }   // i <= j
+
+// ---- tier 3: second derivatives over z = (t_A, theta_A, theta_B) ----------
+// A material point p of the sampled body A, evaluated in the SDF of B (world
+// gradient g, Hessian H), under world-frame left twists of A and B (B's
+// translation held: its derivatives are minus t_A's):
+//   w(z) = exp(-[th_B]x)(exp([th_A]x)(p - t_A) + t_A + dt_A - t_B) + t_B,
+//   d^2 phi = J^T H J + G,  J = [I, -[r_A]x, [r_B]x]  (r_X = p - t_X),
+//   G: (t_A, th_B) = -[g]x;  (th_A, th_A) = sym(g r_A^T) - (g.r_A) I;
+//      (th_A, th_B) = -g r_A^T + (g.r_A) I;  (th_B, th_B) = sym(g r_B^T) - (g.r_B) I;
+//   (the second-order terms of exp and of the cross terms -th_B x (dt_A + th_A x r_A)).
+__device__ __forceinline__ void d2_point(const float* g, const float* h6, const float* p, const float* tA,
+                                         const float* tB, float* o /*45*/) {
+  const float ra[3] = {p[0] - tA[0], p[1] - tA[1], p[2] - tA[2]};
+  const float rb[3] = {p[0] - tB[0], p[1] - tB[1], p[2] - tB[2]};
+  const float H[3][3] = {{h6[0], h6[1], h6[2]}, {h6[1], h6[3], h6[4]}, {h6[2], h6[4], h6[5]}};
+  // J (3 x 9): t_A -> e_a;  th_A -> e_a x r_A;  th_B -> r_B x e_b
+  const float J[3][9] = {{1.f, 0.f, 0.f, 0.f, ra[2], -ra[1], 0.f, -rb[2], rb[1]},
+                         {0.f, 1.f, 0.f, -ra[2], 0.f, ra[0], rb[2], 0.f, -rb[0]},
+                         {0.f, 0.f, 1.f, ra[1], -ra[0], 0.f, -rb[1], rb[0], 0.f}};
+  float HJ[3][9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int c = 0; c < 9; ++c) HJ[i][c] = H[i][0] * J[0][c] + H[i][1] * J[1][c] + H[i][2] * J[2][c];
+  const float gra = g[0] * ra[0] + g[1] * ra[1] + g[2] * ra[2];
+  const float grb = g[0] * rb[0] + g[1] * rb[1] + g[2] * rb[2];
+#pragma unroll
+  for (int c1 = 0; c1 < 9; ++c1)
+#pragma unroll
+    for (int c2 = c1; c2 < 9; ++c2) {
+      float v = J[0][c1] * HJ[0][c2] + J[1][c1] * HJ[1][c2] + J[2][c1] * HJ[2][c2];
+      if (c1 < 3 && c2 >= 6) {                     // (t_A a, th_B b): eps_abk g_k
+        const int a = c1, b = c2 - 6;
+        v += (a == b) ? 0.f : ((b == (a + 1) % 3) ? g[(a + 2) % 3] : -g[(a + 1) % 3]);
+      } else if (c1 >= 3 && c1 < 6 && c2 < 6) {   // (th_A a, th_A b)
+        const int a = c1 - 3, b = c2 - 3;
+        v += 0.5f * (g[a] * ra[b] + g[b] * ra[a]) - (a == b ? gra : 0.f);
+      } else if (c1 >= 3 && c1 < 6 && c2 >= 6) {  // (th_A a, th_B b)
+        const int a = c1 - 3, b = c2 - 6;
+        v += -g[a] * ra[b] + (a == b ? gra : 0.f);
+      } else if (c1 >= 6) {                        // (th_B a, th_B b)
+        const int a = c1 - 6, b = c2 - 6;
+        v += 0.5f * (g[a] * rb[b] + g[b] * rb[a]) - (a == b ? grb : 0.f);
+      }
+      o[p9(c1, c2)] = v;
+    }
+}
+// for a point sliding along the edge direction e_t (world): phi_za (9) =
+// J^T H e_t + (0, e_t x g, g x e_t) and phi_aa = e_t^T H e_t
+__device__ __forceinline__ void d2_alpha(const float* g, const float* h6, const float* p, const float* ew,
+                                         const float* tA, const float* tB, float* fza, float& faa) {
+  const float ra[3] = {p[0] - tA[0], p[1] - tA[1], p[2] - tA[2]};
+  const float rb[3] = {p[0] - tB[0], p[1] - tB[1], p[2] - tB[2]};
+  const float He[3] = {h6[0] * ew[0] + h6[1] * ew[1] + h6[2] * ew[2], h6[1] * ew[0] + h6[3] * ew[1] + h6[4] * ew[2],
+                       h6[2] * ew[0] + h6[4] * ew[1] + h6[5] * ew[2]};
+  const float exg[3] = {ew[1] * g[2] - ew[2] * g[1], ew[2] * g[0] - ew[0] * g[2], ew[0] * g[1] - ew[1] * g[0]};
+  fza[0] = He[0]; fza[1] = He[1]; fza[2] = He[2];
+  fza[3] = ra[1] * He[2] - ra[2] * He[1] + exg[0];    // (r_A x He) + e_t x g
+  fza[4] = ra[2] * He[0] - ra[0] * He[2] + exg[1];
+  fza[5] = ra[0] * He[1] - ra[1] * He[0] + exg[2];
+  fza[6] = He[1] * rb[2] - He[2] * rb[1] - exg[0];    // (He x r_B) + g x e_t
+  fza[7] = He[2] * rb[0] - He[0] * rb[2] - exg[1];
+  fza[8] = He[0] * rb[1] - He[1] * rb[0] - exg[2];
+  faa = ew[0] * He[0] + ew[1] * He[1] + ew[2] * He[2];
+}
+// total second derivative along alpha(z): D2 = fzz + fza da^T + da fza^T + faa da da^T + fa d2a
+__device__ __forceinline__ void d2_total(float* fzz, const float* fza, float faa, float fa, const float* da,
+                                         const float* d2a) {
+#pragma unroll
+  for (int i = 0; i < 9; ++i)
+#pragma unroll
+    for (int j = i; j < 9; ++j) {
+      const int k = p9(i, j);
+      fzz[k] = fmaf(fa, d2a[k], fmaf(faa * da[i], da[j], fmaf(fza[i], da[j], fmaf(da[i], fza[j], fzz[k]))));
+    }
+}
+// 9x9 (z) -> packed 12x12 in the pair's column order: local coordinates
+// (t_s, th_s, t_f, th_f) of the side map to z with t_f = -t_s; the
+// transposed side (side 1) lists the pair's B block first
+template <int SIDE>
+__device__ __forceinline__ void store_d2_t(float* out, int64_t C, int64_t c, const float* h45) {
+  int k = 0;
+#pragma unroll
+  for (int i = 0; i < 12; ++i)
+#pragma unroll
+    for (int j = i; j < 12; ++j, ++k) {
+      const int li = SIDE ? (i + 6) % 12 : i, lj = SIDE ? (j + 6) % 12 : j;
+      const int ui = li < 6 ? li : (li < 9 ? li - 6 : li - 3), uj = lj < 6 ? lj : (lj < 9 ? lj - 6 : lj - 3);
+      const float si = (li >= 6 && li < 9) ? -1.f : 1.f, sj = (lj >= 6 && lj < 9) ? -1.f : 1.f;
+      const int a = ui < uj ? ui : uj, b = ui < uj ? uj : ui;
+      out[(int64_t)k * C + c] = si * sj * h45[p9(a, b)];
+    }
+}
+__device__ __forceinline__ void store_d2(float* out, int64_t C, int64_t c, const float* h45, int side) {
+  if (side) store_d2_t<1>(out, C, c, h45);
+  else store_d2_t<0>(out, C, c, h45);
+}
 
 // Full mode (V + E contacts): candidate i is its own contact.
 //   point p, normal n = grad phi (raw), depth d, W = gamma, q = gamma p (so the
@@ -95,7 +200,7 @@ template <int TIER>
 __device__ __forceinline__ void store_candidate(const cm_manifold_out& out, int64_t C, int64_t c, const float* p,
                                                 const float* n, float d, const float* h, const float* ew,
                                                 const float* dab, const PairFrame& F, int kind, float itcmp, int cTA,
-                                                int cRA, int cTB, int cRB) {
+                                                int cRA, int cTB, int cRB, const float* d2 = nullptr, int side = 0) {
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     out.point[a * C + c] = p[a];
@@ -152,6 +257,7 @@ __device__ __forceinline__ void store_candidate(const cm_manifold_out& out, int6
       }
     }
   }
+  if constexpr (TIER >= 3) store_d2(out.d2depth, C, c, d2, side);
 }
 
 // ============================================================================
@@ -215,9 +321,10 @@ struct UnitCtx {
 #define CM_MF_MINB_M_XP1 1
 #endif
 template <int TIER, int XP> struct MinB {
-  static constexpr int VERTICES = XP == 1 ? CM_MF_MINB_V_XP1 : (XP == 0 ? CM_MF_MINB_V_XP0 : CM_MF_MINB_V);
-  static constexpr int TRACES = XP == 0 ? CM_MF_MINB_T_XP0 : CM_MF_MINB_T;
-  static constexpr int MIDPOINTS = XP == 1 ? CM_MF_MINB_M_XP1 : (XP == 0 ? CM_MF_MINB_M_XP0 : CM_MF_MINB_M);
+  // tier 3 (second derivatives) carries 45-component arrays: full register file
+  static constexpr int VERTICES = TIER >= 3 ? 1 : (XP == 1 ? CM_MF_MINB_V_XP1 : (XP == 0 ? CM_MF_MINB_V_XP0 : CM_MF_MINB_V));
+  static constexpr int TRACES = TIER >= 3 ? 1 : (XP == 0 ? CM_MF_MINB_T_XP0 : CM_MF_MINB_T);
+  static constexpr int MIDPOINTS = TIER >= 3 ? 1 : (XP == 1 ? CM_MF_MINB_M_XP1 : (XP == 0 ? CM_MF_MINB_M_XP0 : CM_MF_MINB_M));
 };
 #ifndef CM_MF_FACE_MINB
 #define CM_MF_FACE_MINB 2   // face kernel: <= 128 registers
@@ -323,9 +430,16 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::VERTICES) k
       st4(rec + 4, h[0], h[1], h[2], h[3]);
       st4(rec + 8, h[4], h[5], 0.f, 0.f);
     }
+    float d2[TIER >= 3 ? N45 : 1];
+    if constexpr (TIER >= 3) {
+      d2_point(n, h, pw, F.tA, F.tB, d2);
+#pragma unroll
+      for (int k = 0; k < N45; ++k) rec[VD2 + k] = d2[k];
+    }
     if (full) {
       CM_COLS(U.side);
-      store_candidate<TIER>(a.out, a.C, U.off + v, pw, n, r.v, h, nullptr, nullptr, F, 0, itcmp, cTA, cRA, cTB, cRB);
+      store_candidate<TIER>(a.out, a.C, U.off + v, pw, n, r.v, h, nullptr, nullptr, F, 0, itcmp, cTA, cRA, cTB, cRB,
+                            d2, U.side);
     }
   }
 }
@@ -335,7 +449,7 @@ template <int TIER, int XP>
 __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::TRACES) k_mf_traces(const MfArgs a) {
   __shared__ UnitCtx U;
   if (!unit_setup(a, U)) return;
-  constexpr int OT = TIER >= 2 ? 1 : 0;   // order inside the trace
+  constexpr int OT = TIER >= 3 ? 2 : (TIER >= 2 ? 1 : 0);   // order inside the trace
   const SmoothDev sp = a.S.sp;
   const float itcmp = sp.i_cmp;
   const float tca = sp.tau_clip_alpha, itca = sp.i_clip_alpha;
@@ -372,20 +486,60 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::TRACES) k_m
     float da[NDQ];
 #pragma unroll
     for (int k = 0; k < NDQ; ++k) da[k] = 0.f;
+    constexpr int N2 = TIER >= 3 ? N45 : 1;
+    float d2a[N2];
+#pragma unroll
+    for (int k = 0; k < N2; ++k) d2a[k] = 0.f;
     for (int it = 0; it < sp.iters; ++it) {
       float phi, g[3];
+      float h[6], fzz[N2];   // tier 3: world Hessian and d^2 phi / dz^2 at the iterate
       if (it == 0) {   // the corner itself: reuse the vertex evaluation (reading #22)
         phi = corner.x;
         g[0] = corner.y; g[1] = corner.z; g[2] = corner.w;
+        if constexpr (TIER >= 3) {
+          const float* cr = sv + v0 * vrec(TIER);
+#pragma unroll
+          for (int k = 0; k < 6; ++k) h[k] = cr[VH + k];
+#pragma unroll
+          for (int k = 0; k < N45; ++k) fzz[k] = cr[VD2 + k];
+        }
       } else {
         const float xb[3] = {fmaf(al, eb[0], xI[0]), fmaf(al, eb[1], xI[1]), fmaf(al, eb[2], xI[2])};
         Res<OT> r;
         eval_shape<OT, ClsTraits<XP>::XPM, ClsTraits<XP>::FLAT>(a.S, U.SB, xb, r);
         phi = r.v;
         if constexpr (TIER >= 2) rot_vec(F.RB, r.g, g);
+        if constexpr (TIER >= 3) {
+          rot_sym(F.RB, r.h, h);
+          const float p[3] = {fmaf(al, ew[0], pI[0]), fmaf(al, ew[1], pI[1]), fmaf(al, ew[2], pI[2])};
+          d2_point(g, h, p, F.tA, F.tB, fzz);
+        }
       }
       // gated step G(phi) = sigma(phi / tau) phi  (reading #20)
       const float s = sigm(phi * itcmp);
+      if constexpr (TIER >= 3) {
+        // d2 alpha_{k+1} = d2 alpha_k + sgn [G'' Dphi Dphi^T + G' D2phi] with
+        // Dphi = phi_z + phi_a d alpha_k and D2phi the total second derivative
+        const float p[3] = {fmaf(al, ew[0], pI[0]), fmaf(al, ew[1], pI[1]), fmaf(al, ew[2], pI[2])};
+        float gj[NDQ], fza[NDQ], faa;
+        gJ(g, p, F, gj);
+        d2_alpha(g, h, p, ew, F.tA, F.tB, fza, faa);
+        const float fa = g[0] * ew[0] + g[1] * ew[1] + g[2] * ew[2];
+        float Dp[NDQ];
+#pragma unroll
+        for (int k = 0; k < NDQ; ++k) Dp[k] = fmaf(fa, da[k], gj[k]);
+        d2_total(fzz, fza, faa, fa, da, d2a);      // fzz <- D2phi
+        const float sq = s * (1.f - s) * itcmp;
+        const float G1 = fmaf(phi, sq, s);
+        const float G2 = sq * fmaf(phi * (1.f - 2.f * s), itcmp, 2.f);
+#pragma unroll
+        for (int i = 0; i < NDQ; ++i)
+#pragma unroll
+          for (int k2 = i; k2 < NDQ; ++k2) {
+            const int q = p9(i, k2);
+            d2a[q] = fmaf(sgn, fmaf(G2 * Dp[i], Dp[k2], G1 * fzz[q]), d2a[q]);
+          }
+      }
       if constexpr (TIER >= 2) {
         // d alpha_{k+1} = d alpha_k + sgn G'(phi) [g^T J(p) dq + (g.e_t) d alpha_k]
         const float Gp = fmaf(phi * s * (1.f - s), itcmp, s);
@@ -402,7 +556,18 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::TRACES) k_m
     // soft clip to the edge (reading #21)
     float* rec = se + e * erec(TIER) + (dir ? trace_b(TIER) : 0);
     const float at = softclip(al, 0.f, L, tca, itca);
-    if constexpr (TIER >= 2) {
+    if constexpr (TIER >= 3) {
+      // d2 a~ = sc'' da da^T + sc' d2a
+      const float s1 = sigm(al * itca), s2 = sigm((al - L) * itca);
+      const float c1 = s1 - s2, c2 = (s1 * (1.f - s1) - s2 * (1.f - s2)) * itca;
+      rec[0] = at;
+#pragma unroll
+      for (int k = 0; k < NDQ; ++k) rec[1 + k] = c1 * da[k];
+#pragma unroll
+      for (int i = 0; i < NDQ; ++i)
+#pragma unroll
+        for (int k2 = i; k2 < NDQ; ++k2) rec[TD2 + p9(i, k2)] = fmaf(c2 * da[i], da[k2], c1 * d2a[p9(i, k2)]);
+    } else if constexpr (TIER >= 2) {
       const float cd = softclip_d(al, 0.f, L, itca);
       float o[10] = {at};
 #pragma unroll
@@ -442,7 +607,15 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::MIDPOINTS) 
     rot_vec(F.RA, el, ew);
     float* rec = se + e * erec(TIER);
     float ab, dab[NDQ];
-    if constexpr (TIER >= 2) {
+    float d2ab[TIER >= 3 ? N45 : 1];
+    if constexpr (TIER >= 3) {
+      const float* rb2 = rec + trace_b(TIER);
+      ab = 0.5f * (rec[0] + rb2[0]);
+#pragma unroll
+      for (int k = 0; k < NDQ; ++k) dab[k] = 0.5f * (rec[1 + k] + rb2[1 + k]);
+#pragma unroll
+      for (int k = 0; k < N45; ++k) d2ab[k] = 0.5f * (rec[TD2 + k] + rb2[TD2 + k]);
+    } else if constexpr (TIER >= 2) {
       float t[20];
 #pragma unroll
       for (int q = 0; q < 5; ++q) {
@@ -479,9 +652,21 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::MIDPOINTS) 
       st4(rec, ab, r.v, n[0], n[1]);
       rec[4] = n[2];
     }
+    float d2[TIER >= 3 ? N45 : 1];
+    if constexpr (TIER >= 3) {
+      // d^2 d_e = phi_zz + phi_za dab^T + dab phi_za^T + phi_aa dab dab^T + phi_a d2ab
+      float fza[NDQ], faa;
+      d2_point(n, h, pw, F.tA, F.tB, d2);
+      d2_alpha(n, h, pw, ew, F.tA, F.tB, fza, faa);
+      const float fa = n[0] * ew[0] + n[1] * ew[1] + n[2] * ew[2];
+      d2_total(d2, fza, faa, fa, dab, d2ab);
+#pragma unroll
+      for (int k = 0; k < N45; ++k) rec[MD2 + k] = d2[k];
+    }
     if (full) {
       CM_COLS(U.side);
-      store_candidate<TIER>(a.out, a.C, U.off + V + e, pw, n, r.v, h, ew, dab, F, 1, itcmp, cTA, cRA, cTB, cRB);
+      store_candidate<TIER>(a.out, a.C, U.off + V + e, pw, n, r.v, h, ew, dab, F, 1, itcmp, cTA, cRA, cTB, cRB,
+                            d2, U.side);
     }
   }
 }
@@ -521,7 +706,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 }
 
 template <int TIER, bool STAGED>
-__global__ void __launch_bounds__(CM_MF_MAX_THREADS, CM_MF_FACE_MINB) k_mf_faces(const MfArgs a) {
+__global__ void __launch_bounds__(CM_MF_MAX_THREADS, TIER >= 3 ? 1 : CM_MF_FACE_MINB) k_mf_faces(const MfArgs a) {
   extern __shared__ __align__(16) float fsm[];
   __shared__ UnitCtx U;
   __shared__ uint64_t bar;
@@ -776,6 +961,44 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, CM_MF_FACE_MINB) k_mf_faces
           dn[q][6 + b] = -Lm[q * 3 + b] - KtB[b] + Mm[q * 3 + b] - HtB[b] - nk[b] + nb * dd[6 + b] + dnE[q][6 + b];
         }
       }
+      if constexpr (TIER >= 3) {
+        // d^2 depth = sum z_i d^2 d_i - (1/tau_min)(sum z_i dd_i dd_i^T - dd dd^T)
+        float A[N45];
+#pragma unroll
+        for (int k = 0; k < N45; ++k) A[k] = 0.f;
+#pragma unroll 1
+        for (int i = 0; i < 6; ++i) {
+          const bool isv = i < 3;
+          const int id = isv ? cv[i] : ce[i - 3];
+          const float* rr = isv ? sv + id * VR : se + id * ER;
+          const float nn[3] = {rr[(isv ? VN : MN) + 0], rr[(isv ? VN : MN) + 1], rr[(isv ? VN : MN) + 2]};
+          float pi3[3], ewi[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            pi3[q] = i == 0 ? pc[0][q] : i == 1 ? pc[1][q] : i == 2 ? pc[2][q] : i == 3 ? pc[3][q] : i == 4 ? pc[4][q] : pc[5][q];
+            if (!isv) ewi[q] = i == 3 ? ewc[0][q] : i == 4 ? ewc[1][q] : ewc[2][q];
+          }
+          float ddi[NDQ];
+          gJ(nn, pi3, F, ddi);
+          if (!isv) {
+            const float ge = nn[0] * ewi[0] + nn[1] * ewi[1] + nn[2] * ewi[2];
+#pragma unroll
+            for (int k = 0; k < NDQ; ++k) ddi[k] = fmaf(ge, rr[MDAB + k], ddi[k]);
+          }
+          const float* d2i = rr + (isv ? VD2 : MD2);
+          const float zi = i == 0 ? z[0] : i == 1 ? z[1] : i == 2 ? z[2] : i == 3 ? z[3] : i == 4 ? z[4] : z[5];
+          const float zt = zi * itmin;
+#pragma unroll
+          for (int q = 0; q < NDQ; ++q)
+#pragma unroll
+            for (int k = q; k < NDQ; ++k) A[p9(q, k)] = fmaf(zi, d2i[p9(q, k)], fmaf(-zt * ddi[q], ddi[k], A[p9(q, k)]));
+        }
+#pragma unroll
+        for (int q = 0; q < NDQ; ++q)
+#pragma unroll
+          for (int k = q; k < NDQ; ++k) A[p9(q, k)] = fmaf(itmin * dd[q], dd[k], A[p9(q, k)]);
+        store_d2(out.d2depth, C, c, A, U.side);
+      }
       // store: q order (tA 0-2, thetaA 3-5, tB 6-8 = -tA, thetaB 9-11)
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
@@ -902,7 +1125,8 @@ int launch_manifold(const SceneDev& s, int class_mask, int max_V, int max_E, con
   a.slot = slot;
   a.mode = mode;
   cudaStream_t const* sts = (cudaStream_t const*)streams;
-  if (tier >= 2) return launch_tier<2>(a, class_mask, max_V, max_E, n_units, chunk, sts, n_streams);
+  if (tier >= 3) return launch_tier<3>(a, class_mask, max_V, max_E, n_units, chunk, sts, n_streams);
+  if (tier == 2) return launch_tier<2>(a, class_mask, max_V, max_E, n_units, chunk, sts, n_streams);
   if (tier == 1) return launch_tier<1>(a, class_mask, max_V, max_E, n_units, chunk, sts, n_streams);
   return launch_tier<0>(a, class_mask, max_V, max_E, n_units, chunk, sts, n_streams);
 }

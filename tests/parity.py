@@ -97,6 +97,12 @@ def manifold_parity(scene, osc, gpu, tier, pair_idx, rng, ell, mode=0):
         nf += compare("ddepth", g("ddepth").T, ref["ddepth"], refp["ddepth"], tol_vec(ref["ddepth"], 1), rep)
         dn = g("dnormal").reshape(3, 12, -1).transpose(2, 0, 1)
         nf += compare("dnormal", dn, ref["dnormal"], refp["dnormal"], tol_hess(ref["dnormal"], (1, 2), ell), rep)
+    if tier >= 3:
+        # second derivatives (f3): Hessian tolerance against the oracle's
+        # second-order q-jets, condition-aware like every other field
+        r2 = osc.manifold_d2depth(pairs=pairs, poses=scene.poses, mode=mode)
+        r2p = osc.manifold_d2depth(pairs=pairs, poses=perturb_inputs(rng, scene.poses), mode=mode)
+        nf += compare("d2depth", g("d2depth").T, r2, r2p, tol_hess(r2, 1, ell), rep)
     # dominant candidate, outside near ties of the two deepest candidates
     # (full mode: the candidate kind, compared exactly)
     ds = np.sort(ref["dcand"], axis=1)

@@ -36,7 +36,7 @@ def test_exports_every_declared_symbol(L):
 
 
 def test_version_and_launch_counter(L):
-    assert L.cm_version() == 1
+    assert L.cm_version() == 2   # 2: cm_manifold_out.d2depth (tier 3)
     assert L.cm_launch_count() == 0
 
 
@@ -45,6 +45,7 @@ def test_struct_layout(L):
     # 4 + 4 + 32*4 + 4 + 7*4 + 4*4 + 6*4 + 64*4 + 9*4 + 3*4
     assert C.sizeof(binding.cm_node) == 4 + 4 + 128 + 4 + 28 + 16 + 24 + 256 + 36 + 12
     assert C.sizeof(binding.cm_smooth_params) == 24
+    assert C.sizeof(binding.cm_manifold_out) == 9 * 8
 
 
 def _desc(nodes):

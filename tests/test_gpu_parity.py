@@ -322,3 +322,31 @@ def test_manifold_large_patch_unstaged(cuda, oracle_mod):
     _report("manifold_patch40", rep)
     assert nf == 0, json.dumps(rep, indent=1)
     assert PT.excluded_fraction(rep) < 0.01
+
+
+@pytest.mark.parametrize("mode", [0, 4, 8])
+def test_manifold_tier3_c1(cuda, oracle_mod, mode):
+    """Tier 3 (second derivatives d^2 depth / dq^2) on C1:
+    reduced, full and two-sided modes against the oracle's second-order jets."""
+    sc = synth.c1_scene()
+    osc = oracle_mod.OracleScene(sc)
+    gpu, _ = PT.gpu_manifold(sc, 3, mode=mode)
+    nf, rep = PT.manifold_parity(sc, osc, gpu, 3, np.arange(len(sc.pairs)), np.random.default_rng(41), sc.ell,
+                                 mode=mode)
+    _report("manifold_c1_t3_mode%d" % mode, rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+    assert PT.excluded_fraction(rep) < 0.01
+
+
+@pytest.mark.parametrize("cfg", ["C4", "C5"])
+def test_manifold_tier3_sampled(cuda, oracle_mod, cfg):
+    """Tier 3 on C4 (cup with its XPSQ handle) and C5 (every SDF class):
+    GPU on a batch, oracle second-order jets on a seeded sample of pairs."""
+    sc = synth.c4_scene(64) if cfg == "C4" else synth.c5_scene(512)
+    osc = oracle_mod.OracleScene(sc)
+    gpu, _ = PT.gpu_manifold(sc, 3)
+    idx = np.sort(np.random.default_rng(42).choice(len(sc.pairs), 12, replace=False))
+    nf, rep = PT.manifold_parity(sc, osc, gpu, 3, idx, np.random.default_rng(43), sc.ell)
+    _report("manifold_%s_t3" % cfg, rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+    assert PT.excluded_fraction(rep) < 0.01
