@@ -326,6 +326,18 @@ template <int TIER, int XP> struct MinB {
   static constexpr int TRACES = TIER >= 3 ? 1 : (XP == 0 ? CM_MF_MINB_T_XP0 : CM_MF_MINB_T);
   static constexpr int MIDPOINTS = TIER >= 3 ? 1 : (XP == 1 ? CM_MF_MINB_M_XP1 : (XP == 0 ? CM_MF_MINB_M_XP0 : CM_MF_MINB_M));
 };
+// per-thread register caps (__maxnreg__) equivalent to MINB resident
+// 256-thread blocks: 3 -> 80, 2 -> 128, 1 -> 255; CM_MF_REG_XP1 overrides the
+// order-2 XPSQ kernels (vertices, midpoints)
+__host__ __device__ constexpr int regs_of(int minb) { return minb >= 3 ? 80 : (minb == 2 ? 128 : 255); }
+#ifndef CM_MF_REG_XP1
+#define CM_MF_REG_XP1 168   // measured: C5 +1%, C4 +5% over 255 (144 and 128 lose)
+#endif
+template <int TIER, int XP> struct RegCap {
+  static constexpr int VERTICES = (TIER == 2 && XP == 1 && CM_MF_REG_XP1) ? CM_MF_REG_XP1 : regs_of(MinB<TIER, XP>::VERTICES);
+  static constexpr int TRACES = regs_of(MinB<TIER, XP>::TRACES);
+  static constexpr int MIDPOINTS = (TIER == 2 && XP == 1 && CM_MF_REG_XP1) ? CM_MF_REG_XP1 : regs_of(MinB<TIER, XP>::MIDPOINTS);
+};
 #ifndef CM_MF_FACE_MINB
 #define CM_MF_FACE_MINB 2   // face kernel: <= 128 registers
 #endif
@@ -405,7 +417,7 @@ __device__ __forceinline__ void vertex_frames(const PairFrame& F, const float* l
 
 // ---- phase 1: vertices: phi, n (and H) of B ----------------
 template <int TIER, int XP>
-__global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::VERTICES) k_mf_vertices(const MfArgs a) {
+__global__ void __maxnreg__((RegCap<TIER, XP>::VERTICES)) k_mf_vertices(const MfArgs a) {
   __shared__ UnitCtx U;
   if (!unit_setup(a, U)) return;
   constexpr int OV = TIER >= 2 ? 2 : 1;
@@ -446,7 +458,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::VERTICES) k
 
 // ---- phase 2: sphere traces (Fig. 2), 2 per edge ----------------
 template <int TIER, int XP>
-__global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::TRACES) k_mf_traces(const MfArgs a) {
+__global__ void __maxnreg__((RegCap<TIER, XP>::TRACES)) k_mf_traces(const MfArgs a) {
   __shared__ UnitCtx U;
   if (!unit_setup(a, U)) return;
   constexpr int OT = TIER >= 3 ? 2 : (TIER >= 2 ? 1 : 0);   // order inside the trace
@@ -589,7 +601,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::TRACES) k_m
 
 // ---- phase 3: edge points p_e = v_I + a_bar e_t, a_bar = (a_I + a_II)/2
 template <int TIER, int XP>
-__global__ void __launch_bounds__(CM_MF_MAX_THREADS, MinB<TIER, XP>::MIDPOINTS) k_mf_midpoints(const MfArgs a) {
+__global__ void __maxnreg__((RegCap<TIER, XP>::MIDPOINTS)) k_mf_midpoints(const MfArgs a) {
   __shared__ UnitCtx U;
   if (!unit_setup(a, U)) return;
   constexpr int OV = TIER >= 2 ? 2 : 1;
