@@ -333,9 +333,12 @@ __host__ __device__ constexpr int regs_of(int minb) { return minb >= 3 ? 80 : (m
 #ifndef CM_MF_REG_XP1
 #define CM_MF_REG_XP1 168   // measured: C5 +1%, C4 +5% over 255 (144 and 128 lose)
 #endif
+#ifndef CM_MF_REG_T_XP1
+#define CM_MF_REG_T_XP1 0
+#endif
 template <int TIER, int XP> struct RegCap {
   static constexpr int VERTICES = (TIER == 2 && XP == 1 && CM_MF_REG_XP1) ? CM_MF_REG_XP1 : regs_of(MinB<TIER, XP>::VERTICES);
-  static constexpr int TRACES = regs_of(MinB<TIER, XP>::TRACES);
+  static constexpr int TRACES = (TIER == 2 && XP == 1 && CM_MF_REG_T_XP1) ? CM_MF_REG_T_XP1 : regs_of(MinB<TIER, XP>::TRACES);
   static constexpr int MIDPOINTS = (TIER == 2 && XP == 1 && CM_MF_REG_XP1) ? CM_MF_REG_XP1 : regs_of(MinB<TIER, XP>::MIDPOINTS);
 };
 #ifndef CM_MF_FACE_MINB
