@@ -76,6 +76,24 @@ __device__ __forceinline__ float softclip(float x, float lo, float hi, float tau
 __device__ __forceinline__ float softclip_d(float x, float lo, float hi, float itau) {
   return sigm((x - lo) * itau) - sigm((x - hi) * itau);
 }
+// s+(x; tau) and sigma(x / tau) from one exponential e = exp(-|x|/tau):
+// s+ = max(x, 0) + tau log(1 + e), sigma = 1/(1+e) (x >= 0) or e/(1+e)
+__device__ __forceinline__ void softplus_sig(float x, float tau, float itau, float& sp, float& sg) {
+  const float e = ex2(-fabsf(x) * (itau * LOG2E));
+  sp = fmaxf(x, 0.f) + (tau * LN2) * lg2(1.f + e);
+  const float r = rcpa(1.f + e);
+  sg = x >= 0.f ? r : e * r;
+}
+// softclip value with its first and second derivatives (two exponentials)
+__device__ __forceinline__ void softclip_12(float x, float lo, float hi, float tau, float itau, float& v, float& d1,
+                                            float& d2) {
+  float sp1, s1, sp2, s2;
+  softplus_sig(x - lo, tau, itau, sp1, s1);
+  softplus_sig(x - hi, tau, itau, sp2, s2);
+  v = lo + sp1 - sp2;
+  d1 = s1 - s2;
+  d2 = (s1 * (1.f - s1) - s2 * (1.f - s2)) * itau;
+}
 
 // cube root from the MUFU log / exp plus one Newton step (rel. error ~1e-7)
 __device__ __forceinline__ float cbrt_fast(float x) {
@@ -699,10 +717,15 @@ __device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3
   const float Delta = -(4.f * P3 + 27.f * Q * Q);
   const float Dl[2] = {-12.f * P2, -54.f * Q};          // dDelta/d(P, Q)
   const float Dll[3] = {-24.f * P, 0.f, -54.f};         // PP, PQ, QQ
-  const float wn = sigm(-Delta * itd), wp = sigm(Delta * itd);
-  const float sp1 = sigm(Delta * itd);                  // s+'(Delta)
+  // one exponential e = exp(-|Delta|/tau) gives both gates sigma(+-Delta/tau),
+  // s+'(Delta) = sigma(Delta/tau) and s+(+-Delta) = max(+-Delta, 0) + tau log(1+e)
+  const float eD = ex2(-fabsf(Delta) * (itd * LOG2E));
+  const float rD = rcpa(1.f + eD);
+  const float wp = Delta >= 0.f ? rD : eD * rD, wn = Delta >= 0.f ? eD * rD : rD;
+  const float lgD = (td * LN2) * lg2(1.f + eD);
+  const float sp1 = wp;                                 // s+'(Delta)
   const float sp2 = sp1 * (1.f - sp1) * itd;            // s+''(Delta)
-  const float spD = softplus(Delta, td, itd);           // s+(Delta)
+  const float spD = fmaxf(Delta, 0.f) + lgD;           // s+(Delta)
   // blend weights and their derivatives
   const float dwn = -wn * (1.f - wn) * itd, dwp = wp * (1.f - wp) * itd;
   const float ddwn = wn * (1.f - wn) * (1.f - 2.f * wn) * itd * itd;
@@ -722,9 +745,8 @@ __device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3
   // soft clip of s - b/3 into (0, 1) with derivatives
   auto clip = [&](float s, const float* sa, const float* sab, float& v, float* va, float* vab) {
     const float x = s - b3;
-    v = softclip(x, 0.f, 1.f, tc, itc);
-    const float s1 = sigm(x * itc), s2 = sigm((x - 1.f) * itc);
-    const float c1 = s1 - s2, c2 = (s1 * (1.f - s1) - s2 * (1.f - s2)) * itc;
+    float c1, c2;
+    softclip_12(x, 0.f, 1.f, tc, itc, v, c1, c2);
     va[0] = c1 * sa[0];
     va[1] = c1 * sa[1];
     if constexpr (O >= 2) {
@@ -741,7 +763,7 @@ __device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3
     const float W = fmaf(0.25f, spD, P3);
     const float Pm = cbrt_fast(W);
     // Cardano's cancellation-free form: u = cbrt(-Q/2 - sign(Q) sqrt(D)), v = -Pm/(3u)
-    const float D = softplus(-Delta, td, itd) * (1.f / 108.f);
+    const float D = (fmaxf(-Delta, 0.f) + lgD) * (1.f / 108.f);   // s+(-Delta) / 108
     const float sD = sqrtf(D);
     const float u = cbrt_fast(Q >= 0.f ? -0.5f * Q - sD : -0.5f * Q + sD);
     const float s = fabsf(u) > 1e-30f ? u - Pm * rcpa(3.f * u) : u;
@@ -844,9 +866,8 @@ __device__ __forceinline__ bool xpsq_root_t(const Xpsq& X, const SmoothDev& sp, 
   }
   if (X.cls == 1) {
     const float s = X.Bn[0] * w[0] + X.Bn[1] * w[1] + X.Bn[2] * w[2];
-    const float v = softclip(s, 0.f, 1.f, tc, itc);
-    const float s1 = sigm(s * itc), s2 = sigm((s - 1.f) * itc);
-    const float d1 = s1 - s2, d2 = (s1 * (1.f - s1) - s2 * (1.f - s2)) * itc;
+    float v, d1, d2;
+    softclip_12(s, 0.f, 1.f, tc, itc, v, d1, d2);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       tv[k] = v;

@@ -570,11 +570,10 @@ __global__ void __maxnreg__((RegCap<TIER, XP>::TRACES)) k_mf_traces(const MfArgs
     }
     // soft clip to the edge (reading #21)
     float* rec = se + e * erec(TIER) + (dir ? trace_b(TIER) : 0);
-    const float at = softclip(al, 0.f, L, tca, itca);
+    float at, c1, c2;   // soft clip and its first two derivatives (shared exponentials)
+    softclip_12(al, 0.f, L, tca, itca, at, c1, c2);
     if constexpr (TIER >= 3) {
       // d2 a~ = sc'' da da^T + sc' d2a
-      const float s1 = sigm(al * itca), s2 = sigm((al - L) * itca);
-      const float c1 = s1 - s2, c2 = (s1 * (1.f - s1) - s2 * (1.f - s2)) * itca;
       rec[0] = at;
 #pragma unroll
       for (int k = 0; k < NDQ; ++k) rec[1 + k] = c1 * da[k];
@@ -583,7 +582,7 @@ __global__ void __maxnreg__((RegCap<TIER, XP>::TRACES)) k_mf_traces(const MfArgs
 #pragma unroll
         for (int k2 = i; k2 < NDQ; ++k2) rec[TD2 + p9(i, k2)] = fmaf(c2 * da[i], da[k2], c1 * d2a[p9(i, k2)]);
     } else if constexpr (TIER >= 2) {
-      const float cd = softclip_d(al, 0.f, L, itca);
+      const float cd = c1;
       float o[10] = {at};
 #pragma unroll
       for (int k = 0; k < NDQ; ++k) o[1 + k] = cd * da[k];
