@@ -48,6 +48,15 @@ enum { VD = 0, VN = 1, VH = 4 };
 enum { MAB = 0, MD = 1, MN = 2, MH = 5, MDAB = 11 };       // midpoint layout
 
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+// 45 floats from a 16-B aligned address (11 x 128-bit + 1)
+__device__ __forceinline__ void ld45(const float* p, float* o) {
+#pragma unroll
+  for (int q = 0; q < 11; ++q) {
+    const float4 v = ld4(p + 4 * q);
+    o[4 * q] = v.x; o[4 * q + 1] = v.y; o[4 * q + 2] = v.z; o[4 * q + 3] = v.w;
+  }
+  o[44] = p[44];
+}
 __device__ __forceinline__ void st4(float* p, float a, float b, float c, float d) {
   *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
 }
@@ -515,8 +524,7 @@ __global__ void __maxnreg__((RegCap<TIER, XP>::TRACES)) k_mf_traces(const MfArgs
           const float* cr = sv + v0 * vrec(TIER);
 #pragma unroll
           for (int k = 0; k < 6; ++k) h[k] = cr[VH + k];
-#pragma unroll
-          for (int k = 0; k < N45; ++k) fzz[k] = cr[VD2 + k];
+          ld45(cr + VD2, fzz);
         }
       } else {
         const float xb[3] = {fmaf(al, eb[0], xI[0]), fmaf(al, eb[1], xI[1]), fmaf(al, eb[2], xI[2])};
@@ -999,7 +1007,8 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, TIER >= 3 ? 1 : CM_MF_FACE_
 #pragma unroll
             for (int k = 0; k < NDQ; ++k) ddi[k] = fmaf(ge, rr[MDAB + k], ddi[k]);
           }
-          const float* d2i = rr + (isv ? VD2 : MD2);
+          float d2i[N45];
+          ld45(rr + (isv ? VD2 : MD2), d2i);
           const float zi = i == 0 ? z[0] : i == 1 ? z[1] : i == 2 ? z[2] : i == 3 ? z[3] : i == 4 ? z[4] : z[5];
           const float zt = zi * itmin;
 #pragma unroll
