@@ -441,6 +441,22 @@ template <class T> T xpsq_phi(const Node& n, const T* y, const Smooth& sp) {
 }
 
 // ---------------------------------------------------------------------------
+// Shape-parameter seeding: the parameter (node, slot) named
+// by the calling thread's g_seed carries the derivative direction of a
+// Dual<double,1>; every other jet type ignores it.  Slots per node:
+// half-space (n_x, n_y, n_z, h); SQ (a_x, a_y, a_z, eps1, eps2); PSQ as SQ
+// then (n_x, n_y, n_z, h) per plane.
+// ---------------------------------------------------------------------------
+thread_local int g_seed_node = -1, g_seed_slot = -1;
+template <class T> struct Seeder { static void apply(T&) {} };
+template <> struct Seeder<Dual<double, 1>> { static void apply(Dual<double, 1>& x) { x.d[0] = 1.0; } };
+template <class T> T pval(double v, int node, int slot) {
+  T x(v);
+  if (node == g_seed_node && slot == g_seed_slot) Seeder<T>::apply(x);
+  return x;
+}
+
+// ---------------------------------------------------------------------------
 // Composite tree (Eqs. (2)-(4); n-ary single LSE, Reading #5;
 // subtraction LSE([phi1, -phi2]), Reading #4).  Each node has a pose relative
 // to its parent; y is in the parent frame.
@@ -452,15 +468,15 @@ template <class T> T node_phi(const Shape& sh, int idx, const T* yparent, const 
   for (int i = 0; i < 3; ++i) y[i] = n.R[0 * 3 + i] * dx[0] + n.R[1 * 3 + i] * dx[1] + n.R[2 * 3 + i] * dx[2];
   switch (n.type) {
     case K_HALFSPACE: {
-      T nv[3] = {T(n.pl[0][0][0]), T(n.pl[0][0][1]), T(n.pl[0][0][2])};
-      return halfspace_phi(y, nv, T(n.pl[0][0][3]));
+      T nv[3] = {pval<T>(n.pl[0][0][0], idx, 0), pval<T>(n.pl[0][0][1], idx, 1), pval<T>(n.pl[0][0][2], idx, 2)};
+      return halfspace_phi(y, nv, pval<T>(n.pl[0][0][3], idx, 3));
     }
     case K_SQ: case K_PSQ: {
-      T a[3] = {T(n.a[0][0]), T(n.a[0][1]), T(n.a[0][2])};
+      T a[3] = {pval<T>(n.a[0][0], idx, 0), pval<T>(n.a[0][1], idx, 1), pval<T>(n.a[0][2], idx, 2)};
       T pl[MAXP][4];
       int np = n.type == K_SQ ? 0 : n.n_planes;
-      for (int j = 0; j < np; ++j) for (int i = 0; i < 4; ++i) pl[j][i] = T(n.pl[0][j][i]);
-      return psq_phi(y, T(n.eps[0][0]), T(n.eps[0][1]), a, np, pl, sp.tau_min);
+      for (int j = 0; j < np; ++j) for (int i = 0; i < 4; ++i) pl[j][i] = pval<T>(n.pl[0][j][i], idx, 5 + 4 * j + i);
+      return psq_phi(y, pval<T>(n.eps[0][0], idx, 3), pval<T>(n.eps[0][1], idx, 4), a, np, pl, sp.tau_min);
     }
     case K_XPSQ:
       return xpsq_phi(n, y, sp);
@@ -916,6 +932,56 @@ int ora_contact_manifold(void* s, const int* pairs, long n_pairs, const double* 
     }
     row0 += m.F;
    }
+  }
+  return 0;
+}
+
+// ---- shape-parameter derivatives of sdf_eval ----------
+// Parameters of a shape: its nodes in index (pre-order) order, slots per node
+// as for pval above; XPSQ nodes are not parametrised here (the shape reports
+// -1).  J[n * pmax + k] = d phi(point n) / d param k of the point's shape,
+// zero beyond the shape's count; one Dual<double,1> evaluation per parameter.
+int ora_shape_param_count(void* s, int shape) {
+  Scene* sc = (Scene*)s;
+  const Shape& sh = sc->shapes[shape];
+  int c = 0;
+  for (const Node& n : sh.nodes) {
+    if (n.type == K_XPSQ) return -1;
+    if (n.type == K_HALFSPACE) c += 4;
+    else if (n.type == K_SQ) c += 5;
+    else if (n.type == K_PSQ) c += 5 + 4 * n.n_planes;
+  }
+  return c;
+}
+int ora_sdf_param_grad(void* s, const int* shape_ids, const double* poses, const double* points, long B, long P,
+                       int pmax, double* J) {
+  Scene* sc = (Scene*)s;
+  const Smooth& sp = sc->sp;
+  long total = B * P;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (long n = 0; n < total; ++n) {
+    const long b = n / P;
+    const Shape& sh = sc->shapes[shape_ids[b]];
+    const double* pz = poses + 8 * b;
+    double R[9], t[3] = {pz[0], pz[1], pz[2]};
+    double q[4] = {pz[3], pz[4], pz[5], pz[6]};
+    quat_to_R(q, R);
+    using D1 = Dual<double, 1>;
+    D1 X[3], Rj[9], tj[3];
+    for (int i = 0; i < 3; ++i) { X[i] = D1(points[3 * n + i]); tj[i] = D1(t[i]); }
+    for (int i = 0; i < 9; ++i) Rj[i] = D1(R[i]);
+    int k = 0;
+    for (int ni = 0; ni < (int)sh.nodes.size(); ++ni) {
+      const Node& nd = sh.nodes[ni];
+      int cnt = nd.type == K_HALFSPACE ? 4 : (nd.type == K_SQ ? 5 : (nd.type == K_PSQ ? 5 + 4 * nd.n_planes : 0));
+      for (int slot = 0; slot < cnt && k < pmax; ++slot, ++k) {
+        g_seed_node = ni;
+        g_seed_slot = slot;
+        J[n * pmax + k] = shape_phi_world(sh, Rj, tj, X, sp).d[0];
+      }
+    }
+    g_seed_node = g_seed_slot = -1;
+    for (; k < pmax; ++k) J[n * pmax + k] = 0.0;
   }
   return 0;
 }

@@ -54,6 +54,9 @@ def lib():
         L.ora_sdf_eval.argtypes = [p, p, p, p, l, l, i, p, p, p, p, p, p]
         L.ora_contact_manifold.argtypes = [p, p, l, p, l, i] + [p] * 12 + [i, i]
         L.ora_manifold_d2depth.argtypes = [p, p, l, p, l, i, p, i, i]
+        L.ora_shape_param_count.argtypes = [p, i]
+        L.ora_shape_param_count.restype = i
+        L.ora_sdf_param_grad.argtypes = [p, p, p, p, l, l, i, p]
         L.ora_max_threads.restype = i
         _lib = L
     return _lib
@@ -224,6 +227,22 @@ class OracleScene:
                                    int(mode), int(n_threads))
         out["offsets"] = np.concatenate([[0], np.cumsum(F)]).astype(np.int64)
         return out
+
+    def param_count(self, shape):
+        """Number of shape parameters (-1: an XPSQ node, not parametrised)."""
+        return lib().ora_shape_param_count(self.h, int(shape))
+
+    def sdf_param_grad(self, shape_ids, poses, points, P, pmax=None):
+        """J [B*P, pmax]: d phi / d (shape parameters), zero-padded."""
+        shape_ids = np.ascontiguousarray(shape_ids, dtype=np.int32)
+        poses = np.ascontiguousarray(poses, dtype=np.float64).reshape(-1, 8)
+        points = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+        if pmax is None:
+            pmax = max(self.param_count(s) for s in np.unique(shape_ids))
+        J = np.zeros((len(points), pmax))
+        lib().ora_sdf_param_grad(self.h, _ptr(shape_ids), _ptr(poses), _ptr(points), len(shape_ids), P, int(pmax),
+                                 _ptr(J))
+        return J
 
     def manifold_d2depth(self, pairs=None, poses=None, n_threads=0, mode=0):
         """d^2 depth / dq^2 per contact (packed upper triangle, 78 per row, q in
