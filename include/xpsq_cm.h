@@ -169,6 +169,26 @@ int cm_sdf_eval(const cm_scene* scene, const int32_t* shape_ids, const float* po
                 int64_t P, uint32_t flags, float* d, float* grad, float* hess, float* dpose, float* d2pose,
                 float* dxdpose, void* stream);
 
+/* ---- shape-parameter derivatives ------------------------
+ * Parameters of shape s, in the order of its SDF nodes (pre-order, as given
+ * to cm_scene_create), endpoint-0 values: half-space (n_x, n_y, n_z, h); SQ
+ * (a_x, a_y, a_z, eps1, eps2); PSQ as SQ then (n_x, n_y, n_z, h) per plane;
+ * boolean nodes have none (the raw plane normal is the parameter: no
+ * renormalisation).  counts[s] (host, [n_shapes]) = the count, 0 without an
+ * SDF, -1 when the shape holds an XPSQ or booleans nested deeper than one
+ * level (not parametrised); offsets (host, [n_shapes + 1]) = prefix sums of
+ * max(count, 0) (the layout of the vjp vector).  Either may be NULL. */
+int cm_param_layout(const cm_scene* scene, int32_t* counts, int64_t* offsets);
+/* For each point n (layout of cm_sdf_eval): J[k*N + n] = d phi(n) / d param k
+ * of point n's shape for k < pmax (zero beyond the shape's count), and
+ * vjp[offsets[s] + k] += sum over the points n of shape s of w[n] J[k, n]
+ * (device, accumulated: zero it first; FP32 atomics, warp-reduced when a
+ * warp's points share one shape, so the summation order is not fixed).
+ * J or vjp may be NULL (not both; vjp needs w).  CM_ERR_UNSUPPORTED when any
+ * SDF shape of the scene has count -1. */
+int cm_sdf_param_grad(const cm_scene* scene, const int32_t* shape_ids, const float* poses, const float* points,
+                      int64_t B, int64_t P, int32_t pmax, float* J, const float* w, float* vjp, void* stream);
+
 /* ---- contact manifold ------------------------------------------------------
  * pairs[5*i ..]: {env, slotA, slotB, shapeA (sampled surface), shapeB (SDF)}
  * (device int32); poses [n_env, n_slot, 8] (device).  One-sided reduced

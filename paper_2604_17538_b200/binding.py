@@ -23,6 +23,7 @@ SDF_VALUE, SDF_GRAD, SDF_HESS, SDF_POSE_GRAD, SDF_POSE_HESS = 1, 2, 4, 8, 16
 FULL_MODE, TWO_SIDED = 4, 8   # manifold mode bits (include/xpsq_cm.h)
 
 EXPORTS = ["cm_version", "cm_last_error", "cm_scene_create", "cm_scene_destroy", "cm_shape_counts",
+           "cm_param_layout", "cm_sdf_param_grad",
            "cm_shape_topology", "cm_sdf_eval", "cm_manifold_size", "cm_manifold_offsets_workspace",
            "cm_manifold_offsets", "cm_contact_manifold", "cm_expand_jacobian", "cm_launch_count"]
 
@@ -73,6 +74,8 @@ def lib():
         L.cm_shape_topology.argtypes = [p, i32, p, p]
         L.cm_sdf_eval.argtypes = [p, p, p, p, i64, i64, u32, p, p, p, p, p, p, p]
         L.cm_manifold_size.argtypes = [p, p, i64, u32, p]
+        L.cm_param_layout.argtypes = [p, p, p]
+        L.cm_sdf_param_grad.argtypes = [p, p, p, p, i64, i64, i32, p, p, p, p]
         L.cm_manifold_offsets_workspace.argtypes = [i64]
         L.cm_manifold_offsets_workspace.restype = i64
         L.cm_manifold_offsets.argtypes = [p, p, i64, u32, p, p, i64, p]
@@ -217,6 +220,31 @@ class Scene:
         _check(lib().cm_sdf_eval(self.h, _ptr(shape_ids), _ptr(poses), _ptr(points), B, P, flags, g("d"), g("grad"),
                                  g("hess"), g("dpose"), g("d2pose"), g("dxdpose"), _stream()), "cm_sdf_eval")
         return out
+
+    # ---- shape-parameter derivatives (f4) -----------------------------------
+    def param_layout(self):
+        """(counts [n_shapes] int32, offsets [n_shapes + 1] int64) of the
+        shape-parameter vectors (-1: not parametrised)."""
+        n = len(self.shapes)
+        counts = np.zeros(n, np.int32)
+        offs = np.zeros(n + 1, np.int64)
+        _check(lib().cm_param_layout(self.h, counts.ctypes.data_as(C.c_void_p), offs.ctypes.data_as(C.c_void_p)),
+               "cm_param_layout")
+        return counts, offs
+
+    def sdf_param_grad(self, shape_ids, poses, points, P: int, pmax: int = 0, w=None, want_J: bool = True):
+        """J [pmax, B*P] (d phi / d shape parameter) and, given w [B*P], the
+        vector-Jacobian product vjp [n_params_total] (CUDA tensors)."""
+        import torch
+        counts, offs = self.param_layout()
+        pmax = pmax or int(max(counts.max(), 1))
+        N = shape_ids.shape[0] * P
+        dev = points.device
+        J = torch.empty(pmax, N, device=dev, dtype=torch.float32) if want_J else None
+        vjp = torch.zeros(int(offs[-1]), device=dev, dtype=torch.float32) if w is not None else None
+        _check(lib().cm_sdf_param_grad(self.h, _ptr(shape_ids), _ptr(poses), _ptr(points), shape_ids.shape[0], P,
+                                       pmax, _ptr(J), _ptr(w), _ptr(vjp), _stream()), "cm_sdf_param_grad")
+        return J, vjp
 
     # ---- contact manifold ---------------------------------------------------
     def manifold_size(self, pairs_host: np.ndarray, mode: int = 0) -> int:

@@ -192,6 +192,9 @@ struct cm_scene {
   std::vector<ShapeRec> shapes;
   std::vector<std::vector<int32_t>> edges, face_edges;
   int max_V = 0, max_E = 0, max_F = 0;
+  std::vector<int32_t> param_count;    // per shape (f4), -1: not parametrised
+  std::vector<int64_t> param_off;      // prefix sums of max(count, 0)
+  int64_t* param_off_dev = nullptr;
   int class_mask = 0;  // bit c: SDF shapes of class c (0 SQ family, 1 XPSQ, 2 varying-schedule XPSQ)
   std::vector<void*> allocs;
   float* scratch = nullptr;
@@ -237,6 +240,7 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
   std::vector<float> edge_geom;   // x_I, L, e_t (computed in FP64 from the FP32 vertices)
   cm_scene* sc = new cm_scene;
   sc->device = device;
+  sc->param_count.assign(n_shapes, 0);
   sc->edges.resize(n_shapes);
   sc->face_edges.resize(n_shapes);
 
@@ -357,6 +361,18 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
       r.has_sdf = 1;
       r.uses_xpsq = (xclass == 0 && max_depth > 1) ? 3 : xclass;
       sc->class_mask |= 1 << r.uses_xpsq;
+      // shape-parameter count (f4): leaves in pre-order; XPSQ or nested
+      // booleans are not parametrised on the GPU (-1)
+      int pc = 0;
+      for (int k = 0; k < d.n_nodes && pc >= 0; ++k) {
+        const int ty = d.nodes[k].type;
+        if (ty == CM_XPSQ) pc = -1;
+        else if (ty == CM_HALFSPACE) pc += 4;
+        else if (ty == CM_SQ) pc += 5;
+        else if (ty == CM_PSQ) pc += 5 + 4 * d.nodes[k].n_planes;
+      }
+      if (r.uses_xpsq != 0) pc = -1;
+      sc->param_count[s] = pc;
     }
     r.prog_len = (int32_t)prog.size() - r.prog_begin;
 
@@ -441,6 +457,10 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
                         (const void*)D.verts, (const void*)D.edges, (const void*)D.faces, (const void*)D.face_edges,
                         (const void*)D.edge_geom})
     if (p) sc->allocs.push_back(const_cast<void*>(p));
+  sc->param_off.assign(n_shapes + 1, 0);
+  for (int s = 0; s < n_shapes; ++s) sc->param_off[s + 1] = sc->param_off[s] + std::max(sc->param_count[s], 0);
+  sc->param_off_dev = dev_copy(sc->param_off, rc);
+  if (sc->param_off_dev) sc->allocs.push_back(sc->param_off_dev);
   D.sp = SmoothDev{sp->tau_cmp, sp->tau_min, sp->tau_clip_alpha, sp->tau_clip_t, sp->tau_delta, sp->trace_iters,
                    (float)(1.0 / sp->tau_cmp), (float)(1.0 / sp->tau_min), (float)(1.0 / sp->tau_clip_alpha),
                    (float)(1.0 / sp->tau_clip_t), (float)(1.0 / sp->tau_delta)};
@@ -514,6 +534,34 @@ int cm_sdf_eval(const cm_scene* sc, const int32_t* ids, const float* poses, cons
   int rc = cml::launch_sdf_eval(sc->dev, sc->class_mask, ids, poses, points, B, P, flags, d,
                                 (flags & CM_SDF_GRAD) ? grad : nullptr, (flags & CM_SDF_HESS) ? hess : nullptr, dpose,
                                 d2pose, dxdpose, stream);
+  if (rc) return fail(rc, cml::last_cuda_error());
+  return CM_OK;
+}
+
+int cm_param_layout(const cm_scene* sc, int32_t* counts, int64_t* offsets) {
+  if (!sc) return fail(CM_ERR_INVALID, "cm_param_layout: NULL scene");
+  const int ns = (int)sc->param_count.size();
+  for (int s = 0; s < ns; ++s) {
+    if (counts) counts[s] = sc->param_count[s];
+    if (offsets) offsets[s] = sc->param_off[s];
+  }
+  if (offsets) offsets[ns] = sc->param_off[ns];
+  return CM_OK;
+}
+
+int cm_sdf_param_grad(const cm_scene* sc, const int32_t* ids, const float* poses, const float* points, int64_t B,
+                      int64_t P, int32_t pmax, float* J, const float* w, float* vjp, void* stream) {
+  if (!sc) return fail(CM_ERR_INVALID, "cm_sdf_param_grad: NULL scene");
+  if (B < 0 || P < 0 || pmax < 0) return fail(CM_ERR_INVALID, "cm_sdf_param_grad: negative size");
+  if (B == 0 || P == 0) return CM_OK;
+  if (!ids || !poses || !points || (!J && !vjp) || (vjp && !w))
+    return fail(CM_ERR_INVALID, "cm_sdf_param_grad: NULL argument");
+  if (((uintptr_t)poses & 15) != 0) return fail(CM_ERR_INVALID, "cm_sdf_param_grad: poses must be 16-byte aligned");
+  for (size_t s = 0; s < sc->param_count.size(); ++s)
+    if (sc->param_count[s] < 0)
+      return fail(CM_ERR_UNSUPPORTED, "cm_sdf_param_grad: shape " + std::to_string(s) +
+                                           " holds an XPSQ or nested booleans (not parametrised)");
+  int rc = cml::launch_sdf_param_grad(sc->dev, ids, poses, points, B, P, pmax, J, w, vjp, sc->param_off_dev, stream);
   if (rc) return fail(rc, cml::last_cuda_error());
   return CM_OK;
 }

@@ -167,3 +167,194 @@ int launch_sdf_eval(const SceneDev& s, int class_mask, const int32_t* ids, const
 }
 
 }  // namespace cml
+
+// ============================================================================
+// shape-parameter derivatives
+// ============================================================================
+namespace {
+
+// d phi / d (a_x, a_y, a_z, eps1, eps2) of the SQ radial distance, from the
+// same log2-domain quantities as sq_eval (cm_device.cuh): with
+// lf = log2 f, h = 2^(-k lf), phi = r (1 - h):
+//   d phi = r h ln2 d(k lf),  d lf = beta d lB + gamma d l3,  lB = m lS,
+//   d lS = w0 d la0 + w1 d la1,  d la_i / d a_i = p2 d log2 q_i / d a_i,
+//   d log2 q_i / d a_i = -2 u_i^2 / (a_i q_i ln2)
+//   eps1: d lB = -p1 lB, d l3 = -p1 l3, d k = 1/2;  eps2: d la_i = -p2 la_i,
+//   d lB = p1 lS + m d lS
+__device__ __forceinline__ float sq_param_grad(const Leaf& L, const float* y, float* o) {
+  const float ia0 = L.ia[0], ia1 = L.ia[1], ia2 = L.ia[2];
+  const float p1 = L.p1, p2 = L.p2, m = L.m, k = L.k;
+  const float u0 = y[0] * ia0, u1 = y[1] * ia1, u2 = y[2] * ia2;
+  const float q0 = fmaf(u0, u0, SQ_GUARD), q1 = fmaf(u1, u1, SQ_GUARD), q2 = fmaf(u2, u2, SQ_GUARD);
+  const float lq0 = lg2(q0), lq1 = lg2(q1), lq2 = lg2(q2);
+  const float la0 = p2 * lq0, la1 = p2 * lq1, l3 = p1 * lq2;
+  const float lS = fmaxf(la0, la1) + lg2(1.f + ex2(-fabsf(la0 - la1)));
+  const float lB = m * lS;
+  const float lf = fmaxf(lB, l3) + lg2(1.f + ex2(-fabsf(lB - l3)));
+  const float h = ex2(-k * lf);
+  const float rr = fmaf(y[0], y[0], fmaf(y[1], y[1], y[2] * y[2]));
+  const float rad = rr * rsqrtf(fmaxf(rr, 1e-30f));
+  const float w0 = ex2(la0 - lS), w1 = ex2(la1 - lS), be = ex2(lB - lf), ga = ex2(l3 - lf);
+  const float c = rad * h * LN2;   // d phi = c d(k lf)
+  const float dq0 = -2.f * u0 * u0 * ia0 * rcpa(q0) * LOG2E;   // d log2 q_i / d a_i (a_i = 1/ia_i)
+  const float dq1 = -2.f * u1 * u1 * ia1 * rcpa(q1) * LOG2E;
+  const float dq2 = -2.f * u2 * u2 * ia2 * rcpa(q2) * LOG2E;
+  o[0] = c * k * be * m * w0 * p2 * dq0;
+  o[1] = c * k * be * m * w1 * p2 * dq1;
+  o[2] = c * k * ga * p1 * dq2;
+  o[3] = c * fmaf(0.5f, lf, -k * p1 * (be * lB + ga * l3));
+  const float dlS2 = -p2 * (w0 * la0 + w1 * la1);
+  o[4] = c * k * be * fmaf(m, dlS2, p1 * lS);
+  return rad * (1.f - h);
+}
+
+// parameters of leaf li at the shape-frame point x, scaled by d phi_shape /
+// d phi_leaf; emit(k, value) is called for k = 0 .. count-1
+template <class Emit>
+__device__ __forceinline__ void leaf_param_grad(const SceneDev& S, int li, const float* x, float scale, Emit emit) {
+  const Leaf& L = S.leaves[li];
+  float y[3];
+  const float t[3] = {L.t[0], L.t[1], L.t[2]};
+  float R[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R[i] = L.R[i];
+  to_local(R, t, x, y);
+  if (L.kind == LK_HALFSPACE) {   // phi = n.y + h
+    emit(0, scale * y[0]); emit(1, scale * y[1]); emit(2, scale * y[2]); emit(3, scale);
+    return;
+  }
+  // SQ, or PSQ = LSE_tau_min(phi_SQ, n_j . y + h_j): weights of the terms
+  float g5[5];
+  const float phs = sq_param_grad(L, y, g5);
+  const int np = L.n_planes;
+  float wsq = 1.f;
+  float mx = phs, Z = 1.f;
+  const float itl = LOG2E * S.sp.i_min;
+  if (np > 0) {
+    for (int j = 0; j < np; ++j) {
+      const float* pl = L.planes[j];
+      mx = fmaxf(mx, fmaf(pl[0], y[0], fmaf(pl[1], y[1], fmaf(pl[2], y[2], pl[3]))));
+    }
+    Z = ex2((phs - mx) * itl);
+    wsq = Z;
+    for (int j = 0; j < np; ++j) {
+      const float* pl = L.planes[j];
+      Z += ex2((fmaf(pl[0], y[0], fmaf(pl[1], y[1], fmaf(pl[2], y[2], pl[3]))) - mx) * itl);
+    }
+    wsq *= rcpa(Z);
+  }
+#pragma unroll
+  for (int q = 0; q < 5; ++q) emit(q, scale * wsq * g5[q]);
+  for (int j = 0; j < np; ++j) {
+    const float* pl = L.planes[j];
+    const float wj = ex2((fmaf(pl[0], y[0], fmaf(pl[1], y[1], fmaf(pl[2], y[2], pl[3]))) - mx) * itl) * rcpa(Z);
+    const float sw = scale * wj;
+    emit(5 + 4 * j, sw * y[0]); emit(6 + 4 * j, sw * y[1]); emit(7 + 4 * j, sw * y[2]); emit(8 + 4 * j, sw);
+  }
+}
+
+__device__ __forceinline__ int leaf_param_count(const Leaf& L) {
+  return L.kind == LK_HALFSPACE ? 4 : 5 + 4 * L.n_planes;
+}
+
+// one thread per point; shapes are single leaves or flat booleans (class 0).
+// J[k * N + n]; vjp[poff[shape] + k] += w[n] J[k, n] (warp-reduced when the
+// warp's points share one shape, else per-lane atomics)
+__global__ void __launch_bounds__(256) k_sdf_param_grad(SceneDev S, const int32_t* __restrict__ shape_ids,
+                                                        const float* __restrict__ poses,
+                                                        const float* __restrict__ points, int64_t B, int64_t P,
+                                                        int32_t pmax, float* __restrict__ J,
+                                                        const float* __restrict__ w, float* __restrict__ vjp,
+                                                        const int64_t* __restrict__ poff) {
+  const int64_t N = B * P;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // every lane of a warp runs the same number of iterations (warp reductions)
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < N; base += stride) {
+    const int64_t n = base + lane;
+    const bool valid = n < N;
+    const int64_t b = valid ? n / P : 0;
+    const int sid = valid ? __ldg(shape_ids + b) : -1;
+    const int sid0 = __shfl_sync(0xffffffffu, sid, 0);
+    const bool uni = __all_sync(0xffffffffu, valid && sid == sid0);
+    if (!valid) continue;
+    const ShapeRec sh = S.shapes[sid];
+    const float4 pa = __ldg(reinterpret_cast<const float4*>(poses) + 2 * b);
+    const float4 pb = __ldg(reinterpret_cast<const float4*>(poses) + 2 * b + 1);
+    const float t[3] = {pa.x, pa.y, pa.z};
+    const float q[4] = {pa.w, pb.x, pb.y, pb.z};
+    float R[9];
+    quat_to_R(q, R);
+    const float x[3] = {__ldg(points + 3 * n), __ldg(points + 3 * n + 1), __ldg(points + 3 * n + 2)};
+    float y[3];
+    to_local(R, t, x, y);
+    const float wn = vjp ? __ldg(w + n) : 0.f;
+    const int64_t off = vjp ? __ldg(poff + sid) : 0;
+    int kbase = 0;
+    auto emit = [&](int k, float v) {
+      const int kk = kbase + k;
+      if (J && kk < pmax) J[(int64_t)kk * N + n] = v;
+      if (vjp) {
+        float s = wn * v;
+        if (uni) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+          if (lane == 0) atomicAdd(vjp + off + kk, s);
+        } else {
+          atomicAdd(vjp + off + kk, s);
+        }
+      }
+    };
+    const Instr* prog = S.prog + sh.prog_begin;
+    if (sh.prog_len == 1) {
+      leaf_param_grad(S, prog[0].idx, y, 1.f, emit);
+      kbase += leaf_param_count(S.leaves[prog[0].idx]);
+    } else {
+      // flat boolean: phi = s_out tau log sum exp(s_i phi_i / tau);
+      // d phi / d phi_i = s_out s_i softmax_i (pass 1: the accumulator)
+      const float itl = LOG2E * S.sp.i_min;
+      float mx = -INFINITY, Z = 0.f, so = 1.f;
+      for (int pc = 1; pc < sh.prog_len; ++pc) {
+        const Instr in = prog[pc];
+        if (in.op != OP_LEAF) { so = in.out_sign; continue; }
+        Res<0> r;
+        leaf_eval<0, 0, false>(S, in.idx, y, r);
+        const float v = in.child_sign * r.v;
+        if (v > mx) { Z = fmaf(Z, ex2((mx - v) * itl), 1.f); mx = v; }
+        else Z += ex2((v - mx) * itl);
+      }
+      const float iZ = rcpa(Z);
+      for (int pc = 1; pc < sh.prog_len; ++pc) {
+        const Instr in = prog[pc];
+        if (in.op != OP_LEAF) continue;
+        Res<0> r;
+        leaf_eval<0, 0, false>(S, in.idx, y, r);
+        const float sc = so * in.child_sign * ex2((in.child_sign * r.v - mx) * itl) * iZ;
+        leaf_param_grad(S, in.idx, y, sc, emit);
+        kbase += leaf_param_count(S.leaves[in.idx]);
+      }
+    }
+    if (J)
+      for (int kk = kbase; kk < pmax; ++kk) J[(int64_t)kk * N + n] = 0.f;
+  }
+}
+
+}  // namespace
+
+namespace cml {
+
+int launch_sdf_param_grad(const SceneDev& s, const int32_t* ids, const float* poses, const float* pts, int64_t B,
+                          int64_t P, int32_t pmax, float* J, const float* w, float* vjp, const int64_t* poff,
+                          void* stream) {
+  const int threads = 256;
+  const int64_t N = B * P;
+  int64_t blocks = (N + threads - 1) / threads;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  k_sdf_param_grad<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(s, ids, poses, pts, B, P, pmax, J, w, vjp,
+                                                                           poff);
+  return check_launch("k_sdf_param_grad");
+}
+
+}  // namespace cml

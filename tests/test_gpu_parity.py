@@ -350,3 +350,76 @@ def test_manifold_tier3_sampled(cuda, oracle_mod, cfg):
     _report("manifold_%s_t3" % cfg, rep)
     assert nf == 0, json.dumps(rep, indent=1)
     assert PT.excluded_fraction(rep) < 0.01
+
+
+def _param_scene():
+    rng = np.random.default_rng(51)
+    a = lambda: rng.uniform(0.03, 0.07, 3)
+    e = lambda: rng.uniform(0.3, 1.5, 2)
+    pose = lambda: [*rng.uniform(-0.03, 0.03, 3), *synth.random_quats(rng, 1)[0]]
+    shapes = [
+        synth.make_shape("sq", synth.sq(a(), e()), None),
+        synth.make_shape("psq", synth.psq(a(), e(), [[*rng.normal(size=3), -0.01], [*rng.normal(size=3), -0.02]]), None),
+        synth.make_shape("hs", synth.halfspace(rng.normal(size=3), 0.01), None),
+        synth.make_shape("uni", synth.op("union", [synth.sq(a(), e(), pose=pose()) for _ in range(4)]), None),
+        synth.make_shape("int", synth.op("intersection", [synth.sq(a(), e()), synth.halfspace(rng.normal(size=3), 0.01)]), None),
+        synth.make_shape("sub", synth.op("subtraction", [synth.psq(a(), e(), [[*rng.normal(size=3), -0.01]]),
+                                                         synth.sq(a() * 0.5, e(), pose=pose())]), None),
+    ]
+    return shapes, rng
+
+
+def test_sdf_param_grad_parity(cuda, oracle_mod):
+    """Shape-parameter derivatives: per-point J of every
+    parametrised leaf kind and flat boolean against the oracle's parameter
+    seeds, and the vector-Jacobian product sum_n w_n J_n against J^T w."""
+    import torch
+    from paper_2604_17538_b200 import binding
+    shapes, rng = _param_scene()
+    sc = scene_of(shapes, ell=0.1)
+    S = binding.Scene(sc.shapes, sc.smooth)
+    counts, offs = S.param_layout()
+    osc = oracle_mod.OracleScene(sc)
+    assert [osc.param_count(s) for s in range(len(shapes))] == list(counts)
+    B, P = 24, 96
+    ids = np.repeat(np.arange(len(shapes)), B // len(shapes)).astype(np.int32)
+    poses = np.stack([synth.pose_row(rng.uniform(-0.1, 0.1, 3), synth.random_quats(rng, 1)[0]) for _ in range(B)])
+    poses = poses.astype(np.float32)
+    pts = (poses[:, None, :3] + rng.normal(size=(B, P, 3)) * 0.05).reshape(-1, 3).astype(np.float32)
+    w = rng.normal(size=B * P).astype(np.float32)
+    pmax = int(counts.max())
+    J, vjp = S.sdf_param_grad(torch.from_numpy(ids).cuda(), torch.from_numpy(poses).cuda(),
+                              torch.from_numpy(pts).cuda(), P, pmax, w=torch.from_numpy(w).cuda())
+    torch.cuda.synchronize()
+    Jg = J.cpu().numpy().T
+    Jr = osc.sdf_param_grad(ids, poses, pts, P, pmax)
+    Jp = osc.sdf_param_grad(ids, PT.perturb_inputs(np.random.default_rng(52), poses), pts, P, pmax)
+    rep = []
+    nf = PT.compare("J", Jg, Jr, Jp, PT.tol_vec(Jr, 1), rep)
+    ref_vjp = np.zeros(int(offs[-1]))
+    for n in range(B * P):
+        s = ids[n // P]
+        ref_vjp[offs[s]:offs[s] + counts[s]] += w[n] * Jr[n, :counts[s]]
+    bound = np.zeros_like(ref_vjp)
+    for n in range(B * P):
+        s = ids[n // P]
+        bound[offs[s]:offs[s] + counts[s]] += np.abs(w[n] * Jr[n, :counts[s]])
+    nf += PT.compare("vjp", vjp.cpu().numpy(), ref_vjp, ref_vjp, 1e-4 * np.maximum(bound, 1e-6), rep)
+    _report("sdf_param_grad", rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+    assert PT.excluded_fraction(rep) < 0.01
+
+
+def test_sdf_param_grad_unsupported(cuda):
+    """Scenes holding an XPSQ report count -1 and the call is refused."""
+    import torch
+    from paper_2604_17538_b200 import binding
+    sc = scene_of([synth.make_shape("cup", synth.cup(), None)], ell=0.04)
+    S = binding.Scene(sc.shapes, sc.smooth)
+    counts, _ = S.param_layout()
+    assert counts[0] == -1
+    z = torch.zeros(1, 8, device="cuda")
+    z[0, 3] = 1
+    with pytest.raises(binding.CMError):
+        S.sdf_param_grad(torch.zeros(1, dtype=torch.int32, device="cuda"), z,
+                         torch.zeros(4, 3, device="cuda"), 4, 4)
