@@ -22,8 +22,11 @@ using cml::num_sms;
 // ============================================================================
 // sdf_eval
 // ============================================================================
+#ifndef CM_SDF_MINB
+#define CM_SDF_MINB 3   // 80 registers: +2% on the SDF workload over 1 and 2
+#endif
 template <int O, int XP, bool PG, bool PH>
-__global__ void __launch_bounds__(256) k_sdf_eval(SceneDev S, const int32_t* __restrict__ shape_ids,
+__global__ void __launch_bounds__(256, CM_SDF_MINB) k_sdf_eval(SceneDev S, const int32_t* __restrict__ shape_ids,
                                                   const float* __restrict__ poses, const float* __restrict__ points,
                                                   int64_t B, int64_t P, float* __restrict__ d,
                                                   float* __restrict__ grad, float* __restrict__ hess,
