@@ -14,8 +14,9 @@ shard.  Weak scaling: every rank owns n_env environments (global env ids
 collective on the data path; timing is max over ranks.  Inputs (poses,
 pairs, offsets) are resident in HBM for `value`; `e2e` re-times the same
 step through the public API with the step's poses copied host->device from
-pinned memory and the fused depths copied back every step.  L2 is flushed
-(256 MiB write) between timed steps.
+pinned memory and the fused depths copied back every step (double buffered:
+the copies of neighbouring steps overlap the compute on separate upload /
+download streams).  L2 is flushed (256 MiB write) between timed steps.
 """
 from __future__ import annotations
 
@@ -287,6 +288,59 @@ def _timed(step, args, stream, flush, world, local):
     return float(t.item()) / args.steps, launches, clk
 
 
+def _e2e_pipelined(run_step, h2d, d2h, steps, world, dev):
+    """End-to-end loop through the public API with host buffers, double
+    buffered: step i's host->device copy of its inputs (pinned) runs on an
+    upload stream and step i-1's device->host read-back on a download stream,
+    both overlapping step i's compute on the caller's stream (PCIe is full
+    duplex).  h2d[s] = (device dst, pinned src), d2h[s] = (pinned dst, device
+    src) for slot s in {0, 1}; run_step(s) enqueues the compute reading and
+    writing slot s.  Every step copies its inputs and reads its result back;
+    the time is from the first upload to the last read-back (CUDA events),
+    max over ranks.  Returns ms per step."""
+    import torch
+    import torch.distributed as dist
+    comp = torch.cuda.current_stream()
+    up, down = torch.cuda.Stream(), torch.cuda.Stream()
+    ev = lambda: torch.cuda.Event()
+    ev_in, ev_comp, ev_out = [ev(), ev()], [ev(), ev()], [ev(), ev()]
+
+    def go(n):
+        for i in range(n):
+            s = i % 2
+            with torch.cuda.stream(up):
+                if i >= 2:
+                    up.wait_event(ev_comp[s])        # slot s inputs no longer read
+                h2d[s][0].copy_(h2d[s][1], non_blocking=True)
+                ev_in[s].record(up)
+            comp.wait_event(ev_in[s])
+            if i >= 2:
+                comp.wait_event(ev_out[s])           # slot s result already read back
+            run_step(s)
+            ev_comp[s].record(comp)
+            with torch.cuda.stream(down):
+                down.wait_event(ev_comp[s])
+                d2h[s][0].copy_(d2h[s][1], non_blocking=True)
+                ev_out[s].record(down)
+        for s in range(min(n, 2)):
+            comp.wait_event(ev_out[s])
+
+    go(2)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(comp)
+    up.wait_event(e0)
+    go(steps)
+    e1.record(comp)
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    return float(te.item())
+
+
 def run_sdf(args, sc, n_body, gen_s, world, rank, local):
     """Secondary metric: cm_sdf_eval of the 32 C5 SDF prototypes
     with value, gradient, Hessian and pose gradient at P points per body."""
@@ -310,29 +364,15 @@ def run_sdf(args, sc, n_body, gen_s, world, rank, local):
     e2e = None
     if not args.no_e2e:
         pts_h = torch.from_numpy(sc.points).pin_memory()
-        d_h = torch.empty(n_pts, dtype=torch.float32).pin_memory()
-        pts_d = torch.empty_like(pts)
-
-        def e2e_step():
-            pts_d.copy_(pts_h, non_blocking=True)
-            o = S.sdf_eval(ids, poses, pts_d, P, flags, out=out)
-            d_h.copy_(o["d"], non_blocking=True)
-        for _ in range(2):
-            e2e_step()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        te = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": n_pts * world / (float(te.item()) / 1e3), "unit": "points/s",
-               "h2d_bytes_per_step": int(pts_h.numel() * 4), "d2h_bytes_per_step": int(n_pts * 4)}
+        d_h = [torch.empty(n_pts, dtype=torch.float32).pin_memory() for _ in range(2)]
+        pts_d = [torch.empty_like(pts) for _ in range(2)]
+        outs = [out, {k: torch.empty_like(v) for k, v in out.items()}]
+        ms_e = _e2e_pipelined(lambda s_: S.sdf_eval(ids, poses, pts_d[s_], P, flags, out=outs[s_]),
+                              [(pts_d[k], pts_h) for k in range(2)], [(d_h[k], outs[k]["d"]) for k in range(2)],
+                              args.steps, world, dev)
+        e2e = {"value": n_pts * world / (ms_e / 1e3), "unit": "points/s",
+               "h2d_bytes_per_step": int(pts_h.numel() * 4), "d2h_bytes_per_step": int(n_pts * 4),
+               "pipeline": "double-buffered: upload / download streams overlap the compute"}
     with open(os.path.join(ROOT, "paper_2604_17538_b200", "costmodel.json")) as f:
         cm = json.load(f)
     names = [sc.shapes[i].name for i in range(len(sc.shapes))]
@@ -434,28 +474,16 @@ def main():
     e2e = None
     if not args.no_e2e:
         poses_h = torch.from_numpy(scene.poses).pin_memory()
-        depth_h = torch.empty(C, dtype=torch.float32).pin_memory()
-        poses_d = torch.empty_like(poses)
-        for _ in range(2):
-            poses_d.copy_(poses_h, non_blocking=True)
-            o = S.contact_manifold(pairs, offs, C, poses_d, args.tier, out)
-            depth_h.copy_(o["depth"], non_blocking=True)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for i in range(args.steps):
-            poses_d.copy_(poses_h, non_blocking=True)
-            o = S.contact_manifold(pairs, offs, C, poses_d, args.tier, out)
-            depth_h.copy_(o["depth"], non_blocking=True)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        te = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": n_pairs_all / (float(te.item()) / 1e3), "unit": "pairs/s",
-               "h2d_bytes_per_step": int(poses_h.numel() * 4), "d2h_bytes_per_step": int(C * 4)}
+        depth_h = [torch.empty(C, dtype=torch.float32).pin_memory() for _ in range(2)]
+        poses_d = [torch.empty_like(poses) for _ in range(2)]
+        # slot 1 shares every output but the read-back field with slot 0
+        outs = [out, dict(out, depth=torch.empty_like(out["depth"]))]
+        ms_e = _e2e_pipelined(lambda s_: S.contact_manifold(pairs, offs, C, poses_d[s_], args.tier, outs[s_]),
+                              [(poses_d[k], poses_h) for k in range(2)],
+                              [(depth_h[k], outs[k]["depth"]) for k in range(2)], args.steps, world, dev)
+        e2e = {"value": n_pairs_all / (ms_e / 1e3), "unit": "pairs/s",
+               "h2d_bytes_per_step": int(poses_h.numel() * 4), "d2h_bytes_per_step": int(C * 4),
+               "pipeline": "double-buffered: upload / download streams overlap the compute"}
 
     # ---- roofline of the manifold kernels ---------------------------------
     peaks, peak_src = load_peaks()
