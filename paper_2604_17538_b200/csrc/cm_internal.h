@@ -1,5 +1,5 @@
 // Internal layouts shared by the host library (cm_host.cpp) and the sm_100a
-// kernels (cm_kernels.cu).  Not part of the ABI.
+// kernels (cm_kernels_*.cu).  Not part of the ABI.
 #pragma once
 #include <stdint.h>
 
@@ -100,7 +100,7 @@ constexpr int64_t kScratchCapBytes = 1024ll << 20;
 
 }  // namespace cmi
 
-// launchers implemented in cm_kernels.cu
+// launchers implemented in cm_kernels_*.cu
 namespace cml {
 int launch_sdf_eval(const cmi::SceneDev& s, int class_mask, const int32_t* shape_ids, const float* poses,
                     const float* points, int64_t B, int64_t P, uint32_t flags, float* d, float* grad, float* hess,

@@ -7,9 +7,12 @@
 `run` launches, in a fixed order:
   1. k_sdf_eval over 2^20 points for every C5 SDF prototype and every C2-C4
      SDF shape, at order 1 (value + gradient) and order 2 (+ Hessian);
-  2. k_contact_manifold (tier 2) with a half-space SDF for each sampled mesh
-     of C2-C5, to measure the manifold's own arithmetic (trace recursion,
-     candidate derivative rows, per-face fusion) per pair.
+  2. the manifold (tier 2) with a half-space SDF for each sampled mesh of
+     C2-C5, to measure the manifold's own arithmetic (trace recursion,
+     candidate derivative rows, per-face fusion) per pair: every launch of a
+     call is summed (the k_mf_* kernels; the frozen table in
+     paper_2604_17538_b200/costmodel.json was measured on the first, fused
+     k_contact_manifold kernel and is kept as the fixed work definition).
 FLOPs = 2 FFMA + FADD + FMUL (+ the paired FFMA2/FADD2/FMUL2 x 2), counted
 per executed thread instruction.  Per-pair algorithmic FLOPs are then
   overhead(mesh) + (V + E) c(B, 2) + 2 E (iters - 1) c(B, 1)
@@ -110,7 +113,7 @@ def parse(csv_path):
         return 2 * g("ffma") + g("fadd") + g("fmul") + 4 * g("ffma2") + 2 * g("fadd2") + 2 * g("fmul2"), mufu
 
     sdf_l = [L for _, L in sorted(launches.items()) if "k_sdf_eval" in L["name"]]
-    man_l = [L for _, L in sorted(launches.items()) if "k_contact_manifold" in L["name"]]
+    man_l = [L for _, L in sorted(launches.items()) if "k_contact_manifold" in L["name"] or "k_mf_" in L["name"]]
     # with several SDF classes a call may launch one kernel per class; the
     # sdf table is built from the per-call sums
     names = order["sdf"]
