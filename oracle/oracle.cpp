@@ -405,7 +405,9 @@ template <class T> void xpsq_frame(const Node& n, const T& t, T* R) {
 
 template <class T> T lerp(double a, double b, const T& t) { return a + (b - a) * t; }
 
-template <class T> T xpsq_phi(const Node& n, const T* y, const Smooth& sp) {
+template <class T> T pval(double v, int node, int slot);
+extern thread_local int g_seed_node;
+template <class T> T xpsq_phi(const Node& n, const T* y, const Smooth& sp, int idx = -1) {
   T tk[3];
   xpsq_roots(n, y, sp, tk, nullptr, nullptr);
   T phis[3];
@@ -421,17 +423,23 @@ template <class T> T xpsq_phi(const Node& n, const T* y, const Smooth& sp) {
     for (int i = 0; i < 3; ++i) yk[i] = R[0 * 3 + i] * dx[0] + R[1 * 3 + i] * dx[1] + R[2 * 3 + i] * dx[2];
     // schedules eps(t), a(t), P(t): linear between endpoint values, plane
     // normals renormalised (Reading #8)
-    T e1 = lerp(n.eps[0][0], n.eps[1][0], t);
-    T e2 = lerp(n.eps[0][1], n.eps[1][1], t);
+    // (shape-parameter seeds, f4: one slot moves both endpoint values)
+    auto L2 = [&](double v0, double v1, int slot) {
+      if (idx != g_seed_node) return lerp(v0, v1, t);          // (no seed: the literal schedule)
+      const T a0 = pval<T>(v0, idx, slot), a1 = pval<T>(v1, idx, slot);
+      return a0 + (a1 - a0) * t;
+    };
+    T e1 = L2(n.eps[0][0], n.eps[1][0], 3);
+    T e2 = L2(n.eps[0][1], n.eps[1][1], 4);
     T a[3];
-    for (int i = 0; i < 3; ++i) a[i] = lerp(n.a[0][i], n.a[1][i], t);
+    for (int i = 0; i < 3; ++i) a[i] = L2(n.a[0][i], n.a[1][i], i);
     T pl[MAXP][4];
     for (int j = 0; j < n.n_planes; ++j) {
       T nv[3];
-      for (int i = 0; i < 3; ++i) nv[i] = lerp(n.pl[0][j][i], n.pl[1][j][i], t);
+      for (int i = 0; i < 3; ++i) nv[i] = L2(n.pl[0][j][i], n.pl[1][j][i], 5 + 4 * j + i);
       T nn = sqrt(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]);
       for (int i = 0; i < 3; ++i) pl[j][i] = nv[i] / nn;
-      pl[j][3] = lerp(n.pl[0][j][3], n.pl[1][j][3], t);
+      pl[j][3] = L2(n.pl[0][j][3], n.pl[1][j][3], 8 + 4 * j);
     }
     phis[k] = psq_phi(yk, e1, e2, a, n.n_planes, pl, sp.tau_min);
   }
@@ -479,7 +487,7 @@ template <class T> T node_phi(const Shape& sh, int idx, const T* yparent, const 
       return psq_phi(y, pval<T>(n.eps[0][0], idx, 3), pval<T>(n.eps[0][1], idx, 4), a, np, pl, sp.tau_min);
     }
     case K_XPSQ:
-      return xpsq_phi(n, y, sp);
+      return xpsq_phi(n, y, sp, idx);
     default: {
       std::vector<T> ops(n.n_children);
       for (int c = 0; c < n.n_children; ++c) ops[c] = node_phi(sh, n.child[c], y, sp);
@@ -938,18 +946,24 @@ int ora_contact_manifold(void* s, const int* pairs, long n_pairs, const double* 
 
 // ---- shape-parameter derivatives of sdf_eval ----------
 // Parameters of a shape: its nodes in index (pre-order) order, slots per node
-// as for pval above; XPSQ nodes are not parametrised here (the shape reports
-// -1).  J[n * pmax + k] = d phi(point n) / d param k of the point's shape,
+// as for pval above; an XPSQ node with constant schedules has the PSQ slots
+// (each moves both endpoint values; the plane normal is renormalised as in
+// xpsq_phi); varying schedules are not parametrised (the shape reports -1).  J[n * pmax + k] = d phi(point n) / d param k of the point's shape,
 // zero beyond the shape's count; one Dual<double,1> evaluation per parameter.
 int ora_shape_param_count(void* s, int shape) {
   Scene* sc = (Scene*)s;
   const Shape& sh = sc->shapes[shape];
   int c = 0;
   for (const Node& n : sh.nodes) {
-    if (n.type == K_XPSQ) return -1;
+    if (n.type == K_XPSQ) {   // constant schedules only (one value per parameter)
+      bool cst = n.eps[0][0] == n.eps[1][0] && n.eps[0][1] == n.eps[1][1];
+      for (int i = 0; i < 3; ++i) cst = cst && n.a[0][i] == n.a[1][i];
+      for (int j = 0; j < n.n_planes; ++j) for (int i = 0; i < 4; ++i) cst = cst && n.pl[0][j][i] == n.pl[1][j][i];
+      if (!cst) return -1;
+    }
     if (n.type == K_HALFSPACE) c += 4;
     else if (n.type == K_SQ) c += 5;
-    else if (n.type == K_PSQ) c += 5 + 4 * n.n_planes;
+    else if (n.type == K_PSQ || n.type == K_XPSQ) c += 5 + 4 * n.n_planes;
   }
   return c;
 }
@@ -973,7 +987,7 @@ int ora_sdf_param_grad(void* s, const int* shape_ids, const double* poses, const
     int k = 0;
     for (int ni = 0; ni < (int)sh.nodes.size(); ++ni) {
       const Node& nd = sh.nodes[ni];
-      int cnt = nd.type == K_HALFSPACE ? 4 : (nd.type == K_SQ ? 5 : (nd.type == K_PSQ ? 5 + 4 * nd.n_planes : 0));
+      int cnt = nd.type == K_HALFSPACE ? 4 : (nd.type == K_SQ ? 5 : ((nd.type == K_PSQ || nd.type == K_XPSQ) ? 5 + 4 * nd.n_planes : 0));
       for (int slot = 0; slot < cnt && k < pmax; ++slot, ++k) {
         g_seed_node = ni;
         g_seed_slot = slot;

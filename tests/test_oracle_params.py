@@ -42,7 +42,7 @@ def _perturbed(shape, node, slot, h):
             if nd[key] is not None and len(nd[key]):
                 pl = np.array(nd[key], dtype=np.float64)
                 pl[j, i] += h
-                nd[key] = pl
+                nd[key] = pl.tolist()
     elif slot < 3:
         nd["a"] = [np.array(a, dtype=np.float64) + h * (np.arange(3) == slot) for a in nd["a"]]
     else:
@@ -53,18 +53,25 @@ def _perturbed(shape, node, slot, h):
 def _slots(shape):
     out = []
     for ni, nd in enumerate(shape.sdf):
-        c = {"halfspace": 4, "sq": 5, "psq": 5 + 4 * len(nd["planes"])}.get(nd["type"], 0)
+        c = {"halfspace": 4, "sq": 5, "psq": 5 + 4 * len(nd["planes"]),
+             "xpsq": 5 + 4 * len(nd["planes"])}.get(nd["type"], 0)
         out += [(ni, s) for s in range(c)]
     return out
 
 
-@pytest.mark.parametrize("kind", ["sq", "psq", "union", "subtraction", "intersection"])
+@pytest.mark.parametrize("kind", ["sq", "psq", "union", "subtraction", "intersection", "xpsq", "cup"])
 def test_param_grad_fd(oracle_mod, kind):
     O = oracle_mod
-    rng = np.random.default_rng({"sq": 2, "psq": 3, "union": 4, "subtraction": 5, "intersection": 6}[kind])
+    rng = np.random.default_rng({"sq": 2, "psq": 3, "union": 4, "subtraction": 5, "intersection": 6, "xpsq": 7,
+                                 "cup": 8}[kind])
     a = lambda: rng.uniform(0.2, 0.4, 3)
     e = lambda: rng.uniform(0.4, 1.4, 2)
-    if kind == "sq":
+    if kind == "xpsq":   # curved spline, constant schedules, one cross-section plane
+        root = synth.xpsq([-0.3, 0, 0, 0.0, 0.35, 0.05, 0.3, 0, 0.02], (0.12, 0.15, 0.1), (0.6, 0.8),
+                          planes0=[[0.2, 0.3, 0.93, -0.05]])
+    elif kind == "cup":   # nested booleans with an XPSQ handle (ell = 0.04 scale)
+        root = synth.cup()
+    elif kind == "sq":
         root = synth.sq(a(), e())
     elif kind == "psq":
         root = synth.psq(a(), e(), [[*rng.normal(size=3), -0.05], [*rng.normal(size=3), -0.1]])
@@ -77,13 +84,13 @@ def test_param_grad_fd(oracle_mod, kind):
         root = synth.op(kind, kids)
     shape = synth.make_shape("p", root, None)
     pose = rand_pose(rng, 0.2)
-    pts = pose[:3] + rng.normal(size=(24, 3)) * 0.35
+    pts = pose[:3] + rng.normal(size=(24, 3)) * (0.05 if kind == "cup" else 0.35)
     osc, J = _J(O, [shape], pose, pts)
     slots = _slots(shape)
     assert osc.param_count(0) == len(slots) == J.shape[1]
     # the oracle stores shape parameters in FP32 (input hygiene, reading #36),
     # so the step is 1e-3 with a fourth-order central stencil
-    h = 1e-3
+    h = 5e-5 if kind == "cup" else 1e-3   # the cup handle's section is ~0.005 across
     f = lambda ni, sl, d: O.OracleScene(scene_of([_perturbed(shape, ni, sl, d)])).sdf_eval(
         [0], pose[None, :], pts, len(pts))["d"]
     for k, (ni, sl) in enumerate(slots):
@@ -91,7 +98,8 @@ def test_param_grad_fd(oracle_mod, kind):
         assert np.allclose(J[:, k], fd, rtol=1e-4, atol=2e-5), (kind, ni, sl, np.abs(J[:, k] - fd).max())
 
 
-def test_param_count_xpsq_unsupported(oracle_mod):
+def test_param_count_varying_xpsq_unsupported(oracle_mod):
     O = oracle_mod
-    osc = O.OracleScene(scene_of([synth.make_shape("c", synth.cup(), None)]))
+    vary = synth.xpsq([-0.3, 0, 0, 0.0, 0.35, 0.05, 0.3, 0, 0.02], (0.12, 0.15, 0.1), (0.6, 0.8), a1=(0.1, 0.1, 0.1))
+    osc = O.OracleScene(scene_of([synth.make_shape("v", vary, None)]))
     assert osc.param_count(0) == -1
