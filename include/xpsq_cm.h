@@ -173,10 +173,13 @@ int cm_sdf_eval(const cm_scene* scene, const int32_t* shape_ids, const float* po
  * Parameters of shape s, in the order of its SDF nodes (pre-order, as given
  * to cm_scene_create), endpoint-0 values: half-space (n_x, n_y, n_z, h); SQ
  * (a_x, a_y, a_z, eps1, eps2); PSQ as SQ then (n_x, n_y, n_z, h) per plane;
- * boolean nodes have none (the raw plane normal is the parameter: no
- * renormalisation).  counts[s] (host, [n_shapes]) = the count, 0 without an
- * SDF, -1 when the shape holds an XPSQ or booleans nested deeper than one
- * level (not parametrised); offsets (host, [n_shapes + 1]) = prefix sums of
+ * XPSQ with constant schedules as PSQ (its cross-section; each parameter
+ * moves both endpoint values, normals renormalised as in the XPSQ; control
+ * points are not parameters here); boolean nodes have none (a PSQ's raw plane
+ * normal is the parameter: no renormalisation).  counts[s] (host,
+ * [n_shapes]) = the count, 0 without an SDF, -1 when the shape holds a
+ * varying-schedule XPSQ or booleans nested deeper than one level (not
+ * parametrised); offsets (host, [n_shapes + 1]) = prefix sums of
  * max(count, 0) (the layout of the vjp vector).  Either may be NULL. */
 int cm_param_layout(const cm_scene* scene, int32_t* counts, int64_t* offsets);
 /* For each point n (layout of cm_sdf_eval): J[k*N + n] = d phi(n) / d param k

@@ -361,17 +361,16 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
       r.has_sdf = 1;
       r.uses_xpsq = (xclass == 0 && max_depth > 1) ? 3 : xclass;
       sc->class_mask |= 1 << r.uses_xpsq;
-      // shape-parameter count (f4): leaves in pre-order; XPSQ or nested
-      // booleans are not parametrised on the GPU (-1)
+      // shape-parameter count (f4): leaves in pre-order; varying-schedule
+      // XPSQ or nested booleans are not parametrised on the GPU (-1)
       int pc = 0;
-      for (int k = 0; k < d.n_nodes && pc >= 0; ++k) {
+      for (int k = 0; k < d.n_nodes; ++k) {
         const int ty = d.nodes[k].type;
-        if (ty == CM_XPSQ) pc = -1;
-        else if (ty == CM_HALFSPACE) pc += 4;
+        if (ty == CM_HALFSPACE) pc += 4;
         else if (ty == CM_SQ) pc += 5;
-        else if (ty == CM_PSQ) pc += 5 + 4 * d.nodes[k].n_planes;
+        else if (ty == CM_PSQ || ty == CM_XPSQ) pc += 5 + 4 * d.nodes[k].n_planes;
       }
-      if (r.uses_xpsq != 0) pc = -1;
+      if (r.uses_xpsq == 2 || max_depth > 1) pc = -1;   // varying schedules / nested booleans
       sc->param_count[s] = pc;
     }
     r.prog_len = (int32_t)prog.size() - r.prog_begin;

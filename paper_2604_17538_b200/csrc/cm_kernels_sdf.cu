@@ -184,9 +184,9 @@ namespace {
 //   d log2 q_i / d a_i = -2 u_i^2 / (a_i q_i ln2)
 //   eps1: d lB = -p1 lB, d l3 = -p1 l3, d k = 1/2;  eps2: d la_i = -p2 la_i,
 //   d lB = p1 lS + m d lS
-__device__ __forceinline__ float sq_param_grad(const Leaf& L, const float* y, float* o) {
-  const float ia0 = L.ia[0], ia1 = L.ia[1], ia2 = L.ia[2];
-  const float p1 = L.p1, p2 = L.p2, m = L.m, k = L.k;
+__device__ __forceinline__ float sq_param_grad_p(const float* ia, float p1, float p2, float m, float k,
+                                                 const float* y, float* o) {
+  const float ia0 = ia[0], ia1 = ia[1], ia2 = ia[2];
   const float u0 = y[0] * ia0, u1 = y[1] * ia1, u2 = y[2] * ia2;
   const float q0 = fmaf(u0, u0, SQ_GUARD), q1 = fmaf(u1, u1, SQ_GUARD), q2 = fmaf(u2, u2, SQ_GUARD);
   const float lq0 = lg2(q0), lq1 = lg2(q1), lq2 = lg2(q2);
@@ -210,6 +210,96 @@ __device__ __forceinline__ float sq_param_grad(const Leaf& L, const float* y, fl
   o[4] = c * k * be * fmaf(m, dlS2, p1 * lS);
   return rad * (1.f - h);
 }
+__device__ __forceinline__ float sq_param_grad(const Leaf& L, const float* y, float* o) {
+  return sq_param_grad_p(L.ia, L.p1, L.p2, L.m, L.k, y, o);
+}
+
+// XPSQ with constant schedules (f4): at each projection root t_k (which does
+// not depend on a, eps or the planes) the PSQ of the root's local point y_k;
+// phi = -tau LSE(-phi_k / tau) over the roots (one root when they coincide),
+// so d phi = sum_k u_k d PSQ_k, u = softmax(-phi / tau); the plane normal is
+// renormalised in the XPSQ (reading #8): d/dn = (I - n n^T) y_k w_j
+template <class Emit>
+__device__ __forceinline__ void xpsq_param_grad(const SceneDev& S, const Xpsq& X, const float* y, float scale,
+                                                Emit emit) {
+  const float w[3] = {y[0] - X.p1[0], y[1] - X.p1[1], y[2] - X.p1[2]};
+  float tv[3], tg[3][3], th[3][6];
+  const bool single = xpsq_root_t<0>(X, S.sp, w, tv, tg, th);
+  const int nr = single ? 1 : 3, np = X.n_planes;
+  const float itl = LOG2E * S.sp.i_min, tau = S.sp.tau_min;
+  float g5[3][5], wsq[3], phk[3], yk[3][3], wpl[3][CM_MAX_PLANES];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (k >= nr) break;
+    const float t = tv[k];
+    float pd[3], d[3], T[3], N[3], bb[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      pd[i] = fmaf(2.f * X.A[i], t, X.B[i]);
+      d[i] = y[i] - fmaf(fmaf(X.A[i], t, X.B[i]), t, X.p1[i]);
+    }
+    if (X.frenet) {
+      const float in = rsqrtf(pd[0] * pd[0] + pd[1] * pd[1] + pd[2] * pd[2]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) { T[i] = pd[i] * in; bb[i] = X.bhat[i]; }
+      N[0] = bb[1] * T[2] - bb[2] * T[1]; N[1] = bb[2] * T[0] - bb[0] * T[2]; N[2] = bb[0] * T[1] - bb[1] * T[0];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) { T[i] = X.R0[i * 3 + 0]; N[i] = X.R0[i * 3 + 1]; bb[i] = X.R0[i * 3 + 2]; }
+    }
+    yk[k][0] = T[0] * d[0] + T[1] * d[1] + T[2] * d[2];
+    yk[k][1] = N[0] * d[0] + N[1] * d[1] + N[2] * d[2];
+    yk[k][2] = bb[0] * d[0] + bb[1] * d[1] + bb[2] * d[2];
+    const float phs = sq_param_grad_p(X.sq_ia, X.sq_p1, X.sq_p2, X.sq_m, X.sq_k, yk[k], g5[k]);
+    float mx = phs;
+    for (int j = 0; j < np; ++j)
+      mx = fmaxf(mx, fmaf(X.pl0[j][0], yk[k][0], fmaf(X.pl0[j][1], yk[k][1], fmaf(X.pl0[j][2], yk[k][2], X.pl0[j][3]))));
+    float Z = ex2((phs - mx) * itl);
+    wsq[k] = Z;
+    for (int j = 0; j < np; ++j) {
+      wpl[k][j] = ex2((fmaf(X.pl0[j][0], yk[k][0], fmaf(X.pl0[j][1], yk[k][1], fmaf(X.pl0[j][2], yk[k][2], X.pl0[j][3]))) -
+                       mx) * itl);
+      Z += wpl[k][j];
+    }
+    const float iZ = rcpa(Z);
+    wsq[k] *= iZ;
+    for (int j = 0; j < np; ++j) wpl[k][j] *= iZ;
+    phk[k] = fmaf(tau * LN2, lg2(Z), mx);   // PSQ = tau log sum exp(v / tau)
+  }
+  float u[3] = {1.f, 0.f, 0.f};
+  if (!single) {   // softmax(-phi_k / tau)
+    const float mn = fminf(phk[0], fminf(phk[1], phk[2]));
+    float Zu = 0.f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { u[k] = ex2((mn - phk[k]) * itl); Zu += u[k]; }
+    const float iZu = rcpa(Zu);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) u[k] *= iZu;
+  }
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    float v = 0.f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      if (k < nr) v = fmaf(u[k] * wsq[k], g5[k][q], v);
+    emit(q, scale * v);
+  }
+  for (int j = 0; j < np; ++j) {
+    const float* nv = X.pl0[j];
+    float dn[3] = {0.f, 0.f, 0.f}, dh = 0.f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (k >= nr) break;
+      const float c = u[k] * wpl[k][j];
+      const float ny = nv[0] * yk[k][0] + nv[1] * yk[k][1] + nv[2] * yk[k][2];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) dn[i] = fmaf(c, yk[k][i] - ny * nv[i], dn[i]);
+      dh += c;
+    }
+    emit(5 + 4 * j, scale * dn[0]); emit(6 + 4 * j, scale * dn[1]); emit(7 + 4 * j, scale * dn[2]);
+    emit(8 + 4 * j, scale * dh);
+  }
+}
 
 // parameters of leaf li at the shape-frame point x, scaled by d phi_shape /
 // d phi_leaf; emit(k, value) is called for k = 0 .. count-1
@@ -222,6 +312,10 @@ __device__ __forceinline__ void leaf_param_grad(const SceneDev& S, int li, const
 #pragma unroll
   for (int i = 0; i < 9; ++i) R[i] = L.R[i];
   to_local(R, t, x, y);
+  if (L.kind == LK_XPSQ) {
+    xpsq_param_grad(S, S.xpsq[L.xidx], y, scale, emit);
+    return;
+  }
   if (L.kind == LK_HALFSPACE) {   // phi = n.y + h
     emit(0, scale * y[0]); emit(1, scale * y[1]); emit(2, scale * y[2]); emit(3, scale);
     return;
@@ -256,11 +350,12 @@ __device__ __forceinline__ void leaf_param_grad(const SceneDev& S, int li, const
   }
 }
 
-__device__ __forceinline__ int leaf_param_count(const Leaf& L) {
-  return L.kind == LK_HALFSPACE ? 4 : 5 + 4 * L.n_planes;
+__device__ __forceinline__ int leaf_param_count(const SceneDev& S, const Leaf& L) {
+  return L.kind == LK_HALFSPACE ? 4 : 5 + 4 * (L.kind == LK_XPSQ ? S.xpsq[L.xidx].n_planes : L.n_planes);
 }
 
-// one thread per point; shapes are single leaves or flat booleans (class 0).
+// one thread per point; shapes are single leaves or flat booleans (SQ family
+// or constant-schedule XPSQ leaves).
 // J[k * N + n]; vjp[poff[shape] + k] += w[n] J[k, n] (warp-reduced when the
 // warp's points share one shape, else per-lane atomics)
 __global__ void __launch_bounds__(256) k_sdf_param_grad(SceneDev S, const int32_t* __restrict__ shape_ids,
@@ -311,7 +406,7 @@ __global__ void __launch_bounds__(256) k_sdf_param_grad(SceneDev S, const int32_
     const Instr* prog = S.prog + sh.prog_begin;
     if (sh.prog_len == 1) {
       leaf_param_grad(S, prog[0].idx, y, 1.f, emit);
-      kbase += leaf_param_count(S.leaves[prog[0].idx]);
+      kbase += leaf_param_count(S, S.leaves[prog[0].idx]);
     } else {
       // flat boolean: phi = s_out tau log sum exp(s_i phi_i / tau);
       // d phi / d phi_i = s_out s_i softmax_i (pass 1: the accumulator)
@@ -321,7 +416,7 @@ __global__ void __launch_bounds__(256) k_sdf_param_grad(SceneDev S, const int32_
         const Instr in = prog[pc];
         if (in.op != OP_LEAF) { so = in.out_sign; continue; }
         Res<0> r;
-        leaf_eval<0, 0, false>(S, in.idx, y, r);
+        leaf_eval<0, 1, false>(S, in.idx, y, r);
         const float v = in.child_sign * r.v;
         if (v > mx) { Z = fmaf(Z, ex2((mx - v) * itl), 1.f); mx = v; }
         else Z += ex2((v - mx) * itl);
@@ -331,10 +426,10 @@ __global__ void __launch_bounds__(256) k_sdf_param_grad(SceneDev S, const int32_
         const Instr in = prog[pc];
         if (in.op != OP_LEAF) continue;
         Res<0> r;
-        leaf_eval<0, 0, false>(S, in.idx, y, r);
+        leaf_eval<0, 1, false>(S, in.idx, y, r);
         const float sc = so * in.child_sign * ex2((in.child_sign * r.v - mx) * itl) * iZ;
         leaf_param_grad(S, in.idx, y, sc, emit);
-        kbase += leaf_param_count(S.leaves[in.idx]);
+        kbase += leaf_param_count(S, S.leaves[in.idx]);
       }
     }
     if (J)

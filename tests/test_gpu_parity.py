@@ -365,14 +365,20 @@ def _param_scene():
         synth.make_shape("int", synth.op("intersection", [synth.sq(a(), e()), synth.halfspace(rng.normal(size=3), 0.01)]), None),
         synth.make_shape("sub", synth.op("subtraction", [synth.psq(a(), e(), [[*rng.normal(size=3), -0.01]]),
                                                          synth.sq(a() * 0.5, e(), pose=pose())]), None),
+        synth.make_shape("xpsq", synth.xpsq([-0.05, 0, 0, 0.0, 0.06, 0.01, 0.05, 0, 0.004], (0.012, 0.015, 0.01),
+                                            (0.6, 0.8), planes0=[[0.2, 0.3, 0.93, -0.005]]), None),
+        synth.make_shape("uxp", synth.op("union", [synth.sq(a(), e()),
+                                                   synth.xpsq([-0.05, 0, 0, 0.0, 0.05, 0.0, 0.05, 0, 0.0],
+                                                              (0.01, 0.012, 0.01), (0.5, 0.9), pose=pose())]), None),
     ]
     return shapes, rng
 
 
 def test_sdf_param_grad_parity(cuda, oracle_mod):
     """Shape-parameter derivatives: per-point J of every
-    parametrised leaf kind and flat boolean against the oracle's parameter
-    seeds, and the vector-Jacobian product sum_n w_n J_n against J^T w."""
+    parametrised leaf kind (half-space, SQ, PSQ, constant-schedule XPSQ) and
+    flat boolean against the oracle's parameter seeds, and the vector-Jacobian
+    product sum_n w_n J_n against J^T w."""
     import torch
     from paper_2604_17538_b200 import binding
     shapes, rng = _param_scene()
@@ -381,7 +387,7 @@ def test_sdf_param_grad_parity(cuda, oracle_mod):
     counts, offs = S.param_layout()
     osc = oracle_mod.OracleScene(sc)
     assert [osc.param_count(s) for s in range(len(shapes))] == list(counts)
-    B, P = 24, 96
+    B, P = 32, 96
     ids = np.repeat(np.arange(len(shapes)), B // len(shapes)).astype(np.int32)
     poses = np.stack([synth.pose_row(rng.uniform(-0.1, 0.1, 3), synth.random_quats(rng, 1)[0]) for _ in range(B)])
     poses = poses.astype(np.float32)
@@ -411,7 +417,8 @@ def test_sdf_param_grad_parity(cuda, oracle_mod):
 
 
 def test_sdf_param_grad_unsupported(cuda):
-    """Scenes holding an XPSQ report count -1 and the call is refused."""
+    """Scenes holding a shape with nested booleans (the cup) report count -1
+    and the call is refused."""
     import torch
     from paper_2604_17538_b200 import binding
     sc = scene_of([synth.make_shape("cup", synth.cup(), None)], ell=0.04)
