@@ -286,15 +286,19 @@ struct MfArgs {
   float* scratch;            // chunk scratch, one slot of `slot` floats per unit
   int64_t slot;
   uint32_t mode;
+  struct UnitCtx* ctx;       // per-unit set-up of the chunk (k_mf_units)
 };
 
-struct UnitCtx {
+struct alignas(16) UnitCtx {
   PairFrame F;
   ShapeRec SA, SB;
   int64_t off;               // first output row of this unit
   int side;
-  int valid;
+  int valid;                 // the unit has a manifold (SDF side and a surface)
+  int cls;                   // SDF class of the unit's SDF shape
+  int pad[3];
 };
+static_assert(sizeof(UnitCtx) % 16 == 0, "UnitCtx is copied as float4");
 
 // threads per unit CTA: 64 for large batches (lane use on V = 56..98 meshes);
 // small batches get up to CM_MF_MAX_THREADS so the SMs still fill
@@ -354,44 +358,63 @@ template <int TIER, int XP> struct RegCap {
 #define CM_MF_FACE_MINB 2   // face kernel: <= 128 registers
 #endif
 
-// Thread 0 resolves the unit (pair, side), its shapes, frame and output
-// offset into shared memory; returns false (uniformly) when another launch
-// owns the unit's SDF class or the unit has no manifold.
-__device__ __forceinline__ bool unit_setup(const MfArgs& a, UnitCtx& U) {
-  if (threadIdx.x == 0) {
-    const bool full = (a.mode & CM_FULL_MODE) != 0;
-    const bool two = (a.mode & CM_TWO_SIDED) != 0;
-    const int64_t un = a.unit0 + blockIdx.x;
-    const int64_t pi = two ? un >> 1 : un;
-    const int side = two ? (int)(un & 1) : 0;          // 1: B sampled against A's SDF
-    const int32_t* pr = a.pairs + 5 * pi;
-    const int env = __ldg(pr + 0);
-    const int slA = __ldg(pr + 1 + side), slB = __ldg(pr + 2 - side);
-    const int shA = __ldg(pr + 3 + side), shB = __ldg(pr + 4 - side);
-    const ShapeRec sa = a.S.shapes[shA];
-    const ShapeRec sb = a.S.shapes[shB];
-    int ok = (a.xp_filter < 0 || sb.uses_xpsq == a.xp_filter) && sb.has_sdf && sa.F > 0;
-    if (ok) {
-      float pa[8], pb[8];
-      const float* A = a.poses + 8 * ((int64_t)env * a.n_slot + slA);
-      const float* B = a.poses + 8 * ((int64_t)env * a.n_slot + slB);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) { pa[i] = __ldg(A + i); pb[i] = __ldg(B + i); }
-      pair_frame(pa, pb, U.F);
-      U.SA = sa;
-      U.SB = sb;
-      int64_t o = __ldg(a.offsets + pi);
-      if (side) {
-        const ShapeRec s0 = a.S.shapes[__ldg(pr + 3)];
-        o += full ? (int64_t)s0.V + s0.E : (int64_t)s0.F;
-      }
-      U.off = o;
-      U.side = side;
+// the set-up of unit un: pair, side, shapes, frame and first output row
+__device__ __forceinline__ void unit_resolve(const MfArgs& a, int64_t un, UnitCtx& U) {
+  const bool full = (a.mode & CM_FULL_MODE) != 0;
+  const bool two = (a.mode & CM_TWO_SIDED) != 0;
+  const int64_t pi = two ? un >> 1 : un;
+  const int side = two ? (int)(un & 1) : 0;          // 1: B sampled against A's SDF
+  const int32_t* pr = a.pairs + 5 * pi;
+  const int env = __ldg(pr + 0);
+  const int slA = __ldg(pr + 1 + side), slB = __ldg(pr + 2 - side);
+  const int shA = __ldg(pr + 3 + side), shB = __ldg(pr + 4 - side);
+  const ShapeRec sa = a.S.shapes[shA];
+  const ShapeRec sb = a.S.shapes[shB];
+  const int ok = sb.has_sdf && sa.F > 0;
+  if (ok) {
+    const float4* A = reinterpret_cast<const float4*>(a.poses + 8 * ((int64_t)env * a.n_slot + slA));
+    const float4* B = reinterpret_cast<const float4*>(a.poses + 8 * ((int64_t)env * a.n_slot + slB));
+    const float4 a0 = __ldg(A), a1 = __ldg(A + 1), b0 = __ldg(B), b1 = __ldg(B + 1);
+    const float pa[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    const float pb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    pair_frame(pa, pb, U.F);
+    U.SA = sa;
+    U.SB = sb;
+    int64_t o = __ldg(a.offsets + pi);
+    if (side) {
+      const ShapeRec s0 = a.S.shapes[__ldg(pr + 3)];
+      o += full ? (int64_t)s0.V + s0.E : (int64_t)s0.F;
     }
-    U.valid = ok;
+    U.off = o;
+    U.side = side;
   }
+  U.valid = ok;
+  U.cls = sb.uses_xpsq;
+}
+
+// per-chunk prologue: one thread per unit resolves its set-up once for the
+// chunk's kernels (they copy it with 128-bit loads instead of each
+// re-deriving it through dependent loads on one thread)
+__global__ void __launch_bounds__(128) k_mf_units(const MfArgs a, int64_t nb) {
+  const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= nb) return;
+  UnitCtx U;
+  unit_resolve(a, a.unit0 + u, U);
+  float4* dst = reinterpret_cast<float4*>(a.ctx + u);
+  const float4* src = reinterpret_cast<const float4*>(&U);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(UnitCtx) / 16); ++i) dst[i] = src[i];
+}
+
+// every kernel: the CTA's unit set-up copied from the chunk's records;
+// false (uniformly) when another launch owns the unit's SDF class or the unit
+// has no manifold
+__device__ __forceinline__ bool unit_setup(const MfArgs& a, UnitCtx& U) {
+  constexpr int n4 = (int)(sizeof(UnitCtx) / 16);
+  const float4* src = reinterpret_cast<const float4*>(a.ctx + blockIdx.x);
+  for (int i = threadIdx.x; i < n4; i += blockDim.x) reinterpret_cast<float4*>(&U)[i] = __ldg(src + i);
   __syncthreads();
-  return U.valid != 0;
+  return U.valid != 0 && (a.xp_filter < 0 || U.cls == a.xp_filter);
 }
 
 // CLS: SDF class (cm_internal.h ShapeRec); XPM: XPSQ mode of leaf_eval
@@ -1070,6 +1093,7 @@ static int launch_tier(MfArgs a, int class_mask, int max_V, int max_E, int64_t n
   const bool full = (a.mode & CM_FULL_MODE) != 0;
   const bool multi = (class_mask & (class_mask - 1)) != 0;
   float* scratch0 = a.scratch;
+  UnitCtx* ctx0 = a.ctx;
   // face-kernel staging in shared memory when the largest unit fits; used
   // for small staged footprints and for chunks too small to fill the SMs
   // anyway (measured: C4 / C2 gain 3-25%, C5 / C3 lose 8-10% to the lower
@@ -1094,6 +1118,9 @@ static int launch_tier(MfArgs a, int class_mask, int max_V, int max_E, int64_t n
     cudaStream_t st = streams[k % n_streams];
     a.unit0 = u0;
     a.scratch = scratch0 + (k % n_streams) * chunk * a.slot;
+    a.ctx = ctx0 + (k % n_streams) * chunk;
+    k_mf_units<<<(unsigned)((nb + 127) / 128), 128, 0, st>>>(a, nb);
+    if (int rcu = check_launch("k_mf_units")) return rcu;
     // >= 32 resident warps per SM over the chunk's units (small batches)
     int T = CM_MF_THREADS;
     while (T < CM_MF_MAX_THREADS && nb * (T / 32) < (int64_t)num_sms() * 32) T *= 2;
@@ -1127,7 +1154,10 @@ int launch_manifold(const SceneDev& s, int class_mask, int max_V, int max_E, con
   const int64_t n_units = (mode & CM_TWO_SIDED) ? 2 * n_pairs : n_pairs;
   const int64_t slot = manifold_slot_floats(max_V, max_E, tier);
   if (n_streams < 1) n_streams = 1;
-  int64_t chunk = slot > 0 ? scratch_floats / n_streams / slot : 0;
+  // each unit of a chunk: its candidate slot and its set-up record (after
+  // all slots; slots are multiples of 4 floats so the records stay aligned)
+  const int64_t ctxf = (int64_t)(sizeof(UnitCtx) / 4);
+  int64_t chunk = slot > 0 ? scratch_floats / n_streams / (slot + ctxf) : 0;
   if (scratch == nullptr || chunk < 1) {
     set_error("manifold: scene scratch missing or too small");
     return CM_ERR_UNSUPPORTED;
@@ -1147,6 +1177,7 @@ int launch_manifold(const SceneDev& s, int class_mask, int max_V, int max_E, con
   a.scratch = scratch;
   a.slot = slot;
   a.mode = mode;
+  a.ctx = reinterpret_cast<UnitCtx*>(scratch + (int64_t)n_streams * chunk * slot);
   cudaStream_t const* sts = (cudaStream_t const*)streams;
   if (tier >= 3) return launch_tier<3>(a, class_mask, max_V, max_E, n_units, chunk, sts, n_streams);
   if (tier == 2) return launch_tier<2>(a, class_mask, max_V, max_E, n_units, chunk, sts, n_streams);
