@@ -94,7 +94,7 @@ struct SceneDev {
 // manifold chunk scratch: the units of one chunk keep their candidate state
 // in a global slot each; the scene allocates kChunkUnits slots (capped at
 // kScratchCapBytes) at creation (CM_CHUNK_UNITS overrides the unit count)
-constexpr int64_t kChunkUnits = 24576;
+constexpr int64_t kChunkUnits = 32768;
 constexpr int kManifoldStreams = 2;     // chunks alternate between the scene's aux streams
 constexpr int64_t kScratchCapBytes = 1024ll << 20;
 
