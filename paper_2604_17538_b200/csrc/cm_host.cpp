@@ -416,10 +416,13 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
         fe[std::get<2>(keys[i])] = E - 1;
       }
       r.V = V; r.E = E; r.F = F;
-      r.v_off = (int32_t)(verts.size() / 3);
+      r.v_off = (int32_t)(verts.size() / 4);
       r.e_off = (int32_t)(edges_all.size() / 2);
       r.f_off = (int32_t)(faces_all.size() / 3);
-      verts.insert(verts.end(), d.vertices, d.vertices + 3 * V);
+      for (int v = 0; v < V; ++v) {   // padded to 16 B: one 128-bit load per vertex
+        verts.insert(verts.end(), d.vertices + 3 * v, d.vertices + 3 * v + 3);
+        verts.push_back(0.f);
+      }
       edges_all.insert(edges_all.end(), eg.begin(), eg.end());
       for (int k = 0; k < E; ++k) {
         const float* xa = d.vertices + 3 * eg[2 * k];

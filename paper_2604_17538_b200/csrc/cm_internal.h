@@ -82,7 +82,7 @@ struct SceneDev {
   const Leaf* leaves;
   const Xpsq* xpsq;
   const ShapeRec* shapes;
-  const float* verts;
+  const float* verts;         // sampled-surface vertices, 4 floats each (x, y, z, 0)
   const int32_t* edges;
   const float* edge_geom;     // per edge 8 floats: x_I[3], L, e_t[3] (unit, local), 0
   const int32_t* faces;

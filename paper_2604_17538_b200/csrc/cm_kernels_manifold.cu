@@ -445,8 +445,12 @@ __device__ __forceinline__ void to_frames(const PairFrame& F, const float* x, fl
     pw[i] = F.RA[i * 3] * x[0] + F.RA[i * 3 + 1] * x[1] + F.RA[i * 3 + 2] * x[2] + F.tA[i];
   }
 }
+__device__ __forceinline__ float4 ldv(const float* lv, int v) {   // padded vertex
+  return __ldg(reinterpret_cast<const float4*>(lv) + v);
+}
 __device__ __forceinline__ void vertex_frames(const PairFrame& F, const float* lv, int v, float* xb, float* pw) {
-  const float x[3] = {__ldg(lv + 3 * v), __ldg(lv + 3 * v + 1), __ldg(lv + 3 * v + 2)};
+  const float4 x4 = ldv(lv, v);
+  const float x[3] = {x4.x, x4.y, x4.z};
   to_frames(F, x, xb, pw);
 }
 
@@ -459,7 +463,7 @@ __global__ void __maxnreg__((RegCap<TIER, XP>::VERTICES)) k_mf_vertices(const Mf
   const PairFrame& F = U.F;
   const int V = U.SA.V;
   float* sv = a.scratch + (int64_t)blockIdx.x * a.slot;
-  const float* lv = a.S.verts + 3 * (int64_t)U.SA.v_off;
+  const float* lv = a.S.verts + 4 * (int64_t)U.SA.v_off;
   const bool full = (a.mode & CM_FULL_MODE) != 0;
   const float itcmp = a.S.sp.i_cmp;
   for (int v = threadIdx.x; v < V; v += blockDim.x) {
@@ -504,7 +508,7 @@ __global__ void __maxnreg__((RegCap<TIER, XP>::TRACES)) k_mf_traces(const MfArgs
   const int V = U.SA.V, E = U.SA.E;
   const float* sv = a.scratch + (int64_t)blockIdx.x * a.slot;
   float* se = a.scratch + (int64_t)blockIdx.x * a.slot + (int64_t)vrec(TIER) * V;
-  const float* lv = a.S.verts + 3 * (int64_t)U.SA.v_off;
+  const float* lv = a.S.verts + 4 * (int64_t)U.SA.v_off;
   const int32_t* ed = a.S.edges + 2 * (int64_t)U.SA.e_off;
   for (int j = threadIdx.x; j < 2 * E; j += blockDim.x) {
     const int e = j < E ? j : j - E;
@@ -516,12 +520,12 @@ __global__ void __maxnreg__((RegCap<TIER, XP>::TRACES)) k_mf_traces(const MfArgs
     float xl[3], el[3], L;
     {
       const int vI = __ldg(ed + 2 * e), vII = __ldg(ed + 2 * e + 1);
-      const float dl[3] = {__ldg(lv + 3 * vII) - __ldg(lv + 3 * vI), __ldg(lv + 3 * vII + 1) - __ldg(lv + 3 * vI + 1),
-                           __ldg(lv + 3 * vII + 2) - __ldg(lv + 3 * vI + 2)};
+      const float4 xa = ldv(lv, vI), xb4 = ldv(lv, vII);
+      const float dl[3] = {xb4.x - xa.x, xb4.y - xa.y, xb4.z - xa.z};
       L = sqrtf(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
       const float iL = 1.f / L;
       el[0] = dl[0] * iL; el[1] = dl[1] * iL; el[2] = dl[2] * iL;
-      xl[0] = __ldg(lv + 3 * vI); xl[1] = __ldg(lv + 3 * vI + 1); xl[2] = __ldg(lv + 3 * vI + 2);
+      xl[0] = xa.x; xl[1] = xa.y; xl[2] = xa.z;
     }
     float eb[3], ew[3];
     rot_vec(F.Rrel, el, eb);
@@ -765,7 +769,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, TIER >= 3 ? 1 : CM_MF_FACE_
   constexpr int VR = vrec(TIER), ER = erec(TIER);
   const float* gv = a.scratch + (int64_t)blockIdx.x * a.slot;
   const float* ge = gv + (int64_t)VR * V;
-  const float* lv = a.S.verts + 3 * (int64_t)U.SA.v_off;
+  const float* lv = a.S.verts + 4 * (int64_t)U.SA.v_off;
   const float* eg = a.S.edge_geom + 8 * (int64_t)U.SA.e_off;
   const int32_t* fv = a.S.faces + 3 * (int64_t)U.SA.f_off;
   const int32_t* fe = a.S.face_edges + 3 * (int64_t)U.SA.f_off;
