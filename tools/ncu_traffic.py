@@ -3,6 +3,7 @@
 bytes of the whole chunk -> JSON (profiles/<round>_traffic_c5.json)."""
 import csv, json, subprocess, sys
 rep, out = sys.argv[1], sys.argv[2]
+workload = sys.argv[3] if len(sys.argv) > 3 else "C5"
 txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout.splitlines()
 rows = list(csv.reader(txt))
 h, units = rows[0], rows[1]
@@ -21,11 +22,11 @@ tot = sum(k["dram_read_bytes"] + k["dram_write_bytes"] for k in ks)
 tns = sum(k["ns"] for k in ks)
 for k in ks:
     k["share_of_chunk_time"] = k["ns"] / tns
-res = {"workload": "C5", "pairs": grid, "dram_read_bytes": sum(k["dram_read_bytes"] for k in ks),
+res = {"workload": workload, "pairs": grid, "dram_read_bytes": sum(k["dram_read_bytes"] for k in ks),
        "dram_write_bytes": sum(k["dram_write_bytes"] for k in ks), "bytes_per_pair": tot / grid,
        "kernels": ks,
-       "source": "%s (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum over the 7 k_mf_* kernels of "
-                 "the first %d-pair chunk of a 65536-env C5 shard; serialised, cold-cache replays)" % (rep, grid)}
+       "source": "%s (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum over the k_mf_* kernels of "
+                 "the first %d-unit chunk of a %s shard; serialised, cold-cache replays)" % (rep, grid, workload)}
 json.dump(res, open(out, "w"), indent=1)
 print(json.dumps({k: v for k, v in res.items() if k != "kernels"}, indent=1))
 for k in ks:
