@@ -23,6 +23,9 @@ using namespace cmi;
 #ifndef CM_XPSQ_NOINLINE
 #define CM_XPSQ_NOINLINE 1
 #endif
+#ifndef CM_XPSQ_CULL
+#define CM_XPSQ_CULL 1   // skip XPSQ union operands with provably negligible weight (eval_shape)
+#endif
 #ifndef CM_XPSQ_INLINE_MAX_O
 #define CM_XPSQ_INLINE_MAX_O 2   // constant-schedule XPSQ inlined up to this order
 #endif
@@ -1113,13 +1116,24 @@ __device__ __forceinline__ void fold_level(Acc<O>& a0, Acc<O>& a1, Acc<O>& a2, i
 // phi, grad, hess of shape `sh` at the body-frame point x
 // FLAT: every boolean node of the shape sits at the root (nesting depth <= 1),
 // so one accumulator level suffices (fewer live registers)
-template <int O, int XP, bool FLAT = false, bool XINL = true>
+template <int O, int XP, bool FLAT, bool XINL, bool CULL>
+__device__ __forceinline__ void eval_prog(const SceneDev& S, const ShapeRec& sh, const float* x, Res<O>& out);
+
+// SINGLE: the shape is one leaf (no program loop compiled); CULL: XPSQ union
+// operands with provably negligible weight are skipped (class-4 shapes only:
+// the check costs the other XPSQ kernels registers)
+template <int O, int XP, bool FLAT = false, bool XINL = true, bool CULL = false, bool SINGLE = false>
 __device__ CM_SINL void eval_shape(const SceneDev& S, const ShapeRec& sh, const float* x, Res<O>& out) {
-  const float tau = S.sp.tau_min, itau = S.sp.i_min, itl = LOG2E * itau;
-  if (sh.prog_len == 1) {  // single leaf: no accumulator needed
+  if (SINGLE || sh.prog_len == 1) {  // single leaf: no accumulator needed
     leaf_eval<O, XP, XINL>(S, S.prog[sh.prog_begin].idx, x, out);
     return;
   }
+  if constexpr (!SINGLE) eval_prog<O, XP, FLAT, XINL, CULL>(S, sh, x, out);
+}
+
+template <int O, int XP, bool FLAT, bool XINL, bool CULL>
+__device__ __forceinline__ void eval_prog(const SceneDev& S, const ShapeRec& sh, const float* x, Res<O>& out) {
+  const float tau = S.sp.tau_min, itau = S.sp.i_min, itl = LOG2E * itau;
   Acc<O> a0, a1, a2;
   int lvl = -1;
   const Instr* prog = S.prog + sh.prog_begin;
@@ -1134,6 +1148,20 @@ __device__ CM_SINL void eval_shape(const SceneDev& S, const ShapeRec& sh, const 
     }
     Res<O> r;
     if (in.op == OP_LEAF) {
+      if constexpr (CULL && XP > 0 && CM_XPSQ_CULL) {
+        // an XPSQ operand of a union whose weight is provably below 2^-66
+        // against the operands folded so far adds nothing representable to
+        // the value or its derivatives: skipped (Leaf::cull bound)
+        if (in.child_sign < 0.f) {
+          const float m = (FLAT || lvl == 0) ? a0.m : (lvl == 1 ? a1.m : a2.m);
+          const Leaf& Lc = S.leaves[in.idx];
+          if (m > -INFINITY && Lc.kind == LK_XPSQ) {
+            const float dx = x[0] - Lc.cull[0], dy = x[1] - Lc.cull[1], dz = x[2] - Lc.cull[2];
+            const float lb = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))) - Lc.cull[3];
+            if ((-lb - m) * itl < -66.f) continue;
+          }
+        }
+      }
       leaf_eval<O, XP, XINL>(S, in.idx, x, r);
     } else {
       if (FLAT || lvl == 0) acc_final(a0, in.out_sign, tau, itau, r);

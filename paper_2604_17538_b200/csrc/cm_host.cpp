@@ -327,6 +327,24 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
             L.n_planes = 0;
             L.xidx = (int32_t)xps.size();
             xps.push_back(pack_xpsq(n));
+            {   // culling sphere in the shape frame (see Leaf::cull)
+              double lo[3], hi[3];
+              for (int i = 0; i < 3; ++i) {
+                lo[i] = std::min({(double)n.ctrl[i], (double)n.ctrl[3 + i], (double)n.ctrl[6 + i]});
+                hi[i] = std::max({(double)n.ctrl[i], (double)n.ctrl[3 + i], (double)n.ctrl[6 + i]});
+              }
+              double cl[3], rho = 0.0, amax = 0.0;
+              for (int i = 0; i < 3; ++i) {
+                cl[i] = 0.5 * (lo[i] + hi[i]);
+                rho += 0.25 * (hi[i] - lo[i]) * (hi[i] - lo[i]);
+              }
+              for (int e = 0; e < 2; ++e)
+                amax = std::max(amax, std::sqrt((double)n.a[e][0] * n.a[e][0] + (double)n.a[e][1] * n.a[e][1] +
+                                                (double)n.a[e][2] * n.a[e][2]));
+              for (int i = 0; i < 3; ++i)   // node frame -> shape frame (x = R y + t)
+                L.cull[i] = (float)(fr.R[i * 3 + 0] * cl[0] + fr.R[i * 3 + 1] * cl[1] + fr.R[i * 3 + 2] * cl[2] + fr.t[i]);
+              L.cull[3] = (float)((std::sqrt(rho) + amax + sp->tau_min * std::log(3.0)) * (1.0 + 1e-5) + 1e-7);
+            }
             xclass = std::max(xclass, xps.back().varying ? 2 : 1);
           } else {
             L.kind = LK_SQ;
@@ -359,7 +377,10 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
       id.t[0] = id.t[1] = id.t[2] = 0.0;
       if (!emit(0, 1.f, id, 0)) { delete sc; return fail(CM_ERR_UNSUPPORTED, "shape " + std::to_string(s) + ": " + err); }
       r.has_sdf = 1;
-      r.uses_xpsq = (xclass == 0 && max_depth > 1) ? 3 : xclass;
+      // classes: 0 SQ family (booleans at most one level deep), 3 deeper SQ
+      // family, 1 a lone constant-schedule XPSQ, 4 constant-schedule XPSQ in
+      // a boolean tree, 2 varying-schedule XPSQ
+      r.uses_xpsq = xclass == 0 ? (max_depth > 1 ? 3 : 0) : (xclass == 1 && max_depth >= 1 ? 4 : xclass);
       sc->class_mask |= 1 << r.uses_xpsq;
       // shape-parameter count (f4): leaves in pre-order; varying-schedule
       // XPSQ or nested booleans are not parametrised on the GPU (-1)

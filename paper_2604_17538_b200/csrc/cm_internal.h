@@ -37,6 +37,12 @@ struct Leaf {
   float ia[3];            // 1 / a
   float p1, p2, m, k;     // 1/eps1, 1/eps2, eps2/eps1, eps1/2
   float planes[CM_MAX_PLANES][4];
+  // XPSQ leaves: phi >= |x - cull[0..2]| - cull[3] for x in the shape frame
+  // (the spline lies in its control points' hull: bounding sphere of their
+  // box; |y| - |a|_max bounds the radial SQ distance; PSQ >= SQ; the 3-root
+  // smooth minimum >= min - tau ln 3), used to skip leaves whose union
+  // weight is below 2^-66
+  float cull[4];
 };
 
 // XPSQ static data: p(t) = p1 + B t + A t^2 (A := 0 for the
@@ -62,8 +68,8 @@ struct Xpsq {
 struct ShapeRec {
   int32_t prog_begin, prog_len;
   // SDF class (one kernel instantiation each): 0 SQ family with nesting depth
-  // <= 1, 1 constant-schedule XPSQ, 2 varying-schedule XPSQ, 3 SQ family
-  // with nested booleans
+  // <= 1, 1 a lone constant-schedule XPSQ, 2 varying-schedule XPSQ, 3 SQ
+  // family with nested booleans, 4 constant-schedule XPSQ in a boolean tree
   int32_t has_sdf, uses_xpsq;
   int32_t V, E, F;
   int32_t v_off, e_off, f_off;   // into verts (x3), edges (x2), faces / face_edges (x3)

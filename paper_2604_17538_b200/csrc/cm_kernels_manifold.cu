@@ -335,9 +335,9 @@ static_assert(sizeof(UnitCtx) % 16 == 0, "UnitCtx is copied as float4");
 #endif
 template <int TIER, int XP> struct MinB {
   // tier 3 (second derivatives) carries 45-component arrays: full register file
-  static constexpr int VERTICES = TIER >= 3 ? 1 : (XP == 1 ? CM_MF_MINB_V_XP1 : (XP == 0 ? CM_MF_MINB_V_XP0 : CM_MF_MINB_V));
+  static constexpr int VERTICES = TIER >= 3 ? 1 : ((XP == 1 || XP == 4) ? CM_MF_MINB_V_XP1 : (XP == 0 ? CM_MF_MINB_V_XP0 : CM_MF_MINB_V));
   static constexpr int TRACES = TIER >= 3 ? 1 : (XP == 0 ? CM_MF_MINB_T_XP0 : CM_MF_MINB_T);
-  static constexpr int MIDPOINTS = TIER >= 3 ? 1 : (XP == 1 ? CM_MF_MINB_M_XP1 : (XP == 0 ? CM_MF_MINB_M_XP0 : CM_MF_MINB_M));
+  static constexpr int MIDPOINTS = TIER >= 3 ? 1 : ((XP == 1 || XP == 4) ? CM_MF_MINB_M_XP1 : (XP == 0 ? CM_MF_MINB_M_XP0 : CM_MF_MINB_M));
 };
 // per-thread register caps (__maxnreg__) equivalent to MINB resident
 // 256-thread blocks: 3 -> 80, 2 -> 128, 1 -> 255; CM_MF_REG_XP1 overrides the
@@ -350,9 +350,9 @@ __host__ __device__ constexpr int regs_of(int minb) { return minb >= 3 ? 80 : (m
 #define CM_MF_REG_T_XP1 0
 #endif
 template <int TIER, int XP> struct RegCap {
-  static constexpr int VERTICES = (TIER == 2 && XP == 1 && CM_MF_REG_XP1) ? CM_MF_REG_XP1 : regs_of(MinB<TIER, XP>::VERTICES);
-  static constexpr int TRACES = (TIER == 2 && XP == 1 && CM_MF_REG_T_XP1) ? CM_MF_REG_T_XP1 : regs_of(MinB<TIER, XP>::TRACES);
-  static constexpr int MIDPOINTS = (TIER == 2 && XP == 1 && CM_MF_REG_XP1) ? CM_MF_REG_XP1 : regs_of(MinB<TIER, XP>::MIDPOINTS);
+  static constexpr int VERTICES = (TIER == 2 && (XP == 1 || XP == 4) && CM_MF_REG_XP1) ? CM_MF_REG_XP1 : regs_of(MinB<TIER, XP>::VERTICES);
+  static constexpr int TRACES = (TIER == 2 && (XP == 1 || XP == 4) && CM_MF_REG_T_XP1) ? CM_MF_REG_T_XP1 : regs_of(MinB<TIER, XP>::TRACES);
+  static constexpr int MIDPOINTS = (TIER == 2 && (XP == 1 || XP == 4) && CM_MF_REG_XP1) ? CM_MF_REG_XP1 : regs_of(MinB<TIER, XP>::MIDPOINTS);
 };
 #ifndef CM_MF_FACE_MINB
 #define CM_MF_FACE_MINB 2   // face kernel: <= 128 registers
@@ -419,9 +419,12 @@ __device__ __forceinline__ bool unit_setup(const MfArgs& a, UnitCtx& U) {
 
 // CLS: SDF class (cm_internal.h ShapeRec); XPM: XPSQ mode of leaf_eval
 template <int CLS> struct ClsTraits {
-  static constexpr int XPM = CLS == 3 ? 0 : CLS;
+  static constexpr int XPM = CLS == 3 ? 0 : (CLS == 4 ? 1 : CLS);
   static constexpr bool FLAT = CLS == 0;
+  static constexpr bool CULL = CLS == 4;     // XPSQ operands of boolean trees
+  static constexpr bool SINGLE = CLS == 1;   // a lone constant-schedule XPSQ
 };
+#define CM_EVAL(O, XP) eval_shape<O, ClsTraits<XP>::XPM, ClsTraits<XP>::FLAT, true, ClsTraits<XP>::CULL, ClsTraits<XP>::SINGLE>
 
 // output columns of the (t_A, theta_A, t_B, theta_B) blocks in the pair's own
 // (A, B) order: the transposed side writes its blocks swapped
@@ -470,7 +473,7 @@ __global__ void __maxnreg__((RegCap<TIER, XP>::VERTICES)) k_mf_vertices(const Mf
     float xb[3], pw[3];
     vertex_frames(F, lv, v, xb, pw);
     Res<OV> r;
-    eval_shape<OV, ClsTraits<XP>::XPM, ClsTraits<XP>::FLAT>(a.S, U.SB, xb, r);
+    CM_EVAL(OV, XP)(a.S, U.SB, xb, r);
     float n[3];
     rot_vec(F.RB, r.g, n);
     float* rec = sv + v * vrec(TIER);
@@ -556,7 +559,7 @@ __global__ void __maxnreg__((RegCap<TIER, XP>::TRACES)) k_mf_traces(const MfArgs
       } else {
         const float xb[3] = {fmaf(al, eb[0], xI[0]), fmaf(al, eb[1], xI[1]), fmaf(al, eb[2], xI[2])};
         Res<OT> r;
-        eval_shape<OT, ClsTraits<XP>::XPM, ClsTraits<XP>::FLAT>(a.S, U.SB, xb, r);
+        CM_EVAL(OT, XP)(a.S, U.SB, xb, r);
         phi = r.v;
         if constexpr (TIER >= 2) rot_vec(F.RB, r.g, g);
         if constexpr (TIER >= 3) {
@@ -686,7 +689,7 @@ __global__ void __maxnreg__((RegCap<TIER, XP>::MIDPOINTS)) k_mf_midpoints(const 
       pw[i] = fmaf(ab, ew[i], pI[i]);
     }
     Res<OV> r;
-    eval_shape<OV, ClsTraits<XP>::XPM, ClsTraits<XP>::FLAT>(a.S, U.SB, xb, r);
+    CM_EVAL(OV, XP)(a.S, U.SB, xb, r);
     float n[3];
     rot_vec(F.RB, r.g, n);
     float h[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -1136,6 +1139,7 @@ static int launch_tier(MfArgs a, int class_mask, int max_V, int max_E, int64_t n
     if (!rc && (class_mask & 2)) { a.xp_filter = multi ? 1 : -1; rc = launch_sdf_phases<TIER, 1>(a, nb, T, st); }
     if (!rc && (class_mask & 4)) { a.xp_filter = multi ? 2 : -1; rc = launch_sdf_phases<TIER, 2>(a, nb, T, st); }
     if (!rc && (class_mask & 8)) { a.xp_filter = multi ? 3 : -1; rc = launch_sdf_phases<TIER, 3>(a, nb, T, st); }
+    if (!rc && (class_mask & 16)) { a.xp_filter = multi ? 4 : -1; rc = launch_sdf_phases<TIER, 4>(a, nb, T, st); }
     if (rc) return rc;
     if (!full) {   // the fusion does not depend on the SDF class: one launch
       a.xp_filter = -1;

@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256, CM_SDF_MINB) k_sdf_eval(SceneDev S, const
     float y[3];
     to_local(R, t, x, y);
     Res<O> r;
-    eval_shape<O, XP == 3 ? 0 : XP, XP == 0, false>(S, sh, y, r);
+    eval_shape<O, XP == 3 ? 0 : (XP == 4 ? 1 : XP), XP == 0, false>(S, sh, y, r);
     d[n] = r.v;
     if constexpr (O >= 1) {
       float g[3];
@@ -166,6 +166,9 @@ int launch_sdf_eval(const SceneDev& s, int class_mask, const int32_t* ids, const
   // nested SQ-family shapes: general interpreter, no XPSQ code
   if (!rc && (class_mask & 8))
     rc = dispatch_sdf<3>(s, multi ? 3 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, st);
+  // constant-schedule XPSQ inside boolean trees
+  if (!rc && (class_mask & 16))
+    rc = dispatch_sdf<4>(s, multi ? 4 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, st);
   return rc;
 }
 
