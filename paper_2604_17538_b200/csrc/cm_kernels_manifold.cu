@@ -282,11 +282,14 @@ struct MfArgs {
   int32_t n_slot;
   cm_manifold_out out;
   int64_t C;
-  int32_t xp_filter;         // SDF class handled by this launch (-1: all)
   float* scratch;            // chunk scratch, one slot of `slot` floats per unit
   int64_t slot;
   uint32_t mode;
   struct UnitCtx* ctx;       // per-unit set-up of the chunk (k_mf_units)
+  int* cls_count;            // [CM_N_CLASSES] valid units of the chunk per SDF class
+  int* cls_list;             // [CM_N_CLASSES][chunk] their unit indices
+  int64_t chunk;             // list stride
+  int64_t nb;                // units of this chunk
 };
 
 struct alignas(16) UnitCtx {
@@ -302,6 +305,7 @@ static_assert(sizeof(UnitCtx) % 16 == 0, "UnitCtx is copied as float4");
 
 // threads per unit CTA: 64 for large batches (lane use on V = 56..98 meshes);
 // small batches get up to CM_MF_MAX_THREADS so the SMs still fill
+#define CM_N_CLASSES 5   // SDF classes (cm_internal.h ShapeRec::uses_xpsq)
 #ifndef CM_MF_THREADS
 #define CM_MF_THREADS 64
 #endif
@@ -397,24 +401,42 @@ __device__ __forceinline__ void unit_resolve(const MfArgs& a, int64_t un, UnitCt
 // re-deriving it through dependent loads on one thread)
 __global__ void __launch_bounds__(128) k_mf_units(const MfArgs a, int64_t nb) {
   const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= nb) return;
+  const bool in = u < nb;
   UnitCtx U;
-  unit_resolve(a, a.unit0 + u, U);
+  U.valid = 0;
+  U.cls = -1;
+  if (in) unit_resolve(a, a.unit0 + u, U);
+  // class lists in unit order within the block (ballot ranks + one atomic per
+  // block and class), so neighbouring CTAs of a phase kernel take
+  // neighbouring units
+  __shared__ int s_cnt[CM_N_CLASSES][4], s_base[CM_N_CLASSES];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  int rank = 0;
+#pragma unroll
+  for (int c = 0; c < CM_N_CLASSES; ++c) {
+    const unsigned m = __ballot_sync(0xffffffffu, in && U.valid && U.cls == c);
+    if (lane == 0) s_cnt[c][warp] = __popc(m);
+    if (in && U.valid && U.cls == c) rank = __popc(m & lt);
+  }
+  __syncthreads();
+  if (threadIdx.x < CM_N_CLASSES) {
+    const int c = threadIdx.x;
+    const int tot = s_cnt[c][0] + s_cnt[c][1] + s_cnt[c][2] + s_cnt[c][3];
+    s_base[c] = tot ? atomicAdd(a.cls_count + c, tot) : 0;
+  }
+  __syncthreads();
+  if (!in) return;
+  if (U.valid) {
+    const int c = U.cls;
+    int pre = 0;
+    for (int w = 0; w < warp; ++w) pre += s_cnt[c][w];
+    a.cls_list[(int64_t)c * a.chunk + s_base[c] + pre + rank] = (int)u;
+  }
   float4* dst = reinterpret_cast<float4*>(a.ctx + u);
   const float4* src = reinterpret_cast<const float4*>(&U);
 #pragma unroll
   for (int i = 0; i < (int)(sizeof(UnitCtx) / 16); ++i) dst[i] = src[i];
-}
-
-// every kernel: the CTA's unit set-up copied from the chunk's records;
-// false (uniformly) when another launch owns the unit's SDF class or the unit
-// has no manifold
-__device__ __forceinline__ bool unit_setup(const MfArgs& a, UnitCtx& U) {
-  constexpr int n4 = (int)(sizeof(UnitCtx) / 16);
-  const float4* src = reinterpret_cast<const float4*>(a.ctx + blockIdx.x);
-  for (int i = threadIdx.x; i < n4; i += blockDim.x) reinterpret_cast<float4*>(&U)[i] = __ldg(src + i);
-  __syncthreads();
-  return U.valid != 0 && (a.xp_filter < 0 || U.cls == a.xp_filter);
 }
 
 // CLS: SDF class (cm_internal.h ShapeRec); XPM: XPSQ mode of leaf_eval
@@ -459,13 +481,11 @@ __device__ __forceinline__ void vertex_frames(const PairFrame& F, const float* l
 
 // ---- phase 1: vertices: phi, n (and H) of B ----------------
 template <int TIER, int XP>
-__global__ void __maxnreg__((RegCap<TIER, XP>::VERTICES)) k_mf_vertices(const MfArgs a) {
-  __shared__ UnitCtx U;
-  if (!unit_setup(a, U)) return;
+__device__ __forceinline__ void mf_vertices_unit(const MfArgs& a, const UnitCtx& U, int u) {
   constexpr int OV = TIER >= 2 ? 2 : 1;
   const PairFrame& F = U.F;
   const int V = U.SA.V;
-  float* sv = a.scratch + (int64_t)blockIdx.x * a.slot;
+  float* sv = a.scratch + (int64_t)u * a.slot;
   const float* lv = a.S.verts + 4 * (int64_t)U.SA.v_off;
   const bool full = (a.mode & CM_FULL_MODE) != 0;
   const float itcmp = a.S.sp.i_cmp;
@@ -500,17 +520,15 @@ __global__ void __maxnreg__((RegCap<TIER, XP>::VERTICES)) k_mf_vertices(const Mf
 
 // ---- phase 2: sphere traces (Fig. 2), 2 per edge ----------------
 template <int TIER, int XP>
-__global__ void __maxnreg__((RegCap<TIER, XP>::TRACES)) k_mf_traces(const MfArgs a) {
-  __shared__ UnitCtx U;
-  if (!unit_setup(a, U)) return;
+__device__ __forceinline__ void mf_traces_unit(const MfArgs& a, const UnitCtx& U, int u) {
   constexpr int OT = TIER >= 3 ? 2 : (TIER >= 2 ? 1 : 0);   // order inside the trace
   const SmoothDev sp = a.S.sp;
   const float itcmp = sp.i_cmp;
   const float tca = sp.tau_clip_alpha, itca = sp.i_clip_alpha;
   const PairFrame& F = U.F;
   const int V = U.SA.V, E = U.SA.E;
-  const float* sv = a.scratch + (int64_t)blockIdx.x * a.slot;
-  float* se = a.scratch + (int64_t)blockIdx.x * a.slot + (int64_t)vrec(TIER) * V;
+  const float* sv = a.scratch + (int64_t)u * a.slot;
+  float* se = a.scratch + (int64_t)u * a.slot + (int64_t)vrec(TIER) * V;
   const float* lv = a.S.verts + 4 * (int64_t)U.SA.v_off;
   const int32_t* ed = a.S.edges + 2 * (int64_t)U.SA.e_off;
   for (int j = threadIdx.x; j < 2 * E; j += blockDim.x) {
@@ -641,13 +659,11 @@ __global__ void __maxnreg__((RegCap<TIER, XP>::TRACES)) k_mf_traces(const MfArgs
 
 // ---- phase 3: edge points p_e = v_I + a_bar e_t, a_bar = (a_I + a_II)/2
 template <int TIER, int XP>
-__global__ void __maxnreg__((RegCap<TIER, XP>::MIDPOINTS)) k_mf_midpoints(const MfArgs a) {
-  __shared__ UnitCtx U;
-  if (!unit_setup(a, U)) return;
+__device__ __forceinline__ void mf_midpoints_unit(const MfArgs& a, const UnitCtx& U, int u) {
   constexpr int OV = TIER >= 2 ? 2 : 1;
   const PairFrame& F = U.F;
   const int V = U.SA.V, E = U.SA.E;
-  float* se = a.scratch + (int64_t)blockIdx.x * a.slot + (int64_t)vrec(TIER) * V;
+  float* se = a.scratch + (int64_t)u * a.slot + (int64_t)vrec(TIER) * V;
   const float* eg = a.S.edge_geom + 8 * (int64_t)U.SA.e_off;
   const bool full = (a.mode & CM_FULL_MODE) != 0;
   const float itcmp = a.S.sp.i_cmp;
@@ -758,19 +774,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 }
 
 template <int TIER, bool STAGED>
-__global__ void __launch_bounds__(CM_MF_MAX_THREADS, TIER >= 3 ? 1 : CM_MF_FACE_MINB) k_mf_faces(const MfArgs a) {
-  extern __shared__ __align__(16) float fsm[];
-  __shared__ UnitCtx U;
-  __shared__ uint64_t bar;
-  if (STAGED && threadIdx.x == 0) mbar_init(&bar, 1);   // published by unit_setup's barrier
-  if (!unit_setup(a, U)) return;
+__device__ __forceinline__ void mf_faces_unit(const MfArgs& a, const UnitCtx& U, int u, float* fsm, uint64_t* barp,
+                                              uint32_t phase) {
   const SmoothDev sp = a.S.sp;
   const float itcmp = sp.i_cmp;
   const float tmin = sp.tau_min, itmin = sp.i_min;
   const PairFrame& F = U.F;
   const int V = U.SA.V, E = U.SA.E, NF = U.SA.F;
   constexpr int VR = vrec(TIER), ER = erec(TIER);
-  const float* gv = a.scratch + (int64_t)blockIdx.x * a.slot;
+  const float* gv = a.scratch + (int64_t)u * a.slot;
   const float* ge = gv + (int64_t)VR * V;
   const float* lv = a.S.verts + 4 * (int64_t)U.SA.v_off;
   const float* eg = a.S.edge_geom + 8 * (int64_t)U.SA.e_off;
@@ -784,7 +796,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, TIER >= 3 ? 1 : CM_MF_FACE_
   float* s_pe = nullptr;   // staged edge p_I[3][E], e_t[3][E]
   if constexpr (STAGED) {
     const int used = VR * V + ER * E;
-    if (threadIdx.x == 0) bulk_g2s(fsm, gv, (uint32_t)used * 4u, &bar);
+    if (threadIdx.x == 0) bulk_g2s(fsm, gv, (uint32_t)used * 4u, barp);
     s_pv = fsm + used;
     s_pe = s_pv + 3 * V;
     // overlapped with the copy: the candidates' world geometry
@@ -805,7 +817,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, TIER >= 3 ? 1 : CM_MF_FACE_
         s_pe[(3 + k) * E + e] = ew[k];
       }
     }
-    mbar_wait(&bar, 0);
+    mbar_wait(barp, phase);
     __syncthreads();
     sv = fsm;
     se = fsm + VR * V;
@@ -1073,6 +1085,56 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, TIER >= 3 ? 1 : CM_MF_FACE_
   }
 }
 
+
+// ---- phase kernels ----------------------------------------------------------
+// k_mf_units files every valid unit of the chunk under its SDF class (in unit
+// order); CTA b of a class's phase kernel takes entry b of that list (CTAs
+// past the class's count exit after one broadcast load, without a barrier).
+// A persistent variant (resident CTAs pulling units from an atomic counter)
+// measured slower: C5 -5%, C4 -2%, C2 -10%.
+__device__ __forceinline__ bool list_unit(const MfArgs& a, int list, UnitCtx& U, int& u) {
+  const int b = blockIdx.x;
+  if (list >= 0) {
+    if (b >= __ldcg(a.cls_count + list)) return false;
+    u = __ldcg(a.cls_list + (int64_t)list * a.chunk + b);
+  } else {
+    u = b;
+  }
+  constexpr int n4 = (int)(sizeof(UnitCtx) / 16);
+  const float4* src = reinterpret_cast<const float4*>(a.ctx + u);
+  for (int i = threadIdx.x; i < n4; i += blockDim.x) reinterpret_cast<float4*>(&U)[i] = __ldcg(src + i);
+  __syncthreads();
+  return true;
+}
+
+template <int TIER, int XP>
+__global__ void __maxnreg__((RegCap<TIER, XP>::VERTICES)) k_mf_vertices(const MfArgs a) {
+  __shared__ UnitCtx U;
+  int u;
+  if (list_unit(a, XP, U, u)) mf_vertices_unit<TIER, XP>(a, U, u);
+}
+template <int TIER, int XP>
+__global__ void __maxnreg__((RegCap<TIER, XP>::TRACES)) k_mf_traces(const MfArgs a) {
+  __shared__ UnitCtx U;
+  int u;
+  if (list_unit(a, XP, U, u)) mf_traces_unit<TIER, XP>(a, U, u);
+}
+template <int TIER, int XP>
+__global__ void __maxnreg__((RegCap<TIER, XP>::MIDPOINTS)) k_mf_midpoints(const MfArgs a) {
+  __shared__ UnitCtx U;
+  int u;
+  if (list_unit(a, XP, U, u)) mf_midpoints_unit<TIER, XP>(a, U, u);
+}
+template <int TIER, bool STAGED>
+__global__ void __launch_bounds__(CM_MF_MAX_THREADS, TIER >= 3 ? 1 : CM_MF_FACE_MINB) k_mf_faces(const MfArgs a) {
+  extern __shared__ __align__(16) float fsm[];
+  __shared__ UnitCtx U;
+  __shared__ uint64_t bar;
+  if (STAGED && threadIdx.x == 0) mbar_init(&bar, 1);   // published by list_unit's barrier
+  int u;
+  if (list_unit(a, -1, U, u) && U.valid) mf_faces_unit<TIER, STAGED>(a, U, u, fsm, &bar, 0u);
+}
+
 namespace cml {
 
 // floats of one unit's scratch slot
@@ -1098,9 +1160,10 @@ template <int TIER>
 static int launch_tier(MfArgs a, int class_mask, int max_V, int max_E, int64_t n_units, int64_t chunk,
                        cudaStream_t const* streams, int n_streams) {
   const bool full = (a.mode & CM_FULL_MODE) != 0;
-  const bool multi = (class_mask & (class_mask - 1)) != 0;
   float* scratch0 = a.scratch;
   UnitCtx* ctx0 = a.ctx;
+  int* lists0 = a.cls_list;
+  int* ctrl0 = a.cls_count;   // per stream: [32] counts + counters
   // face-kernel staging in shared memory when the largest unit fits; used
   // for small staged footprints and for chunks too small to fill the SMs
   // anyway (measured: C4 / C2 gain 3-25%, C5 / C3 lose 8-10% to the lower
@@ -1126,23 +1189,30 @@ static int launch_tier(MfArgs a, int class_mask, int max_V, int max_E, int64_t n
     a.unit0 = u0;
     a.scratch = scratch0 + (k % n_streams) * chunk * a.slot;
     a.ctx = ctx0 + (k % n_streams) * chunk;
+    a.cls_count = ctrl0 + 32 * (k % n_streams);
+    a.cls_list = lists0 + (k % n_streams) * chunk * CM_N_CLASSES;
+    a.chunk = chunk;
+    a.nb = nb;
+    if (cudaMemsetAsync(a.cls_count, 0, 32 * sizeof(int), st) != cudaSuccess) {
+      set_error("manifold: counter reset failed");
+      return CM_ERR_CUDA;
+    }
     k_mf_units<<<(unsigned)((nb + 127) / 128), 128, 0, st>>>(a, nb);
     if (int rcu = check_launch("k_mf_units")) return rcu;
     // >= 32 resident warps per SM over the chunk's units (small batches)
     int T = CM_MF_THREADS;
     while (T < CM_MF_MAX_THREADS && nb * (T / 32) < (int64_t)num_sms() * 32) T *= 2;
     int rc = CM_OK;
-    // SDF phases: one instantiation per SDF class present (0 SQ family flat,
-    // 1 constant-schedule XPSQ, 2 varying-schedule XPSQ, 3 nested SQ family);
-    // with several classes each launch skips the other classes' units
-    if (class_mask & 1) { a.xp_filter = multi ? 0 : -1; rc = launch_sdf_phases<TIER, 0>(a, nb, T, st); }
-    if (!rc && (class_mask & 2)) { a.xp_filter = multi ? 1 : -1; rc = launch_sdf_phases<TIER, 1>(a, nb, T, st); }
-    if (!rc && (class_mask & 4)) { a.xp_filter = multi ? 2 : -1; rc = launch_sdf_phases<TIER, 2>(a, nb, T, st); }
-    if (!rc && (class_mask & 8)) { a.xp_filter = multi ? 3 : -1; rc = launch_sdf_phases<TIER, 3>(a, nb, T, st); }
-    if (!rc && (class_mask & 16)) { a.xp_filter = multi ? 4 : -1; rc = launch_sdf_phases<TIER, 4>(a, nb, T, st); }
+    // SDF phases: one instantiation per SDF class present in the scene
+    // (cm_internal.h ShapeRec::uses_xpsq); each takes its class's units from
+    // the list k_mf_units built
+    if (class_mask & 1) rc = launch_sdf_phases<TIER, 0>(a, nb, T, st);
+    if (!rc && (class_mask & 2)) rc = launch_sdf_phases<TIER, 1>(a, nb, T, st);
+    if (!rc && (class_mask & 4)) rc = launch_sdf_phases<TIER, 2>(a, nb, T, st);
+    if (!rc && (class_mask & 8)) rc = launch_sdf_phases<TIER, 3>(a, nb, T, st);
+    if (!rc && (class_mask & 16)) rc = launch_sdf_phases<TIER, 4>(a, nb, T, st);
     if (rc) return rc;
     if (!full) {   // the fusion does not depend on the SDF class: one launch
-      a.xp_filter = -1;
       if (stage_bytes > 0 && (stage_bytes <= kStageSmallBytes || nb < 8 * (int64_t)num_sms()))
         k_mf_faces<TIER, true><<<(unsigned)nb, T, stage_bytes, st>>>(a);
       else
@@ -1164,8 +1234,8 @@ int launch_manifold(const SceneDev& s, int class_mask, int max_V, int max_E, con
   if (n_streams < 1) n_streams = 1;
   // each unit of a chunk: its candidate slot and its set-up record (after
   // all slots; slots are multiples of 4 floats so the records stay aligned)
-  const int64_t ctxf = (int64_t)(sizeof(UnitCtx) / 4);
-  int64_t chunk = slot > 0 ? scratch_floats / n_streams / (slot + ctxf) : 0;
+  const int64_t ctxf = (int64_t)(sizeof(UnitCtx) / 4) + CM_N_CLASSES;   // + the class-list entries
+  int64_t chunk = slot > 0 ? (scratch_floats - 32 * n_streams) / n_streams / (slot + ctxf) : 0;
   if (scratch == nullptr || chunk < 1) {
     set_error("manifold: scene scratch missing or too small");
     return CM_ERR_UNSUPPORTED;
@@ -1181,11 +1251,15 @@ int launch_manifold(const SceneDev& s, int class_mask, int max_V, int max_E, con
   a.n_slot = n_slot;
   a.out = *out;
   a.C = C;
-  a.xp_filter = -1;
   a.scratch = scratch;
   a.slot = slot;
   a.mode = mode;
+  // scratch layout: [slots | unit records | class lists | counters], per stream
   a.ctx = reinterpret_cast<UnitCtx*>(scratch + (int64_t)n_streams * chunk * slot);
+  a.cls_list = reinterpret_cast<int*>(a.ctx + (int64_t)n_streams * chunk);
+  a.cls_count = a.cls_list + (int64_t)n_streams * chunk * CM_N_CLASSES;
+  a.chunk = chunk;
+  a.nb = 0;
   cudaStream_t const* sts = (cudaStream_t const*)streams;
   if (tier >= 3) return launch_tier<3>(a, class_mask, max_V, max_E, n_units, chunk, sts, n_streams);
   if (tier == 2) return launch_tier<2>(a, class_mask, max_V, max_E, n_units, chunk, sts, n_streams);
