@@ -19,9 +19,9 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   --log-file $O/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/ncu_launches.log 2>&1
 fi
 [ -n "${SKIP_FULL:-}" ] && { echo done; exit 0; }
-# the 8 manifold kernels of the first chunk (unit set-up; vertices, traces,
-# midpoints for the two SDF classes of C5; faces), then the same for C4
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_mf_ -c 8 \
+# the 11 manifold kernels of the first chunk (unit set-up; vertices, traces,
+# midpoints for the three SDF classes of C5; faces), then C4's 8 (two classes)
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_mf_ -c 11 \
   -o $O/manifold -f python bench.py --n-env 65536 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $O/ncu_full.log 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_mf_ -c 8 \
   -o $O/manifold_c4 -f python bench.py --workload C4 --n-env 4096 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e \
