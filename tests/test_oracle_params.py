@@ -59,11 +59,11 @@ def _slots(shape):
     return out
 
 
-@pytest.mark.parametrize("kind", ["sq", "psq", "union", "subtraction", "intersection", "xpsq", "cup"])
+@pytest.mark.parametrize("kind", ["sq", "psq", "union", "subtraction", "intersection", "xpsq", "cup", "nest3"])
 def test_param_grad_fd(oracle_mod, kind):
     O = oracle_mod
     rng = np.random.default_rng({"sq": 2, "psq": 3, "union": 4, "subtraction": 5, "intersection": 6, "xpsq": 7,
-                                 "cup": 8}[kind])
+                                 "cup": 8, "nest3": 9}[kind])
     a = lambda: rng.uniform(0.2, 0.4, 3)
     e = lambda: rng.uniform(0.4, 1.4, 2)
     if kind == "xpsq":   # curved spline, constant schedules, one cross-section plane
@@ -71,6 +71,15 @@ def test_param_grad_fd(oracle_mod, kind):
                           planes0=[[0.2, 0.3, 0.93, -0.05]])
     elif kind == "cup":   # nested booleans with an XPSQ handle (ell = 0.04 scale)
         root = synth.cup()
+    elif kind == "nest3":   # SQ-family tree three levels deep, every operator
+        pz = lambda: [*rng.uniform(-0.2, 0.2, 3), *synth.random_quats(rng, 1)[0]]
+        root = synth.op("union", [
+            synth.op("intersection", [synth.sq(a(), e(), pose=pz()),
+                                      synth.op("union", [synth.sq(a(), e(), pose=pz()), synth.sq(a(), e(), pose=pz())],
+                                               pose=pz())]),
+            synth.op("subtraction", [synth.psq(a(), e(), [[*rng.normal(size=3), -0.05]]),
+                                     synth.sq(a() * 0.5, e(), pose=pz())], pose=pz()),
+            synth.halfspace(rng.normal(size=3), -0.3)])
     elif kind == "sq":
         root = synth.sq(a(), e())
     elif kind == "psq":
