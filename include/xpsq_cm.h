@@ -178,8 +178,10 @@ int cm_sdf_eval(const cm_scene* scene, const int32_t* shape_ids, const float* po
  * points are not parameters here); boolean nodes have none (a PSQ's raw plane
  * normal is the parameter: no renormalisation).  counts[s] (host,
  * [n_shapes]) = the count, 0 without an SDF, -1 when the shape holds a
- * varying-schedule XPSQ or booleans nested deeper than one level (not
- * parametrised); offsets (host, [n_shapes + 1]) = prefix sums of
+ * varying-schedule XPSQ, more than 16 boolean nodes, or leaves whose node
+ * indices are not in depth-first (pre-order) order (not parametrised);
+ * booleans nested up to CM_MAX_DEPTH are parametrised (chain rule through
+ * every enclosing LSE, Eqs. (2)-(4)); offsets (host, [n_shapes + 1]) = prefix sums of
  * max(count, 0) (the layout of the vjp vector).  Either may be NULL. */
 int cm_param_layout(const cm_scene* scene, int32_t* counts, int64_t* offsets);
 /* For each point n (layout of cm_sdf_eval): J[k*N + n] = d phi(n) / d param k

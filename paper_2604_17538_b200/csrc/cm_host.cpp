@@ -303,6 +303,7 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
       int max_depth = 0;
       struct Item { int node; float child_sign; Frame parent; int depth; };
       std::string err;
+      std::vector<int> leaf_nodes;   // node index of each emitted leaf (program order)
       std::function<bool(int, float, const Frame&, int)> emit;
       emit = [&](int k, float cs, const Frame& parent, int depth) -> bool {
         const cm_node& n = d.nodes[k];
@@ -357,6 +358,7 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
           }
           prog.push_back(Instr{OP_LEAF, (int32_t)leaves.size(), cs, 1.f});
           leaves.push_back(L);
+          leaf_nodes.push_back(k);
           return true;
         }
         if (depth >= CM_MAX_DEPTH) {
@@ -383,15 +385,20 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
       r.uses_xpsq = xclass == 0 ? (max_depth > 1 ? 3 : 0) : (xclass == 1 && max_depth >= 1 ? 4 : xclass);
       sc->class_mask |= 1 << r.uses_xpsq;
       // shape-parameter count (f4): leaves in pre-order; varying-schedule
-      // XPSQ or nested booleans are not parametrised on the GPU (-1)
-      int pc = 0;
+      // XPSQ, trees of more than kParamMaxNodes boolean nodes or node lists
+      // whose leaves are not in depth-first order are not parametrised (-1)
+      int pc = 0, n_bool = 0;
       for (int k = 0; k < d.n_nodes; ++k) {
         const int ty = d.nodes[k].type;
         if (ty == CM_HALFSPACE) pc += 4;
         else if (ty == CM_SQ) pc += 5;
         else if (ty == CM_PSQ || ty == CM_XPSQ) pc += 5 + 4 * d.nodes[k].n_planes;
+        else ++n_bool;
       }
-      if (r.uses_xpsq == 2 || max_depth > 1) pc = -1;   // varying schedules / nested booleans
+      if (r.uses_xpsq == 2 || n_bool > cmi::kParamMaxNodes) pc = -1;   // varying schedules / large trees
+      // the kernel lays the parameters out in program order: it must be the
+      // node-index order the layout promises (true for pre-order node lists)
+      if (!std::is_sorted(leaf_nodes.begin(), leaf_nodes.end())) pc = -1;
       sc->param_count[s] = pc;
     }
     r.prog_len = (int32_t)prog.size() - r.prog_begin;
@@ -583,7 +590,7 @@ int cm_sdf_param_grad(const cm_scene* sc, const int32_t* ids, const float* poses
   for (size_t s = 0; s < sc->param_count.size(); ++s)
     if (sc->param_count[s] < 0)
       return fail(CM_ERR_UNSUPPORTED, "cm_sdf_param_grad: shape " + std::to_string(s) +
-                                           " holds an XPSQ or nested booleans (not parametrised)");
+                                           " holds a varying-schedule XPSQ or too many boolean nodes (not parametrised)");
   int rc = cml::launch_sdf_param_grad(sc->dev, ids, poses, points, B, P, pmax, J, w, vjp, sc->param_off_dev, stream);
   if (rc) return fail(rc, cml::last_cuda_error());
   return CM_OK;

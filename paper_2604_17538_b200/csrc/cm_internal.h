@@ -104,6 +104,10 @@ constexpr int64_t kChunkUnits = 32768;
 constexpr int kManifoldStreams = 2;     // chunks alternate between the scene's aux streams
 constexpr int64_t kScratchCapBytes = 1024ll << 20;
 
+// shape-parameter derivatives (f4): boolean nodes of one shape the
+// parameter kernel tracks per point (shapes with more report count -1)
+constexpr int kParamMaxNodes = 16;
+
 }  // namespace cmi
 
 // launchers implemented in cm_kernels_*.cu

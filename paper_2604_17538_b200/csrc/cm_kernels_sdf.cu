@@ -357,8 +357,8 @@ __device__ __forceinline__ int leaf_param_count(const SceneDev& S, const Leaf& L
   return L.kind == LK_HALFSPACE ? 4 : 5 + 4 * (L.kind == LK_XPSQ ? S.xpsq[L.xidx].n_planes : L.n_planes);
 }
 
-// one thread per point; shapes are single leaves or flat booleans (SQ family
-// or constant-schedule XPSQ leaves).
+// one thread per point; shapes are single leaves or boolean trees of up to
+// kParamMaxNodes nodes (SQ family or constant-schedule XPSQ leaves).
 // J[k * N + n]; vjp[poff[shape] + k] += w[n] J[k, n] (warp-reduced when the
 // warp's points share one shape, else per-lane atomics)
 __global__ void __launch_bounds__(256) k_sdf_param_grad(SceneDev S, const int32_t* __restrict__ shape_ids,
@@ -411,26 +411,68 @@ __global__ void __launch_bounds__(256) k_sdf_param_grad(SceneDev S, const int32_
       leaf_param_grad(S, prog[0].idx, y, 1.f, emit);
       kbase += leaf_param_count(S, S.leaves[prog[0].idx]);
     } else {
-      // flat boolean: phi = s_out tau log sum exp(s_i phi_i / tau);
-      // d phi / d phi_i = s_out s_i softmax_i (pass 1: the accumulator)
-      const float itl = LOG2E * S.sp.i_min;
-      float mx = -INFINITY, Z = 0.f, so = 1.f;
-      for (int pc = 1; pc < sh.prog_len; ++pc) {
+      // boolean tree (Eqs. (2)-(4), postfix program, nesting <= CM_MAX_DEPTH):
+      // node N: phi_N = s_N tau log sum_c exp(s_c phi_c / tau), so
+      // d phi_N / d phi_c = s_N s_c softmax_N(c) and d phi / d phi_leaf is the
+      // product of these factors over the leaf's ancestors.
+      // Pass 1: every node's accumulator (max m, sum Z), its signs and its
+      // folded value s_c phi_N; pass 2: the factors down the tree, one leaf
+      // parameter block at a time (leaves in program = pre-order).
+      const float tau = S.sp.tau_min, itl = LOG2E * S.sp.i_min;
+      float nm[kParamMaxNodes], nz[kParamMaxNodes], nfv[kParamMaxNodes], nos[kParamMaxNodes], ncs[kParamMaxNodes];
+      int stk[CM_MAX_DEPTH + 1];
+      float am[CM_MAX_DEPTH + 1], az[CM_MAX_DEPTH + 1];
+      int lvl = -1, nn = 0;
+      for (int pc = 0; pc < sh.prog_len; ++pc) {
         const Instr in = prog[pc];
-        if (in.op != OP_LEAF) { so = in.out_sign; continue; }
-        Res<0> r;
-        leaf_eval<0, 1, false>(S, in.idx, y, r);
-        const float v = in.child_sign * r.v;
-        if (v > mx) { Z = fmaf(Z, ex2((mx - v) * itl), 1.f); mx = v; }
-        else Z += ex2((v - mx) * itl);
+        if (in.op == OP_BEGIN) {
+          ++lvl;
+          stk[lvl] = nn++;
+          am[lvl] = -INFINITY;
+          az[lvl] = 0.f;
+          continue;
+        }
+        float v;
+        if (in.op == OP_LEAF) {
+          Res<0> r;
+          leaf_eval<0, 1, false>(S, in.idx, y, r);
+          v = in.child_sign * r.v;
+        } else {   // OP_END: node value from its accumulator, folded into the parent
+          const int k = stk[lvl];
+          nm[k] = am[lvl];
+          nz[k] = az[lvl];
+          nos[k] = in.out_sign;
+          ncs[k] = in.child_sign;
+          v = in.child_sign * (in.out_sign * fmaf(tau * LN2, lg2(az[lvl]), am[lvl]));
+          nfv[k] = v;
+          --lvl;
+        }
+        if (lvl >= 0) {
+          if (v > am[lvl]) { az[lvl] = fmaf(az[lvl], ex2((am[lvl] - v) * itl), 1.f); am[lvl] = v; }
+          else az[lvl] += ex2((v - am[lvl]) * itl);
+        }
       }
-      const float iZ = rcpa(Z);
-      for (int pc = 1; pc < sh.prog_len; ++pc) {
+      float fac[CM_MAX_DEPTH + 1];
+      lvl = -1;
+      nn = 0;
+      for (int pc = 0; pc < sh.prog_len; ++pc) {
         const Instr in = prog[pc];
-        if (in.op != OP_LEAF) continue;
+        if (in.op == OP_BEGIN) {
+          const int k = nn++;
+          if (lvl < 0) {
+            fac[0] = 1.f;
+          } else {   // d phi_parent / d phi_k = s_parent s_k softmax_parent(k)
+            const int p = stk[lvl];
+            fac[lvl + 1] = fac[lvl] * nos[p] * ncs[k] * ex2((nfv[k] - nm[p]) * itl) * rcpa(nz[p]);
+          }
+          stk[++lvl] = k;
+          continue;
+        }
+        if (in.op == OP_END) { --lvl; continue; }
+        const int k = stk[lvl];
         Res<0> r;
         leaf_eval<0, 1, false>(S, in.idx, y, r);
-        const float sc = so * in.child_sign * ex2((in.child_sign * r.v - mx) * itl) * iZ;
+        const float sc = fac[lvl] * nos[k] * in.child_sign * ex2((in.child_sign * r.v - nm[k]) * itl) * rcpa(nz[k]);
         leaf_param_grad(S, in.idx, y, sc, emit);
         kbase += leaf_param_count(S, S.leaves[in.idx]);
       }

@@ -370,14 +370,25 @@ def _param_scene():
         synth.make_shape("uxp", synth.op("union", [synth.sq(a(), e()),
                                                    synth.xpsq([-0.05, 0, 0, 0.0, 0.05, 0.0, 0.05, 0, 0.0],
                                                               (0.01, 0.012, 0.01), (0.5, 0.9), pose=pose())]), None),
+        # nested booleans: the cup (XPSQ handle, depth 2) and an SQ-family
+        # tree three levels deep with every operator
+        synth.make_shape("cup", synth.cup(), None),
+        synth.make_shape("nest", synth.op("union", [
+            synth.op("intersection", [synth.sq(a(), e(), pose=pose()),
+                                      synth.op("union", [synth.sq(a(), e(), pose=pose()),
+                                                         synth.sq(a(), e(), pose=pose())], pose=pose())]),
+            synth.op("subtraction", [synth.psq(a(), e(), [[*rng.normal(size=3), -0.01]]),
+                                     synth.sq(a() * 0.5, e(), pose=pose())], pose=pose()),
+            synth.halfspace(rng.normal(size=3), -0.04)]), None),
     ]
     return shapes, rng
 
 
 def test_sdf_param_grad_parity(cuda, oracle_mod):
     """Shape-parameter derivatives: per-point J of every
-    parametrised leaf kind (half-space, SQ, PSQ, constant-schedule XPSQ) and
-    flat boolean against the oracle's parameter seeds, and the vector-Jacobian
+    parametrised leaf kind (half-space, SQ, PSQ, constant-schedule XPSQ),
+    flat booleans and nested boolean trees (the cup; a three-level SQ-family
+    tree) against the oracle's parameter seeds, and the vector-Jacobian
     product sum_n w_n J_n against J^T w."""
     import torch
     from paper_2604_17538_b200 import binding
@@ -387,7 +398,7 @@ def test_sdf_param_grad_parity(cuda, oracle_mod):
     counts, offs = S.param_layout()
     osc = oracle_mod.OracleScene(sc)
     assert [osc.param_count(s) for s in range(len(shapes))] == list(counts)
-    B, P = 32, 96
+    B, P = 40, 96
     ids = np.repeat(np.arange(len(shapes)), B // len(shapes)).astype(np.int32)
     poses = np.stack([synth.pose_row(rng.uniform(-0.1, 0.1, 3), synth.random_quats(rng, 1)[0]) for _ in range(B)])
     poses = poses.astype(np.float32)
@@ -417,11 +428,14 @@ def test_sdf_param_grad_parity(cuda, oracle_mod):
 
 
 def test_sdf_param_grad_unsupported(cuda):
-    """Scenes holding a shape with nested booleans (the cup) report count -1
-    and the call is refused."""
+    """Scenes holding a varying-schedule XPSQ (not parametrised: its
+    derivatives run through the soft-Cardano roots) report count -1 and the
+    call is refused."""
     import torch
     from paper_2604_17538_b200 import binding
-    sc = scene_of([synth.make_shape("cup", synth.cup(), None)], ell=0.04)
+    vary = synth.xpsq([-0.05, 0, 0, 0.0, 0.06, 0.01, 0.05, 0, 0.004], (0.012, 0.015, 0.01), (0.6, 0.8),
+                      a1=(0.008, 0.01, 0.01), eps1=(0.4, 0.9))
+    sc = scene_of([synth.make_shape("vary", vary, None)], ell=0.04)
     S = binding.Scene(sc.shapes, sc.smooth)
     counts, _ = S.param_layout()
     assert counts[0] == -1
