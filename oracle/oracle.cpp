@@ -407,6 +407,13 @@ template <class T> T lerp(double a, double b, const T& t) { return a + (b - a) *
 
 template <class T> T pval(double v, int node, int slot);
 extern thread_local int g_seed_node;
+// an XPSQ's schedules differ between its endpoints (any of eps, a, planes)
+static bool xpsq_varying(const Node& n) {
+  bool cst = n.eps[0][0] == n.eps[1][0] && n.eps[0][1] == n.eps[1][1];
+  for (int i = 0; i < 3; ++i) cst = cst && n.a[0][i] == n.a[1][i];
+  for (int j = 0; j < n.n_planes; ++j) for (int i = 0; i < 4; ++i) cst = cst && n.pl[0][j][i] == n.pl[1][j][i];
+  return !cst;
+}
 template <class T> T xpsq_phi(const Node& n, const T* y, const Smooth& sp, int idx = -1) {
   T tk[3];
   xpsq_roots(n, y, sp, tk, nullptr, nullptr);
@@ -423,10 +430,14 @@ template <class T> T xpsq_phi(const Node& n, const T* y, const Smooth& sp, int i
     for (int i = 0; i < 3; ++i) yk[i] = R[0 * 3 + i] * dx[0] + R[1 * 3 + i] * dx[1] + R[2 * 3 + i] * dx[2];
     // schedules eps(t), a(t), P(t): linear between endpoint values, plane
     // normals renormalised (Reading #8)
-    // (shape-parameter seeds, f4: one slot moves both endpoint values)
+    // (shape-parameter seeds, f4: with constant schedules one slot moves
+    // both endpoint values; with varying schedules slot s is the t = 0 value
+    // and slot M + s the t = 1 value, M = 5 + 4 n_planes)
+    const int M = 5 + 4 * n.n_planes;
+    const bool vary = xpsq_varying(n);
     auto L2 = [&](double v0, double v1, int slot) {
       if (idx != g_seed_node) return lerp(v0, v1, t);          // (no seed: the literal schedule)
-      const T a0 = pval<T>(v0, idx, slot), a1 = pval<T>(v1, idx, slot);
+      const T a0 = pval<T>(v0, idx, slot), a1 = pval<T>(v1, idx, vary ? M + slot : slot);
       return a0 + (a1 - a0) * t;
     };
     T e1 = L2(n.eps[0][0], n.eps[1][0], 3);
@@ -948,23 +959,22 @@ int ora_contact_manifold(void* s, const int* pairs, long n_pairs, const double* 
 // Parameters of a shape: its nodes in index (pre-order) order, slots per node
 // as for pval above; an XPSQ node with constant schedules has the PSQ slots
 // (each moves both endpoint values; the plane normal is renormalised as in
-// xpsq_phi); varying schedules are not parametrised (the shape reports -1).  J[n * pmax + k] = d phi(point n) / d param k of the point's shape,
-// zero beyond the shape's count; one Dual<double,1> evaluation per parameter.
+// xpsq_phi); with varying schedules the PSQ slots of the t = 0 endpoint, then
+// those of the t = 1 endpoint (the schedules are linear in t, reading #8).
+// J[n * pmax + k] = d phi(point n) / d param k of the point's shape, zero
+// beyond the shape's count; one Dual<double,1> evaluation per parameter.
+static int node_param_count(const Node& n) {
+  if (n.type == K_HALFSPACE) return 4;
+  if (n.type == K_SQ) return 5;
+  if (n.type == K_PSQ) return 5 + 4 * n.n_planes;
+  if (n.type == K_XPSQ) return (xpsq_varying(n) ? 2 : 1) * (5 + 4 * n.n_planes);
+  return 0;
+}
 int ora_shape_param_count(void* s, int shape) {
   Scene* sc = (Scene*)s;
   const Shape& sh = sc->shapes[shape];
   int c = 0;
-  for (const Node& n : sh.nodes) {
-    if (n.type == K_XPSQ) {   // constant schedules only (one value per parameter)
-      bool cst = n.eps[0][0] == n.eps[1][0] && n.eps[0][1] == n.eps[1][1];
-      for (int i = 0; i < 3; ++i) cst = cst && n.a[0][i] == n.a[1][i];
-      for (int j = 0; j < n.n_planes; ++j) for (int i = 0; i < 4; ++i) cst = cst && n.pl[0][j][i] == n.pl[1][j][i];
-      if (!cst) return -1;
-    }
-    if (n.type == K_HALFSPACE) c += 4;
-    else if (n.type == K_SQ) c += 5;
-    else if (n.type == K_PSQ || n.type == K_XPSQ) c += 5 + 4 * n.n_planes;
-  }
+  for (const Node& n : sh.nodes) c += node_param_count(n);
   return c;
 }
 int ora_sdf_param_grad(void* s, const int* shape_ids, const double* poses, const double* points, long B, long P,
@@ -987,7 +997,7 @@ int ora_sdf_param_grad(void* s, const int* shape_ids, const double* poses, const
     int k = 0;
     for (int ni = 0; ni < (int)sh.nodes.size(); ++ni) {
       const Node& nd = sh.nodes[ni];
-      int cnt = nd.type == K_HALFSPACE ? 4 : (nd.type == K_SQ ? 5 : ((nd.type == K_PSQ || nd.type == K_XPSQ) ? 5 + 4 * nd.n_planes : 0));
+      const int cnt = node_param_count(nd);
       for (int slot = 0; slot < cnt && k < pmax; ++slot, ++k) {
         g_seed_node = ni;
         g_seed_slot = slot;

@@ -33,20 +33,39 @@ def test_param_grad_closed_forms(oracle_mod):
     assert np.allclose(J[:, :3], y, atol=1e-12) and np.allclose(J[:, 3], 1.0)
 
 
+def _varying(nd):
+    """An XPSQ whose schedules differ between its endpoints."""
+    if nd["type"] != "xpsq":
+        return False
+    pl0, pl1 = np.asarray(nd["planes"] or []), np.asarray(nd["planes1"] or [])
+    return (not np.array_equal(nd["a"][0], nd["a"][1]) or not np.array_equal(nd["eps"][0], nd["eps"][1])
+            or not np.array_equal(pl0, pl1))
+
+
 def _perturbed(shape, node, slot, h):
+    """The shape with parameter `slot` of node `node` moved by h: both
+    endpoint values (constant schedules), else slot s < M the t = 0 value and
+    slot M + s the t = 1 value (M = 5 + 4 n_planes)."""
     s2 = copy.deepcopy(shape)
     nd = s2.sdf[node]
+    ends = (0, 1)
+    if _varying(nd):
+        M = 5 + 4 * len(nd["planes"])
+        ends = (slot // M,)
+        slot = slot % M
     if nd["type"] == "halfspace" or slot >= 5:
         j, i = (0, slot) if nd["type"] == "halfspace" else ((slot - 5) // 4, (slot - 5) % 4)
-        for key in ("planes", "planes1"):
-            if nd[key] is not None and len(nd[key]):
+        for e, key in enumerate(("planes", "planes1")):
+            if e in ends and nd[key] is not None and len(nd[key]):
                 pl = np.array(nd[key], dtype=np.float64)
                 pl[j, i] += h
                 nd[key] = pl.tolist()
     elif slot < 3:
-        nd["a"] = [np.array(a, dtype=np.float64) + h * (np.arange(3) == slot) for a in nd["a"]]
+        nd["a"] = [np.array(a, dtype=np.float64) + h * (np.arange(3) == slot) * (e in ends)
+                   for e, a in enumerate(nd["a"])]
     else:
-        nd["eps"] = [np.array(e, dtype=np.float64) + h * (np.arange(2) == slot - 3) for e in nd["eps"]]
+        nd["eps"] = [np.array(x, dtype=np.float64) + h * (np.arange(2) == slot - 3) * (e in ends)
+                     for e, x in enumerate(nd["eps"])]
     return s2
 
 
@@ -54,21 +73,26 @@ def _slots(shape):
     out = []
     for ni, nd in enumerate(shape.sdf):
         c = {"halfspace": 4, "sq": 5, "psq": 5 + 4 * len(nd["planes"]),
-             "xpsq": 5 + 4 * len(nd["planes"])}.get(nd["type"], 0)
+             "xpsq": (2 if _varying(nd) else 1) * (5 + 4 * len(nd["planes"]))}.get(nd["type"], 0)
         out += [(ni, s) for s in range(c)]
     return out
 
 
-@pytest.mark.parametrize("kind", ["sq", "psq", "union", "subtraction", "intersection", "xpsq", "cup", "nest3"])
+@pytest.mark.parametrize("kind", ["sq", "psq", "union", "subtraction", "intersection", "xpsq", "cup", "nest3",
+                                  "xpsq_vary"])
 def test_param_grad_fd(oracle_mod, kind):
     O = oracle_mod
     rng = np.random.default_rng({"sq": 2, "psq": 3, "union": 4, "subtraction": 5, "intersection": 6, "xpsq": 7,
-                                 "cup": 8, "nest3": 9}[kind])
+                                 "cup": 8, "nest3": 9, "xpsq_vary": 10}[kind])
     a = lambda: rng.uniform(0.2, 0.4, 3)
     e = lambda: rng.uniform(0.4, 1.4, 2)
     if kind == "xpsq":   # curved spline, constant schedules, one cross-section plane
         root = synth.xpsq([-0.3, 0, 0, 0.0, 0.35, 0.05, 0.3, 0, 0.02], (0.12, 0.15, 0.1), (0.6, 0.8),
                           planes0=[[0.2, 0.3, 0.93, -0.05]])
+    elif kind == "xpsq_vary":   # curved spline, every schedule varying, one plane (normal varies too)
+        root = synth.xpsq([-0.3, 0, 0, 0.0, 0.35, 0.05, 0.3, 0, 0.02], (0.12, 0.15, 0.1), (0.6, 0.8),
+                          a1=(0.08, 0.1, 0.14), eps1=(0.9, 0.5), planes0=[[0.2, 0.3, 0.93, -0.05]],
+                          planes1=[[-0.1, 0.4, 0.9, -0.08]])
     elif kind == "cup":   # nested booleans with an XPSQ handle (ell = 0.04 scale)
         root = synth.cup()
     elif kind == "nest3":   # SQ-family tree three levels deep, every operator
@@ -107,8 +131,10 @@ def test_param_grad_fd(oracle_mod, kind):
         assert np.allclose(J[:, k], fd, rtol=1e-4, atol=2e-5), (kind, ni, sl, np.abs(J[:, k] - fd).max())
 
 
-def test_param_count_varying_xpsq_unsupported(oracle_mod):
+def test_param_count_varying_xpsq(oracle_mod):
+    """A varying-schedule XPSQ has both endpoints' cross-section slots."""
     O = oracle_mod
-    vary = synth.xpsq([-0.3, 0, 0, 0.0, 0.35, 0.05, 0.3, 0, 0.02], (0.12, 0.15, 0.1), (0.6, 0.8), a1=(0.1, 0.1, 0.1))
+    vary = synth.xpsq([-0.3, 0, 0, 0.0, 0.35, 0.05, 0.3, 0, 0.02], (0.12, 0.15, 0.1), (0.6, 0.8), a1=(0.1, 0.1, 0.1),
+                      planes0=[[0.2, 0.3, 0.93, -0.05]])
     osc = O.OracleScene(scene_of([synth.make_shape("v", vary, None)]))
-    assert osc.param_count(0) == -1
+    assert osc.param_count(0) == 2 * (5 + 4)
