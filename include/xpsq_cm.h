@@ -174,12 +174,14 @@ int cm_sdf_eval(const cm_scene* scene, const int32_t* shape_ids, const float* po
  * to cm_scene_create), endpoint-0 values: half-space (n_x, n_y, n_z, h); SQ
  * (a_x, a_y, a_z, eps1, eps2); PSQ as SQ then (n_x, n_y, n_z, h) per plane;
  * XPSQ with constant schedules as PSQ (its cross-section; each parameter
- * moves both endpoint values, normals renormalised as in the XPSQ; control
+ * moves both endpoint values, normals renormalised as in the XPSQ); XPSQ
+ * with varying schedules: the PSQ slots of the t = 0 endpoint, then those of
+ * the t = 1 endpoint (schedules linear in t, P:108 / reading #8; control
  * points are not parameters here); boolean nodes have none (a PSQ's raw plane
  * normal is the parameter: no renormalisation).  counts[s] (host,
- * [n_shapes]) = the count, 0 without an SDF, -1 when the shape holds a
- * varying-schedule XPSQ, more than 16 boolean nodes, or leaves whose node
- * indices are not in depth-first (pre-order) order (not parametrised);
+ * [n_shapes]) = the count, 0 without an SDF, -1 when the shape has more
+ * than 16 boolean nodes, or leaves whose node indices are not in
+ * depth-first (pre-order) order (not parametrised);
  * booleans nested up to CM_MAX_DEPTH are parametrised (chain rule through
  * every enclosing LSE, Eqs. (2)-(4)); offsets (host, [n_shapes + 1]) = prefix sums of
  * max(count, 0) (the layout of the vjp vector).  Either may be NULL. */

@@ -384,18 +384,20 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
       // a boolean tree, 2 varying-schedule XPSQ
       r.uses_xpsq = xclass == 0 ? (max_depth > 1 ? 3 : 0) : (xclass == 1 && max_depth >= 1 ? 4 : xclass);
       sc->class_mask |= 1 << r.uses_xpsq;
-      // shape-parameter count (f4): leaves in pre-order; varying-schedule
-      // XPSQ, trees of more than kParamMaxNodes boolean nodes or node lists
-      // whose leaves are not in depth-first order are not parametrised (-1)
+      // shape-parameter count (f4): leaves in pre-order, a varying-schedule
+      // XPSQ with both endpoints' slots; trees of more than kParamMaxNodes
+      // boolean nodes or node lists whose leaves are not in depth-first
+      // order are not parametrised (-1)
       int pc = 0, n_bool = 0;
       for (int k = 0; k < d.n_nodes; ++k) {
         const int ty = d.nodes[k].type;
         if (ty == CM_HALFSPACE) pc += 4;
         else if (ty == CM_SQ) pc += 5;
-        else if (ty == CM_PSQ || ty == CM_XPSQ) pc += 5 + 4 * d.nodes[k].n_planes;
+        else if (ty == CM_PSQ) pc += 5 + 4 * d.nodes[k].n_planes;
+        else if (ty == CM_XPSQ) pc += (pack_xpsq(d.nodes[k]).varying ? 2 : 1) * (5 + 4 * d.nodes[k].n_planes);
         else ++n_bool;
       }
-      if (r.uses_xpsq == 2 || n_bool > cmi::kParamMaxNodes) pc = -1;   // varying schedules / large trees
+      if (n_bool > cmi::kParamMaxNodes) pc = -1;   // large trees
       // the kernel lays the parameters out in program order: it must be the
       // node-index order the layout promises (true for pre-order node lists)
       if (!std::is_sorted(leaf_nodes.begin(), leaf_nodes.end())) pc = -1;
@@ -590,7 +592,7 @@ int cm_sdf_param_grad(const cm_scene* sc, const int32_t* ids, const float* poses
   for (size_t s = 0; s < sc->param_count.size(); ++s)
     if (sc->param_count[s] < 0)
       return fail(CM_ERR_UNSUPPORTED, "cm_sdf_param_grad: shape " + std::to_string(s) +
-                                           " holds a varying-schedule XPSQ or too many boolean nodes (not parametrised)");
+                                           " has more than 16 boolean nodes or leaves out of depth-first order (not parametrised)");
   int rc = cml::launch_sdf_param_grad(sc->dev, ids, poses, points, B, P, pmax, J, w, vjp, sc->param_off_dev, stream);
   if (rc) return fail(rc, cml::last_cuda_error());
   return CM_OK;

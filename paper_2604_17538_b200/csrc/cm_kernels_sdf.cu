@@ -217,11 +217,17 @@ __device__ __forceinline__ float sq_param_grad(const Leaf& L, const float* y, fl
   return sq_param_grad_p(L.ia, L.p1, L.p2, L.m, L.k, y, o);
 }
 
-// XPSQ with constant schedules (f4): at each projection root t_k (which does
+// XPSQ cross-section parameters (f4): at each projection root t_k (which does
 // not depend on a, eps or the planes) the PSQ of the root's local point y_k;
 // phi = -tau LSE(-phi_k / tau) over the roots (one root when they coincide),
-// so d phi = sum_k u_k d PSQ_k, u = softmax(-phi / tau); the plane normal is
-// renormalised in the XPSQ (reading #8): d/dn = (I - n n^T) y_k w_j
+// so d phi = sum_k u_k d PSQ_k, u = softmax(-phi / tau).  Constant
+// schedules: one slot per cross-section parameter.  Varying schedules
+// (linear in t, reading #8): the cross-section at t_k is (1 - t_k) theta_0 +
+// t_k theta_1, so slot s (the t = 0 value) takes (1 - t_k) and slot M + s
+// (the t = 1 value) takes t_k of root k's derivative, M = 5 + 4 n_planes.
+// Plane normals are renormalised in the XPSQ: n = v / |v| gives
+// d/dv = (I - n n^T) y_k w_j / |v| (|v| = 1 for the constant schedule's
+// unit normal)
 template <class Emit>
 __device__ __forceinline__ void xpsq_param_grad(const SceneDev& S, const Xpsq& X, const float* y, float scale,
                                                 Emit emit) {
@@ -229,8 +235,26 @@ __device__ __forceinline__ void xpsq_param_grad(const SceneDev& S, const Xpsq& X
   float tv[3], tg[3][3], th[3][6];
   const bool single = xpsq_root_t<0>(X, S.sp, w, tv, tg, th);
   const int nr = single ? 1 : 3, np = X.n_planes;
+  const bool vary = X.varying != 0;
   const float itl = LOG2E * S.sp.i_min, tau = S.sp.tau_min;
   float g5[3][5], wsq[3], phk[3], yk[3][3], wpl[3][CM_MAX_PLANES];
+  // the plane j at root parameter t: unit normal n, 1 / |v|, offset h
+  auto plane_at = [&](int j, float t, float* n, float& iv, float& h) {
+    if (vary) {
+      float v[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) v[i] = fmaf(t, X.dpl[j][i], X.pl0[j][i]);
+      iv = rsqrtf(fmaf(v[0], v[0], fmaf(v[1], v[1], v[2] * v[2])));
+#pragma unroll
+      for (int i = 0; i < 3; ++i) n[i] = v[i] * iv;
+      h = fmaf(t, X.dpl[j][3], X.pl0[j][3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) n[i] = X.pl0[j][i];
+      iv = 1.f;
+      h = X.pl0[j][3];
+    }
+  };
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     if (k >= nr) break;
@@ -253,15 +277,29 @@ __device__ __forceinline__ void xpsq_param_grad(const SceneDev& S, const Xpsq& X
     yk[k][0] = T[0] * d[0] + T[1] * d[1] + T[2] * d[2];
     yk[k][1] = N[0] * d[0] + N[1] * d[1] + N[2] * d[2];
     yk[k][2] = bb[0] * d[0] + bb[1] * d[1] + bb[2] * d[2];
-    const float phs = sq_param_grad_p(X.sq_ia, X.sq_p1, X.sq_p2, X.sq_m, X.sq_k, yk[k], g5[k]);
+    float phs;
+    if (vary) {   // the SQ constants of the cross-section at t_k
+      float ia[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) ia[i] = 1.f / fmaf(t, X.da[i], X.a0[i]);
+      const float e1 = fmaf(t, X.deps[0], X.eps0[0]), e2 = fmaf(t, X.deps[1], X.eps0[1]);
+      const float ie1 = 1.f / e1;
+      phs = sq_param_grad_p(ia, ie1, 1.f / e2, e2 * ie1, 0.5f * e1, yk[k], g5[k]);
+    } else {
+      phs = sq_param_grad_p(X.sq_ia, X.sq_p1, X.sq_p2, X.sq_m, X.sq_k, yk[k], g5[k]);
+    }
     float mx = phs;
-    for (int j = 0; j < np; ++j)
-      mx = fmaxf(mx, fmaf(X.pl0[j][0], yk[k][0], fmaf(X.pl0[j][1], yk[k][1], fmaf(X.pl0[j][2], yk[k][2], X.pl0[j][3]))));
+    float pv[CM_MAX_PLANES];
+    for (int j = 0; j < np; ++j) {
+      float n[3], iv, h;
+      plane_at(j, t, n, iv, h);
+      pv[j] = fmaf(n[0], yk[k][0], fmaf(n[1], yk[k][1], fmaf(n[2], yk[k][2], h)));
+      mx = fmaxf(mx, pv[j]);
+    }
     float Z = ex2((phs - mx) * itl);
     wsq[k] = Z;
     for (int j = 0; j < np; ++j) {
-      wpl[k][j] = ex2((fmaf(X.pl0[j][0], yk[k][0], fmaf(X.pl0[j][1], yk[k][1], fmaf(X.pl0[j][2], yk[k][2], X.pl0[j][3]))) -
-                       mx) * itl);
+      wpl[k][j] = ex2((pv[j] - mx) * itl);
       Z += wpl[k][j];
     }
     const float iZ = rcpa(Z);
@@ -279,28 +317,52 @@ __device__ __forceinline__ void xpsq_param_grad(const SceneDev& S, const Xpsq& X
 #pragma unroll
     for (int k = 0; k < 3; ++k) u[k] *= iZu;
   }
+  const int M = 5 + 4 * np;
 #pragma unroll
   for (int q = 0; q < 5; ++q) {
-    float v = 0.f;
+    float v0 = 0.f, v1 = 0.f;
 #pragma unroll
     for (int k = 0; k < 3; ++k)
-      if (k < nr) v = fmaf(u[k] * wsq[k], g5[k][q], v);
-    emit(q, scale * v);
+      if (k < nr) {
+        const float c = u[k] * wsq[k] * g5[k][q];
+        v0 = fmaf(c, 1.f - tv[k], v0);
+        v1 = fmaf(c, tv[k], v1);
+      }
+    if (vary) {
+      emit(q, scale * v0);
+      emit(M + q, scale * v1);
+    } else {
+      emit(q, scale * (v0 + v1));
+    }
   }
   for (int j = 0; j < np; ++j) {
-    const float* nv = X.pl0[j];
-    float dn[3] = {0.f, 0.f, 0.f}, dh = 0.f;
+    float dn0[3] = {0.f, 0.f, 0.f}, dn1[3] = {0.f, 0.f, 0.f}, dh0 = 0.f, dh1 = 0.f;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       if (k >= nr) break;
+      float n[3], iv, h;
+      plane_at(j, tv[k], n, iv, h);
       const float c = u[k] * wpl[k][j];
-      const float ny = nv[0] * yk[k][0] + nv[1] * yk[k][1] + nv[2] * yk[k][2];
+      const float ny = n[0] * yk[k][0] + n[1] * yk[k][1] + n[2] * yk[k][2];
+      const float a1 = tv[k], a0 = 1.f - a1;
 #pragma unroll
-      for (int i = 0; i < 3; ++i) dn[i] = fmaf(c, yk[k][i] - ny * nv[i], dn[i]);
-      dh += c;
+      for (int i = 0; i < 3; ++i) {
+        const float g = c * iv * (yk[k][i] - ny * n[i]);
+        dn0[i] = fmaf(a0, g, dn0[i]);
+        dn1[i] = fmaf(a1, g, dn1[i]);
+      }
+      dh0 = fmaf(a0, c, dh0);
+      dh1 = fmaf(a1, c, dh1);
     }
-    emit(5 + 4 * j, scale * dn[0]); emit(6 + 4 * j, scale * dn[1]); emit(7 + 4 * j, scale * dn[2]);
-    emit(8 + 4 * j, scale * dh);
+    if (vary) {
+      emit(5 + 4 * j, scale * dn0[0]); emit(6 + 4 * j, scale * dn0[1]); emit(7 + 4 * j, scale * dn0[2]);
+      emit(8 + 4 * j, scale * dh0);
+      emit(M + 5 + 4 * j, scale * dn1[0]); emit(M + 6 + 4 * j, scale * dn1[1]); emit(M + 7 + 4 * j, scale * dn1[2]);
+      emit(M + 8 + 4 * j, scale * dh1);
+    } else {
+      emit(5 + 4 * j, scale * (dn0[0] + dn1[0])); emit(6 + 4 * j, scale * (dn0[1] + dn1[1]));
+      emit(7 + 4 * j, scale * (dn0[2] + dn1[2])); emit(8 + 4 * j, scale * (dh0 + dh1));
+    }
   }
 }
 
@@ -354,11 +416,14 @@ __device__ __forceinline__ void leaf_param_grad(const SceneDev& S, int li, const
 }
 
 __device__ __forceinline__ int leaf_param_count(const SceneDev& S, const Leaf& L) {
-  return L.kind == LK_HALFSPACE ? 4 : 5 + 4 * (L.kind == LK_XPSQ ? S.xpsq[L.xidx].n_planes : L.n_planes);
+  if (L.kind == LK_HALFSPACE) return 4;
+  if (L.kind != LK_XPSQ) return 5 + 4 * L.n_planes;
+  const Xpsq& X = S.xpsq[L.xidx];
+  return (X.varying ? 2 : 1) * (5 + 4 * X.n_planes);
 }
 
 // one thread per point; shapes are single leaves or boolean trees of up to
-// kParamMaxNodes nodes (SQ family or constant-schedule XPSQ leaves).
+// kParamMaxNodes nodes (SQ family or XPSQ leaves).
 // J[k * N + n]; vjp[poff[shape] + k] += w[n] J[k, n] (warp-reduced when the
 // warp's points share one shape, else per-lane atomics)
 __global__ void __launch_bounds__(256) k_sdf_param_grad(SceneDev S, const int32_t* __restrict__ shape_ids,
@@ -435,7 +500,7 @@ __global__ void __launch_bounds__(256) k_sdf_param_grad(SceneDev S, const int32_
         float v;
         if (in.op == OP_LEAF) {
           Res<0> r;
-          leaf_eval<0, 1, false>(S, in.idx, y, r);
+          leaf_eval<0, 2, false>(S, in.idx, y, r);
           v = in.child_sign * r.v;
         } else {   // OP_END: node value from its accumulator, folded into the parent
           const int k = stk[lvl];
@@ -471,7 +536,7 @@ __global__ void __launch_bounds__(256) k_sdf_param_grad(SceneDev S, const int32_
         if (in.op == OP_END) { --lvl; continue; }
         const int k = stk[lvl];
         Res<0> r;
-        leaf_eval<0, 1, false>(S, in.idx, y, r);
+        leaf_eval<0, 2, false>(S, in.idx, y, r);
         const float sc = fac[lvl] * nos[k] * in.child_sign * ex2((in.child_sign * r.v - nm[k]) * itl) * rcpa(nz[k]);
         leaf_param_grad(S, in.idx, y, sc, emit);
         kbase += leaf_param_count(S, S.leaves[in.idx]);
