@@ -217,6 +217,17 @@ static int n_aux_streams() {
   return n;
 }
 
+// sdf_eval with several SDF classes runs the class kernels concurrently on
+// the scene's streams (CM_SDF_CONCURRENT=0: in order on the caller's stream;
+// experiments only)
+static bool sdf_concurrent() {
+  static const bool on = [] {
+    const char* e = std::getenv("CM_SDF_CONCURRENT");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 extern "C" {
 
 int cm_version(void) { return CM_ABI_VERSION; }
@@ -508,6 +519,10 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
     e = cudaMalloc(&sc->scratch, sc->scratch_floats * sizeof(float));
     if (e != cudaSuccess) { rc = CM_ERR_OOM; g_err = "scratch allocation failed"; }
     else sc->allocs.push_back(sc->scratch);
+  }
+  // aux streams: manifold chunks, and the class kernels of sdf_eval when the
+  // scene holds several SDF classes
+  if (rc == CM_OK && (sc->max_F > 0 || (sc->class_mask & (sc->class_mask - 1)) != 0)) {
     for (int i = 0; rc == CM_OK && i < cmi::kManifoldStreams; ++i) {
       if (cudaStreamCreateWithFlags(&sc->aux[i], cudaStreamNonBlocking) != cudaSuccess ||
           cudaEventCreateWithFlags(&sc->ev_join[i], cudaEventDisableTiming) != cudaSuccess) {
@@ -563,9 +578,33 @@ int cm_sdf_eval(const cm_scene* sc, const int32_t* ids, const float* poses, cons
   if ((flags & CM_SDF_HESS) && !hess) return fail(CM_ERR_INVALID, "cm_sdf_eval: hess is NULL");
   if ((flags & CM_SDF_POSE_GRAD) && !dpose) return fail(CM_ERR_INVALID, "cm_sdf_eval: dpose is NULL");
   if ((flags & CM_SDF_POSE_HESS) && (!d2pose || !dxdpose)) return fail(CM_ERR_INVALID, "cm_sdf_eval: d2pose/dxdpose NULL");
-  int rc = cml::launch_sdf_eval(sc->dev, sc->class_mask, ids, poses, points, B, P, flags, d,
-                                (flags & CM_SDF_GRAD) ? grad : nullptr, (flags & CM_SDF_HESS) ? hess : nullptr, dpose,
-                                d2pose, dxdpose, stream);
+  grad = (flags & CM_SDF_GRAD) ? grad : nullptr;
+  hess = (flags & CM_SDF_HESS) ? hess : nullptr;
+  const int cm = sc->class_mask;
+  if ((cm & (cm - 1)) == 0 || !sdf_concurrent()) {   // one SDF class: one kernel on the caller's stream
+    void* st1[1] = {stream};
+    const int rc = cml::launch_sdf_eval(sc->dev, cm, ids, poses, points, B, P, flags, d, grad, hess, dpose, d2pose,
+                                        dxdpose, st1, 1);
+    if (rc) return fail(rc, cml::last_cuda_error());
+    return CM_OK;
+  }
+  // several classes: fork onto the scene's aux streams (the caller's stream
+  // and the aux streams each run one class kernel concurrently), then join
+  cm_scene* ms = const_cast<cm_scene*>(sc);   // internal scheduling state only
+  std::lock_guard<std::mutex> lock(ms->mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaEventRecord(ms->ev_fork, st) != cudaSuccess) return fail(CM_ERR_CUDA, "cm_sdf_eval: event record");
+  void* sts[1 + cmi::kManifoldStreams] = {stream};
+  for (int i = 0; i < cmi::kManifoldStreams; ++i) {
+    cudaStreamWaitEvent(ms->aux[i], ms->ev_fork, 0);
+    sts[1 + i] = ms->aux[i];
+  }
+  const int rc = cml::launch_sdf_eval(sc->dev, cm, ids, poses, points, B, P, flags, d, grad, hess, dpose, d2pose,
+                                      dxdpose, sts, 1 + cmi::kManifoldStreams);
+  for (int i = 0; i < cmi::kManifoldStreams; ++i) {
+    cudaEventRecord(ms->ev_join[i], ms->aux[i]);
+    cudaStreamWaitEvent(st, ms->ev_join[i], 0);
+  }
   if (rc) return fail(rc, cml::last_cuda_error());
   return CM_OK;
 }

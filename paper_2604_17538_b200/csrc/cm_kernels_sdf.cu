@@ -151,24 +151,26 @@ namespace cml {
 
 int launch_sdf_eval(const SceneDev& s, int class_mask, const int32_t* ids, const float* poses, const float* pts,
                     int64_t B, int64_t P, uint32_t flags, float* d, float* g, float* h, float* dp, float* d2p,
-                    float* dxp, void* stream) {
+                    float* dxp, void* const* streams, int n_streams) {
   // class_mask bit c: the scene has SDF shapes of class c (0 SQ family, 1
   // constant-schedule XPSQ, 2 varying-schedule XPSQ); one instantiation per
-  // present class, each filtering its own shapes when several are present
-  cudaStream_t st = (cudaStream_t)stream;
+  // present class, each filtering its own shapes when several are present;
+  // the j-th present class runs on streams[j % n_streams] (concurrent classes
+  // fill each other's wave tails)
   const bool multi = (class_mask & (class_mask - 1)) != 0;
-  int rc = CM_OK;
-  if (class_mask & 1) rc = dispatch_sdf<0>(s, multi ? 0 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, st);
+  int rc = CM_OK, j = 0;
+  auto next = [&]() { return (cudaStream_t)streams[(j++) % n_streams]; };
+  if (class_mask & 1) rc = dispatch_sdf<0>(s, multi ? 0 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
   if (!rc && (class_mask & 2))
-    rc = dispatch_sdf<1>(s, multi ? 1 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, st);
+    rc = dispatch_sdf<1>(s, multi ? 1 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
   if (!rc && (class_mask & 4))
-    rc = dispatch_sdf<2>(s, multi ? 2 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, st);
+    rc = dispatch_sdf<2>(s, multi ? 2 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
   // nested SQ-family shapes: general interpreter, no XPSQ code
   if (!rc && (class_mask & 8))
-    rc = dispatch_sdf<3>(s, multi ? 3 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, st);
+    rc = dispatch_sdf<3>(s, multi ? 3 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
   // constant-schedule XPSQ inside boolean trees
   if (!rc && (class_mask & 16))
-    rc = dispatch_sdf<4>(s, multi ? 4 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, st);
+    rc = dispatch_sdf<4>(s, multi ? 4 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
   return rc;
 }
 
