@@ -101,7 +101,10 @@ struct SceneDev {
 // in a global slot each; the scene allocates kChunkUnits slots (capped at
 // kScratchCapBytes) at creation (CM_CHUNK_UNITS overrides the unit count)
 constexpr int64_t kChunkUnits = 32768;
-constexpr int kManifoldStreams = 2;     // chunks alternate between the scene's aux streams
+#ifndef CM_N_AUX_STREAMS
+#define CM_N_AUX_STREAMS 2
+#endif
+constexpr int kManifoldStreams = CM_N_AUX_STREAMS;   // chunks alternate between the scene's aux streams
 constexpr int64_t kScratchCapBytes = 1024ll << 20;
 
 // shape-parameter derivatives (f4): boolean nodes of one shape the
