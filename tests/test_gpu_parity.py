@@ -99,6 +99,37 @@ def test_sdf_eval_mixed_batch(cuda, oracle_mod):
     assert nf == 0, json.dumps(rep, indent=1)
 
 
+def test_sdf_eval_side_stream_join(cuda):
+    """A multi-class scene forks its class kernels onto the scene's streams
+    and joins them back into the caller's stream: work queued on a side
+    stream after the call sees every output (NaN-prefilled buffers, a large
+    batch so the class kernels overlap), bit-identical to a default-stream
+    call."""
+    import torch
+    from paper_2604_17538_b200 import binding
+    shapes = [synth.make_shape(n, r) for n, r in _sdf_shapes() if n != "cup"]
+    sc = scene_of(shapes)
+    S = binding.Scene(sc.shapes, sc.smooth)
+    rng = np.random.default_rng(17)
+    B, P = 4096, 64
+    ids = torch.from_numpy(rng.integers(0, len(shapes), B).astype(np.int32)).cuda()
+    poses = torch.from_numpy(np.stack([pose8(rng.uniform(-0.1, 0.1, 3), synth.random_quats(rng, 1)[0])
+                                       for _ in range(B)]).astype(np.float32)).cuda()
+    pts = torch.from_numpy(rng.uniform(-0.5, 0.5, (B * P, 3)).astype(np.float32)).cuda()
+    flags = binding.SDF_VALUE | binding.SDF_GRAD | binding.SDF_HESS
+    ref = S.sdf_eval(ids, poses, pts, P, flags)
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        out = {k: torch.full_like(v, float("nan")) for k, v in ref.items()}
+        S.sdf_eval(ids, poses, pts, P, flags, out=out)
+        seen = {k: v.clone() for k, v in out.items()}   # queued behind the join on `side`
+    side.synchronize()
+    for k in ref:
+        assert torch.equal(seen[k], ref[k]), k
+
+
 def test_sdf_eval_c1(cuda, oracle_mod):
     from paper_2604_17538_b200 import binding
     sc = synth.c1_scene()
