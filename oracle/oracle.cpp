@@ -223,7 +223,7 @@ static void normalize3(double* v) {
 // Frenet frame when the spline is genuinely curved, else a constant frame
 // built from the up hint by Gram-Schmidt.
 constexpr double XPSQ_EPS_POINT = 1e-6;   // |A|,|B| below this: point spline
-constexpr double XPSQ_EPS_LINE = 1e-2;    // |A| < 1e-2 |B|: snapped straight (A := 0)
+constexpr double XPSQ_EPS_LINE = 1e-4;    // |A| < 1e-4 |B|: snapped straight
 constexpr double XPSQ_EPS_FRAME = 1e-3;   // |BxA| < 1e-3 |A||B|: constant frame
 
 static void xpsq_static(Node& n) {
@@ -234,7 +234,9 @@ static void xpsq_static(Node& n) {
   if (nA < XPSQ_EPS_POINT && nB < XPSQ_EPS_POINT) {
     n.xcls = 0; T0[0] = 1; T0[1] = 0; T0[2] = 0;
   } else if (nA < XPSQ_EPS_LINE * nB) {
-    n.xcls = 1; for (int i = 0; i < 3; ++i) { n.A[i] = 0.0; T0[i] = n.B[i]; }
+    // straight: the segment p1 -> p3 (the chord B := p3 - p1 = A + B, A := 0;
+    // it keeps both end points and lies within |A|/4 of the spline)
+    n.xcls = 1; for (int i = 0; i < 3; ++i) { n.B[i] += n.A[i]; n.A[i] = 0.0; T0[i] = n.B[i]; }
   } else {
     n.xcls = 2;
     for (int i = 0; i < 3; ++i) T0[i] = n.A[i] + n.B[i];
