@@ -11,12 +11,17 @@ with derivatives").
 One step = one cm_contact_manifold call (tier 2) over the rank's whole env
 shard.  Weak scaling: every rank owns n_env environments (global env ids
 [rank*n_env, (rank+1)*n_env), inputs keyed by global env index), no
-collective on the data path; timing is max over ranks.  Inputs (poses,
-pairs, offsets) are resident in HBM for `value`; `e2e` re-times the same
-step through the public API with the step's poses copied host->device from
-pinned memory and the fused depths copied back every step (double buffered:
-the copies of neighbouring steps overlap the compute on separate upload /
-download streams).  L2 is flushed (256 MiB write) between timed steps.
+collective on the data path; timing is max over ranks.  `--gpus N` without a
+torchrun environment re-launches itself under torch.distributed.run with N
+ranks (127.0.0.1).  Inputs (poses, pairs, offsets) are resident in HBM for
+`value`; `e2e` re-times the step through the public API with the poses
+copied host->device from pinned memory and EVERY output field of the tier
+copied back device->host (the whole manifold, in 8 sub-batches so the
+copies of one sub-batch overlap the compute of the next on separate upload /
+download streams); `e2e_depth_only` is the same loop reading back only the
+fused depths.  L2 is flushed (256 MiB write) between timed steps.  With
+N > 1 the optional NCCL all-gather of the tier-0 fields is timed separately
+(`allgather`), never inside `value`.
 """
 from __future__ import annotations
 
@@ -43,7 +48,21 @@ sys.path.insert(0, ROOT)
 # outputs: F contacts x 237 B at tier 2).
 OUT_BYTES_PER_CONTACT = {0: 33, 1: 45, 2: 237, 3: 237 + 78 * 4}
 IN_BYTES_PER_PAIR = 2 * 32 + 20
-FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4 at the 1965 MHz max SM clock
+FP32_PEAK_DERIVED_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4 at the 1965 MHz max SM clock
+XU_PEAK_DERIVED_TOPS = 148 * 16 * 1.965e9 / 1e12           # 4.65 (16 MUFU lanes per SM per clock)
+
+
+def load_alu_peaks():
+    """FP32 and MUFU/XU peaks measured on a B200 of this pool by the K5
+    microbenchmarks (tools/k5_peaks.cu -> profiles/peaks_fp32_xu.json);
+    the spec arithmetic when that file is missing (say which)."""
+    p = os.path.join(ROOT, "profiles", "peaks_fp32_xu.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            k = json.load(f)
+        return (k["fp32_tflops"], k["xu_tops"],
+                "measured: tools/k5_peaks.cu FFMA / MUFU chains on a B200 (profiles/peaks_fp32_xu.json, %s)" % k["when"])
+    return FP32_PEAK_DERIVED_TFLOPS, XU_PEAK_DERIVED_TOPS, "derived: 148 SM x 128 FP32 / 16 MUFU lanes x 1965 MHz"
 
 
 def _cost_key(workload, shape, kind):
@@ -56,25 +75,69 @@ def _cost_key(workload, shape, kind):
 
 
 def flop_per_launch(workload, scene, S):
-    """Algorithmic FP32 FLOPs of one tier-2 call over scene.pairs."""
+    """Algorithmic work of one tier-2 call over scene.pairs from the frozen
+    cost table: (FP32 FLOPs, MUFU ops of the SDF evaluations).  The MUFU
+    count covers the (V + E) second-order and 2 E (iters - 1) first-order
+    evaluations of the SDF side only (the table has no MUFU count of the
+    manifold's own gates and softmax)."""
     with open(os.path.join(ROOT, "paper_2604_17538_b200", "costmodel.json")) as f:
         cm = json.load(f)
     hs1, hs2 = cm["halfspace_eval"]["order1"], cm["halfspace_eval"]["order2"]
     it = scene.smooth["trace_iters"]
-    per_shape_pair = {}
-    total = 0.0
+    total = mufu = 0.0
     a_ids, b_ids = scene.pairs[:, 3], scene.pairs[:, 4]
     keys, counts = np.unique(np.stack([a_ids, b_ids], 1), axis=0, return_counts=True)
     for (a, b), n in zip(keys, counts):
         sa, sb = scene.shapes[a], scene.shapes[b]
         ka, kb = _cost_key(workload, sa, "mesh"), _cost_key(workload, sb, "sdf")
         if ka not in cm["manifold_with_halfspace"] or kb not in cm["sdf"]:
-            return None
+            return None, None
         V, E, F = S.counts(int(a))
         c = cm["manifold_with_halfspace"][ka]["flop_per_pair_total_with_halfspace"]
         c += (V + E) * (cm["sdf"][kb]["order2"]["flop"] - hs2) + 2 * E * (it - 1) * (cm["sdf"][kb]["order1"]["flop"] - hs1)
         total += n * c
-    return total
+        mufu += n * ((V + E) * cm["sdf"][kb]["order2"]["mufu"] + 2 * E * (it - 1) * cm["sdf"][kb]["order1"]["mufu"])
+    return total, mufu
+
+
+def roofline(flop, mufu, bytes_alg, kern_s, peaks, peak_src, extra=None):
+    """The three roofs of SURVEY §8(d) (FP32 pipe, MUFU/XU pipe, HBM), each
+    achieved = algorithmic work / time and frac = achieved / measured peak;
+    `bound` is the roof with the largest fraction (the binding one)."""
+    fp32_peak, xu_peak, alu_src = load_alu_peaks()
+    roofs = {}
+    if flop:
+        a = flop / kern_s / 1e12
+        roofs["fp32"] = {"achieved": a, "peak": fp32_peak, "unit": "TFLOP/s", "frac": a / fp32_peak,
+                         "peak_source": alu_src}
+    if mufu:
+        a = mufu / kern_s / 1e12
+        roofs["xu"] = {"achieved": a, "peak": xu_peak, "unit": "Tops/s", "frac": a / xu_peak, "peak_source": alu_src,
+                       "scope": "MUFU ops of the SDF evaluations (cost table); the manifold's gates not counted"}
+    a = bytes_alg / kern_s / 1e9
+    roofs["hbm"] = {"achieved": a, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": a / peaks["hbm_gbs"],
+                    "peak_source": "%s (MEASURED_PEAKS.json hbm_gbs)" % peak_src, "bytes_alg": bytes_alg}
+    name = max(roofs, key=lambda k: roofs[k]["frac"])
+    b = roofs[name]
+    out = {"bound": {"fp32": "alu", "xu": "alu", "hbm": "hbm"}[name], "binding_roof": name,
+           "achieved": b["achieved"], "peak": b["peak"], "unit": b["unit"], "frac": b["frac"],
+           "peak_source": b["peak_source"], "traffic": None, "roofs": roofs}
+    if extra:
+        out.update(extra)
+    return out
+
+
+def cpu_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
 
 
 def load_peaks():
@@ -320,7 +383,8 @@ def _e2e_pipelined(run_step, h2d, d2h, steps, world, dev):
             ev_comp[s].record(comp)
             with torch.cuda.stream(down):
                 down.wait_event(ev_comp[s])
-                d2h[s][0].copy_(d2h[s][1], non_blocking=True)
+                for dst, src in (d2h[s] if isinstance(d2h[s], list) else [d2h[s]]):
+                    dst.copy_(src, non_blocking=True)
                 ev_out[s].record(down)
         for s in range(min(n, 2)):
             comp.wait_event(ev_out[s])
@@ -364,34 +428,29 @@ def run_sdf(args, sc, n_body, gen_s, world, rank, local):
     e2e = None
     if not args.no_e2e:
         pts_h = torch.from_numpy(sc.points).pin_memory()
-        d_h = [torch.empty(n_pts, dtype=torch.float32).pin_memory() for _ in range(2)]
         pts_d = [torch.empty_like(pts) for _ in range(2)]
         outs = [out, {k: torch.empty_like(v) for k, v in out.items()}]
+        host = [{k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in out.items()} for _ in range(2)]
         ms_e = _e2e_pipelined(lambda s_: S.sdf_eval(ids, poses, pts_d[s_], P, flags, out=outs[s_]),
-                              [(pts_d[k], pts_h) for k in range(2)], [(d_h[k], outs[k]["d"]) for k in range(2)],
-                              args.steps, world, dev)
+                              [(pts_d[k], pts_h) for k in range(2)],
+                              [[(host[k][f], outs[k][f]) for f in out] for k in range(2)], args.steps, world, dev)
         e2e = {"value": n_pts * world / (ms_e / 1e3), "unit": "points/s",
-               "h2d_bytes_per_step": int(pts_h.numel() * 4), "d2h_bytes_per_step": int(n_pts * 4),
+               "h2d_bytes_per_step": int(pts_h.numel() * 4),
+               "d2h_bytes_per_step": int(sum(v.numel() * v.element_size() for v in out.values())),
+               "readback": "every output field (d, grad, hess, dpose)",
                "pipeline": "double-buffered: upload / download streams overlap the compute"}
     with open(os.path.join(ROOT, "paper_2604_17538_b200", "costmodel.json")) as f:
         cm = json.load(f)
     names = [sc.shapes[i].name for i in range(len(sc.shapes))]
     cnt = np.bincount(sc.point_shapes, minlength=len(names))
     flop = float(sum(cnt[i] * P * cm["sdf"][names[i]]["order2"]["flop"] for i in range(len(names))))
+    mufu = float(sum(cnt[i] * P * cm["sdf"][names[i]]["order2"]["mufu"] for i in range(len(names))))
     kern_s = ms / 1e3
     bytes_alg = n_pts * SDF_BYTES_PER_POINT + len(sc.point_shapes) * 36
     peaks, peak_src = load_peaks()
-    achieved = flop / kern_s / 1e12
-    hbm = bytes_alg / kern_s / 1e9
-    roof = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": achieved / FP32_PEAK_TFLOPS, "traffic": None,
-            "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
-            "flop_per_point": flop / n_pts, "flop_source": "costmodel.json order-2 evaluation FLOPs per shape",
-            "hbm": {"achieved_gbs": hbm, "peak_gbs": peaks["hbm_gbs"], "frac": hbm / peaks["hbm_gbs"],
-                    "bytes_alg": bytes_alg, "peak_source": peak_src}}
-    if hbm / peaks["hbm_gbs"] > achieved / FP32_PEAK_TFLOPS:
-        roof.update({"bound": "hbm", "achieved": hbm, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": hbm / peaks["hbm_gbs"]})
+    roof = roofline(flop, mufu, bytes_alg, kern_s, peaks, peak_src,
+                    {"flop_per_point": flop / n_pts, "flop_source": "costmodel.json order-2 evaluation FLOPs per shape",
+                     "scope": "every k_sdf_eval launch of the step (one per SDF class present)"})
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import oracle as O
@@ -421,6 +480,162 @@ def run_sdf(args, sc, n_body, gen_s, world, rank, local):
         dist.destroy_process_group()
 
 
+def maybe_spawn(args):
+    """`python bench.py --gpus N` outside torchrun: re-run this command under
+    torch.distributed.run with N ranks on this node (rendezvous on
+    127.0.0.1).  Returns True when this process only spawned the ranks."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    s = __import__("socket").socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    r = subprocess.run(cmd)
+    if r.returncode:
+        raise SystemExit(r.returncode)
+    return True
+
+
+def dry_run(args):
+    """Process-group plumbing only (no GPU work): every rank reports its
+    RANK / LOCAL_RANK / WORLD_SIZE; rank 0 prints one JSON line."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    me = {"rank": rank, "local_rank": int(os.environ.get("LOCAL_RANK", "0")), "world": world,
+          "env_range": [rank * (args.n_env or DEFAULT_NENV[args.workload]),
+                        (rank + 1) * (args.n_env or DEFAULT_NENV[args.workload])]}
+    ranks = [me]
+    if world > 1:
+        dist.init_process_group("gloo")
+        ranks = [None] * world
+        dist.all_gather_object(ranks, me)
+        t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        me["max_over_ranks"] = float(t.item())
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks": ranks}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_full(S, scene, args, world, dev, n_sub=8):
+    """End to end through the public API with host buffers: each step uploads
+    the poses from pinned memory and reads EVERY output field of the tier back
+    into pinned memory, in n_sub env sub-batches pipelined over an upload, a
+    compute and a download stream (sub-batch i's read-back overlaps sub-batch
+    i+1's compute).  Returns (ms per step, h2d bytes, d2h bytes)."""
+    import torch
+    import torch.distributed as dist
+    n_env = scene.poses.shape[0]
+    bounds = np.linspace(0, n_env, n_sub + 1).astype(np.int64)
+    subs = []
+    for i in range(n_sub):
+        e0, e1 = int(bounds[i]), int(bounds[i + 1])
+        m = (scene.pairs[:, 0] >= e0) & (scene.pairs[:, 0] < e1)
+        pr = scene.pairs[m].copy()
+        pr[:, 0] -= e0
+        pairs_d = torch.from_numpy(pr).to(dev)
+        C = S.manifold_size(pr)
+        subs.append(dict(e0=e0, e1=e1, pairs=pairs_d, offs=S.manifold_offsets(pairs_d), C=C))
+    Cmax = max(x["C"] for x in subs)
+    nmax = max(x["e1"] - x["e0"] for x in subs)
+    poses_h = torch.from_numpy(scene.poses).pin_memory()
+    # flat per-field buffers; sub-batch b uses the contiguous [rows, C_b]
+    # prefix view (the library's field stride is the call's n_contacts)
+    proto = S.alloc_manifold(1, args.tier, dev)
+    rows = {k: (v.shape[0] if v.dim() == 2 else 1) for k, v in proto.items()}
+    dev_flat = [{k: torch.empty(rows[k] * Cmax, dtype=v.dtype, device=dev) for k, v in proto.items()}
+                for _ in range(2)]
+    host_flat = [{k: torch.empty(rows[k] * Cmax, dtype=v.dtype).pin_memory() for k, v in proto.items()}
+                 for _ in range(2)]
+    view = lambda buf, k, C: buf[k][:rows[k] * C].view(rows[k], C) if proto[k].dim() == 2 else buf[k][:C]
+    dev_poses = [torch.empty((nmax,) + tuple(scene.poses.shape[1:]), dtype=torch.float32, device=dev)
+                 for _ in range(2)]
+    comp = torch.cuda.current_stream()
+    up, down = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_in, ev_comp, ev_out = ([torch.cuda.Event() for _ in range(2)] for _ in range(3))
+
+    def go(steps):
+        j = 0
+        for _ in range(steps):
+            for sb in subs:
+                s_ = j % 2
+                n, C = sb["e1"] - sb["e0"], sb["C"]
+                with torch.cuda.stream(up):
+                    if j >= 2:
+                        up.wait_event(ev_comp[s_])           # slot s_ poses no longer read
+                    dev_poses[s_][:n].copy_(poses_h[sb["e0"]:sb["e1"]], non_blocking=True)
+                    ev_in[s_].record(up)
+                comp.wait_event(ev_in[s_])
+                if j >= 2:
+                    comp.wait_event(ev_out[s_])              # slot s_ outputs already read back
+                out = {k: view(dev_flat[s_], k, C) for k in proto}
+                S.contact_manifold(sb["pairs"], sb["offs"], C, dev_poses[s_][:n], args.tier, out)
+                ev_comp[s_].record(comp)
+                with torch.cuda.stream(down):
+                    down.wait_event(ev_comp[s_])
+                    for k in proto:
+                        host_flat[s_][k][:rows[k] * C].copy_(dev_flat[s_][k][:rows[k] * C], non_blocking=True)
+                    ev_out[s_].record(down)
+                j += 1
+        for s_ in range(2):
+            comp.wait_event(ev_out[s_])
+
+    go(1)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(comp)
+    up.wait_event(e0)
+    steps = max(1, min(args.steps, args.e2e_steps))
+    go(steps)
+    e1.record(comp)
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    h2d = int(scene.poses.nbytes)
+    per_contact = sum(v.element_size() * rows[k] for k, v in proto.items())
+    d2h = int(sum(x["C"] for x in subs) * per_contact)
+    return float(te.item()), h2d, d2h, steps
+
+
+def allgather_tier0(out, C, world, dev):
+    """Optional NCCL all-gather of the tier-0 fields (point, normal, depth) of
+    every rank over NVLink, timed separately from the step."""
+    import torch
+    import torch.distributed as dist
+    C_all = torch.tensor([C], dtype=torch.int64, device=dev)
+    dist.all_reduce(C_all, op=dist.ReduceOp.MAX)
+    Cm = int(C_all.item())
+    send = torch.zeros(7, Cm, dtype=torch.float32, device=dev)
+    send[0:3, :C] = out["point"]
+    send[3:6, :C] = out["normal"]
+    send[6, :C] = out["depth"]
+    recv = torch.empty(world * 7 * Cm, dtype=torch.float32, device=dev)
+    dist.all_gather_into_tensor(recv, send.reshape(-1))
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(3):
+        dist.all_gather_into_tensor(recv, send.reshape(-1))
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / 3], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    nbytes = world * 7 * Cm * 4
+    return {"fields": "point, normal, depth (tier 0, 28 B per contact)", "bytes_gathered_per_rank": nbytes,
+            "ms": ms, "recv_gbs_per_rank": (world - 1) / world * nbytes / (ms / 1e3) / 1e9,
+            "note": "timed separately (max over ranks); not part of value"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -433,7 +648,14 @@ def main():
     ap.add_argument("--tier", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5, help="steps of the full-readback e2e loop (PCIe-bound)")
+    ap.add_argument("--no-allgather", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="process-group plumbing only (CPU tests)")
     args = ap.parse_args()
+    if maybe_spawn(args):
+        return
+    if args.dry_run:
+        return dry_run(args)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -470,67 +692,62 @@ def main():
     n_pairs_all = len(scene.pairs) * world
     value = n_pairs_all / (ms_per_step / 1e3)
 
+    gather = None
+    if world > 1 and not args.no_allgather:
+        gather = allgather_tier0(out, C, world, dev)
+
     # ---- end to end through the public API with host buffers --------------
-    e2e = None
+    e2e = e2e_depth = None
     if not args.no_e2e:
+        del flush
+        ms_e, h2d, d2h, e_steps = e2e_full(S, scene, args, world, dev)
+        e2e = {"value": n_pairs_all / (ms_e / 1e3), "unit": "pairs/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": e_steps,
+               "readback": "every tier-%d output field (the whole manifold)" % args.tier,
+               "pipeline": "8 env sub-batches per step; upload / compute / download streams overlap"}
         poses_h = torch.from_numpy(scene.poses).pin_memory()
         depth_h = [torch.empty(C, dtype=torch.float32).pin_memory() for _ in range(2)]
         poses_d = [torch.empty_like(poses) for _ in range(2)]
         # slot 1 shares every output but the read-back field with slot 0
         outs = [out, dict(out, depth=torch.empty_like(out["depth"]))]
-        ms_e = _e2e_pipelined(lambda s_: S.contact_manifold(pairs, offs, C, poses_d[s_], args.tier, outs[s_]),
+        ms_d = _e2e_pipelined(lambda s_: S.contact_manifold(pairs, offs, C, poses_d[s_], args.tier, outs[s_]),
                               [(poses_d[k], poses_h) for k in range(2)],
                               [(depth_h[k], outs[k]["depth"]) for k in range(2)], args.steps, world, dev)
-        e2e = {"value": n_pairs_all / (ms_e / 1e3), "unit": "pairs/s",
-               "h2d_bytes_per_step": int(poses_h.numel() * 4), "d2h_bytes_per_step": int(C * 4),
-               "pipeline": "double-buffered: upload / download streams overlap the compute"}
+        e2e_depth = {"value": n_pairs_all / (ms_d / 1e3), "unit": "pairs/s",
+                     "h2d_bytes_per_step": int(poses_h.numel() * 4), "d2h_bytes_per_step": int(C * 4),
+                     "readback": "fused depths only (4 of %d B per contact)" % OUT_BYTES_PER_CONTACT[args.tier]}
 
-    # ---- roofline of the manifold kernels ---------------------------------
+    # ---- roofline of the step's kernels ------------------------------------
     peaks, peak_src = load_peaks()
     n_pairs = len(scene.pairs)
     bytes_alg = n_pairs * IN_BYTES_PER_PAIR + C * OUT_BYTES_PER_CONTACT[args.tier]
-    # the step is exactly the k_mf_* launches of one cm_contact_manifold call
-    # (per chunk of units: vertices, traces, midpoints per SDF class, then
-    # faces), timed together with CUDA events on the caller's stream; the
-    # algorithmic FLOPs are those of the whole method, so the roofline covers
-    # the kernels of the step together (per-kernel shares: profiles/traffic_*.json)
     kern_s = ms_per_step / 1e3
-    hbm_gbs = bytes_alg / kern_s / 1e9
-    flop_launch = flop_per_launch(args.workload, scene, S) if args.tier == 2 else None
-    fpp = flop_launch / n_pairs if flop_launch else None
-    if fpp:
-        achieved = flop_launch / kern_s / 1e12
-        traffic = None
-        dominant = None
-        tpath = os.path.join(ROOT, "profiles", "traffic_%s.json" % args.workload.lower())
-        if os.path.exists(tpath) and args.tier == 2:
-            with open(tpath) as f:
-                tj = json.load(f)
-            traffic = tj["bytes_per_pair"] * n_pairs   # measured DRAM bytes per step
-            top = max(tj["kernels"], key=lambda k: k["share_of_chunk_time"])
-            dominant = {"kernel": top["kernel"], "share_of_step": round(top["share_of_chunk_time"], 3),
-                        "source": "ncu launch durations of one chunk (%s)" % os.path.basename(tpath)}
-        roof = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,
-                "scope": "all k_mf_* kernels of the step (the step is exactly these launches)",
-                "dominant_kernel": dominant,
-                "traffic_unit": "bytes per step (ncu dram read + write of one chunk's kernels, cold-cache replays, "
-                                "scaled per pair)",
-                "bytes_alg": bytes_alg,
-                "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
-                "flop_per_pair": fpp, "flop_source": "costmodel.json (ncu-measured per-shape/order table, DESIGN.md §7)",
-                "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks["hbm_gbs"],
-                                              "frac": hbm_gbs / peaks["hbm_gbs"], "peak_source": peak_src}}
-    else:
-        roof = {"bound": "hbm", "achieved": hbm_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": hbm_gbs / peaks["hbm_gbs"], "traffic": None, "peak_source": peak_src,
-                "note": "FLOP/pair not yet frozen; HBM fraction of algorithmic bytes only"}
+    flop_launch, mufu_launch = flop_per_launch(args.workload, scene, S) if args.tier == 2 else (None, None)
+    extra = {"scope": "every k_mf_* kernel of the step together (the step is exactly these launches)"}
+    if flop_launch:
+        extra.update({"flop_per_pair": flop_launch / n_pairs, "mufu_per_pair_sdf": mufu_launch / n_pairs,
+                      "flop_source": "costmodel.json: frozen per-(shape, order) FP32 op table (DESIGN.md §7)"})
+    roof = roofline(flop_launch, mufu_launch, bytes_alg, kern_s, peaks, peak_src, extra)
+    tpath = os.path.join(ROOT, "profiles", "traffic_%s.json" % args.workload.lower())
+    if os.path.exists(tpath) and args.tier == 2:
+        with open(tpath) as f:
+            tj = json.load(f)
+        roof["traffic"] = tj["bytes_per_pair"] * n_pairs   # measured DRAM bytes per step
+        roof["traffic_unit"] = ("bytes per step (ncu dram read + write of one chunk's kernels, cold-cache replays, "
+                                "scaled per pair; %s)" % os.path.basename(tpath))
+        top = max(tj["kernels"], key=lambda k: k["share_of_chunk_time"])
+        roof["dominant_kernel"] = {"kernel": top["kernel"], "share_of_step": round(top["share_of_chunk_time"], 3),
+                                   "source": "ncu launch durations of one chunk (%s)" % os.path.basename(tpath)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, m, cores, dt = oracle_rate(scene, budget_s=20.0)
+        rate1, m1, _, dt1 = oracle_rate(scene, budget_s=4.0, threads=1, max_pairs=256)
         cpu = {"value": rate, "unit": "pairs/s", "cores": cores, "kind": "oracle",
-               "sample": "first %d pairs of the %s shard, FP64 jet oracle, OpenMP over pairs, %.1f s" % (m, args.workload, dt)}
+               "sample": "first %d pairs of the %s shard, FP64 jet oracle, OpenMP over pairs, %.1f s"
+                         % (m, args.workload, dt),
+               "single_thread": {"value": rate1, "sample": "first %d pairs, 1 thread, %.1f s" % (m1, dt1)}}
+        cpu.update(cpu_info())
 
     if rank == 0:
         line = {"metric": "contact-manifold evals/sec with derivatives (tier %d)" % args.tier, "value": value,
@@ -542,8 +759,10 @@ def main():
                            "contacts_per_gpu": C, "tier": args.tier, "l2": "flushed (256 MiB write) between steps",
                            "parallelism": "env-sharded dp%d, no data-path collective" % world,
                            "input_gen_s": round(gen_s, 1)},
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-                "clocks": clk}
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_depth_only": e2e_depth,
+                "gpu_launches": int(launches), "clocks": clk}
+        if gather:
+            line["allgather"] = gather
         if args.workload == "C3" and args.k != 18:
             line["config"]["sqs_in_union"] = args.k
         if args.workload == "C1":   # latency-bound: report the per-call latency

@@ -90,6 +90,14 @@ __device__ __forceinline__ void softplus_sig(float x, float tau, float itau, flo
 // softclip value with its first and second derivatives (two exponentials)
 __device__ __forceinline__ void softclip_12(float x, float lo, float hi, float tau, float itau, float& v, float& d1,
                                             float& d2) {
+  // interior: both exponentials are below 2^-144 and flush to 0 (ftz), so the
+  // general path below returns exactly lo + (x - lo), 1, 0 -- skip its 6 MUFU ops
+  if ((x - lo) * itau > 100.f && (hi - x) * itau > 100.f) {
+    v = lo + (x - lo);
+    d1 = 1.f;
+    d2 = 0.f;
+    return;
+  }
   float sp1, s1, sp2, s2;
   softplus_sig(x - lo, tau, itau, sp1, s1);
   softplus_sig(x - hi, tau, itau, sp2, s2);
@@ -253,9 +261,13 @@ template <int O, class SP> __device__ __forceinline__ void sq_eval(const SP& Lf,
   float u0 = y[0] * ia0, u1 = y[1] * ia1, u2 = y[2] * ia2;
   float q0 = fmaf(u0, u0, SQ_GUARD), q1 = fmaf(u1, u1, SQ_GUARD), q2 = fmaf(u2, u2, SQ_GUARD);
   float la0 = p2 * lg2(q0), la1 = p2 * lg2(q1), l3 = p1 * lg2(q2);
-  float lS = fmaxf(la0, la1) + lg2(1.f + ex2(-fabsf(la0 - la1)));
+  // log-sum-exp in base 2; e = 2^-|difference| also gives both weights
+  // (w_big = 1/(1+e), w_small = e/(1+e)) without two more exponentials
+  const float eS = ex2(-fabsf(la0 - la1));
+  float lS = fmaxf(la0, la1) + lg2(1.f + eS);
   float lB = m * lS;
-  float lf = fmaxf(lB, l3) + lg2(1.f + ex2(-fabsf(lB - l3)));
+  const float ef = ex2(-fabsf(lB - l3));
+  float lf = fmaxf(lB, l3) + lg2(1.f + ef);
   float h = ex2(-k * lf);
   float rr = fmaf(y[0], y[0], fmaf(y[1], y[1], y[2] * y[2]));
   float ir = rsqrtf(fmaxf(rr, 1e-30f));
@@ -263,9 +275,12 @@ template <int O, class SP> __device__ __forceinline__ void sq_eval(const SP& Lf,
   float omh = 1.f - h;
   r.v = rad * omh;
   if constexpr (O >= 1) {
-    float w0 = ex2(la0 - lS), w1 = ex2(la1 - lS);
-    float be = ex2(lB - lf), ga = ex2(l3 - lf);
-    float iq0 = rcpa(q0), iq1 = rcpa(q1), iq2 = rcpa(q2);
+    const float rS = rcpa(1.f + eS), rf = rcpa(1.f + ef);
+    const bool a0big = la0 >= la1, bbig = lB >= l3;
+    float w0 = a0big ? rS : eS * rS, w1 = a0big ? eS * rS : rS;   // A_i / S
+    float be = bbig ? rf : ef * rf, ga = bbig ? ef * rf : rf;      // B / f, C / f
+    const float r01 = rcpa(q0 * q1);   // q >= 1e-12: the product stays normal
+    float iq0 = q1 * r01, iq1 = q0 * r01, iq2 = rcpa(q2);
     float s0 = u0 * ia0 * iq0, s1 = u1 * ia1 * iq1, s2 = u2 * ia2 * iq2;
     float tp1 = 2.f * p1;
     float L0 = tp1 * be * w0 * s0, L1 = tp1 * be * w1 * s1, L2 = tp1 * ga * s2;
@@ -577,36 +592,129 @@ template <int O> __device__ __forceinline__ J3<O> lse_jets(const J3<O>* x, int n
 template <int O>
 __device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3, const SmoothDev& sp, J2<O>* t);
 
-// XPSQ leaf (P:102-126) in its local frame
-template <int O> __device__ CM_XINL void xpsq_eval(const Xpsq& X, const SmoothDev& sp, const float* y, Res<O>& out) {
-  const float tc = sp.tau_clip_t, itc = sp.i_clip_t;
-  float w[3] = {y[0] - X.p1[0], y[1] - X.p1[1], y[2] - X.p1[2]};
-  J3<O> tk[3];
-  if (X.cls == 0) {
+// Roots t_k(w) of the projection with their gradient and Hessian
+// with respect to w = y - p1 (packed xx, xy, xz, yy, yz, zz).  Returns true
+// when the three roots are bitwise identical (point / straight splines, or
+// the curved case in the one-real-root regime): then the three PSQ terms
+// coincide and -LSE(-phi, -phi, -phi) = phi - tau ln 3 exactly, so one PSQ
+// evaluation suffices.
+//
+// Curved splines outside the soft-Cardano band (|Delta| > 46 tau_Delta:
+// the other branch's gate weight sigma(-|Delta|/tau) < 1e-20 is skipped,
+// reading #34, and s+(Delta) < tau e^-46 leaves P and the discriminant
+// unchanged in FP32) are the exact roots of the cubic g(t) = c3 t^3 + c2 t^2
+// + c1 t + c0, c1 = 2 A.w - B.B, c0 = B.w.  There the Cardano / trigonometric
+// value is polished by Newton steps on g in t (for nearly straight splines
+// the depressed coefficients grow like (|B| / |A|)^2 and (|B| / |A|)^3, so
+// the FP32 Cardano / trigonometric values and t = s - b/3 cancel digits)
+// and differentiated implicitly: g_t dt + (B + 2 A t) dw = 0,
+//   t_i = -(B_i + 2 A_i t) / g_t,
+//   t_ij = -(g_tt t_i t_j + 2 A_i t_j + 2 A_j t_i) / g_t.
+// Inside the band both branches are blended literally (soft_cardano_implicit).
+template <int O>
+__device__ __forceinline__ void xpsq_t_implicit(const Xpsq& X, const SmoothDev& sp, const float* w, float t,
+                                                int newton, float* tv, float* tg, float* th) {
+  const float c1 = fmaf(2.f * X.A[0], w[0], fmaf(2.f * X.A[1], w[1], fmaf(2.f * X.A[2], w[2], -X.BB)));
+  const float c0 = fmaf(X.B[0], w[0], fmaf(X.B[1], w[1], X.B[2] * w[2]));
+  float r = 0.f;
+  for (int it = 0; it < newton; ++it) {
+    const float g = fmaf(fmaf(fmaf(X.c3, t, X.c2), t, c1), t, c0);
+    const float gp = fmaf(fmaf(3.f * X.c3, t, 2.f * X.c2), t, c1);
+    r = rcpa(gp);
+    t = fmaf(-g, r, t);
+  }
+  if (newton == 0 && O >= 1) r = rcpa(fmaf(fmaf(3.f * X.c3, t, 2.f * X.c2), t, c1));
+  float v, d1, d2;
+  softclip_12(t, 0.f, 1.f, sp.tau_clip_t, sp.i_clip_t, v, d1, d2);
+  *tv = v;
+  if constexpr (O >= 1) {
+    float ti[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) tk[k] = jconst<3, O>(0.5f);
-  } else if (X.cls == 1) {
-    float s = X.Bn[0] * w[0] + X.Bn[1] * w[1] + X.Bn[2] * w[2];
-    J3<O> sj = jconst<3, O>(s);
-    if constexpr (O >= 1) {
-#pragma unroll
-      for (int i = 0; i < 3; ++i) sj.g[i] = X.Bn[i];
+    for (int i = 0; i < 3; ++i) {
+      ti[i] = -fmaf(2.f * X.A[i], t, X.B[i]) * r;
+      tg[i] = d1 * ti[i];
     }
-    J3<O> t = jsoftclip(sj, 0.f, 1.f, tc, itc);
+    if constexpr (O >= 2) {
+      const float gtt = fmaf(6.f * X.c3, t, 2.f * X.c2);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) tk[k] = t;
-  } else {
-    float Pv = X.gP[0] * w[0] + X.gP[1] * w[1] + X.gP[2] * w[2] + X.P0;
-    float Qv = X.gQ[0] * w[0] + X.gQ[1] * w[1] + X.gQ[2] * w[2] + X.Q0;
-    J2<O> t2[3];
-    soft_cardano_implicit<O>(Pv, Qv, X.b3, sp, t2);
-    // chain (P, Q) -> y: grad t = tP gP + tQ gQ; hess = [gP gQ] H [gP gQ]^T
+      for (int q = 0; q < 6; ++q) {
+        const int i = jhi<3>(q), j = jhj<3>(q);
+        const float tij = -fmaf(gtt * ti[i], ti[j], 2.f * fmaf(X.A[i], ti[j], X.A[j] * ti[i])) * r;
+        th[q] = fmaf(d2 * ti[i], ti[j], d1 * tij);
+      }
+    }
+  }
+}
+
+template <int O>
+__device__ __forceinline__ bool xpsq_root_t(const Xpsq& X, const SmoothDev& sp, const float* w, float* tv, float (*tg)[3],
+                                            float (*th)[6]) {
+  const float tc = sp.tau_clip_t, itc = sp.i_clip_t;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    tv[k] = 0.5f;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) tg[k][i] = 0.f;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) th[k][q] = 0.f;
+  }
+  if (X.cls == 1) {
+    const float s = X.Bn[0] * w[0] + X.Bn[1] * w[1] + X.Bn[2] * w[2];
+    float v, d1, d2;
+    softclip_12(s, 0.f, 1.f, tc, itc, v, d1, d2);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      tk[k].v = t2[k].v;
+      tv[k] = v;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) tg[k][i] = d1 * X.Bn[i];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) th[k][q] = d2 * X.Bn[jhi<3>(q)] * X.Bn[jhj<3>(q)];
+    }
+  } else if (X.cls == 2) {
+    const float Pv = X.gP[0] * w[0] + X.gP[1] * w[1] + X.gP[2] * w[2] + X.P0;
+    const float Qv = X.gQ[0] * w[0] + X.gQ[1] * w[1] + X.gQ[2] * w[2] + X.Q0;
+    const float Delta = -(4.f * Pv * Pv * Pv + 27.f * Qv * Qv);
+    // Newton steps: one always (s = u - P/(3u) and 2 rho cos(.) cancel
+    // digits when |P| is large, e.g. A nearly perpendicular to B with
+    // |A| << |B|), two when t = s - b/3 cancels digits too (|b/3| > 4)
+    const int newton = fabsf(X.b3) > 4.f ? 2 : 1;
+    if (Delta * sp.i_delta < -46.f) {
+      // one real root: Cardano in its cancellation-free form
+      const float sD = sqrtf(-Delta * (1.f / 108.f));
+      const float u = cbrt_fast(Qv >= 0.f ? -0.5f * Qv - sD : -0.5f * Qv + sD);
+      const float s = fabsf(u) > 1e-30f ? u - Pv * rcpa(3.f * u) : u;
+      xpsq_t_implicit<O>(X, sp, w, s - X.b3, newton, &tv[0], tg[0], th[0]);
+#pragma unroll
+      for (int k = 1; k < 3; ++k) {
+        tv[k] = tv[0];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) tg[k][i] = tg[0][i];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) th[k][q] = th[0][q];
+      }
+      return true;
+    }
+    if (Delta * sp.i_delta > 46.f) {
+      // three real roots: trigonometric form, k = 0, 1, 2
+      const float rho = sqrtf(fmaxf(-Pv * (1.f / 3.f), 0.f));
+      const float th3 = atan2_pos(sqrtf(Delta * (1.f / 108.f)), -0.5f * Qv) * (1.f / 3.f);
+      float sn3, cs3;
+      __sincosf(th3, &sn3, &cs3);
+      const float ck[3] = {cs3, fmaf(-0.8660254037844386f, sn3, -0.5f * cs3),
+                           fmaf(0.8660254037844386f, sn3, -0.5f * cs3)};
+#pragma unroll 1
+      for (int k = 0; k < 3; ++k) xpsq_t_implicit<O>(X, sp, w, 2.f * rho * ck[k] - X.b3, newton, &tv[k], tg[k], th[k]);
+      return false;
+    }
+    constexpr int OC = O;
+    J2<OC> t2[3];
+    const bool single = soft_cardano_implicit<OC>(Pv, Qv, X.b3, sp, t2);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      tv[k] = t2[k].v;
       if constexpr (O >= 1) {
 #pragma unroll
-        for (int i = 0; i < 3; ++i) tk[k].g[i] = fmaf(t2[k].g[0], X.gP[i], t2[k].g[1] * X.gQ[i]);
+        for (int i = 0; i < 3; ++i) tg[k][i] = fmaf(t2[k].g[0], X.gP[i], t2[k].g[1] * X.gQ[i]);
       }
       if constexpr (O >= 2) {
 #pragma unroll
@@ -614,10 +722,29 @@ template <int O> __device__ CM_XINL void xpsq_eval(const Xpsq& X, const SmoothDe
           const int i = jhi<3>(q), j = jhj<3>(q);
           float v = t2[k].h[0] * X.gP[i] * X.gP[j];
           v = fmaf(t2[k].h[1], fmaf(X.gP[i], X.gQ[j], X.gQ[i] * X.gP[j]), v);
-          v = fmaf(t2[k].h[2], X.gQ[i] * X.gQ[j], v);
-          tk[k].h[q] = v;
+          th[k][q] = fmaf(t2[k].h[2], X.gQ[i] * X.gQ[j], v);
         }
       }
+    }
+    return single;
+  }
+  return true;
+}
+
+// XPSQ leaf (P:102-126) in its local frame
+template <int O> __device__ CM_XINL void xpsq_eval(const Xpsq& X, const SmoothDev& sp, const float* y, Res<O>& out) {
+  float w[3] = {y[0] - X.p1[0], y[1] - X.p1[1], y[2] - X.p1[2]};
+  J3<O> tk[3];
+  {
+    float tv[3], tg[3][3], th[3][6];
+    xpsq_root_t<O>(X, sp, w, tv, tg, th);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      tk[k].v = tv[k];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) tk[k].g[i] = tg[k][i];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) tk[k].h[q] = th[k][q];
     }
   }
   J3<O> yj[3] = {jvar<3, O>(y[0], 0), jvar<3, O>(y[1], 1), jvar<3, O>(y[2], 2)};
@@ -849,62 +976,6 @@ __device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3
     }
   }
   return !use_p;
-}
-
-// returns true when the three roots are bitwise identical (point / straight
-// splines, or the curved case when the positive-branch weight is exactly 0 in
-// FP32): then the three PSQ terms coincide and -LSE(-phi, -phi, -phi) =
-// phi - tau ln 3 exactly, so one PSQ evaluation suffices
-template <int O>
-__device__ __forceinline__ bool xpsq_root_t(const Xpsq& X, const SmoothDev& sp, const float* w, float* tv, float (*tg)[3],
-                                            float (*th)[6]) {
-  const float tc = sp.tau_clip_t, itc = sp.i_clip_t;
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    tv[k] = 0.5f;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) tg[k][i] = 0.f;
-#pragma unroll
-    for (int q = 0; q < 6; ++q) th[k][q] = 0.f;
-  }
-  if (X.cls == 1) {
-    const float s = X.Bn[0] * w[0] + X.Bn[1] * w[1] + X.Bn[2] * w[2];
-    float v, d1, d2;
-    softclip_12(s, 0.f, 1.f, tc, itc, v, d1, d2);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      tv[k] = v;
-#pragma unroll
-      for (int i = 0; i < 3; ++i) tg[k][i] = d1 * X.Bn[i];
-#pragma unroll
-      for (int q = 0; q < 6; ++q) th[k][q] = d2 * X.Bn[jhi<3>(q)] * X.Bn[jhj<3>(q)];
-    }
-  } else if (X.cls == 2) {
-    const float Pv = X.gP[0] * w[0] + X.gP[1] * w[1] + X.gP[2] * w[2] + X.P0;
-    const float Qv = X.gQ[0] * w[0] + X.gQ[1] * w[1] + X.gQ[2] * w[2] + X.Q0;
-    constexpr int OC = O;
-    J2<OC> t2[3];
-    const bool single = soft_cardano_implicit<OC>(Pv, Qv, X.b3, sp, t2);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      tv[k] = t2[k].v;
-      if constexpr (O >= 1) {
-#pragma unroll
-        for (int i = 0; i < 3; ++i) tg[k][i] = fmaf(t2[k].g[0], X.gP[i], t2[k].g[1] * X.gQ[i]);
-      }
-      if constexpr (O >= 2) {
-#pragma unroll
-        for (int q = 0; q < 6; ++q) {
-          const int i = jhi<3>(q), j = jhj<3>(q);
-          float v = t2[k].h[0] * X.gP[i] * X.gP[j];
-          v = fmaf(t2[k].h[1], fmaf(X.gP[i], X.gQ[j], X.gQ[i] * X.gP[j]), v);
-          th[k][q] = fmaf(t2[k].h[2], X.gQ[i] * X.gQ[j], v);
-        }
-      }
-    }
-    return single;
-  }
-  return true;
 }
 
 template <int O>

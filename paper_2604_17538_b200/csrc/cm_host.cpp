@@ -71,7 +71,7 @@ bool finite_all(const float* p, int n) {
 
 // XPSQ classification thresholds (reading #14; the same rule is
 // written independently in the oracle)
-constexpr double X_EPS_POINT = 1e-6, X_EPS_LINE = 1e-2, X_EPS_FRAME = 1e-3;
+constexpr double X_EPS_POINT = 1e-6, X_EPS_LINE = 1e-4, X_EPS_FRAME = 1e-3;
 
 Xpsq pack_xpsq(const cm_node& n) {
   Xpsq X;
@@ -84,8 +84,10 @@ Xpsq pack_xpsq(const cm_node& n) {
   if (nA < X_EPS_POINT && nB < X_EPS_POINT) {
     X.cls = 0;
   } else if (nA < X_EPS_LINE * nB) {
+    // straight: the chord p1 -> p3 (B := A + B = p3 - p1, A := 0; both end
+    // points kept, within |A|/4 of the spline)
     X.cls = 1;
-    for (int i = 0; i < 3; ++i) { A[i] = 0; T0[i] = B[i]; }
+    for (int i = 0; i < 3; ++i) { B[i] += A[i]; A[i] = 0; T0[i] = B[i]; }
   } else {
     X.cls = 2;
     for (int i = 0; i < 3; ++i) T0[i] = A[i] + B[i];
@@ -137,6 +139,9 @@ Xpsq pack_xpsq(const cm_node& n) {
       X.gP[i] = (float)(2 * A[i] / c3);
       X.gQ[i] = (float)((B[i] - (2 * b / 3) * A[i]) / c3);
     }
+    X.c3 = (float)c3;
+    X.c2 = (float)c2;
+    X.BB = (float)BB;
     X.P0 = (float)(-BB / c3 - b * b / 3);
     X.Q0 = (float)(2 * b * b * b / 27 + (b / 3) * BB / c3);
     X.b3 = (float)(b / 3);
@@ -204,6 +209,8 @@ struct cm_scene {
   std::mutex mu;
   cudaStream_t aux[cmi::kManifoldStreams] = {};
   cudaEvent_t ev_fork = nullptr, ev_join[cmi::kManifoldStreams] = {};
+  int64_t manifold_calls = 0;   // under mu
+  unsigned long long last_capture_id = 0;   // capture of the last manifold call (0: none)
 };
 
 // aux streams used per manifold call (CM_MANIFOLD_STREAMS=1 serialises the
@@ -688,14 +695,30 @@ int cm_contact_manifold(const cm_scene* sc, const int32_t* pairs, int64_t n_pair
   cm_scene* ms = const_cast<cm_scene*>(sc);   // internal scheduling state only
   std::lock_guard<std::mutex> lock(ms->mu);
   cudaStream_t st = (cudaStream_t)stream;
-  // fork: the aux streams wait for the caller's prior work; join: the
-  // caller's stream waits for every chunk
+  // fork: the aux streams wait for the caller's prior work and for every aux
+  // stream's part of the previous manifold call on this scene (its join
+  // events): how a call splits the scratch between the streams depends on its
+  // tier and mode, so two calls must never overlap on the device, whichever
+  // streams they were issued from; join: the caller's stream waits for every
+  // chunk
   if (cudaEventRecord(ms->ev_fork, st) != cudaSuccess) return fail(CM_ERR_CUDA, "cm_contact_manifold: event record");
+  // (under stream capture only join events recorded by the same capture can
+  // be waited on: a captured graph's calls are ordered by its own edges)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  unsigned long long cap_id = 0;
+  if (cudaStreamGetCaptureInfo(st, &cap, &cap_id) != cudaSuccess) return fail(CM_ERR_CUDA, "cm_contact_manifold: capture info");
+  if (cap != cudaStreamCaptureStatusActive) cap_id = 0;
+  const bool wait_prev = ms->manifold_calls > 0 && ms->last_capture_id == cap_id;
   void* aux[cmi::kManifoldStreams];
   for (int i = 0; i < cmi::kManifoldStreams; ++i) {
     cudaStreamWaitEvent(ms->aux[i], ms->ev_fork, 0);
+    if (wait_prev)
+      for (int j = 0; j < cmi::kManifoldStreams; ++j)
+        if (j != i) cudaStreamWaitEvent(ms->aux[i], ms->ev_join[j], 0);
     aux[i] = ms->aux[i];
   }
+  ++ms->manifold_calls;
+  ms->last_capture_id = cap_id;
   int rc = cml::launch_manifold(sc->dev, sc->class_mask, sc->max_V, sc->max_E, pairs, n_pairs, offsets, poses, n_slot,
                                 flags, out, n_contacts, sc->scratch, sc->scratch_floats, aux, n_aux_streams());
   for (int i = 0; i < cmi::kManifoldStreams; ++i) {

@@ -45,13 +45,14 @@ struct Leaf {
   float cull[4];
 };
 
-// XPSQ static data: p(t) = p1 + B t + A t^2 (A := 0 for the
-// snapped straight class), projection cubic constants in the affine form
+// XPSQ static data: p(t) = p1 + B t + A t^2 (A := 0, B := p3 - p1
+// for the snapped straight class), projection cubic constants in the affine form
 //   P = gP . w + P0,  Q = gQ . w + Q0,  w = y - p1
 // (c3, c2 depend only on the spline; c1, c0 are affine in w), b3 = b/3.
 struct Xpsq {
   float p1[3], A[3], B[3];
   float gP[3], gQ[3], P0, Q0, b3;
+  float c3, c2, BB;       // the cubic in t: c3 t^3 + c2 t^2 + (2 A.w - BB) t + B.w
   float Bn[3];            // straight class: t = softclip(Bn . w)
   float bhat[3];          // Frenet binormal (constant for a quadratic)
   float R0[9];            // constant frame (straight / point / A || B)
