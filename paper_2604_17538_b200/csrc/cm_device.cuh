@@ -29,6 +29,15 @@ using namespace cmi;
 #ifndef CM_XPSQ_INLINE_MAX_O
 #define CM_XPSQ_INLINE_MAX_O 2   // constant-schedule XPSQ inlined up to this order
 #endif
+#ifndef CM_SQ_SHARED_W
+#define CM_SQ_SHARED_W 1      // SQ weights from the LSE exponentials (fewer MUFU ops)
+#endif
+#ifndef CM_SOFTCLIP_FAST
+#define CM_SOFTCLIP_FAST 1    // softclip interior shortcut
+#endif
+#ifndef CM_LEAF_LAZY_R
+#define CM_LEAF_LAZY_R 1      // leaf rotation loaded only for rotated leaves
+#endif
 #ifndef CM_SHAPE_NOINLINE
 #define CM_SHAPE_NOINLINE 0
 #endif
@@ -81,10 +90,12 @@ __device__ __forceinline__ float softclip_d(float x, float lo, float hi, float i
 }
 // s+(x; tau) and sigma(x / tau) from one exponential e = exp(-|x|/tau):
 // s+ = max(x, 0) + tau log(1 + e), sigma = 1/(1+e) (x >= 0) or e/(1+e)
-__device__ __forceinline__ void softplus_sig(float x, float tau, float itau, float& sp, float& sg) {
-  const float e = ex2(-fabsf(x) * (itau * LOG2E));
+// (e and r = 1/(1+e) are returned too: sigma (1 - sigma) = e r^2 without
+// the cancellation of 1 - sigma)
+__device__ __forceinline__ void softplus_sig(float x, float tau, float itau, float& sp, float& sg, float& e, float& r) {
+  e = ex2(-fabsf(x) * (itau * LOG2E));
   sp = fmaxf(x, 0.f) + (tau * LN2) * lg2(1.f + e);
-  const float r = rcpa(1.f + e);
+  r = rcpa(1.f + e);
   sg = x >= 0.f ? r : e * r;
 }
 // softclip value with its first and second derivatives (two exponentials)
@@ -92,18 +103,19 @@ __device__ __forceinline__ void softclip_12(float x, float lo, float hi, float t
                                             float& d2) {
   // interior: both exponentials are below 2^-144 and flush to 0 (ftz), so the
   // general path below returns exactly lo + (x - lo), 1, 0 -- skip its 6 MUFU ops
-  if ((x - lo) * itau > 100.f && (hi - x) * itau > 100.f) {
+  if (CM_SOFTCLIP_FAST && (x - lo) * itau > 100.f && (hi - x) * itau > 100.f) {
     v = lo + (x - lo);
     d1 = 1.f;
     d2 = 0.f;
     return;
   }
-  float sp1, s1, sp2, s2;
-  softplus_sig(x - lo, tau, itau, sp1, s1);
-  softplus_sig(x - hi, tau, itau, sp2, s2);
+  float sp1, s1, e1, r1, sp2, s2, e2, r2;
+  softplus_sig(x - lo, tau, itau, sp1, s1, e1, r1);
+  softplus_sig(x - hi, tau, itau, sp2, s2, e2, r2);
   v = lo + sp1 - sp2;
-  d1 = s1 - s2;
-  d2 = (s1 * (1.f - s1) - s2 * (1.f - s2)) * itau;
+  // above hi both sigmas are ~1: their difference is (e2 - e1) r1 r2
+  d1 = x >= hi ? (e2 - e1) * r1 * r2 : s1 - s2;
+  d2 = (e1 * r1 * r1 - e2 * r2 * r2) * itau;
 }
 
 // cube root from the MUFU log / exp plus one Newton step (rel. error ~1e-7)
@@ -275,12 +287,18 @@ template <int O, class SP> __device__ __forceinline__ void sq_eval(const SP& Lf,
   float omh = 1.f - h;
   r.v = rad * omh;
   if constexpr (O >= 1) {
+#if CM_SQ_SHARED_W
     const float rS = rcpa(1.f + eS), rf = rcpa(1.f + ef);
     const bool a0big = la0 >= la1, bbig = lB >= l3;
     float w0 = a0big ? rS : eS * rS, w1 = a0big ? eS * rS : rS;   // A_i / S
     float be = bbig ? rf : ef * rf, ga = bbig ? ef * rf : rf;      // B / f, C / f
     const float r01 = rcpa(q0 * q1);   // q >= 1e-12: the product stays normal
     float iq0 = q1 * r01, iq1 = q0 * r01, iq2 = rcpa(q2);
+#else
+    float w0 = ex2(la0 - lS), w1 = ex2(la1 - lS);
+    float be = ex2(lB - lf), ga = ex2(l3 - lf);
+    float iq0 = rcpa(q0), iq1 = rcpa(q1), iq2 = rcpa(q2);
+#endif
     float s0 = u0 * ia0 * iq0, s1 = u1 * ia1 * iq1, s2 = u2 * ia2 * iq2;
     float tp1 = 2.f * p1;
     float L0 = tp1 * be * w0 * s0, L1 = tp1 * be * w1 * s1, L2 = tp1 * ga * s2;
@@ -852,14 +870,20 @@ __device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3
   const float eD = ex2(-fabsf(Delta) * (itd * LOG2E));
   const float rD = rcpa(1.f + eD);
   const float wp = Delta >= 0.f ? rD : eD * rD, wn = Delta >= 0.f ? eD * rD : rD;
-  const float lgD = (td * LN2) * lg2(1.f + eD);
+  // tau log(1 + e): log1p form below 1e-2 (1 + e rounds e away in FP32, and
+  // the projected discriminants s+(+-Delta) below enter square / cube roots
+  // whose derivatives need them to full relative precision)
+  const float lgD = td * (eD < 1e-2f ? eD * fmaf(-eD, fmaf(-eD, 1.f / 3.f, 0.5f), 1.f) : LN2 * lg2(1.f + eD));
+  // blend weights and their derivatives; sigma (1 - sigma) = wn wp and
+  // 1 - 2 sigma = wn - wp with both weights formed directly (1 - wn rounds
+  // the smaller weight away: 20% off at |Delta| = 17 tau in FP32)
+  const float ww = wn * wp;
   const float sp1 = wp;                                 // s+'(Delta)
-  const float sp2 = sp1 * (1.f - sp1) * itd;            // s+''(Delta)
+  const float sp2 = ww * itd;                           // s+''(Delta)
   const float spD = fmaxf(Delta, 0.f) + lgD;           // s+(Delta)
-  // blend weights and their derivatives
-  const float dwn = -wn * (1.f - wn) * itd, dwp = wp * (1.f - wp) * itd;
-  const float ddwn = wn * (1.f - wn) * (1.f - 2.f * wn) * itd * itd;
-  const float ddwp = wp * (1.f - wp) * (1.f - 2.f * wp) * itd * itd;
+  const float dwn = -ww * itd, dwp = ww * itd;
+  const float ddwn = ww * (wp - wn) * itd * itd;
+  const float ddwp = ww * (wn - wp) * itd * itd;
   // derivatives of the modified coefficient and of the root
   auto root_derivs = [&](float s, float Pt, const float* Pa, const float* Pab, float* sa, float* sab) {
     const float Fs = fmaf(3.f * s, s, Pt);
@@ -890,7 +914,11 @@ __device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3
   constexpr float W_SKIP = 1e-20f;   // negligible branches are skipped (reading #34)
   const bool use_n = wn > W_SKIP, use_p = wp > W_SKIP;
   if (use_n) {
-    const float W = fmaf(0.25f, spD, P3);
+    // W = P^3 + s+(Delta)/4; above Delta = 0 its two terms cancel (P^3 ~
+    // -s+(Delta)/4 near the cusp, reading #15): there the identity s+(Delta)
+    // = Delta + s+(-Delta), Delta = -(4 P^3 + 27 Q^2), gives the
+    // cancellation-free W = (s+(-Delta) - 27 Q^2) / 4
+    const float W = Delta > 0.f ? 0.25f * fmaf(-27.f * Q, Q, lgD) : fmaf(0.25f, spD, P3);
     const float Pm = cbrt_fast(W);
     // Cardano's cancellation-free form: u = cbrt(-Q/2 - sign(Q) sqrt(D)), v = -Pm/(3u)
     const float D = (fmaxf(-Delta, 0.f) + lgD) * (1.f / 108.f);   // s+(-Delta) / 108
@@ -899,12 +927,14 @@ __device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3
     const float s = fabsf(u) > 1e-30f ? u - Pm * rcpa(3.f * u) : u;
     float sa[2] = {0.f, 0.f}, sab[3] = {0.f, 0.f, 0.f};
     if constexpr (O >= 1) {
-      const float Wa[2] = {fmaf(3.f, P2, 0.25f * sp1 * Dl[0]), 0.25f * sp1 * Dl[1]};
+      // dW/dP = 3 P^2 (1 - s+') = 3 P^2 wn, dW/dQ = -13.5 Q wp (1 - wp
+      // formed as wn: no cancellation where the negative branch is weak)
+      const float Wa[2] = {3.f * P2 * wn, 0.25f * sp1 * Dl[1]};
       const float ip2 = rcpa(fmaxf(3.f * Pm * Pm, 1e-30f));   // guarded at the cusp (reading #15)
       const float Pa[2] = {Wa[0] * ip2, Wa[1] * ip2};
       float Pab[3] = {0.f, 0.f, 0.f};
       if constexpr (O >= 2) {
-        const float Wab[3] = {fmaf(6.f, P, 0.25f * fmaf(sp2 * Dl[0], Dl[0], sp1 * Dll[0])),
+        const float Wab[3] = {fmaf(6.f * P, wn, 0.25f * sp2 * Dl[0] * Dl[0]),   // 6P + s+' Delta_PP/4 = 6 P wn
                               0.25f * sp2 * Dl[0] * Dl[1], 0.25f * fmaf(sp2 * Dl[1], Dl[1], sp1 * Dll[2])};
         const float den = 3.f * Pm * Pm * Pm;
         const float c = 2.f * ip2 * rcpa(fabsf(den) > 1e-30f ? den : copysignf(1e-30f, den));
@@ -917,40 +947,78 @@ __device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3
     clip(s, sa, sab, tm, tma, tmab);
   }
   if (use_p) {
-    const float V = fmaf(0.25f * Q, Q, spD * (1.f / 108.f));
+    // trigonometric form: with X = -Q/2, Y = sqrt(D), D = s+(Delta)/108,
+    // z = X + iY = sqrt(V) e^(i th), V = X^2 + Y^2, the roots are
+    // s_k = w_k + conj(w_k), w_k = z^(1/3) e^(2 pi i k/3) = rho e^(i phi_k).
+    // Derivatives straight from the cube roots (no implicit 1/F'(s), which
+    // is 0/0 when two roots nearly coincide at a small positive weight):
+    //   ds_k = (2/3) Re(E_k dz),  E_k = w_k / z = V^(-1/3) e^(i(phi_k - th)),
+    //   d2s_k = 2 Re((-2/9) F_k dz dz + (1/3) E_k d2z),  F_k = w_k / z^2,
+    //   dX = -dQ/2, dY = s+'(Delta) dDelta / (216 Y),
+    //   d2Y = (s+'' dDelta dDelta + s+' d2Delta) / (216 Y) - (s+' / Y)^2 dDelta dDelta / (46656 Y)
+    const float D = spD * (1.f / 108.f);
+    const float V = fmaf(0.25f * Q, Q, D);
     const float rho = ex2(lg2(V) * (1.f / 6.f));
-    // roots 2 rho cos((th + 2 pi k)/3) from one sincos of th/3 (angle addition)
-    const float th3 = atan2_pos(sqrtf(spD * (1.f / 108.f)), -0.5f * Q) * (1.f / 3.f);
+    const float Y = sqrtf(D);
+    const float th3 = atan2_pos(Y, -0.5f * Q) * (1.f / 3.f);
     float sn3, cs3;
     __sincosf(th3, &sn3, &cs3);
     const float ck1 = fmaf(-0.8660254037844386f, sn3, -0.5f * cs3), ck2 = fmaf(0.8660254037844386f, sn3, -0.5f * cs3);
-    float Pa[2] = {0.f, 0.f}, Pab[3] = {0.f, 0.f, 0.f};
-    const float Pt = -3.f * rho * rho;
+    constexpr float C120 = -0.5f, S120 = 0.8660254037844386f;   // e^(2 pi i / 3)
+    float Ya[2] = {0.f, 0.f}, Yab[3] = {0.f, 0.f, 0.f}, e_re = 0.f, e_im = 0.f, f_re = 0.f, f_im = 0.f;
     if constexpr (O >= 1) {
-      const float Va[2] = {sp1 * Dl[0] * (1.f / 108.f), fmaf(0.5f, Q, sp1 * Dl[1] * (1.f / 108.f))};
-      const float iV23 = rcpa(fmaxf(rho * rho * rho * rho, 1e-30f));   // V^(-2/3)
-      Pa[0] = -Va[0] * iV23;
-      Pa[1] = -Va[1] * iV23;
+      const float iY = rsqrtf(fmaxf(D, 1e-37f));
+      const float A1 = sp1 * iY;                               // s+'(Delta) / Y
+      Ya[0] = A1 * Dl[0] * (1.f / 216.f);
+      Ya[1] = A1 * Dl[1] * (1.f / 216.f);
+      const float iV13 = rcpa(fmaxf(rho * rho, 1e-30f));      // V^(-1/3)
+      float s2, c2;
+      __sincosf(2.f * th3, &s2, &c2);                          // E_0 phase -2 th / 3
+      e_re = iV13 * c2;
+      e_im = -iV13 * s2;
       if constexpr (O >= 2) {
-        const float Vab[3] = {fmaf(sp2 * Dl[0], Dl[0], sp1 * Dll[0]) * (1.f / 108.f),
-                              sp2 * Dl[0] * Dl[1] * (1.f / 108.f),
-                              fmaf(fmaf(sp2 * Dl[1], Dl[1], sp1 * Dll[2]), 1.f / 108.f, 0.5f)};
-        const float c = (2.f / 3.f) * iV23 * rcpa(fmaxf(V, 1e-30f));
-        Pab[0] = fmaf(c, Va[0] * Va[0], -Vab[0] * iV23);
-        Pab[1] = fmaf(c, Va[0] * Va[1], -Vab[1] * iV23);
-        Pab[2] = fmaf(c, Va[1] * Va[1], -Vab[2] * iV23);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const int i = q == 2 ? 1 : 0, j = q == 0 ? 0 : 1;
+          Yab[q] = fmaf(fmaf(sp2 * Dl[i], Dl[j], sp1 * Dll[q]), iY * (1.f / 216.f),
+                        -A1 * A1 * iY * Dl[i] * Dl[j] * (1.f / 46656.f));
+        }
+        float s5, c5;
+        __sincosf(5.f * th3, &s5, &c5);                        // F_0 phase -5 th / 3
+        const float iV56 = iV13 * rsqrtf(fmaxf(V, 1e-30f));     // V^(-5/6)
+        f_re = iV56 * c5;
+        f_im = -iV56 * s5;
       }
     }
+    const float Xa[2] = {0.f, -0.5f};
 #pragma unroll 1
     for (int k = 0; k < 3; ++k) {
       const float s = 2.f * rho * (k == 0 ? cs3 : (k == 1 ? ck1 : ck2));
       float sa[2] = {0.f, 0.f}, sab[3] = {0.f, 0.f, 0.f};
-      if constexpr (O >= 1) root_derivs(s, Pt, Pa, Pab, sa, sab);
+      if constexpr (O >= 1) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) sa[i] = (2.f / 3.f) * fmaf(e_re, Xa[i], -e_im * Ya[i]);
+        if constexpr (O >= 2) {
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            const int i = q == 2 ? 1 : 0, j = q == 0 ? 0 : 1;
+            const float zz_re = fmaf(Xa[i], Xa[j], -Ya[i] * Ya[j]), zz_im = fmaf(Xa[i], Ya[j], Ya[i] * Xa[j]);
+            const float fz = fmaf(f_re, zz_re, -f_im * zz_im);
+            sab[q] = 2.f * fmaf(-2.f / 9.f, fz, (-1.f / 3.f) * e_im * Yab[q]);
+          }
+        }
+      }
       float v, va[2], vab[3];
       clip(s, sa, sab, v, va, vab);
       tp[k] = v;
       tpa[k][0] = va[0]; tpa[k][1] = va[1];
       if constexpr (O >= 2) { tpab[k][0] = vab[0]; tpab[k][1] = vab[1]; tpab[k][2] = vab[2]; }
+      // next root: E_k and F_k turn by e^(2 pi i / 3)
+      const float er = e_re, fr = f_re;
+      e_re = fmaf(er, C120, -e_im * S120);
+      e_im = fmaf(er, S120, e_im * C120);
+      f_re = fmaf(fr, C120, -f_im * S120);
+      f_im = fmaf(fr, S120, f_im * C120);
     }
   }
   // blend t_k = wn t- + wp t+_k (product rule)
@@ -1118,11 +1186,17 @@ __device__ __forceinline__ void leaf_eval(const SceneDev& S, int li, const float
   float t[3] = {L.t[0], L.t[1], L.t[2]};
   const bool ident = L.rot_identity != 0;
   float R[9];
+#if !CM_LEAF_LAZY_R
 #pragma unroll
   for (int i = 0; i < 9; ++i) R[i] = L.R[i];
+#endif
   if (ident) {
     y[0] = x[0] - t[0]; y[1] = x[1] - t[1]; y[2] = x[2] - t[2];
-  } else {
+  } else {   // (the rotation is loaded only for rotated leaves)
+#if CM_LEAF_LAZY_R
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R[i] = L.R[i];
+#endif
     to_local(R, t, x, y);
   }
   Res<O> l;

@@ -211,6 +211,7 @@ struct cm_scene {
   cudaEvent_t ev_fork = nullptr, ev_join[cmi::kManifoldStreams] = {};
   int64_t manifold_calls = 0;   // under mu
   unsigned long long last_capture_id = 0;   // capture of the last manifold call (0: none)
+  int last_tier = -1;                        // tier of the last manifold call (its scratch layout)
 };
 
 // aux streams used per manifold call (CM_MANIFOLD_STREAMS=1 serialises the
@@ -695,12 +696,14 @@ int cm_contact_manifold(const cm_scene* sc, const int32_t* pairs, int64_t n_pair
   cm_scene* ms = const_cast<cm_scene*>(sc);   // internal scheduling state only
   std::lock_guard<std::mutex> lock(ms->mu);
   cudaStream_t st = (cudaStream_t)stream;
-  // fork: the aux streams wait for the caller's prior work and for every aux
-  // stream's part of the previous manifold call on this scene (its join
-  // events): how a call splits the scratch between the streams depends on its
-  // tier and mode, so two calls must never overlap on the device, whichever
-  // streams they were issued from; join: the caller's stream waits for every
-  // chunk
+  // fork: the aux streams wait for the caller's prior work and, when the
+  // previous manifold call on this scene used another tier, for every aux
+  // stream's part of that call (its join events): how a call splits the
+  // scratch between the streams depends on its tier, so calls of different
+  // tiers must never overlap on the device, whichever streams they were
+  // issued from; calls of the same tier give each aux stream the same
+  // scratch region, already ordered by that stream.  join: the caller's
+  // stream waits for every chunk
   if (cudaEventRecord(ms->ev_fork, st) != cudaSuccess) return fail(CM_ERR_CUDA, "cm_contact_manifold: event record");
   // (under stream capture only join events recorded by the same capture can
   // be waited on: a captured graph's calls are ordered by its own edges)
@@ -708,7 +711,8 @@ int cm_contact_manifold(const cm_scene* sc, const int32_t* pairs, int64_t n_pair
   unsigned long long cap_id = 0;
   if (cudaStreamGetCaptureInfo(st, &cap, &cap_id) != cudaSuccess) return fail(CM_ERR_CUDA, "cm_contact_manifold: capture info");
   if (cap != cudaStreamCaptureStatusActive) cap_id = 0;
-  const bool wait_prev = ms->manifold_calls > 0 && ms->last_capture_id == cap_id;
+  const int tier_now = (int)(flags & CM_TIER_MASK);
+  const bool wait_prev = ms->manifold_calls > 0 && ms->last_capture_id == cap_id && ms->last_tier != tier_now;
   void* aux[cmi::kManifoldStreams];
   for (int i = 0; i < cmi::kManifoldStreams; ++i) {
     cudaStreamWaitEvent(ms->aux[i], ms->ev_fork, 0);
@@ -719,6 +723,7 @@ int cm_contact_manifold(const cm_scene* sc, const int32_t* pairs, int64_t n_pair
   }
   ++ms->manifold_calls;
   ms->last_capture_id = cap_id;
+  ms->last_tier = tier_now;
   int rc = cml::launch_manifold(sc->dev, sc->class_mask, sc->max_V, sc->max_E, pairs, n_pairs, offsets, poses, n_slot,
                                 flags, out, n_contacts, sc->scratch, sc->scratch_floats, aux, n_aux_streams());
   for (int i = 0; i < cmi::kManifoldStreams; ++i) {

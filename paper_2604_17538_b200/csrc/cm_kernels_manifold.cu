@@ -61,6 +61,27 @@ __device__ __forceinline__ void st4(float* p, float a, float b, float c, float d
   *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
 }
 
+// ---- TMA bulk copies (cp.async.bulk global -> shared, mbarrier completion)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// global -> shared bulk copy of `bytes` (multiple of 16, 16-B aligned ends)
+// by the calling thread; completion is counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n"
+      ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+
 struct PairFrame {
   float RA[9], tA[3], RB[9], tB[3];
   float Rrel[9], trel[3];   // x_B = Rrel v_A + trel
@@ -306,6 +327,12 @@ static_assert(sizeof(UnitCtx) % 16 == 0, "UnitCtx is copied as float4");
 // threads per unit CTA: 64 for large batches (lane use on V = 56..98 meshes);
 // small batches get up to CM_MF_MAX_THREADS so the SMs still fill
 #define CM_N_CLASSES 5   // SDF classes (cm_internal.h ShapeRec::uses_xpsq)
+#ifndef CM_MF_STAGE_MID
+#define CM_MF_STAGE_MID 0   // TMA-staged trace records in the midpoint kernel: C5 -7%, C4 -0.5% (r02i sweep)
+#endif
+#ifndef CM_TRACE6
+#define CM_TRACE6 1         // 6-component trace derivative recursion (tiers 0-2)
+#endif
 #ifndef CM_MF_THREADS
 #define CM_MF_THREADS 64
 #endif
@@ -657,13 +684,112 @@ __device__ __forceinline__ void mf_traces_unit(const MfArgs& a, const UnitCtx& U
   }
 }
 
+// Tiers 0-2: the tier-2 derivative recursion carried in 6 components
+// instead of 9: every g^T J(p) = [g, (p - tA) x g, g x (p - tB)]
+// is [X, Y - tA x X, -Y + tB x X] with X = g, Y = p x g, a form the
+// recursion d alpha_{k+1} = d alpha_k + c [(g.e_t) d alpha_k + g^T J(p)]
+// preserves (X <- X + c (ge X + g), Y <- Y + c (ge Y + p x g)); the 9
+// components are formed once, after the clip.
+template <int TIER, int XP>
+__device__ __forceinline__ void mf_traces_unit_n(const MfArgs& a, const UnitCtx& U, int u) {
+  static_assert(TIER <= 2, "tier 3 carries second derivatives: mf_traces_unit");
+  constexpr int OT = TIER >= 2 ? 1 : 0;
+  const SmoothDev sp = a.S.sp;
+  const float itcmp = sp.i_cmp;
+  const float tca = sp.tau_clip_alpha, itca = sp.i_clip_alpha;
+  const PairFrame& F = U.F;
+  const int V = U.SA.V, E = U.SA.E;
+  const float* sv = a.scratch + (int64_t)u * a.slot;
+  float* se = a.scratch + (int64_t)u * a.slot + (int64_t)vrec(TIER) * V;
+  const float* lv = a.S.verts + 4 * (int64_t)U.SA.v_off;
+  const int32_t* ed = a.S.edges + 2 * (int64_t)U.SA.e_off;
+  for (int j = threadIdx.x; j < 2 * E; j += blockDim.x) {
+    const int e = j < E ? j : j - E;
+    const int dir = j < E ? 0 : 1;     // 0: from v_I along +e_t; 1: from v_II along -e_t
+    const int vI = __ldg(ed + 2 * e), vII = __ldg(ed + 2 * e + 1);
+    const float4 corner = ld4(sv + (dir ? vII : vI) * vrec(TIER));   // d, n of the start vertex
+    float xl[3], el[3], L;
+    {
+      const float4 xa = ldv(lv, vI), xb4 = ldv(lv, vII);
+      const float dl[3] = {xb4.x - xa.x, xb4.y - xa.y, xb4.z - xa.z};
+      L = sqrtf(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
+      const float iL = 1.f / L;
+      el[0] = dl[0] * iL; el[1] = dl[1] * iL; el[2] = dl[2] * iL;
+      xl[0] = xa.x; xl[1] = xa.y; xl[2] = xa.z;
+    }
+    float eb[3], ew[3];
+    rot_vec(F.Rrel, el, eb);
+    rot_vec(F.RA, el, ew);
+    float xI[3], pI[3];
+    to_frames(F, xl, xI, pI);
+    float al = dir ? L : 0.f;
+    const float sgn = dir ? -1.f : 1.f;
+    float X[3] = {0.f, 0.f, 0.f}, Y[3] = {0.f, 0.f, 0.f};
+    float phi = corner.x;
+    float g[3] = {corner.y, corner.z, corner.w};   // the corner itself: the vertex evaluation (reading #22)
+#pragma unroll 1
+    for (int it = 0; it < sp.iters; ++it) {
+      if (it > 0) {
+        const float xb[3] = {fmaf(al, eb[0], xI[0]), fmaf(al, eb[1], xI[1]), fmaf(al, eb[2], xI[2])};
+        Res<OT> r;
+        CM_EVAL(OT, XP)(a.S, U.SB, xb, r);
+        phi = r.v;
+        if constexpr (TIER >= 2) rot_vec(F.RB, r.g, g);
+      }
+      // gated step G(phi) = sigma(phi / tau) phi  (reading #20)
+      const float s = sigm(phi * itcmp);
+      if constexpr (TIER >= 2) {
+        const float Gp = fmaf(phi * s * (1.f - s), itcmp, s);
+        const float p[3] = {fmaf(al, ew[0], pI[0]), fmaf(al, ew[1], pI[1]), fmaf(al, ew[2], pI[2])};
+        const float m[3] = {p[1] * g[2] - p[2] * g[1], p[2] * g[0] - p[0] * g[2], p[0] * g[1] - p[1] * g[0]};
+        const float ge = g[0] * ew[0] + g[1] * ew[1] + g[2] * ew[2];
+        const float c = sgn * Gp;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          X[k] = fmaf(c, fmaf(ge, X[k], g[k]), X[k]);
+          Y[k] = fmaf(c, fmaf(ge, Y[k], m[k]), Y[k]);
+        }
+      }
+      al = fmaf(sgn * s, phi, al);
+    }
+    // soft clip to the edge (reading #21)
+    float* rec = se + e * erec(TIER) + (dir ? trace_b(TIER) : 0);
+    float at, c1, c2;
+    softclip_12(al, 0.f, L, tca, itca, at, c1, c2);
+    if constexpr (TIER >= 2) {
+      const float* tA = F.tA;
+      const float* tB = F.tB;
+      // d alpha = [X, Y - tA x X, -Y + tB x X], times the clip derivative
+      const float o[10] = {at, c1 * X[0], c1 * X[1], c1 * X[2],
+                           c1 * (Y[0] - (tA[1] * X[2] - tA[2] * X[1])),
+                           c1 * (Y[1] - (tA[2] * X[0] - tA[0] * X[2])),
+                           c1 * (Y[2] - (tA[0] * X[1] - tA[1] * X[0])),
+                           c1 * (-Y[0] + (tB[1] * X[2] - tB[2] * X[1])),
+                           c1 * (-Y[1] + (tB[2] * X[0] - tB[0] * X[2])),
+                           c1 * (-Y[2] + (tB[0] * X[1] - tB[1] * X[0]))};
+      if (dir == 0) {   // record floats 0-9: two float4 + one float2
+        st4(rec, o[0], o[1], o[2], o[3]);
+        st4(rec + 4, o[4], o[5], o[6], o[7]);
+        *reinterpret_cast<float2*>(rec + 8) = make_float2(o[8], o[9]);
+      } else {          // record floats 10-19: one float2 + two float4
+        *reinterpret_cast<float2*>(rec) = make_float2(o[0], o[1]);
+        st4(rec + 2, o[2], o[3], o[4], o[5]);
+        st4(rec + 6, o[6], o[7], o[8], o[9]);
+      }
+    } else {
+      *rec = at;
+    }
+  }
+}
+
 // ---- phase 3: edge points p_e = v_I + a_bar e_t, a_bar = (a_I + a_II)/2
 template <int TIER, int XP>
-__device__ __forceinline__ void mf_midpoints_unit(const MfArgs& a, const UnitCtx& U, int u) {
+__device__ __forceinline__ void mf_midpoints_unit(const MfArgs& a, const UnitCtx& U, int u, const float* srec) {
   constexpr int OV = TIER >= 2 ? 2 : 1;
   const PairFrame& F = U.F;
   const int V = U.SA.V, E = U.SA.E;
   float* se = a.scratch + (int64_t)u * a.slot + (int64_t)vrec(TIER) * V;
+  if (srec == nullptr) srec = se;   // trace records: staged in shared memory, or the slot
   const float* eg = a.S.edge_geom + 8 * (int64_t)U.SA.e_off;
   const bool full = (a.mode & CM_FULL_MODE) != 0;
   const float itcmp = a.S.sp.i_cmp;
@@ -674,27 +800,28 @@ __device__ __forceinline__ void mf_midpoints_unit(const MfArgs& a, const UnitCtx
     rot_vec(F.Rrel, el, eb);
     rot_vec(F.RA, el, ew);
     float* rec = se + e * erec(TIER);
+    const float* rin = srec + e * erec(TIER);
     float ab, dab[NDQ];
     float d2ab[TIER >= 3 ? N45 : 1];
     if constexpr (TIER >= 3) {
-      const float* rb2 = rec + trace_b(TIER);
-      ab = 0.5f * (rec[0] + rb2[0]);
+      const float* rb2 = rin + trace_b(TIER);
+      ab = 0.5f * (rin[0] + rb2[0]);
 #pragma unroll
-      for (int k = 0; k < NDQ; ++k) dab[k] = 0.5f * (rec[1 + k] + rb2[1 + k]);
+      for (int k = 0; k < NDQ; ++k) dab[k] = 0.5f * (rin[1 + k] + rb2[1 + k]);
 #pragma unroll
-      for (int k = 0; k < N45; ++k) d2ab[k] = 0.5f * (rec[TD2 + k] + rb2[TD2 + k]);
+      for (int k = 0; k < N45; ++k) d2ab[k] = 0.5f * (rin[TD2 + k] + rb2[TD2 + k]);
     } else if constexpr (TIER >= 2) {
       float t[20];
 #pragma unroll
       for (int q = 0; q < 5; ++q) {
-        const float4 v4 = ld4(rec + 4 * q);
+        const float4 v4 = ld4(rin + 4 * q);
         t[4 * q] = v4.x; t[4 * q + 1] = v4.y; t[4 * q + 2] = v4.z; t[4 * q + 3] = v4.w;
       }
       ab = 0.5f * (t[0] + t[10]);
 #pragma unroll
       for (int k = 0; k < NDQ; ++k) dab[k] = 0.5f * (t[1 + k] + t[11 + k]);
     } else {
-      ab = 0.5f * (rec[0] + rec[1]);
+      ab = 0.5f * (rin[0] + rin[1]);
     }
     float xI[3], pI[3];
     to_frames(F, xl, xI, pI);
@@ -751,26 +878,6 @@ __device__ __forceinline__ void mf_midpoints_unit(const MfArgs& a, const UnitCtx
 // p_I + a_bar e_t).
 __host__ __device__ constexpr int face_stage_floats(int V, int E, int tier) {
   return vrec(tier) * V + erec(tier) * E + 3 * V + 6 * E;
-}
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-// global -> shared bulk copy of `bytes` (multiple of 16, 16-B aligned ends)
-// by the calling thread; completion is counted on `bar`
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n"
-      ::"r"(smem_u32(bar)), "r"(phase) : "memory");
 }
 
 template <int TIER, bool STAGED>
@@ -1117,13 +1224,30 @@ template <int TIER, int XP>
 __global__ void __maxnreg__((RegCap<TIER, XP>::TRACES)) k_mf_traces(const MfArgs a) {
   __shared__ UnitCtx U;
   int u;
-  if (list_unit(a, XP, U, u)) mf_traces_unit<TIER, XP>(a, U, u);
+  if (!list_unit(a, XP, U, u)) return;
+  if constexpr (TIER <= 2 && CM_TRACE6) mf_traces_unit_n<TIER, XP>(a, U, u);
+  else mf_traces_unit<TIER, XP>(a, U, u);
 }
-template <int TIER, int XP>
+// STAGED: the unit's trace records (E x erec floats, contiguous in its slot)
+// are first copied into shared memory with one TMA bulk copy, so the edge
+// loop does not wait on HBM for every edge
+
+template <int TIER, int XP, bool STAGED>
 __global__ void __maxnreg__((RegCap<TIER, XP>::MIDPOINTS)) k_mf_midpoints(const MfArgs a) {
+  extern __shared__ __align__(16) float msm[];
   __shared__ UnitCtx U;
+  __shared__ uint64_t bar;
+  if (STAGED && threadIdx.x == 0) mbar_init(&bar, 1);   // published by list_unit's barrier
   int u;
-  if (list_unit(a, XP, U, u)) mf_midpoints_unit<TIER, XP>(a, U, u);
+  if (!list_unit(a, XP, U, u)) return;
+  if constexpr (STAGED) {
+    const float* se = a.scratch + (int64_t)u * a.slot + (int64_t)vrec(TIER) * U.SA.V;
+    if (threadIdx.x == 0) bulk_g2s(msm, se, (uint32_t)(U.SA.E * erec(TIER)) * 4u, &bar);
+    mbar_wait(&bar, 0u);
+    mf_midpoints_unit<TIER, XP>(a, U, u, msm);
+  } else {
+    mf_midpoints_unit<TIER, XP>(a, U, u, nullptr);
+  }
 }
 template <int TIER, bool STAGED>
 __global__ void __launch_bounds__(CM_MF_MAX_THREADS, TIER >= 3 ? 1 : CM_MF_FACE_MINB) k_mf_faces(const MfArgs a) {
@@ -1144,13 +1268,20 @@ int64_t manifold_slot_floats(int V, int E, int tier) {
 }
 
 template <int TIER, int XP>
-static int launch_sdf_phases(MfArgs& a, int64_t nb, int T, cudaStream_t st) {
+static int launch_sdf_phases(MfArgs& a, int64_t nb, int T, int max_E, cudaStream_t st) {
   k_mf_vertices<TIER, XP><<<(unsigned)nb, T, 0, st>>>(a);
   int rc = check_launch("k_mf_vertices");
   if (rc) return rc;
   k_mf_traces<TIER, XP><<<(unsigned)nb, T, 0, st>>>(a);
   if ((rc = check_launch("k_mf_traces"))) return rc;
-  k_mf_midpoints<TIER, XP><<<(unsigned)nb, T, 0, st>>>(a);
+  const int mid_bytes = max_E * erec(TIER) * 4;
+  if (CM_MF_STAGE_MID && mid_bytes <= 96 * 1024) {
+    if (mid_bytes > 48 * 1024)
+      cudaFuncSetAttribute(k_mf_midpoints<TIER, XP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mid_bytes);
+    k_mf_midpoints<TIER, XP, true><<<(unsigned)nb, T, mid_bytes, st>>>(a);
+  } else {
+    k_mf_midpoints<TIER, XP, false><<<(unsigned)nb, T, 0, st>>>(a);
+  }
   return check_launch("k_mf_midpoints");
 }
 
@@ -1206,11 +1337,11 @@ static int launch_tier(MfArgs a, int class_mask, int max_V, int max_E, int64_t n
     // SDF phases: one instantiation per SDF class present in the scene
     // (cm_internal.h ShapeRec::uses_xpsq); each takes its class's units from
     // the list k_mf_units built
-    if (class_mask & 1) rc = launch_sdf_phases<TIER, 0>(a, nb, T, st);
-    if (!rc && (class_mask & 2)) rc = launch_sdf_phases<TIER, 1>(a, nb, T, st);
-    if (!rc && (class_mask & 4)) rc = launch_sdf_phases<TIER, 2>(a, nb, T, st);
-    if (!rc && (class_mask & 8)) rc = launch_sdf_phases<TIER, 3>(a, nb, T, st);
-    if (!rc && (class_mask & 16)) rc = launch_sdf_phases<TIER, 4>(a, nb, T, st);
+    if (class_mask & 1) rc = launch_sdf_phases<TIER, 0>(a, nb, T, max_E, st);
+    if (!rc && (class_mask & 2)) rc = launch_sdf_phases<TIER, 1>(a, nb, T, max_E, st);
+    if (!rc && (class_mask & 4)) rc = launch_sdf_phases<TIER, 2>(a, nb, T, max_E, st);
+    if (!rc && (class_mask & 8)) rc = launch_sdf_phases<TIER, 3>(a, nb, T, max_E, st);
+    if (!rc && (class_mask & 16)) rc = launch_sdf_phases<TIER, 4>(a, nb, T, max_E, st);
     if (rc) return rc;
     if (!full) {   // the fusion does not depend on the SDF class: one launch
       if (stage_bytes > 0 && (stage_bytes <= kStageSmallBytes || nb < 8 * (int64_t)num_sms()))

@@ -513,3 +513,74 @@ def test_sdf_param_grad_unsupported(cuda):
     with pytest.raises(binding.CMError):
         S.sdf_param_grad(torch.zeros(1, dtype=torch.int32, device="cuda"), z,
                          torch.zeros(4, 3, device="cuda"), 4, 4)
+
+
+def test_sdf_eval_xpsq_soft_cardano_band(cuda, oracle_mod):
+    """Points inside the soft-Cardano band 10 tau_Delta < |Delta| < 46
+    tau_Delta of a curved XPSQ (both branches blended): every
+    output finite and within tolerance.  Near the band's edge the weaker
+    branch's trigonometric roots nearly coincide (its projected discriminant
+    s+(Delta) is tiny); their derivatives are taken from the cube roots, not
+    through the implicit 1 / F'(s) (0 / 0 there: found as NaN normals on C5
+    pairs in round 2)."""
+    from paper_2604_17538_b200 import binding
+    sampled, sdf = synth.c5_library()
+    shape = next(s for s in sdf if s.name == "xpsq3")
+    sc = scene_of([shape], ell=0.1)
+    osc = oracle_mod.OracleScene(sc)
+    S = binding.Scene(sc.shapes, sc.smooth)
+    rng = np.random.default_rng(77)
+    cand = rng.uniform(-0.12, 0.12, (40000, 3))
+    keep = []
+    for p in cand:
+        _, delta, _ = osc.xpsq_roots(0, 0, p)
+        if 10 < abs(delta) / sc.smooth["tau_delta"] < 46:
+            keep.append(p)
+        if len(keep) >= 400:
+            break
+    assert len(keep) >= 100, len(keep)
+    pts = np.asarray(keep, np.float32)
+    ids = np.zeros(1, np.int32)
+    poses = pose8().reshape(1, 8).astype(np.float32)
+    gpu = PT.gpu_sdf(S, ids, poses, pts, len(pts), ALL)
+    for k, v in gpu.items():
+        assert np.isfinite(v).all(), k
+    nf, rep = PT.sdf_parity(osc, gpu, ids, poses, pts, len(pts), rng, 0.1)
+    _report("sdf_xpsq_band", rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+
+
+def test_sdf_eval_xpsq_cusp_finite(cuda, oracle_mod):
+    """Points on and near the negative branch's cube-root cusp (Q ~ 0 with
+    0 < Delta < 46 tau_Delta, reading #15: excluded from parity)
+    give finite values, gradients and Hessians (found as NaN Hessians on C5
+    pairs in round 2: P^3 + s+(Delta)/4 cancelled in FP32)."""
+    from paper_2604_17538_b200 import binding
+    sampled, sdf = synth.c5_library()
+    shape = next(s for s in sdf if s.name == "xpsq3")
+    n = shape.sdf[0]
+    c = np.asarray(n["ctrl"], np.float64).reshape(3, 3)
+    A, B = c[0] - 2 * c[1] + c[2], 2 * (c[1] - c[0])
+    c3, c2 = -2 * A @ A, -3 * A @ B
+    b = c2 / c3
+    # depressed Q(w) = 2b^3/27 - b c1/(3 c3) + c0/c3, c1 = 2A.w - B.B, c0 = B.w: affine in w
+    gQ = (B - (2 * b / 3) * A) / c3
+    Q0 = 2 * b ** 3 / 27 + (b / 3) * (B @ B) / c3
+    sc = scene_of([shape], ell=0.1)
+    osc = oracle_mod.OracleScene(sc)
+    S = binding.Scene(sc.shapes, sc.smooth)
+    rng = np.random.default_rng(78)
+    pts = []
+    for q in (0.0, 1e-7, -1e-7, 1e-6, -1e-6, 1e-5):
+        w = rng.uniform(-0.12, 0.12, (3000, 3))
+        w -= np.outer((w @ gQ + Q0 - q) / (gQ @ gQ), gQ)      # onto the plane Q(w) = q
+        y = w + c[0]
+        for p in y:
+            _, delta, _ = osc.xpsq_roots(0, 0, p)
+            if 0 < delta / sc.smooth["tau_delta"] < 46:
+                pts.append(p)
+    assert len(pts) > 100, len(pts)
+    pts = np.asarray(pts, np.float32)
+    gpu = PT.gpu_sdf(S, np.zeros(1, np.int32), pose8().reshape(1, 8).astype(np.float32), pts, len(pts), ALL)
+    for k, v in gpu.items():
+        assert np.isfinite(v).all(), (k, int((~np.isfinite(v)).sum()))

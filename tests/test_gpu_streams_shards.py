@@ -1,0 +1,92 @@
+"""GPU tests of the call scheduling (scratch shared by manifold calls on one
+scene) and of the env-range sharding of SURVEY §8(e): the library's outputs
+do not depend on which stream a call came from, on chunk boundaries, or on
+which shard of the global env sequence a rank owns.  Needs a B200."""
+import numpy as np
+import pytest
+
+from paper_2604_17538_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_17538_b200 import binding
+    binding.lib()
+    return torch
+
+
+def _same(a, b):
+    """bitwise-equal values (NaN at the same places counts as equal)"""
+    import torch
+    if a.dtype.is_floating_point:
+        return bool(((a == b) | (torch.isnan(a) & torch.isnan(b))).all())
+    return bool(torch.equal(a, b))
+
+
+def _inputs(S, sc, torch):
+    pairs = torch.from_numpy(sc.pairs).cuda()
+    poses = torch.from_numpy(sc.poses).cuda()
+    offs = S.manifold_offsets(pairs)
+    return pairs, poses, offs, S.manifold_size(sc.pairs)
+
+
+def test_manifold_calls_on_two_streams(cuda):
+    """A tier-2 call on stream s1 and a tier-0 call on stream s2, issued back
+    to back on one scene without host synchronisation (their
+    scratch splits between the internal streams differ by tier), give the
+    same bits as the two calls run one after the other on one stream."""
+    torch = cuda
+    from paper_2604_17538_b200 import binding
+    sc = synth.c5_scene(1 << 17)
+    S = binding.Scene(sc.shapes, sc.smooth)
+    pairs, poses, offs, C = _inputs(S, sc, torch)
+    ref2 = S.contact_manifold(pairs, offs, C, poses, 2)
+    ref0 = S.contact_manifold(pairs, offs, C, poses, 0)
+    torch.cuda.synchronize()
+    for rep in range(3):
+        o2 = S.alloc_manifold(C, 2, poses.device)
+        o0 = S.alloc_manifold(C, 0, poses.device)
+        for v in list(o2.values()) + list(o0.values()):
+            if v.dtype == torch.float32:
+                v.fill_(float("nan"))
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s1):
+            S.contact_manifold(pairs, offs, C, poses, 2, out=o2)
+        with torch.cuda.stream(s2):
+            S.contact_manifold(pairs, offs, C, poses, 0, out=o0)
+        torch.cuda.synchronize()
+        for k in ref2:
+            assert _same(o2[k], ref2[k]), (rep, "tier 2", k)
+        for k in ref0:
+            assert _same(o0[k], ref0[k]), (rep, "tier 0", k)
+
+
+@pytest.mark.parametrize("lo,n", [(300001, 262144), (1 << 19, 65536)])
+def test_shard_rows_equal_full_run(cuda, lo, n):
+    """SURVEY §8(e) check: the C5 envs [lo, lo + n) run as their own shard
+    (what rank r of a G-GPU job computes) give outputs bitwise equal to the
+    same rows of the full 1M-env single-GPU run (different chunk boundaries,
+    different unit order inside the chunks)."""
+    torch = cuda
+    from paper_2604_17538_b200 import binding
+    full = synth.c5_scene(1 << 20)
+    shard = synth.c5_scene(n, env_lo=lo)
+    assert np.array_equal(shard.pairs[:, 3:], full.pairs[lo:lo + n, 3:])
+    assert np.array_equal(shard.poses, full.poses[lo:lo + n])
+    S = binding.Scene(full.shapes, full.smooth)
+    pairs, poses, offs, C = _inputs(S, full, torch)
+    out_full = S.contact_manifold(pairs, offs, C, poses, 2)
+    torch.cuda.synchronize()
+    r0 = int(offs[lo].item())
+    del pairs, poses
+    ps, po, os_, Cs = _inputs(S, shard, torch)
+    out_sh = S.contact_manifold(ps, os_, Cs, po, 2)
+    torch.cuda.synchronize()
+    for k, v in out_sh.items():
+        assert _same(v, out_full[k][..., r0:r0 + Cs]), k
