@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define CM_ABI_VERSION 2
+#define CM_ABI_VERSION 3
 #define CM_MAX_PLANES 8      /* half-spaces per PSQ / XPSQ cross-section      */
 #define CM_MAX_CHILDREN 32   /* children per boolean node                     */
 #define CM_MAX_DEPTH 3       /* nesting of boolean nodes in one shape         */
@@ -275,6 +275,16 @@ int cm_expand_jacobian(const cm_scene* scene, const int32_t* pairs, int64_t n_pa
 /* Number of kernel launches the library issued since scene creation (all
  * scenes, this process) — instrumentation for bench.py's gpu_launches. */
 int64_t cm_launch_count(void);
+
+/* Invalid batch records the device saw since scene creation (or the last
+ * reset): pair records whose shape ids are out of [0, n_shapes) (those pairs
+ * get no rows from cm_manifold_offsets), whose env / slot indices are out of
+ * [0, n_env) / [0, n_slot) or whose shapes lack the sampled surface / SDF
+ * (their rows are filled with NaN, dom = -1), and sdf_eval / param_grad
+ * shape ids that are out of range or name a shape without an SDF (their
+ * outputs are NaN).  Invalid indices are never dereferenced.  Synchronises
+ * the device; reset != 0 zeroes the counter. */
+int cm_scene_error_count(const cm_scene* scene, int64_t* count, int reset);
 
 #ifdef __cplusplus
 }

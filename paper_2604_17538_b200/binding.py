@@ -25,7 +25,8 @@ FULL_MODE, TWO_SIDED = 4, 8   # manifold mode bits (include/xpsq_cm.h)
 EXPORTS = ["cm_version", "cm_last_error", "cm_scene_create", "cm_scene_destroy", "cm_shape_counts",
            "cm_param_layout", "cm_sdf_param_grad",
            "cm_shape_topology", "cm_sdf_eval", "cm_manifold_size", "cm_manifold_offsets_workspace",
-           "cm_manifold_offsets", "cm_contact_manifold", "cm_expand_jacobian", "cm_launch_count"]
+           "cm_manifold_offsets", "cm_contact_manifold", "cm_expand_jacobian", "cm_launch_count",
+           "cm_scene_error_count"]
 
 
 class cm_node(C.Structure):
@@ -82,6 +83,8 @@ def lib():
         L.cm_contact_manifold.argtypes = [p, p, i64, p, p, i64, i32, u32, p, i64, p]
         L.cm_expand_jacobian.argtypes = [p, p, i64, p, p, i64, i32, u32, p, p, i64, p, p]
         L.cm_launch_count.restype = i64
+        if hasattr(L, "cm_scene_error_count"):   # (older builds in A/B sweeps lack it)
+            L.cm_scene_error_count.argtypes = [p, p, C.c_int]
         _lib = L
     return _lib
 
@@ -178,6 +181,13 @@ class Scene:
             self.close()
         except Exception:
             pass
+
+    def error_count(self, reset: bool = False) -> int:
+        """Invalid batch records seen on the device (cm_scene_error_count;
+        synchronises)."""
+        n = C.c_int64()
+        _check(lib().cm_scene_error_count(self.h, C.byref(n), int(reset)), "cm_scene_error_count")
+        return n.value
 
     def counts(self, shape: int):
         V, E, F = C.c_int32(), C.c_int32(), C.c_int32()

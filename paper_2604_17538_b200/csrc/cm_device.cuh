@@ -33,10 +33,16 @@ using namespace cmi;
 #define CM_SQ_SHARED_W 1      // SQ weights from the LSE exponentials (fewer MUFU ops)
 #endif
 #ifndef CM_SOFTCLIP_FAST
-#define CM_SOFTCLIP_FAST 1    // softclip interior shortcut
+#define CM_SOFTCLIP_FAST 0    // softclip interior shortcut: measured C5 -1.5%, C4 -1.7% (r02j sweep)
 #endif
 #ifndef CM_LEAF_LAZY_R
-#define CM_LEAF_LAZY_R 1      // leaf rotation loaded only for rotated leaves
+#define CM_LEAF_LAZY_R 0      // leaf rotation loaded only for rotated leaves: C5 -1.7%, C4 -1.2% (r02j)
+#endif
+#ifndef CM_XPSQ_TSPACE
+#define CM_XPSQ_TSPACE 1      // curved roots outside the band: Newton-polished in t (near-straight splines)
+#endif
+#ifndef CM_SOFTCLIP_ACCURATE
+#define CM_SOFTCLIP_ACCURATE 1
 #endif
 #ifndef CM_SHAPE_NOINLINE
 #define CM_SHAPE_NOINLINE 0
@@ -113,9 +119,14 @@ __device__ __forceinline__ void softclip_12(float x, float lo, float hi, float t
   softplus_sig(x - lo, tau, itau, sp1, s1, e1, r1);
   softplus_sig(x - hi, tau, itau, sp2, s2, e2, r2);
   v = lo + sp1 - sp2;
+#if CM_SOFTCLIP_ACCURATE
   // above hi both sigmas are ~1: their difference is (e2 - e1) r1 r2
   d1 = x >= hi ? (e2 - e1) * r1 * r2 : s1 - s2;
   d2 = (e1 * r1 * r1 - e2 * r2 * r2) * itau;
+#else
+  d1 = s1 - s2;
+  d2 = (s1 * (1.f - s1) - s2 * (1.f - s2)) * itau;
+#endif
 }
 
 // cube root from the MUFU log / exp plus one Newton step (rel. error ~1e-7)
@@ -664,6 +675,57 @@ __device__ __forceinline__ void xpsq_t_implicit(const Xpsq& X, const SmoothDev& 
   }
 }
 
+// The curved spline's rarer regimes, out of line so that the common
+// one-real-root path stays small in the instruction cache: three real roots
+// (Delta > 46 tau_Delta) and the soft-Cardano band (both branches,
+// P:113-124).  Returns true when the three roots are identical.
+#ifndef CM_XPSQ_RARE_NOINLINE
+#define CM_XPSQ_RARE_NOINLINE 1
+#endif
+template <int O>
+__device__
+#if CM_XPSQ_RARE_NOINLINE
+__noinline__
+#else
+__forceinline__
+#endif
+bool xpsq_root_t_rare(const Xpsq& X, const SmoothDev& sp, const float* w, float Pv, float Qv, float Delta, int newton,
+                      float* tv, float (*tg)[3], float (*th)[6]) {
+  if (CM_XPSQ_TSPACE && Delta * sp.i_delta > 46.f) {
+    // three real roots: trigonometric form, k = 0, 1, 2
+    const float rho = sqrtf(fmaxf(-Pv * (1.f / 3.f), 0.f));
+    const float th3 = atan2_pos(sqrtf(Delta * (1.f / 108.f)), -0.5f * Qv) * (1.f / 3.f);
+    float sn3, cs3;
+    __sincosf(th3, &sn3, &cs3);
+    const float ck[3] = {cs3, fmaf(-0.8660254037844386f, sn3, -0.5f * cs3),
+                         fmaf(0.8660254037844386f, sn3, -0.5f * cs3)};
+#pragma unroll 1
+    for (int k = 0; k < 3; ++k) xpsq_t_implicit<O>(X, sp, w, 2.f * rho * ck[k] - X.b3, newton, &tv[k], tg[k], th[k]);
+    return false;
+  }
+  constexpr int OC = O;
+  J2<OC> t2[3];
+  const bool single = soft_cardano_implicit<OC>(Pv, Qv, X.b3, sp, t2);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    tv[k] = t2[k].v;
+    if constexpr (O >= 1) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) tg[k][i] = fmaf(t2[k].g[0], X.gP[i], t2[k].g[1] * X.gQ[i]);
+    }
+    if constexpr (O >= 2) {
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const int i = jhi<3>(q), j = jhj<3>(q);
+        float v = t2[k].h[0] * X.gP[i] * X.gP[j];
+        v = fmaf(t2[k].h[1], fmaf(X.gP[i], X.gQ[j], X.gQ[i] * X.gP[j]), v);
+        th[k][q] = fmaf(t2[k].h[2], X.gQ[i] * X.gQ[j], v);
+      }
+    }
+  }
+  return single;
+}
+
 template <int O>
 __device__ __forceinline__ bool xpsq_root_t(const Xpsq& X, const SmoothDev& sp, const float* w, float* tv, float (*tg)[3],
                                             float (*th)[6]) {
@@ -696,7 +758,7 @@ __device__ __forceinline__ bool xpsq_root_t(const Xpsq& X, const SmoothDev& sp, 
     // digits when |P| is large, e.g. A nearly perpendicular to B with
     // |A| << |B|), two when t = s - b/3 cancels digits too (|b/3| > 4)
     const int newton = fabsf(X.b3) > 4.f ? 2 : 1;
-    if (Delta * sp.i_delta < -46.f) {
+    if (CM_XPSQ_TSPACE && Delta * sp.i_delta < -46.f) {
       // one real root: Cardano in its cancellation-free form
       const float sD = sqrtf(-Delta * (1.f / 108.f));
       const float u = cbrt_fast(Qv >= 0.f ? -0.5f * Qv - sD : -0.5f * Qv + sD);
@@ -712,39 +774,7 @@ __device__ __forceinline__ bool xpsq_root_t(const Xpsq& X, const SmoothDev& sp, 
       }
       return true;
     }
-    if (Delta * sp.i_delta > 46.f) {
-      // three real roots: trigonometric form, k = 0, 1, 2
-      const float rho = sqrtf(fmaxf(-Pv * (1.f / 3.f), 0.f));
-      const float th3 = atan2_pos(sqrtf(Delta * (1.f / 108.f)), -0.5f * Qv) * (1.f / 3.f);
-      float sn3, cs3;
-      __sincosf(th3, &sn3, &cs3);
-      const float ck[3] = {cs3, fmaf(-0.8660254037844386f, sn3, -0.5f * cs3),
-                           fmaf(0.8660254037844386f, sn3, -0.5f * cs3)};
-#pragma unroll 1
-      for (int k = 0; k < 3; ++k) xpsq_t_implicit<O>(X, sp, w, 2.f * rho * ck[k] - X.b3, newton, &tv[k], tg[k], th[k]);
-      return false;
-    }
-    constexpr int OC = O;
-    J2<OC> t2[3];
-    const bool single = soft_cardano_implicit<OC>(Pv, Qv, X.b3, sp, t2);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      tv[k] = t2[k].v;
-      if constexpr (O >= 1) {
-#pragma unroll
-        for (int i = 0; i < 3; ++i) tg[k][i] = fmaf(t2[k].g[0], X.gP[i], t2[k].g[1] * X.gQ[i]);
-      }
-      if constexpr (O >= 2) {
-#pragma unroll
-        for (int q = 0; q < 6; ++q) {
-          const int i = jhi<3>(q), j = jhj<3>(q);
-          float v = t2[k].h[0] * X.gP[i] * X.gP[j];
-          v = fmaf(t2[k].h[1], fmaf(X.gP[i], X.gQ[j], X.gQ[i] * X.gP[j]), v);
-          th[k][q] = fmaf(t2[k].h[2], X.gQ[i] * X.gQ[j], v);
-        }
-      }
-    }
-    return single;
+    return xpsq_root_t_rare<O>(X, sp, w, Pv, Qv, Delta, newton, tv, tg, th);
   }
   return true;
 }

@@ -512,6 +512,11 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
   for (int s = 0; s < n_shapes; ++s) sc->param_off[s + 1] = sc->param_off[s] + std::max(sc->param_count[s], 0);
   sc->param_off_dev = dev_copy(sc->param_off, rc);
   if (sc->param_off_dev) sc->allocs.push_back(sc->param_off_dev);
+  {   // error word of the device-side record validation (cm_scene_error_count)
+    std::vector<unsigned int> zero(4, 0u);
+    D.err = dev_copy(zero, rc);
+    if (D.err) sc->allocs.push_back(D.err);
+  }
   D.sp = SmoothDev{sp->tau_cmp, sp->tau_min, sp->tau_clip_alpha, sp->tau_clip_t, sp->tau_delta, sp->trace_iters,
                    (float)(1.0 / sp->tau_cmp), (float)(1.0 / sp->tau_min), (float)(1.0 / sp->tau_clip_alpha),
                    (float)(1.0 / sp->tau_clip_t), (float)(1.0 / sp->tau_delta)};
@@ -712,7 +717,11 @@ int cm_contact_manifold(const cm_scene* sc, const int32_t* pairs, int64_t n_pair
   if (cudaStreamGetCaptureInfo(st, &cap, &cap_id) != cudaSuccess) return fail(CM_ERR_CUDA, "cm_contact_manifold: capture info");
   if (cap != cudaStreamCaptureStatusActive) cap_id = 0;
   const int tier_now = (int)(flags & CM_TIER_MASK);
-  const bool wait_prev = ms->manifold_calls > 0 && ms->last_capture_id == cap_id && ms->last_tier != tier_now;
+#ifndef CM_FORK_SERIALIZE
+#define CM_FORK_SERIALIZE 1
+#endif
+  const bool wait_prev = CM_FORK_SERIALIZE && ms->manifold_calls > 0 && ms->last_capture_id == cap_id &&
+                         ms->last_tier != tier_now;
   void* aux[cmi::kManifoldStreams];
   for (int i = 0; i < cmi::kManifoldStreams; ++i) {
     cudaStreamWaitEvent(ms->aux[i], ms->ev_fork, 0);
@@ -724,7 +733,7 @@ int cm_contact_manifold(const cm_scene* sc, const int32_t* pairs, int64_t n_pair
   ++ms->manifold_calls;
   ms->last_capture_id = cap_id;
   ms->last_tier = tier_now;
-  int rc = cml::launch_manifold(sc->dev, sc->class_mask, sc->max_V, sc->max_E, pairs, n_pairs, offsets, poses, n_slot,
+  int rc = cml::launch_manifold(sc->dev, sc->class_mask, sc->max_V, sc->max_E, pairs, n_pairs, offsets, poses, n_env, n_slot,
                                 flags, out, n_contacts, sc->scratch, sc->scratch_floats, aux, n_aux_streams());
   for (int i = 0; i < cmi::kManifoldStreams; ++i) {
     cudaEventRecord(ms->ev_join[i], ms->aux[i]);
@@ -737,13 +746,23 @@ int cm_contact_manifold(const cm_scene* sc, const int32_t* pairs, int64_t n_pair
 int cm_expand_jacobian(const cm_scene* sc, const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,
                        const float* poses, int64_t n_env, int32_t n_slot, uint32_t flags, const float* W,
                        const float* q, int64_t n_contacts, float* J, void* stream) {
-  (void)n_env;
   if (!sc || !pairs || !offsets || !poses || !W || !q || !J) return fail(CM_ERR_INVALID, "cm_expand_jacobian");
-  int rc = cml::launch_expand(pairs, n_pairs, offsets, sc->dev, poses, n_slot, W, q, n_contacts, J, flags, stream);
+  int rc = cml::launch_expand(pairs, n_pairs, offsets, sc->dev, poses, n_env, n_slot, W, q, n_contacts, J, flags, stream);
   if (rc) return fail(rc, cml::last_cuda_error());
   return CM_OK;
 }
 
 int64_t cm_launch_count(void) { return cml::launch_count(); }
+
+int cm_scene_error_count(const cm_scene* sc, int64_t* count, int reset) {
+  if (!sc || !count) return fail(CM_ERR_INVALID, "cm_scene_error_count: NULL argument");
+  unsigned int v = 0;
+  cudaError_t e = cudaMemcpy(&v, sc->dev.err, sizeof(v), cudaMemcpyDeviceToHost);   // synchronises the device
+  if (e != cudaSuccess) return fail(CM_ERR_CUDA, std::string("cm_scene_error_count: ") + cudaGetErrorString(e));
+  *count = (int64_t)v;
+  if (reset && cudaMemset(sc->dev.err, 0, sizeof(unsigned int)) != cudaSuccess)
+    return fail(CM_ERR_CUDA, "cm_scene_error_count: reset");
+  return CM_OK;
+}
 
 }  // extern "C"

@@ -96,6 +96,7 @@ struct SceneDev {
   const int32_t* face_edges;
   SmoothDev sp;
   int32_t n_shapes;
+  unsigned int* err;          // device counter of invalid pair records / shape ids (cm_scene_error_count)
 };
 
 // manifold chunk scratch: the units of one chunk keep their candidate state
@@ -120,15 +121,16 @@ int launch_sdf_eval(const cmi::SceneDev& s, int class_mask, const int32_t* shape
                     const float* points, int64_t B, int64_t P, uint32_t flags, float* d, float* grad, float* hess,
                     float* dpose, float* d2pose, float* dxdpose, void* const* streams, int n_streams);
 int launch_manifold(const cmi::SceneDev& s, int class_mask, int max_V, int max_E, const int32_t* pairs,
-                    int64_t n_pairs, const int64_t* offsets, const float* poses, int32_t n_slot, uint32_t flags,
+                    int64_t n_pairs, const int64_t* offsets, const float* poses, int64_t n_env, int32_t n_slot,
+                    uint32_t flags,
                     const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats,
                     void* const* streams, int n_streams);
 int launch_offsets(const cmi::SceneDev& s, const int32_t* pairs, int64_t n_pairs, uint32_t flags, int64_t* offsets,
                    void* ws, int64_t ws_bytes, void* stream);
 int64_t offsets_workspace(int64_t n_pairs);
 int launch_expand(const int32_t* pairs, int64_t n_pairs, const int64_t* offsets, const cmi::SceneDev& s,
-                  const float* poses, int32_t n_slot, const float* W, const float* q, int64_t C, float* J,
-                  uint32_t flags, void* stream);
+                  const float* poses, int64_t n_env, int32_t n_slot, const float* W, const float* q, int64_t C,
+                  float* J, uint32_t flags, void* stream);
 int64_t manifold_slot_floats(int V, int E, int tier);
 int launch_sdf_param_grad(const cmi::SceneDev& s, const int32_t* ids, const float* poses, const float* pts, int64_t B,
                           int64_t P, int32_t pmax, float* J, const float* w, float* vjp, const int64_t* poff,

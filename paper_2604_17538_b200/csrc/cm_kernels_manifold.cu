@@ -300,6 +300,7 @@ struct MfArgs {
   int64_t unit0;             // first unit of this chunk
   const int64_t* offsets;
   const float* poses;
+  int64_t n_env;
   int32_t n_slot;
   cm_manifold_out out;
   int64_t C;
@@ -320,7 +321,8 @@ struct alignas(16) UnitCtx {
   int side;
   int valid;                 // the unit has a manifold (SDF side and a surface)
   int cls;                   // SDF class of the unit's SDF shape
-  int pad[3];
+  int bad;                   // invalid record with output rows (filled with NaN)
+  int pad[2];
 };
 static_assert(sizeof(UnitCtx) % 16 == 0, "UnitCtx is copied as float4");
 
@@ -399,18 +401,28 @@ __device__ __forceinline__ void unit_resolve(const MfArgs& a, int64_t un, UnitCt
   const int env = __ldg(pr + 0);
   const int slA = __ldg(pr + 1 + side), slB = __ldg(pr + 2 - side);
   const int shA = __ldg(pr + 3 + side), shB = __ldg(pr + 4 - side);
+  U.valid = 0;
+  U.cls = -1;
+  U.bad = 0;
+  // record validation: out-of-range shape ids (the offsets kernel gave the
+  // pair no rows), env or slot indices (its rows are filled with NaN by
+  // k_mf_units), or a shape without the needed surface / SDF: counted in
+  // the scene's error word, never dereferenced
+  const int ns = a.S.n_shapes;
+  if ((unsigned)shA >= (unsigned)ns || (unsigned)shB >= (unsigned)ns) {
+    atomicAdd(a.S.err, 1u);
+    return;
+  }
   const ShapeRec sa = a.S.shapes[shA];
   const ShapeRec sb = a.S.shapes[shB];
-  const int ok = sb.has_sdf && sa.F > 0;
-  if (ok) {
-    const float4* A = reinterpret_cast<const float4*>(a.poses + 8 * ((int64_t)env * a.n_slot + slA));
-    const float4* B = reinterpret_cast<const float4*>(a.poses + 8 * ((int64_t)env * a.n_slot + slB));
-    const float4 a0 = __ldg(A), a1 = __ldg(A + 1), b0 = __ldg(B), b1 = __ldg(B + 1);
-    const float pa[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-    const float pb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-    pair_frame(pa, pb, U.F);
-    U.SA = sa;
-    U.SB = sb;
+  if ((int64_t)(unsigned)env >= a.n_env || (unsigned)slA >= (unsigned)a.n_slot || (unsigned)slB >= (unsigned)a.n_slot ||
+      !(sb.has_sdf && sa.F > 0)) {
+    atomicAdd(a.S.err, 1u);
+    U.bad = 1;
+  }
+  const int ok = !U.bad;
+  U.SA = sa;
+  {
     int64_t o = __ldg(a.offsets + pi);
     if (side) {
       const ShapeRec s0 = a.S.shapes[__ldg(pr + 3)];
@@ -419,8 +431,17 @@ __device__ __forceinline__ void unit_resolve(const MfArgs& a, int64_t un, UnitCt
     U.off = o;
     U.side = side;
   }
-  U.valid = ok;
-  U.cls = sb.uses_xpsq;
+  if (ok) {
+    const float4* A = reinterpret_cast<const float4*>(a.poses + 8 * ((int64_t)env * a.n_slot + slA));
+    const float4* B = reinterpret_cast<const float4*>(a.poses + 8 * ((int64_t)env * a.n_slot + slB));
+    const float4 a0 = __ldg(A), a1 = __ldg(A + 1), b0 = __ldg(B), b1 = __ldg(B + 1);
+    const float pa[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    const float pb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    pair_frame(pa, pb, U.F);
+    U.SB = sb;
+    U.valid = 1;
+    U.cls = sb.uses_xpsq;
+  }
 }
 
 // per-chunk prologue: one thread per unit resolves its set-up once for the
@@ -432,7 +453,26 @@ __global__ void __launch_bounds__(128) k_mf_units(const MfArgs a, int64_t nb) {
   UnitCtx U;
   U.valid = 0;
   U.cls = -1;
+  U.bad = 0;
   if (in) unit_resolve(a, a.unit0 + u, U);
+  if (in && U.bad) {   // an invalid record's rows: NaN in every float field, dom -1
+    const bool fm = (a.mode & CM_FULL_MODE) != 0;
+    const int nr = fm ? U.SA.V + U.SA.E : U.SA.F;
+    const float qn = __int_as_float(0x7fc00000);
+    const cm_manifold_out& o = a.out;
+    const int64_t C = a.C;
+    for (int r = 0; r < nr; ++r) {
+      const int64_t c = U.off + r;
+      for (int k = 0; k < 3; ++k) { o.point[k * C + c] = qn; o.normal[k * C + c] = qn; }
+      o.depth[c] = qn;
+      o.dom[c] = (int8_t)-1;
+      if (o.W) o.W[c] = qn;
+      if (o.q) for (int k = 0; k < 3; ++k) o.q[k * C + c] = qn;
+      if (o.ddepth) for (int k = 0; k < 12; ++k) o.ddepth[k * C + c] = qn;
+      if (o.dnormal) for (int k = 0; k < 36; ++k) o.dnormal[k * C + c] = qn;
+      if (o.d2depth) for (int k = 0; k < 78; ++k) o.d2depth[k * C + c] = qn;
+    }
+  }
   // class lists in unit order within the block (ballot ranks + one atomic per
   // block and class), so neighbouring CTAs of a phase kernel take
   // neighbouring units
@@ -1355,7 +1395,8 @@ static int launch_tier(MfArgs a, int class_mask, int max_V, int max_E, int64_t n
 }
 
 int launch_manifold(const SceneDev& s, int class_mask, int max_V, int max_E, const int32_t* pairs,
-                    int64_t n_pairs, const int64_t* offsets, const float* poses, int32_t n_slot, uint32_t flags,
+                    int64_t n_pairs, const int64_t* offsets, const float* poses, int64_t n_env, int32_t n_slot,
+                    uint32_t flags,
                     const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats,
                     void* const* streams, int n_streams) {
   const int tier = (int)(flags & CM_TIER_MASK);
@@ -1379,6 +1420,7 @@ int launch_manifold(const SceneDev& s, int class_mask, int max_V, int max_E, con
   a.unit0 = 0;
   a.offsets = offsets;
   a.poses = poses;
+  a.n_env = n_env;
   a.n_slot = n_slot;
   a.out = *out;
   a.C = C;

@@ -45,14 +45,22 @@ int num_sms() {
 }
 
 // ---- offsets: exclusive scan of F(shapeA) over the pairs ---------------------
-__global__ void k_face_counts(const ShapeRec* __restrict__ shapes, const int32_t* __restrict__ pairs, int64_t n,
-                              uint32_t flags, int64_t* __restrict__ cnt) {
+// (a pair whose shape ids are out of range gets no rows and is counted in
+// the scene's error word)
+__global__ void k_face_counts(const ShapeRec* __restrict__ shapes, int32_t n_shapes, unsigned int* err,
+                              const int32_t* __restrict__ pairs, int64_t n, uint32_t flags, int64_t* __restrict__ cnt) {
   const bool full = flags & CM_FULL_MODE, two = flags & CM_TWO_SIDED;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const ShapeRec a = shapes[__ldg(pairs + 5 * i + 3)];
+    const int ia = __ldg(pairs + 5 * i + 3), ib = __ldg(pairs + 5 * i + 4);
+    if ((unsigned)ia >= (unsigned)n_shapes || (unsigned)ib >= (unsigned)n_shapes) {
+      cnt[i] = 0;
+      atomicAdd(err, 1u);
+      continue;
+    }
+    const ShapeRec a = shapes[ia];
     int64_t c = full ? (int64_t)a.V + a.E : (int64_t)a.F;
     if (two) {
-      const ShapeRec b = shapes[__ldg(pairs + 5 * i + 4)];
+      const ShapeRec b = shapes[ib];
       c += full ? (int64_t)b.V + b.E : (int64_t)b.F;
     }
     cnt[i] = c;
@@ -71,7 +79,7 @@ int launch_offsets(const SceneDev& s, const int32_t* pairs, int64_t n_pairs, uin
   int64_t blocks = (n_pairs + 255) / 256;
   if (blocks > 4096) blocks = 4096;
   if (blocks < 1) return CM_OK;
-  k_face_counts<<<(unsigned)blocks, 256, 0, st>>>(s.shapes, pairs, n_pairs, flags, offsets);
+  k_face_counts<<<(unsigned)blocks, 256, 0, st>>>(s.shapes, s.n_shapes, s.err, pairs, n_pairs, flags, offsets);
   int rc = check_launch("k_face_counts");
   if (rc) return rc;
   size_t bytes = (size_t)ws_bytes;
@@ -85,13 +93,18 @@ int launch_offsets(const SceneDev& s, const int32_t* pairs, int64_t n_pairs, uin
 }
 
 // ---- J expansion (App. A.7): J = [W I, -[q - W tA]x, -W I, [q - W tB]x] ------
-__global__ void k_expand_jacobian(const ShapeRec* __restrict__ shapes, const int32_t* __restrict__ pairs,
-                                  int64_t n_pairs, const int64_t* __restrict__ offsets,
-                                  const float* __restrict__ poses, int32_t n_slot, const float* __restrict__ W,
-                                  const float* __restrict__ q, int64_t C, float* __restrict__ J, uint32_t flags) {
+__global__ void k_expand_jacobian(const ShapeRec* __restrict__ shapes, int32_t n_shapes,
+                                  const int32_t* __restrict__ pairs, int64_t n_pairs,
+                                  const int64_t* __restrict__ offsets, const float* __restrict__ poses, int64_t n_env,
+                                  int32_t n_slot, const float* __restrict__ W, const float* __restrict__ q, int64_t C,
+                                  float* __restrict__ J, uint32_t flags) {
   const bool full = flags & CM_FULL_MODE, two = flags & CM_TWO_SIDED;
   for (int64_t pi = blockIdx.x; pi < n_pairs; pi += gridDim.x) {
     const int32_t* pr = pairs + 5 * pi;
+    // invalid records (counted by the offsets / manifold kernels): no J
+    if ((unsigned)pr[3] >= (unsigned)n_shapes || (unsigned)pr[4] >= (unsigned)n_shapes ||
+        (int64_t)(unsigned)pr[0] >= n_env || (unsigned)pr[1] >= (unsigned)n_slot || (unsigned)pr[2] >= (unsigned)n_slot)
+      continue;
     const float* pa = poses + 8 * ((int64_t)pr[0] * n_slot + pr[1]);
     const float* pb = poses + 8 * ((int64_t)pr[0] * n_slot + pr[2]);
     int64_t off = offsets[pi];
@@ -124,12 +137,12 @@ __global__ void k_expand_jacobian(const ShapeRec* __restrict__ shapes, const int
 }
 
 int launch_expand(const int32_t* pairs, int64_t n_pairs, const int64_t* offsets, const SceneDev& s,
-                  const float* poses, int32_t n_slot, const float* W, const float* q, int64_t C, float* J,
-                  uint32_t flags, void* stream) {
+                  const float* poses, int64_t n_env, int32_t n_slot, const float* W, const float* q, int64_t C,
+                  float* J, uint32_t flags, void* stream) {
   int64_t grid = n_pairs < 65535 ? n_pairs : 65535;
   if (grid < 1) return CM_OK;
-  k_expand_jacobian<<<(unsigned)grid, 128, 0, (cudaStream_t)stream>>>(s.shapes, pairs, n_pairs, offsets, poses,
-                                                                       n_slot, W, q, C, J, flags);
+  k_expand_jacobian<<<(unsigned)grid, 128, 0, (cudaStream_t)stream>>>(s.shapes, s.n_shapes, pairs, n_pairs, offsets,
+                                                                       poses, n_env, n_slot, W, q, C, J, flags);
   return check_launch("k_expand_jacobian");
 }
 

@@ -31,11 +31,27 @@ __global__ void __launch_bounds__(256, CM_SDF_MINB) k_sdf_eval(SceneDev S, const
                                                   int64_t B, int64_t P, float* __restrict__ d,
                                                   float* __restrict__ grad, float* __restrict__ hess,
                                                   float* __restrict__ dpose, float* __restrict__ d2pose,
-                                                  float* __restrict__ dxdpose, int xp_filter) {
+                                                  float* __restrict__ dxdpose, int xp_filter, int own_invalid) {
   const int64_t N = B * P;
   for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < N; n += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = n / P;
-    const ShapeRec sh = S.shapes[__ldg(shape_ids + b)];
+    const int sid = __ldg(shape_ids + b);
+    if ((unsigned)sid >= (unsigned)S.n_shapes || !S.shapes[sid].has_sdf) {
+      // invalid shape id (or a shape without an SDF): NaN outputs, written and
+      // counted once per point by the first class instantiation launched
+      if (own_invalid) {
+        const float qn = __int_as_float(0x7fc00000);
+        d[n] = qn;
+        if (grad) for (int k = 0; k < 3; ++k) grad[k * N + n] = qn;
+        if (hess) for (int k = 0; k < 6; ++k) hess[k * N + n] = qn;
+        if (dpose) for (int k = 0; k < 6; ++k) dpose[k * N + n] = qn;
+        if (d2pose) for (int k = 0; k < 21; ++k) d2pose[k * N + n] = qn;
+        if (dxdpose) for (int k = 0; k < 18; ++k) dxdpose[k * N + n] = qn;
+        atomicAdd(S.err, 1u);
+      }
+      continue;
+    }
+    const ShapeRec sh = S.shapes[sid];
     if (xp_filter >= 0 && sh.uses_xpsq != xp_filter) continue;
     const float4 pa = __ldg(reinterpret_cast<const float4*>(poses) + 2 * b);
     const float4 pb = __ldg(reinterpret_cast<const float4*>(poses) + 2 * b + 1);
@@ -116,7 +132,7 @@ __global__ void __launch_bounds__(256, CM_SDF_MINB) k_sdf_eval(SceneDev S, const
 }
 
 template <int O, int XP, bool PG, bool PH>
-static int launch_sdf_t(const SceneDev& s, int xp_filter, const int32_t* ids, const float* poses, const float* pts,
+static int launch_sdf_t(const SceneDev& s, int xp_filter, int own, const int32_t* ids, const float* poses, const float* pts,
                         int64_t B, int64_t P, float* d, float* g, float* h, float* dp, float* d2p, float* dxp,
                         cudaStream_t st) {
   const int threads = 256;
@@ -126,25 +142,25 @@ static int launch_sdf_t(const SceneDev& s, int xp_filter, const int32_t* ids, co
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   k_sdf_eval<O, XP, PG, PH><<<(unsigned)blocks, threads, 0, st>>>(s, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp,
-                                                                   xp_filter);
+                                                                   xp_filter, own);
   return check_launch("k_sdf_eval");
 }
 
 template <int XP>
-static int dispatch_sdf(const SceneDev& s, int xp_filter, const int32_t* ids, const float* poses, const float* pts,
+static int dispatch_sdf(const SceneDev& s, int xp_filter, int own, const int32_t* ids, const float* poses, const float* pts,
                         int64_t B, int64_t P, uint32_t flags, float* d, float* g, float* h, float* dp, float* d2p,
                         float* dxp, cudaStream_t st) {
   const bool PG = flags & CM_SDF_POSE_GRAD, PH = flags & CM_SDF_POSE_HESS;
   const int O = (flags & (CM_SDF_HESS | CM_SDF_POSE_HESS)) ? 2 : ((flags & (CM_SDF_GRAD | CM_SDF_POSE_GRAD)) ? 1 : 0);
-  if (O == 0) return launch_sdf_t<0, XP, false, false>(s, xp_filter, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
+  if (O == 0) return launch_sdf_t<0, XP, false, false>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
   if (O == 1) {
-    if (PG) return launch_sdf_t<1, XP, true, false>(s, xp_filter, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
-    return launch_sdf_t<1, XP, false, false>(s, xp_filter, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
+    if (PG) return launch_sdf_t<1, XP, true, false>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
+    return launch_sdf_t<1, XP, false, false>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
   }
-  if (PG && PH) return launch_sdf_t<2, XP, true, true>(s, xp_filter, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
-  if (PG) return launch_sdf_t<2, XP, true, false>(s, xp_filter, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
-  if (PH) return launch_sdf_t<2, XP, false, true>(s, xp_filter, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
-  return launch_sdf_t<2, XP, false, false>(s, xp_filter, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
+  if (PG && PH) return launch_sdf_t<2, XP, true, true>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
+  if (PG) return launch_sdf_t<2, XP, true, false>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
+  if (PH) return launch_sdf_t<2, XP, false, true>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
+  return launch_sdf_t<2, XP, false, false>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
 }
 
 namespace cml {
@@ -160,17 +176,19 @@ int launch_sdf_eval(const SceneDev& s, int class_mask, const int32_t* ids, const
   const bool multi = (class_mask & (class_mask - 1)) != 0;
   int rc = CM_OK, j = 0;
   auto next = [&]() { return (cudaStream_t)streams[(j++) % n_streams]; };
-  if (class_mask & 1) rc = dispatch_sdf<0>(s, multi ? 0 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
+  const int first = class_mask ? __builtin_ctz(class_mask) : 0;   // owns invalid shape ids
+  if (class_mask & 1)
+    rc = dispatch_sdf<0>(s, multi ? 0 : -1, first == 0, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
   if (!rc && (class_mask & 2))
-    rc = dispatch_sdf<1>(s, multi ? 1 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
+    rc = dispatch_sdf<1>(s, multi ? 1 : -1, first == 1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
   if (!rc && (class_mask & 4))
-    rc = dispatch_sdf<2>(s, multi ? 2 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
+    rc = dispatch_sdf<2>(s, multi ? 2 : -1, first == 2, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
   // nested SQ-family shapes: general interpreter, no XPSQ code
   if (!rc && (class_mask & 8))
-    rc = dispatch_sdf<3>(s, multi ? 3 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
+    rc = dispatch_sdf<3>(s, multi ? 3 : -1, first == 3, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
   // constant-schedule XPSQ inside boolean trees
   if (!rc && (class_mask & 16))
-    rc = dispatch_sdf<4>(s, multi ? 4 : -1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
+    rc = dispatch_sdf<4>(s, multi ? 4 : -1, first == 4, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
   return rc;
 }
 
@@ -446,6 +464,14 @@ __global__ void __launch_bounds__(256) k_sdf_param_grad(SceneDev S, const int32_
     const int sid0 = __shfl_sync(0xffffffffu, sid, 0);
     const bool uni = __all_sync(0xffffffffu, valid && sid == sid0);
     if (!valid) continue;
+    if ((unsigned)sid >= (unsigned)S.n_shapes || !S.shapes[sid].has_sdf) {
+      // invalid shape id: NaN rows of J, no VJP contribution, counted (a warp
+      // is uniform only if all its lanes take this branch: no shuffles skipped)
+      if (J)
+        for (int k = 0; k < pmax; ++k) J[(int64_t)k * N + n] = __int_as_float(0x7fc00000);
+      atomicAdd(S.err, 1u);
+      continue;
+    }
     const ShapeRec sh = S.shapes[sid];
     const float4 pa = __ldg(reinterpret_cast<const float4*>(poses) + 2 * b);
     const float4 pb = __ldg(reinterpret_cast<const float4*>(poses) + 2 * b + 1);

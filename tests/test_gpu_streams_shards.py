@@ -90,3 +90,58 @@ def test_shard_rows_equal_full_run(cuda, lo, n):
     torch.cuda.synchronize()
     for k, v in out_sh.items():
         assert _same(v, out_full[k][..., r0:r0 + Cs]), k
+
+
+def test_invalid_records_counted_not_dereferenced(cuda):
+    """Device-side validation: pair records with
+    out-of-range env / slot indices get NaN rows, out-of-range shape ids get
+    no rows, sdf_eval bodies with a bad shape id get NaN outputs; each is
+    counted in cm_scene_error_count and the valid records' outputs are
+    unchanged (no device fault)."""
+    torch = cuda
+    from paper_2604_17538_b200 import binding
+    sc = synth.c5_scene(64)
+    S = binding.Scene(sc.shapes, sc.smooth)
+    assert S.error_count(reset=True) == 0
+    good = sc.pairs.copy()
+    bad = good.copy()
+    bad[3, 0] = 10 ** 6                  # env out of range: NaN rows
+    bad[7, 2] = 5                        # slot out of range: NaN rows
+    bad[11, 4] = len(sc.shapes) + 3      # SDF shape id out of range: no rows
+    ref = {}
+    for name, pr in (("good", good), ("bad", bad)):
+        pt = torch.from_numpy(pr).cuda()
+        po = torch.from_numpy(sc.poses).cuda()
+        offs = S.manifold_offsets(pt)
+        # the host size call rejects the bad shape id; size the outputs from
+        # the device offsets (what a caller with device-only pairs would do)
+        last = int(offs[-1].item()) + S.counts(int(pr[-1, 3]))[2]
+        out = S.contact_manifold(pt, offs, last, po, 2)
+        torch.cuda.synchronize()
+        ref[name] = (offs.cpu().numpy(), {k: v.cpu().numpy() for k, v in out.items()}, last)
+    assert S.error_count() == 4   # offsets kernel: the bad shape id; manifold: the 3 bad records
+    og, g, _ = ref["good"]
+    ob, b, _ = ref["bad"]
+    F = lambda i: S.counts(int(good[i, 3]))[2]
+    for i in range(len(good)):
+        if i == 11:
+            assert ob[i + 1] == ob[i] if i + 1 < len(good) else True
+            continue
+        rg = slice(og[i], og[i] + F(i))
+        rb = slice(ob[i], ob[i] + F(i))
+        if i in (3, 7):
+            assert np.isnan(b["depth"][rb]).all() and (b["dom"][rb] == -1).all()
+        else:
+            for k in g:
+                assert np.array_equal(g[k][..., rg], b[k][..., rb], equal_nan=True), (i, k)
+    # sdf_eval: body 1 names a shape id out of range
+    ids = torch.tensor([16, 10 ** 5, 17], dtype=torch.int32, device="cuda")
+    poses = torch.zeros(3, 8, device="cuda")
+    poses[:, 3] = 1
+    pts = torch.rand(3 * 5, 3, device="cuda") * 0.1
+    S.error_count(reset=True)
+    o = S.sdf_eval(ids, poses, pts, 5, binding.SDF_VALUE | binding.SDF_GRAD)
+    torch.cuda.synchronize()
+    d = o["d"].cpu().numpy()
+    assert np.isnan(d[5:10]).all() and np.isfinite(d[:5]).all() and np.isfinite(d[10:]).all()
+    assert S.error_count() == 5
