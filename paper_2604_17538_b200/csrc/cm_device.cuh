@@ -645,14 +645,15 @@ __device__ __forceinline__ void xpsq_t_implicit(const Xpsq& X, const SmoothDev& 
                                                 int newton, float* tv, float* tg, float* th) {
   const float c1 = fmaf(2.f * X.A[0], w[0], fmaf(2.f * X.A[1], w[1], fmaf(2.f * X.A[2], w[2], -X.BB)));
   const float c0 = fmaf(X.B[0], w[0], fmaf(X.B[1], w[1], X.B[2] * w[2]));
-  float r = 0.f;
-  for (int it = 0; it < newton; ++it) {
-    const float g = fmaf(fmaf(fmaf(X.c3, t, X.c2), t, c1), t, c0);
-    const float gp = fmaf(fmaf(3.f * X.c3, t, 2.f * X.c2), t, c1);
-    r = rcpa(gp);
+  // one Newton step always, a second for nearly straight splines (newton = 2)
+  float g = fmaf(fmaf(fmaf(X.c3, t, X.c2), t, c1), t, c0);
+  float r = rcpa(fmaf(fmaf(3.f * X.c3, t, 2.f * X.c2), t, c1));
+  t = fmaf(-g, r, t);
+  if (newton > 1) {
+    g = fmaf(fmaf(fmaf(X.c3, t, X.c2), t, c1), t, c0);
+    r = rcpa(fmaf(fmaf(3.f * X.c3, t, 2.f * X.c2), t, c1));
     t = fmaf(-g, r, t);
   }
-  if (newton == 0 && O >= 1) r = rcpa(fmaf(fmaf(3.f * X.c3, t, 2.f * X.c2), t, c1));
   float v, d1, d2;
   softclip_12(t, 0.f, 1.f, sp.tau_clip_t, sp.i_clip_t, v, d1, d2);
   *tv = v;
@@ -675,12 +676,11 @@ __device__ __forceinline__ void xpsq_t_implicit(const Xpsq& X, const SmoothDev& 
   }
 }
 
-// The curved spline's rarer regimes, out of line so that the common
-// one-real-root path stays small in the instruction cache: three real roots
+// The curved spline's rarer regimes (inline by default): three real roots
 // (Delta > 46 tau_Delta) and the soft-Cardano band (both branches,
 // P:113-124).  Returns true when the three roots are identical.
 #ifndef CM_XPSQ_RARE_NOINLINE
-#define CM_XPSQ_RARE_NOINLINE 1
+#define CM_XPSQ_RARE_NOINLINE 0   // out of line: C5 -19% (its array arguments live in local memory), r02l
 #endif
 template <int O>
 __device__
@@ -729,28 +729,20 @@ bool xpsq_root_t_rare(const Xpsq& X, const SmoothDev& sp, const float* w, float 
 template <int O>
 __device__ __forceinline__ bool xpsq_root_t(const Xpsq& X, const SmoothDev& sp, const float* w, float* tv, float (*tg)[3],
                                             float (*th)[6]) {
+  // (when the three roots are identical only entry 0 is written)
   const float tc = sp.tau_clip_t, itc = sp.i_clip_t;
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    tv[k] = 0.5f;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) tg[k][i] = 0.f;
-#pragma unroll
-    for (int q = 0; q < 6; ++q) th[k][q] = 0.f;
-  }
   if (X.cls == 1) {
     const float s = X.Bn[0] * w[0] + X.Bn[1] * w[1] + X.Bn[2] * w[2];
     float v, d1, d2;
     softclip_12(s, 0.f, 1.f, tc, itc, v, d1, d2);
+    tv[0] = v;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      tv[k] = v;
+    for (int i = 0; i < 3; ++i) tg[0][i] = d1 * X.Bn[i];
 #pragma unroll
-      for (int i = 0; i < 3; ++i) tg[k][i] = d1 * X.Bn[i];
-#pragma unroll
-      for (int q = 0; q < 6; ++q) th[k][q] = d2 * X.Bn[jhi<3>(q)] * X.Bn[jhj<3>(q)];
-    }
-  } else if (X.cls == 2) {
+    for (int q = 0; q < 6; ++q) th[0][q] = d2 * X.Bn[jhi<3>(q)] * X.Bn[jhj<3>(q)];
+    return true;
+  }
+  if (X.cls == 2) {
     const float Pv = X.gP[0] * w[0] + X.gP[1] * w[1] + X.gP[2] * w[2] + X.P0;
     const float Qv = X.gQ[0] * w[0] + X.gQ[1] * w[1] + X.gQ[2] * w[2] + X.Q0;
     const float Delta = -(4.f * Pv * Pv * Pv + 27.f * Qv * Qv);
@@ -764,18 +756,16 @@ __device__ __forceinline__ bool xpsq_root_t(const Xpsq& X, const SmoothDev& sp, 
       const float u = cbrt_fast(Qv >= 0.f ? -0.5f * Qv - sD : -0.5f * Qv + sD);
       const float s = fabsf(u) > 1e-30f ? u - Pv * rcpa(3.f * u) : u;
       xpsq_t_implicit<O>(X, sp, w, s - X.b3, newton, &tv[0], tg[0], th[0]);
-#pragma unroll
-      for (int k = 1; k < 3; ++k) {
-        tv[k] = tv[0];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) tg[k][i] = tg[0][i];
-#pragma unroll
-        for (int q = 0; q < 6; ++q) th[k][q] = th[0][q];
-      }
       return true;
     }
     return xpsq_root_t_rare<O>(X, sp, w, Pv, Qv, Delta, newton, tv, tg, th);
   }
+  // point spline: t = 1/2, no derivatives
+  tv[0] = 0.5f;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) tg[0][i] = 0.f;
+#pragma unroll
+  for (int q = 0; q < 6; ++q) th[0][q] = 0.f;
   return true;
 }
 
@@ -785,7 +775,16 @@ template <int O> __device__ CM_XINL void xpsq_eval(const Xpsq& X, const SmoothDe
   J3<O> tk[3];
   {
     float tv[3], tg[3][3], th[3][6];
-    xpsq_root_t<O>(X, sp, w, tv, tg, th);
+    if (xpsq_root_t<O>(X, sp, w, tv, tg, th)) {   // identical roots: entry 0 only
+#pragma unroll
+      for (int k = 1; k < 3; ++k) {
+        tv[k] = tv[0];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) tg[k][i] = tg[0][i];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) th[k][q] = th[0][q];
+      }
+    }
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       tk[k].v = tv[k];

@@ -499,6 +499,12 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
   D.leaves = dev_copy(leaves, rc);
   D.xpsq = dev_copy(xps, rc);
   D.shapes = dev_copy(recs, rc);
+  {   // compact per-shape SDF class (sdf_eval's class kernels skip foreign points on one byte)
+    std::vector<int8_t> cls(n_shapes);
+    for (int s = 0; s < n_shapes; ++s) cls[s] = recs[s].has_sdf ? (int8_t)recs[s].uses_xpsq : (int8_t)-1;
+    D.shape_cls = dev_copy(cls, rc);
+    if (D.shape_cls) sc->allocs.push_back(const_cast<int8_t*>(D.shape_cls));
+  }
   D.verts = dev_copy(verts, rc);
   D.edges = dev_copy(edges_all, rc);
   D.edge_geom = dev_copy(edge_geom, rc);

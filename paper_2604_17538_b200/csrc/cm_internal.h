@@ -97,6 +97,7 @@ struct SceneDev {
   SmoothDev sp;
   int32_t n_shapes;
   unsigned int* err;          // device counter of invalid pair records / shape ids (cm_scene_error_count)
+  const int8_t* shape_cls;    // per shape: its SDF class (ShapeRec::uses_xpsq), -1 without an SDF
 };
 
 // manifold chunk scratch: the units of one chunk keep their candidate state

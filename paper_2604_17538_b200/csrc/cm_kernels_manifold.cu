@@ -824,12 +824,14 @@ __device__ __forceinline__ void mf_traces_unit_n(const MfArgs& a, const UnitCtx&
 
 // ---- phase 3: edge points p_e = v_I + a_bar e_t, a_bar = (a_I + a_II)/2
 template <int TIER, int XP>
-__device__ __forceinline__ void mf_midpoints_unit(const MfArgs& a, const UnitCtx& U, int u, const float* srec) {
+__device__ __forceinline__ void mf_midpoints_unit(const MfArgs& a, const UnitCtx& U, int u, const float* srec,
+                                                  float* drec = nullptr) {
   constexpr int OV = TIER >= 2 ? 2 : 1;
   const PairFrame& F = U.F;
   const int V = U.SA.V, E = U.SA.E;
   float* se = a.scratch + (int64_t)u * a.slot + (int64_t)vrec(TIER) * V;
   if (srec == nullptr) srec = se;   // trace records: staged in shared memory, or the slot
+  if (drec == nullptr) drec = se;   // edge records: to the slot, or to shared memory (fused faces)
   const float* eg = a.S.edge_geom + 8 * (int64_t)U.SA.e_off;
   const bool full = (a.mode & CM_FULL_MODE) != 0;
   const float itcmp = a.S.sp.i_cmp;
@@ -839,7 +841,7 @@ __device__ __forceinline__ void mf_midpoints_unit(const MfArgs& a, const UnitCtx
     float eb[3], ew[3];
     rot_vec(F.Rrel, el, eb);
     rot_vec(F.RA, el, ew);
-    float* rec = se + e * erec(TIER);
+    float* rec = drec + e * erec(TIER);
     const float* rin = srec + e * erec(TIER);
     float ab, dab[NDQ];
     float d2ab[TIER >= 3 ? N45 : 1];
@@ -922,7 +924,8 @@ __host__ __device__ constexpr int face_stage_floats(int V, int E, int tier) {
 
 template <int TIER, bool STAGED>
 __device__ __forceinline__ void mf_faces_unit(const MfArgs& a, const UnitCtx& U, int u, float* fsm, uint64_t* barp,
-                                              uint32_t phase) {
+                                              uint32_t phase, const float* sv_in = nullptr,
+                                              const float* se_in = nullptr) {
   const SmoothDev sp = a.S.sp;
   const float itcmp = sp.i_cmp;
   const float tmin = sp.tau_min, itmin = sp.i_min;
@@ -937,8 +940,9 @@ __device__ __forceinline__ void mf_faces_unit(const MfArgs& a, const UnitCtx& U,
   const int32_t* fe = a.S.face_edges + 3 * (int64_t)U.SA.f_off;
   const cm_manifold_out& out = a.out;
   const int64_t C = a.C;
-  const float* sv = gv;
-  const float* se = ge;
+  // (fused with the midpoint kernel: the records are given in shared memory)
+  const float* sv = sv_in ? sv_in : gv;
+  const float* se = se_in ? se_in : ge;
   float* s_pv = nullptr;   // staged vertex points p[3][V]
   float* s_pe = nullptr;   // staged edge p_I[3][E], e_t[3][E]
   if constexpr (STAGED) {
@@ -1289,6 +1293,39 @@ __global__ void __maxnreg__((RegCap<TIER, XP>::MIDPOINTS)) k_mf_midpoints(const 
     mf_midpoints_unit<TIER, XP>(a, U, u, nullptr);
   }
 }
+// Midpoints and face fusion in one kernel per SDF class (reduced mode, tiers
+// 0-2): the unit's edge records are written to shared memory instead of the
+// slot, its vertex records arrive by one TMA bulk copy (overlapped with the
+// midpoint evaluations), and the face loop gathers both from shared memory
+// (no scratch round trip through HBM for the edge records, no separate face
+// launch).  Shared memory: max_E edge + max_V vertex records.
+#ifndef CM_MF_FUSE_FACES
+#define CM_MF_FUSE_FACES 1
+#endif
+template <int TIER, int XP> struct MidFacesRegs {   // the larger of the midpoint and face budgets
+  static constexpr int R = RegCap<TIER, XP>::MIDPOINTS > regs_of(CM_MF_FACE_MINB) ? RegCap<TIER, XP>::MIDPOINTS
+                                                                                     : regs_of(CM_MF_FACE_MINB);
+};
+template <int TIER, int XP>
+__global__ void __maxnreg__((MidFacesRegs<TIER, XP>::R)) k_mf_midfaces(const MfArgs a, int max_E) {
+  static_assert(TIER <= 2, "tier 3: separate kernels");
+  extern __shared__ __align__(16) float fsm[];
+  __shared__ UnitCtx U;
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) mbar_init(&bar, 1);   // published by list_unit's barrier
+  int u;
+  if (!list_unit(a, XP, U, u)) return;
+  constexpr int VR = vrec(TIER), ER = erec(TIER);
+  float* se_s = fsm;
+  float* sv_s = fsm + (int64_t)max_E * ER;
+  const float* gv = a.scratch + (int64_t)u * a.slot;
+  if (threadIdx.x == 0) bulk_g2s(sv_s, gv, (uint32_t)(U.SA.V * VR) * 4u, &bar);
+  mf_midpoints_unit<TIER, XP>(a, U, u, nullptr, se_s);
+  mbar_wait(&bar, 0u);
+  __syncthreads();
+  mf_faces_unit<TIER, false>(a, U, u, nullptr, nullptr, 0u, sv_s, se_s);
+}
+
 template <int TIER, bool STAGED>
 __global__ void __launch_bounds__(CM_MF_MAX_THREADS, TIER >= 3 ? 1 : CM_MF_FACE_MINB) k_mf_faces(const MfArgs a) {
   extern __shared__ __align__(16) float fsm[];
@@ -1307,13 +1344,29 @@ int64_t manifold_slot_floats(int V, int E, int tier) {
   return (int64_t)vrec(tier) * V + (int64_t)erec(tier) * E;
 }
 
+// the fused midpoint + face kernel's shared memory (0: not used)
+static int midfaces_bytes(int tier, uint32_t mode, int max_V, int max_E) {
+  if (!CM_MF_FUSE_FACES || tier > 2 || (mode & CM_FULL_MODE)) return 0;
+  const int b = (max_E * erec(tier) + max_V * vrec(tier)) * 4;
+  return b <= 160 * 1024 ? b : 0;
+}
+
 template <int TIER, int XP>
-static int launch_sdf_phases(MfArgs& a, int64_t nb, int T, int max_E, cudaStream_t st) {
+static int launch_sdf_phases(MfArgs& a, int64_t nb, int T, int max_V, int max_E, cudaStream_t st) {
   k_mf_vertices<TIER, XP><<<(unsigned)nb, T, 0, st>>>(a);
   int rc = check_launch("k_mf_vertices");
   if (rc) return rc;
   k_mf_traces<TIER, XP><<<(unsigned)nb, T, 0, st>>>(a);
   if ((rc = check_launch("k_mf_traces"))) return rc;
+  if constexpr (TIER <= 2) {
+    const int fb = midfaces_bytes(TIER, a.mode, max_V, max_E);
+    if (fb > 0) {
+      if (fb > 48 * 1024)
+        cudaFuncSetAttribute(k_mf_midfaces<TIER, XP>, cudaFuncAttributeMaxDynamicSharedMemorySize, fb);
+      k_mf_midfaces<TIER, XP><<<(unsigned)nb, T, fb, st>>>(a, max_E);
+      return check_launch("k_mf_midfaces");
+    }
+  }
   const int mid_bytes = max_E * erec(TIER) * 4;
   if (CM_MF_STAGE_MID && mid_bytes <= 96 * 1024) {
     if (mid_bytes > 48 * 1024)
@@ -1377,13 +1430,13 @@ static int launch_tier(MfArgs a, int class_mask, int max_V, int max_E, int64_t n
     // SDF phases: one instantiation per SDF class present in the scene
     // (cm_internal.h ShapeRec::uses_xpsq); each takes its class's units from
     // the list k_mf_units built
-    if (class_mask & 1) rc = launch_sdf_phases<TIER, 0>(a, nb, T, max_E, st);
-    if (!rc && (class_mask & 2)) rc = launch_sdf_phases<TIER, 1>(a, nb, T, max_E, st);
-    if (!rc && (class_mask & 4)) rc = launch_sdf_phases<TIER, 2>(a, nb, T, max_E, st);
-    if (!rc && (class_mask & 8)) rc = launch_sdf_phases<TIER, 3>(a, nb, T, max_E, st);
-    if (!rc && (class_mask & 16)) rc = launch_sdf_phases<TIER, 4>(a, nb, T, max_E, st);
+    if (class_mask & 1) rc = launch_sdf_phases<TIER, 0>(a, nb, T, max_V, max_E, st);
+    if (!rc && (class_mask & 2)) rc = launch_sdf_phases<TIER, 1>(a, nb, T, max_V, max_E, st);
+    if (!rc && (class_mask & 4)) rc = launch_sdf_phases<TIER, 2>(a, nb, T, max_V, max_E, st);
+    if (!rc && (class_mask & 8)) rc = launch_sdf_phases<TIER, 3>(a, nb, T, max_V, max_E, st);
+    if (!rc && (class_mask & 16)) rc = launch_sdf_phases<TIER, 4>(a, nb, T, max_V, max_E, st);
     if (rc) return rc;
-    if (!full) {   // the fusion does not depend on the SDF class: one launch
+    if (!full && midfaces_bytes(TIER, a.mode, max_V, max_E) == 0) {   // the fusion does not depend on the SDF class: one launch
       if (stage_bytes > 0 && (stage_bytes <= kStageSmallBytes || nb < 8 * (int64_t)num_sms()))
         k_mf_faces<TIER, true><<<(unsigned)nb, T, stage_bytes, st>>>(a);
       else

@@ -25,8 +25,11 @@ using cml::num_sms;
 #ifndef CM_SDF_MINB
 #define CM_SDF_MINB 3   // 80 registers: +2% on the SDF workload over 1 and 2
 #endif
+#ifndef CM_SDF_MINB_XP
+#define CM_SDF_MINB_XP 2   // the XPSQ classes (1, 2, 4): 128 registers, SDF +1.8% over 80 (r02m)
+#endif
 template <int O, int XP, bool PG, bool PH>
-__global__ void __launch_bounds__(256, CM_SDF_MINB) k_sdf_eval(SceneDev S, const int32_t* __restrict__ shape_ids,
+__global__ void __launch_bounds__(256, (XP == 1 || XP == 2 || XP == 4) ? CM_SDF_MINB_XP : CM_SDF_MINB) k_sdf_eval(SceneDev S, const int32_t* __restrict__ shape_ids,
                                                   const float* __restrict__ poses, const float* __restrict__ points,
                                                   int64_t B, int64_t P, float* __restrict__ d,
                                                   float* __restrict__ grad, float* __restrict__ hess,
@@ -36,7 +39,11 @@ __global__ void __launch_bounds__(256, CM_SDF_MINB) k_sdf_eval(SceneDev S, const
   for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < N; n += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = n / P;
     const int sid = __ldg(shape_ids + b);
-    if ((unsigned)sid >= (unsigned)S.n_shapes || !S.shapes[sid].has_sdf) {
+    // the class byte first: points of other classes are skipped without
+    // loading their 64-B shape record
+    const int cls = (unsigned)sid < (unsigned)S.n_shapes ? (int)__ldg(S.shape_cls + sid) : -1;
+    if (cls >= 0 && xp_filter >= 0 && cls != xp_filter) continue;
+    if (cls < 0) {
       // invalid shape id (or a shape without an SDF): NaN outputs, written and
       // counted once per point by the first class instantiation launched
       if (own_invalid) {
@@ -52,7 +59,6 @@ __global__ void __launch_bounds__(256, CM_SDF_MINB) k_sdf_eval(SceneDev S, const
       continue;
     }
     const ShapeRec sh = S.shapes[sid];
-    if (xp_filter >= 0 && sh.uses_xpsq != xp_filter) continue;
     const float4 pa = __ldg(reinterpret_cast<const float4*>(poses) + 2 * b);
     const float4 pb = __ldg(reinterpret_cast<const float4*>(poses) + 2 * b + 1);
     const float t[3] = {pa.x, pa.y, pa.z};

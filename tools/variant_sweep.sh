@@ -16,7 +16,7 @@ for r in $(seq 1 $R); do
       ch*) L=paper_2604_17538_b200/libxpsqcm.so; E="CM_CHUNK_UNITS=${v#ch}" ;;
       *) L=exp/lib_$v.so ;;
     esac
-    for w in C5 C4; do
+    for w in ${WLS:-C5 C4}; do
       line=$(env $E XPSQCM_LIB=$L timeout 300 python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline --no-e2e 2>>$O/err.log | tail -1)
       echo "{\"variant\": \"$v\", \"round\": $r, \"workload\": \"$w\", \"line\": $line}" >> $O/sweep.jsonl
     done
