@@ -15,10 +15,20 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges around the C-ABI compute calls
+
 #include "cm_internal.h"
 #include "xpsq_cm.h"
 
 using namespace cmi;
+
+namespace {
+// NVTX range of one C-ABI call (visible in Nsight Systems / ncu --nvtx)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace {
 thread_local std::string g_err;
@@ -527,6 +537,8 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
                    (float)(1.0 / sp->tau_cmp), (float)(1.0 / sp->tau_min), (float)(1.0 / sp->tau_clip_alpha),
                    (float)(1.0 / sp->tau_clip_t), (float)(1.0 / sp->tau_delta)};
   D.n_shapes = n_shapes;
+  D.n_leaves = (int32_t)leaves.size();
+  D.n_xpsq = (int32_t)xps.size();
   // chunk scratch of the manifold kernels (one candidate-state slot per unit)
   if (rc == CM_OK && sc->max_F > 0) {
     const int64_t slot = cml::manifold_slot_floats(sc->max_V, sc->max_E, 2);
@@ -588,6 +600,7 @@ int cm_shape_topology(const cm_scene* sc, int32_t s, int32_t* edges, int32_t* fa
 int cm_sdf_eval(const cm_scene* sc, const int32_t* ids, const float* poses, const float* points, int64_t B, int64_t P,
                 uint32_t flags, float* d, float* grad, float* hess, float* dpose, float* d2pose, float* dxdpose,
                 void* stream) {
+  NvtxRange nvtx_range("cm_sdf_eval");
   if (!sc) return fail(CM_ERR_INVALID, "cm_sdf_eval: NULL scene");
   if (B < 0 || P < 0) return fail(CM_ERR_INVALID, "cm_sdf_eval: negative size");
   if (B == 0 || P == 0) return CM_OK;   // empty batch: nothing to launch
@@ -641,6 +654,7 @@ int cm_param_layout(const cm_scene* sc, int32_t* counts, int64_t* offsets) {
 
 int cm_sdf_param_grad(const cm_scene* sc, const int32_t* ids, const float* poses, const float* points, int64_t B,
                       int64_t P, int32_t pmax, float* J, const float* w, float* vjp, void* stream) {
+  NvtxRange nvtx_range("cm_sdf_param_grad");
   if (!sc) return fail(CM_ERR_INVALID, "cm_sdf_param_grad: NULL scene");
   if (B < 0 || P < 0 || pmax < 0) return fail(CM_ERR_INVALID, "cm_sdf_param_grad: negative size");
   if (B == 0 || P == 0) return CM_OK;
@@ -680,6 +694,7 @@ int64_t cm_manifold_offsets_workspace(int64_t n_pairs) { return cml::offsets_wor
 
 int cm_manifold_offsets(const cm_scene* sc, const int32_t* pairs, int64_t n_pairs, uint32_t flags, int64_t* offsets,
                         void* ws, int64_t ws_bytes, void* stream) {
+  NvtxRange nvtx_range("cm_manifold_offsets");
   if (!sc) return fail(CM_ERR_INVALID, "cm_manifold_offsets: NULL scene");
   if (n_pairs == 0) return CM_OK;
   if (!pairs || !offsets || !ws) return fail(CM_ERR_INVALID, "cm_manifold_offsets: NULL argument");
@@ -693,6 +708,7 @@ int cm_manifold_offsets(const cm_scene* sc, const int32_t* pairs, int64_t n_pair
 int cm_contact_manifold(const cm_scene* sc, const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,
                         const float* poses, int64_t n_env, int32_t n_slot, uint32_t flags, const cm_manifold_out* out,
                         int64_t n_contacts, void* stream) {
+  NvtxRange nvtx_range("cm_contact_manifold");
   if (!sc || !out) return fail(CM_ERR_INVALID, "cm_contact_manifold: NULL argument");
   if (n_pairs < 0 || n_env < 0 || n_slot <= 0 || n_contacts < 0) return fail(CM_ERR_INVALID, "cm_contact_manifold: sizes");
   if (n_pairs == 0) return CM_OK;   // empty batch: nothing to launch
@@ -752,6 +768,7 @@ int cm_contact_manifold(const cm_scene* sc, const int32_t* pairs, int64_t n_pair
 int cm_expand_jacobian(const cm_scene* sc, const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,
                        const float* poses, int64_t n_env, int32_t n_slot, uint32_t flags, const float* W,
                        const float* q, int64_t n_contacts, float* J, void* stream) {
+  NvtxRange nvtx_range("cm_expand_jacobian");
   if (!sc || !pairs || !offsets || !poses || !W || !q || !J) return fail(CM_ERR_INVALID, "cm_expand_jacobian");
   int rc = cml::launch_expand(pairs, n_pairs, offsets, sc->dev, poses, n_env, n_slot, W, q, n_contacts, J, flags, stream);
   if (rc) return fail(rc, cml::last_cuda_error());

@@ -98,17 +98,18 @@ struct SceneDev {
   int32_t n_shapes;
   unsigned int* err;          // device counter of invalid pair records / shape ids (cm_scene_error_count)
   const int8_t* shape_cls;    // per shape: its SDF class (ShapeRec::uses_xpsq), -1 without an SDF
+  int32_t n_leaves, n_xpsq;   // sizes of leaves[] and xpsq[] (shared-memory staging)
 };
 
 // manifold chunk scratch: the units of one chunk keep their candidate state
 // in a global slot each; the scene allocates kChunkUnits slots (capped at
 // kScratchCapBytes) at creation (CM_CHUNK_UNITS overrides the unit count)
-constexpr int64_t kChunkUnits = 32768;
+constexpr int64_t kChunkUnits = 262144;   // C5 +5%, C4 +2% over 32768 (r02q sweep; 4-7 GB of scratch)
 #ifndef CM_N_AUX_STREAMS
 #define CM_N_AUX_STREAMS 2
 #endif
 constexpr int kManifoldStreams = CM_N_AUX_STREAMS;   // chunks alternate between the scene's aux streams
-constexpr int64_t kScratchCapBytes = 1024ll << 20;
+constexpr int64_t kScratchCapBytes = 8192ll << 20;
 
 // shape-parameter derivatives (f4): boolean nodes of one shape the
 // parameter kernel tracks per point (shapes with more report count -1)

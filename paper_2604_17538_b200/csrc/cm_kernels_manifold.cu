@@ -1300,7 +1300,7 @@ __global__ void __maxnreg__((RegCap<TIER, XP>::MIDPOINTS)) k_mf_midpoints(const 
 // (no scratch round trip through HBM for the edge records, no separate face
 // launch).  Shared memory: max_E edge + max_V vertex records.
 #ifndef CM_MF_FUSE_FACES
-#define CM_MF_FUSE_FACES 1
+#define CM_MF_FUSE_FACES 0   // measured slower: C5 -3.5%, C4 -12.6% (r02n sweep)
 #endif
 template <int TIER, int XP> struct MidFacesRegs {   // the larger of the midpoint and face budgets
   static constexpr int R = RegCap<TIER, XP>::MIDPOINTS > regs_of(CM_MF_FACE_MINB) ? RegCap<TIER, XP>::MIDPOINTS
