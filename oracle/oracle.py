@@ -228,6 +228,29 @@ class OracleScene:
         out["offsets"] = np.concatenate([[0], np.cumsum(F)]).astype(np.int64)
         return out
 
+    @staticmethod
+    def pair_reduce(out, tau_min, w_depth=None, w_normal=None):
+        """Pair-level reductions of a manifold computed by contact_manifold
+        (plain numpy over its rows, pair i at rows offsets[i]:offsets[i+1]):
+        pair_depth = -tau_min log sum exp(-depth / tau_min) (the fusion's
+        smooth minimum, P:161 / reading #25), pair_W = sum W, and the
+        vector-Jacobian product g_pose[i] = sum_rows w_depth ddepth + sum_k
+        w_normal[:, k] dnormal[:, k, :] (12 per pair)."""
+        off = out["offsets"]
+        n = len(off) - 1
+        pd, pw, gp = np.zeros(n), np.zeros(n), np.zeros((n, 12))
+        for i in range(n):
+            r = slice(off[i], off[i + 1])
+            d = out["depth"][r]
+            m = np.max(-d)
+            pd[i] = -(m + tau_min * np.log(np.sum(np.exp((-d - m) / tau_min))))
+            pw[i] = np.sum(out["W"][r])
+            if w_depth is not None:
+                gp[i] += w_depth[r] @ out["ddepth"][r]
+            if w_normal is not None:
+                gp[i] += np.einsum("rk,rkj->j", w_normal[r], out["dnormal"][r])
+        return pd, pw, gp
+
     def param_count(self, shape):
         """Number of shape parameters (-1: an XPSQ node, not parametrised)."""
         return lib().ora_shape_param_count(self.h, int(shape))

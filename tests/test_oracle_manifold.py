@@ -502,3 +502,44 @@ def test_manifold_d2depth_two_sided(oracle_mod):
     Hs = Ht[:, perm][:, :, perm]
     H2 = _unpack78(two[n:])
     assert np.allclose(H2, Hs, rtol=0, atol=1e-12 * np.abs(Hs).max())
+
+
+def test_pair_reduce_pins(oracle_mod):
+    """Pair-level reductions: pair_depth lies in the LSE
+    sandwich [min d - tau ln n, min d]; pair_W = sum W; the pose VJP equals
+    the central finite difference of sum(w_depth depth + w_normal . normal)
+    over the world-frame twist chart of both bodies."""
+    import numpy as np
+    from helpers import perturb
+    from paper_2604_17538_b200 import synth
+    O = oracle_mod
+    sc = synth.c4_scene(2)
+    osc = O.OracleScene(sc)
+    pairs = sc.pairs[:6]
+    out = osc.contact_manifold(pairs=pairs)
+    tau = sc.smooth["tau_min"]
+    rng = np.random.default_rng(5)
+    wd = rng.normal(size=out["depth"].shape)
+    wn = rng.normal(size=out["normal"].shape)
+    pd, pw, gp = O.OracleScene.pair_reduce(out, tau, wd, wn)
+    off = out["offsets"]
+    for i in range(len(pairs)):
+        d = out["depth"][off[i]:off[i + 1]]
+        assert d.min() - tau * np.log(len(d)) - 1e-12 <= pd[i] <= d.min() + 1e-12
+        assert pw[i] == np.sum(out["W"][off[i]:off[i + 1]])
+    h = 1e-6
+    for i in (0, 3):
+        env, sa, sb = pairs[i, 0], pairs[i, 1], pairs[i, 2]
+        r = slice(off[i], off[i + 1])
+        for j in range(12):
+            dq = np.zeros(6)
+            dq[j % 6] = h
+            vals = []
+            for sgn in (1, -1):
+                poses = sc.poses.astype(np.float64).copy()
+                slot = sa if j < 6 else sb
+                poses[env, slot] = perturb(poses[env, slot], sgn * dq)
+                o2 = osc.contact_manifold(pairs=pairs[i:i + 1], poses=poses)
+                vals.append(np.sum(wd[r] * o2["depth"]) + np.sum(wn[r] * o2["normal"]))
+            fd = (vals[0] - vals[1]) / (2 * h)
+            assert abs(fd - gp[i, j]) <= 1e-4 * max(1.0, abs(gp[i, j])), (i, j, fd, gp[i, j])
