@@ -272,6 +272,26 @@ int cm_expand_jacobian(const cm_scene* scene, const int32_t* pairs, int64_t n_pa
                        const float* poses, int64_t n_env, int32_t n_slot, uint32_t flags, const float* W,
                        const float* q, int64_t n_contacts, float* J, void* stream);
 
+/* Pair-level reductions of a manifold computed with the same mode bits
+ * (`flags`; rows of pair i at [offsets[i], offsets[i] + its contact count)),
+ * one warp per pair with shuffle reductions (SURVEY §8(b) optional outputs,
+ * §8(f) f4 reverse mode).  Every output is device [n_pairs] (g_pose
+ * [12 * n_pairs]) and may be NULL:
+ *   pair_depth[i] = -tau_min log sum exp(-depth / tau_min) over the pair's
+ *                   contacts (the smooth minimum of the fusion, P:161 and
+ *                   DESIGN.md reading #25); NaN for a pair without contacts
+ *   pair_W[i]     = sum of W (needs tier >= 1 outputs)
+ *   g_pose[12 i + j] = sum over the pair's rows of w_depth[row] ddepth[j, row]
+ *                   + sum_k w_normal[k, row] dnormal[k*12 + j, row]: the
+ *                   vector-Jacobian product of the depths and raw normals with
+ *                   respect to q = (dt_A, dtheta_A, dt_B, dtheta_B) (needs
+ *                   tier-2 outputs; w_depth [C] and w_normal [3C] device, either
+ *                   may be NULL).
+ * Errors: CM_ERR_INVALID (NULL where an output needs it), CM_ERR_CUDA. */
+int cm_manifold_pair_reduce(const cm_scene* scene, const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,
+                            uint32_t flags, const cm_manifold_out* out, int64_t n_contacts, const float* w_depth,
+                            const float* w_normal, float* pair_depth, float* pair_W, float* g_pose, void* stream);
+
 /* Number of kernel launches the library issued since scene creation (all
  * scenes, this process) — instrumentation for bench.py's gpu_launches. */
 int64_t cm_launch_count(void);

@@ -26,7 +26,7 @@ EXPORTS = ["cm_version", "cm_last_error", "cm_scene_create", "cm_scene_destroy",
            "cm_param_layout", "cm_sdf_param_grad",
            "cm_shape_topology", "cm_sdf_eval", "cm_manifold_size", "cm_manifold_offsets_workspace",
            "cm_manifold_offsets", "cm_contact_manifold", "cm_expand_jacobian", "cm_launch_count",
-           "cm_scene_error_count"]
+           "cm_scene_error_count", "cm_manifold_pair_reduce"]
 
 
 class cm_node(C.Structure):
@@ -83,8 +83,10 @@ def lib():
         L.cm_contact_manifold.argtypes = [p, p, i64, p, p, i64, i32, u32, p, i64, p]
         L.cm_expand_jacobian.argtypes = [p, p, i64, p, p, i64, i32, u32, p, p, i64, p, p]
         L.cm_launch_count.restype = i64
-        if hasattr(L, "cm_scene_error_count"):   # (older builds in A/B sweeps lack it)
+        if hasattr(L, "cm_scene_error_count"):   # (older builds in A/B sweeps lack these)
             L.cm_scene_error_count.argtypes = [p, p, C.c_int]
+        if hasattr(L, "cm_manifold_pair_reduce"):
+            L.cm_manifold_pair_reduce.argtypes = [p, p, i64, p, u32, p, i64, p, p, p, p, p, p]
         _lib = L
     return _lib
 
@@ -308,6 +310,25 @@ class Scene:
                                          poses.shape[0], poses.shape[1], tier | mode, C.byref(o), n_contacts,
                                          _stream()), "cm_contact_manifold")
         return out
+
+    def pair_reduce(self, pairs, offsets, out, n_contacts: int, mode: int = 0, w_depth=None, w_normal=None,
+                    want_depth: bool = True, want_W: bool = True):
+        """Pair-level reductions (cm_manifold_pair_reduce): pair_depth [NP],
+        pair_W [NP] and, given w_depth [C] / w_normal [3, C], the pose VJP
+        g_pose [NP, 12]."""
+        import torch
+        n = pairs.shape[0]
+        dev = pairs.device
+        pd = torch.empty(n, device=dev, dtype=torch.float32) if want_depth else None
+        pw = torch.empty(n, device=dev, dtype=torch.float32) if want_W and "W" in out else None
+        gp = torch.empty(n, 12, device=dev, dtype=torch.float32) if (w_depth is not None or w_normal is not None) \
+            else None
+        o = cm_manifold_out(*[out[k].data_ptr() if k in out else None
+                              for k in ("point", "normal", "depth", "W", "q", "ddepth", "dnormal", "dom", "d2depth")])
+        _check(lib().cm_manifold_pair_reduce(self.h, _ptr(pairs), n, _ptr(offsets), mode, C.byref(o), n_contacts,
+                                             _ptr(w_depth), _ptr(w_normal), _ptr(pd), _ptr(pw), _ptr(gp), _stream()),
+               "cm_manifold_pair_reduce")
+        return pd, pw, gp
 
     def expand_jacobian(self, pairs, offsets, poses, W, q, n_contacts: int, mode: int = 0):
         import torch

@@ -775,6 +775,24 @@ int cm_expand_jacobian(const cm_scene* sc, const int32_t* pairs, int64_t n_pairs
   return CM_OK;
 }
 
+int cm_manifold_pair_reduce(const cm_scene* sc, const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,
+                            uint32_t flags, const cm_manifold_out* out, int64_t n_contacts, const float* w_depth,
+                            const float* w_normal, float* pair_depth, float* pair_W, float* g_pose, void* stream) {
+  NvtxRange nvtx_range("cm_manifold_pair_reduce");
+  if (!sc || !out) return fail(CM_ERR_INVALID, "cm_manifold_pair_reduce: NULL argument");
+  if (n_pairs < 0 || n_contacts < 0) return fail(CM_ERR_INVALID, "cm_manifold_pair_reduce: sizes");
+  if (n_pairs == 0) return CM_OK;
+  if (!pairs || !offsets) return fail(CM_ERR_INVALID, "cm_manifold_pair_reduce: NULL argument");
+  if (pair_depth && !out->depth) return fail(CM_ERR_INVALID, "cm_manifold_pair_reduce: pair_depth needs out->depth");
+  if (pair_W && !out->W) return fail(CM_ERR_INVALID, "cm_manifold_pair_reduce: pair_W needs out->W (tier >= 1)");
+  if (g_pose && (!out->ddepth || !out->dnormal || (!w_depth && !w_normal)))
+    return fail(CM_ERR_INVALID, "cm_manifold_pair_reduce: g_pose needs tier-2 outputs and w_depth or w_normal");
+  int rc = cml::launch_pair_reduce(sc->dev, pairs, n_pairs, offsets, flags, out, n_contacts, w_depth, w_normal,
+                                   pair_depth, pair_W, g_pose, stream);
+  if (rc) return fail(rc, cml::last_cuda_error());
+  return CM_OK;
+}
+
 int64_t cm_launch_count(void) { return cml::launch_count(); }
 
 int cm_scene_error_count(const cm_scene* sc, int64_t* count, int reset) {

@@ -26,6 +26,20 @@ using namespace cmd;
 using cml::check_launch;
 using cml::num_sms;
 
+// CM_DEBUG_BOUNDS=1 builds (tests only: tools/build_variant.py dbg
+// -DCM_DEBUG_BOUNDS=1) assert every gathered index and output row against
+// its bounds -- the stand-in for compute-sanitizer, which is closed on this
+// pool
+#ifndef CM_DEBUG_BOUNDS
+#define CM_DEBUG_BOUNDS 0
+#endif
+#if CM_DEBUG_BOUNDS
+#include <cassert>
+#define CM_ASSERT(c) assert(c)
+#else
+#define CM_ASSERT(c) ((void)0)
+#endif
+
 // ============================================================================
 // per-unit scratch slot: one 16-B aligned record per candidate (vertex records
 // first, then edge records), loaded and stored with 128-bit accesses
@@ -747,6 +761,7 @@ __device__ __forceinline__ void mf_traces_unit_n(const MfArgs& a, const UnitCtx&
     const int e = j < E ? j : j - E;
     const int dir = j < E ? 0 : 1;     // 0: from v_I along +e_t; 1: from v_II along -e_t
     const int vI = __ldg(ed + 2 * e), vII = __ldg(ed + 2 * e + 1);
+    CM_ASSERT(vI >= 0 && vI < V && vII >= 0 && vII < V);
     const float4 corner = ld4(sv + (dir ? vII : vI) * vrec(TIER));   // d, n of the start vertex
     float xl[3], el[3], L;
     {
@@ -947,6 +962,7 @@ __device__ __forceinline__ void mf_faces_unit(const MfArgs& a, const UnitCtx& U,
   float* s_pe = nullptr;   // staged edge p_I[3][E], e_t[3][E]
   if constexpr (STAGED) {
     const int used = VR * V + ER * E;
+    CM_ASSERT(V >= 0 && E >= 0 && (int64_t)used <= a.slot);
     if (threadIdx.x == 0) bulk_g2s(fsm, gv, (uint32_t)used * 4u, barp);
     s_pv = fsm + used;
     s_pe = s_pv + 3 * V;
@@ -978,7 +994,11 @@ __device__ __forceinline__ void mf_faces_unit(const MfArgs& a, const UnitCtx& U,
   for (int f = threadIdx.x; f < NF; f += blockDim.x) {
     int cv[3], ce[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) { cv[k] = __ldg(fv + 3 * f + k); ce[k] = __ldg(fe + 3 * f + k); }
+    for (int k = 0; k < 3; ++k) {
+      cv[k] = __ldg(fv + 3 * f + k);
+      ce[k] = __ldg(fe + 3 * f + k);
+      CM_ASSERT(cv[k] >= 0 && cv[k] < V && ce[k] >= 0 && ce[k] < E);
+    }
     // candidate depths d_i; order [v_i0, v_i1, v_i2, e(i0,i1), e(i1,i2), e(i2,i0)]
     float dc[6];
 #pragma unroll
@@ -1046,6 +1066,7 @@ __device__ __forceinline__ void mf_faces_unit(const MfArgs& a, const UnitCtx& U,
       }
     }
     const int64_t c = U.off + f;
+    CM_ASSERT(c >= 0 && c < C);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       out.point[k * C + c] = pt[k];
@@ -1248,6 +1269,7 @@ __device__ __forceinline__ bool list_unit(const MfArgs& a, int list, UnitCtx& U,
   if (list >= 0) {
     if (b >= __ldcg(a.cls_count + list)) return false;
     u = __ldcg(a.cls_list + (int64_t)list * a.chunk + b);
+    CM_ASSERT(u >= 0 && u < a.nb);
   } else {
     u = b;
   }

@@ -146,6 +146,102 @@ int launch_expand(const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,
   return check_launch("k_expand_jacobian");
 }
 
+// ---- pair-level reductions (SURVEY §8(b) optional outputs; §8(f) f4 VJP) ----
+// One warp per pair (grid-stride), lanes over the pair's rows, shuffles for
+// the reductions:
+//   pair_depth = -tau LSE(-depth / tau) over the pair's contacts (smooth
+//                minimum, the fusion's own depth operator, reading #25)
+//   pair_W     = sum W
+//   g_pose     = sum_rows (w_depth ddepth[:, row] + sum_k w_normal[k, row] dnormal[k, :, row])
+//                (the vector-Jacobian product of the depths and normals with
+//                respect to q = (dt_A, dtheta_A, dt_B, dtheta_B))
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__global__ void __launch_bounds__(256) k_pair_reduce(const ShapeRec* __restrict__ shapes, int32_t n_shapes,
+                                                     const int32_t* __restrict__ pairs, int64_t n_pairs,
+                                                     const int64_t* __restrict__ offsets, uint32_t flags,
+                                                     cm_manifold_out o, int64_t C, const float* __restrict__ w_depth,
+                                                     const float* __restrict__ w_normal, float tau, float* pair_depth,
+                                                     float* pair_W, float* g_pose) {
+  const bool full = flags & CM_FULL_MODE, two = flags & CM_TWO_SIDED;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const float itl = 1.4426950408889634f / tau;
+  for (int64_t pi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; pi < n_pairs; pi += warps) {
+    const int ia = __ldg(pairs + 5 * pi + 3), ib = __ldg(pairs + 5 * pi + 4);
+    int64_t n = 0;
+    if ((unsigned)ia < (unsigned)n_shapes && (unsigned)ib < (unsigned)n_shapes) {
+      const ShapeRec a = shapes[ia];
+      n = full ? (int64_t)a.V + a.E : (int64_t)a.F;
+      if (two) {
+        const ShapeRec b = shapes[ib];
+        n += full ? (int64_t)b.V + b.E : (int64_t)b.F;
+      }
+    }
+    const int64_t r0 = __ldg(offsets + pi);
+    if (pair_depth) {
+      float m = -INFINITY;
+      for (int64_t r = lane; r < n; r += 32) m = fmaxf(m, -o.depth[r0 + r]);
+      m = warp_max(m);
+      float z = 0.f;
+      for (int64_t r = lane; r < n; r += 32) z += exp2f((-o.depth[r0 + r] - m) * itl);
+      z = warp_sum(z);
+      if (lane == 0) pair_depth[pi] = n > 0 ? -(m + tau * logf(z)) : __int_as_float(0x7fc00000);
+    }
+    if (pair_W) {
+      float w = 0.f;
+      for (int64_t r = lane; r < n; r += 32) w += o.W[r0 + r];
+      w = warp_sum(w);
+      if (lane == 0) pair_W[pi] = w;
+    }
+    if (g_pose) {
+      float g[12];
+#pragma unroll
+      for (int j = 0; j < 12; ++j) g[j] = 0.f;
+      for (int64_t r = lane; r < n; r += 32) {
+        const int64_t c = r0 + r;
+        const float wd = w_depth ? w_depth[c] : 0.f;
+        const float wn[3] = {w_normal ? w_normal[c] : 0.f, w_normal ? w_normal[C + c] : 0.f,
+                             w_normal ? w_normal[2 * C + c] : 0.f};
+#pragma unroll
+        for (int j = 0; j < 12; ++j) {
+          float v = wd * o.ddepth[(int64_t)j * C + c];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) v = fmaf(wn[k], o.dnormal[(int64_t)(k * 12 + j) * C + c], v);
+          g[j] += v;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 12; ++j) {
+        const float v = warp_sum(g[j]);
+        if (lane == 0) g_pose[12 * pi + j] = v;
+      }
+    }
+  }
+}
+
+int launch_pair_reduce(const SceneDev& s, const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,
+                       uint32_t flags, const cm_manifold_out* out, int64_t C, const float* w_depth,
+                       const float* w_normal, float* pair_depth, float* pair_W, float* g_pose, void* stream) {
+  int64_t blocks = (n_pairs * 32 + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) return CM_OK;
+  k_pair_reduce<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(s.shapes, s.n_shapes, pairs, n_pairs, offsets,
+                                                                      flags, *out, C, w_depth, w_normal,
+                                                                      s.sp.tau_min, pair_depth, pair_W, g_pose);
+  return check_launch("k_pair_reduce");
+}
+
 const char* last_cuda_error() { return g_cuda_msg; }
 int64_t launch_count() { return g_launches.load(); }
 

@@ -75,7 +75,9 @@ __global__ void __launch_bounds__(256, (XP == 1 || XP == 2 || XP == 4) ? CM_SDF_
     float y[3];
     to_local(R, t, x, y);
     Res<O> r;
-    eval_shape<O, XP == 3 ? 0 : (XP == 4 ? 1 : XP), XP == 0, CM_SDF_XINL>(S, sh, y, r);
+    // class 4 (XPSQ operands of boolean trees): provably negligible union
+    // operands culled, as in the manifold kernels (cm_device.cuh eval_prog)
+    eval_shape<O, XP == 3 ? 0 : (XP == 4 ? 1 : XP), XP == 0, CM_SDF_XINL, XP == 4>(S, sh, y, r);
     d[n] = r.v;
     if constexpr (O >= 1) {
       float g[3];

@@ -584,3 +584,50 @@ def test_sdf_eval_xpsq_cusp_finite(cuda, oracle_mod):
     gpu = PT.gpu_sdf(S, np.zeros(1, np.int32), pose8().reshape(1, 8).astype(np.float32), pts, len(pts), ALL)
     for k, v in gpu.items():
         assert np.isfinite(v).all(), (k, int((~np.isfinite(v)).sum()))
+
+
+@pytest.mark.parametrize("cfg", ["C4", "C5"])
+def test_pair_reduce(cuda, oracle_mod, cfg):
+    """cm_manifold_pair_reduce (pair-level smooth-min depth, sum W, pose VJP
+    of depths and normals, one warp per pair) against the oracle's reduction
+    of its own contacts, on 64 sampled pairs of a 512-env scene.  Tolerances
+    carried from the per-contact ones."""
+    import torch
+    sc = synth.c4_scene(512) if cfg == "C4" else synth.c5_scene(512)
+    osc = oracle_mod.OracleScene(sc)
+    gpu, S = PT.gpu_manifold(sc, 2)
+    rng = np.random.default_rng(21)
+    C = gpu["C"]
+    wd = rng.normal(size=C).astype(np.float32)
+    wn = rng.normal(size=(3, C)).astype(np.float32)
+    dev = "cuda"
+    out = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in gpu.items() if k not in ("offsets", "C")}
+    pairs_t = torch.from_numpy(sc.pairs).to(dev)
+    offs_t = torch.from_numpy(gpu["offsets"]).to(dev)
+    pd, pw, gp = S.pair_reduce(pairs_t, offs_t, out, C, w_depth=torch.from_numpy(wd).to(dev),
+                               w_normal=torch.from_numpy(wn).to(dev))
+    pd, pw, gp = pd.cpu().numpy(), pw.cpu().numpy(), gp.cpu().numpy()
+    idx = np.sort(rng.choice(len(sc.pairs), 64, replace=False))
+    ref = osc.contact_manifold(pairs=sc.pairs[idx])
+    refp = osc.contact_manifold(pairs=sc.pairs[idx], poses=PT.perturb_inputs(rng, sc.poses))
+    rows = np.concatenate([np.arange(gpu["offsets"][i], gpu["offsets"][i] + (ref["offsets"][k + 1] - ref["offsets"][k]))
+                           for k, i in enumerate(idx)])
+    wd_s, wn_s = wd[rows].astype(np.float64), wn[:, rows].T.astype(np.float64)
+    tau = sc.smooth["tau_min"]
+    r_pd, r_pw, r_gp = oracle_mod.OracleScene.pair_reduce(ref, tau, wd_s, wn_s)
+    p_pd, p_pw, p_gp = oracle_mod.OracleScene.pair_reduce(refp, tau, wd_s, wn_s)
+    rep = []
+    nf = PT.compare("pair_depth", pd[idx], r_pd, p_pd, PT.tol_value(r_pd, sc.ell), rep)
+    off = ref["offsets"]
+    cnt = np.diff(off)
+    nf += PT.compare("pair_W", pw[idx], r_pw, p_pw, 1e-4 * np.maximum(np.abs(r_pw), cnt), rep)
+    # g tolerance: the per-contact tolerances of ddepth and dnormal through |w|
+    tg = np.zeros((len(idx), 1))
+    for k in range(len(idx)):
+        r = slice(off[k], off[k + 1])
+        t_dd = 1e-4 * np.maximum(np.abs(ref["ddepth"][r]).max(1), 1.0)
+        t_dn = 1e-3 * np.maximum(np.abs(ref["dnormal"][r]).max((1, 2)), 1.0 / sc.ell)
+        tg[k] = np.sum(np.abs(wd_s[r]) * t_dd) + np.sum(np.abs(wn_s[r]).sum(1) * t_dn)
+    nf += PT.compare("g_pose", gp[idx], r_gp, p_gp, tg, rep)
+    _report("pair_reduce_%s" % cfg, rep)
+    assert nf == 0, json.dumps(rep, indent=1)
