@@ -725,6 +725,109 @@ int ora_sdf_eval(void* s, const int* shape_ids, const double* poses, const doubl
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// Broad phase ("utilizing [a broad phase] to filter
+// edges prior to passing them to the edge-SDF routine"; DESIGN.md reading
+// #46).  A pair is culled when a certified lower bound of the SDF over every
+// candidate of the sampled surface exceeds M = 40 tau_cmp (every gate
+// sigma(-d/tau_cmp) is then below e^-40): every candidate lies in the convex
+// hull of the sampled vertices, inside their bounding sphere (c_A, r_A), and
+// phi_B(x) >= |x - c_B| - rho_B, so d_i >= |c_A - c_B| - r_A - rho_B =: lb.
+// Bounds of phi_B, in the node frames composed down the tree:
+//   SQ / PSQ: the SQ lies in the box |y_i| <= a_i (eps <= 2) and the radial
+//     distance is |y| minus the surface radius along the ray, so phi >= |y| -
+//     |a|_2 (PSQ = LSE(SQ, planes) >= SQ);
+//   XPSQ: the spline lies in its control points' box; phi >= |x - c| - (half
+//     the box diagonal + max_e |a_e|_2 + tau_min ln 3) (three-root smooth min
+//     >= min - tau ln 3);
+//   half-space: unbounded below (no bound);
+//   union: -LSE(-phi_i) >= min_i phi_i - tau_min ln n >= |x - c| - max_i(|c_i
+//     - c| + rho_i) - tau_min ln n;  intersection LSE(phi_i) >= any phi_i: the
+//     child with the smallest radius;  subtraction LSE(phi_1, -phi_2) >= phi_1.
+// A culled pair's rows: point = the face centroid (full mode: the vertex /
+// edge midpoint), depth = lb - tau_min ln 6 (full mode: lb), a certified lower
+// bound of the fused depth; normal, W, q, derivatives, J, z, gamma = 0;
+// dcand = lb; dom = -2.
+// ---------------------------------------------------------------------------
+struct OBound { double c[3]; double rho; };   // rho = +inf: no bound
+
+static OBound node_bound(const Shape& sh, int idx, const double* Rp, const double* tp, double tau_min) {
+  const Node& n = sh.nodes[idx];
+  double R[9], t[3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) R[i * 3 + j] = Rp[i * 3 + 0] * n.R[0 * 3 + j] + Rp[i * 3 + 1] * n.R[1 * 3 + j] + Rp[i * 3 + 2] * n.R[2 * 3 + j];
+  for (int i = 0; i < 3; ++i) t[i] = Rp[i * 3 + 0] * n.t[0] + Rp[i * 3 + 1] * n.t[1] + Rp[i * 3 + 2] * n.t[2] + tp[i];
+  OBound b;
+  b.rho = INFINITY;
+  for (int i = 0; i < 3; ++i) b.c[i] = t[i];
+  switch (n.type) {
+    case K_HALFSPACE: return b;
+    case K_SQ: case K_PSQ:
+      b.rho = std::sqrt(dot3(n.a[0], n.a[0]));
+      return b;
+    case K_XPSQ: {
+      double lo[3], hi[3], cl[3], h2 = 0.0;
+      for (int i = 0; i < 3; ++i) {
+        lo[i] = std::min({n.ctrl[i], n.ctrl[3 + i], n.ctrl[6 + i]});
+        hi[i] = std::max({n.ctrl[i], n.ctrl[3 + i], n.ctrl[6 + i]});
+        cl[i] = 0.5 * (lo[i] + hi[i]);
+        h2 += 0.25 * (hi[i] - lo[i]) * (hi[i] - lo[i]);
+      }
+      const double am = std::max(std::sqrt(dot3(n.a[0], n.a[0])), std::sqrt(dot3(n.a[1], n.a[1])));
+      for (int i = 0; i < 3; ++i) b.c[i] = R[i * 3 + 0] * cl[0] + R[i * 3 + 1] * cl[1] + R[i * 3 + 2] * cl[2] + t[i];
+      b.rho = std::sqrt(h2) + am + tau_min * std::log(3.0);
+      return b;
+    }
+    default: break;
+  }
+  std::vector<OBound> ch;
+  for (int c = 0; c < n.n_children; ++c) ch.push_back(node_bound(sh, n.child[c], R, t, tau_min));
+  if (n.type == K_SUB) return ch[0];
+  if (n.type == K_INTER) {
+    for (const OBound& x : ch) if (x.rho < b.rho) b = x;
+    return b;
+  }
+  // union
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (const OBound& x : ch) {
+    if (!(x.rho < INFINITY)) return b;   // an unbounded operand
+    for (int i = 0; i < 3; ++i) { lo[i] = std::min(lo[i], x.c[i]); hi[i] = std::max(hi[i], x.c[i]); }
+  }
+  for (int i = 0; i < 3; ++i) b.c[i] = 0.5 * (lo[i] + hi[i]);
+  double r = 0.0;
+  for (const OBound& x : ch) {
+    const double d[3] = {x.c[0] - b.c[0], x.c[1] - b.c[1], x.c[2] - b.c[2]};
+    r = std::max(r, std::sqrt(dot3(d, d)) + x.rho);
+  }
+  b.rho = r + tau_min * std::log((double)ch.size());
+  return b;
+}
+
+static OBound shape_bound(const Shape& sh, double tau_min) {
+  OBound b;
+  b.rho = INFINITY;
+  b.c[0] = b.c[1] = b.c[2] = 0.0;
+  if (sh.nodes.empty()) return b;
+  const double I[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, z[3] = {0, 0, 0};
+  return node_bound(sh, 0, I, z, tau_min);
+}
+
+static OBound mesh_sphere(const Mesh& m) {
+  OBound b;
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int k = 0; k < m.V; ++k)
+    for (int i = 0; i < 3; ++i) { lo[i] = std::min(lo[i], m.v[3 * k + i]); hi[i] = std::max(hi[i], m.v[3 * k + i]); }
+  for (int i = 0; i < 3; ++i) b.c[i] = 0.5 * (lo[i] + hi[i]);
+  double r = 0.0;
+  for (int k = 0; k < m.V; ++k) {
+    const double d[3] = {m.v[3 * k] - b.c[0], m.v[3 * k + 1] - b.c[1], m.v[3 * k + 2] - b.c[2]};
+    r = std::max(r, std::sqrt(dot3(d, d)));
+  }
+  b.rho = r;
+  return b;
+}
+
+
 // ---- contact manifold -------------------------------------------
 // Reduced manifold: shape A (pairs[5i+3]) is the sampled mesh, shape B
 // (pairs[5i+4]) the SDF.  mode bit 4: full mode (one contact
@@ -739,6 +842,20 @@ int ora_sdf_eval(void* s, const int* shape_ids, const double* poses, const doubl
 //   ddepth[12], dnormal[36] ([i*12+j] = d n_i / d q_j), dom (int),
 //   J[36] (literal sum_i z_i gamma_i J_i, [r*12+c]), z[6], dcand[6], gam[6].
 // q = (dt_A, dtheta_A, dt_B, dtheta_B), world-frame left twists (Reading #28).
+// broad-phase bounds (f2): out4 = (c_x, c_y, c_z, rho); rho = inf without a bound
+void ora_shape_bound(void* s, int shape, double* out4) {
+  Scene* sc = (Scene*)s;
+  const OBound b = shape_bound(sc->shapes[shape], sc->sp.tau_min);
+  for (int i = 0; i < 3; ++i) out4[i] = b.c[i];
+  out4[3] = b.rho;
+}
+void ora_mesh_sphere(void* s, int shape, double* out4) {
+  Scene* sc = (Scene*)s;
+  const OBound b = mesh_sphere(sc->shapes[shape].mesh);
+  for (int i = 0; i < 3; ++i) out4[i] = b.c[i];
+  out4[3] = b.rho;
+}
+
 int ora_contact_manifold(void* s, const int* pairs, long n_pairs, const double* poses, long n_env, int n_slot,
                          double* point, double* normal, double* depth, double* W, double* qv, double* ddepth,
                          double* dnormal, int* dom, double* J, double* zout, double* dcand, double* gout,
@@ -746,11 +863,18 @@ int ora_contact_manifold(void* s, const int* pairs, long n_pairs, const double* 
   Scene* sc = (Scene*)s;
   const Smooth sp = sc->sp;
   (void)n_env;
-  const bool full = (mode & 4) != 0, two = (mode & 8) != 0;
+  const bool full = (mode & 4) != 0, two = (mode & 8) != 0, broad = (mode & 16) != 0;
   auto count = [&](int shape) { const Mesh& m = sc->shapes[shape].mesh; return full ? (long)m.V + m.E : (long)m.F; };
   std::vector<long> off(n_pairs + 1, 0);
   for (long i = 0; i < n_pairs; ++i)
     off[i + 1] = off[i] + count(pairs[5 * i + 3]) + (two ? count(pairs[5 * i + 4]) : 0);
+  // broad-phase bounds per shape (f2)
+  std::vector<OBound> sdfb(sc->shapes.size()), meshb(sc->shapes.size());
+  if (broad)
+    for (size_t k = 0; k < sc->shapes.size(); ++k) {
+      sdfb[k] = shape_bound(sc->shapes[k], sp.tau_min);
+      if (sc->shapes[k].mesh.V > 0) meshb[k] = mesh_sphere(sc->shapes[k].mesh);
+    }
 #ifdef _OPENMP
   if (n_threads > 0) omp_set_num_threads(n_threads);
 #endif
@@ -768,6 +892,51 @@ int ora_contact_manifold(void* s, const int* pairs, long n_pairs, const double* 
     double RA[9], RB[9], tA[3] = {pa[0], pa[1], pa[2]}, tB[3] = {pb[0], pb[1], pb[2]};
     double qa[4] = {pa[3], pa[4], pa[5], pa[6]}, qb[4] = {pb[3], pb[4], pb[5], pb[6]};
     quat_to_R(qa, RA); quat_to_R(qb, RB);
+    if (broad) {
+      const OBound& bA = meshb[pr[3 + side]];
+      const OBound& bB = sdfb[pr[4 - side]];
+      double cA[3], cB[3];
+      for (int i = 0; i < 3; ++i) {
+        cA[i] = RA[i * 3 + 0] * bA.c[0] + RA[i * 3 + 1] * bA.c[1] + RA[i * 3 + 2] * bA.c[2] + tA[i];
+        cB[i] = RB[i * 3 + 0] * bB.c[0] + RB[i * 3 + 1] * bB.c[1] + RB[i * 3 + 2] * bB.c[2] + tB[i];
+      }
+      const double dc[3] = {cA[0] - cB[0], cA[1] - cB[1], cA[2] - cB[2]};
+      const double lb = std::sqrt(dot3(dc, dc)) - bA.rho - bB.rho;
+      if (lb > 40.0 * sp.tau_cmp) {   // culled: no candidate can carry a gate above e^-40
+        const long nr = full ? (long)m.V + m.E : (long)m.F;
+        for (long k = 0; k < nr; ++k) {
+          const long c = row0 + k;
+          double loc[3] = {0, 0, 0};
+          if (!full) {
+            for (int a = 0; a < 3; ++a)
+              for (int i = 0; i < 3; ++i) loc[i] += m.v[3 * m.f[3 * k + a] + i] / 3.0;
+          } else if (k < m.V) {
+            for (int i = 0; i < 3; ++i) loc[i] = m.v[3 * k + i];
+          } else {
+            // edges in sorted (lo, hi) order after the vertices
+            std::vector<std::pair<int, int>> es(m.E);
+            for (int e = 0; e < m.E; ++e) es[e] = std::make_pair(m.e[2 * e], m.e[2 * e + 1]);
+            std::sort(es.begin(), es.end());
+            const auto& ee = es[k - m.V];
+            for (int i = 0; i < 3; ++i) loc[i] = 0.5 * (m.v[3 * ee.first + i] + m.v[3 * ee.second + i]);
+          }
+          for (int a = 0; a < 3; ++a) {
+            point[3 * c + a] = RA[a * 3 + 0] * loc[0] + RA[a * 3 + 1] * loc[1] + RA[a * 3 + 2] * loc[2] + tA[a];
+            normal[3 * c + a] = 0.0;
+            qv[3 * c + a] = 0.0;
+            for (int j = 0; j < 12; ++j) dnormal[36 * c + a * 12 + j] = 0.0;
+          }
+          depth[c] = full ? lb : lb - sp.tau_min * std::log(6.0);
+          W[c] = 0.0;
+          dom[c] = -2;
+          for (int j = 0; j < 12; ++j) ddepth[12 * c + j] = 0.0;
+          for (int j = 0; j < 36; ++j) J[36 * c + j] = 0.0;
+          for (int i = 0; i < 6; ++i) { zout[6 * c + i] = 0.0; dcand[6 * c + i] = lb; gout[6 * c + i] = 0.0; }
+        }
+        row0 += nr;
+        continue;
+      }
+    }
 
     // q-jet poses (first order, 12 seeds): q = (dt, dtheta) of the pair's
     // first body, then of its second body, whichever plays the sampled role

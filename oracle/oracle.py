@@ -58,6 +58,8 @@ def lib():
         L.ora_shape_param_count.restype = i
         L.ora_sdf_param_grad.argtypes = [p, p, p, p, l, l, i, p]
         L.ora_max_threads.restype = i
+        L.ora_shape_bound.argtypes = [p, i, p]
+        L.ora_mesh_sphere.argtypes = [p, i, p]
         _lib = L
     return _lib
 
@@ -207,7 +209,7 @@ class OracleScene:
         return out
 
     def contact_manifold(self, pairs=None, poses=None, n_threads=0, mode=0):
-        """mode bits: 4 full mode (V + E contacts), 8 two-sided."""
+        """mode bits: 4 full mode (V + E contacts), 8 two-sided, 16 broad phase (f2)."""
         sc = self.scene
         pairs = np.ascontiguousarray(sc.pairs if pairs is None else pairs, dtype=np.int32)
         poses = np.ascontiguousarray(sc.poses if poses is None else poses, dtype=np.float64)
@@ -227,6 +229,18 @@ class OracleScene:
                                    int(mode), int(n_threads))
         out["offsets"] = np.concatenate([[0], np.cumsum(F)]).astype(np.int64)
         return out
+
+    def shape_bound(self, shape):
+        """Broad phase (f2): (c, rho) with phi(x) >= |x - c| - rho in the body
+        frame (rho = inf: no bound, e.g. a half-space)."""
+        o = np.zeros(4)
+        lib().ora_shape_bound(self.h, int(shape), _ptr(o))
+        return o[:3], o[3]
+
+    def mesh_sphere(self, shape):
+        o = np.zeros(4)
+        lib().ora_mesh_sphere(self.h, int(shape), _ptr(o))
+        return o[:3], o[3]
 
     @staticmethod
     def pair_reduce(out, tau_min, w_depth=None, w_normal=None):
