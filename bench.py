@@ -162,10 +162,12 @@ def make_scene(workload, n_env, env_lo, K=18):
         return synth.c2_scene(n_env, seed=2 + 1000 * (env_lo // max(n_env, 1)))
     if workload == "SDF":
         return synth.sdf_scene(n_env, SDF_P, env_lo=env_lo)
+    if workload == "C6":
+        return synth.c6_scene(n_env, env_lo=env_lo)
     raise SystemExit("unknown workload " + workload)
 
 
-DEFAULT_NENV = {"C5": 1 << 20, "C4": 1 << 16, "C3": 1 << 14, "C2": 1000, "SDF": 1 << 18, "C1": 1}
+DEFAULT_NENV = {"C5": 1 << 20, "C4": 1 << 16, "C3": 1 << 14, "C2": 1000, "SDF": 1 << 18, "C1": 1, "C6": 4096}
 SDF_P = 64            # query points per body (SDF workload)
 SDF_METRIC = "sdf_eval point-evaluations/sec (value + gradient + Hessian + pose gradient)"
 SDF_BYTES_PER_POINT = 12 + 4 + 12 + 24 + 24   # point in; d, grad, hess (6), dpose (6) out
@@ -289,17 +291,18 @@ def run_reference(args):
     cores = O.max_threads()
     # each step: a bounded sample of the workload's pairs (same sample size
     # every step) sized so that W + K steps take a few minutes at most
+    mode = 16 if args.broad else 0
     n = min(len(scene.pairs), max(cores, 8))
     t0 = time.perf_counter()
-    osc.contact_manifold(pairs=scene.pairs[:n])
+    osc.contact_manifold(pairs=scene.pairs[:n], mode=mode)
     per = (time.perf_counter() - t0) / n
     m = int(max(n, min(len(scene.pairs), 150.0 / max(args.steps + args.warmup, 1) / max(per, 1e-9))))
     sample = scene.pairs[:m]
     for _ in range(args.warmup):
-        osc.contact_manifold(pairs=sample)
+        osc.contact_manifold(pairs=sample, mode=mode)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        osc.contact_manifold(pairs=sample)
+        osc.contact_manifold(pairs=sample, mode=mode)
     dt = (time.perf_counter() - t0) / args.steps
     val = m / dt
     line = {"impl": "reference", "metric": "contact-manifold evals/sec with derivatives (tier 2)", "value": val,
@@ -530,6 +533,7 @@ def e2e_full(S, scene, args, world, dev, n_sub=8):
     i+1's compute).  Returns (ms per step, h2d bytes, d2h bytes)."""
     import torch
     import torch.distributed as dist
+    from paper_2604_17538_b200 import binding
     n_env = scene.poses.shape[0]
     bounds = np.linspace(0, n_env, n_sub + 1).astype(np.int64)
     subs = []
@@ -574,7 +578,8 @@ def e2e_full(S, scene, args, world, dev, n_sub=8):
                 if j >= 2:
                     comp.wait_event(ev_out[s_])              # slot s_ outputs already read back
                 out = {k: view(dev_flat[s_], k, C) for k in proto}
-                S.contact_manifold(sb["pairs"], sb["offs"], C, dev_poses[s_][:n], args.tier, out)
+                S.contact_manifold(sb["pairs"], sb["offs"], C, dev_poses[s_][:n], args.tier, out,
+                                   binding.BROAD_PHASE if args.broad else 0)
                 ev_comp[s_].record(comp)
                 with torch.cuda.stream(down):
                     down.wait_event(ev_comp[s_])
@@ -642,7 +647,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C5", choices=["C5", "C4", "C3", "C2", "SDF", "C1"])
+    ap.add_argument("--workload", default="C5", choices=["C5", "C4", "C3", "C2", "SDF", "C1", "C6"])
+    ap.add_argument("--broad", action="store_true", help="CM_BROAD_PHASE (f2): certified pair culling")
     ap.add_argument("--k", type=int, default=18, help="C3: number of SQs in the smooth union (P:200 sweep)")
     ap.add_argument("--n-env", type=int, default=0)
     ap.add_argument("--tier", type=int, default=2)
@@ -684,9 +690,10 @@ def main():
     out = S.alloc_manifold(C, args.tier, dev)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)   # 256 MiB > 126 MB L2
     stream = torch.cuda.current_stream()
+    mode = binding.BROAD_PHASE if args.broad else 0
 
     def step():
-        S.contact_manifold(pairs, offs, C, poses, args.tier, out)
+        S.contact_manifold(pairs, offs, C, poses, args.tier, out, mode)
 
     ms_per_step, launches, clk = _timed(step, args, stream, flush, world, local)
     n_pairs_all = len(scene.pairs) * world
@@ -710,7 +717,7 @@ def main():
         poses_d = [torch.empty_like(poses) for _ in range(2)]
         # slot 1 shares every output but the read-back field with slot 0
         outs = [out, dict(out, depth=torch.empty_like(out["depth"]))]
-        ms_d = _e2e_pipelined(lambda s_: S.contact_manifold(pairs, offs, C, poses_d[s_], args.tier, outs[s_]),
+        ms_d = _e2e_pipelined(lambda s_: S.contact_manifold(pairs, offs, C, poses_d[s_], args.tier, outs[s_], mode),
                               [(poses_d[k], poses_h) for k in range(2)],
                               [(depth_h[k], outs[k]["depth"]) for k in range(2)], args.steps, world, dev)
         e2e_depth = {"value": n_pairs_all / (ms_d / 1e3), "unit": "pairs/s",
@@ -763,6 +770,9 @@ def main():
                 "gpu_launches": int(launches), "clocks": clk}
         if gather:
             line["allgather"] = gather
+        if args.broad:
+            line["config"]["broad_phase"] = "CM_BROAD_PHASE (certified pair culling, DESIGN.md reading #46)"
+            line["config"]["culled_fraction"] = float((out["dom"] == -2).float().mean().item())
         if args.workload == "C3" and args.k != 18:
             line["config"]["sqs_in_union"] = args.k
         if args.workload == "C1":   # latency-bound: report the per-call latency

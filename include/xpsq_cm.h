@@ -235,6 +235,18 @@ int cm_sdf_param_grad(const cm_scene* scene, const int32_t* shape_ids, const flo
  * pair's own order (t_A, theta_A, t_B, theta_B). */
 #define CM_FULL_MODE 4u
 #define CM_TWO_SIDED 8u
+/* CM_BROAD_PHASE ("utilizing [a broad phase] to filter
+ * edges prior to passing them to the edge-SDF routine"): a (pair, side) whose
+ * certified bound lb = |c_A - c_B| - r_A - rho_B on every candidate depth
+ * exceeds 40 tau_cmp (every gate below e^-40) skips the traces, evaluations
+ * and fusion.  (c_A, r_A): the sampled vertices' bounding sphere; phi_B >=
+ * |x - c_B| - rho_B from the SDF tree (shapes containing an unbounded
+ * half-space operand are never culled).  Its rows: point = the face centroid
+ * (full mode: the vertex / edge midpoint), depth = lb - tau_min ln 6 (full
+ * mode: lb), a certified lower bound of the fused depth; normal, W, q and
+ * every derivative 0; dom = -2.  Kept pairs are bit-identical to the call
+ * without the flag (reading #46). */
+#define CM_BROAD_PHASE 16u
 
 typedef struct cm_manifold_out {
   float* point;

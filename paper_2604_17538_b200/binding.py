@@ -20,7 +20,7 @@ CM_MAX_CHILDREN = 32
 NODE_TYPES = {"halfspace": 0, "sq": 1, "psq": 2, "xpsq": 3, "union": 10, "intersection": 11, "subtraction": 12}
 
 SDF_VALUE, SDF_GRAD, SDF_HESS, SDF_POSE_GRAD, SDF_POSE_HESS = 1, 2, 4, 8, 16
-FULL_MODE, TWO_SIDED = 4, 8   # manifold mode bits (include/xpsq_cm.h)
+FULL_MODE, TWO_SIDED, BROAD_PHASE = 4, 8, 16   # manifold mode bits (include/xpsq_cm.h)
 
 EXPORTS = ["cm_version", "cm_last_error", "cm_scene_create", "cm_scene_destroy", "cm_shape_counts",
            "cm_param_layout", "cm_sdf_param_grad",

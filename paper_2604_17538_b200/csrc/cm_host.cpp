@@ -183,6 +183,63 @@ Xpsq pack_xpsq(const cm_node& n) {
   return X;
 }
 
+// ---- broad-phase bounds (f2, reading #46) ------------------------
+// phi >= |x - c| - r over the whole space (r = +inf: unbounded below), in the
+// body frame, from the SDF tree with node frames composed on the way down
+struct HBound {
+  double c[3];
+  double r;
+};
+HBound tree_bound(const cm_shape_desc& d, int k, const Frame& parent, double tau_min) {
+  const cm_node& n = d.nodes[k];
+  const Frame fr = compose(parent, n.pose);
+  HBound b;
+  b.r = INFINITY;
+  for (int i = 0; i < 3; ++i) b.c[i] = fr.t[i];
+  if (n.type == CM_HALFSPACE) return b;
+  if (n.type == CM_SQ || n.type == CM_PSQ) {   // inside the box |y_i| <= a_i; PSQ >= SQ
+    b.r = std::sqrt((double)n.a[0][0] * n.a[0][0] + (double)n.a[0][1] * n.a[0][1] + (double)n.a[0][2] * n.a[0][2]);
+    return b;
+  }
+  if (n.type == CM_XPSQ) {   // the spline in its control points' box; three-root smooth min >= min - tau ln 3
+    double mid[3], half2 = 0.0, am = 0.0;
+    for (int i = 0; i < 3; ++i) {
+      const double lo = std::min({(double)n.ctrl[i], (double)n.ctrl[3 + i], (double)n.ctrl[6 + i]});
+      const double hi = std::max({(double)n.ctrl[i], (double)n.ctrl[3 + i], (double)n.ctrl[6 + i]});
+      mid[i] = 0.5 * (lo + hi);
+      half2 += 0.25 * (hi - lo) * (hi - lo);
+    }
+    for (int e = 0; e < 2; ++e)
+      am = std::max(am, std::sqrt((double)n.a[e][0] * n.a[e][0] + (double)n.a[e][1] * n.a[e][1] +
+                                  (double)n.a[e][2] * n.a[e][2]));
+    for (int i = 0; i < 3; ++i)
+      b.c[i] = fr.R[i * 3 + 0] * mid[0] + fr.R[i * 3 + 1] * mid[1] + fr.R[i * 3 + 2] * mid[2] + fr.t[i];
+    b.r = std::sqrt(half2) + am + tau_min * std::log(3.0);
+    return b;
+  }
+  std::vector<HBound> kids;
+  for (int c = 0; c < n.n_children; ++c) kids.push_back(tree_bound(d, n.children[c], fr, tau_min));
+  if (n.type == CM_SUBTRACTION) return kids[0];             // LSE(phi1, -phi2) >= phi1
+  if (n.type == CM_INTERSECTION) {                          // LSE(phi_i) >= each phi_i
+    for (const HBound& x : kids) if (x.r < b.r) b = x;
+    return b;
+  }
+  // union: -LSE(-phi_i) >= min phi_i - tau ln n
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (const HBound& x : kids) {
+    if (!(x.r < INFINITY)) return b;
+    for (int i = 0; i < 3; ++i) { lo[i] = std::min(lo[i], x.c[i]); hi[i] = std::max(hi[i], x.c[i]); }
+  }
+  for (int i = 0; i < 3; ++i) b.c[i] = 0.5 * (lo[i] + hi[i]);
+  double r = 0.0;
+  for (const HBound& x : kids) {
+    const double dx = x.c[0] - b.c[0], dy = x.c[1] - b.c[1], dz = x.c[2] - b.c[2];
+    r = std::max(r, std::sqrt(dx * dx + dy * dy + dz * dz) + x.r);
+  }
+  b.r = r + tau_min * std::log((double)kids.size());
+  return b;
+}
+
 template <class T> T* dev_copy(const std::vector<T>& v, int& rc) {
   if (v.empty()) return nullptr;
   T* p = nullptr;
@@ -499,6 +556,33 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
     }
   }
   sc->shapes = recs;
+  // broad-phase bounds per shape (f2): float, rounded outward
+  std::vector<float4> bounds(2 * (size_t)n_shapes);
+  for (int s = 0; s < n_shapes; ++s) {
+    const cm_shape_desc& d = shapes[s];
+    float4 mb = make_float4(0.f, 0.f, 0.f, -1.f), sb = make_float4(0.f, 0.f, 0.f, INFINITY);
+    if (d.n_faces > 0) {
+      double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY}, c[3], r = 0.0;
+      for (int v = 0; v < d.n_vertices; ++v)
+        for (int i = 0; i < 3; ++i) { lo[i] = std::min(lo[i], (double)d.vertices[3 * v + i]); hi[i] = std::max(hi[i], (double)d.vertices[3 * v + i]); }
+      for (int i = 0; i < 3; ++i) c[i] = 0.5 * (lo[i] + hi[i]);
+      for (int v = 0; v < d.n_vertices; ++v) {
+        const double dx = d.vertices[3 * v] - c[0], dy = d.vertices[3 * v + 1] - c[1], dz = d.vertices[3 * v + 2] - c[2];
+        r = std::max(r, std::sqrt(dx * dx + dy * dy + dz * dz));
+      }
+      mb = make_float4((float)c[0], (float)c[1], (float)c[2], (float)(r * (1.0 + 1e-6) + 1e-7));
+    }
+    if (d.n_nodes > 0) {
+      Frame id;
+      for (int i = 0; i < 9; ++i) id.R[i] = (i % 4 == 0) ? 1.0 : 0.0;
+      id.t[0] = id.t[1] = id.t[2] = 0.0;
+      const HBound hb = tree_bound(d, 0, id, sp->tau_min);
+      if (hb.r < INFINITY)
+        sb = make_float4((float)hb.c[0], (float)hb.c[1], (float)hb.c[2], (float)(hb.r * (1.0 + 1e-6) + 1e-7));
+    }
+    bounds[2 * s] = mb;
+    bounds[2 * s + 1] = sb;
+  }
 
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) { delete sc; return fail(CM_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)); }
@@ -518,11 +602,12 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
   D.verts = dev_copy(verts, rc);
   D.edges = dev_copy(edges_all, rc);
   D.edge_geom = dev_copy(edge_geom, rc);
+  D.bounds = dev_copy(bounds, rc);
   D.faces = dev_copy(faces_all, rc);
   D.face_edges = dev_copy(fe_all, rc);
   for (const void* p : {(const void*)D.prog, (const void*)D.leaves, (const void*)D.xpsq, (const void*)D.shapes,
                         (const void*)D.verts, (const void*)D.edges, (const void*)D.faces, (const void*)D.face_edges,
-                        (const void*)D.edge_geom})
+                        (const void*)D.edge_geom, (const void*)D.bounds})
     if (p) sc->allocs.push_back(const_cast<void*>(p));
   sc->param_off.assign(n_shapes + 1, 0);
   for (int s = 0; s < n_shapes; ++s) sc->param_off[s + 1] = sc->param_off[s] + std::max(sc->param_count[s], 0);
@@ -673,7 +758,7 @@ int cm_sdf_param_grad(const cm_scene* sc, const int32_t* ids, const float* poses
 int cm_manifold_size(const cm_scene* sc, const int32_t* pairs, int64_t n_pairs, uint32_t flags, int64_t* n) {
   if (!sc || (!pairs && n_pairs > 0) || !n) return fail(CM_ERR_INVALID, "cm_manifold_size");
   const bool full = flags & CM_FULL_MODE, two = flags & CM_TWO_SIDED;
-  const int ns = (int)sc->shapes.size();
+  const int ns = (int)sc->shapes.size();   // (CM_BROAD_PHASE does not change the row count)
   int64_t c = 0;
   for (int64_t i = 0; i < n_pairs; ++i) {
     const int a = pairs[5 * i + 3], b = pairs[5 * i + 4];

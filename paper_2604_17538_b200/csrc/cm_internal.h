@@ -1,6 +1,7 @@
 // Internal layouts shared by the host library (cm_host.cpp) and the sm_100a
 // kernels (cm_kernels_*.cu).  Not part of the ABI.
 #pragma once
+#include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "xpsq_cm.h"
@@ -99,6 +100,7 @@ struct SceneDev {
   unsigned int* err;          // device counter of invalid pair records / shape ids (cm_scene_error_count)
   const int8_t* shape_cls;    // per shape: its SDF class (ShapeRec::uses_xpsq), -1 without an SDF
   int32_t n_leaves, n_xpsq;   // sizes of leaves[] and xpsq[] (shared-memory staging)
+  const float4* bounds;       // broad phase (f2): [2 s] sampled-vertex sphere (c, r), [2 s + 1] SDF bound (c, rho)
 };
 
 // manifold chunk scratch: the units of one chunk keep their candidate state

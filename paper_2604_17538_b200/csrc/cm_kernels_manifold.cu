@@ -336,13 +336,15 @@ struct alignas(16) UnitCtx {
   int valid;                 // the unit has a manifold (SDF side and a surface)
   int cls;                   // SDF class of the unit's SDF shape
   int bad;                   // invalid record with output rows (filled with NaN)
-  int pad[2];
+  int culled;                // broad phase (f2): certified inactive, rows written by k_mf_culled
+  float lb;                  // its certified lower bound on every candidate depth
 };
 static_assert(sizeof(UnitCtx) % 16 == 0, "UnitCtx is copied as float4");
 
 // threads per unit CTA: 64 for large batches (lane use on V = 56..98 meshes);
 // small batches get up to CM_MF_MAX_THREADS so the SMs still fill
 #define CM_N_CLASSES 5   // SDF classes (cm_internal.h ShapeRec::uses_xpsq)
+#define CM_N_LISTS 6     // + the broad phase's culled units (list CM_N_CLASSES)
 #ifndef CM_MF_STAGE_MID
 #define CM_MF_STAGE_MID 0   // TMA-staged trace records in the midpoint kernel: C5 -7%, C4 -0.5% (r02i sweep)
 #endif
@@ -418,6 +420,8 @@ __device__ __forceinline__ void unit_resolve(const MfArgs& a, int64_t un, UnitCt
   U.valid = 0;
   U.cls = -1;
   U.bad = 0;
+  U.culled = 0;
+  U.lb = 0.f;
   // record validation: out-of-range shape ids (the offsets kernel gave the
   // pair no rows), env or slot indices (its rows are filled with NaN by
   // k_mf_units), or a shape without the needed surface / SDF: counted in
@@ -455,6 +459,25 @@ __device__ __forceinline__ void unit_resolve(const MfArgs& a, int64_t un, UnitCt
     U.SB = sb;
     U.valid = 1;
     U.cls = sb.uses_xpsq;
+    if (a.mode & CM_BROAD_PHASE) {
+      // certified culling (reading #46): every candidate lies in
+      // A's vertex sphere and phi_B >= |x - c_B| - rho_B
+      const float4 ma = __ldg(a.S.bounds + 2 * shA), mb = __ldg(a.S.bounds + 2 * shB + 1);
+      if (mb.w < INFINITY && ma.w >= 0.f) {
+        const float ca[3] = {ma.x, ma.y, ma.z}, cb[3] = {mb.x, mb.y, mb.z};
+        float wa[3], wb[3];
+        rot_vec(U.F.RA, ca, wa);
+        rot_vec(U.F.RB, cb, wb);
+        const float dx = wa[0] + U.F.tA[0] - wb[0] - U.F.tB[0], dy = wa[1] + U.F.tA[1] - wb[1] - U.F.tB[1],
+                    dz = wa[2] + U.F.tA[2] - wb[2] - U.F.tB[2];
+        const float lb = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))) - ma.w - mb.w;
+        if (lb > 40.f * a.S.sp.tau_cmp) {
+          U.valid = 0;
+          U.culled = 1;
+          U.lb = lb;
+        }
+      }
+    }
   }
 }
 
@@ -468,6 +491,7 @@ __global__ void __launch_bounds__(128) k_mf_units(const MfArgs a, int64_t nb) {
   U.valid = 0;
   U.cls = -1;
   U.bad = 0;
+  U.culled = 0;
   if (in) unit_resolve(a, a.unit0 + u, U);
   if (in && U.bad) {   // an invalid record's rows: NaN in every float field, dom -1
     const bool fm = (a.mode & CM_FULL_MODE) != 0;
@@ -490,26 +514,28 @@ __global__ void __launch_bounds__(128) k_mf_units(const MfArgs a, int64_t nb) {
   // class lists in unit order within the block (ballot ranks + one atomic per
   // block and class), so neighbouring CTAs of a phase kernel take
   // neighbouring units
-  __shared__ int s_cnt[CM_N_CLASSES][4], s_base[CM_N_CLASSES];
+  __shared__ int s_cnt[CM_N_LISTS][4], s_base[CM_N_LISTS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
   int rank = 0;
+  // list of the unit: its SDF class, or the culled list
+  const int mylist = !in ? -1 : (U.valid ? U.cls : (U.culled ? CM_N_CLASSES : -1));
 #pragma unroll
-  for (int c = 0; c < CM_N_CLASSES; ++c) {
-    const unsigned m = __ballot_sync(0xffffffffu, in && U.valid && U.cls == c);
+  for (int c = 0; c < CM_N_LISTS; ++c) {
+    const unsigned m = __ballot_sync(0xffffffffu, mylist == c);
     if (lane == 0) s_cnt[c][warp] = __popc(m);
-    if (in && U.valid && U.cls == c) rank = __popc(m & lt);
+    if (mylist == c) rank = __popc(m & lt);
   }
   __syncthreads();
-  if (threadIdx.x < CM_N_CLASSES) {
+  if (threadIdx.x < CM_N_LISTS) {
     const int c = threadIdx.x;
     const int tot = s_cnt[c][0] + s_cnt[c][1] + s_cnt[c][2] + s_cnt[c][3];
     s_base[c] = tot ? atomicAdd(a.cls_count + c, tot) : 0;
   }
   __syncthreads();
   if (!in) return;
-  if (U.valid) {
-    const int c = U.cls;
+  if (mylist >= 0) {
+    const int c = mylist;
     int pre = 0;
     for (int w = 0; w < warp; ++w) pre += s_cnt[c][w];
     a.cls_list[(int64_t)c * a.chunk + s_base[c] + pre + rank] = (int)u;
@@ -1348,6 +1374,65 @@ __global__ void __maxnreg__((MidFacesRegs<TIER, XP>::R)) k_mf_midfaces(const MfA
   mf_faces_unit<TIER, false>(a, U, u, nullptr, nullptr, 0u, sv_s, se_s);
 }
 
+// broad phase (f2): rows of the culled units (list CM_N_CLASSES), one CTA per
+// unit, threads over its rows (coalesced field-major stores)
+template <int TIER>
+__global__ void __launch_bounds__(CM_MF_MAX_THREADS) k_mf_culled(const MfArgs a) {
+  __shared__ UnitCtx U;
+  int u;
+  if (!list_unit(a, CM_N_CLASSES, U, u)) return;
+  const bool full = (a.mode & CM_FULL_MODE) != 0;
+  const PairFrame& F = U.F;
+  const int V = U.SA.V, E = U.SA.E;
+  const int nr = full ? V + E : U.SA.F;
+  const float* lv = a.S.verts + 4 * (int64_t)U.SA.v_off;
+  const int32_t* fv = a.S.faces + 3 * (int64_t)U.SA.f_off;
+  const int32_t* ed = a.S.edges + 2 * (int64_t)U.SA.e_off;
+  const cm_manifold_out& o = a.out;
+  const int64_t C = a.C;
+  const float depth = full ? U.lb : fmaf(-a.S.sp.tau_min, 1.791759469228055f, U.lb);   // lb - tau ln 6
+  for (int r = threadIdx.x; r < nr; r += blockDim.x) {
+    float x[3];
+    if (!full) {   // the face centroid
+      const float4 p0 = ldv(lv, __ldg(fv + 3 * r)), p1 = ldv(lv, __ldg(fv + 3 * r + 1)), p2 = ldv(lv, __ldg(fv + 3 * r + 2));
+      x[0] = (p0.x + p1.x + p2.x) * (1.f / 3.f);
+      x[1] = (p0.y + p1.y + p2.y) * (1.f / 3.f);
+      x[2] = (p0.z + p1.z + p2.z) * (1.f / 3.f);
+    } else if (r < V) {
+      const float4 p0 = ldv(lv, r);
+      x[0] = p0.x; x[1] = p0.y; x[2] = p0.z;
+    } else {        // edge midpoint (edges in sorted (lo, hi) order)
+      const float4 p0 = ldv(lv, __ldg(ed + 2 * (r - V))), p1 = ldv(lv, __ldg(ed + 2 * (r - V) + 1));
+      x[0] = 0.5f * (p0.x + p1.x); x[1] = 0.5f * (p0.y + p1.y); x[2] = 0.5f * (p0.z + p1.z);
+    }
+    float xb[3], pw[3];
+    to_frames(F, x, xb, pw);
+    const int64_t c = U.off + r;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      o.point[k * C + c] = pw[k];
+      o.normal[k * C + c] = 0.f;
+    }
+    o.depth[c] = depth;
+    o.dom[c] = (int8_t)-2;
+    if constexpr (TIER >= 1) {
+      o.W[c] = 0.f;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) o.q[k * C + c] = 0.f;
+    }
+    if constexpr (TIER >= 2) {
+#pragma unroll
+      for (int k = 0; k < 12; ++k) o.ddepth[k * C + c] = 0.f;
+#pragma unroll
+      for (int k = 0; k < 36; ++k) o.dnormal[k * C + c] = 0.f;
+    }
+    if constexpr (TIER >= 3) {
+#pragma unroll 6
+      for (int k = 0; k < 78; ++k) o.d2depth[k * C + c] = 0.f;
+    }
+  }
+}
+
 template <int TIER, bool STAGED>
 __global__ void __launch_bounds__(CM_MF_MAX_THREADS, TIER >= 3 ? 1 : CM_MF_FACE_MINB) k_mf_faces(const MfArgs a) {
   extern __shared__ __align__(16) float fsm[];
@@ -1436,7 +1521,7 @@ static int launch_tier(MfArgs a, int class_mask, int max_V, int max_E, int64_t n
     a.scratch = scratch0 + (k % n_streams) * chunk * a.slot;
     a.ctx = ctx0 + (k % n_streams) * chunk;
     a.cls_count = ctrl0 + 32 * (k % n_streams);
-    a.cls_list = lists0 + (k % n_streams) * chunk * CM_N_CLASSES;
+    a.cls_list = lists0 + (k % n_streams) * chunk * CM_N_LISTS;
     a.chunk = chunk;
     a.nb = nb;
     if (cudaMemsetAsync(a.cls_count, 0, 32 * sizeof(int), st) != cudaSuccess) {
@@ -1458,6 +1543,10 @@ static int launch_tier(MfArgs a, int class_mask, int max_V, int max_E, int64_t n
     if (!rc && (class_mask & 8)) rc = launch_sdf_phases<TIER, 3>(a, nb, T, max_V, max_E, st);
     if (!rc && (class_mask & 16)) rc = launch_sdf_phases<TIER, 4>(a, nb, T, max_V, max_E, st);
     if (rc) return rc;
+    if (a.mode & CM_BROAD_PHASE) {   // the culled units' rows (f2)
+      k_mf_culled<TIER><<<(unsigned)nb, T, 0, st>>>(a);
+      if ((rc = check_launch("k_mf_culled"))) return rc;
+    }
     if (!full && midfaces_bytes(TIER, a.mode, max_V, max_E) == 0) {   // the fusion does not depend on the SDF class: one launch
       if (stage_bytes > 0 && (stage_bytes <= kStageSmallBytes || nb < 8 * (int64_t)num_sms()))
         k_mf_faces<TIER, true><<<(unsigned)nb, T, stage_bytes, st>>>(a);
@@ -1475,13 +1564,13 @@ int launch_manifold(const SceneDev& s, int class_mask, int max_V, int max_E, con
                     const cm_manifold_out* out, int64_t C, float* scratch, int64_t scratch_floats,
                     void* const* streams, int n_streams) {
   const int tier = (int)(flags & CM_TIER_MASK);
-  const uint32_t mode = flags & (CM_FULL_MODE | CM_TWO_SIDED);
+  const uint32_t mode = flags & (CM_FULL_MODE | CM_TWO_SIDED | CM_BROAD_PHASE);
   const int64_t n_units = (mode & CM_TWO_SIDED) ? 2 * n_pairs : n_pairs;
   const int64_t slot = manifold_slot_floats(max_V, max_E, tier);
   if (n_streams < 1) n_streams = 1;
   // each unit of a chunk: its candidate slot and its set-up record (after
   // all slots; slots are multiples of 4 floats so the records stay aligned)
-  const int64_t ctxf = (int64_t)(sizeof(UnitCtx) / 4) + CM_N_CLASSES;   // + the class-list entries
+  const int64_t ctxf = (int64_t)(sizeof(UnitCtx) / 4) + CM_N_LISTS;   // + the class-list entries
   int64_t chunk = slot > 0 ? (scratch_floats - 32 * n_streams) / n_streams / (slot + ctxf) : 0;
   if (scratch == nullptr || chunk < 1) {
     set_error("manifold: scene scratch missing or too small");
@@ -1505,7 +1594,7 @@ int launch_manifold(const SceneDev& s, int class_mask, int max_V, int max_E, con
   // scratch layout: [slots | unit records | class lists | counters], per stream
   a.ctx = reinterpret_cast<UnitCtx*>(scratch + (int64_t)n_streams * chunk * slot);
   a.cls_list = reinterpret_cast<int*>(a.ctx + (int64_t)n_streams * chunk);
-  a.cls_count = a.cls_list + (int64_t)n_streams * chunk * CM_N_CLASSES;
+  a.cls_count = a.cls_list + (int64_t)n_streams * chunk * CM_N_LISTS;
   a.chunk = chunk;
   a.nb = 0;
   cudaStream_t const* sts = (cudaStream_t const*)streams;

@@ -656,6 +656,62 @@ def c5_scene(n_env: int = 1 << 20, env_lo: int = 0, seed: int = 5) -> Scene:
                  meta=dict(env_lo=env_lo, n_sampled=n_s, n_sdf=len(sdf)))
 
 
+def c6_parts(seed: int, K: int = 18):
+    """The K SQ parts of blob18(seed) as separate shapes: each with its SDF
+    (the SQ with its part pose as node pose) and its sampled surface (the
+    cube-sphere SQ mesh, k = 3, moved by the part pose): the SQ-pair
+    decomposition of the paper's efficiency experiment."""
+    rng = np.random.Generator(np.random.Philox(key=seed + 1000))
+    parts = []
+    for i in range(K):
+        a = rng.uniform(0.04, 0.12, 3)
+        eps = rng.uniform(0.3, 1.5, 2)
+        c = rng.uniform(-0.15, 0.15, 3)
+        q = random_quats(rng, 1)[0]
+        v, f = sq_mesh(_f32(a), _f32(eps), 3)
+        R = quat_to_mat(np.asarray(_f32(q), np.float64))
+        vw = (v.astype(np.float64) @ R.T + np.asarray(_f32(c), np.float64)).astype(F32)
+        parts.append(make_shape("part%d_%d" % (seed, i), sq(a, eps, pose=[*c, *q]), (vw, f)))
+    return parts
+
+
+def c6_scene(n_env: int = 1024, env_lo: int = 0, seed: int = 7, K: int = 18) -> Scene:
+    """C6 (broad-phase workload; the paper's efficiency
+    experiment P:188-201): two objects of K = 18 SQ parts each (blob18 seeds
+    3 and 11); every env pairs every part of A (sampled) with every part of B
+    (SDF): K^2 = 324 pairs.  B at the origin, A uniformly rotated at a
+    distance U[0.15, 0.45] along a random direction (the objects' parts
+    reach ~0.25 from their centres), so some part pairs touch and most are
+    far apart -- the case a broad phase filters.  ell = 0.1."""
+    A, B = c6_parts(3, K), c6_parts(11, K)
+    shapes = A + B
+    poses = np.zeros((n_env, 2, 8))
+    e = env_lo
+    blk_pairs = []
+    while e < env_lo + n_env:
+        blk = e // C5_BLOCK
+        lo, hi = blk * C5_BLOCK, (blk + 1) * C5_BLOCK
+        rng = np.random.Generator(np.random.Philox(key=[seed, blk]))
+        qa = random_quats(rng, C5_BLOCK)
+        qb = random_quats(rng, C5_BLOCK)
+        u = rng.standard_normal((C5_BLOCK, 3))
+        u /= np.linalg.norm(u, axis=1, keepdims=True)
+        dist = rng.uniform(0.15, 0.45, C5_BLOCK)
+        s_, t_ = max(e, lo), min(env_lo + n_env, hi)
+        sl = slice(s_ - lo, t_ - lo)
+        o = slice(s_ - env_lo, t_ - env_lo)
+        poses[o, 0, :3] = u[sl] * dist[sl, None]
+        poses[o, 0, 3:7] = qa[sl]
+        poses[o, 1, 3:7] = qb[sl]
+        e = t_
+    ia, ib = np.meshgrid(np.arange(K), np.arange(K), indexing="ij")
+    per_env = np.stack([np.zeros(K * K), np.zeros(K * K), np.ones(K * K), ia.ravel(), K + ib.ravel()], 1)
+    pairs = np.tile(per_env, (n_env, 1)).astype(np.int32)
+    pairs[:, 0] = np.repeat(np.arange(n_env), K * K)
+    return Scene("C6", shapes, smooth_params(0.1), np.ascontiguousarray(pairs), poses.astype(F32), ell=0.1,
+                 meta=dict(env_lo=env_lo, parts=K))
+
+
 def sdf_scene(n_body: int = 1 << 16, P: int = 64, env_lo: int = 0, seed: int = 6) -> Scene:
     """sdf_eval workload (SURVEY §8d secondary metric): the 32 C5 SDF
     prototypes, one body per batch item with a uniform rotation and a

@@ -631,3 +631,47 @@ def test_pair_reduce(cuda, oracle_mod, cfg):
     nf += PT.compare("g_pose", gp[idx], r_gp, p_gp, tg, rep)
     _report("pair_reduce_%s" % cfg, rep)
     assert nf == 0, json.dumps(rep, indent=1)
+
+
+def test_broad_phase_c6(cuda, oracle_mod):
+    """CM_BROAD_PHASE (f2) on C6 (two 18-part SQ objects, 324 part pairs per
+    env): the GPU's culled set equals the oracle's (outside a 1e-5 ell band
+    around the 40 tau_cmp threshold), culled rows match the oracle's culled
+    rows, kept pairs match the oracle's all-edges manifold (tolerances of
+    DESIGN.md §6) and are bit-identical to the GPU call without the flag."""
+    import torch
+    from paper_2604_17538_b200 import binding
+    sc = synth.c6_scene(32)
+    osc = oracle_mod.OracleScene(sc)
+    gb, S = PT.gpu_manifold(sc, 2, mode=binding.BROAD_PHASE)
+    g0, _ = PT.gpu_manifold(sc, 2, S=S)
+    C = gb["C"]
+    off = gb["offsets"]
+    F = np.array([S.counts(int(a))[2] for a in sc.pairs[:, 3]])
+    culled = np.array([gb["dom"][off[i]] == -2 for i in range(len(sc.pairs))])
+    assert 0.5 < culled.mean() < 0.99, culled.mean()
+    # kept pairs: bit-identical to the unflagged call
+    for i in np.nonzero(~culled)[0][:400]:
+        r = slice(off[i], off[i] + F[i])
+        for k in ("point", "normal", "depth", "W", "q", "ddepth", "dnormal", "dom"):
+            assert np.array_equal(gb[k][..., r], g0[k][..., r]), (i, k)
+    # oracle parity on a sample of pairs with both decisions compared
+    rng = np.random.default_rng(23)
+    idx = np.sort(rng.choice(len(sc.pairs), 256, replace=False))
+    ref = osc.contact_manifold(pairs=sc.pairs[idx], mode=16)
+    tau_cmp = sc.smooth["tau_cmp"]
+    n_band = 0
+    for k, i in enumerate(idx):
+        lb = ref["dcand"][ref["offsets"][k], 0]
+        ref_cull = ref["dom"][ref["offsets"][k]] == -2
+        if abs(lb - 40 * tau_cmp) < 1e-5 * sc.ell and ref_cull:
+            n_band += 1
+            continue
+        assert ref_cull == culled[i], (i, lb)
+    kept = idx[~culled[idx]]
+    nf, rep = PT.manifold_parity(sc, osc, gb, 2, kept, rng, sc.ell, mode=16)
+    cul = idx[culled[idx]]
+    nf2, rep2 = PT.manifold_parity(sc, osc, gb, 2, cul, rng, sc.ell, mode=16)
+    _report("broad_phase_c6", rep + rep2)
+    assert nf == 0 and nf2 == 0, json.dumps(rep + rep2, indent=1)
+    assert (gb["dom"][np.concatenate([np.arange(off[i], off[i] + F[i]) for i in cul])] == -2).all()

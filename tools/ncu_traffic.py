@@ -4,6 +4,7 @@ bytes of the whole chunk -> JSON (profiles/<round>_traffic_c5.json)."""
 import csv, json, subprocess, sys
 rep, out = sys.argv[1], sys.argv[2]
 workload = sys.argv[3] if len(sys.argv) > 3 else "C5"
+first_n = int(sys.argv[4]) if len(sys.argv) > 4 else 0   # only the first N kernels (one chunk)
 txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout.splitlines()
 rows = list(csv.reader(txt))
 h, units = rows[0], rows[1]
@@ -13,7 +14,7 @@ def col(r, k):
     return float(v) * scale
 ks = []
 grid = None
-for r in rows[2:]:
+for r in (rows[2:2 + first_n] if first_n else rows[2:]):
     g = int(r[h.index("Grid Size")].strip("()").split(",")[0])
     grid = g if grid is None else max(grid, g)
     ks.append({"kernel": r[h.index("Kernel Name")].split("(")[0], "ns": col(r, "gpu__time_duration.sum"),
