@@ -68,6 +68,8 @@ def load_alu_peaks():
 def _cost_key(workload, shape, kind):
     if workload == "C5":
         return shape.name
+    if workload not in ("C1", "C2", "C3", "C4"):
+        return None   # (no frozen cost entries: HBM roof only)
     if kind == "sdf":
         return {"C1": "C1:", "C2": "C2:", "C3": "C3:", "C4": "C4:"}[workload] + (
             {"blob18": "blob18"}.get(shape.name, shape.name))
@@ -90,7 +92,7 @@ def flop_per_launch(workload, scene, S):
     for (a, b), n in zip(keys, counts):
         sa, sb = scene.shapes[a], scene.shapes[b]
         ka, kb = _cost_key(workload, sa, "mesh"), _cost_key(workload, sb, "sdf")
-        if ka not in cm["manifold_with_halfspace"] or kb not in cm["sdf"]:
+        if ka is None or kb is None or ka not in cm["manifold_with_halfspace"] or kb not in cm["sdf"]:
             return None, None
         V, E, F = S.counts(int(a))
         c = cm["manifold_with_halfspace"][ka]["flop_per_pair_total_with_halfspace"]
@@ -545,6 +547,7 @@ def e2e_full(S, scene, args, world, dev, n_sub=8):
         pairs_d = torch.from_numpy(pr).to(dev)
         C = S.manifold_size(pr)
         subs.append(dict(e0=e0, e1=e1, pairs=pairs_d, offs=S.manifold_offsets(pairs_d), C=C))
+    subs = [x for x in subs if x["C"] > 0]   # (tiny workloads: empty sub-batches)
     Cmax = max(x["C"] for x in subs)
     nmax = max(x["e1"] - x["e0"] for x in subs)
     poses_h = torch.from_numpy(scene.poses).pin_memory()
