@@ -321,9 +321,65 @@ template <class T> T psq_phi(const T* y, const T& e1, const T& e2, const T* a,
 //   t-  = Cardano real root with Delta- substituted,
 //   t+k = trigonometric form with Delta+ substituted, k = 0, 1, 2;
 //   both soft-clipped to (0,1);  t*_k = sig(-Delta/tau) t- + sig(Delta/tau) t+_k
-template <class T> void xpsq_roots(const Node& n, const T* y, const Smooth& sp, T* tk, double* delta_out,
-                                   double* wneg_out) {
-  const double* p1 = n.ctrl;
+// The spline's static data as a type S: double (the node's own values) or a
+// jet type when the control points are seeded (shape parameters, f4): p1, A,
+// B, the Frenet binormal and the constant frame, by the rule of xpsq_static
+// (the class, frenet flag and snap decided on the values).
+template <class S> struct XS { S p1[3], A[3], B[3], bhat[3], R0[9]; };
+static XS<double> xs_plain(const Node& n) {
+  XS<double> x;
+  for (int i = 0; i < 3; ++i) { x.p1[i] = n.ctrl[i]; x.A[i] = n.A[i]; x.B[i] = n.B[i]; x.bhat[i] = n.bhat[i]; }
+  for (int i = 0; i < 9; ++i) x.R0[i] = n.R0[i];
+  return x;
+}
+template <class S> void normalize3t(S* v) {
+  S nn = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+  for (int i = 0; i < 3; ++i) v[i] = v[i] / nn;
+}
+template <class S> XS<S> xs_seeded(const Node& n, const S* ctrl) {
+  XS<S> x;
+  const S* p1 = ctrl; const S* p2 = ctrl + 3; const S* p3 = ctrl + 6;
+  for (int i = 0; i < 3; ++i) { x.p1[i] = p1[i]; x.A[i] = p1[i] - 2.0 * p2[i] + p3[i]; x.B[i] = 2.0 * (p2[i] - p1[i]); }
+  S T0[3];
+  if (n.xcls == 0) {
+    for (int i = 0; i < 3; ++i) T0[i] = S(0.0);
+  } else if (n.xcls == 1) {
+    for (int i = 0; i < 3; ++i) { x.B[i] = x.B[i] + x.A[i]; x.A[i] = S(0.0); T0[i] = x.B[i]; }
+  } else {
+    for (int i = 0; i < 3; ++i) T0[i] = x.A[i] + x.B[i];
+    double t0v[3] = {val(T0[0]), val(T0[1]), val(T0[2])};
+    if (std::sqrt(dot3(t0v, t0v)) < XPSQ_EPS_POINT) {
+      double nB = std::sqrt(dot3(n.B, n.B));
+      for (int i = 0; i < 3; ++i) T0[i] = nB > XPSQ_EPS_POINT ? x.B[i] : x.A[i];
+    }
+  }
+  if (n.frenet) {
+    cross3(x.B, x.A, x.bhat);
+    normalize3t(x.bhat);
+    for (int i = 0; i < 9; ++i) x.R0[i] = S(n.R0[i]);
+    return x;
+  }
+  S b[3] = {S(n.up[0]), S(n.up[1]), S(n.up[2])};
+  if (n.xcls == 0) {   // point spline: the frame from the up hint only
+    for (int i = 0; i < 3; ++i) x.bhat[i] = S(n.bhat[i]);
+    for (int i = 0; i < 9; ++i) x.R0[i] = S(n.R0[i]);
+    return x;
+  }
+  normalize3t(T0);
+  S c = b[0] * T0[0] + b[1] * T0[1] + b[2] * T0[2];
+  for (int i = 0; i < 3; ++i) b[i] = b[i] - c * T0[i];
+  normalize3t(b);
+  for (int i = 0; i < 3; ++i) x.bhat[i] = b[i];
+  S N[3]; cross3(x.bhat, T0, N);
+  for (int i = 0; i < 3; ++i) { x.R0[i * 3 + 0] = T0[i]; x.R0[i * 3 + 1] = N[i]; x.R0[i * 3 + 2] = x.bhat[i]; }
+  return x;
+}
+template <class T> T as_t(double v) { return T(v); }
+template <class T> T as_t(const T& v) { return v; }
+
+template <class T, class S> void xpsq_roots(const Node& n, const XS<S>& xs, const T* y, const Smooth& sp, T* tk,
+                                            double* delta_out, double* wneg_out) {
+  const S* p1 = xs.p1;
   T w[3] = {y[0] - p1[0], y[1] - p1[1], y[2] - p1[2]};
   if (delta_out) *delta_out = 0.0;
   if (wneg_out) *wneg_out = 0.0;
@@ -331,19 +387,19 @@ template <class T> void xpsq_roots(const Node& n, const T* y, const Smooth& sp, 
     for (int k = 0; k < 3; ++k) tk[k] = T(0.5);
     return;
   }
-  const double* A = n.A; const double* B = n.B;
+  const S* A = xs.A; const S* B = xs.B;
   T Bw = w[0] * B[0] + w[1] * B[1] + w[2] * B[2];
-  double BB = dot3(B, B);
+  S BB = dot3(B, B);
   if (n.xcls == 1) {  // straight spline: the cubic degenerates to B.w - t B.B = 0
     T t = softclip(Bw / BB, 0.0, 1.0, sp.tau_clip_t);
     for (int k = 0; k < 3; ++k) tk[k] = t;
     return;
   }
-  double c3 = -2.0 * dot3(A, A);
-  double c2 = -3.0 * dot3(A, B);
+  S c3 = -2.0 * dot3(A, A);
+  S c2 = -3.0 * dot3(A, B);
   T c1 = 2.0 * (w[0] * A[0] + w[1] * A[1] + w[2] * A[2]) - BB;
   T c0 = Bw;
-  double b = c2 / c3;
+  S b = c2 / c3;
   T c = c1 / c3, d = c0 / c3;
   T P = c - b * b / 3.0;
   T Q = 2.0 * b * b * b / 27.0 - b * c / 3.0 + d;
@@ -394,13 +450,13 @@ template <class T> void xpsq_roots(const Node& n, const T* y, const Smooth& sp, 
 
 // moving frame R(t) ("e.g. the Frenet frame"; Reading #7), row-major,
 // columns [T, bhat x T, bhat]
-template <class T> void xpsq_frame(const Node& n, const T& t, T* R) {
-  if (!n.frenet) { for (int i = 0; i < 9; ++i) R[i] = T(n.R0[i]); return; }
+template <class T, class S> void xpsq_frame(const Node& n, const XS<S>& xs, const T& t, T* R) {
+  if (!n.frenet) { for (int i = 0; i < 9; ++i) R[i] = as_t<T>(xs.R0[i]); return; }
   T pd[3];
-  for (int i = 0; i < 3; ++i) pd[i] = n.B[i] + 2.0 * n.A[i] * t;
+  for (int i = 0; i < 3; ++i) pd[i] = xs.B[i] + 2.0 * xs.A[i] * t;
   T nn = sqrt(pd[0] * pd[0] + pd[1] * pd[1] + pd[2] * pd[2]);
   T Tt[3] = {pd[0] / nn, pd[1] / nn, pd[2] / nn};
-  T bh[3] = {T(n.bhat[0]), T(n.bhat[1]), T(n.bhat[2])};
+  T bh[3] = {as_t<T>(xs.bhat[0]), as_t<T>(xs.bhat[1]), as_t<T>(xs.bhat[2])};
   T N[3]; cross3(bh, Tt, N);
   for (int i = 0; i < 3; ++i) { R[i * 3 + 0] = Tt[i]; R[i * 3 + 1] = N[i]; R[i * 3 + 2] = bh[i]; }
 }
@@ -408,7 +464,7 @@ template <class T> void xpsq_frame(const Node& n, const T& t, T* R) {
 template <class T> T lerp(double a, double b, const T& t) { return a + (b - a) * t; }
 
 template <class T> T pval(double v, int node, int slot);
-extern thread_local int g_seed_node;
+extern thread_local int g_seed_node, g_seed_slot;
 // an XPSQ's schedules differ between its endpoints (any of eps, a, planes)
 static bool xpsq_varying(const Node& n) {
   bool cst = n.eps[0][0] == n.eps[1][0] && n.eps[0][1] == n.eps[1][1];
@@ -416,17 +472,32 @@ static bool xpsq_varying(const Node& n) {
   for (int j = 0; j < n.n_planes; ++j) for (int i = 0; i < 4; ++i) cst = cst && n.pl[0][j][i] == n.pl[1][j][i];
   return !cst;
 }
+template <class T, class S>
+T xpsq_phi_s(const Node& n, const XS<S>& xs, const T* y, const Smooth& sp, int idx);
 template <class T> T xpsq_phi(const Node& n, const T* y, const Smooth& sp, int idx = -1) {
+  // control points seeded (f4 shape parameters: slots base .. base + 8 after
+  // the cross-section's, base = (varying ? 2 : 1) (5 + 4 n_planes)): the
+  // spline's static data as jets
+  const int base = (xpsq_varying(n) ? 2 : 1) * (5 + 4 * n.n_planes);
+  if (idx >= 0 && idx == g_seed_node && g_seed_slot >= base && g_seed_slot < base + 9) {
+    T c[9];
+    for (int i = 0; i < 9; ++i) c[i] = pval<T>(n.ctrl[i], idx, base + i);
+    return xpsq_phi_s(n, xs_seeded<T>(n, c), y, sp, idx);
+  }
+  return xpsq_phi_s(n, xs_plain(n), y, sp, idx);
+}
+template <class T, class S>
+T xpsq_phi_s(const Node& n, const XS<S>& xs, const T* y, const Smooth& sp, int idx) {
   T tk[3];
-  xpsq_roots(n, y, sp, tk, nullptr, nullptr);
+  xpsq_roots(n, xs, y, sp, tk, nullptr, nullptr);
   T phis[3];
   for (int k = 0; k < 3; ++k) {
     const T& t = tk[k];
     // PSQ pose at the root: translation p(t) (Eq. (5)), rotation R(t)
     T pt[3];
-    for (int i = 0; i < 3; ++i) pt[i] = n.ctrl[i] + n.B[i] * t + n.A[i] * (t * t);
+    for (int i = 0; i < 3; ++i) pt[i] = xs.p1[i] + xs.B[i] * t + xs.A[i] * (t * t);
     T R[9];
-    xpsq_frame(n, t, R);
+    xpsq_frame(n, xs, t, R);
     T dx[3] = {y[0] - pt[0], y[1] - pt[1], y[2] - pt[2]};
     T yk[3];
     for (int i = 0; i < 3; ++i) yk[i] = R[0 * 3 + i] * dx[0] + R[1 * 3 + i] * dx[1] + R[2 * 3 + i] * dx[2];
@@ -647,12 +718,14 @@ double ora_sq_phi(const double* y, double e1, double e2, const double* a) { retu
 // XPSQ projection internals for node `node` of shape `shape`: t*, Delta, w_neg
 void ora_xpsq_roots(void* s, int shape, int node, const double* y, double* t, double* delta, double* wneg) {
   Scene* sc = (Scene*)s;
-  xpsq_roots(sc->shapes[shape].nodes[node], y, sc->sp, t, delta, wneg);
+  const Node& nd = sc->shapes[shape].nodes[node];
+  xpsq_roots(nd, xs_plain(nd), y, sc->sp, t, delta, wneg);
 }
 // moving frame of an XPSQ node at parameter t (row-major 3x3)
 void ora_xpsq_frame(void* s, int shape, int node, double t, double* R) {
   Scene* sc = (Scene*)s;
-  xpsq_frame(sc->shapes[shape].nodes[node], t, R);
+  const Node& nd = sc->shapes[shape].nodes[node];
+  xpsq_frame(nd, xs_plain(nd), t, R);
 }
 int ora_xpsq_class(void* s, int shape, int node) {
   Scene* sc = (Scene*)s;
@@ -1138,7 +1211,7 @@ static int node_param_count(const Node& n) {
   if (n.type == K_HALFSPACE) return 4;
   if (n.type == K_SQ) return 5;
   if (n.type == K_PSQ) return 5 + 4 * n.n_planes;
-  if (n.type == K_XPSQ) return (xpsq_varying(n) ? 2 : 1) * (5 + 4 * n.n_planes);
+  if (n.type == K_XPSQ) return (xpsq_varying(n) ? 2 : 1) * (5 + 4 * n.n_planes) + 9;   // + control points p1, p2, p3
   return 0;
 }
 int ora_shape_param_count(void* s, int shape) {

@@ -1,5 +1,7 @@
 """Pins of the oracle's shape-parameter derivatives:
-d phi / d (a, eps, planes) of half-spaces, SQs, PSQs and flat booleans, from
+d phi / d (a, eps, planes) of half-spaces, SQs, PSQs and flat booleans, and
+d phi / d (p1, p2, p3) of XPSQ control points (through the projection roots,
+the Frenet frame and p(t)), from
 Dual<double,1> seeds on each parameter in turn.  Pinned by closed forms
 (sphere: d phi / d a_i = -y_i^2 / |y|^2 for phi = |y| - r; half-space:
 d phi / dn = y, d phi / dh = 1) and by central differences of the oracle's
@@ -48,6 +50,13 @@ def _perturbed(shape, node, slot, h):
     slot M + s the t = 1 value (M = 5 + 4 n_planes)."""
     s2 = copy.deepcopy(shape)
     nd = s2.sdf[node]
+    if nd["type"] == "xpsq":   # control points after the cross-section slots
+        base = (2 if _varying(nd) else 1) * (5 + 4 * len(nd["planes"]))
+        if slot >= base:
+            c = np.array(nd["ctrl"], dtype=np.float64)
+            c[slot - base] += h
+            nd["ctrl"] = c.tolist()
+            return s2
     ends = (0, 1)
     if _varying(nd):
         M = 5 + 4 * len(nd["planes"])
@@ -73,7 +82,7 @@ def _slots(shape):
     out = []
     for ni, nd in enumerate(shape.sdf):
         c = {"halfspace": 4, "sq": 5, "psq": 5 + 4 * len(nd["planes"]),
-             "xpsq": (2 if _varying(nd) else 1) * (5 + 4 * len(nd["planes"]))}.get(nd["type"], 0)
+             "xpsq": (2 if _varying(nd) else 1) * (5 + 4 * len(nd["planes"])) + 9}.get(nd["type"], 0)
         out += [(ni, s) for s in range(c)]
     return out
 
@@ -137,4 +146,4 @@ def test_param_count_varying_xpsq(oracle_mod):
     vary = synth.xpsq([-0.3, 0, 0, 0.0, 0.35, 0.05, 0.3, 0, 0.02], (0.12, 0.15, 0.1), (0.6, 0.8), a1=(0.1, 0.1, 0.1),
                       planes0=[[0.2, 0.3, 0.93, -0.05]])
     osc = O.OracleScene(scene_of([synth.make_shape("v", vary, None)]))
-    assert osc.param_count(0) == 2 * (5 + 4)
+    assert osc.param_count(0) == 2 * (5 + 4) + 9   # + the control points
