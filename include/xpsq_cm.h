@@ -176,8 +176,10 @@ int cm_sdf_eval(const cm_scene* scene, const int32_t* shape_ids, const float* po
  * XPSQ with constant schedules as PSQ (its cross-section; each parameter
  * moves both endpoint values, normals renormalised as in the XPSQ); XPSQ
  * with varying schedules: the PSQ slots of the t = 0 endpoint, then those of
- * the t = 1 endpoint (schedules linear in t, P:108 / reading #8; control
- * points are not parameters here); boolean nodes have none (a PSQ's raw plane
+ * the t = 1 endpoint (schedules linear in t, P:108 / reading #8); every XPSQ
+ * then the 9 control-point slots p1, p2, p3 (Eq. (5): through the
+ * projection roots, the frame and p(t); within the spline's static class --
+ * a straight spline's p2 has no effect, its chord is p1 -> p3); boolean nodes have none (a PSQ's raw plane
  * normal is the parameter: no renormalisation).  counts[s] (host,
  * [n_shapes]) = the count, 0 without an SDF, -1 when the shape has more
  * than 16 boolean nodes, or leaves whose node indices are not in

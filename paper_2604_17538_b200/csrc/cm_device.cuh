@@ -619,7 +619,8 @@ template <int O> __device__ __forceinline__ J3<O> lse_jets(const J3<O>* x, int n
 
 // soft Cardano (Eq. (6)) with implicit derivatives, defined below
 template <int O>
-__device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3, const SmoothDev& sp, J2<O>* t);
+__device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3, const SmoothDev& sp, J2<O>* t,
+                                                      float* tb3 = nullptr);
 
 // Roots t_k(w) of the projection with their gradient and Hessian
 // with respect to w = y - p1 (packed xx, xy, xz, yy, yz, zz).  Returns true
@@ -887,7 +888,8 @@ struct XsqParams {
 //   s_ab = -(6 s s_a s_b + Pt_b s_a + Pt_a s_b + Pt_ab s)/F_s.
 // The values use the cancellation-free forms of soft_cardano.
 template <int O>
-__device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3, const SmoothDev& sp, J2<O>* t) {
+__device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3, const SmoothDev& sp, J2<O>* t,
+                                                      float* tb3) {
   const float td = sp.tau_delta, itd = sp.i_delta;
   const float tc = sp.tau_clip_t, itc = sp.i_clip_t;
   const float P2 = P * P, P3 = P2 * P;
@@ -926,10 +928,12 @@ __device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3
     }
   };
   // soft clip of s - b/3 into (0, 1) with derivatives
+  float clip_d1 = 0.f;   // the last clip's derivative (d t / d b3 = -wn c1- - wp c1+, optional output)
   auto clip = [&](float s, const float* sa, const float* sab, float& v, float* va, float* vab) {
     const float x = s - b3;
     float c1, c2;
     softclip_12(x, 0.f, 1.f, tc, itc, v, c1, c2);
+    clip_d1 = c1;
     va[0] = c1 * sa[0];
     va[1] = c1 * sa[1];
     if constexpr (O >= 2) {
@@ -974,6 +978,7 @@ __device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3
       root_derivs(s, Pm, Pa, Pab, sa, sab);
     }
     clip(s, sa, sab, tm, tma, tmab);
+    if (tb3) tb3[0] = tb3[1] = tb3[2] = -wn * clip_d1;
   }
   if (use_p) {
     // trigonometric form: with X = -Q/2, Y = sqrt(D), D = s+(Delta)/108,
@@ -1039,6 +1044,7 @@ __device__ __forceinline__ bool soft_cardano_implicit(float P, float Q, float b3
       }
       float v, va[2], vab[3];
       clip(s, sa, sab, v, va, vab);
+      if (tb3) tb3[k] = (use_n ? tb3[k] : 0.f) - wp * clip_d1;
       tp[k] = v;
       tpa[k][0] = va[0]; tpa[k][1] = va[1];
       if constexpr (O >= 2) { tpab[k][0] = vab[0]; tpab[k][1] = vab[1]; tpab[k][2] = vab[2]; }

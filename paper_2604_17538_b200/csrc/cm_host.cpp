@@ -137,6 +137,7 @@ Xpsq pack_xpsq(const cm_node& n) {
   }
   for (int i = 0; i < 3; ++i) {
     X.p1[i] = (float)p1[i]; X.A[i] = (float)A[i]; X.B[i] = (float)B[i]; X.bhat[i] = (float)bh[i];
+    X.up[i] = n.up[i];
   }
   double BB = dot3(B, B);
   if (X.cls == 1)
@@ -480,7 +481,7 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
         if (ty == CM_HALFSPACE) pc += 4;
         else if (ty == CM_SQ) pc += 5;
         else if (ty == CM_PSQ) pc += 5 + 4 * d.nodes[k].n_planes;
-        else if (ty == CM_XPSQ) pc += (pack_xpsq(d.nodes[k]).varying ? 2 : 1) * (5 + 4 * d.nodes[k].n_planes);
+        else if (ty == CM_XPSQ) pc += (pack_xpsq(d.nodes[k]).varying ? 2 : 1) * (5 + 4 * d.nodes[k].n_planes) + 9;
         else ++n_bool;
       }
       if (n_bool > cmi::kParamMaxNodes) pc = -1;   // large trees

@@ -57,6 +57,7 @@ struct Xpsq {
   float Bn[3];            // straight class: t = softclip(Bn . w)
   float bhat[3];          // Frenet binormal (constant for a quadratic)
   float R0[9];            // constant frame (straight / point / A || B)
+  float up[3];            // the up hint (control-point derivatives of the constant frame, f4)
   int32_t cls;            // 0 point, 1 straight, 2 curve
   int32_t frenet;
   int32_t varying;        // schedules differ between the endpoints

@@ -262,6 +262,218 @@ __device__ __forceinline__ float sq_param_grad(const Leaf& L, const float* y, fl
 // Plane normals are renormalised in the XPSQ: n = v / |v| gives
 // d/dv = (I - n n^T) y_k w_j / |v| (|v| = 1 for the constant schedule's
 // unit normal)
+// ---- XPSQ control points (f4): d t_k / d(A, B, w) of the
+// projection roots.  Outside the soft-Cardano band the roots are exact roots
+// of g(t) = (w - B t - A t^2).(B + 2 A t) (reading #43):
+//   dt_raw = -(g_A dA + g_B dB + g_w dw) / g_t,  g_A = 2t (w - p) - t^2 p',
+//   g_B = (w - p) - t p',  g_w = p',  g_t = 2 A.(w - p) - |p'|^2,
+// then the soft clip's derivative; inside the band the literal blend through
+// (P, Q, b): P = c1/c3 - b^2/3, Q = 2b^3/27 - b c1/(3 c3) + c0/c3, b = c2/c3
+// with c3 = -2 A.A, c2 = -3 A.B, c1 = 2 A.w - B.B, c0 = B.w.  Straight
+// splines: t = softclip(B.w / B.B) with B the chord; points: t = 1/2.
+__device__ __forceinline__ void xpsq_root_dtheta(const Xpsq& X, const SmoothDev& sp, const float* w,
+                                                 float (*dtA)[3], float (*dtB)[3], float (*dtw)[3]) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int m = 0; m < 3; ++m) dtA[k][m] = dtB[k][m] = dtw[k][m] = 0.f;
+  if (X.cls == 0) return;
+  if (X.cls == 1) {
+    const float BB = X.B[0] * X.B[0] + X.B[1] * X.B[1] + X.B[2] * X.B[2];
+    const float iBB = 1.f / BB;
+    const float sv = (X.B[0] * w[0] + X.B[1] * w[1] + X.B[2] * w[2]) * iBB;
+    float v, d1, d2;
+    softclip_12(sv, 0.f, 1.f, sp.tau_clip_t, sp.i_clip_t, v, d1, d2);
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        dtw[k][m] = d1 * X.B[m] * iBB;
+        dtB[k][m] = d1 * (w[m] - 2.f * sv * X.B[m]) * iBB;
+      }
+    return;
+  }
+  const float Pv = X.gP[0] * w[0] + X.gP[1] * w[1] + X.gP[2] * w[2] + X.P0;
+  const float Qv = X.gQ[0] * w[0] + X.gQ[1] * w[1] + X.gQ[2] * w[2] + X.Q0;
+  const float Delta = -(4.f * Pv * Pv * Pv + 27.f * Qv * Qv);
+  const int newton = fabsf(X.b3) > 4.f ? 2 : 1;
+  const float c1 = fmaf(2.f * X.A[0], w[0], fmaf(2.f * X.A[1], w[1], fmaf(2.f * X.A[2], w[2], -X.BB)));
+  const float c0 = fmaf(X.B[0], w[0], fmaf(X.B[1], w[1], X.B[2] * w[2]));
+  // the exact-root regimes: implicit derivative of g at the polished root
+  auto implicit = [&](float t, int k) {
+    float g = fmaf(fmaf(fmaf(X.c3, t, X.c2), t, c1), t, c0);
+    float r = rcpa(fmaf(fmaf(3.f * X.c3, t, 2.f * X.c2), t, c1));
+    t = fmaf(-g, r, t);
+    if (newton > 1) {
+      g = fmaf(fmaf(fmaf(X.c3, t, X.c2), t, c1), t, c0);
+      r = rcpa(fmaf(fmaf(3.f * X.c3, t, 2.f * X.c2), t, c1));
+      t = fmaf(-g, r, t);
+    }
+    float v, d1, d2;
+    softclip_12(t, 0.f, 1.f, sp.tau_clip_t, sp.i_clip_t, v, d1, d2);
+    float pd[3], dm[3];
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      pd[m] = fmaf(2.f * X.A[m], t, X.B[m]);
+      dm[m] = w[m] - fmaf(fmaf(X.A[m], t, X.B[m]), t, 0.f);
+    }
+    const float gt = 2.f * (X.A[0] * dm[0] + X.A[1] * dm[1] + X.A[2] * dm[2]) -
+                     (pd[0] * pd[0] + pd[1] * pd[1] + pd[2] * pd[2]);
+    const float c = -d1 / gt;
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      dtA[k][m] = c * fmaf(2.f * t, dm[m], -t * t * pd[m]);
+      dtB[k][m] = c * fmaf(-t, pd[m], dm[m]);
+      dtw[k][m] = c * pd[m];
+    }
+  };
+  if (Delta * sp.i_delta < -46.f) {   // one real root
+    const float sD = sqrtf(-Delta * (1.f / 108.f));
+    const float u = cbrt_fast(Qv >= 0.f ? -0.5f * Qv - sD : -0.5f * Qv + sD);
+    const float sr = fabsf(u) > 1e-30f ? u - Pv * rcpa(3.f * u) : u;
+    implicit(sr - X.b3, 0);
+    return;
+  }
+  if (Delta * sp.i_delta > 46.f) {    // three real roots
+    const float rho = sqrtf(fmaxf(-Pv * (1.f / 3.f), 0.f));
+    const float th3 = atan2_pos(sqrtf(Delta * (1.f / 108.f)), -0.5f * Qv) * (1.f / 3.f);
+    float sn3, cs3;
+    __sincosf(th3, &sn3, &cs3);
+    const float ck[3] = {cs3, fmaf(-0.8660254037844386f, sn3, -0.5f * cs3),
+                         fmaf(0.8660254037844386f, sn3, -0.5f * cs3)};
+#pragma unroll 1
+    for (int k = 0; k < 3; ++k) implicit(2.f * rho * ck[k] - X.b3, k);
+    return;
+  }
+  // the band: the literal blend through (P, Q, b)
+  J2<1> t2[3];
+  float tb3[3] = {0.f, 0.f, 0.f};
+  soft_cardano_implicit<1>(Pv, Qv, X.b3, sp, t2, tb3);
+  const float b = 3.f * X.b3, ic3 = 1.f / X.c3;
+  const float cc = c1 * ic3, dd = c0 * ic3;
+#pragma unroll
+  for (int m = 0; m < 3; ++m)
+#pragma unroll
+    for (int which = 0; which < 3; ++which) {   // A_m, B_m, w_m
+      const float dc3 = which == 0 ? -4.f * X.A[m] : 0.f;
+      const float dc2 = which == 0 ? -3.f * X.B[m] : (which == 1 ? -3.f * X.A[m] : 0.f);
+      const float dc1 = which == 0 ? 2.f * w[m] : (which == 1 ? -2.f * X.B[m] : 2.f * X.A[m]);
+      const float dc0 = which == 0 ? 0.f : (which == 1 ? w[m] : X.B[m]);
+      const float db = (dc2 - b * dc3) * ic3;
+      const float dcc = (dc1 - cc * dc3) * ic3;
+      const float ddd = (dc0 - dd * dc3) * ic3;
+      const float dP = fmaf(-(2.f / 3.f) * b, db, dcc);
+      const float dQ = fmaf((2.f / 9.f) * b * b - cc * (1.f / 3.f), db, fmaf(-b * (1.f / 3.f), dcc, ddd));
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float v = fmaf(t2[k].g[0], dP, fmaf(t2[k].g[1], dQ, tb3[k] * db * (1.f / 3.f)));
+        if (which == 0) dtA[k][m] = v;
+        else if (which == 1) dtB[k][m] = v;
+        else dtw[k][m] = v;
+      }
+    }
+}
+
+// d y / d(A, B, w) of the cross-section coordinates y = R(t)^T d at a fixed
+// t (d = w - B t - A t^2; the frame R = [T, b x T, b]: the Frenet frame of
+// p' = B + 2 A t with b = B x A / |B x A|, or the constant frame from T0 =
+// (A + B) / |A + B| (B / |B| for straight splines) and the up hint by
+// Gram-Schmidt), and y_t = d y / d t; out [3 (A, B, w)][3 m][3 y]
+__device__ __forceinline__ void xpsq_dy_dtheta(const Xpsq& X, float t, const float* d, const float* T, const float* N,
+                                               const float* bb, float (*out)[3][3], float* yt) {
+  float pd[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) pd[i] = fmaf(2.f * X.A[i], t, X.B[i]);
+  // frame derivatives dT[which][m][i], db[which][m][i] (N = b x T)
+  float dT[3][3][3] = {}, dbv[3][3][3] = {};
+  if (X.cls == 2 && X.frenet) {
+    const float ip = rsqrtf(pd[0] * pd[0] + pd[1] * pd[1] + pd[2] * pd[2]);
+    const float bxa[3] = {X.B[1] * X.A[2] - X.B[2] * X.A[1], X.B[2] * X.A[0] - X.B[0] * X.A[2],
+                          X.B[0] * X.A[1] - X.B[1] * X.A[0]};
+    const float ib = rsqrtf(bxa[0] * bxa[0] + bxa[1] * bxa[1] + bxa[2] * bxa[2]);
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      // dp'/dA_m = 2t e_m, dp'/dB_m = e_m;  d(BxA)/dA_m = B x e_m, d(BxA)/dB_m = e_m x A
+      const float e[3] = {m == 0 ? 1.f : 0.f, m == 1 ? 1.f : 0.f, m == 2 ? 1.f : 0.f};
+      const float cA[3] = {X.B[1] * e[2] - X.B[2] * e[1], X.B[2] * e[0] - X.B[0] * e[2], X.B[0] * e[1] - X.B[1] * e[0]};
+      const float cB[3] = {e[1] * X.A[2] - e[2] * X.A[1], e[2] * X.A[0] - e[0] * X.A[2], e[0] * X.A[1] - e[1] * X.A[0]};
+      const float Tm = T[m];
+      const float bA = bb[0] * cA[0] + bb[1] * cA[1] + bb[2] * cA[2];
+      const float bB = bb[0] * cB[0] + bb[1] * cB[1] + bb[2] * cB[2];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const float proj = (e[i] - T[i] * Tm) * ip;   // (I - T T^T) e_m / |p'|
+        dT[0][m][i] = 2.f * t * proj;
+        dT[1][m][i] = proj;
+        dbv[0][m][i] = (cA[i] - bb[i] * bA) * ib;
+        dbv[1][m][i] = (cB[i] - bb[i] * bB) * ib;
+      }
+    }
+  } else if (X.cls >= 1) {
+    // constant frame: T0 from A + B (curved, A || B) or the chord B (straight)
+    float T0r[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) T0r[i] = X.cls == 1 ? X.B[i] : X.A[i] + X.B[i];
+    const float i0 = rsqrtf(T0r[0] * T0r[0] + T0r[1] * T0r[1] + T0r[2] * T0r[2]);
+    const float ut = X.up[0] * T[0] + X.up[1] * T[1] + X.up[2] * T[2];
+    float v[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) v[i] = X.up[i] - ut * T[i];
+    const float iv = rsqrtf(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      float dT0[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) dT0[i] = ((i == m ? 1.f : 0.f) - T[i] * T[m]) * i0;   // d T0 / d(T0r)_m
+      const float udT = X.up[0] * dT0[0] + X.up[1] * dT0[1] + X.up[2] * dT0[2];
+      float dv[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) dv[i] = -udT * T[i] - ut * dT0[i];
+      const float bdv = bb[0] * dv[0] + bb[1] * dv[1] + bb[2] * dv[2];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const float db = (dv[i] - bb[i] * bdv) * iv;
+        // T0r = A + B (curved) or B (straight: the chord; A = 0)
+        dT[1][m][i] = dT0[i];
+        dbv[1][m][i] = db;
+        if (X.cls == 2) { dT[0][m][i] = dT0[i]; dbv[0][m][i] = db; }
+      }
+    }
+  }
+  const float tt = t * t;
+#pragma unroll
+  for (int which = 0; which < 3; ++which)
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      // d d / d theta at fixed t: A_m -> -t^2 e_m, B_m -> -t e_m, w_m -> e_m
+      const float sd = which == 0 ? -tt : (which == 1 ? -t : 1.f);
+      const float* dTm = dT[which][m];
+      const float* dbm = dbv[which][m];
+      // dN = db x T + b x dT
+      const float dN[3] = {dbm[1] * T[2] - dbm[2] * T[1] + bb[1] * dTm[2] - bb[2] * dTm[1],
+                           dbm[2] * T[0] - dbm[0] * T[2] + bb[2] * dTm[0] - bb[0] * dTm[2],
+                           dbm[0] * T[1] - dbm[1] * T[0] + bb[0] * dTm[1] - bb[1] * dTm[0]};
+      out[which][m][0] = dTm[0] * d[0] + dTm[1] * d[1] + dTm[2] * d[2] + sd * T[m];
+      out[which][m][1] = dN[0] * d[0] + dN[1] * d[1] + dN[2] * d[2] + sd * N[m];
+      out[which][m][2] = dbm[0] * d[0] + dbm[1] * d[1] + dbm[2] * d[2] + sd * bb[m];
+    }
+  // y_t: Frenet T' = (p'' - T (T.p'')) / |p'|, N' = b x T'; constant frames: -R^T p'
+  if (X.cls == 2 && X.frenet) {
+    const float ip = rsqrtf(pd[0] * pd[0] + pd[1] * pd[1] + pd[2] * pd[2]);
+    const float tp = 2.f * (T[0] * X.A[0] + T[1] * X.A[1] + T[2] * X.A[2]);
+    float Tp[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) Tp[i] = (2.f * X.A[i] - T[i] * tp) * ip;
+    const float Np[3] = {bb[1] * Tp[2] - bb[2] * Tp[1], bb[2] * Tp[0] - bb[0] * Tp[2], bb[0] * Tp[1] - bb[1] * Tp[0]};
+    yt[0] = (Tp[0] * d[0] + Tp[1] * d[1] + Tp[2] * d[2]) - (T[0] * pd[0] + T[1] * pd[1] + T[2] * pd[2]);
+    yt[1] = (Np[0] * d[0] + Np[1] * d[1] + Np[2] * d[2]) - (N[0] * pd[0] + N[1] * pd[1] + N[2] * pd[2]);
+  } else {
+    yt[0] = -(T[0] * pd[0] + T[1] * pd[1] + T[2] * pd[2]);
+    yt[1] = -(N[0] * pd[0] + N[1] * pd[1] + N[2] * pd[2]);
+  }
+  yt[2] = -(bb[0] * pd[0] + bb[1] * pd[1] + bb[2] * pd[2]);
+}
+
 template <class Emit>
 __device__ __forceinline__ void xpsq_param_grad(const SceneDev& S, const Xpsq& X, const float* y, float scale,
                                                 Emit emit) {
@@ -398,6 +610,90 @@ __device__ __forceinline__ void xpsq_param_grad(const SceneDev& S, const Xpsq& X
       emit(7 + 4 * j, scale * (dn0[2] + dn1[2])); emit(8 + 4 * j, scale * (dh0 + dh1));
     }
   }
+  // control points p1, p2, p3 (slots base .. base + 8): through the roots,
+  // the frame and p(t) of every root's PSQ, weighted by the smooth minimum
+  // (DESIGN.md §2 f4; the oracle seeds the control points)
+  float dtA[3][3], dtB[3][3], dtw[3][3];
+  xpsq_root_dtheta(X, S.sp, w, dtA, dtB, dtw);
+  float dph[3][3] = {};   // [A, B, w][m]
+#pragma unroll 1
+  for (int k = 0; k < nr; ++k) {
+    const float t = tv[k];
+    float pd[3], d[3], T[3], N[3], bb[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      pd[i] = fmaf(2.f * X.A[i], t, X.B[i]);
+      d[i] = y[i] - fmaf(fmaf(X.A[i], t, X.B[i]), t, X.p1[i]);
+    }
+    if (X.frenet) {
+      const float in = rsqrtf(pd[0] * pd[0] + pd[1] * pd[1] + pd[2] * pd[2]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) { T[i] = pd[i] * in; bb[i] = X.bhat[i]; }
+      N[0] = bb[1] * T[2] - bb[2] * T[1]; N[1] = bb[2] * T[0] - bb[0] * T[2]; N[2] = bb[0] * T[1] - bb[1] * T[0];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) { T[i] = X.R0[i * 3 + 0]; N[i] = X.R0[i * 3 + 1]; bb[i] = X.R0[i * 3 + 2]; }
+    }
+    // G = grad_y of the PSQ at y_k; S_t = its derivative along t through the
+    // schedules (varying only)
+    XsqParams q;
+    if (vary) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) q.ia[i] = 1.f / fmaf(t, X.da[i], X.a0[i]);
+      const float e1 = fmaf(t, X.deps[0], X.eps0[0]), e2 = fmaf(t, X.deps[1], X.eps0[1]);
+      q.p1 = 1.f / e1; q.p2 = 1.f / e2; q.m = e2 / e1; q.k = 0.5f * e1;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) q.ia[i] = X.sq_ia[i];
+      q.p1 = X.sq_p1; q.p2 = X.sq_p2; q.m = X.sq_m; q.k = X.sq_k;
+    }
+    Res<1> rs;
+    sq_eval<1>(q, yk[k], rs);
+    float G[3] = {wsq[k] * rs.g[0], wsq[k] * rs.g[1], wsq[k] * rs.g[2]};
+    float St = 0.f;
+    if (vary) {
+      St = wsq[k] * (g5[k][0] * X.da[0] + g5[k][1] * X.da[1] + g5[k][2] * X.da[2] + g5[k][3] * X.deps[0] +
+                     g5[k][4] * X.deps[1]);
+    }
+    for (int j = 0; j < np; ++j) {
+      float n[3], iv, h;
+      plane_at(j, t, n, iv, h);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) G[i] = fmaf(wpl[k][j], n[i], G[i]);
+      if (vary) {   // d(n.y + h)/dt = ((I - n n^T) dpl / |v|).y + dh
+        const float nd = n[0] * X.dpl[j][0] + n[1] * X.dpl[j][1] + n[2] * X.dpl[j][2];
+        float dn = 0.f;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) dn = fmaf((X.dpl[j][i] - n[i] * nd) * iv, yk[k][i], dn);
+        St = fmaf(wpl[k][j], dn + X.dpl[j][3], St);
+      }
+    }
+    float dyt[3][3][3], yt[3];
+    xpsq_dy_dtheta(X, t, d, T, N, bb, dyt, yt);
+    const float Gyt = G[0] * yt[0] + G[1] * yt[1] + G[2] * yt[2] + St;
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const float dts[3] = {dtA[k][m], dtB[k][m], dtw[k][m]};
+#pragma unroll
+      for (int which = 0; which < 3; ++which) {
+        const float v = G[0] * dyt[which][m][0] + G[1] * dyt[which][m][1] + G[2] * dyt[which][m][2] + Gyt * dts[which];
+        dph[which][m] = fmaf(u[k], v, dph[which][m]);
+      }
+    }
+  }
+  const int base = (vary ? 2 : 1) * M;
+#pragma unroll
+  for (int m = 0; m < 3; ++m) {
+    if (X.cls == 1) {   // straight: the chord B = p3 - p1 (A = 0), w = x - p1
+      emit(base + m, scale * (-dph[1][m] - dph[2][m]));
+      emit(base + 3 + m, 0.f);
+      emit(base + 6 + m, scale * dph[1][m]);
+    } else {            // A = p1 - 2 p2 + p3, B = 2 (p2 - p1), w = x - p1
+      emit(base + m, scale * (dph[0][m] - 2.f * dph[1][m] - dph[2][m]));
+      emit(base + 3 + m, scale * (-2.f * dph[0][m] + 2.f * dph[1][m]));
+      emit(base + 6 + m, scale * dph[0][m]);
+    }
+  }
 }
 
 // parameters of leaf li at the shape-frame point x, scaled by d phi_shape /
@@ -453,7 +749,7 @@ __device__ __forceinline__ int leaf_param_count(const SceneDev& S, const Leaf& L
   if (L.kind == LK_HALFSPACE) return 4;
   if (L.kind != LK_XPSQ) return 5 + 4 * L.n_planes;
   const Xpsq& X = S.xpsq[L.xidx];
-  return (X.varying ? 2 : 1) * (5 + 4 * X.n_planes);
+  return (X.varying ? 2 : 1) * (5 + 4 * X.n_planes) + 9;   // + control points
 }
 
 // one thread per point; shapes are single leaves or boolean trees of up to

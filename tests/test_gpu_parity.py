@@ -437,6 +437,12 @@ def _param_scene():
                                              (0.6, 0.8), a1=(0.008, 0.01, 0.016), eps1=(0.9, 0.5),
                                              planes0=[[0.2, 0.3, 0.93, -0.005]],
                                              planes1=[[-0.1, 0.4, 0.9, -0.008]]), None),
+        # straight (p2 the midpoint: the chord p1 -> p3) and point splines:
+        # control-point derivatives within their static class
+        synth.make_shape("xline", synth.xpsq([-0.04, 0.01, 0.0, 0.0, 0.02, 0.01, 0.04, 0.03, 0.02], (0.01, 0.012, 0.01),
+                                             (0.5, 0.9), up=(0.2, 0.1, 1.0)), None),
+        synth.make_shape("xpoint", synth.xpsq([0.01, 0.0, 0.0] * 3, (0.01, 0.012, 0.015), (0.5, 0.9),
+                                              planes0=[[0.1, 0.2, 0.97, -0.004]]), None),
         synth.make_shape("svary", synth.op("subtraction", [
             synth.sq(a(), e()),
             synth.xpsq([-0.05, 0, 0, 0.0, 0.05, 0.0, 0.05, 0, 0.0], (0.01, 0.012, 0.01), (0.5, 0.9),
@@ -460,7 +466,7 @@ def test_sdf_param_grad_parity(cuda, oracle_mod):
     counts, offs = S.param_layout()
     osc = oracle_mod.OracleScene(sc)
     assert [osc.param_count(s) for s in range(len(shapes))] == list(counts)
-    B, P = 48, 96
+    B, P = 4 * len(shapes), 96
     ids = np.repeat(np.arange(len(shapes)), B // len(shapes)).astype(np.int32)
     poses = np.stack([synth.pose_row(rng.uniform(-0.1, 0.1, 3), synth.random_quats(rng, 1)[0]) for _ in range(B)])
     poses = poses.astype(np.float32)
