@@ -351,6 +351,19 @@ static_assert(sizeof(UnitCtx) % 16 == 0, "UnitCtx is copied as float4");
 #ifndef CM_TRACE6
 #define CM_TRACE6 1         // 6-component trace derivative recursion (tiers 0-2)
 #endif
+#ifndef CM_MF_FUSE_EDGES
+#define CM_MF_FUSE_EDGES 0  // traces + midpoints in one kernel, one thread per edge (tiers 0-2): bitwise equal,
+                            // C5 -19%, C4 -47% (XPSQ classes: instruction-cache stalls; r02z2)
+#endif
+#ifndef CM_MF_EDGE_SMEM
+#define CM_MF_EDGE_SMEM 0   // the edge kernel parks the first trace's result in shared memory
+#endif
+#ifndef CM_MF_REG_E_XP0
+#define CM_MF_REG_E_XP0 0   // register cap of the SQ-family edge kernel (0: the trace / midpoint budget)
+#endif
+#ifndef CM_MF_REG_E_XP1
+#define CM_MF_REG_E_XP1 0   // register cap of the order-2 XPSQ edge kernels (0: the midpoint budget)
+#endif
 #ifndef CM_MF_THREADS
 #define CM_MF_THREADS 64
 #endif
@@ -770,14 +783,81 @@ __device__ __forceinline__ void mf_traces_unit(const MfArgs& a, const UnitCtx& U
 // recursion d alpha_{k+1} = d alpha_k + c [(g.e_t) d alpha_k + g^T J(p)]
 // preserves (X <- X + c (ge X + g), Y <- Y + c (ge Y + p x g)); the 9
 // components are formed once, after the clip.
+// One trace of edge e (vertex indices vI, vII) in direction dir: o[0] = the
+// clipped alpha, o[1..9] its derivative over (t_A, theta_A, t_B) (tier 2)
+template <int TIER, int XP>
+__device__ __forceinline__ void trace_one_n(const MfArgs& a, const UnitCtx& U, const float* sv, const float* lv,
+                                            int vI, int vII, int dir, float* o) {
+  constexpr int OT = TIER >= 2 ? 1 : 0;
+  const SmoothDev& sp = a.S.sp;
+  const float itcmp = sp.i_cmp;
+  const PairFrame& F = U.F;
+  const float4 corner = ld4(sv + (dir ? vII : vI) * vrec(TIER));   // d, n of the start vertex
+  float xl[3], el[3], L;
+  {
+    const float4 xa = ldv(lv, vI), xb4 = ldv(lv, vII);
+    const float dl[3] = {xb4.x - xa.x, xb4.y - xa.y, xb4.z - xa.z};
+    L = sqrtf(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
+    const float iL = 1.f / L;
+    el[0] = dl[0] * iL; el[1] = dl[1] * iL; el[2] = dl[2] * iL;
+    xl[0] = xa.x; xl[1] = xa.y; xl[2] = xa.z;
+  }
+  float eb[3], ew[3];
+  rot_vec(F.Rrel, el, eb);
+  rot_vec(F.RA, el, ew);
+  float xI[3], pI[3];
+  to_frames(F, xl, xI, pI);
+  float al = dir ? L : 0.f;
+  const float sgn = dir ? -1.f : 1.f;
+  float X[3] = {0.f, 0.f, 0.f}, Y[3] = {0.f, 0.f, 0.f};
+  float phi = corner.x;
+  float g[3] = {corner.y, corner.z, corner.w};   // the corner itself: the vertex evaluation (reading #22)
+#pragma unroll 1
+  for (int it = 0; it < sp.iters; ++it) {
+    if (it > 0) {
+      const float xb[3] = {fmaf(al, eb[0], xI[0]), fmaf(al, eb[1], xI[1]), fmaf(al, eb[2], xI[2])};
+      Res<OT> r;
+      CM_EVAL(OT, XP)(a.S, U.SB, xb, r);
+      phi = r.v;
+      if constexpr (TIER >= 2) rot_vec(F.RB, r.g, g);
+    }
+    // gated step G(phi) = sigma(phi / tau) phi  (reading #20)
+    const float s = sigm(phi * itcmp);
+    if constexpr (TIER >= 2) {
+      const float Gp = fmaf(phi * s * (1.f - s), itcmp, s);
+      const float p[3] = {fmaf(al, ew[0], pI[0]), fmaf(al, ew[1], pI[1]), fmaf(al, ew[2], pI[2])};
+      const float m[3] = {p[1] * g[2] - p[2] * g[1], p[2] * g[0] - p[0] * g[2], p[0] * g[1] - p[1] * g[0]};
+      const float ge = g[0] * ew[0] + g[1] * ew[1] + g[2] * ew[2];
+      const float c = sgn * Gp;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        X[k] = fmaf(c, fmaf(ge, X[k], g[k]), X[k]);
+        Y[k] = fmaf(c, fmaf(ge, Y[k], m[k]), Y[k]);
+      }
+    }
+    al = fmaf(sgn * s, phi, al);
+  }
+  // soft clip to the edge (reading #21)
+  float at, c1, c2;
+  softclip_12(al, 0.f, L, sp.tau_clip_alpha, sp.i_clip_alpha, at, c1, c2);
+  o[0] = at;
+  if constexpr (TIER >= 2) {
+    const float* tA = F.tA;
+    const float* tB = F.tB;
+    // d alpha = [X, Y - tA x X, -Y + tB x X], times the clip derivative
+    o[1] = c1 * X[0]; o[2] = c1 * X[1]; o[3] = c1 * X[2];
+    o[4] = c1 * (Y[0] - (tA[1] * X[2] - tA[2] * X[1]));
+    o[5] = c1 * (Y[1] - (tA[2] * X[0] - tA[0] * X[2]));
+    o[6] = c1 * (Y[2] - (tA[0] * X[1] - tA[1] * X[0]));
+    o[7] = c1 * (-Y[0] + (tB[1] * X[2] - tB[2] * X[1]));
+    o[8] = c1 * (-Y[1] + (tB[2] * X[0] - tB[0] * X[2]));
+    o[9] = c1 * (-Y[2] + (tB[0] * X[1] - tB[1] * X[0]));
+  }
+}
+
 template <int TIER, int XP>
 __device__ __forceinline__ void mf_traces_unit_n(const MfArgs& a, const UnitCtx& U, int u) {
   static_assert(TIER <= 2, "tier 3 carries second derivatives: mf_traces_unit");
-  constexpr int OT = TIER >= 2 ? 1 : 0;
-  const SmoothDev sp = a.S.sp;
-  const float itcmp = sp.i_cmp;
-  const float tca = sp.tau_clip_alpha, itca = sp.i_clip_alpha;
-  const PairFrame& F = U.F;
   const int V = U.SA.V, E = U.SA.E;
   const float* sv = a.scratch + (int64_t)u * a.slot;
   float* se = a.scratch + (int64_t)u * a.slot + (int64_t)vrec(TIER) * V;
@@ -788,66 +868,10 @@ __device__ __forceinline__ void mf_traces_unit_n(const MfArgs& a, const UnitCtx&
     const int dir = j < E ? 0 : 1;     // 0: from v_I along +e_t; 1: from v_II along -e_t
     const int vI = __ldg(ed + 2 * e), vII = __ldg(ed + 2 * e + 1);
     CM_ASSERT(vI >= 0 && vI < V && vII >= 0 && vII < V);
-    const float4 corner = ld4(sv + (dir ? vII : vI) * vrec(TIER));   // d, n of the start vertex
-    float xl[3], el[3], L;
-    {
-      const float4 xa = ldv(lv, vI), xb4 = ldv(lv, vII);
-      const float dl[3] = {xb4.x - xa.x, xb4.y - xa.y, xb4.z - xa.z};
-      L = sqrtf(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
-      const float iL = 1.f / L;
-      el[0] = dl[0] * iL; el[1] = dl[1] * iL; el[2] = dl[2] * iL;
-      xl[0] = xa.x; xl[1] = xa.y; xl[2] = xa.z;
-    }
-    float eb[3], ew[3];
-    rot_vec(F.Rrel, el, eb);
-    rot_vec(F.RA, el, ew);
-    float xI[3], pI[3];
-    to_frames(F, xl, xI, pI);
-    float al = dir ? L : 0.f;
-    const float sgn = dir ? -1.f : 1.f;
-    float X[3] = {0.f, 0.f, 0.f}, Y[3] = {0.f, 0.f, 0.f};
-    float phi = corner.x;
-    float g[3] = {corner.y, corner.z, corner.w};   // the corner itself: the vertex evaluation (reading #22)
-#pragma unroll 1
-    for (int it = 0; it < sp.iters; ++it) {
-      if (it > 0) {
-        const float xb[3] = {fmaf(al, eb[0], xI[0]), fmaf(al, eb[1], xI[1]), fmaf(al, eb[2], xI[2])};
-        Res<OT> r;
-        CM_EVAL(OT, XP)(a.S, U.SB, xb, r);
-        phi = r.v;
-        if constexpr (TIER >= 2) rot_vec(F.RB, r.g, g);
-      }
-      // gated step G(phi) = sigma(phi / tau) phi  (reading #20)
-      const float s = sigm(phi * itcmp);
-      if constexpr (TIER >= 2) {
-        const float Gp = fmaf(phi * s * (1.f - s), itcmp, s);
-        const float p[3] = {fmaf(al, ew[0], pI[0]), fmaf(al, ew[1], pI[1]), fmaf(al, ew[2], pI[2])};
-        const float m[3] = {p[1] * g[2] - p[2] * g[1], p[2] * g[0] - p[0] * g[2], p[0] * g[1] - p[1] * g[0]};
-        const float ge = g[0] * ew[0] + g[1] * ew[1] + g[2] * ew[2];
-        const float c = sgn * Gp;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          X[k] = fmaf(c, fmaf(ge, X[k], g[k]), X[k]);
-          Y[k] = fmaf(c, fmaf(ge, Y[k], m[k]), Y[k]);
-        }
-      }
-      al = fmaf(sgn * s, phi, al);
-    }
-    // soft clip to the edge (reading #21)
+    float o[10];
+    trace_one_n<TIER, XP>(a, U, sv, lv, vI, vII, dir, o);
     float* rec = se + e * erec(TIER) + (dir ? trace_b(TIER) : 0);
-    float at, c1, c2;
-    softclip_12(al, 0.f, L, tca, itca, at, c1, c2);
     if constexpr (TIER >= 2) {
-      const float* tA = F.tA;
-      const float* tB = F.tB;
-      // d alpha = [X, Y - tA x X, -Y + tB x X], times the clip derivative
-      const float o[10] = {at, c1 * X[0], c1 * X[1], c1 * X[2],
-                           c1 * (Y[0] - (tA[1] * X[2] - tA[2] * X[1])),
-                           c1 * (Y[1] - (tA[2] * X[0] - tA[0] * X[2])),
-                           c1 * (Y[2] - (tA[0] * X[1] - tA[1] * X[0])),
-                           c1 * (-Y[0] + (tB[1] * X[2] - tB[2] * X[1])),
-                           c1 * (-Y[1] + (tB[2] * X[0] - tB[0] * X[2])),
-                           c1 * (-Y[2] + (tB[0] * X[1] - tB[1] * X[0]))};
       if (dir == 0) {   // record floats 0-9: two float4 + one float2
         st4(rec, o[0], o[1], o[2], o[3]);
         st4(rec + 4, o[4], o[5], o[6], o[7]);
@@ -858,30 +882,75 @@ __device__ __forceinline__ void mf_traces_unit_n(const MfArgs& a, const UnitCtx&
         st4(rec + 6, o[6], o[7], o[8], o[9]);
       }
     } else {
-      *rec = at;
+      *rec = o[0];
     }
   }
 }
 
 // ---- phase 3: edge points p_e = v_I + a_bar e_t, a_bar = (a_I + a_II)/2
+// the candidate at edge e from its averaged trace (ab, dab, d2ab): phi, n, H
+// of B at p_e, the edge record and (full mode) the candidate's output row
+template <int TIER, int XP>
+__device__ __forceinline__ void midpoint_one(const MfArgs& a, const UnitCtx& U, int e, float ab, const float* dab,
+                                             const float* d2ab, float* rec) {
+  constexpr int OV = TIER >= 2 ? 2 : 1;
+  const PairFrame& F = U.F;
+  const float* eg = a.S.edge_geom + 8 * (int64_t)U.SA.e_off;
+  float xl[3], el[3], L;
+  edge_geom(eg, e, xl, L, el);
+  float eb[3], ew[3];
+  rot_vec(F.Rrel, el, eb);
+  rot_vec(F.RA, el, ew);
+  float xI[3], pI[3];
+  to_frames(F, xl, xI, pI);
+  float xb[3], pw[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    xb[i] = fmaf(ab, eb[i], xI[i]);
+    pw[i] = fmaf(ab, ew[i], pI[i]);
+  }
+  Res<OV> r;
+  CM_EVAL(OV, XP)(a.S, U.SB, xb, r);
+  float n[3];
+  rot_vec(F.RB, r.g, n);
+  float h[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if constexpr (TIER >= 2) {
+    rot_sym(F.RB, r.h, h);
+    st4(rec, ab, r.v, n[0], n[1]);
+    st4(rec + 4, n[2], h[0], h[1], h[2]);
+    st4(rec + 8, h[3], h[4], h[5], dab[0]);
+    st4(rec + 12, dab[1], dab[2], dab[3], dab[4]);
+    st4(rec + 16, dab[5], dab[6], dab[7], dab[8]);
+  } else {
+    st4(rec, ab, r.v, n[0], n[1]);
+    rec[4] = n[2];
+  }
+  float d2[TIER >= 3 ? N45 : 1];
+  if constexpr (TIER >= 3) {
+    // d^2 d_e = phi_zz + phi_za dab^T + dab phi_za^T + phi_aa dab dab^T + phi_a d2ab
+    float fza[NDQ], faa;
+    d2_point(n, h, pw, F.tA, F.tB, d2);
+    d2_alpha(n, h, pw, ew, F.tA, F.tB, fza, faa);
+    const float fa = n[0] * ew[0] + n[1] * ew[1] + n[2] * ew[2];
+    d2_total(d2, fza, faa, fa, dab, d2ab);
+#pragma unroll
+    for (int k = 0; k < N45; ++k) rec[MD2 + k] = d2[k];
+  }
+  if (a.mode & CM_FULL_MODE) {
+    CM_COLS(U.side);
+    store_candidate<TIER>(a.out, a.C, U.off + U.SA.V + e, pw, n, r.v, h, ew, dab, F, 1, a.S.sp.i_cmp, cTA, cRA, cTB,
+                          cRB, d2, U.side);
+  }
+}
+
 template <int TIER, int XP>
 __device__ __forceinline__ void mf_midpoints_unit(const MfArgs& a, const UnitCtx& U, int u, const float* srec,
                                                   float* drec = nullptr) {
-  constexpr int OV = TIER >= 2 ? 2 : 1;
-  const PairFrame& F = U.F;
   const int V = U.SA.V, E = U.SA.E;
   float* se = a.scratch + (int64_t)u * a.slot + (int64_t)vrec(TIER) * V;
   if (srec == nullptr) srec = se;   // trace records: staged in shared memory, or the slot
   if (drec == nullptr) drec = se;   // edge records: to the slot, or to shared memory (fused faces)
-  const float* eg = a.S.edge_geom + 8 * (int64_t)U.SA.e_off;
-  const bool full = (a.mode & CM_FULL_MODE) != 0;
-  const float itcmp = a.S.sp.i_cmp;
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    float xl[3], el[3], L;
-    edge_geom(eg, e, xl, L, el);
-    float eb[3], ew[3];
-    rot_vec(F.Rrel, el, eb);
-    rot_vec(F.RA, el, ew);
     float* rec = drec + e * erec(TIER);
     const float* rin = srec + e * erec(TIER);
     float ab, dab[NDQ];
@@ -906,46 +975,54 @@ __device__ __forceinline__ void mf_midpoints_unit(const MfArgs& a, const UnitCtx
     } else {
       ab = 0.5f * (rin[0] + rin[1]);
     }
-    float xI[3], pI[3];
-    to_frames(F, xl, xI, pI);
-    float xb[3], pw[3];
+    midpoint_one<TIER, XP>(a, U, e, ab, dab, d2ab, rec);
+  }
+}
+
+// ---- phases 2 + 3 in one thread per edge (tiers 0-2): both traces of the
+// edge, then its midpoint candidate; the trace results stay in registers
+// (no trace records through the scratch slot: -2 x 40 B of HBM traffic per
+// edge and one launch per class and chunk).  Bitwise equal to the separate
+// kernels: the sums a_I + a_II are formed in the same order with the same
+// roundings (0 + a_I is exact).
+template <int TIER, int XP>
+__device__ __forceinline__ void mf_edges_unit(const MfArgs& a, const UnitCtx& U, int u, float* esm) {
+  static_assert(TIER <= 2, "tier 3: separate trace and midpoint kernels");
+  const int V = U.SA.V, E = U.SA.E;
+  const float* sv = a.scratch + (int64_t)u * a.slot;
+  float* se = a.scratch + (int64_t)u * a.slot + (int64_t)vrec(TIER) * V;
+  const float* lv = a.S.verts + 4 * (int64_t)U.SA.v_off;
+  const int32_t* ed = a.S.edges + 2 * (int64_t)U.SA.e_off;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const int vI = __ldg(ed + 2 * e), vII = __ldg(ed + 2 * e + 1);
+    CM_ASSERT(vI >= 0 && vI < V && vII >= 0 && vII < V);
+    constexpr int NS = TIER >= 2 ? 10 : 1;
+    float sum[10];
+    // one copy of the trace code for both directions (a second inlined copy
+    // of the SDF evaluation costs instruction-cache misses)
+#pragma unroll 1
+    for (int dir = 0; dir < 2; ++dir) {
+      float o[10];
+      trace_one_n<TIER, XP>(a, U, sv, lv, vI, vII, dir, o);
+      if constexpr (CM_MF_EDGE_SMEM) {   // the first trace parked in shared memory
+        if (dir == 0) {
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      xb[i] = fmaf(ab, eb[i], xI[i]);
-      pw[i] = fmaf(ab, ew[i], pI[i]);
-    }
-    Res<OV> r;
-    CM_EVAL(OV, XP)(a.S, U.SB, xb, r);
-    float n[3];
-    rot_vec(F.RB, r.g, n);
-    float h[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if constexpr (TIER >= 2) {
-      rot_sym(F.RB, r.h, h);
-      st4(rec, ab, r.v, n[0], n[1]);
-      st4(rec + 4, n[2], h[0], h[1], h[2]);
-      st4(rec + 8, h[3], h[4], h[5], dab[0]);
-      st4(rec + 12, dab[1], dab[2], dab[3], dab[4]);
-      st4(rec + 16, dab[5], dab[6], dab[7], dab[8]);
-    } else {
-      st4(rec, ab, r.v, n[0], n[1]);
-      rec[4] = n[2];
-    }
-    float d2[TIER >= 3 ? N45 : 1];
-    if constexpr (TIER >= 3) {
-      // d^2 d_e = phi_zz + phi_za dab^T + dab phi_za^T + phi_aa dab dab^T + phi_a d2ab
-      float fza[NDQ], faa;
-      d2_point(n, h, pw, F.tA, F.tB, d2);
-      d2_alpha(n, h, pw, ew, F.tA, F.tB, fza, faa);
-      const float fa = n[0] * ew[0] + n[1] * ew[1] + n[2] * ew[2];
-      d2_total(d2, fza, faa, fa, dab, d2ab);
+          for (int k = 0; k < NS; ++k) esm[k * blockDim.x + threadIdx.x] = o[k];
+        } else {
 #pragma unroll
-      for (int k = 0; k < N45; ++k) rec[MD2 + k] = d2[k];
+          for (int k = 0; k < NS; ++k) sum[k] = __fadd_rn(esm[k * blockDim.x + threadIdx.x], o[k]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < NS; ++k) sum[k] = dir ? __fadd_rn(sum[k], o[k]) : o[k];
+      }
     }
-    if (full) {
-      CM_COLS(U.side);
-      store_candidate<TIER>(a.out, a.C, U.off + V + e, pw, n, r.v, h, ew, dab, F, 1, itcmp, cTA, cRA, cTB, cRB,
-                            d2, U.side);
-    }
+    const float ab = 0.5f * sum[0];
+    float dab[NDQ];
+#pragma unroll
+    for (int k = 0; k < NDQ; ++k) dab[k] = TIER >= 2 ? 0.5f * sum[1 + k] : 0.f;
+    const float d2ab[1] = {0.f};
+    midpoint_one<TIER, XP>(a, U, e, ab, dab, d2ab, se + e * erec(TIER));
   }
 }
 
@@ -1320,6 +1397,19 @@ __global__ void __maxnreg__((RegCap<TIER, XP>::TRACES)) k_mf_traces(const MfArgs
   if constexpr (TIER <= 2 && CM_TRACE6) mf_traces_unit_n<TIER, XP>(a, U, u);
   else mf_traces_unit<TIER, XP>(a, U, u);
 }
+template <int TIER, int XP> struct EdgeRegs {   // the larger of the trace and midpoint budgets
+  static constexpr int R0 = RegCap<TIER, XP>::MIDPOINTS > RegCap<TIER, XP>::TRACES ? RegCap<TIER, XP>::MIDPOINTS
+                                                                                    : RegCap<TIER, XP>::TRACES;
+  static constexpr int R = (XP == 0 && CM_MF_REG_E_XP0) ? CM_MF_REG_E_XP0
+                         : (((XP == 1 || XP == 4) && CM_MF_REG_E_XP1) ? CM_MF_REG_E_XP1 : R0);
+};
+template <int TIER, int XP>
+__global__ void __maxnreg__((EdgeRegs<TIER, XP>::R)) k_mf_edges(const MfArgs a) {
+  extern __shared__ __align__(16) float esm[];
+  __shared__ UnitCtx U;
+  int u;
+  if (list_unit(a, XP, U, u)) mf_edges_unit<TIER, XP>(a, U, u, esm);
+}
 // STAGED: the unit's trace records (E x erec floats, contiguous in its slot)
 // are first copied into shared memory with one TMA bulk copy, so the edge
 // loop does not wait on HBM for every edge
@@ -1463,6 +1553,12 @@ static int launch_sdf_phases(MfArgs& a, int64_t nb, int T, int max_V, int max_E,
   k_mf_vertices<TIER, XP><<<(unsigned)nb, T, 0, st>>>(a);
   int rc = check_launch("k_mf_vertices");
   if (rc) return rc;
+  if constexpr (TIER <= 2 && CM_MF_FUSE_EDGES && CM_TRACE6) {
+    if (midfaces_bytes(TIER, a.mode, max_V, max_E) == 0) {
+      k_mf_edges<TIER, XP><<<(unsigned)nb, T, CM_MF_EDGE_SMEM ? T * 10 * 4 : 0, st>>>(a);
+      return check_launch("k_mf_edges");
+    }
+  }
   k_mf_traces<TIER, XP><<<(unsigned)nb, T, 0, st>>>(a);
   if ((rc = check_launch("k_mf_traces"))) return rc;
   if constexpr (TIER <= 2) {
