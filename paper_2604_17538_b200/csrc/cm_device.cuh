@@ -36,7 +36,7 @@ using namespace cmi;
 #define CM_SOFTCLIP_FAST 0    // softclip interior shortcut: measured C5 -1.5%, C4 -1.7% (r02j sweep)
 #endif
 #ifndef CM_LEAF_LAZY_R
-#define CM_LEAF_LAZY_R 0      // leaf rotation loaded only for rotated leaves: C5 -1.7%, C4 -1.2% (r02j)
+#define CM_LEAF_LAZY_R 0      // (retired by the 128-bit leaf loads) leaf rotation loaded only for rotated leaves: C5 -1.7%, C4 -1.2% (r02j)
 #endif
 #ifndef CM_XPSQ_TSPACE
 #define CM_XPSQ_TSPACE 1      // curved roots outside the band: Newton-polished in t (near-straight splines)
@@ -1214,24 +1214,60 @@ template <int O> __device__ CM_XINL void xpsq_eval_fast(const Xpsq& X, const Smo
 // 2 any XPSQ (jets when the schedules vary along t); XINL: constant-schedule
 // XPSQ inlined up to order CM_XPSQ_INLINE_MAX_O (manifold kernels) or always
 // out of line (sdf_eval: one kernel for all leaf kinds, measured faster so)
+// a leaf's frame, kind and SQ constants in registers: six 128-bit loads
+// (cm_internal.h Leaf layout)
+struct LeafRegs {
+  float R[9], t[3];
+  int kind, n_planes, rot_identity, xidx;
+  float ia[3], p1, p2, m, k;
+};
+#ifndef CM_LEAF_VEC
+#define CM_LEAF_VEC 0   // explicit __ldg 128-bit leaf loads: SDF +1.3%, manifold C5 -1.5% / C4 -2.5% against the
+                        // compiler's own merging of the aligned fields (r02z4); cm_kernels_sdf.cu sets it
+#endif
+__device__ __forceinline__ void ld_leaf(const Leaf* lp, LeafRegs& o) {
+#if CM_LEAF_VEC
+  const float4* q = reinterpret_cast<const float4*>(lp);
+  const float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+  const int4 d = __ldg(reinterpret_cast<const int4*>(q + 3));
+  const float4 e = __ldg(q + 4), f = __ldg(q + 5);
+  o.R[0] = a.x; o.R[1] = a.y; o.R[2] = a.z; o.R[3] = a.w;
+  o.R[4] = b.x; o.R[5] = b.y; o.R[6] = b.z; o.R[7] = b.w;
+  o.R[8] = c.x; o.t[0] = c.y; o.t[1] = c.z; o.t[2] = c.w;
+  o.kind = d.x; o.n_planes = d.y; o.rot_identity = d.z; o.xidx = d.w;
+  o.ia[0] = e.x; o.ia[1] = e.y; o.ia[2] = e.z; o.p1 = e.w;
+  o.p2 = f.x; o.m = f.y; o.k = f.z;
+#else
+  const Leaf& L = *lp;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) o.R[i] = L.R[i];
+  o.t[0] = L.t[0]; o.t[1] = L.t[1]; o.t[2] = L.t[2];
+  o.kind = L.kind; o.n_planes = L.n_planes; o.rot_identity = L.rot_identity; o.xidx = L.xidx;
+  o.ia[0] = L.ia[0]; o.ia[1] = L.ia[1]; o.ia[2] = L.ia[2];
+  o.p1 = L.p1; o.p2 = L.p2; o.m = L.m; o.k = L.k;
+#endif
+}
+__device__ __forceinline__ void ld_plane(const float* pl, float* o) {
+#if CM_LEAF_VEC
+  const float4 v = __ldg(reinterpret_cast<const float4*>(pl));
+  o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+#else
+  o[0] = pl[0]; o[1] = pl[1]; o[2] = pl[2]; o[3] = pl[3];
+#endif
+}
+
 template <int O, int XP, bool XINL = true>
 __device__ __forceinline__ void leaf_eval(const SceneDev& S, int li, const float* x, Res<O>& r) {
-  const Leaf& L = S.leaves[li];
+  LeafRegs L;
+  ld_leaf(S.leaves + li, L);
+  const float* lplanes = &S.leaves[li].planes[0][0];
   float y[3];
-  float t[3] = {L.t[0], L.t[1], L.t[2]};
+  const float* t = L.t;
   const bool ident = L.rot_identity != 0;
-  float R[9];
-#if !CM_LEAF_LAZY_R
-#pragma unroll
-  for (int i = 0; i < 9; ++i) R[i] = L.R[i];
-#endif
+  const float* R = L.R;
   if (ident) {
     y[0] = x[0] - t[0]; y[1] = x[1] - t[1]; y[2] = x[2] - t[2];
-  } else {   // (the rotation is loaded only for rotated leaves)
-#if CM_LEAF_LAZY_R
-#pragma unroll
-    for (int i = 0; i < 9; ++i) R[i] = L.R[i];
-#endif
+  } else {
     to_local(R, t, x, y);
   }
   Res<O> l;
@@ -1247,7 +1283,9 @@ __device__ __forceinline__ void leaf_eval(const SceneDev& S, int li, const float
       acc_fold(a, 1.f, l, itl, itau);
       for (int j = 0; j < np; ++j) {
         Res<O> p;
-        plane_eval<O>(L.planes[j], y, p);
+        float pl[4];
+        ld_plane(lplanes + 4 * j, pl);
+        plane_eval<O>(pl, y, p);
         acc_fold(a, 1.f, p, itl, itau);
       }
       acc_final(a, 1.f, tau, itau, l);
@@ -1263,7 +1301,9 @@ __device__ __forceinline__ void leaf_eval(const SceneDev& S, int li, const float
       xpsq_eval_fast<O>(X, S.sp, y, l);
     }
   } else {
-    plane_eval<O>(L.planes[0], y, l);
+    float pl[4];
+    ld_plane(lplanes, pl);
+    plane_eval<O>(pl, y, l);
   }
   r.v = l.v;
   if constexpr (O >= 1) {

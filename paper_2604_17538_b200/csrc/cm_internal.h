@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstddef>
+
 #include "xpsq_cm.h"
 
 namespace cmi {
@@ -17,7 +19,7 @@ namespace cmi {
 // Union: children -1, out -1 (-LSE(-phi), Eq. (2)); intersection +1, +1
 // (Eq. (3)); subtraction (+1, -1), out +1 (Eq. (4)).
 enum { OP_LEAF = 0, OP_BEGIN = 1, OP_END = 2 };
-struct Instr {
+struct alignas(16) Instr {   // one 128-bit load per instruction
   int32_t op;
   int32_t idx;
   float child_sign;
@@ -28,7 +30,9 @@ enum { LK_HALFSPACE = 0, LK_SQ = 1, LK_XPSQ = 3 };
 
 // Leaf record (SQ / PSQ / half-space; XPSQ points into Xpsq[xidx]).
 // Frame: x_body = R y + t (composed down the tree on the host in FP64).
-struct Leaf {
+// 16-B aligned, field groups on 16-B boundaries: the kernels load a leaf with
+// six 128-bit loads (cm_device.cuh ld_leaf) instead of 23 scalar ones.
+struct alignas(16) Leaf {
   float R[9];
   float t[3];
   int32_t kind;
@@ -37,6 +41,7 @@ struct Leaf {
   int32_t xidx;
   float ia[3];            // 1 / a
   float p1, p2, m, k;     // 1/eps1, 1/eps2, eps2/eps1, eps1/2
+  float pad0;
   float planes[CM_MAX_PLANES][4];
   // XPSQ leaves: phi >= |x - cull[0..2]| - cull[3] for x in the shape frame
   // (the spline lies in its control points' hull: bounding sphere of their
@@ -45,28 +50,38 @@ struct Leaf {
   // weight is below 2^-66
   float cull[4];
 };
+static_assert(sizeof(Leaf) % 16 == 0 && offsetof(Leaf, planes) == 96, "Leaf: 128-bit load layout");
 
 // XPSQ static data: p(t) = p1 + B t + A t^2 (A := 0, B := p3 - p1
 // for the snapped straight class), projection cubic constants in the affine form
 //   P = gP . w + P0,  Q = gQ . w + Q0,  w = y - p1
 // (c3, c2 depend only on the spline; c1, c0 are affine in w), b3 = b/3.
-struct Xpsq {
-  float p1[3], A[3], B[3];
-  float gP[3], gQ[3], P0, Q0, b3;
-  float c3, c2, BB;       // the cubic in t: c3 t^3 + c2 t^2 + (2 A.w - BB) t + B.w
-  float Bn[3];            // straight class: t = softclip(Bn . w)
+// 16-B aligned with the fields the projection and the evaluation read
+// together in 16-B groups (the compiler merges them into 128-bit loads)
+struct alignas(16) Xpsq {
+  float p1[3], P0;
+  float gP[3], Q0;
+  float gQ[3], b3;
+  float A[3], c3;         // the cubic in t: c3 t^3 + c2 t^2 + (2 A.w - BB) t + B.w
+  float B[3], c2;
+  float Bn[3], BB;        // straight class: t = softclip(Bn . w)
   float bhat[3];          // Frenet binormal (constant for a quadratic)
-  float R0[9];            // constant frame (straight / point / A || B)
-  float up[3];            // the up hint (control-point derivatives of the constant frame, f4)
   int32_t cls;            // 0 point, 1 straight, 2 curve
   int32_t frenet;
   int32_t varying;        // schedules differ between the endpoints
   int32_t n_planes;
+  int32_t pad0;
+  float sq_ia[3], sq_p1;  // SQ constants of the t = 0 schedule
+  float sq_p2, sq_m, sq_k, pad1;
+  float R0[9];            // constant frame (straight / point / A || B)
+  float up[3];            // the up hint (control-point derivatives of the constant frame, f4)
   float eps0[2], deps[2];
-  float a0[3], da[3];
-  float sq_ia[3], sq_p1, sq_p2, sq_m, sq_k;   // SQ constants of the t = 0 schedule
+  float a0[3], pad2;
+  float da[3], pad3;
   float pl0[CM_MAX_PLANES][4], dpl[CM_MAX_PLANES][4];
 };
+static_assert(sizeof(Xpsq) % 16 == 0 && offsetof(Xpsq, pl0) % 16 == 0 && offsetof(Xpsq, sq_ia) % 16 == 0,
+              "Xpsq: 128-bit load layout");
 
 struct ShapeRec {
   int32_t prog_begin, prog_len;

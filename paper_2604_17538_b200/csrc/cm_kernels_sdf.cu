@@ -9,6 +9,9 @@
 
 #include <cstdio>
 
+#ifndef CM_LEAF_VEC
+#define CM_LEAF_VEC 1   // explicit 128-bit leaf loads in this unit (SDF +1.3%, r02z4)
+#endif
 #include "cm_device.cuh"
 #include "cm_internal.h"
 #include "cm_launch.h"
