@@ -553,11 +553,31 @@ template <class T> T pval(double v, int node, int slot) {
 // subtraction LSE([phi1, -phi2]), Reading #4).  Each node has a pose relative
 // to its parent; y is in the parent frame.
 // ---------------------------------------------------------------------------
+// Node-pose seeding (node poses; DESIGN reading #47): the
+// twist (dt, dtheta) of node g_pose_node's pose in its parent frame, slots
+// 0-2 dt, 3-5 dtheta, with the body poses' convention (reading #28):
+// R <- exp([dtheta]x) R, t <- t + dt, where x_parent = R x_node + t.
+thread_local int g_pose_node = -1, g_pose_slot = -1;
+template <class T> T pose_seed(int idx, int slot) {
+  T x(0.0);
+  if (idx == g_pose_node && slot == g_pose_slot) Seeder<T>::apply(x);
+  return x;
+}
+template <class T> void perturbed_pose(const double* R, const double* t, const T* dt, const T* w, T* Rp, T* tp);
+
 template <class T> T node_phi(const Shape& sh, int idx, const T* yparent, const Smooth& sp) {
   const Node& n = sh.nodes[idx];
   T y[3];
-  T dx[3] = {yparent[0] - n.t[0], yparent[1] - n.t[1], yparent[2] - n.t[2]};
-  for (int i = 0; i < 3; ++i) y[i] = n.R[0 * 3 + i] * dx[0] + n.R[1 * 3 + i] * dx[1] + n.R[2 * 3 + i] * dx[2];
+  if (idx == g_pose_node) {   // the seeded node: its perturbed pose
+    T dt[3], w[3], Rp[9], tp[3];
+    for (int i = 0; i < 3; ++i) { dt[i] = pose_seed<T>(idx, i); w[i] = pose_seed<T>(idx, 3 + i); }
+    perturbed_pose(n.R, n.t, dt, w, Rp, tp);
+    T dx[3] = {yparent[0] - tp[0], yparent[1] - tp[1], yparent[2] - tp[2]};
+    for (int i = 0; i < 3; ++i) y[i] = Rp[0 * 3 + i] * dx[0] + Rp[1 * 3 + i] * dx[1] + Rp[2 * 3 + i] * dx[2];
+  } else {
+    T dx[3] = {yparent[0] - n.t[0], yparent[1] - n.t[1], yparent[2] - n.t[2]};
+    for (int i = 0; i < 3; ++i) y[i] = n.R[0 * 3 + i] * dx[0] + n.R[1 * 3 + i] * dx[1] + n.R[2 * 3 + i] * dx[2];
+  }
   switch (n.type) {
     case K_HALFSPACE: {
       T nv[3] = {pval<T>(n.pl[0][0][0], idx, 0), pval<T>(n.pl[0][0][1], idx, 1), pval<T>(n.pl[0][0][2], idx, 2)};
@@ -1253,6 +1273,43 @@ int ora_sdf_param_grad(void* s, const int* shape_ids, const double* poses, const
   }
   return 0;
 }
+
+// ---- node-pose derivatives of sdf_eval ---------------
+// J[n * nmax + 6 k + j] = d phi(point n) / d twist j of node k of the point's
+// shape (nodes in index order, every node incl. boolean ones and the root;
+// twist in the node's parent frame, slots dt_x, dt_y, dt_z, dtheta_x,
+// dtheta_y, dtheta_z, the convention of pose_seed above), zero beyond
+// 6 x the shape's node count; one Dual<double,1> evaluation per slot.
+int ora_sdf_node_pose_grad(void* s, const int* shape_ids, const double* poses, const double* points, long B, long P,
+                           int nmax, double* J) {
+  Scene* sc = (Scene*)s;
+  const Smooth& sp = sc->sp;
+  long total = B * P;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (long n = 0; n < total; ++n) {
+    const long b = n / P;
+    const Shape& sh = sc->shapes[shape_ids[b]];
+    const double* pz = poses + 8 * b;
+    double R[9], t[3] = {pz[0], pz[1], pz[2]};
+    double q[4] = {pz[3], pz[4], pz[5], pz[6]};
+    quat_to_R(q, R);
+    using D1 = Dual<double, 1>;
+    D1 X[3], Rj[9], tj[3];
+    for (int i = 0; i < 3; ++i) { X[i] = D1(points[3 * n + i]); tj[i] = D1(t[i]); }
+    for (int i = 0; i < 9; ++i) Rj[i] = D1(R[i]);
+    int k = 0;
+    for (int ni = 0; ni < (int)sh.nodes.size(); ++ni)
+      for (int slot = 0; slot < 6 && k < nmax; ++slot, ++k) {
+        g_pose_node = ni;
+        g_pose_slot = slot;
+        J[n * nmax + k] = shape_phi_world(sh, Rj, tj, X, sp).d[0];
+      }
+    g_pose_node = g_pose_slot = -1;
+    for (; k < nmax; ++k) J[n * nmax + k] = 0.0;
+  }
+  return 0;
+}
+int ora_shape_node_count(void* s, int shape) { return (int)((Scene*)s)->shapes[shape].nodes.size(); }
 
 // ---- second-order manifold derivatives (P:8 motivates
 // Hessians for second-order control) ----------------------------------------

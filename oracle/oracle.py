@@ -57,6 +57,9 @@ def lib():
         L.ora_shape_param_count.argtypes = [p, i]
         L.ora_shape_param_count.restype = i
         L.ora_sdf_param_grad.argtypes = [p, p, p, p, l, l, i, p]
+        L.ora_sdf_node_pose_grad.argtypes = [p, p, p, p, l, l, i, p]
+        L.ora_shape_node_count.argtypes = [p, i]
+        L.ora_shape_node_count.restype = i
         L.ora_max_threads.restype = i
         L.ora_shape_bound.argtypes = [p, i, p]
         L.ora_mesh_sphere.argtypes = [p, i, p]
@@ -279,6 +282,24 @@ class OracleScene:
         J = np.zeros((len(points), pmax))
         lib().ora_sdf_param_grad(self.h, _ptr(shape_ids), _ptr(poses), _ptr(points), len(shape_ids), P, int(pmax),
                                  _ptr(J))
+        return J
+
+    def node_count(self, shape):
+        """Number of SDF nodes of a shape (boolean nodes and leaves)."""
+        return lib().ora_shape_node_count(self.h, int(shape))
+
+    def sdf_node_pose_grad(self, shape_ids, poses, points, P, nmax=None):
+        """J [B*P, nmax]: d phi / d (node twists), 6 per node in node order
+        (dt, dtheta in the node's parent frame: R <- exp([dtheta]x) R,
+        t <- t + dt), zero-padded (f4 node poses, DESIGN reading #47)."""
+        shape_ids = np.ascontiguousarray(shape_ids, dtype=np.int32)
+        poses = np.ascontiguousarray(poses, dtype=np.float64).reshape(-1, 8)
+        points = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+        if nmax is None:
+            nmax = 6 * max(self.node_count(s) for s in np.unique(shape_ids))
+        J = np.zeros((len(points), nmax))
+        lib().ora_sdf_node_pose_grad(self.h, _ptr(shape_ids), _ptr(poses), _ptr(points), len(shape_ids), P,
+                                     int(nmax), _ptr(J))
         return J
 
     def manifold_d2depth(self, pairs=None, poses=None, n_threads=0, mode=0):
