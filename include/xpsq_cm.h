@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define CM_ABI_VERSION 3
+#define CM_ABI_VERSION 4
 #define CM_MAX_PLANES 8      /* half-spaces per PSQ / XPSQ cross-section      */
 #define CM_MAX_CHILDREN 32   /* children per boolean node                     */
 #define CM_MAX_DEPTH 3       /* nesting of boolean nodes in one shape         */
@@ -197,6 +197,30 @@ int cm_param_layout(const cm_scene* scene, int32_t* counts, int64_t* offsets);
  * SDF shape of the scene has count -1. */
 int cm_sdf_param_grad(const cm_scene* scene, const int32_t* shape_ids, const float* poses, const float* points,
                       int64_t B, int64_t P, int32_t pmax, float* J, const float* w, float* vjp, void* stream);
+
+/* ---- node-pose derivatives (DESIGN reading #47) ----------
+ * Node poses as shape parameters (fitting needs d/d shape; the paper
+ * defines no parametrisation): six slots per SDF node of shape s, for the
+ * nodes in the order of its description (every boolean node and leaf, the
+ * root included; a node unreachable from the root has zero slots' values):
+ * the twist (dt_x, dt_y, dt_z, dtheta_x, dtheta_y, dtheta_z) of the node's
+ * pose (R, t) in its PARENT's frame (the root's: the body frame) with the
+ * body poses' convention, R <- exp([dtheta]x) R and t <- t + dt, where
+ * x_parent = R x_node + t.  counts[s] (host, [n_shapes]) = 6 x the shape's
+ * node count, 0 without an SDF, -1 with more than 16 boolean nodes (not
+ * parametrised); offsets (host, [n_shapes + 1]) = prefix sums of
+ * max(count, 0).  Either may be NULL. */
+int cm_node_pose_layout(const cm_scene* scene, int32_t* counts, int64_t* offsets);
+/* For each point n (layout of cm_sdf_eval): J[k*N + n] = d phi(n) / d slot k
+ * of point n's shape for k < nmax (zero beyond 6 x its node count), and
+ * vjp[offsets[s] + k] += sum over the points n of shape s of w[n] J[k, n]
+ * (device, accumulated: zero it first; FP32 atomics, warp-reduced when a
+ * warp's points share one shape: the summation order is not fixed).  J or
+ * vjp may be NULL (not both; vjp needs w).  Invalid shape ids: NaN rows,
+ * counted in cm_scene_error_count.  CM_ERR_UNSUPPORTED when any SDF shape of
+ * the scene has count -1. */
+int cm_sdf_node_pose_grad(const cm_scene* scene, const int32_t* shape_ids, const float* poses, const float* points,
+                          int64_t B, int64_t P, int32_t nmax, float* J, const float* w, float* vjp, void* stream);
 
 /* ---- contact manifold ------------------------------------------------------
  * pairs[5*i ..]: {env, slotA, slotB, shapeA (sampled surface), shapeB (SDF)}

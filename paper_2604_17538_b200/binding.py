@@ -26,7 +26,7 @@ EXPORTS = ["cm_version", "cm_last_error", "cm_scene_create", "cm_scene_destroy",
            "cm_param_layout", "cm_sdf_param_grad",
            "cm_shape_topology", "cm_sdf_eval", "cm_manifold_size", "cm_manifold_offsets_workspace",
            "cm_manifold_offsets", "cm_contact_manifold", "cm_expand_jacobian", "cm_launch_count",
-           "cm_scene_error_count", "cm_manifold_pair_reduce"]
+           "cm_scene_error_count", "cm_manifold_pair_reduce", "cm_node_pose_layout", "cm_sdf_node_pose_grad"]
 
 
 class cm_node(C.Structure):
@@ -87,6 +87,9 @@ def lib():
             L.cm_scene_error_count.argtypes = [p, p, C.c_int]
         if hasattr(L, "cm_manifold_pair_reduce"):
             L.cm_manifold_pair_reduce.argtypes = [p, p, i64, p, u32, p, i64, p, p, p, p, p, p]
+        if hasattr(L, "cm_sdf_node_pose_grad"):
+            L.cm_node_pose_layout.argtypes = [p, p, p]
+            L.cm_sdf_node_pose_grad.argtypes = [p, p, p, p, i64, i64, i32, p, p, p, p]
         _lib = L
     return _lib
 
@@ -256,6 +259,31 @@ class Scene:
         vjp = torch.zeros(int(offs[-1]), device=dev, dtype=torch.float32) if w is not None else None
         _check(lib().cm_sdf_param_grad(self.h, _ptr(shape_ids), _ptr(poses), _ptr(points), shape_ids.shape[0], P,
                                        pmax, _ptr(J), _ptr(w), _ptr(vjp), _stream()), "cm_sdf_param_grad")
+        return J, vjp
+
+    # ---- node-pose derivatives (f4, reading #47) ----------------------------
+    def node_pose_layout(self):
+        """(counts [n_shapes] int32 = 6 x SDF nodes, offsets [n_shapes + 1]
+        int64) of the node-pose parameter vectors (-1: not parametrised)."""
+        n = len(self.shapes)
+        counts = np.zeros(n, np.int32)
+        offs = np.zeros(n + 1, np.int64)
+        _check(lib().cm_node_pose_layout(self.h, counts.ctypes.data_as(C.c_void_p),
+                                         offs.ctypes.data_as(C.c_void_p)), "cm_node_pose_layout")
+        return counts, offs
+
+    def sdf_node_pose_grad(self, shape_ids, poses, points, P: int, nmax: int = 0, w=None, want_J: bool = True):
+        """J [nmax, B*P] (d phi / d node twist, 6 per node) and, given w
+        [B*P], the vector-Jacobian product vjp [total] (CUDA tensors)."""
+        import torch
+        counts, offs = self.node_pose_layout()
+        nmax = nmax or int(max(counts.max(), 1))
+        N = shape_ids.shape[0] * P
+        dev = points.device
+        J = torch.empty(nmax, N, device=dev, dtype=torch.float32) if want_J else None
+        vjp = torch.zeros(int(offs[-1]), device=dev, dtype=torch.float32) if w is not None else None
+        _check(lib().cm_sdf_node_pose_grad(self.h, _ptr(shape_ids), _ptr(poses), _ptr(points), shape_ids.shape[0],
+                                           P, nmax, _ptr(J), _ptr(w), _ptr(vjp), _stream()), "cm_sdf_node_pose_grad")
         return J, vjp
 
     # ---- contact manifold ---------------------------------------------------

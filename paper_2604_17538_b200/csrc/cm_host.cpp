@@ -268,6 +268,9 @@ struct cm_scene {
   std::vector<int32_t> param_count;    // per shape (f4), -1: not parametrised
   std::vector<int64_t> param_off;      // prefix sums of max(count, 0)
   int64_t* param_off_dev = nullptr;
+  std::vector<int32_t> pose_count;     // per shape: 6 x its SDF nodes (f4 node poses), -1: not parametrised
+  std::vector<int64_t> pose_off;       // prefix sums of max(count, 0)
+  int64_t* pose_off_dev = nullptr;
   int class_mask = 0;  // bit c: SDF shapes of class c (0 SQ family, 1 XPSQ, 2 varying-schedule XPSQ)
   std::vector<void*> allocs;
   float* scratch = nullptr;
@@ -319,6 +322,7 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
   if (sp->trace_iters < 0 || sp->trace_iters > 64) return fail(CM_ERR_INVALID, "trace_iters out of range");
 
   std::vector<Instr> prog;
+  std::vector<NodeFrame> op_frames;   // parallel to prog (node-pose derivatives, f4)
   std::vector<Leaf> leaves;
   std::vector<Xpsq> xps;
   std::vector<ShapeRec> recs(n_shapes);
@@ -328,6 +332,7 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
   cm_scene* sc = new cm_scene;
   sc->device = device;
   sc->param_count.assign(n_shapes, 0);
+  sc->pose_count.assign(n_shapes, 0);
   sc->edges.resize(n_shapes);
   sc->face_edges.resize(n_shapes);
 
@@ -392,6 +397,14 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
       std::string err;
       std::vector<int> leaf_nodes;   // node index of each emitted leaf (program order)
       std::function<bool(int, float, const Frame&, int)> emit;
+      auto op_frame = [&](int k, const Frame& parent) {
+        NodeFrame nf;
+        std::memset(&nf, 0, sizeof(nf));
+        for (int i = 0; i < 9; ++i) nf.RP[i] = (float)parent.R[i];
+        for (int i = 0; i < 3; ++i) { nf.tP[i] = (float)parent.t[i]; nf.tk[i] = d.nodes[k].pose[i]; }
+        nf.node = k;
+        return nf;
+      };
       emit = [&](int k, float cs, const Frame& parent, int depth) -> bool {
         const cm_node& n = d.nodes[k];
         Frame fr = compose(parent, n.pose);
@@ -444,6 +457,7 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
             L.k = (float)(0.5 * e1);
           }
           prog.push_back(Instr{OP_LEAF, (int32_t)leaves.size(), cs, 1.f});
+          op_frames.push_back(op_frame(k, parent));
           leaves.push_back(L);
           leaf_nodes.push_back(k);
           return true;
@@ -454,11 +468,13 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
         }
         max_depth = std::max(max_depth, depth + 1);
         prog.push_back(Instr{OP_BEGIN, 0, 0.f, 0.f});
+        op_frames.push_back(op_frame(k, parent));
         for (int c = 0; c < n.n_children; ++c) {
           float s2 = n.type == CM_UNION ? -1.f : (n.type == CM_INTERSECTION ? 1.f : (c == 0 ? 1.f : -1.f));
           if (!emit(n.children[c], s2, fr, depth + 1)) return false;
         }
         prog.push_back(Instr{OP_END, 0, cs, n.type == CM_UNION ? -1.f : 1.f});
+        op_frames.push_back(op_frame(k, parent));
         return true;
       };
       Frame id;
@@ -489,6 +505,9 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
       // node-index order the layout promises (true for pre-order node lists)
       if (!std::is_sorted(leaf_nodes.begin(), leaf_nodes.end())) pc = -1;
       sc->param_count[s] = pc;
+      // node poses: six slots per node (the kernel writes them by the node
+      // index of each op, so any node order is parametrised)
+      sc->pose_count[s] = n_bool > cmi::kParamMaxNodes ? -1 : 6 * d.n_nodes;
     }
     r.prog_len = (int32_t)prog.size() - r.prog_begin;
 
@@ -591,6 +610,8 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
   SceneDev& D = sc->dev;
   std::memset(&D, 0, sizeof(D));
   D.prog = dev_copy(prog, rc);
+  D.op_frames = dev_copy(op_frames, rc);
+  if (D.op_frames) sc->allocs.push_back(const_cast<NodeFrame*>(D.op_frames));
   D.leaves = dev_copy(leaves, rc);
   D.xpsq = dev_copy(xps, rc);
   D.shapes = dev_copy(recs, rc);
@@ -614,6 +635,10 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
   for (int s = 0; s < n_shapes; ++s) sc->param_off[s + 1] = sc->param_off[s] + std::max(sc->param_count[s], 0);
   sc->param_off_dev = dev_copy(sc->param_off, rc);
   if (sc->param_off_dev) sc->allocs.push_back(sc->param_off_dev);
+  sc->pose_off.assign(n_shapes + 1, 0);
+  for (int s = 0; s < n_shapes; ++s) sc->pose_off[s + 1] = sc->pose_off[s] + std::max(sc->pose_count[s], 0);
+  sc->pose_off_dev = dev_copy(sc->pose_off, rc);
+  if (sc->pose_off_dev) sc->allocs.push_back(sc->pose_off_dev);
   {   // error word of the device-side record validation (cm_scene_error_count)
     std::vector<unsigned int> zero(4, 0u);
     D.err = dev_copy(zero, rc);
@@ -752,6 +777,35 @@ int cm_sdf_param_grad(const cm_scene* sc, const int32_t* ids, const float* poses
       return fail(CM_ERR_UNSUPPORTED, "cm_sdf_param_grad: shape " + std::to_string(s) +
                                            " has more than 16 boolean nodes or leaves out of depth-first order (not parametrised)");
   int rc = cml::launch_sdf_param_grad(sc->dev, ids, poses, points, B, P, pmax, J, w, vjp, sc->param_off_dev, stream);
+  if (rc) return fail(rc, cml::last_cuda_error());
+  return CM_OK;
+}
+
+int cm_node_pose_layout(const cm_scene* sc, int32_t* counts, int64_t* offsets) {
+  if (!sc) return fail(CM_ERR_INVALID, "cm_node_pose_layout: NULL scene");
+  const int ns = (int)sc->pose_count.size();
+  for (int s = 0; s < ns; ++s) {
+    if (counts) counts[s] = sc->pose_count[s];
+    if (offsets) offsets[s] = sc->pose_off[s];
+  }
+  if (offsets) offsets[ns] = sc->pose_off[ns];
+  return CM_OK;
+}
+
+int cm_sdf_node_pose_grad(const cm_scene* sc, const int32_t* ids, const float* poses, const float* points, int64_t B,
+                          int64_t P, int32_t nmax, float* J, const float* w, float* vjp, void* stream) {
+  NvtxRange nvtx_range("cm_sdf_node_pose_grad");
+  if (!sc) return fail(CM_ERR_INVALID, "cm_sdf_node_pose_grad: NULL scene");
+  if (B < 0 || P < 0 || nmax < 0) return fail(CM_ERR_INVALID, "cm_sdf_node_pose_grad: negative size");
+  if (B == 0 || P == 0) return CM_OK;
+  if (!ids || !poses || !points || (!J && !vjp) || (vjp && !w))
+    return fail(CM_ERR_INVALID, "cm_sdf_node_pose_grad: NULL argument");
+  if (((uintptr_t)poses & 15) != 0) return fail(CM_ERR_INVALID, "cm_sdf_node_pose_grad: poses must be 16-byte aligned");
+  for (size_t s = 0; s < sc->pose_count.size(); ++s)
+    if (sc->pose_count[s] < 0)
+      return fail(CM_ERR_UNSUPPORTED, "cm_sdf_node_pose_grad: shape " + std::to_string(s) +
+                                           " has more than 16 boolean nodes (not parametrised)");
+  int rc = cml::launch_sdf_node_pose_grad(sc->dev, ids, poses, points, B, P, nmax, J, w, vjp, sc->pose_off_dev, stream);
   if (rc) return fail(rc, cml::last_cuda_error());
   return CM_OK;
 }

@@ -101,8 +101,21 @@ struct SmoothDev {
 };
 
 // everything a kernel needs to evaluate any shape of the scene
+// node-pose derivatives (f4, reading #47): per program op (BEGIN / LEAF; END
+// unused) the node's index in its shape description, the composed frame of
+// its parent in the shape frame (x_shape = RP x_parent + tP) and the node's
+// own pose translation tk (in the parent frame)
+struct alignas(16) NodeFrame {
+  float RP[9];
+  float tP[3];
+  float tk[3];
+  int32_t node;
+};
+static_assert(sizeof(NodeFrame) == 64, "NodeFrame: 64 B");
+
 struct SceneDev {
   const Instr* prog;
+  const NodeFrame* op_frames; // parallel to prog
   const Leaf* leaves;
   const Xpsq* xpsq;
   const ShapeRec* shapes;
@@ -155,6 +168,9 @@ int64_t manifold_slot_floats(int V, int E, int tier);
 int launch_pair_reduce(const cmi::SceneDev& s, const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,
                        uint32_t flags, const cm_manifold_out* out, int64_t C, const float* w_depth,
                        const float* w_normal, float* pair_depth, float* pair_W, float* g_pose, void* stream);
+int launch_sdf_node_pose_grad(const cmi::SceneDev& s, const int32_t* ids, const float* poses, const float* pts,
+                              int64_t B, int64_t P, int32_t nmax, float* J, const float* w, float* vjp,
+                              const int64_t* noff, void* stream);
 int launch_sdf_param_grad(const cmi::SceneDev& s, const int32_t* ids, const float* poses, const float* pts, int64_t B,
                           int64_t P, int32_t pmax, float* J, const float* w, float* vjp, const int64_t* poff,
                           void* stream);

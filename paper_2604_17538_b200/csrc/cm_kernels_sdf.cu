@@ -888,9 +888,173 @@ __global__ void __launch_bounds__(256) k_sdf_param_grad(SceneDev S, const int32_
   }
 }
 
+
+// ---- node-pose derivatives (f4, reading #47) --------------------------------
+// d phi / d twist of node k (in its parent frame P, x_shape = RP x_P + tP):
+// phi depends on the node's pose only through the node's own SDF phi_k, which
+// the twist moves rigidly about the node origin tk (in P), so
+//   d phi / d dt = -f_k gP,  d phi / d dtheta = f_k gP x (xP - tk),
+// f_k = d phi / d phi_k (through the enclosing LSEs, Eqs. (2)-(4)),
+// gP = RP^T grad phi_k(x), xP = RP^T (x - tP).
+template <class Emit>
+__device__ __forceinline__ void node_twist(const NodeFrame& nf, const float* y, float fac, const float* g,
+                                           Emit emit) {
+  float gP[3], xr[3];
+  const float d[3] = {y[0] - nf.tP[0], y[1] - nf.tP[1], y[2] - nf.tP[2]};
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    gP[i] = nf.RP[i] * g[0] + nf.RP[3 + i] * g[1] + nf.RP[6 + i] * g[2];
+    xr[i] = nf.RP[i] * d[0] + nf.RP[3 + i] * d[1] + nf.RP[6 + i] * d[2] - nf.tk[i];
+  }
+  const int b = 6 * nf.node;
+  emit(b + 0, -fac * gP[0]);
+  emit(b + 1, -fac * gP[1]);
+  emit(b + 2, -fac * gP[2]);
+  emit(b + 3, fac * (gP[1] * xr[2] - gP[2] * xr[1]));
+  emit(b + 4, fac * (gP[2] * xr[0] - gP[0] * xr[2]));
+  emit(b + 5, fac * (gP[0] * xr[1] - gP[1] * xr[0]));
+}
+
+// one thread per point (the layout of k_sdf_param_grad): pass 1 evaluates the
+// shape program at order 1 keeping every boolean node's accumulator (max,
+// sum), its folded value and the gradient of its own value; pass 2 walks the
+// program again with the factors d phi / d phi_node down the tree and emits
+// each node's six slots (boolean nodes at their BEGIN, leaves with their
+// order-1 evaluation)
+__global__ void __launch_bounds__(256) k_sdf_node_pose_grad(SceneDev S, const int32_t* __restrict__ shape_ids,
+                                                            const float* __restrict__ poses,
+                                                            const float* __restrict__ points, int64_t B, int64_t P,
+                                                            int32_t nmax, float* __restrict__ J,
+                                                            const float* __restrict__ w, float* __restrict__ vjp,
+                                                            const int64_t* __restrict__ noff) {
+  const int64_t N = B * P;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < N; base += stride) {
+    const int64_t n = base + lane;
+    const bool valid = n < N;
+    const int64_t b = valid ? n / P : 0;
+    const int sid = valid ? __ldg(shape_ids + b) : -1;
+    const int sid0 = __shfl_sync(0xffffffffu, sid, 0);
+    const bool uni = __all_sync(0xffffffffu, valid && sid == sid0);
+    if (!valid) continue;
+    if ((unsigned)sid >= (unsigned)S.n_shapes || !S.shapes[sid].has_sdf) {
+      if (J)
+        for (int k = 0; k < nmax; ++k) J[(int64_t)k * N + n] = __int_as_float(0x7fc00000);
+      atomicAdd(S.err, 1u);
+      continue;
+    }
+    const ShapeRec sh = S.shapes[sid];
+    const float4 pa = __ldg(reinterpret_cast<const float4*>(poses) + 2 * b);
+    const float4 pb = __ldg(reinterpret_cast<const float4*>(poses) + 2 * b + 1);
+    const float t[3] = {pa.x, pa.y, pa.z};
+    const float q[4] = {pa.w, pb.x, pb.y, pb.z};
+    float R[9];
+    quat_to_R(q, R);
+    const float x[3] = {__ldg(points + 3 * n), __ldg(points + 3 * n + 1), __ldg(points + 3 * n + 2)};
+    float y[3];
+    to_local(R, t, x, y);
+    const float wn = vjp ? __ldg(w + n) : 0.f;
+    const int64_t off = vjp ? __ldg(noff + sid) : 0;
+    // slots of nodes the program does not reach stay zero
+    if (J)
+      for (int k = 0; k < nmax; ++k) J[(int64_t)k * N + n] = 0.f;
+    auto emit = [&](int kk, float v) {
+      if (J && kk < nmax) J[(int64_t)kk * N + n] = v;
+      if (vjp) {
+        float s = wn * v;
+        if (uni) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+          if (lane == 0) atomicAdd(vjp + off + kk, s);
+        } else {
+          atomicAdd(vjp + off + kk, s);
+        }
+      }
+    };
+    const Instr* prog = S.prog + sh.prog_begin;
+    const NodeFrame* nfr = S.op_frames + sh.prog_begin;
+    if (sh.prog_len == 1) {
+      Res<1> r;
+      leaf_eval<1, 2, false>(S, prog[0].idx, y, r);
+      node_twist(nfr[0], y, 1.f, r.g, emit);
+      continue;
+    }
+    const float tau = S.sp.tau_min, itau = S.sp.i_min, itl = LOG2E * itau;
+    float nm[kParamMaxNodes], nz[kParamMaxNodes], nfv[kParamMaxNodes], nos[kParamMaxNodes], ncs[kParamMaxNodes];
+    float ng[kParamMaxNodes][3];
+    int stk[CM_MAX_DEPTH + 1];
+    Acc<1> acc[CM_MAX_DEPTH + 1];
+    int lvl = -1, nn = 0;
+    for (int pc = 0; pc < sh.prog_len; ++pc) {   // pass 1: node accumulators and gradients
+      const Instr in = prog[pc];
+      if (in.op == OP_BEGIN) {
+        ++lvl;
+        stk[lvl] = nn++;
+        acc_init(acc[lvl]);
+        continue;
+      }
+      Res<1> r;
+      if (in.op == OP_LEAF) {
+        leaf_eval<1, 2, false>(S, in.idx, y, r);
+      } else {   // OP_END: the node's own value and gradient
+        const int k = stk[lvl];
+        nm[k] = acc[lvl].m;
+        nz[k] = acc[lvl].S;
+        nos[k] = in.out_sign;
+        ncs[k] = in.child_sign;
+        acc_final(acc[lvl], in.out_sign, tau, itau, r);
+        nfv[k] = in.child_sign * r.v;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) ng[k][i] = r.g[i];
+        --lvl;
+      }
+      if (lvl >= 0) acc_fold(acc[lvl], in.child_sign, r, itl, itau);
+    }
+    float fac[CM_MAX_DEPTH + 1];
+    lvl = -1;
+    nn = 0;
+    for (int pc = 0; pc < sh.prog_len; ++pc) {   // pass 2: factors down the tree, six slots per node
+      const Instr in = prog[pc];
+      if (in.op == OP_BEGIN) {
+        const int k = nn++;
+        if (lvl < 0) {
+          fac[0] = 1.f;
+        } else {   // d phi_parent / d phi_k = s_parent s_k softmax_parent(k)
+          const int p = stk[lvl];
+          fac[lvl + 1] = fac[lvl] * nos[p] * ncs[k] * ex2((nfv[k] - nm[p]) * itl) * rcpa(nz[p]);
+        }
+        stk[++lvl] = k;
+        node_twist(nfr[pc], y, fac[lvl], ng[k], emit);
+        continue;
+      }
+      if (in.op == OP_END) { --lvl; continue; }
+      const int k = stk[lvl];
+      Res<1> r;
+      leaf_eval<1, 2, false>(S, in.idx, y, r);
+      const float sc = fac[lvl] * nos[k] * in.child_sign * ex2((in.child_sign * r.v - nm[k]) * itl) * rcpa(nz[k]);
+      node_twist(nfr[pc], y, sc, r.g, emit);
+    }
+  }
+}
+
 }  // namespace
 
 namespace cml {
+
+int launch_sdf_node_pose_grad(const SceneDev& s, const int32_t* ids, const float* poses, const float* pts, int64_t B,
+                              int64_t P, int32_t nmax, float* J, const float* w, float* vjp, const int64_t* noff,
+                              void* stream) {
+  const int threads = 256;
+  const int64_t N = B * P;
+  int64_t blocks = (N + threads - 1) / threads;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  k_sdf_node_pose_grad<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(s, ids, poses, pts, B, P, nmax, J, w,
+                                                                               vjp, noff);
+  return check_launch("k_sdf_node_pose_grad");
+}
 
 int launch_sdf_param_grad(const SceneDev& s, const int32_t* ids, const float* poses, const float* pts, int64_t B,
                           int64_t P, int32_t pmax, float* J, const float* w, float* vjp, const int64_t* poff,

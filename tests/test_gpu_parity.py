@@ -521,6 +521,76 @@ def test_sdf_param_grad_unsupported(cuda):
                          torch.zeros(4, 3, device="cuda"), 4, 4)
 
 
+def test_sdf_node_pose_grad_parity(cuda, oracle_mod):
+    """Node poses as shape parameters (DESIGN reading #47):
+    per-point d phi / d twist of every node (boolean nodes, leaves, the root)
+    of the parameter scene against the oracle's node-pose seeds, and the
+    vector-Jacobian product against J^T w."""
+    import torch
+    from paper_2604_17538_b200 import binding
+    shapes, rng = _param_scene()
+    sc = scene_of(shapes, ell=0.1)
+    S = binding.Scene(sc.shapes, sc.smooth)
+    counts, offs = S.node_pose_layout()
+    osc = oracle_mod.OracleScene(sc)
+    assert [6 * osc.node_count(s) for s in range(len(shapes))] == list(counts)
+    B, P = 4 * len(shapes), 96
+    ids = np.repeat(np.arange(len(shapes)), B // len(shapes)).astype(np.int32)
+    poses = np.stack([synth.pose_row(rng.uniform(-0.1, 0.1, 3), synth.random_quats(rng, 1)[0]) for _ in range(B)])
+    poses = poses.astype(np.float32)
+    pts = (poses[:, None, :3] + rng.normal(size=(B, P, 3)) * 0.05).reshape(-1, 3).astype(np.float32)
+    w = rng.normal(size=B * P).astype(np.float32)
+    nmax = int(counts.max())
+    J, vjp = S.sdf_node_pose_grad(torch.from_numpy(ids).cuda(), torch.from_numpy(poses).cuda(),
+                                  torch.from_numpy(pts).cuda(), P, nmax, w=torch.from_numpy(w).cuda())
+    torch.cuda.synchronize()
+    Jg = J.cpu().numpy().T
+    Jr = osc.sdf_node_pose_grad(ids, poses, pts, P, nmax)
+    Jp = osc.sdf_node_pose_grad(ids, PT.perturb_inputs(np.random.default_rng(53), poses), pts, P, nmax)
+    rep = []
+    nf = PT.compare("J", Jg, Jr, Jp, PT.tol_vec(Jr, 1), rep)
+    ref_vjp = np.zeros(int(offs[-1]))
+    bound = np.zeros_like(ref_vjp)
+    floor = np.zeros_like(ref_vjp)
+    tolJ = PT.tol_vec(Jr, 1)[:, 0]
+    for n in range(B * P):
+        s = ids[n // P]
+        ref_vjp[offs[s]:offs[s] + counts[s]] += w[n] * Jr[n, :counts[s]]
+        bound[offs[s]:offs[s] + counts[s]] += np.abs(w[n] * Jr[n, :counts[s]])
+        floor[offs[s]:offs[s] + counts[s]] += 1e-3 * abs(w[n]) * tolJ[n]
+    nf += PT.compare("vjp", vjp.cpu().numpy(), ref_vjp, ref_vjp, 1e-4 * bound + floor, rep)
+    _report("sdf_node_pose_grad", rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+    assert PT.excluded_fraction(rep) < 0.01
+    # the root's translation slots are the negated body gradient: a check of
+    # the kernel against its own sdf_eval (rows of boolean-rooted shapes too)
+    o = S.sdf_eval(torch.from_numpy(ids).cuda(), torch.from_numpy(poses).cuda(), torch.from_numpy(pts).cuda(), P,
+                   binding.SDF_VALUE | binding.SDF_GRAD)
+    torch.cuda.synchronize()
+    g = o["grad"].cpu().numpy().T                       # world gradient
+    R = synth.quats_to_mats(poses[:, 3:7].astype(np.float64))
+    gb = np.einsum("bji,bpj->bpi", R, g.reshape(B, P, 3)).reshape(-1, 3)   # body frame
+    assert np.allclose(Jg[:, 0:3], -gb, atol=2e-4 * max(1.0, np.abs(gb).max()))
+
+
+def test_sdf_node_pose_grad_unsupported(cuda):
+    """More boolean nodes than the kernel tracks (17 > 16): count -1, refused."""
+    import torch
+    from paper_2604_17538_b200 import binding
+    big = synth.op("union", [synth.op("union", [synth.sq((0.01, 0.01, 0.01), (1, 1), pose=[0.02 * i, 0, 0, 1, 0, 0, 0]),
+                                                synth.sq((0.01, 0.01, 0.01), (1, 1), pose=[0.02 * i, 0.02, 0, 1, 0, 0, 0])])
+                             for i in range(16)])
+    sc = scene_of([synth.make_shape("big", big, None)], ell=0.04)
+    S = binding.Scene(sc.shapes, sc.smooth)
+    counts, _ = S.node_pose_layout()
+    assert counts[0] == -1
+    z = torch.zeros(1, 8, device="cuda")
+    z[0, 3] = 1
+    with pytest.raises(binding.CMError):
+        S.sdf_node_pose_grad(torch.zeros(1, dtype=torch.int32, device="cuda"), z,
+                             torch.zeros(4, 3, device="cuda"), 4, 6)
+
+
 def test_sdf_eval_xpsq_soft_cardano_band(cuda, oracle_mod):
     """Points inside the soft-Cardano band 10 tau_Delta < |Delta| < 46
     tau_Delta of a curved XPSQ (both branches blended): every
