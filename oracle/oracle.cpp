@@ -540,8 +540,19 @@ T xpsq_phi_s(const Node& n, const XS<S>& xs, const T* y, const Smooth& sp, int i
 // then (n_x, n_y, n_z, h) per plane.
 // ---------------------------------------------------------------------------
 thread_local int g_seed_node = -1, g_seed_slot = -1;
+// manifold shape-parameter derivatives (f4, reading #48): with this flag set
+// the manifold's pose jets are not seeded and the shape parameter named by
+// g_seed takes their component 0 (the first-order q-jet D12 and the nested
+// candidate jet N12 = Dual<D3, 12>), so ddepth[., 0] = d depth / d param
+thread_local bool g_param_comp0 = false;
 template <class T> struct Seeder { static void apply(T&) {} };
 template <> struct Seeder<Dual<double, 1>> { static void apply(Dual<double, 1>& x) { x.d[0] = 1.0; } };
+template <> struct Seeder<Dual<double, 12>> {
+  static void apply(Dual<double, 12>& x) { if (g_param_comp0) x.d[0] = 1.0; }
+};
+template <> struct Seeder<Dual<Dual<double, 3>, 12>> {
+  static void apply(Dual<Dual<double, 3>, 12>& x) { if (g_param_comp0) x.d[0].v = 1.0; }
+};
 template <class T> T pval(double v, int node, int slot) {
   T x(v);
   if (node == g_seed_node && slot == g_seed_slot) Seeder<T>::apply(x);
@@ -1036,10 +1047,12 @@ int ora_contact_manifold(void* s, const int* pairs, long n_pairs, const double* 
     const int sA = side ? 6 : 0, sB = side ? 0 : 6;
     D12 dtA[3], wA[3], dtB[3], wB[3];
     for (int i = 0; i < 3; ++i) {
-      dtA[i] = D12(0.0); dtA[i].d[sA + i] = 1.0;
-      wA[i] = D12(0.0); wA[i].d[sA + 3 + i] = 1.0;
-      dtB[i] = D12(0.0); dtB[i].d[sB + i] = 1.0;
-      wB[i] = D12(0.0); wB[i].d[sB + 3 + i] = 1.0;
+      dtA[i] = D12(0.0); wA[i] = D12(0.0); dtB[i] = D12(0.0); wB[i] = D12(0.0);
+      if (g_param_comp0) continue;   // (shape-parameter mode: component 0 carries the parameter)
+      dtA[i].d[sA + i] = 1.0;
+      wA[i].d[sA + 3 + i] = 1.0;
+      dtB[i].d[sB + i] = 1.0;
+      wB[i].d[sB + 3 + i] = 1.0;
     }
     // J_i rows are v_sampled - v_sdf; written in the pair's (A, B) columns
     const double sg = side ? -1.0 : 1.0;
@@ -1310,6 +1323,52 @@ int ora_sdf_node_pose_grad(void* s, const int* shape_ids, const double* poses, c
   return 0;
 }
 int ora_shape_node_count(void* s, int shape) { return (int)((Scene*)s)->shapes[shape].nodes.size(); }
+
+// ---- shape-parameter derivatives of the manifold depth (
+// reading #48) -----------------------------------------------------------
+// Jd[row * pmax + k] = d depth(row) / d parameter k of the pair's SDF shape B
+// (the layout of ora_sdf_param_grad), one-sided modes (reduced or full): the
+// literal manifold of ora_contact_manifold with the parameter seeded in
+// component 0 of its jets (g_param_comp0), one evaluation per pair and slot.
+int ora_manifold_param_jac(void* s, const int* pairs, long n_pairs, const double* poses, long n_env, int n_slot,
+                           int mode, int pmax, double* Jd) {
+  Scene* sc = (Scene*)s;
+  if (mode & (8 | 16)) return -1;   // two-sided / broad phase: not parametrised here
+  const bool full = (mode & 4) != 0;
+  std::vector<long> off(n_pairs + 1, 0);
+  for (long i = 0; i < n_pairs; ++i) {
+    const Mesh& m = sc->shapes[pairs[5 * i + 3]].mesh;
+    off[i + 1] = off[i] + (full ? (long)m.V + m.E : (long)m.F);
+  }
+#pragma omp parallel for schedule(dynamic, 1)
+  for (long pi = 0; pi < n_pairs; ++pi) {
+    const long nr = off[pi + 1] - off[pi];
+    std::vector<double> pt(3 * nr), nm(3 * nr), dp(nr), W(nr), q(3 * nr), dd(12 * nr), dn(36 * nr), J(36 * nr),
+        z(6 * nr), dc(6 * nr), g(6 * nr);
+    std::vector<int> dom(nr);
+    const Shape& SB = sc->shapes[pairs[5 * pi + 4]];
+    int k = 0;
+    for (int ni = 0; ni < (int)SB.nodes.size(); ++ni) {
+      const int cnt = node_param_count(SB.nodes[ni]);
+      for (int slot = 0; slot < cnt && k < pmax; ++slot, ++k) {
+        g_seed_node = ni;
+        g_seed_slot = slot;
+        g_param_comp0 = true;
+        // (nested inside this parallel loop the manifold's own loop runs on
+        // this thread, which holds the thread-local seeds)
+        ora_contact_manifold(s, pairs + 5 * pi, 1, poses, n_env, n_slot, pt.data(), nm.data(), dp.data(), W.data(),
+                             q.data(), dd.data(), dn.data(), dom.data(), J.data(), z.data(), dc.data(), g.data(),
+                             mode, 0);
+        g_param_comp0 = false;
+        for (long r = 0; r < nr; ++r) Jd[(off[pi] + r) * pmax + k] = dd[12 * r + 0];
+      }
+    }
+    g_seed_node = g_seed_slot = -1;
+    for (; k < pmax; ++k)
+      for (long r = 0; r < nr; ++r) Jd[(off[pi] + r) * pmax + k] = 0.0;
+  }
+  return 0;
+}
 
 // ---- second-order manifold derivatives (P:8 motivates
 // Hessians for second-order control) ----------------------------------------

@@ -58,6 +58,7 @@ def lib():
         L.ora_shape_param_count.restype = i
         L.ora_sdf_param_grad.argtypes = [p, p, p, p, l, l, i, p]
         L.ora_sdf_node_pose_grad.argtypes = [p, p, p, p, l, l, i, p]
+        L.ora_manifold_param_jac.argtypes = [p, p, l, p, l, i, i, i, p]
         L.ora_shape_node_count.argtypes = [p, i]
         L.ora_shape_node_count.restype = i
         L.ora_max_threads.restype = i
@@ -301,6 +302,27 @@ class OracleScene:
         lib().ora_sdf_node_pose_grad(self.h, _ptr(shape_ids), _ptr(poses), _ptr(points), len(shape_ids), P,
                                      int(nmax), _ptr(J))
         return J
+
+    def manifold_param_jac(self, pairs=None, poses=None, mode=0, pmax=None):
+        """Jd [rows, pmax]: d depth(row) / d shape parameter of the pair's SDF
+        shape B (one-sided modes; the layout of sdf_param_grad), from the
+        literal manifold with the parameter seeded (f4, reading #48)."""
+        sc = self.scene
+        pairs = np.ascontiguousarray(sc.pairs if pairs is None else pairs, dtype=np.int32)
+        poses = np.ascontiguousarray(sc.poses if poses is None else poses, dtype=np.float64)
+        n_env, n_slot = poses.shape[0], poses.shape[1]
+        if pmax is None:
+            pmax = max(self.param_count(int(b)) for b in np.unique(pairs[:, 4]))
+        full = bool(mode & 4)
+        rows = 0
+        for a in pairs[:, 3]:
+            V, E, F = self.mesh_counts(int(a))
+            rows += V + E if full else F
+        Jd = np.zeros((rows, pmax))
+        rc = lib().ora_manifold_param_jac(self.h, _ptr(pairs), len(pairs), _ptr(poses), n_env, n_slot, int(mode),
+                                          int(pmax), _ptr(Jd))
+        assert rc == 0, "one-sided modes only"
+        return Jd
 
     def manifold_d2depth(self, pairs=None, poses=None, n_threads=0, mode=0):
         """d^2 depth / dq^2 per contact (packed upper triangle, 78 per row, q in
