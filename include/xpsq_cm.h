@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define CM_ABI_VERSION 4
+#define CM_ABI_VERSION 5
 #define CM_MAX_PLANES 8      /* half-spaces per PSQ / XPSQ cross-section      */
 #define CM_MAX_CHILDREN 32   /* children per boolean node                     */
 #define CM_MAX_DEPTH 3       /* nesting of boolean nodes in one shape         */
@@ -309,6 +309,24 @@ int cm_contact_manifold(const cm_scene* scene, const int32_t* pairs, int64_t n_p
 int cm_expand_jacobian(const cm_scene* scene, const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,
                        const float* poses, int64_t n_env, int32_t n_slot, uint32_t flags, const float* W,
                        const float* q, int64_t n_contacts, float* J, void* stream);
+
+/* Shape-parameter vector-Jacobian product of the manifold depths (SURVEY
+ * §8f row f4 "reverse-mode VJPs"; DESIGN reading #48): vjp[po[s] + k] +=
+ * sum over the rows r of every pair whose SDF shape is s of
+ * w_depth[r] d depth_r / d theta_k, theta = the parameters of shape s in the
+ * cm_param_layout order (po its offsets).  Everything the manifold derives
+ * from phi_s is differentiated: the candidate values, the sphere-trace
+ * iterates and soft clips, the edge points and the face softmax
+ * (P:158-161); the sampled surface is data.  pairs / offsets / poses /
+ * n_env / n_slot as for cm_contact_manifold with the same flags; one-sided
+ * modes only (reduced, or CM_FULL_MODE: the rows' candidate depths), else
+ * CM_ERR_UNSUPPORTED (also when a shape is not parametrised, or with more
+ * than 16 trace iterations).  w_depth [C] and vjp (accumulated: zero it
+ * first; FP32 atomics, order not fixed) are device pointers.  Invalid pair
+ * records are skipped (counted by cm_contact_manifold's validation rules). */
+int cm_manifold_param_vjp(const cm_scene* scene, const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,
+                          const float* poses, int64_t n_env, int32_t n_slot, uint32_t flags, const float* w_depth,
+                          float* vjp, void* stream);
 
 /* Pair-level reductions of a manifold computed with the same mode bits
  * (`flags`; rows of pair i at [offsets[i], offsets[i] + its contact count)),

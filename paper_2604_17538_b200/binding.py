@@ -26,7 +26,8 @@ EXPORTS = ["cm_version", "cm_last_error", "cm_scene_create", "cm_scene_destroy",
            "cm_param_layout", "cm_sdf_param_grad",
            "cm_shape_topology", "cm_sdf_eval", "cm_manifold_size", "cm_manifold_offsets_workspace",
            "cm_manifold_offsets", "cm_contact_manifold", "cm_expand_jacobian", "cm_launch_count",
-           "cm_scene_error_count", "cm_manifold_pair_reduce", "cm_node_pose_layout", "cm_sdf_node_pose_grad"]
+           "cm_scene_error_count", "cm_manifold_pair_reduce", "cm_node_pose_layout", "cm_sdf_node_pose_grad",
+           "cm_manifold_param_vjp"]
 
 
 class cm_node(C.Structure):
@@ -90,6 +91,8 @@ def lib():
         if hasattr(L, "cm_sdf_node_pose_grad"):
             L.cm_node_pose_layout.argtypes = [p, p, p]
             L.cm_sdf_node_pose_grad.argtypes = [p, p, p, p, i64, i64, i32, p, p, p, p]
+        if hasattr(L, "cm_manifold_param_vjp"):
+            L.cm_manifold_param_vjp.argtypes = [p, p, i64, p, p, i64, i32, u32, p, p, p]
         _lib = L
     return _lib
 
@@ -285,6 +288,19 @@ class Scene:
         _check(lib().cm_sdf_node_pose_grad(self.h, _ptr(shape_ids), _ptr(poses), _ptr(points), shape_ids.shape[0],
                                            P, nmax, _ptr(J), _ptr(w), _ptr(vjp), _stream()), "cm_sdf_node_pose_grad")
         return J, vjp
+
+    def manifold_param_vjp(self, pairs, offsets, poses, w_depth, mode: int = 0):
+        """vjp [n_params_total] (cm_param_layout order) = sum_rows w_depth
+        d depth / d theta of each pair's SDF shape (one-sided modes; CUDA
+        tensors in, a new zeroed-then-accumulated CUDA tensor out)."""
+        import torch
+        _, offs = self.param_layout()
+        vjp = torch.zeros(int(offs[-1]), device=poses.device, dtype=torch.float32)
+        n_env, n_slot = poses.shape[0], poses.shape[1]
+        _check(lib().cm_manifold_param_vjp(self.h, _ptr(pairs), pairs.shape[0], _ptr(offsets), _ptr(poses), n_env,
+                                           n_slot, mode, _ptr(w_depth), _ptr(vjp), _stream()),
+               "cm_manifold_param_vjp")
+        return vjp
 
     # ---- contact manifold ---------------------------------------------------
     def manifold_size(self, pairs_host: np.ndarray, mode: int = 0) -> int:

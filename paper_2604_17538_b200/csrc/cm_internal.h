@@ -168,6 +168,10 @@ int64_t manifold_slot_floats(int V, int E, int tier);
 int launch_pair_reduce(const cmi::SceneDev& s, const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,
                        uint32_t flags, const cm_manifold_out* out, int64_t C, const float* w_depth,
                        const float* w_normal, float* pair_depth, float* pair_W, float* g_pose, void* stream);
+int launch_manifold_param_vjp(const cmi::SceneDev& s, int max_V, int max_E, int pmax, const int32_t* pairs,
+                              int64_t n_pairs, const int64_t* offsets, const float* poses, int64_t n_env,
+                              int32_t n_slot, uint32_t mode, const float* w, float* vjp, const int64_t* poff,
+                              void* stream);
 int launch_sdf_node_pose_grad(const cmi::SceneDev& s, const int32_t* ids, const float* poses, const float* pts,
                               int64_t B, int64_t P, int32_t nmax, float* J, const float* w, float* vjp,
                               const int64_t* noff, void* stream);

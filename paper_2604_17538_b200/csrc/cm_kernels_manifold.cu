@@ -15,9 +15,11 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstring>
 
 #include "cm_device.cuh"
 #include "cm_internal.h"
+#include "cm_param.cuh"
 #include "cm_launch.h"
 
 using namespace cmi;
@@ -1533,6 +1535,196 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS, TIER >= 3 ? 1 : CM_MF_FACE_
   if (list_unit(a, -1, U, u) && U.valid) mf_faces_unit<TIER, STAGED>(a, U, u, fsm, &bar, 0u);
 }
 
+// ---- shape-parameter VJP of the manifold depths (f4, reading #48) ----------
+// vjp[poff[B] + k] += sum_rows w_r d depth_r / d theta_k for the parameters
+// theta of the pair's SDF shape B (one-sided units; the sampled surface is
+// data).  One CTA per unit, the manifold re-derived in B's frame:
+//   forward  vertices phi_B(x_v); both traces of every edge (alpha_{k+1} =
+//            alpha_k + sgn G(phi(x_k)), G(phi) = sigma(phi/tau) phi, the corner
+//            iterate at the vertex), soft clips, the midpoint candidate
+//            phi_B(x_e) and d phi / d alpha_bar = grad phi . e_B;
+//   rows     reduced: depth = -tau LSE(-d_i / tau) over the face's six
+//            candidates, so the candidate adjoints are dbar_i = sum_faces
+//            w_f z_i (shared-memory atomics); full: dbar = w of its row;
+//   reverse  dbar_v J(x_v) + dbar_e J(x_e), then the edge's alpha adjoint
+//            dbar_e (grad phi . e_B) / 2 times each clip derivative, carried
+//            back through the trace: theta_bar += lambda sgn G'(phi_k) J(x_k),
+//            lambda <- lambda (1 + sgn G'(phi_k) grad phi_k . e_B),
+// J(x) = d phi_B / d theta at x (cm_param.cuh shape_param_grad), summed per
+// CTA in shared memory, one global atomic per parameter and unit.
+#define CM_PV_THREADS 128
+#define CM_PV_MAX_ITERS 16
+__global__ void __launch_bounds__(CM_PV_THREADS) k_mf_param_vjp(const MfArgs a, const float* __restrict__ w,
+                                                                float* __restrict__ vjp,
+                                                                const int64_t* __restrict__ poff, int max_V,
+                                                                int max_E) {
+  extern __shared__ __align__(16) float psm[];
+  __shared__ UnitCtx U;
+  __shared__ int shB;
+  if (threadIdx.x == 0) {
+    unit_resolve(a, blockIdx.x, U);
+    shB = __ldg(a.pairs + 5 * (int64_t)blockIdx.x + 4);
+  }
+  __syncthreads();
+  if (!U.valid) return;
+  const int V = U.SA.V, E = U.SA.E, NF = U.SA.F;
+  const int64_t pb = __ldg(poff + shB);
+  const int np = (int)(__ldg(poff + shB + 1) - pb);
+  float* dV = psm;                  // [max_V] vertex candidate values
+  float* adjV = dV + max_V;         // [max_V] their adjoints
+  float* dE = adjV + max_V;         // [max_E] edge candidate values
+  float* gE = dE + max_E;           // [max_E] grad phi . e_B at the edge point
+  float* aE = gE + max_E;           // [max_E] alpha_bar
+  float* adjE = aE + max_E;         // [max_E] adjoints
+  float* thb = adjE + max_E;        // [np] parameter adjoint of this unit
+  const PairFrame& F = U.F;
+  const SmoothDev& sp = a.S.sp;
+  const float* lv = a.S.verts + 4 * (int64_t)U.SA.v_off;
+  const int32_t* ed = a.S.edges + 2 * (int64_t)U.SA.e_off;
+  const int32_t* fv = a.S.faces + 3 * (int64_t)U.SA.f_off;
+  const int32_t* fe = a.S.face_edges + 3 * (int64_t)U.SA.f_off;
+  const bool full = (a.mode & CM_FULL_MODE) != 0;
+  for (int k = threadIdx.x; k < np; k += blockDim.x) thb[k] = 0.f;
+  auto xB_of = [&](int v, float* xb) {
+    const float4 x4 = ldv(lv, v);
+    const float x[3] = {x4.x, x4.y, x4.z};
+    float pw[3];
+    to_frames(F, x, xb, pw);
+  };
+  // the edge in B's frame: start point, unit direction, length
+  auto edge_B = [&](int e, float* xI, float* eb, float& L, int& vI, int& vII) {
+    vI = __ldg(ed + 2 * e);
+    vII = __ldg(ed + 2 * e + 1);
+    const float4 xa = ldv(lv, vI), xc = ldv(lv, vII);
+    const float dl[3] = {xc.x - xa.x, xc.y - xa.y, xc.z - xa.z};
+    L = sqrtf(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
+    const float iL = 1.f / L;
+    const float el[3] = {dl[0] * iL, dl[1] * iL, dl[2] * iL};
+    rot_vec(F.Rrel, el, eb);
+    xB_of(vI, xI);
+  };
+  auto phi1 = [&](const float* x, Res<1>& r) { eval_shape<1, 2, false, false, false, false>(a.S, U.SB, x, r); };
+  // one trace: the final alpha; its iterates' alphas in al[] (al[0] the corner's)
+  auto trace = [&](const float* xI, const float* eb, float L, const float* xc, int dir, float* al) {
+    float alpha = dir ? L : 0.f;
+    const float sgn = dir ? -1.f : 1.f;
+    for (int it = 0; it < sp.iters; ++it) {
+      al[it] = alpha;
+      float x[3];
+      if (it == 0) { x[0] = xc[0]; x[1] = xc[1]; x[2] = xc[2]; }
+      else { for (int i = 0; i < 3; ++i) x[i] = fmaf(alpha, eb[i], xI[i]); }
+      Res<0> r;
+      eval_shape<0, 2, false, false, false, false>(a.S, U.SB, x, r);
+      alpha = fmaf(sgn * sigm(r.v * sp.i_cmp), r.v, alpha);
+    }
+    return alpha;
+  };
+  // forward: vertex candidates
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    float xb[3];
+    xB_of(v, xb);
+    Res<0> r;
+    eval_shape<0, 2, false, false, false, false>(a.S, U.SB, xb, r);
+    dV[v] = r.v;
+    adjV[v] = full ? __ldg(w + U.off + v) : 0.f;
+  }
+  // forward: edge candidates
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    float xI[3], eb[3], L;
+    int vI, vII;
+    edge_B(e, xI, eb, L, vI, vII);
+    float xc[3], al[CM_PV_MAX_ITERS];
+    float ab = 0.f;
+    for (int dir = 0; dir < 2; ++dir) {
+      xB_of(dir ? vII : vI, xc);
+      const float afin = trace(xI, eb, L, xc, dir, al);
+      float at, c1, c2;
+      softclip_12(afin, 0.f, L, sp.tau_clip_alpha, sp.i_clip_alpha, at, c1, c2);
+      ab += at;
+    }
+    ab *= 0.5f;
+    const float x[3] = {fmaf(ab, eb[0], xI[0]), fmaf(ab, eb[1], xI[1]), fmaf(ab, eb[2], xI[2])};
+    Res<1> r;
+    phi1(x, r);
+    dE[e] = r.v;
+    gE[e] = r.g[0] * eb[0] + r.g[1] * eb[1] + r.g[2] * eb[2];
+    aE[e] = ab;
+    adjE[e] = full ? __ldg(w + U.off + V + e) : 0.f;
+  }
+  __syncthreads();
+  // rows: the candidates' depth adjoints (reduced mode: face softmax)
+  if (!full) {
+    const float itl = LOG2E * sp.i_min;
+    for (int f = threadIdx.x; f < NF; f += blockDim.x) {
+      const float wf = __ldg(w + U.off + f);
+      if (wf == 0.f) continue;
+      int cv[3], ce[3];
+      float dc[6];
+      for (int k = 0; k < 3; ++k) {
+        cv[k] = __ldg(fv + 3 * f + k);
+        ce[k] = __ldg(fe + 3 * f + k);
+        dc[k] = dV[cv[k]];
+        dc[3 + k] = dE[ce[k]];
+      }
+      float dm = dc[0];
+      for (int i = 1; i < 6; ++i) dm = fminf(dm, dc[i]);
+      float z[6], Z = 0.f;
+      for (int i = 0; i < 6; ++i) { z[i] = ex2((dm - dc[i]) * itl); Z += z[i]; }
+      const float iZ = wf / Z;
+      for (int k = 0; k < 3; ++k) {
+        atomicAdd(adjV + cv[k], z[k] * iZ);
+        atomicAdd(adjE + ce[k], z[3 + k] * iZ);
+      }
+    }
+    __syncthreads();
+  }
+  auto accum = [&](const float* x, float scale) {
+    shape_param_grad(a.S, U.SB, x, [&](int k, float v) { if (k < np) atomicAdd(thb + k, scale * v); });
+  };
+  // reverse: vertex candidates
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    if (adjV[v] == 0.f) continue;
+    float xb[3];
+    xB_of(v, xb);
+    accum(xb, adjV[v]);
+  }
+  // reverse: edge candidates, their points and traces
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const float de = adjE[e];
+    if (de == 0.f) continue;
+    float xI[3], eb[3], L;
+    int vI, vII;
+    edge_B(e, xI, eb, L, vI, vII);
+    const float ab = aE[e];
+    const float x[3] = {fmaf(ab, eb[0], xI[0]), fmaf(ab, eb[1], xI[1]), fmaf(ab, eb[2], xI[2])};
+    accum(x, de);
+    const float abar_adj = de * gE[e];   // d depth / d alpha_bar
+    float xc[3], al[CM_PV_MAX_ITERS];
+    for (int dir = 0; dir < 2; ++dir) {
+      xB_of(dir ? vII : vI, xc);
+      const float afin = trace(xI, eb, L, xc, dir, al);
+      float at, c1, c2;
+      softclip_12(afin, 0.f, L, sp.tau_clip_alpha, sp.i_clip_alpha, at, c1, c2);
+      const float sgn = dir ? -1.f : 1.f;
+      float lam = 0.5f * abar_adj * c1;
+      for (int it = sp.iters - 1; it >= 0; --it) {
+        float xk[3];
+        if (it == 0) { xk[0] = xc[0]; xk[1] = xc[1]; xk[2] = xc[2]; }
+        else { for (int i = 0; i < 3; ++i) xk[i] = fmaf(al[it], eb[i], xI[i]); }
+        Res<1> r;
+        phi1(xk, r);
+        const float s = sigm(r.v * sp.i_cmp);
+        const float Gp = fmaf(r.v * s * (1.f - s), sp.i_cmp, s);
+        accum(xk, lam * sgn * Gp);
+        lam *= fmaf(sgn * Gp, r.g[0] * eb[0] + r.g[1] * eb[1] + r.g[2] * eb[2], 1.f);
+      }
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < np; k += blockDim.x)
+    if (thb[k] != 0.f) atomicAdd(vjp + pb + k, thb[k]);
+}
+
 namespace cml {
 
 // floats of one unit's scratch slot
@@ -1698,6 +1890,43 @@ int launch_manifold(const SceneDev& s, int class_mask, int max_V, int max_E, con
   if (tier == 2) return launch_tier<2>(a, class_mask, max_V, max_E, n_units, chunk, sts, n_streams);
   if (tier == 1) return launch_tier<1>(a, class_mask, max_V, max_E, n_units, chunk, sts, n_streams);
   return launch_tier<0>(a, class_mask, max_V, max_E, n_units, chunk, sts, n_streams);
+}
+
+int launch_manifold_param_vjp(const SceneDev& s, int max_V, int max_E, int pmax, const int32_t* pairs,
+                              int64_t n_pairs, const int64_t* offsets, const float* poses, int64_t n_env,
+                              int32_t n_slot, uint32_t mode, const float* w, float* vjp, const int64_t* poff,
+                              void* stream) {
+  if (s.sp.iters > CM_PV_MAX_ITERS) {
+    set_error("manifold_param_vjp: more than 16 trace iterations");
+    return CM_ERR_UNSUPPORTED;
+  }
+  if (n_pairs <= 0) return CM_OK;
+  MfArgs a;
+  memset(&a, 0, sizeof(a));
+  a.S = s;
+  a.pairs = pairs;
+  a.n_pairs = n_pairs;
+  a.offsets = offsets;
+  a.poses = poses;
+  a.n_env = n_env;
+  a.n_slot = n_slot;
+  a.mode = mode;
+  const int bytes = (2 * max_V + 4 * max_E + pmax) * 4;
+  if (bytes > 48 * 1024 &&
+      cudaFuncSetAttribute(k_mf_param_vjp, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) {
+    set_error("manifold_param_vjp: shared memory");
+    return CM_ERR_UNSUPPORTED;
+  }
+  for (int64_t p0 = 0; p0 < n_pairs; p0 += 0x7fffffff) {   // (grids of at most 2^31 - 1 CTAs)
+    const int64_t nb = n_pairs - p0 < 0x7fffffff ? n_pairs - p0 : 0x7fffffff;
+    MfArgs ac = a;
+    ac.pairs = pairs + 5 * p0;
+    ac.offsets = offsets + p0;
+    ac.n_pairs = nb;
+    k_mf_param_vjp<<<(unsigned)nb, CM_PV_THREADS, bytes, (cudaStream_t)stream>>>(ac, w, vjp, poff, max_V, max_E);
+    if (int rc = check_launch("k_mf_param_vjp")) return rc;
+  }
+  return CM_OK;
 }
 
 }  // namespace cml

@@ -591,6 +591,103 @@ def test_sdf_node_pose_grad_unsupported(cuda):
                              torch.zeros(4, 3, device="cuda"), 4, 6)
 
 
+def _vjp_scene():
+    """A ball mesh against an SQ union, a curved XPSQ and the cup, plus the C1
+    pairs (box on the ground half-space both ways): several envs each."""
+    rng = np.random.default_rng(71)
+    c1 = synth.c1_scene()
+    ball = synth.make_shape("ball", None, synth.sq_mesh((0.12, 0.12, 0.12), (1.0, 1.0), 3))
+    uni = synth.make_shape("uni", synth.op("union", [
+        synth.sq((0.2, 0.15, 0.1), (0.5, 0.8)),
+        synth.sq((0.1, 0.1, 0.25), (0.9, 0.4), pose=[0.1, 0.05, 0.0, 0.96, 0.2, 0.1, 0.17])]), None)
+    xp = synth.make_shape("xp", synth.xpsq([-0.3, 0, 0, 0.0, 0.35, 0.05, 0.3, 0, 0.02], (0.12, 0.15, 0.1), (0.6, 0.8),
+                                           planes0=[[0.2, 0.3, 0.93, -0.05]]), None)
+    shapes = list(c1.shapes) + [ball, uni, xp]
+    n_env = 6
+    poses = np.zeros((n_env, 3, 8))
+    pairs = []
+    for e in range(n_env):
+        poses[e, 0] = c1.poses[0, 0]
+        poses[e, 1] = c1.poses[0, 1]
+        poses[e, 1, :3] += rng.uniform(-0.002, 0.002, 3)
+        t = [(0.05, 0.02, 0.3), (0.02, 0.22, 0.2), (0.04, 0.18, 0.18)][e % 3]
+        poses[e, 2] = synth.pose_row(np.asarray(t) + rng.uniform(-0.02, 0.02, 3), synth.random_quats(rng, 1)[0])
+        pairs += [[e, 0, 1, 0, 1], [e, 1, 0, 1, 0]]
+        pairs += [[e, 2, 1, 2, 3 + e % 2]]   # ball (slot 2) against the union / the XPSQ at the ground's slot
+    # the SDF bodies of the ball pairs sit at slot 1 (the ground pose, near the identity)
+    pairs = np.asarray(pairs, dtype=np.int32)
+    return scene_of(shapes, pairs=pairs, poses=poses.astype(np.float32)), rng
+
+
+@pytest.mark.parametrize("mode", [0, 4])
+def test_manifold_param_vjp_parity(cuda, oracle_mod, mode):
+    """Shape-parameter VJP of the manifold depths (DESIGN
+    reading #48) against the oracle's seeded manifold: random weights over
+    all rows (each vjp entry within the sum of |w_r| x the per-row derivative
+    tolerance 1e-4 max(|d depth_r / d theta|_inf, 1)), and one-hot weights on
+    sampled rows (the rows' parameter Jacobians element by element)."""
+    import torch
+    from paper_2604_17538_b200 import binding
+    sc, rng = _vjp_scene()
+    S = binding.Scene(sc.shapes, sc.smooth)
+    osc = oracle_mod.OracleScene(sc)
+    counts, offs = S.param_layout()
+    pairs_t = torch.from_numpy(sc.pairs).cuda()
+    poses_t = torch.from_numpy(sc.poses).cuda()
+    offs_t = S.manifold_offsets(pairs_t, mode)
+    C = S.manifold_size(sc.pairs, mode)
+    pmax = int(counts.max())
+    Jd = osc.manifold_param_jac(sc.pairs, sc.poses, mode=mode, pmax=pmax)
+    Jp = osc.manifold_param_jac(sc.pairs, PT.perturb_inputs(np.random.default_rng(72), sc.poses), mode=mode, pmax=pmax)
+    assert Jd.shape[0] == C
+    row_pair = np.searchsorted(offs_t.cpu().numpy(), np.arange(C), side="right") - 1
+    shape_of_row = sc.pairs[row_pair, 4]
+    tol_row = 1e-4 * np.maximum(np.abs(Jd).max(axis=1), 1.0)
+
+    def ref_vjp(w, J):
+        out = np.zeros(int(offs[-1]))
+        for r in np.nonzero(w)[0]:
+            s = shape_of_row[r]
+            out[offs[s]:offs[s] + counts[s]] += w[r] * J[r, :counts[s]]
+        return out
+
+    def tol_vjp(w):
+        out = np.full(int(offs[-1]), 1e-30)   # (entries no row touches must come back exactly 0)
+        for r in np.nonzero(w)[0]:
+            s = shape_of_row[r]
+            out[offs[s]:offs[s] + counts[s]] += abs(w[r]) * tol_row[r]
+        return out
+
+    rep = []
+    nf = 0
+    for trial in range(3):
+        w = rng.normal(size=C).astype(np.float32)
+        got = S.manifold_param_vjp(pairs_t, offs_t, poses_t, torch.from_numpy(w).cuda(), mode).cpu().numpy()
+        nf += PT.compare("vjp%d" % trial, got, ref_vjp(w, Jd), ref_vjp(w, Jp), tol_vjp(w), rep)
+    for r in rng.choice(C, size=24, replace=False):
+        w = np.zeros(C, np.float32)
+        w[r] = 1.0
+        got = S.manifold_param_vjp(pairs_t, offs_t, poses_t, torch.from_numpy(w).cuda(), mode).cpu().numpy()
+        nf += PT.compare("row%d" % r, got, ref_vjp(w, Jd), ref_vjp(w, Jp), tol_vjp(w), rep)
+    _report("manifold_param_vjp_m%d" % mode, rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+    assert PT.excluded_fraction(rep) < 0.01
+    assert np.abs(Jd).max() > 0.1
+
+
+def test_manifold_param_vjp_unsupported(cuda):
+    import torch
+    from paper_2604_17538_b200 import binding
+    sc, _ = _vjp_scene()
+    S = binding.Scene(sc.shapes, sc.smooth)
+    pairs_t = torch.from_numpy(sc.pairs).cuda()
+    poses_t = torch.from_numpy(sc.poses).cuda()
+    offs_t = S.manifold_offsets(pairs_t, binding.TWO_SIDED)
+    C = S.manifold_size(sc.pairs[:2], binding.TWO_SIDED)
+    with pytest.raises(binding.CMError):
+        S.manifold_param_vjp(pairs_t[:2], offs_t, poses_t, torch.zeros(C, device="cuda"), binding.TWO_SIDED)
+
+
 def test_sdf_eval_xpsq_soft_cardano_band(cuda, oracle_mod):
     """Points inside the soft-Cardano band 10 tau_Delta < |Delta| < 46
     tau_Delta of a curved XPSQ (both branches blended): every
