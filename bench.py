@@ -356,6 +356,34 @@ def _timed(step, args, stream, flush, world, local):
     return float(t.item()) / args.steps, launches, clk
 
 
+def c1_graph_latency(step, args, dev):
+    """Per-call latency of the same call captured once into a CUDA graph and
+    replayed (C1 is launch-bound: ~11 kernels for 2 pairs); CUDA events
+    around each replay on the current stream, median over K."""
+    import torch
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(side):
+        step()
+    torch.cuda.current_stream(dev).wait_stream(side)
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    for _ in range(max(args.warmup, 3)):
+        g.replay()
+    torch.cuda.synchronize(dev)
+    ts = []
+    for _ in range(max(args.steps, 20)):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b) * 1e3)
+    return float(np.median(ts))
+
+
 def _e2e_pipelined(run_step, h2d, d2h, steps, world, dev):
     """End-to-end loop through the public API with host buffers, double
     buffered: step i's host->device copy of its inputs (pinned) runs on an
@@ -700,6 +728,7 @@ def main():
 
     ms_per_step, launches, clk = _timed(step, args, stream, flush, world, local)
     n_pairs_all = len(scene.pairs) * world
+    graph_us = c1_graph_latency(step, args, dev) if args.workload == "C1" else None
     value = n_pairs_all / (ms_per_step / 1e3)
 
     gather = None
@@ -780,6 +809,8 @@ def main():
             line["config"]["sqs_in_union"] = args.k
         if args.workload == "C1":   # latency-bound: report the per-call latency
             line["config"]["latency_us_per_call"] = ms_per_step * 1e3
+            if graph_us is not None:
+                line["config"]["latency_us_per_call_cuda_graph"] = graph_us
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

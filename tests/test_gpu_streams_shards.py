@@ -145,3 +145,40 @@ def test_invalid_records_counted_not_dereferenced(cuda):
     d = o["d"].cpu().numpy()
     assert np.isnan(d[5:10]).all() and np.isfinite(d[:5]).all() and np.isfinite(d[10:]).all()
     assert S.error_count() == 5
+
+
+@pytest.mark.parametrize("wl", ["C1", "C5"])
+def test_manifold_cuda_graph_capture(cuda, wl):
+    """cm_contact_manifold inside a CUDA graph (stream capture: the fork onto
+    the scene's internal streams and the join back are events recorded on
+    the capturing stream): replays with new poses copied into the captured
+    input buffer give the same bits as eager calls."""
+    torch = cuda
+    from paper_2604_17538_b200 import binding
+    sc = synth.c1_scene() if wl == "C1" else synth.c5_scene(4096)
+    S = binding.Scene(sc.shapes, sc.smooth)
+    pairs, poses, offs, C = _inputs(S, sc, torch)
+    out = S.alloc_manifold(C, 2, poses.device)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):   # warm-up outside the capture
+        S.contact_manifold(pairs, offs, C, poses, 2, out=out)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        S.contact_manifold(pairs, offs, C, poses, 2, out=out)
+    rng = np.random.default_rng(9)
+    for rep in range(3):
+        p2 = sc.poses.copy()
+        p2[..., :3] += rng.normal(size=p2[..., :3].shape).astype(np.float32) * 1e-3
+        poses.copy_(torch.from_numpy(p2))
+        for v in out.values():
+            if v.dtype == torch.float32:
+                v.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+        ref = S.contact_manifold(pairs, offs, C, torch.from_numpy(p2).cuda(), 2)
+        torch.cuda.synchronize()
+        for k in ref:
+            assert _same(out[k], ref[k]), (rep, k)
