@@ -1495,6 +1495,31 @@ __global__ void __maxnreg__((MidFacesRegs<TIER, XP>::R)) k_mf_midfaces(const MfA
   mf_faces_unit<TIER, false>(a, U, u, nullptr, nullptr, 0u, sv_s, se_s);
 }
 
+// Small batches (at most CM_MF_SMALL_UNITS units in a chunk, e.g. C1's two
+// pairs): the four phases of a unit in ONE kernel per SDF class, separated
+// by CTA barriers (the per-phase kernels' dependent launches dominate there;
+// at large batches the split kernels win).  The same device
+// functions and the same scratch slot as the split path: bitwise equal.
+#ifndef CM_MF_SMALL_UNITS
+#define CM_MF_SMALL_UNITS 64
+#endif
+template <int TIER, int XP>
+__global__ void __launch_bounds__(CM_MF_MAX_THREADS) k_mf_small(const MfArgs a) {
+  __shared__ UnitCtx U;
+  int u;
+  if (!list_unit(a, XP, U, u)) return;
+  mf_vertices_unit<TIER, XP>(a, U, u);
+  __syncthreads();
+  if constexpr (TIER <= 2 && CM_TRACE6) mf_traces_unit_n<TIER, XP>(a, U, u);
+  else mf_traces_unit<TIER, XP>(a, U, u);
+  __syncthreads();
+  mf_midpoints_unit<TIER, XP>(a, U, u, nullptr);
+  if (!(a.mode & CM_FULL_MODE)) {
+    __syncthreads();
+    mf_faces_unit<TIER, false>(a, U, u, nullptr, nullptr, 0u);
+  }
+}
+
 // broad phase (f2): rows of the culled units (list CM_N_CLASSES), one CTA per
 // unit, threads over its rows (coalesced field-major stores)
 template <int TIER>
@@ -1771,6 +1796,10 @@ static int midfaces_bytes(int tier, uint32_t mode, int max_V, int max_E) {
 
 template <int TIER, int XP>
 static int launch_sdf_phases(MfArgs& a, int64_t nb, int T, int max_V, int max_E, cudaStream_t st) {
+  if (nb <= CM_MF_SMALL_UNITS) {   // small batch: one kernel per class (faces included)
+    k_mf_small<TIER, XP><<<(unsigned)nb, T, 0, st>>>(a);
+    return check_launch("k_mf_small");
+  }
   k_mf_vertices<TIER, XP><<<(unsigned)nb, T, 0, st>>>(a);
   int rc = check_launch("k_mf_vertices");
   if (rc) return rc;
@@ -1864,7 +1893,7 @@ static int launch_tier(MfArgs a, int class_mask, int max_V, int max_E, int64_t n
       k_mf_culled<TIER><<<(unsigned)nb, T, 0, st>>>(a);
       if ((rc = check_launch("k_mf_culled"))) return rc;
     }
-    if (!full && midfaces_bytes(TIER, a.mode, max_V, max_E) == 0) {   // the fusion does not depend on the SDF class: one launch
+    if (!full && midfaces_bytes(TIER, a.mode, max_V, max_E) == 0 && nb > CM_MF_SMALL_UNITS) {   // the fusion does not depend on the SDF class: one launch
       if (stage_bytes > 0 && (stage_bytes <= kStageSmallBytes || nb < 8 * (int64_t)num_sms()))
         k_mf_faces<TIER, true><<<(unsigned)nb, T, stage_bytes, st>>>(a);
       else

@@ -12,7 +12,8 @@ import torch
 sys.path.insert(0, ".")
 from paper_2604_17538_b200 import binding, synth  # noqa: E402
 
-CASES = [("C5", lambda: synth.c5_scene(1 << 16)), ("C4", lambda: synth.c4_scene(256)),
+CASES = [("C1", lambda: synth.c1_scene()), ("C5s", lambda: synth.c5_scene(48)), ("C4s", lambda: synth.c4_scene(2)),
+         ("C5", lambda: synth.c5_scene(1 << 16)), ("C4", lambda: synth.c4_scene(256)),
          ("C2", lambda: synth.c2_scene()), ("C3", lambda: synth.c3_scene(512))]
 rep = {}
 for name, mk in CASES:
