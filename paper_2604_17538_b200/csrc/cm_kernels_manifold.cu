@@ -93,6 +93,11 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+// bulk prefetch of `bytes` (multiple of 16, 16-B aligned) into L2 (no
+// destination, no completion)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 // global -> shared bulk copy of `bytes` (multiple of 16, 16-B aligned ends)
 // by the calling thread; completion is counted on `bar`
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -1579,13 +1584,36 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS) k_mf_culled(const MfArgs a)
   }
 }
 
+#ifndef CM_MF_FACE_L2PF
+#define CM_MF_FACE_L2PF 0   // face kernel: L2 bulk prefetch of the records of the unit this many CTAs ahead
+                           // (768 / 1536 / 3072: C5 -0.4 / -2.0 / -2.2%, C4 -0.2 / +0.5 / +0.4%; r02ze)
+#endif
+#ifndef CM_MF_FACE_REGS
+#define CM_MF_FACE_REGS 0   // explicit register cap of the tier-0-2 face kernel (0: CM_MF_FACE_MINB)
+#endif
+template <int TIER> struct FaceRegs {
+  static constexpr int R = TIER >= 3 ? 255 : (CM_MF_FACE_REGS ? CM_MF_FACE_REGS : regs_of(CM_MF_FACE_MINB));
+};
 template <int TIER, bool STAGED>
-__global__ void __launch_bounds__(CM_MF_MAX_THREADS, TIER >= 3 ? 1 : CM_MF_FACE_MINB) k_mf_faces(const MfArgs a) {
+__global__ void __launch_bounds__(CM_MF_MAX_THREADS) __maxnreg__((FaceRegs<TIER>::R)) k_mf_faces(const MfArgs a) {
   extern __shared__ __align__(16) float fsm[];
   __shared__ UnitCtx U;
   __shared__ uint64_t bar;
   if (STAGED && threadIdx.x == 0) mbar_init(&bar, 1);   // published by list_unit's barrier
   int u;
+  if (CM_MF_FACE_L2PF && !STAGED && threadIdx.x == 0) {
+    // the candidate records of the unit CM_MF_FACE_L2PF CTAs ahead (about
+    // one wave of resident CTAs) into L2, so that its face loads hit L2
+    // instead of waiting on HBM; the first wave prefetches its own
+    const int64_t b = blockIdx.x;
+    for (int64_t v = (b < CM_MF_FACE_L2PF ? b : b + CM_MF_FACE_L2PF); v <= b + CM_MF_FACE_L2PF; v += CM_MF_FACE_L2PF) {
+      if (v >= a.nb) break;
+      const UnitCtx& c = a.ctx[v];
+      const int V = c.SA.V, E = c.SA.E;
+      const uint32_t bytes = (uint32_t)(vrec(TIER) * V + erec(TIER) * E) * 4u;
+      if (bytes > 0 && c.valid) bulk_prefetch_l2(a.scratch + v * a.slot, bytes);
+    }
+  }
   if (list_unit(a, -1, U, u) && U.valid) mf_faces_unit<TIER, STAGED>(a, U, u, fsm, &bar, 0u);
 }
 
