@@ -366,6 +366,11 @@ static_assert(sizeof(UnitCtx) % 16 == 0, "UnitCtx is copied as float4");
 #ifndef CM_TRACE6
 #define CM_TRACE6 1         // 6-component trace derivative recursion (tiers 0-2)
 #endif
+#ifndef CM_TRACE_PAIRED
+#define CM_TRACE_PAIRED 0   // tiers 0-2: both traces of an edge on adjacent lanes, one averaged record
+                            // (-18 KB DRAM per C5 pair, bitwise equal; C5 -1.3%, C4 0, C3 +0.3%: r02zf)
+#endif
+#define CM_PAIRED_REC (CM_TRACE_PAIRED && CM_TRACE6)   // (the paired traces are the 6-component kernel's)
 #ifndef CM_MF_MID_PREFETCH
 #define CM_MF_MID_PREFETCH 0   // tier-2 midpoint kernel: next trace record by cp.async into shared memory:
                                // bitwise equal, C5 -4.5%, C4 -2.3% (r02z9)
@@ -882,6 +887,39 @@ __device__ __forceinline__ void mf_traces_unit_n(const MfArgs& a, const UnitCtx&
   float* se = a.scratch + (int64_t)u * a.slot + (int64_t)vrec(TIER) * V;
   const float* lv = a.S.verts + 4 * (int64_t)U.SA.v_off;
   const int32_t* ed = a.S.edges + 2 * (int64_t)U.SA.e_off;
+#if CM_TRACE_PAIRED
+  // the two traces of edge e on adjacent lanes (j = 2e + dir): their sum by
+  // one shuffle, the averaged record (a_bar, d a_bar: 10 floats, half the
+  // two traces' records) written by the dir-0 lane; the sums are the
+  // midpoint kernel's a_I + a_II in the same order (bitwise equal)
+  const int nj = 2 * E;
+  for (int jb = threadIdx.x & ~31; jb < nj; jb += blockDim.x) {
+    const int j = jb + (threadIdx.x & 31);
+    const bool act = j < nj;
+    const int e = act ? j >> 1 : 0;
+    const int dir = j & 1;             // 0: from v_I along +e_t; 1: from v_II along -e_t
+    constexpr int NS = TIER >= 2 ? 10 : 1;
+    float o[10] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (act) {
+      const int vI = __ldg(ed + 2 * e), vII = __ldg(ed + 2 * e + 1);
+      CM_ASSERT(vI >= 0 && vI < V && vII >= 0 && vII < V);
+      trace_one_n<TIER, XP>(a, U, sv, lv, vI, vII, dir, o);
+    }
+    float m[10];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) m[k] = 0.5f * (o[k] + __shfl_xor_sync(0xffffffffu, o[k], 1));
+    if (act && dir == 0) {
+      float* rec = se + e * erec(TIER);
+      if constexpr (TIER >= 2) {
+        st4(rec, m[0], m[1], m[2], m[3]);
+        st4(rec + 4, m[4], m[5], m[6], m[7]);
+        *reinterpret_cast<float2*>(rec + 8) = make_float2(m[8], m[9]);
+      } else {
+        *rec = m[0];
+      }
+    }
+  }
+#else
   for (int j = threadIdx.x; j < 2 * E; j += blockDim.x) {
     const int e = j < E ? j : j - E;
     const int dir = j < E ? 0 : 1;     // 0: from v_I along +e_t; 1: from v_II along -e_t
@@ -904,6 +942,7 @@ __device__ __forceinline__ void mf_traces_unit_n(const MfArgs& a, const UnitCtx&
       *rec = o[0];
     }
   }
+#endif
 }
 
 // ---- phase 3: edge points p_e = v_I + a_bar e_t, a_bar = (a_I + a_II)/2
@@ -992,6 +1031,13 @@ __device__ __forceinline__ void mf_midpoints_unit(const MfArgs& a, const UnitCtx
       for (int k = 0; k < NDQ; ++k) dab[k] = 0.5f * (rin[1 + k] + rb2[1 + k]);
 #pragma unroll
       for (int k = 0; k < N45; ++k) d2ab[k] = 0.5f * (rin[TD2 + k] + rb2[TD2 + k]);
+    } else if constexpr (TIER >= 2 && CM_PAIRED_REC) {   // the traces' averaged record (a_bar, d a_bar)
+      const float4 r0 = ld4(rin), r1 = ld4(rin + 4);
+      const float2 r2 = *reinterpret_cast<const float2*>(rin + 8);
+      ab = r0.x;
+      dab[0] = r0.y; dab[1] = r0.z; dab[2] = r0.w;
+      dab[3] = r1.x; dab[4] = r1.y; dab[5] = r1.z; dab[6] = r1.w;
+      dab[7] = r2.x; dab[8] = r2.y;
     } else if constexpr (TIER >= 2) {
       float t[20];
       const float* src = rin;
@@ -1008,6 +1054,8 @@ __device__ __forceinline__ void mf_midpoints_unit(const MfArgs& a, const UnitCtx
       ab = 0.5f * (t[0] + t[10]);
 #pragma unroll
       for (int k = 0; k < NDQ; ++k) dab[k] = 0.5f * (t[1 + k] + t[11 + k]);
+    } else if constexpr (CM_PAIRED_REC) {
+      ab = rin[0];
     } else {
       ab = 0.5f * (rin[0] + rin[1]);
     }
