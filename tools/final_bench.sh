@@ -7,6 +7,9 @@ T=$1
 O=gpurun_out/$T
 mkdir -p $O
 nvidia-smi -q | grep -E "Product Name|Driver Version" > $O/box.txt 2>&1
+timeout 900 python bench.py > $O/bench_C5.json 2> $O/bench_C5.err
+timeout 900 python bench.py --tier 3 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > $O/bench_C5_t3.json 2> $O/bench_C5_t3.err
+timeout 900 python bench.py --workload C4 --tier 3 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > $O/bench_C4_t3.json 2> $O/bench_C4_t3.err
 for w in C4 C3 C2 C1 SDF; do
   timeout 900 python bench.py --workload $w --e2e-steps 2 > $O/bench_$w.json 2> $O/bench_$w.err
 done
