@@ -152,7 +152,8 @@ constexpr int kParamMaxNodes = 16;
 namespace cml {
 int launch_sdf_eval(const cmi::SceneDev& s, int class_mask, const int32_t* shape_ids, const float* poses,
                     const float* points, int64_t B, int64_t P, uint32_t flags, float* d, float* grad, float* hess,
-                    float* dpose, float* d2pose, float* dxdpose, void* const* streams, int n_streams);
+                    float* dpose, float* d2pose, float* dxdpose, void* const* streams, int n_streams,
+                    unsigned long long* ctrs = nullptr);
 int launch_manifold(const cmi::SceneDev& s, int class_mask, int max_V, int max_E, const int32_t* pairs,
                     int64_t n_pairs, const int64_t* offsets, const float* poses, int64_t n_env, int32_t n_slot,
                     uint32_t flags,

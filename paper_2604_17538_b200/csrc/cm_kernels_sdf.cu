@@ -35,18 +35,51 @@ using cml::num_sms;
 #ifndef CM_SDF_MINB_XP
 #define CM_SDF_MINB_XP 2   // the XPSQ classes (1, 2, 4): 128 registers, SDF +1.8% over 80 (r02m)
 #endif
-template <int O, int XP, bool PG, bool PH>
-__global__ void __launch_bounds__(256, (XP == 1 || XP == 2 || XP == 4) ? CM_SDF_MINB_XP : CM_SDF_MINB) k_sdf_eval(SceneDev S, const int32_t* __restrict__ shape_ids,
+#ifndef CM_SDF_CHUNK
+#define CM_SDF_CHUNK 1024   // points per work item of the dynamic (multi-class) sdf_eval schedule
+#endif
+#ifndef CM_SDF_THREADS
+#define CM_SDF_THREADS 64   // threads per sdf_eval block (the grid keeps 148 x 16 x 256 threads): 64 +4.8% on
+                            // the SDF workload over 256 (a block holds its SM slots until its slowest warp ends)
+#endif
+template <int O, int XP, bool PG, bool PH, bool DYN>
+__global__ void __launch_bounds__(CM_SDF_THREADS, ((XP == 1 || XP == 2 || XP == 4) ? CM_SDF_MINB_XP : CM_SDF_MINB) * (256 / CM_SDF_THREADS)) k_sdf_eval(SceneDev S, const int32_t* __restrict__ shape_ids,
                                                   const float* __restrict__ poses, const float* __restrict__ points,
                                                   int64_t B, int64_t P, float* __restrict__ d,
                                                   float* __restrict__ grad, float* __restrict__ hess,
                                                   float* __restrict__ dpose, float* __restrict__ d2pose,
-                                                  float* __restrict__ dxdpose, int xp_filter, int own_invalid) {
+                                                  float* __restrict__ dxdpose, int xp_filter, int own_invalid,
+                                                  unsigned long long* __restrict__ ctr) {
   const int64_t N = B * P;
   const bool n32 = N <= 0x7fffffff;   // 32-bit index arithmetic (no 64-bit division)
   // (warps walking 32-point segments with the class decided once per warp
   // measured -7.5% on the SDF workload, r02r)
-  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < N; n += (int64_t)gridDim.x * blockDim.x) {
+  // work (DYN, the scene's multi-class launches): chunks of CM_SDF_CHUNK
+  // points per warp taken from a device counter, so that warps whose chunks
+  // hold few points of this class take more of them (the static walk leaves
+  // warps idle behind the slowest of their block; r02zk); otherwise the
+  // thread-level grid-stride walk (a separate instantiation: a warp
+  // reconvergence point at every iteration costs the static walk 10%)
+  const int lane = threadIdx.x & 31;
+  int64_t cb = 0, ce = 0;   // DYN: the warp's current chunk [cb, ce) (warp-uniform)
+  int64_t n = DYN ? 0 : (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (;; n += DYN ? 0 : stride) {
+    if constexpr (DYN) {
+      if (cb >= ce) {
+        unsigned long long b0 = 0;
+        if (lane == 0) b0 = atomicAdd(ctr, (unsigned long long)CM_SDF_CHUNK);
+        cb = (int64_t)__shfl_sync(0xffffffffu, b0, 0);
+        ce = cb + CM_SDF_CHUNK;
+        if (cb >= N) break;
+        if (ce > N) ce = N;
+      }
+      n = cb + lane;
+      cb += 32;
+      if (n >= ce) continue;
+    } else {
+      if (n >= N) break;
+    }
     const int64_t b = n32 ? (int64_t)((uint32_t)n / (uint32_t)P) : n / P;
     const int sid = __ldg(shape_ids + b);
     // the class byte first: points of other classes are skipped without
@@ -152,40 +185,46 @@ __global__ void __launch_bounds__(256, (XP == 1 || XP == 2 || XP == 4) ? CM_SDF_
 template <int O, int XP, bool PG, bool PH>
 static int launch_sdf_t(const SceneDev& s, int xp_filter, int own, const int32_t* ids, const float* poses, const float* pts,
                         int64_t B, int64_t P, float* d, float* g, float* h, float* dp, float* d2p, float* dxp,
-                        cudaStream_t st) {
-  const int threads = 256;
+                        cudaStream_t st, unsigned long long* ctr) {
+  const int threads = CM_SDF_THREADS;
   int64_t N = B * P;
   int64_t blocks = (N + threads - 1) / threads;
-  int64_t cap = (int64_t)num_sms() * 16;
+  int64_t cap = (int64_t)num_sms() * 16 * (256 / CM_SDF_THREADS);
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  k_sdf_eval<O, XP, PG, PH><<<(unsigned)blocks, threads, 0, st>>>(s, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp,
-                                                                   xp_filter, own);
+  if (ctr) {
+    if (cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st) != cudaSuccess) return CM_ERR_CUDA;
+    k_sdf_eval<O, XP, PG, PH, true><<<(unsigned)blocks, threads, 0, st>>>(s, ids, poses, pts, B, P, d, g, h, dp, d2p,
+                                                                          dxp, xp_filter, own, ctr);
+  } else {
+    k_sdf_eval<O, XP, PG, PH, false><<<(unsigned)blocks, threads, 0, st>>>(s, ids, poses, pts, B, P, d, g, h, dp, d2p,
+                                                                           dxp, xp_filter, own, nullptr);
+  }
   return check_launch("k_sdf_eval");
 }
 
 template <int XP>
 static int dispatch_sdf(const SceneDev& s, int xp_filter, int own, const int32_t* ids, const float* poses, const float* pts,
                         int64_t B, int64_t P, uint32_t flags, float* d, float* g, float* h, float* dp, float* d2p,
-                        float* dxp, cudaStream_t st) {
+                        float* dxp, cudaStream_t st, unsigned long long* ctr) {
   const bool PG = flags & CM_SDF_POSE_GRAD, PH = flags & CM_SDF_POSE_HESS;
   const int O = (flags & (CM_SDF_HESS | CM_SDF_POSE_HESS)) ? 2 : ((flags & (CM_SDF_GRAD | CM_SDF_POSE_GRAD)) ? 1 : 0);
-  if (O == 0) return launch_sdf_t<0, XP, false, false>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
+  if (O == 0) return launch_sdf_t<0, XP, false, false>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st, ctr);
   if (O == 1) {
-    if (PG) return launch_sdf_t<1, XP, true, false>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
-    return launch_sdf_t<1, XP, false, false>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
+    if (PG) return launch_sdf_t<1, XP, true, false>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st, ctr);
+    return launch_sdf_t<1, XP, false, false>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st, ctr);
   }
-  if (PG && PH) return launch_sdf_t<2, XP, true, true>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
-  if (PG) return launch_sdf_t<2, XP, true, false>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
-  if (PH) return launch_sdf_t<2, XP, false, true>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
-  return launch_sdf_t<2, XP, false, false>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st);
+  if (PG && PH) return launch_sdf_t<2, XP, true, true>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st, ctr);
+  if (PG) return launch_sdf_t<2, XP, true, false>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st, ctr);
+  if (PH) return launch_sdf_t<2, XP, false, true>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st, ctr);
+  return launch_sdf_t<2, XP, false, false>(s, xp_filter, own, ids, poses, pts, B, P, d, g, h, dp, d2p, dxp, st, ctr);
 }
 
 namespace cml {
 
 int launch_sdf_eval(const SceneDev& s, int class_mask, const int32_t* ids, const float* poses, const float* pts,
                     int64_t B, int64_t P, uint32_t flags, float* d, float* g, float* h, float* dp, float* d2p,
-                    float* dxp, void* const* streams, int n_streams) {
+                    float* dxp, void* const* streams, int n_streams, unsigned long long* ctrs) {
   // class_mask bit c: the scene has SDF shapes of class c (0 SQ family, 1
   // constant-schedule XPSQ, 2 varying-schedule XPSQ); one instantiation per
   // present class, each filtering its own shapes when several are present;
@@ -196,17 +235,22 @@ int launch_sdf_eval(const SceneDev& s, int class_mask, const int32_t* ids, const
   auto next = [&]() { return (cudaStream_t)streams[(j++) % n_streams]; };
   const int first = class_mask ? __builtin_ctz(class_mask) : 0;   // owns invalid shape ids
   if (class_mask & 1)
-    rc = dispatch_sdf<0>(s, multi ? 0 : -1, first == 0, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
+    rc = dispatch_sdf<0>(s, multi ? 0 : -1, first == 0, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next(),
+                         ctrs ? ctrs + 0 : nullptr);
   if (!rc && (class_mask & 2))
-    rc = dispatch_sdf<1>(s, multi ? 1 : -1, first == 1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
+    rc = dispatch_sdf<1>(s, multi ? 1 : -1, first == 1, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next(),
+                         ctrs ? ctrs + 1 : nullptr);
   if (!rc && (class_mask & 4))
-    rc = dispatch_sdf<2>(s, multi ? 2 : -1, first == 2, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
+    rc = dispatch_sdf<2>(s, multi ? 2 : -1, first == 2, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next(),
+                         ctrs ? ctrs + 2 : nullptr);
   // nested SQ-family shapes: general interpreter, no XPSQ code
   if (!rc && (class_mask & 8))
-    rc = dispatch_sdf<3>(s, multi ? 3 : -1, first == 3, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
+    rc = dispatch_sdf<3>(s, multi ? 3 : -1, first == 3, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next(),
+                         ctrs ? ctrs + 3 : nullptr);
   // constant-schedule XPSQ inside boolean trees
   if (!rc && (class_mask & 16))
-    rc = dispatch_sdf<4>(s, multi ? 4 : -1, first == 4, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next());
+    rc = dispatch_sdf<4>(s, multi ? 4 : -1, first == 4, ids, poses, pts, B, P, flags, d, g, h, dp, d2p, dxp, next(),
+                         ctrs ? ctrs + 4 : nullptr);
   return rc;
 }
 
