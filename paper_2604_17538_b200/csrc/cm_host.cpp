@@ -313,6 +313,21 @@ static bool sdf_concurrent() {
                            // streams (SDF +3.6% at 256 threads, +4.1% at 64; static at 64 threads +4.8%: r02zk3)
 #endif
 
+// makes the scene's device current for a call and restores the caller's
+// device afterwards (compute calls must not depend on, or change,
+// the caller's current device)
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 extern "C" {
 
 int cm_version(void) { return CM_ABI_VERSION; }
@@ -610,8 +625,14 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
     bounds[2 * s + 1] = sb;
   }
 
+  int prev_dev = -1;
+  cudaGetDevice(&prev_dev);
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) { delete sc; return fail(CM_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)); }
+  struct RestoreDev {
+    int d;
+    ~RestoreDev() { if (d >= 0) cudaSetDevice(d); }
+  } restore_dev{prev_dev};
   int rc = CM_OK;
   SceneDev& D = sc->dev;
   std::memset(&D, 0, sizeof(D));
@@ -696,6 +717,7 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
 
 int cm_scene_destroy(cm_scene* sc) {
   if (!sc) return CM_OK;
+  DeviceGuard device_guard(sc->device);
   for (int i = 0; i < cmi::kManifoldStreams; ++i) {
     if (sc->aux[i]) cudaStreamDestroy(sc->aux[i]);
     if (sc->ev_join[i]) cudaEventDestroy(sc->ev_join[i]);
@@ -724,6 +746,7 @@ int cm_sdf_eval(const cm_scene* sc, const int32_t* ids, const float* poses, cons
                 void* stream) {
   NvtxRange nvtx_range("cm_sdf_eval");
   if (!sc) return fail(CM_ERR_INVALID, "cm_sdf_eval: NULL scene");
+  DeviceGuard device_guard(sc->device);
   if (B < 0 || P < 0) return fail(CM_ERR_INVALID, "cm_sdf_eval: negative size");
   if (B == 0 || P == 0) return CM_OK;   // empty batch: nothing to launch
   if (!ids || !poses || !points || !d) return fail(CM_ERR_INVALID, "cm_sdf_eval: NULL argument");
@@ -784,6 +807,7 @@ int cm_sdf_param_grad(const cm_scene* sc, const int32_t* ids, const float* poses
                       int64_t P, int32_t pmax, float* J, const float* w, float* vjp, void* stream) {
   NvtxRange nvtx_range("cm_sdf_param_grad");
   if (!sc) return fail(CM_ERR_INVALID, "cm_sdf_param_grad: NULL scene");
+  DeviceGuard device_guard(sc->device);
   if (B < 0 || P < 0 || pmax < 0) return fail(CM_ERR_INVALID, "cm_sdf_param_grad: negative size");
   if (B == 0 || P == 0) return CM_OK;
   if (!ids || !poses || !points || (!J && !vjp) || (vjp && !w))
@@ -813,6 +837,7 @@ int cm_sdf_node_pose_grad(const cm_scene* sc, const int32_t* ids, const float* p
                           int64_t P, int32_t nmax, float* J, const float* w, float* vjp, void* stream) {
   NvtxRange nvtx_range("cm_sdf_node_pose_grad");
   if (!sc) return fail(CM_ERR_INVALID, "cm_sdf_node_pose_grad: NULL scene");
+  DeviceGuard device_guard(sc->device);
   if (B < 0 || P < 0 || nmax < 0) return fail(CM_ERR_INVALID, "cm_sdf_node_pose_grad: negative size");
   if (B == 0 || P == 0) return CM_OK;
   if (!ids || !poses || !points || (!J && !vjp) || (vjp && !w))
@@ -832,6 +857,7 @@ int cm_manifold_param_vjp(const cm_scene* sc, const int32_t* pairs, int64_t n_pa
                           float* vjp, void* stream) {
   NvtxRange nvtx_range("cm_manifold_param_vjp");
   if (!sc) return fail(CM_ERR_INVALID, "cm_manifold_param_vjp: NULL scene");
+  DeviceGuard device_guard(sc->device);
   if (n_pairs < 0 || n_env < 0 || n_slot < 0) return fail(CM_ERR_INVALID, "cm_manifold_param_vjp: negative size");
   if (n_pairs == 0) return CM_OK;
   if (!pairs || !offsets || !poses || !w_depth || !vjp) return fail(CM_ERR_INVALID, "cm_manifold_param_vjp: NULL argument");
@@ -876,6 +902,7 @@ int cm_manifold_offsets(const cm_scene* sc, const int32_t* pairs, int64_t n_pair
                         void* ws, int64_t ws_bytes, void* stream) {
   NvtxRange nvtx_range("cm_manifold_offsets");
   if (!sc) return fail(CM_ERR_INVALID, "cm_manifold_offsets: NULL scene");
+  DeviceGuard device_guard(sc->device);
   if (n_pairs == 0) return CM_OK;
   if (!pairs || !offsets || !ws) return fail(CM_ERR_INVALID, "cm_manifold_offsets: NULL argument");
   if (n_pairs > (int64_t)0x7fffffff) return fail(CM_ERR_UNSUPPORTED, "cm_manifold_offsets: too many pairs");
@@ -890,6 +917,7 @@ int cm_contact_manifold(const cm_scene* sc, const int32_t* pairs, int64_t n_pair
                         int64_t n_contacts, void* stream) {
   NvtxRange nvtx_range("cm_contact_manifold");
   if (!sc || !out) return fail(CM_ERR_INVALID, "cm_contact_manifold: NULL argument");
+  DeviceGuard device_guard(sc->device);
   if (n_pairs < 0 || n_env < 0 || n_slot <= 0 || n_contacts < 0) return fail(CM_ERR_INVALID, "cm_contact_manifold: sizes");
   if (n_pairs == 0) return CM_OK;   // empty batch: nothing to launch
   if (!pairs || !offsets || !poses) return fail(CM_ERR_INVALID, "cm_contact_manifold: NULL argument");
@@ -950,6 +978,7 @@ int cm_expand_jacobian(const cm_scene* sc, const int32_t* pairs, int64_t n_pairs
                        const float* q, int64_t n_contacts, float* J, void* stream) {
   NvtxRange nvtx_range("cm_expand_jacobian");
   if (!sc || !pairs || !offsets || !poses || !W || !q || !J) return fail(CM_ERR_INVALID, "cm_expand_jacobian");
+  DeviceGuard device_guard(sc->device);
   int rc = cml::launch_expand(pairs, n_pairs, offsets, sc->dev, poses, n_env, n_slot, W, q, n_contacts, J, flags, stream);
   if (rc) return fail(rc, cml::last_cuda_error());
   return CM_OK;
@@ -960,6 +989,7 @@ int cm_manifold_pair_reduce(const cm_scene* sc, const int32_t* pairs, int64_t n_
                             const float* w_normal, float* pair_depth, float* pair_W, float* g_pose, void* stream) {
   NvtxRange nvtx_range("cm_manifold_pair_reduce");
   if (!sc || !out) return fail(CM_ERR_INVALID, "cm_manifold_pair_reduce: NULL argument");
+  DeviceGuard device_guard(sc->device);
   if (n_pairs < 0 || n_contacts < 0) return fail(CM_ERR_INVALID, "cm_manifold_pair_reduce: sizes");
   if (n_pairs == 0) return CM_OK;
   if (!pairs || !offsets) return fail(CM_ERR_INVALID, "cm_manifold_pair_reduce: NULL argument");
@@ -977,6 +1007,7 @@ int64_t cm_launch_count(void) { return cml::launch_count(); }
 
 int cm_scene_error_count(const cm_scene* sc, int64_t* count, int reset) {
   if (!sc || !count) return fail(CM_ERR_INVALID, "cm_scene_error_count: NULL argument");
+  DeviceGuard device_guard(sc->device);
   unsigned int v = 0;
   cudaError_t e = cudaMemcpy(&v, sc->dev.err, sizeof(v), cudaMemcpyDeviceToHost);   // synchronises the device
   if (e != cudaSuccess) return fail(CM_ERR_CUDA, std::string("cm_scene_error_count: ") + cudaGetErrorString(e));

@@ -1923,15 +1923,18 @@ static int launch_tier(MfArgs a, int class_mask, int max_V, int max_E, int64_t n
   // occupancy)
   int stage_bytes = (int)(face_stage_floats(max_V, max_E, TIER) * 4);
   {
-    static int configured = 0;
+    // (the attribute is per device and per kernel: set on every call for the
+    // current device, no process-wide cache; a failure disables the staging)
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (stage_bytes + (int)sizeof(UnitCtx) + 1024 > optin) {
       stage_bytes = 0;
-    } else if (stage_bytes > configured) {
-      cudaFuncSetAttribute(k_mf_faces<TIER, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
-      configured = stage_bytes;
+    } else if (stage_bytes > 48 * 1024 &&
+               cudaFuncSetAttribute(k_mf_faces<TIER, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    stage_bytes) != cudaSuccess) {
+      cudaGetLastError();
+      stage_bytes = 0;
     }
   }
   // chunk k runs on stream k % n_streams in that stream's scratch region, so

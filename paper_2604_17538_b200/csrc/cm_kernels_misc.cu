@@ -33,13 +33,16 @@ int check_launch(const char* what) {
   }
   return CM_OK;
 }
-int num_sms() {
-  static int n = 0;
+int num_sms() {   // of the current device (cached per device)
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  int n = cache[dev];
   if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+    cache[dev] = n;
   }
   return n;
 }
