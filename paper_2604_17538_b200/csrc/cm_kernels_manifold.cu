@@ -1451,8 +1451,9 @@ __device__ __forceinline__ void mf_faces_unit(const MfArgs& a, const UnitCtx& U,
 // past the class's count exit after one broadcast load, without a barrier).
 // A persistent variant (resident CTAs pulling units from an atomic counter)
 // measured slower: C5 -5%, C4 -2%, C2 -10%.
-__device__ __forceinline__ bool list_unit(const MfArgs& a, int list, UnitCtx& U, int& u) {
-  const int b = blockIdx.x;
+__device__ __forceinline__ bool list_unit(const MfArgs& a, int list, UnitCtx& U, int& u, int b = -1) {
+  if (b < 0) b = blockIdx.x;
+  if (list < 0 && b >= a.nb) return false;
   if (list >= 0) {
     if (b >= __ldcg(a.cls_count + list)) return false;
     u = __ldcg(a.cls_list + (int64_t)list * a.chunk + b);
@@ -1467,19 +1468,32 @@ __device__ __forceinline__ bool list_unit(const MfArgs& a, int list, UnitCtx& U,
   return true;
 }
 
+// CM_MF_UPC units per CTA (list entries blockIdx.x * UPC + r): fewer CTAs
+// per launch, so that the launches of a chunk's absent classes (their CTAs
+// exit after one broadcast load) cost less
+#ifndef CM_MF_UPC
+#define CM_MF_UPC 1
+#endif
 template <int TIER, int XP>
 __global__ void __maxnreg__((RegCap<TIER, XP>::VERTICES)) k_mf_vertices(const MfArgs a) {
   __shared__ UnitCtx U;
   int u;
-  if (list_unit(a, XP, U, u)) mf_vertices_unit<TIER, XP>(a, U, u);
+  for (int r = 0; r < CM_MF_UPC; ++r) {
+    if (!list_unit(a, XP, U, u, blockIdx.x * CM_MF_UPC + r)) return;
+    mf_vertices_unit<TIER, XP>(a, U, u);
+    if (CM_MF_UPC > 1) __syncthreads();
+  }
 }
 template <int TIER, int XP>
 __global__ void __maxnreg__((RegCap<TIER, XP>::TRACES)) k_mf_traces(const MfArgs a) {
   __shared__ UnitCtx U;
   int u;
-  if (!list_unit(a, XP, U, u)) return;
-  if constexpr (TIER <= 2 && CM_TRACE6) mf_traces_unit_n<TIER, XP>(a, U, u);
-  else mf_traces_unit<TIER, XP>(a, U, u);
+  for (int r = 0; r < CM_MF_UPC; ++r) {
+    if (!list_unit(a, XP, U, u, blockIdx.x * CM_MF_UPC + r)) return;
+    if constexpr (TIER <= 2 && CM_TRACE6) mf_traces_unit_n<TIER, XP>(a, U, u);
+    else mf_traces_unit<TIER, XP>(a, U, u);
+    if (CM_MF_UPC > 1) __syncthreads();
+  }
 }
 template <int TIER, int XP> struct EdgeRegs {   // the larger of the trace and midpoint budgets
   static constexpr int R0 = RegCap<TIER, XP>::MIDPOINTS > RegCap<TIER, XP>::TRACES ? RegCap<TIER, XP>::MIDPOINTS
@@ -1505,14 +1519,19 @@ __global__ void __maxnreg__((RegCap<TIER, XP>::MIDPOINTS)) k_mf_midpoints(const 
   __shared__ uint64_t bar;
   if (STAGED && threadIdx.x == 0) mbar_init(&bar, 1);   // published by list_unit's barrier
   int u;
-  if (!list_unit(a, XP, U, u)) return;
+  if (!list_unit(a, XP, U, u, STAGED ? (int)blockIdx.x : (int)blockIdx.x * CM_MF_UPC)) return;
   if constexpr (STAGED) {
     const float* se = a.scratch + (int64_t)u * a.slot + (int64_t)vrec(TIER) * U.SA.V;
     if (threadIdx.x == 0) bulk_g2s(msm, se, (uint32_t)(U.SA.E * erec(TIER)) * 4u, &bar);
     mbar_wait(&bar, 0u);
     mf_midpoints_unit<TIER, XP>(a, U, u, msm);
   } else {
-    mf_midpoints_unit<TIER, XP>(a, U, u, nullptr, nullptr, (TIER == 2 && CM_MF_MID_PREFETCH) ? msm : nullptr);
+    for (int r = 0;;) {
+      mf_midpoints_unit<TIER, XP>(a, U, u, nullptr, nullptr, (TIER == 2 && CM_MF_MID_PREFETCH) ? msm : nullptr);
+      if (++r >= CM_MF_UPC) break;
+      __syncthreads();
+      if (!list_unit(a, XP, U, u, blockIdx.x * CM_MF_UPC + r)) return;
+    }
   }
 }
 // Midpoints and face fusion in one kernel per SDF class (reduced mode, tiers
@@ -1662,7 +1681,15 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS) __maxnreg__((FaceRegs<TIER>
       if (bytes > 0 && c.valid) bulk_prefetch_l2(a.scratch + v * a.slot, bytes);
     }
   }
-  if (list_unit(a, -1, U, u) && U.valid) mf_faces_unit<TIER, STAGED>(a, U, u, fsm, &bar, 0u);
+  if constexpr (STAGED) {
+    if (list_unit(a, -1, U, u) && U.valid) mf_faces_unit<TIER, STAGED>(a, U, u, fsm, &bar, 0u);
+  } else {
+    for (int r = 0; r < CM_MF_UPC; ++r) {
+      if (!list_unit(a, -1, U, u, blockIdx.x * CM_MF_UPC + r)) return;
+      if (U.valid) mf_faces_unit<TIER, STAGED>(a, U, u, fsm, &bar, 0u);
+      if (CM_MF_UPC > 1) __syncthreads();
+    }
+  }
 }
 
 // ---- shape-parameter VJP of the manifold depths (f4, reading #48) ----------
@@ -1876,7 +1903,8 @@ static int launch_sdf_phases(MfArgs& a, int64_t nb, int T, int max_V, int max_E,
     k_mf_small<TIER, XP><<<(unsigned)nb, T, 0, st>>>(a);
     return check_launch("k_mf_small");
   }
-  k_mf_vertices<TIER, XP><<<(unsigned)nb, T, 0, st>>>(a);
+  const unsigned gu = (unsigned)((nb + CM_MF_UPC - 1) / CM_MF_UPC);   // CTAs of CM_MF_UPC units
+  k_mf_vertices<TIER, XP><<<gu, T, 0, st>>>(a);
   int rc = check_launch("k_mf_vertices");
   if (rc) return rc;
   if constexpr (TIER <= 2 && CM_MF_FUSE_EDGES && CM_TRACE6) {
@@ -1885,7 +1913,7 @@ static int launch_sdf_phases(MfArgs& a, int64_t nb, int T, int max_V, int max_E,
       return check_launch("k_mf_edges");
     }
   }
-  k_mf_traces<TIER, XP><<<(unsigned)nb, T, 0, st>>>(a);
+  k_mf_traces<TIER, XP><<<gu, T, 0, st>>>(a);
   if ((rc = check_launch("k_mf_traces"))) return rc;
   if constexpr (TIER <= 2) {
     const int fb = midfaces_bytes(TIER, a.mode, max_V, max_E);
@@ -1902,7 +1930,7 @@ static int launch_sdf_phases(MfArgs& a, int64_t nb, int T, int max_V, int max_E,
       cudaFuncSetAttribute(k_mf_midpoints<TIER, XP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mid_bytes);
     k_mf_midpoints<TIER, XP, true><<<(unsigned)nb, T, mid_bytes, st>>>(a);
   } else {
-    k_mf_midpoints<TIER, XP, false><<<(unsigned)nb, T, (TIER == 2 && CM_MF_MID_PREFETCH) ? T * 80 : 0, st>>>(a);
+    k_mf_midpoints<TIER, XP, false><<<gu, T, (TIER == 2 && CM_MF_MID_PREFETCH) ? T * 80 : 0, st>>>(a);
   }
   return check_launch("k_mf_midpoints");
 }
@@ -1976,7 +2004,7 @@ static int launch_tier(MfArgs a, int class_mask, int max_V, int max_E, int64_t n
       if (stage_bytes > 0 && (stage_bytes <= kStageSmallBytes || nb < 8 * (int64_t)num_sms()))
         k_mf_faces<TIER, true><<<(unsigned)nb, T, stage_bytes, st>>>(a);
       else
-        k_mf_faces<TIER, false><<<(unsigned)nb, T, 0, st>>>(a);
+        k_mf_faces<TIER, false><<<(unsigned)((nb + CM_MF_UPC - 1) / CM_MF_UPC), T, 0, st>>>(a);
       if ((rc = check_launch("k_mf_faces"))) return rc;
     }
   }
