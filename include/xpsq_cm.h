@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define CM_ABI_VERSION 5
+#define CM_ABI_VERSION 6
 #define CM_MAX_PLANES 8      /* half-spaces per PSQ / XPSQ cross-section      */
 #define CM_MAX_CHILDREN 32   /* children per boolean node                     */
 #define CM_MAX_DEPTH 3       /* nesting of boolean nodes in one shape         */
@@ -105,7 +105,10 @@ typedef struct cm_node {
 
 /* A shape: optional SDF (n_nodes > 0) and optional sampled surface (the
  * paper's mesh side): local-frame vertices [V,3] and triangles [F,3]
- * (int32 vertex indices).  Host pointers, copied at scene creation. */
+ * (int32 vertex indices).  Host pointers, copied at scene creation.  With
+ * n_faces == 0 and sample_res > 0 the library tessellates the shape's single
+ * SQ / PSQ / XPSQ node itself (cm_tessellate, placed by the node's pose):
+ * SURVEY §8(b) `sample_res`. */
 typedef struct cm_shape_desc {
   int32_t n_nodes;
   const cm_node* nodes;
@@ -113,7 +116,22 @@ typedef struct cm_shape_desc {
   const float* vertices;
   int32_t n_faces;
   const int32_t* faces;
+  int32_t sample_res;
 } cm_shape_desc;
+
+/* Library-side sampled surface of one SQ / PSQ / XPSQ node in its own frame
+ * (host; SURVEY §8(b) sample_res): SQ a cube-sphere with res x res
+ * cells per face on the parametric surface of Eq. (1) (V = 6 res^2 + 2,
+ * F = 12 res^2); PSQ the same with the vertices outside each plane pulled
+ * radially onto it (planes must keep the centre inside: h < 0); XPSQ a tube
+ * of 2 res + 1 rings x 4 res points on the t = 0 cross-section along the
+ * spline (Eq. (5)) plus two end caps (V = 4 res (2 res + 1) + 2).  Endpoint-0
+ * schedules.  n_vertices / n_faces (host) receive the counts; vertices
+ * [3V] and faces [3F] (host) are filled when both are non-NULL (size them by
+ * a first call with NULL).  CM_ERR_INVALID (bad node / res outside
+ * [1, 256]), CM_ERR_UNSUPPORTED (half-space, boolean node, point spline). */
+int cm_tessellate(const cm_node* node, int32_t res, float* vertices, int32_t* faces, int32_t* n_vertices,
+                  int32_t* n_faces);
 
 /* Temperatures of the smooth operators (§II-A; one generic tau in
  * the paper, five named ones here — DESIGN.md reading #1), all > 0:

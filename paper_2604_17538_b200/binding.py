@@ -27,7 +27,7 @@ EXPORTS = ["cm_version", "cm_last_error", "cm_scene_create", "cm_scene_destroy",
            "cm_shape_topology", "cm_sdf_eval", "cm_manifold_size", "cm_manifold_offsets_workspace",
            "cm_manifold_offsets", "cm_contact_manifold", "cm_expand_jacobian", "cm_launch_count",
            "cm_scene_error_count", "cm_manifold_pair_reduce", "cm_node_pose_layout", "cm_sdf_node_pose_grad",
-           "cm_manifold_param_vjp"]
+           "cm_manifold_param_vjp", "cm_tessellate"]
 
 
 class cm_node(C.Structure):
@@ -39,7 +39,8 @@ class cm_node(C.Structure):
 
 class cm_shape_desc(C.Structure):
     _fields_ = [("n_nodes", C.c_int32), ("nodes", C.POINTER(cm_node)), ("n_vertices", C.c_int32),
-                ("vertices", C.POINTER(C.c_float)), ("n_faces", C.c_int32), ("faces", C.POINTER(C.c_int32))]
+                ("vertices", C.POINTER(C.c_float)), ("n_faces", C.c_int32), ("faces", C.POINTER(C.c_int32)),
+                ("sample_res", C.c_int32)]
 
 
 class cm_smooth_params(C.Structure):
@@ -91,10 +92,26 @@ def lib():
         if hasattr(L, "cm_sdf_node_pose_grad"):
             L.cm_node_pose_layout.argtypes = [p, p, p]
             L.cm_sdf_node_pose_grad.argtypes = [p, p, p, p, i64, i64, i32, p, p, p, p]
+        if hasattr(L, "cm_tessellate"):
+            L.cm_tessellate.argtypes = [p, i32, p, p, p, p]
         if hasattr(L, "cm_manifold_param_vjp"):
             L.cm_manifold_param_vjp.argtypes = [p, p, i64, p, p, i64, i32, u32, p, p, p]
         _lib = L
     return _lib
+
+
+def tessellate(node: dict, res: int):
+    """Library-side sampled surface of one SQ / PSQ / XPSQ node (host call,
+    no GPU needed): (vertices [V,3] float32, faces [F,3] int32)."""
+    L = lib()
+    cn = _pack_node(node)
+    nv, nf = C.c_int32(), C.c_int32()
+    _check(L.cm_tessellate(C.byref(cn), int(res), None, None, C.byref(nv), C.byref(nf)), "cm_tessellate")
+    v = np.zeros((nv.value, 3), np.float32)
+    f = np.zeros((nf.value, 3), np.int32)
+    _check(L.cm_tessellate(C.byref(cn), int(res), v.ctypes.data_as(C.c_void_p), f.ctypes.data_as(C.c_void_p),
+                           C.byref(nv), C.byref(nf)), "cm_tessellate")
+    return v, f
 
 
 def _check(rc, what):
@@ -171,6 +188,8 @@ class Scene:
                 d.n_vertices, d.n_faces = len(v), len(f)
                 d.vertices = v.ctypes.data_as(C.POINTER(C.c_float))
                 d.faces = f.ctypes.data_as(C.POINTER(C.c_int32))
+            elif getattr(sh, "sample_res", 0):
+                d.sample_res = int(sh.sample_res)   # library-side tessellation (cm_tessellate)
         sp = cm_smooth_params(smooth["tau_cmp"], smooth["tau_min"], smooth["tau_clip_alpha"], smooth["tau_clip_t"],
                               smooth["tau_delta"], int(smooth["trace_iters"]))
         h = C.c_void_p()

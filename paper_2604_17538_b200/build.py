@@ -15,7 +15,7 @@ LIB = os.path.join(HERE, "libxpsqcm.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
-SOURCES = ["cm_kernels_sdf.cu", "cm_kernels_manifold.cu", "cm_kernels_misc.cu", "cm_host.cpp"]
+SOURCES = ["cm_kernels_sdf.cu", "cm_kernels_manifold.cu", "cm_kernels_misc.cu", "cm_host.cpp", "cm_tessellate.cpp"]
 
 
 def _deps():

@@ -357,8 +357,46 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
   sc->edges.resize(n_shapes);
   sc->face_edges.resize(n_shapes);
 
+  std::vector<std::vector<float>> tess_v(n_shapes);
+  std::vector<std::vector<int32_t>> tess_f(n_shapes);
   for (int s = 0; s < n_shapes; ++s) {
-    const cm_shape_desc& d = shapes[s];
+    cm_shape_desc dloc = shapes[s];
+    if (dloc.n_faces == 0 && dloc.sample_res > 0) {
+      // library-side sampled surface (SURVEY §8(b) sample_res): the single
+      // SQ / PSQ / XPSQ node tessellated in its frame, placed by its pose
+      if (dloc.n_nodes != 1 || !dloc.nodes) {
+        delete sc;
+        return fail(CM_ERR_UNSUPPORTED, "shape " + std::to_string(s) + ": sample_res needs a single SQ / PSQ / XPSQ node");
+      }
+      int32_t nv = 0, nf = 0;
+      int trc = cm_tessellate(dloc.nodes, dloc.sample_res, nullptr, nullptr, &nv, &nf);
+      if (trc == CM_OK) {
+        tess_v[s].resize(3 * (size_t)nv);
+        tess_f[s].resize(3 * (size_t)nf);
+        trc = cm_tessellate(dloc.nodes, dloc.sample_res, tess_v[s].data(), tess_f[s].data(), &nv, &nf);
+      }
+      if (trc != CM_OK) {
+        delete sc;
+        return fail(trc, "shape " + std::to_string(s) + ": cannot tessellate this node (cm_tessellate)");
+      }
+      double q[4] = {dloc.nodes[0].pose[3], dloc.nodes[0].pose[4], dloc.nodes[0].pose[5], dloc.nodes[0].pose[6]};
+      const double qn = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+      for (double& c : q) c /= qn;
+      const double w = q[0], x = q[1], y = q[2], z = q[3];
+      const double R[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                           2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                           2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
+      for (int32_t v = 0; v < nv; ++v) {
+        const double p[3] = {tess_v[s][3 * v], tess_v[s][3 * v + 1], tess_v[s][3 * v + 2]};
+        for (int i = 0; i < 3; ++i)
+          tess_v[s][3 * v + i] = (float)(R[3 * i] * p[0] + R[3 * i + 1] * p[1] + R[3 * i + 2] * p[2] + dloc.nodes[0].pose[i]);
+      }
+      dloc.n_vertices = nv;
+      dloc.vertices = tess_v[s].data();
+      dloc.n_faces = nf;
+      dloc.faces = tess_f[s].data();
+    }
+    const cm_shape_desc& d = dloc;
     ShapeRec& r = recs[s];
     std::memset(&r, 0, sizeof(r));
     r.prog_begin = (int32_t)prog.size();
@@ -600,7 +638,14 @@ int cm_scene_create(const cm_shape_desc* shapes, int32_t n_shapes, const cm_smoo
   // broad-phase bounds per shape (f2): float, rounded outward
   std::vector<float4> bounds(2 * (size_t)n_shapes);
   for (int s = 0; s < n_shapes; ++s) {
-    const cm_shape_desc& d = shapes[s];
+    cm_shape_desc dloc = shapes[s];
+    if (!tess_f[s].empty()) {   // the library-side tessellation
+      dloc.n_vertices = (int32_t)(tess_v[s].size() / 3);
+      dloc.vertices = tess_v[s].data();
+      dloc.n_faces = (int32_t)(tess_f[s].size() / 3);
+      dloc.faces = tess_f[s].data();
+    }
+    const cm_shape_desc& d = dloc;
     float4 mb = make_float4(0.f, 0.f, 0.f, -1.f), sb = make_float4(0.f, 0.f, 0.f, INFINITY);
     if (d.n_faces > 0) {
       double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY}, c[3], r = 0.0;

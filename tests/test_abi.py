@@ -36,7 +36,7 @@ def test_exports_every_declared_symbol(L):
 
 
 def test_version_and_launch_counter(L):
-    assert L.cm_version() == 5   # 3: cm_scene_error_count; 4: node-pose derivatives; 5: manifold parameter VJP
+    assert L.cm_version() == 6   # 3: error count; 4: node-pose derivatives; 5: manifold parameter VJP; 6: sample_res
     # no launch happens at load (a process that already ran GPU tests counts those)
     n = L.cm_launch_count()
     assert n >= 0

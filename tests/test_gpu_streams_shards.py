@@ -182,3 +182,40 @@ def test_manifold_cuda_graph_capture(cuda, wl):
         torch.cuda.synchronize()
         for k in ref:
             assert _same(out[k], ref[k]), (rep, k)
+
+
+@pytest.mark.parametrize("rotated", [False, True])
+def test_scene_sample_res_equals_explicit_mesh(cuda, rotated):
+    """cm_shape_desc.sample_res: a shape whose sampled surface
+    the library tessellates itself (placed by its root node's pose) gives the
+    manifold of the same shape given the explicit mesh of cm_tessellate
+    placed by that pose: bit for bit at the identity pose, within FP32
+    rounding of the vertex placement otherwise."""
+    torch = cuda
+    import copy
+    from paper_2604_17538_b200 import binding
+    sc = synth.c1_scene()
+    box, ground = sc.shapes
+    pose = [0.01, -0.02, 0.005, 0.96, 0.1, 0.2, 0.17] if rotated else [0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0]
+    root = synth.sq((0.2, 0.15, 0.1), (0.3, 0.3), pose=pose)
+    node = synth.flatten(root)[0]
+    v, f = binding.tessellate(node, 3)
+    pz = np.asarray(node["pose"], dtype=np.float32).astype(np.float64)   # (the FP32 node pose)
+    R = synth.quats_to_mats((pz[3:] / np.linalg.norm(pz[3:]))[None, :])[0]
+    vt = (v.astype(np.float64) @ R.T + pz[:3]).astype(np.float32)
+    explicit = synth.make_shape("box_mesh", root, (vt, f))
+    implicit = copy.deepcopy(explicit)
+    implicit.vertices, implicit.faces = None, None
+    implicit.sample_res = 3
+    outs = []
+    for shp in (explicit, implicit):
+        S = binding.Scene([shp, ground], sc.smooth)
+        assert S.counts(0) == (len(v), 3 * (len(v) - 2), len(f))
+        pairs, poses, offs, C = _inputs(S, sc, torch)
+        outs.append({k: o.cpu() for k, o in S.contact_manifold(pairs, offs, C, poses, 2).items()})
+    for k in outs[0]:
+        if rotated and outs[0][k].dtype == torch.float32:
+            a, b = outs[0][k].double(), outs[1][k].double()
+            assert torch.allclose(a, b, rtol=1e-3, atol=1e-5 * max(1.0, float(a.abs().max()))), k
+        elif not rotated:
+            assert _same(outs[0][k], outs[1][k]), k

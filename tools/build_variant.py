@@ -18,7 +18,7 @@ os.makedirs(bdir, exist_ok=True)
 NVCC = "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I" + src, "-I" + os.path.join(ROOT, "include")]
-srcs = ["cm_kernels_sdf.cu", "cm_kernels_manifold.cu", "cm_kernels_misc.cu", "cm_host.cpp"]
+srcs = ["cm_kernels_sdf.cu", "cm_kernels_manifold.cu", "cm_kernels_misc.cu", "cm_host.cpp", "cm_tessellate.cpp"]
 
 
 def run(f):
