@@ -806,6 +806,26 @@ def test_pair_reduce(cuda, oracle_mod, cfg):
     assert nf == 0, json.dumps(rep, indent=1)
 
 
+@pytest.mark.parametrize("mode", [4, 8])
+def test_broad_phase_modes(cuda, oracle_mod, mode):
+    """CM_BROAD_PHASE with full mode (candidate rows) and two-sided manifolds
+    (each side culled on its own bound): every row of a 128-pair C6 sample
+    against the oracle's same mode, culled and kept alike."""
+    from paper_2604_17538_b200 import binding
+    sc = synth.c6_scene(8)
+    osc = oracle_mod.OracleScene(sc)
+    gb, S = PT.gpu_manifold(sc, 2, mode=binding.BROAD_PHASE | mode)
+    assert 0.3 < float((gb["dom"] == -2).mean()) < 0.99
+    rng = np.random.default_rng(29 + mode)
+    idx = np.sort(rng.choice(len(sc.pairs), 128, replace=False))
+    nf, rep = PT.manifold_parity(sc, osc, gb, 2, idx, rng, sc.ell, mode=16 | mode)
+    _report("broad_phase_mode%d" % mode, rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+    # (culled rows carry six equal candidate depths: the dom comparison skips
+    # them as near ties, which is not a conditioning exclusion)
+    assert PT.excluded_fraction([r for r in rep if r["field"] != "dom"]) < 0.01
+
+
 def test_broad_phase_c6(cuda, oracle_mod):
     """CM_BROAD_PHASE (f2) on C6 (two 18-part SQ objects, 324 part pairs per
     env): the GPU's culled set equals the oracle's (outside a 1e-5 ell band
