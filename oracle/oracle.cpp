@@ -545,6 +545,7 @@ thread_local int g_seed_node = -1, g_seed_slot = -1;
 // g_seed takes their component 0 (the first-order q-jet D12 and the nested
 // candidate jet N12 = Dual<D3, 12>), so ddepth[., 0] = d depth / d param
 thread_local bool g_param_comp0 = false;
+thread_local int g_param_shape = -1;   // the seeded parameters' shape (its SDF sides only)
 template <class T> struct Seeder { static void apply(T&) {} };
 template <> struct Seeder<Dual<double, 1>> { static void apply(Dual<double, 1>& x) { x.d[0] = 1.0; } };
 template <> struct Seeder<Dual<double, 12>> {
@@ -986,6 +987,16 @@ int ora_contact_manifold(void* s, const int* pairs, long n_pairs, const double* 
   for (long pi = 0; pi < n_pairs; ++pi) {
    long row0 = off[pi];
    for (int side = 0; side < (two ? 2 : 1); ++side) {
+    // (shape-parameter mode: a side whose SDF shape is not the seeded one
+    // evaluates without the seed)
+    struct SeedSuspend {
+      int saved = -2;
+      ~SeedSuspend() { if (saved != -2) g_seed_node = saved; }
+    } seed_suspend;
+    if (g_param_comp0 && pairs[5 * pi + 4 - side] != g_param_shape) {
+      seed_suspend.saved = g_seed_node;
+      g_seed_node = -1;
+    }
     // "A" below is the sampled body of this side, "B" the SDF body
     const int* pr = pairs + 5 * pi;
     const Shape& SA = sc->shapes[pr[3 + side]];
@@ -1333,39 +1344,48 @@ int ora_shape_node_count(void* s, int shape) { return (int)((Scene*)s)->shapes[s
 int ora_manifold_param_jac(void* s, const int* pairs, long n_pairs, const double* poses, long n_env, int n_slot,
                            int mode, int pmax, double* Jd) {
   Scene* sc = (Scene*)s;
-  if (mode & (8 | 16)) return -1;   // two-sided / broad phase: not parametrised here
-  const bool full = (mode & 4) != 0;
+  const bool full = (mode & 4) != 0, two = (mode & 8) != 0;
+  auto count = [&](int shape) { const Mesh& m = sc->shapes[shape].mesh; return full ? (long)m.V + m.E : (long)m.F; };
   std::vector<long> off(n_pairs + 1, 0);
-  for (long i = 0; i < n_pairs; ++i) {
-    const Mesh& m = sc->shapes[pairs[5 * i + 3]].mesh;
-    off[i + 1] = off[i] + (full ? (long)m.V + m.E : (long)m.F);
-  }
+  for (long i = 0; i < n_pairs; ++i)
+    off[i + 1] = off[i] + count(pairs[5 * i + 3]) + (two ? count(pairs[5 * i + 4]) : 0);
 #pragma omp parallel for schedule(dynamic, 1)
   for (long pi = 0; pi < n_pairs; ++pi) {
     const long nr = off[pi + 1] - off[pi];
     std::vector<double> pt(3 * nr), nm(3 * nr), dp(nr), W(nr), q(3 * nr), dd(12 * nr), dn(36 * nr), J(36 * nr),
         z(6 * nr), dc(6 * nr), g(6 * nr);
     std::vector<int> dom(nr);
-    const Shape& SB = sc->shapes[pairs[5 * pi + 4]];
-    int k = 0;
-    for (int ni = 0; ni < (int)SB.nodes.size(); ++ni) {
-      const int cnt = node_param_count(SB.nodes[ni]);
-      for (int slot = 0; slot < cnt && k < pmax; ++slot, ++k) {
-        g_seed_node = ni;
-        g_seed_slot = slot;
-        g_param_comp0 = true;
-        // (nested inside this parallel loop the manifold's own loop runs on
-        // this thread, which holds the thread-local seeds)
-        ora_contact_manifold(s, pairs + 5 * pi, 1, poses, n_env, n_slot, pt.data(), nm.data(), dp.data(), W.data(),
-                             q.data(), dd.data(), dn.data(), dom.data(), J.data(), z.data(), dc.data(), g.data(),
-                             mode, 0);
-        g_param_comp0 = false;
-        for (long r = 0; r < nr; ++r) Jd[(off[pi] + r) * pmax + k] = dd[12 * r + 0];
+    for (long r = 0; r < nr; ++r)
+      for (int k = 0; k < pmax; ++k) Jd[(off[pi] + r) * pmax + k] = 0.0;
+    // rows of side 0 (SDF shape B) then side 1 (SDF shape A, two-sided)
+    const long n0 = count(pairs[5 * pi + 3]);
+    for (int side = 0; side < (two ? 2 : 1); ++side) {
+      const int shp = pairs[5 * pi + 4 - side];
+      if (side == 1 && shp == pairs[5 * pi + 4]) continue;   // (A == B: done with side 0)
+      const Shape& SB = sc->shapes[shp];
+      int k = 0;
+      for (int ni = 0; ni < (int)SB.nodes.size(); ++ni) {
+        const int cnt = node_param_count(SB.nodes[ni]);
+        for (int slot = 0; slot < cnt && k < pmax; ++slot, ++k) {
+          g_seed_node = ni;
+          g_seed_slot = slot;
+          g_param_comp0 = true;
+          g_param_shape = shp;
+          // (nested inside this parallel loop the manifold's own loop runs on
+          // this thread, which holds the thread-local seeds)
+          ora_contact_manifold(s, pairs + 5 * pi, 1, poses, n_env, n_slot, pt.data(), nm.data(), dp.data(), W.data(),
+                               q.data(), dd.data(), dn.data(), dom.data(), J.data(), z.data(), dc.data(), g.data(),
+                               mode, 0);
+          g_param_comp0 = false;
+          g_param_shape = -1;
+          for (long r = 0; r < nr; ++r) {
+            const int row_shape = r < n0 ? pairs[5 * pi + 4] : pairs[5 * pi + 3];
+            if (row_shape == shp) Jd[(off[pi] + r) * pmax + k] = dd[12 * r + 0];
+          }
+        }
       }
     }
     g_seed_node = g_seed_slot = -1;
-    for (; k < pmax; ++k)
-      for (long r = 0; r < nr; ++r) Jd[(off[pi] + r) * pmax + k] = 0.0;
   }
   return 0;
 }

@@ -304,24 +304,30 @@ class OracleScene:
         return J
 
     def manifold_param_jac(self, pairs=None, poses=None, mode=0, pmax=None):
-        """Jd [rows, pmax]: d depth(row) / d shape parameter of the pair's SDF
-        shape B (one-sided modes; the layout of sdf_param_grad), from the
-        literal manifold with the parameter seeded (f4, reading #48)."""
+        """Jd [rows, pmax]: d depth(row) / d shape parameter of the row's SDF
+        shape (B for the pair's first half, A for the second half of a
+        two-sided manifold; the layout of sdf_param_grad), from the literal
+        manifold with the parameter seeded (f4, reading #48).  Broad-phase
+        culled rows have zero rows (their depth is a certified bound, not a
+        differentiated output)."""
         sc = self.scene
         pairs = np.ascontiguousarray(sc.pairs if pairs is None else pairs, dtype=np.int32)
         poses = np.ascontiguousarray(sc.poses if poses is None else poses, dtype=np.float64)
         n_env, n_slot = poses.shape[0], poses.shape[1]
+        two = bool(mode & 8)
         if pmax is None:
-            pmax = max(self.param_count(int(b)) for b in np.unique(pairs[:, 4]))
+            sdf = np.unique(np.concatenate([pairs[:, 4], pairs[:, 3]] if two else [pairs[:, 4]]))
+            pmax = max(self.param_count(int(b)) for b in sdf)
         full = bool(mode & 4)
         rows = 0
-        for a in pairs[:, 3]:
-            V, E, F = self.mesh_counts(int(a))
-            rows += V + E if full else F
+        for pr in pairs:
+            for a in ((pr[3], pr[4]) if two else (pr[3],)):
+                V, E, F = self.mesh_counts(int(a))
+                rows += V + E if full else F
         Jd = np.zeros((rows, pmax))
         rc = lib().ora_manifold_param_jac(self.h, _ptr(pairs), len(pairs), _ptr(poses), n_env, n_slot, int(mode),
                                           int(pmax), _ptr(Jd))
-        assert rc == 0, "one-sided modes only"
+        assert rc == 0
         return Jd
 
     def manifold_d2depth(self, pairs=None, poses=None, n_threads=0, mode=0):

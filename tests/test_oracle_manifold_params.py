@@ -100,3 +100,34 @@ def test_manifold_param_jac_fd(oracle_mod, kind):
         assert np.allclose(Jd[:, k], fd, rtol=1e-4, atol=1e-5), (kind, ni, sl, np.abs(Jd[:, k] - fd).max())
         touched += np.abs(fd).max() > 1e-3
     assert touched >= 2
+
+
+def test_two_sided_and_broad_halves(oracle_mod):
+    """Two-sided: the first half's rows are the one-sided manifold's (the
+    parameters of B) and the second half's are the transposed pair's
+    one-sided rows (the parameters of A): the seed reaches only the side
+    whose SDF it parametrises.  Broad phase: culled rows are zero, kept rows
+    those of the all-edges manifold."""
+    O = oracle_mod
+    sc = synth.c1_scene()
+    osc = O.OracleScene(sc)
+    pair = sc.pairs[:1]                                   # box sampled on the ground, both ways
+    pmax = max(osc.param_count(0), osc.param_count(1))
+    two = osc.manifold_param_jac(pair, mode=8, pmax=pmax)
+    one = osc.manifold_param_jac(pair, mode=0, pmax=pmax)
+    tr = pair[:, [0, 2, 1, 4, 3]]
+    one_t = osc.manifold_param_jac(tr, mode=0, pmax=pmax)
+    assert two.shape[0] == one.shape[0] + one_t.shape[0]
+    assert np.allclose(two[:len(one)], one, atol=1e-12) and np.allclose(two[len(one):], one_t, atol=1e-12)
+    assert np.abs(one).max() > 0.1 and np.abs(one_t).max() > 0.1
+    # broad phase (the ground patch sampled against the box, whose SDF is
+    # bounded): a far-apart copy is culled (zero rows), the contact pair kept
+    pb = sc.pairs[1:2]
+    poses = sc.poses.astype(np.float64).copy()
+    far = poses.copy()
+    far[0, 0, 2] += 5.0
+    Jb = osc.manifold_param_jac(pb, far, mode=16, pmax=pmax)
+    assert np.abs(Jb).max() == 0.0
+    Jk = osc.manifold_param_jac(pb, poses, mode=16, pmax=pmax)
+    assert np.allclose(Jk, osc.manifold_param_jac(pb, poses, mode=0, pmax=pmax), atol=1e-12)
+    assert np.abs(Jk).max() > 0.1
