@@ -336,10 +336,11 @@ int cm_expand_jacobian(const cm_scene* scene, const int32_t* pairs, int64_t n_pa
  * from phi_s is differentiated: the candidate values, the sphere-trace
  * iterates and soft clips, the edge points and the face softmax
  * (P:158-161); the sampled surface is data.  pairs / offsets / poses /
- * n_env / n_slot as for cm_contact_manifold with the same flags; one-sided
- * modes only (reduced, or CM_FULL_MODE: the rows' candidate depths), else
- * CM_ERR_UNSUPPORTED (also when a shape is not parametrised, or with more
- * than 16 trace iterations).  w_depth [C] and vjp (accumulated: zero it
+ * n_env / n_slot as for cm_contact_manifold with the same flags (reduced or
+ * CM_FULL_MODE: the rows' candidate depths; CM_TWO_SIDED: each half with
+ * respect to its own SDF shape, B then A; CM_BROAD_PHASE: culled rows add
+ * nothing); CM_ERR_UNSUPPORTED when a shape is not parametrised or with more
+ * than 16 trace iterations.  w_depth [C] and vjp (accumulated: zero it
  * first; FP32 atomics, order not fixed) are device pointers.  Invalid pair
  * records are skipped (counted by cm_contact_manifold's validation rules). */
 int cm_manifold_param_vjp(const cm_scene* scene, const int32_t* pairs, int64_t n_pairs, const int64_t* offsets,

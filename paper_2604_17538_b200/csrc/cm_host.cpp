@@ -907,8 +907,6 @@ int cm_manifold_param_vjp(const cm_scene* sc, const int32_t* pairs, int64_t n_pa
   if (n_pairs == 0) return CM_OK;
   if (!pairs || !offsets || !poses || !w_depth || !vjp) return fail(CM_ERR_INVALID, "cm_manifold_param_vjp: NULL argument");
   if (((uintptr_t)poses & 15) != 0) return fail(CM_ERR_INVALID, "cm_manifold_param_vjp: poses must be 16-byte aligned");
-  if (flags & (CM_TWO_SIDED | CM_BROAD_PHASE))
-    return fail(CM_ERR_UNSUPPORTED, "cm_manifold_param_vjp: one-sided modes only (reduced or CM_FULL_MODE)");
   int pmax = 0;
   for (size_t s = 0; s < sc->param_count.size(); ++s) {
     if (sc->param_count[s] < 0 && sc->shapes[s].has_sdf)
@@ -916,7 +914,8 @@ int cm_manifold_param_vjp(const cm_scene* sc, const int32_t* pairs, int64_t n_pa
     pmax = std::max(pmax, sc->param_count[s]);
   }
   int rc = cml::launch_manifold_param_vjp(sc->dev, sc->max_V, sc->max_E, pmax, pairs, n_pairs, offsets, poses, n_env,
-                                          n_slot, flags & CM_FULL_MODE, w_depth, vjp, sc->param_off_dev, stream);
+                                          n_slot, flags & (CM_FULL_MODE | CM_TWO_SIDED | CM_BROAD_PHASE), w_depth, vjp,
+                                          sc->param_off_dev, stream);
   if (rc) return fail(rc, cml::last_cuda_error());
   return CM_OK;
 }

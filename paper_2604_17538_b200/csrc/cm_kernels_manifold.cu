@@ -1720,7 +1720,11 @@ __global__ void __launch_bounds__(CM_PV_THREADS) k_mf_param_vjp(const MfArgs a, 
   __shared__ int shB;
   if (threadIdx.x == 0) {
     unit_resolve(a, blockIdx.x, U);
-    shB = __ldg(a.pairs + 5 * (int64_t)blockIdx.x + 4);
+    // the unit's SDF shape: B, or A for the transposed half of a two-sided pair
+    const bool two = (a.mode & CM_TWO_SIDED) != 0;
+    const int64_t pi = two ? (int64_t)blockIdx.x >> 1 : (int64_t)blockIdx.x;
+    const int side = two ? (int)(blockIdx.x & 1) : 0;
+    shB = __ldg(a.pairs + 5 * pi + 4 - side);
   }
   __syncthreads();
   if (!U.valid) return;
@@ -2082,13 +2086,15 @@ int launch_manifold_param_vjp(const SceneDev& s, int max_V, int max_E, int pmax,
     set_error("manifold_param_vjp: shared memory");
     return CM_ERR_UNSUPPORTED;
   }
-  for (int64_t p0 = 0; p0 < n_pairs; p0 += 0x7fffffff) {   // (grids of at most 2^31 - 1 CTAs)
-    const int64_t nb = n_pairs - p0 < 0x7fffffff ? n_pairs - p0 : 0x7fffffff;
+  const int upp = (mode & CM_TWO_SIDED) ? 2 : 1;   // units per pair
+  for (int64_t p0 = 0; p0 < n_pairs; p0 += 0x3fffffff) {   // (grids of at most 2^31 - 1 CTAs)
+    const int64_t nb = n_pairs - p0 < 0x3fffffff ? n_pairs - p0 : 0x3fffffff;
     MfArgs ac = a;
     ac.pairs = pairs + 5 * p0;
     ac.offsets = offsets + p0;
     ac.n_pairs = nb;
-    k_mf_param_vjp<<<(unsigned)nb, CM_PV_THREADS, bytes, (cudaStream_t)stream>>>(ac, w, vjp, poff, max_V, max_E);
+    k_mf_param_vjp<<<(unsigned)(nb * upp), CM_PV_THREADS, bytes, (cudaStream_t)stream>>>(ac, w, vjp, poff, max_V,
+                                                                                           max_E);
     if (int rc = check_launch("k_mf_param_vjp")) return rc;
   }
   return CM_OK;

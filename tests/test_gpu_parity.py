@@ -619,7 +619,7 @@ def _vjp_scene():
     return scene_of(shapes, pairs=pairs, poses=poses.astype(np.float32)), rng
 
 
-@pytest.mark.parametrize("mode", [0, 4])
+@pytest.mark.parametrize("mode", [0, 4, 8, 16])
 def test_manifold_param_vjp_parity(cuda, oracle_mod, mode):
     """Shape-parameter VJP of the manifold depths (DESIGN
     reading #48) against the oracle's seeded manifold: random weights over
@@ -629,6 +629,8 @@ def test_manifold_param_vjp_parity(cuda, oracle_mod, mode):
     import torch
     from paper_2604_17538_b200 import binding
     sc, rng = _vjp_scene()
+    if mode & binding.TWO_SIDED:   # both shapes need a surface and an SDF: the C1 pairs
+        sc.pairs = np.ascontiguousarray(sc.pairs[sc.pairs[:, 3] <= 1])
     S = binding.Scene(sc.shapes, sc.smooth)
     osc = oracle_mod.OracleScene(sc)
     counts, offs = S.param_layout()
@@ -640,8 +642,14 @@ def test_manifold_param_vjp_parity(cuda, oracle_mod, mode):
     Jd = osc.manifold_param_jac(sc.pairs, sc.poses, mode=mode, pmax=pmax)
     Jp = osc.manifold_param_jac(sc.pairs, PT.perturb_inputs(np.random.default_rng(72), sc.poses), mode=mode, pmax=pmax)
     assert Jd.shape[0] == C
-    row_pair = np.searchsorted(offs_t.cpu().numpy(), np.arange(C), side="right") - 1
-    shape_of_row = sc.pairs[row_pair, 4]
+    # each row's SDF shape: B, or A for the transposed half of a two-sided pair
+    offs_h = offs_t.cpu().numpy()
+    row_pair = np.searchsorted(offs_h, np.arange(C), side="right") - 1
+    shape_of_row = sc.pairs[row_pair, 4].copy()
+    if mode & binding.TWO_SIDED:
+        nA = np.array([S.counts(int(a))[2 if not mode & binding.FULL_MODE else 0] for a in sc.pairs[:, 3]])
+        second = np.arange(C) - offs_h[row_pair] >= nA[row_pair]
+        shape_of_row[second] = sc.pairs[row_pair[second], 3]
     tol_row = 1e-4 * np.maximum(np.abs(Jd).max(axis=1), 1.0)
 
     def ref_vjp(w, J):
@@ -676,16 +684,23 @@ def test_manifold_param_vjp_parity(cuda, oracle_mod, mode):
 
 
 def test_manifold_param_vjp_unsupported(cuda):
+    """A scene holding a shape the parameter layout cannot describe (more
+    than 16 boolean nodes: count -1) refuses the manifold VJP."""
     import torch
     from paper_2604_17538_b200 import binding
-    sc, _ = _vjp_scene()
+    big = synth.op("union", [synth.op("union", [synth.sq((0.01, 0.01, 0.01), (1, 1), pose=[0.02 * i, 0, 0, 1, 0, 0, 0]),
+                                                synth.sq((0.01, 0.01, 0.01), (1, 1), pose=[0.02 * i, 0.02, 0, 1, 0, 0, 0])])
+                             for i in range(16)])
+    c1 = synth.c1_scene()
+    shapes = list(c1.shapes) + [synth.make_shape("big", big, None)]
+    sc = scene_of(shapes, pairs=c1.pairs, poses=c1.poses)
     S = binding.Scene(sc.shapes, sc.smooth)
     pairs_t = torch.from_numpy(sc.pairs).cuda()
     poses_t = torch.from_numpy(sc.poses).cuda()
-    offs_t = S.manifold_offsets(pairs_t, binding.TWO_SIDED)
-    C = S.manifold_size(sc.pairs[:2], binding.TWO_SIDED)
+    offs_t = S.manifold_offsets(pairs_t)
+    C = S.manifold_size(sc.pairs)
     with pytest.raises(binding.CMError):
-        S.manifold_param_vjp(pairs_t[:2], offs_t, poses_t, torch.zeros(C, device="cuda"), binding.TWO_SIDED)
+        S.manifold_param_vjp(pairs_t, offs_t, poses_t, torch.zeros(C, device="cuda"))
 
 
 def test_sdf_eval_xpsq_soft_cardano_band(cuda, oracle_mod):
