@@ -9,7 +9,9 @@ sys.path.insert(0, ".")
 from paper_2604_17538_b200 import binding, synth
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 17
-sc = synth.c5_scene(n)
+wl = sys.argv[2] if len(sys.argv) > 2 else "C5"
+sc = {"C5": lambda: synth.c5_scene(n), "C4": lambda: synth.c4_scene(n), "C3": lambda: synth.c3_scene(n),
+      "C6": lambda: synth.c6_scene(n)}[wl]()
 S = binding.Scene(sc.shapes, sc.smooth)
 pairs = torch.from_numpy(sc.pairs).cuda()
 poses = torch.from_numpy(sc.poses).cuda()
