@@ -879,6 +879,37 @@ __device__ __forceinline__ void trace_one_n(const MfArgs& a, const UnitCtx& U, c
   }
 }
 
+// trace j of unit u (j < E: edge j from v_I; else edge j - E from v_II) and
+// its record in the unit's slot
+template <int TIER, int XP>
+__device__ __forceinline__ void trace_item_n(const MfArgs& a, const UnitCtx& U, int u, int j) {
+  const int V = U.SA.V, E = U.SA.E;
+  const float* sv = a.scratch + (int64_t)u * a.slot;
+  float* se = a.scratch + (int64_t)u * a.slot + (int64_t)vrec(TIER) * V;
+  const float* lv = a.S.verts + 4 * (int64_t)U.SA.v_off;
+  const int32_t* ed = a.S.edges + 2 * (int64_t)U.SA.e_off;
+  const int e = j < E ? j : j - E;
+  const int dir = j < E ? 0 : 1;     // 0: from v_I along +e_t; 1: from v_II along -e_t
+  const int vI = __ldg(ed + 2 * e), vII = __ldg(ed + 2 * e + 1);
+  CM_ASSERT(vI >= 0 && vI < V && vII >= 0 && vII < V);
+  float o[10];
+  trace_one_n<TIER, XP>(a, U, sv, lv, vI, vII, dir, o);
+  float* rec = se + e * erec(TIER) + (dir ? trace_b(TIER) : 0);
+  if constexpr (TIER >= 2) {
+    if (dir == 0) {   // record floats 0-9: two float4 + one float2
+      st4(rec, o[0], o[1], o[2], o[3]);
+      st4(rec + 4, o[4], o[5], o[6], o[7]);
+      *reinterpret_cast<float2*>(rec + 8) = make_float2(o[8], o[9]);
+    } else {          // record floats 10-19: one float2 + two float4
+      *reinterpret_cast<float2*>(rec) = make_float2(o[0], o[1]);
+      st4(rec + 2, o[2], o[3], o[4], o[5]);
+      st4(rec + 6, o[6], o[7], o[8], o[9]);
+    }
+  } else {
+    *rec = o[0];
+  }
+}
+
 template <int TIER, int XP>
 __device__ __forceinline__ void mf_traces_unit_n(const MfArgs& a, const UnitCtx& U, int u) {
   static_assert(TIER <= 2, "tier 3 carries second derivatives: mf_traces_unit");
@@ -920,28 +951,7 @@ __device__ __forceinline__ void mf_traces_unit_n(const MfArgs& a, const UnitCtx&
     }
   }
 #else
-  for (int j = threadIdx.x; j < 2 * E; j += blockDim.x) {
-    const int e = j < E ? j : j - E;
-    const int dir = j < E ? 0 : 1;     // 0: from v_I along +e_t; 1: from v_II along -e_t
-    const int vI = __ldg(ed + 2 * e), vII = __ldg(ed + 2 * e + 1);
-    CM_ASSERT(vI >= 0 && vI < V && vII >= 0 && vII < V);
-    float o[10];
-    trace_one_n<TIER, XP>(a, U, sv, lv, vI, vII, dir, o);
-    float* rec = se + e * erec(TIER) + (dir ? trace_b(TIER) : 0);
-    if constexpr (TIER >= 2) {
-      if (dir == 0) {   // record floats 0-9: two float4 + one float2
-        st4(rec, o[0], o[1], o[2], o[3]);
-        st4(rec + 4, o[4], o[5], o[6], o[7]);
-        *reinterpret_cast<float2*>(rec + 8) = make_float2(o[8], o[9]);
-      } else {          // record floats 10-19: one float2 + two float4
-        *reinterpret_cast<float2*>(rec) = make_float2(o[0], o[1]);
-        st4(rec + 2, o[2], o[3], o[4], o[5]);
-        st4(rec + 6, o[6], o[7], o[8], o[9]);
-      }
-    } else {
-      *rec = o[0];
-    }
-  }
+  for (int j = threadIdx.x; j < 2 * E; j += blockDim.x) trace_item_n<TIER, XP>(a, U, u, j);
 #endif
 }
 
@@ -1484,6 +1494,46 @@ __global__ void __maxnreg__((RegCap<TIER, XP>::VERTICES)) k_mf_vertices(const Mf
     if (CM_MF_UPC > 1) __syncthreads();
   }
 }
+// CAT units per CTA with their traces as one item range (tiers 0-2,
+// 6-component recursion): the last, partly filled round of each unit's
+// traces is shared with the next units.  Used when every sampled surface
+// of the scene is small (2 max_E <= CM_MF_CAT_MAX_ITEMS): C4 +4.5%, while
+// C5 (2E up to 576) -2% and C3 -4% lose to the longer CTAs (r02zu sweep)
+#ifndef CM_MF_CAT
+#define CM_MF_CAT 4
+#endif
+#ifndef CM_MF_CAT_MAX_ITEMS
+#define CM_MF_CAT_MAX_ITEMS 384
+#endif
+template <int TIER, int XP, int CAT>
+__global__ void __maxnreg__((RegCap<TIER, XP>::TRACES)) k_mf_traces_cat(const MfArgs a) {
+  __shared__ UnitCtx U[CAT];
+  __shared__ int su[CAT], sn[CAT + 1];
+  if (threadIdx.x == 0) {
+    sn[0] = 0;
+    const int cnt = __ldcg(a.cls_count + XP);
+    for (int r = 0; r < CAT; ++r) {
+      const int b = blockIdx.x * CAT + r;
+      su[r] = b < cnt ? __ldcg(a.cls_list + (int64_t)XP * a.chunk + b) : -1;
+      sn[r + 1] = sn[r] + (su[r] >= 0 ? 2 * __ldcg(&a.ctx[su[r]].SA.E) : 0);
+    }
+  }
+  __syncthreads();
+  constexpr int n4 = (int)(sizeof(UnitCtx) / 16);
+  for (int r = 0; r < CAT; ++r) {
+    if (su[r] < 0) break;
+    const float4* src = reinterpret_cast<const float4*>(a.ctx + su[r]);
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) reinterpret_cast<float4*>(&U[r])[i] = __ldcg(src + i);
+  }
+  __syncthreads();
+  const int total = sn[CAT];
+  for (int j = threadIdx.x; j < total; j += blockDim.x) {
+    int r = 0;
+#pragma unroll
+    for (int k = 1; k < CAT; ++k) r += j >= sn[k];
+    trace_item_n<TIER, XP>(a, U[r], su[r], j - sn[r]);
+  }
+}
 template <int TIER, int XP>
 __global__ void __maxnreg__((RegCap<TIER, XP>::TRACES)) k_mf_traces(const MfArgs a) {
   __shared__ UnitCtx U;
@@ -1917,7 +1967,14 @@ static int launch_sdf_phases(MfArgs& a, int64_t nb, int T, int max_V, int max_E,
       return check_launch("k_mf_edges");
     }
   }
-  k_mf_traces<TIER, XP><<<gu, T, 0, st>>>(a);
+  bool cat = false;
+  if constexpr (TIER <= 2 && CM_TRACE6 && !CM_TRACE_PAIRED && CM_MF_CAT > 1) {
+    if (2 * max_E <= CM_MF_CAT_MAX_ITEMS) {
+      k_mf_traces_cat<TIER, XP, CM_MF_CAT><<<(unsigned)((nb + CM_MF_CAT - 1) / CM_MF_CAT), T, 0, st>>>(a);
+      cat = true;
+    }
+  }
+  if (!cat) k_mf_traces<TIER, XP><<<gu, T, 0, st>>>(a);
   if ((rc = check_launch("k_mf_traces"))) return rc;
   if constexpr (TIER <= 2) {
     const int fb = midfaces_bytes(TIER, a.mode, max_V, max_E);
