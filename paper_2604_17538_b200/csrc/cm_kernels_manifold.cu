@@ -951,7 +951,28 @@ __device__ __forceinline__ void mf_traces_unit_n(const MfArgs& a, const UnitCtx&
     }
   }
 #else
-  for (int j = threadIdx.x; j < 2 * E; j += blockDim.x) trace_item_n<TIER, XP>(a, U, u, j);
+  for (int j = threadIdx.x; j < 2 * E; j += blockDim.x) {
+    const int e = j < E ? j : j - E;
+    const int dir = j < E ? 0 : 1;     // 0: from v_I along +e_t; 1: from v_II along -e_t
+    const int vI = __ldg(ed + 2 * e), vII = __ldg(ed + 2 * e + 1);
+    CM_ASSERT(vI >= 0 && vI < V && vII >= 0 && vII < V);
+    float o[10];
+    trace_one_n<TIER, XP>(a, U, sv, lv, vI, vII, dir, o);
+    float* rec = se + e * erec(TIER) + (dir ? trace_b(TIER) : 0);
+    if constexpr (TIER >= 2) {
+      if (dir == 0) {   // record floats 0-9: two float4 + one float2
+        st4(rec, o[0], o[1], o[2], o[3]);
+        st4(rec + 4, o[4], o[5], o[6], o[7]);
+        *reinterpret_cast<float2*>(rec + 8) = make_float2(o[8], o[9]);
+      } else {          // record floats 10-19: one float2 + two float4
+        *reinterpret_cast<float2*>(rec) = make_float2(o[0], o[1]);
+        st4(rec + 2, o[2], o[3], o[4], o[5]);
+        st4(rec + 6, o[6], o[7], o[8], o[9]);
+      }
+    } else {
+      *rec = o[0];
+    }
+  }
 #endif
 }
 
