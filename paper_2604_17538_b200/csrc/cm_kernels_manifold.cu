@@ -435,10 +435,13 @@ __host__ __device__ constexpr int regs_of(int minb) { return minb >= 3 ? 80 : (m
 #ifndef CM_MF_REG_T_XP1
 #define CM_MF_REG_T_XP1 0
 #endif
+#ifndef CM_MF_REG_T3
+#define CM_MF_REG_T3 0   // register cap of the tier-3 kernels (0: 255)
+#endif
 template <int TIER, int XP> struct RegCap {
-  static constexpr int VERTICES = (TIER == 2 && (XP == 1 || XP == 4) && CM_MF_REG_XP1) ? CM_MF_REG_XP1 : regs_of(MinB<TIER, XP>::VERTICES);
-  static constexpr int TRACES = (TIER == 2 && (XP == 1 || XP == 4) && CM_MF_REG_T_XP1) ? CM_MF_REG_T_XP1 : regs_of(MinB<TIER, XP>::TRACES);
-  static constexpr int MIDPOINTS = (TIER == 2 && (XP == 1 || XP == 4) && CM_MF_REG_XP1) ? CM_MF_REG_XP1 : regs_of(MinB<TIER, XP>::MIDPOINTS);
+  static constexpr int VERTICES = (TIER >= 3 && CM_MF_REG_T3) ? CM_MF_REG_T3 : ((TIER == 2 && (XP == 1 || XP == 4) && CM_MF_REG_XP1) ? CM_MF_REG_XP1 : regs_of(MinB<TIER, XP>::VERTICES));
+  static constexpr int TRACES = (TIER >= 3 && CM_MF_REG_T3) ? CM_MF_REG_T3 : ((TIER == 2 && (XP == 1 || XP == 4) && CM_MF_REG_T_XP1) ? CM_MF_REG_T_XP1 : regs_of(MinB<TIER, XP>::TRACES));
+  static constexpr int MIDPOINTS = (TIER >= 3 && CM_MF_REG_T3) ? CM_MF_REG_T3 : ((TIER == 2 && (XP == 1 || XP == 4) && CM_MF_REG_XP1) ? CM_MF_REG_XP1 : regs_of(MinB<TIER, XP>::MIDPOINTS));
 };
 #ifndef CM_MF_FACE_MINB
 #define CM_MF_FACE_MINB 2   // face kernel: <= 128 registers
@@ -1730,7 +1733,7 @@ __global__ void __launch_bounds__(CM_MF_MAX_THREADS) k_mf_culled(const MfArgs a)
 #define CM_MF_FACE_REGS 0   // explicit register cap of the tier-0-2 face kernel (0: CM_MF_FACE_MINB)
 #endif
 template <int TIER> struct FaceRegs {
-  static constexpr int R = TIER >= 3 ? 255 : (CM_MF_FACE_REGS ? CM_MF_FACE_REGS : regs_of(CM_MF_FACE_MINB));
+  static constexpr int R = TIER >= 3 ? (CM_MF_REG_T3 ? CM_MF_REG_T3 : 255) : (CM_MF_FACE_REGS ? CM_MF_FACE_REGS : regs_of(CM_MF_FACE_MINB));
 };
 template <int TIER, bool STAGED>
 __global__ void __launch_bounds__(CM_MF_MAX_THREADS) __maxnreg__((FaceRegs<TIER>::R)) k_mf_faces(const MfArgs a) {
