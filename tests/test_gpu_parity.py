@@ -683,6 +683,43 @@ def test_manifold_param_vjp_parity(cuda, oracle_mod, mode):
     assert np.abs(Jd).max() > 0.1
 
 
+def test_manifold_param_vjp_cup(cuda, oracle_mod):
+    """The manifold shape-parameter VJP on C4 (2 envs x 20 links against the
+    cup: a nested boolean tree with an XPSQ handle, 24 parameters incl. the
+    handle's control points): random weights and one-hot rows."""
+    import torch
+    from paper_2604_17538_b200 import binding
+    sc = synth.c4_scene(2)
+    S = binding.Scene(sc.shapes, sc.smooth)
+    osc = oracle_mod.OracleScene(sc)
+    counts, offs = S.param_layout()
+    pairs_t = torch.from_numpy(sc.pairs).cuda()
+    poses_t = torch.from_numpy(sc.poses).cuda()
+    offs_t = S.manifold_offsets(pairs_t)
+    C = S.manifold_size(sc.pairs)
+    pmax = int(counts.max())
+    Jd = osc.manifold_param_jac(sc.pairs, sc.poses, pmax=pmax)
+    Jp = osc.manifold_param_jac(sc.pairs, PT.perturb_inputs(np.random.default_rng(74), sc.poses), pmax=pmax)
+    nc = counts[0]                      # every row's SDF shape is the cup (shape 0)
+    tol_row = 1e-4 * np.maximum(np.abs(Jd).max(axis=1), 1.0)
+    rng = np.random.default_rng(75)
+    rep = []
+    nf = 0
+    for trial in range(3):
+        w = rng.normal(size=C).astype(np.float32)
+        got = S.manifold_param_vjp(pairs_t, offs_t, poses_t, torch.from_numpy(w).cuda()).cpu().numpy()
+        nf += PT.compare("vjp%d" % trial, got[offs[0]:offs[0] + nc], w @ Jd[:, :nc], w @ Jp[:, :nc],
+                         np.abs(w) @ tol_row + 1e-30, rep)
+    for r in rng.choice(C, size=16, replace=False):
+        w = np.zeros(C, np.float32)
+        w[r] = 1.0
+        got = S.manifold_param_vjp(pairs_t, offs_t, poses_t, torch.from_numpy(w).cuda()).cpu().numpy()
+        nf += PT.compare("row%d" % r, got[offs[0]:offs[0] + nc], Jd[r, :nc], Jp[r, :nc], tol_row[r], rep)
+    _report("manifold_param_vjp_cup", rep)
+    assert nf == 0, json.dumps(rep, indent=1)
+    assert PT.excluded_fraction(rep) < 0.01
+
+
 def test_manifold_param_vjp_unsupported(cuda):
     """A scene holding a shape the parameter layout cannot describe (more
     than 16 boolean nodes: count -1) refuses the manifold VJP."""
