@@ -366,6 +366,10 @@ static_assert(sizeof(UnitCtx) % 16 == 0, "UnitCtx is copied as float4");
 #ifndef CM_TRACE6
 #define CM_TRACE6 1         // 6-component trace derivative recursion (tiers 0-2)
 #endif
+#ifndef CM_MF_FACE_L1PF
+#define CM_MF_FACE_L1PF 1   // face kernel: L1 prefetch of the unit's records at the start (C5 +1.5%, r02zz3);
+                            // 2: also the mesh's vertex and edge-geometry tables
+#endif
 #ifndef CM_TRACE_PAIRED
 #define CM_TRACE_PAIRED 0   // tiers 0-2: both traces of an edge on adjacent lanes, one averaged record
                             // (-18 KB DRAM per C5 pair, bitwise equal; C5 -1.3%, C4 0, C3 +0.3%: r02zf)
@@ -1211,6 +1215,21 @@ __device__ __forceinline__ void mf_faces_unit(const MfArgs& a, const UnitCtx& U,
     se = fsm + VR * V;
   }
   CM_COLS(U.side);
+  if constexpr (!STAGED && CM_MF_FACE_L1PF) {
+    // the unit's candidate records into L1 (one prefetch per 128-B line),
+    // ahead of the faces' dependent gathers
+    const int used = VR * V + ER * E;
+    if (!sv_in && used <= 8192) {   // (slots up to 32 KB: a large unit's would evict its own lines)
+      for (int o = threadIdx.x * 32; o < used; o += blockDim.x * 32)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(gv + o));
+      if (CM_MF_FACE_L1PF >= 2) {
+        for (int o = threadIdx.x * 32; o < 4 * V; o += blockDim.x * 32)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(lv + o));
+        for (int o = threadIdx.x * 32; o < 8 * E; o += blockDim.x * 32)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(eg + o));
+      }
+    }
+  }
   const float itlm = LOG2E * itmin;
   for (int f = threadIdx.x; f < NF; f += blockDim.x) {
     int cv[3], ce[3];
