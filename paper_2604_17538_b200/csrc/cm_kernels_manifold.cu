@@ -370,6 +370,9 @@ static_assert(sizeof(UnitCtx) % 16 == 0, "UnitCtx is copied as float4");
 #define CM_MF_FACE_L1PF 1   // face kernel: L1 prefetch of the unit's records at the start (C5 +1.5%, r02zz3);
                             // 2: also the mesh's vertex and edge-geometry tables
 #endif
+#ifndef CM_MF_MID_L1PF
+#define CM_MF_MID_L1PF 1   // midpoint kernel: L1 prefetch of the unit's trace records at the start
+#endif
 #ifndef CM_TRACE_PAIRED
 #define CM_TRACE_PAIRED 0   // tiers 0-2: both traces of an edge on adjacent lanes, one averaged record
                             // (-18 KB DRAM per C5 pair, bitwise equal; C5 -1.3%, C4 0, C3 +0.3%: r02zf)
@@ -1057,6 +1060,11 @@ __device__ __forceinline__ void mf_midpoints_unit(const MfArgs& a, const UnitCtx
     cp_async_commit();
   };
   if (TIER == 2 && pb && (int)threadIdx.x < E) fetch(threadIdx.x);
+  if (CM_MF_MID_L1PF && srec == se && E * erec(TIER) <= 8192) {
+    // the unit's trace records into L1 (one prefetch per 128-B line)
+    for (int o = threadIdx.x * 32; o < E * erec(TIER); o += blockDim.x * 32)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(srec + o));
+  }
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     float* rec = drec + e * erec(TIER);
     const float* rin = srec + e * erec(TIER);
