@@ -370,6 +370,9 @@ static_assert(sizeof(UnitCtx) % 16 == 0, "UnitCtx is copied as float4");
 #define CM_MF_FACE_L1PF 1   // face kernel: L1 prefetch of the unit's records at the start (C5 +1.5%, r02zz3);
                             // 2: also the mesh's vertex and edge-geometry tables
 #endif
+#ifndef CM_MF_TRACE_L1PF
+#define CM_MF_TRACE_L1PF 0   // trace kernel: L1 prefetch of the unit's vertex records at the start (no gain: r02zz7)
+#endif
 #ifndef CM_MF_MID_L1PF
 #define CM_MF_MID_L1PF 1   // midpoint kernel: L1 prefetch of the unit's trace records at the start
 #endif
@@ -961,6 +964,10 @@ __device__ __forceinline__ void mf_traces_unit_n(const MfArgs& a, const UnitCtx&
     }
   }
 #else
+  if (CM_MF_TRACE_L1PF && vrec(TIER) * V <= 8192) {   // the unit's vertex records (the corners) into L1
+    for (int o = threadIdx.x * 32; o < vrec(TIER) * V; o += blockDim.x * 32)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(sv + o));
+  }
   for (int j = threadIdx.x; j < 2 * E; j += blockDim.x) {
     const int e = j < E ? j : j - E;
     const int dir = j < E ? 0 : 1;     // 0: from v_I along +e_t; 1: from v_II along -e_t
