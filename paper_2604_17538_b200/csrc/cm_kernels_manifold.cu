@@ -373,6 +373,9 @@ static_assert(sizeof(UnitCtx) % 16 == 0, "UnitCtx is copied as float4");
 #ifndef CM_MF_TRACE_L1PF
 #define CM_MF_TRACE_L1PF 0   // trace kernel: L1 prefetch of the unit's vertex records at the start (no gain: r02zz7)
 #endif
+#ifndef CM_MF_TABLE_L1PF
+#define CM_MF_TABLE_L1PF 0   // vertex / midpoint kernels: L1 prefetch of the mesh's vertex / edge tables (C5 -0.3%: r02zz8)
+#endif
 #ifndef CM_MF_MID_L1PF
 #define CM_MF_MID_L1PF 1   // midpoint kernel: L1 prefetch of the unit's trace records at the start
 #endif
@@ -646,6 +649,10 @@ __device__ __forceinline__ void mf_vertices_unit(const MfArgs& a, const UnitCtx&
   const float* lv = a.S.verts + 4 * (int64_t)U.SA.v_off;
   const bool full = (a.mode & CM_FULL_MODE) != 0;
   const float itcmp = a.S.sp.i_cmp;
+  if (CM_MF_TABLE_L1PF) {   // the mesh's vertex table into L1
+    for (int o = threadIdx.x * 32; o < 4 * V; o += blockDim.x * 32)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(lv + o));
+  }
   for (int v = threadIdx.x; v < V; v += blockDim.x) {
     float xb[3], pw[3];
     vertex_frames(F, lv, v, xb, pw);
@@ -1067,6 +1074,11 @@ __device__ __forceinline__ void mf_midpoints_unit(const MfArgs& a, const UnitCtx
     cp_async_commit();
   };
   if (TIER == 2 && pb && (int)threadIdx.x < E) fetch(threadIdx.x);
+  if (CM_MF_TABLE_L1PF) {   // the mesh's edge-geometry table into L1
+    const float* egt = a.S.edge_geom + 8 * (int64_t)U.SA.e_off;
+    for (int o = threadIdx.x * 32; o < 8 * E; o += blockDim.x * 32)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(egt + o));
+  }
   if (CM_MF_MID_L1PF && srec == se && E * erec(TIER) <= 8192) {
     // the unit's trace records into L1 (one prefetch per 128-B line)
     for (int o = threadIdx.x * 32; o < E * erec(TIER); o += blockDim.x * 32)
